@@ -1,0 +1,487 @@
+"""Pins for the fp64 oracle (-m "not gpu").
+
+Each test pins an oracle function to something OTHER than the oracle itself:
+values printed in the paper or SPEC (tests/golden, cited), closed forms evaluated by
+library routines (numpy matmul / kron, scipy cdist, numpy.linalg.solve), the
+paper's operator algebra (P, Q from Definition 1, the Corollary operators, Theorem 2,
+Table 4a feature maps), invariants and brute force on tiny inputs.  A plausible
+mistake (dropped term, wrong sign, transposed operand, wrong selector) fails one.
+"""
+import itertools
+import json
+
+import numpy as np
+import pytest
+from scipy.spatial.distance import cdist
+
+import oracle as O
+import synth
+from conftest import golden_path, load_golden_matrix
+
+K_ALL = [O.LINEAR, O.POLY2D, O.GAUSSIAN, O.KRONECKER, O.SYMMETRIC, O.ANTISYMMETRIC, O.RANKING, O.MLPK,
+         O.CARTESIAN]
+HET = [O.LINEAR, O.POLY2D, O.GAUSSIAN, O.KRONECKER, O.CARTESIAN]
+HOM = [O.SYMMETRIC, O.ANTISYMMETRIC, O.RANKING, O.MLPK]
+SPEC = json.load(open(golden_path("spec_worked_values.json")))
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x, float), np.asarray(ref, float)
+    nr = np.linalg.norm(ref)
+    return np.linalg.norm(x - ref) / (nr if nr > 1e-30 else 1.0)
+
+
+# ----------------------------------------------------------------------------- base Grams
+def test_gram_spec_worked_values():
+    g = SPEC["linear_base"]
+    assert O.gram(O.BASE_LINEAR, g["X"], g["Y"])[0, 0] == 11.0
+    g = SPEC["gaussian_base"]
+    assert O.gram(O.BASE_GAUSSIAN, g["X"], g["Y"], gamma=g["gamma"])[0, 0] == pytest.approx(np.exp(-1.0), abs=1e-15)
+
+
+def test_gram_matches_library_closed_forms():
+    rng = np.random.default_rng(0)
+    X, Y = rng.standard_normal((13, 7)), rng.standard_normal((9, 7))
+    assert np.abs(O.gram(O.BASE_LINEAR, X, Y) - X @ Y.T).max() < 1e-12
+    gam = 0.37
+    ref = np.exp(-gam * cdist(X, Y, "sqeuclidean"))
+    assert np.abs(O.gram(O.BASE_GAUSSIAN, X, Y, gamma=gam) - ref).max() < 1e-13
+    ref = (0.2 * (X @ Y.T) + 1.5) ** 3
+    assert np.abs(O.gram(O.BASE_POLY, X, Y, gamma=0.2, coef0=1.5, degree=3) - ref).max() < 1e-10
+
+
+def test_gram_gaussian_diag_exact_and_psd():
+    X = synth.config1().Xd
+    K = O.gram(O.BASE_GAUSSIAN, X, gamma=1 / 16)
+    assert np.all(np.diag(K) == 1.0)                       # SPEC.md:201, reading S29
+    ev = np.linalg.eigvalsh(K)
+    assert ev.min() >= -1e-10 * ev.max()                    # PSD
+    assert np.abs(K - K.T).max() == 0.0
+
+
+def test_gram_rejects_bad_gamma():
+    with pytest.raises(O.OracleError) as e:
+        O.gram(O.BASE_GAUSSIAN, [[0.0]], gamma=0.0)
+    assert e.value.code == O.E_PARAM
+
+
+# ----------------------------------------------------------------------------- kernel values
+def test_kernel_value_spec_worked_values():
+    kv = SPEC["kernel_value"]
+    D, T = np.array([[kv["D00"]]]), np.array([[kv["T00"]]])
+    assert O.kernel_value(O.LINEAR, D, T, (0, 0), (0, 0)) == kv["linear"]
+    assert O.kernel_value(O.POLY2D, D, T, (0, 0), (0, 0)) == kv["poly2d"]
+    assert O.kernel_value(O.KRONECKER, D, T, (0, 0), (0, 0)) == 6.0
+    rng = np.random.default_rng(1)
+    F = rng.standard_normal((4, 3))
+    Dh = F @ F.T
+    for dd in range(4):   # MLPK / Ranking / Anti vanish on a self pair (S18)
+        for b in itertools.product(range(4), repeat=2):
+            assert abs(O.kernel_value(O.MLPK, Dh, None, (dd, dd), b)) < 1e-28
+            assert abs(O.kernel_value(O.RANKING, Dh, None, (dd, dd), b)) < 1e-14
+            assert abs(O.kernel_value(O.ANTISYMMETRIC, Dh, None, (dd, dd), b)) < 1e-14
+
+
+def _feature_map(kernel, fd, ft, ed=None, et=None):
+    """Table 4a: the pair feature maps, written from the table."""
+    if kernel == O.LINEAR:
+        return np.concatenate([fd, ft])
+    if kernel == O.POLY2D:
+        c = np.concatenate([fd, ft])
+        return np.kron(c, c)
+    if kernel in (O.KRONECKER, O.GAUSSIAN):
+        return np.kron(fd, ft)
+    if kernel == O.SYMMETRIC:
+        return np.sqrt(0.5) * (np.kron(fd, ft) + np.kron(ft, fd))
+    if kernel == O.ANTISYMMETRIC:
+        return np.sqrt(0.5) * (np.kron(fd, ft) - np.kron(ft, fd))
+    if kernel == O.RANKING:
+        return fd - ft
+    if kernel == O.MLPK:
+        return np.kron(fd - ft, fd - ft)
+    if kernel == O.CARTESIAN:
+        return np.concatenate([np.kron(fd, et), np.kron(ed, ft)])
+    raise ValueError
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_kernel_value_equals_feature_map_inner_product(kernel):
+    """Table 4a feature maps vs Table 4b kernel values: a sign error (e.g. the
+    Corollary's printed (P-I) for Anti-symmetric) or a dropped term fails here."""
+    rng = np.random.default_rng(100 + kernel)
+    hom = kernel in HOM
+    m, q, r = 4, 3, 3
+    Fd = rng.standard_normal((m, r))
+    Ft = Fd if hom else rng.standard_normal((q, r))
+    qq = m if hom else q
+    D, T = Fd @ Fd.T, (None if hom else Ft @ Ft.T)
+    Id, It = np.eye(m), np.eye(qq)
+    for (d, t), (db, tb) in itertools.product(itertools.product(range(m), range(qq)), repeat=2):
+        if (d * qq + t) % 3 and (db * qq + tb) % 2:    # thin the 144..256 combos a little
+            continue
+        phi_o = _feature_map(kernel, Fd[d], Ft[t], Id[d], It[t])
+        phi_i = _feature_map(kernel, Fd[db], Ft[tb], Id[db], It[tb])
+        assert O.kernel_value(kernel, D, T, (d, t), (db, tb)) == pytest.approx(phi_o @ phi_i, abs=1e-11)
+
+
+def test_gaussian_pairwise_is_gaussian_on_concatenated_features():
+    """exp(-g||(xd,xt)-(xd',xt')||^2) = k_D * k_T (squared norm, S4)."""
+    rng = np.random.default_rng(7)
+    Xd, Xt, g = rng.standard_normal((5, 3)), rng.standard_normal((4, 2)), 0.3
+    D, T = O.gram(O.BASE_GAUSSIAN, Xd, gamma=g), O.gram(O.BASE_GAUSSIAN, Xt, gamma=g)
+    for d, t, db, tb in [(0, 1, 2, 3), (4, 0, 4, 0), (1, 3, 0, 2)]:
+        direct = np.exp(-g * np.sum((np.concatenate([Xd[d], Xt[t]]) - np.concatenate([Xd[db], Xt[tb]])) ** 2))
+        assert O.kernel_value(O.GAUSSIAN, D, T, (d, t), (db, tb)) == pytest.approx(direct, rel=1e-13)
+
+
+def test_kernel_value_invariants():
+    rng = np.random.default_rng(3)
+    F = rng.standard_normal((5, 4))
+    D = F @ F.T
+    for _ in range(50):
+        d, dp, db, dbp = rng.integers(0, 5, 4)
+        kv = lambda k, o, i: O.kernel_value(k, D, None, o, i)
+        # symmetric: invariant to swapping either pair; anti/ranking flip; mlpk invariant
+        assert kv(O.SYMMETRIC, (d, dp), (db, dbp)) == pytest.approx(kv(O.SYMMETRIC, (dp, d), (db, dbp)))
+        assert kv(O.SYMMETRIC, (d, dp), (db, dbp)) == pytest.approx(kv(O.SYMMETRIC, (d, dp), (dbp, db)))
+        assert kv(O.ANTISYMMETRIC, (d, dp), (db, dbp)) == pytest.approx(-kv(O.ANTISYMMETRIC, (dp, d), (db, dbp)))
+        assert kv(O.RANKING, (d, dp), (db, dbp)) == pytest.approx(-kv(O.RANKING, (dp, d), (db, dbp)))
+        assert kv(O.MLPK, (d, dp), (db, dbp)) == pytest.approx(kv(O.MLPK, (dp, d), (dbp, db)))
+        # Poly2D = Linear^2, MLPK = Ranking^2
+        assert kv(O.POLY2D, (d, dp), (db, dbp)) == pytest.approx(kv(O.LINEAR, (d, dp), (db, dbp)) ** 2)
+        assert kv(O.MLPK, (d, dp), (db, dbp)) == pytest.approx(kv(O.RANKING, (d, dp), (db, dbp)) ** 2)
+
+
+# ----------------------------------------------------------------------------- P, Q, Corollary
+def commutation(nd, nt):
+    """Definition 1: P[(t,d),(d',t')] = 1 iff d=d', t=t'."""
+    P = np.zeros((nt * nd, nd * nt))
+    for t in range(nt):
+        for d in range(nd):
+            P[t * nd + d, d * nt + t] = 1
+    return P
+
+
+def unification(nd, nt):
+    """Definition 1: Q[(d,t),(d',d'')] = 1 iff d=d'=d''."""
+    Q = np.zeros((nd * nt, nd * nd))
+    for d in range(nd):
+        for t in range(nt):
+            Q[d * nt + t, d * nd + d] = 1
+    return Q
+
+
+def pq_product(nd, nt):
+    """PQ values given in Definition 1: PQ[(d,t),(t',t'')] = 1 iff t=t'=t''."""
+    M = np.zeros((nd * nt, nt * nt))
+    for d in range(nd):
+        for t in range(nt):
+            M[d * nt + t, t * nt + t] = 1
+    return M
+
+
+def test_P_Q_match_paper_example():
+    assert np.array_equal(commutation(3, 2), load_golden_matrix("paper_P_3drugs_2targets.txt"))
+    assert np.array_equal(unification(3, 2), load_golden_matrix("paper_Q_3drugs_2targets.txt"))
+
+
+def test_theorem2_identities():
+    """Theorem 2 checked with explicit matrices."""
+    rng = np.random.default_rng(11)
+    nd, nt = 3, 4
+    Fd, Ft = rng.standard_normal((nd, 2)), rng.standard_normal((nt, 2))
+    D, T = Fd @ Fd.T, Ft @ Ft.T
+    P = commutation(nd, nt)
+    assert np.allclose(P @ P.T, np.eye(nd * nt)) and np.allclose(P.T @ P, np.eye(nd * nt))
+    assert np.allclose(P @ np.kron(D, T), np.kron(T, D) @ P)
+    assert np.allclose(P @ np.kron(D, T) @ P.T, np.kron(T, D))
+    Ph = commutation(nd, nd)
+    assert np.array_equal(Ph, Ph.T)
+    assert np.allclose(Ph @ np.kron(D, D), np.kron(D, D) @ Ph)
+    Q = unification(nd, nt)
+    assert np.allclose(Q @ np.kron(D, D) @ Q.T, np.kron(D * D, np.ones((nt, nt))))
+
+
+def corollary_operator(kernel, D, T):
+    """The Corollary table as explicit matrices over the whole domain,
+    natural pair order.  Anti-symmetric uses (I-P) (reading S3); MLPK uses (I-Q)^T on the
+    right (reading S22)."""
+    if kernel in HOM:
+        n = D.shape[0]
+        P, Q, I, one = commutation(n, n), unification(n, n), np.eye(n * n), np.ones((n, n))
+        DD = np.kron(D, D)
+        if kernel == O.SYMMETRIC:
+            return (P + I) @ DD
+        if kernel == O.ANTISYMMETRIC:
+            return (I - P) @ DD
+        if kernel == O.RANKING:
+            return (I - P) @ np.kron(D, one) @ (I - P)
+        if kernel == O.MLPK:
+            return (I + P) @ (I - Q) @ DD @ (I - Q).T @ (I + P)
+    nd, nt = D.shape[0], T.shape[0]
+    if kernel == O.LINEAR:
+        return np.kron(D, np.ones((nt, nt))) + np.kron(np.ones((nd, nd)), T)
+    if kernel == O.POLY2D:
+        Q, PQ = unification(nd, nt), pq_product(nd, nt)
+        return Q @ np.kron(D, D) @ Q.T + 2 * np.kron(D, T) + PQ @ np.kron(T, T) @ PQ.T
+    if kernel in (O.KRONECKER, O.GAUSSIAN):
+        return np.kron(D, T)
+    if kernel == O.CARTESIAN:
+        return np.kron(D, np.eye(nt)) + np.kron(np.eye(nd), T)
+    raise ValueError
+
+
+def sampling_operator(f, s, nd, nt):
+    """R(d,t) of PAPER.md:302-310: R[i,(d,t)] = 1 iff (d,t) = (d_i,t_i)."""
+    R = np.zeros((len(f), nd * nt))
+    R[np.arange(len(f)), np.asarray(f) * nt + np.asarray(s)] = 1
+    return R
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_explicit_matrix_equals_corollary_operator(kernel):
+    """Table 4b (the oracle's definition) == R_bar K_op R^T with the Corollary operator."""
+    for seed in range(5):
+        w = synth.tiny(seed, m=4, q=3, n=10, n_out=7, homogeneous=kernel in HOM)
+        D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=0.5)
+        T = None if w.Xt is None else O.gram(O.BASE_GAUSSIAN, w.Xt, gamma=0.5)
+        nt = D.shape[0] if T is None else T.shape[0]
+        Kop = corollary_operator(kernel, D, T)
+        Rin = sampling_operator(w.train_first, w.train_second, D.shape[0], nt)
+        Rout = sampling_operator(w.test_first, w.test_second, D.shape[0], nt)
+        Kref = Rout @ Kop @ Rin.T
+        K = O.explicit_matrix(kernel, D, T, w.test_first, w.test_second, w.train_first, w.train_second)
+        assert np.abs(K - Kref).max() < 1e-12
+
+
+def test_printed_antisymmetric_sign_is_negative_semidefinite():
+    """Reading S3: the Corollary's printed (P-I)(D(x)D) is NSD on the full domain, so it
+    cannot be the kernel of Table 4b; (I-P)(D(x)D) is PSD."""
+    rng = np.random.default_rng(5)
+    F = rng.standard_normal((4, 4))
+    D = F @ F.T
+    n = 4
+    P, I = commutation(n, n), np.eye(n * n)
+    ev_printed = np.linalg.eigvalsh((P - I) @ np.kron(D, D))
+    ev_used = np.linalg.eigvalsh((I - P) @ np.kron(D, D))
+    assert ev_printed.max() <= 1e-10 and ev_printed.min() < -1e-3
+    assert ev_used.min() >= -1e-10
+
+
+# ----------------------------------------------------------------------------- term lists
+def test_term_counts_and_mlpk_coefficients():
+    tc = SPEC["term_counts"]
+    for name, k in zip(synth.KERNEL_NAMES, range(9)):
+        assert len(O.kernel_terms(k)) == tc[name], name
+    assert [t.coef for t in O.kernel_terms(O.MLPK)] == SPEC["mlpk_coefficients"]["coefs"]
+    with pytest.raises(O.OracleError):
+        O.kernel_terms(42)
+
+
+def eval_term_python(t, D, T, o, i):
+    """The KernelTerm meaning: coef * L[rl(o), cl(i)] * R[rr(o), cr(i)]."""
+    coef, left, right, rl, rr, cl, cr = t.as_tuple()
+    Tm = D if T is None else T
+
+    def fv(kind, r, c):
+        return {O.DRUG: lambda: D[r, c], O.TARGET: lambda: Tm[r, c], O.ONES: lambda: 1.0,
+                O.IDENTITY: lambda: float(r == c)}[kind]()
+    return coef * fv(left, o[rl], i[cl]) * fv(right, o[rr], i[cr])
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_term_assembly_equals_table4b(kernel):
+    """Decomposition soundness: summing the Corollary terms entrywise
+    reproduces the Table 4b value of every argument pair."""
+    w = synth.tiny(3, m=4, q=3, homogeneous=kernel in HOM)
+    D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=0.5)
+    T = None if w.Xt is None else O.gram(O.BASE_GAUSSIAN, w.Xt, gamma=0.5)
+    qq = D.shape[0] if T is None else T.shape[0]
+    terms = O.kernel_terms(kernel)
+    for o in itertools.product(range(4), range(qq)):
+        for i in itertools.product(range(4), range(qq)):
+            v = sum(eval_term_python(t, D, T, o, i) for t in terms)
+            assert v == pytest.approx(O.kernel_value(kernel, D, T, o, i), abs=1e-12)
+
+
+# ----------------------------------------------------------------------------- GVT exactness
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_gvt_equals_explicit_on_200_tiny_instances(kernel):
+    """Theorem 1 is exact: the per-term GVT (both variants and auto)
+    equals the explicit product within 1e-12 relative on
+    out != in samples with duplicate and self pairs."""
+    terms = O.kernel_terms(kernel)
+    hom = kernel in HOM
+    for seed in range(200):
+        rng = np.random.default_rng(seed)
+        m, q = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        w = synth.tiny(seed, m=m, q=q, n=int(rng.integers(0, 20)), n_out=int(rng.integers(0, 15)),
+                       homogeneous=hom)
+        D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=0.5)
+        T = None if w.Xt is None else O.gram(O.BASE_GAUSSIAN, w.Xt, gamma=0.5)
+        a = synth.random_vector(seed, w.n)
+        ref = O.explicit_matvec(kernel, D, T, w.test_first, w.test_second, w.train_first, w.train_second, a)
+        for variant in (1, 2, 0):
+            u = O.gvt_matvec(terms, D, T, w.test_first, w.test_second, w.train_first, w.train_second, a,
+                             variant=variant)
+            assert rel(u, ref) <= 1e-12 or np.abs(u - ref).max() < 1e-13, (seed, variant)
+
+
+def test_gvt_spec_small_cases():
+    g = SPEC["gvt_single"]
+    kron = O.kernel_terms(O.KRONECKER)
+    u = O.gvt_matvec(kron, [[g["A"]]], [[g["B"]]], [0], [0], [0], [0], [g["v"]])
+    assert u[0] == g["u"]
+    # identity Kronecker over the full grid returns v
+    f, s = np.repeat(np.arange(2), 2), np.tile(np.arange(2), 2)
+    v = np.array([0.3, -1.2, 2.5, 7.0])
+    assert np.array_equal(O.gvt_matvec(kron, np.eye(2), np.eye(2), f, s, f, s, v), v)
+    # empty samples are legal
+    assert O.gvt_matvec(kron, np.eye(2), np.eye(2), [], [], f, s, v).shape == (0,)
+    assert np.array_equal(O.gvt_matvec(kron, np.eye(2), np.eye(2), f, s, [], [], []), np.zeros(4))
+
+
+def test_gvt_cost_and_op_count_spec_example():
+    """costs 17 / 14 and the FMA counter of variant 1."""
+    c = SPEC["gvt_cost"]
+    # out sample: 3 pairs over 2 drugs, 2 targets; in sample: 4 pairs over 3 drugs, 2 targets
+    of, os_ = [0, 1, 1], [0, 1, 0]
+    inf, ins = [0, 1, 2, 2], [0, 1, 1, 0]
+    term = O.kernel_terms(O.KRONECKER)[0]
+    c1, c2 = O.term_cost(term, 3, 2, False, of, os_, inf, ins)
+    assert (c1, c2) == (c["cost1"], c["cost2"])
+    D, T = np.eye(3), np.eye(2)
+    _, ops1 = O.term_gvt(term, D, T, of, os_, inf, ins, np.ones(4), variant=1)
+    _, ops2 = O.term_gvt(term, D, T, of, os_, inf, ins, np.ones(4), variant=2)
+    assert (ops1, ops2) == (c["cost1"], c["cost2"])
+    _, ops_auto = O.gvt_matvec([term], D, T, of, os_, inf, ins, np.ones(4), variant=0, return_ops=True)
+    assert ops_auto == min(c1, c2)
+
+
+def test_roth_vec_trick_complete_grid():
+    """PAPER.md:324 (Roth's column lemma): on the complete grid, the Kronecker matvec is
+    U = D A T^T with A the m x q reshape of a -- checked against numpy matmul."""
+    w = synth.config2()
+    Xd, Xt = w.Xd.astype(np.float64), w.Xt.astype(np.float64)
+    D, T = Xd @ Xd.T, Xt @ Xt.T
+    a = synth.random_vector(0, w.n).astype(np.float64)
+    u = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.train_first,
+                     w.train_second, a)
+    U = D @ a.reshape(68, 442) @ T.T
+    assert rel(u, U.reshape(-1)) < 1e-12
+
+
+def test_ranking_equals_oriented_incidence():
+    """the Ranking kernel matrix is M^T D M with the oriented
+    incidence operator M."""
+    w = synth.tiny(9, m=6, n=15, n_out=15, homogeneous=True)
+    D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=0.5)
+    M = np.zeros((6, w.n))
+    M[w.train_first, np.arange(w.n)] += 1
+    M[w.train_second, np.arange(w.n)] -= 1
+    K = O.explicit_matrix(O.RANKING, D, None, w.train_first, w.train_second, w.train_first, w.train_second)
+    assert np.abs(K - M.T @ D @ M).max() < 1e-12
+
+
+def test_gvt_linearity_and_psd():
+    w = synth.tiny(4, m=5, n=14, n_out=14, homogeneous=True)
+    D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=0.5)
+    for k in HOM:
+        terms = O.kernel_terms(k)
+        a, b = synth.random_vector(1, w.n).astype(np.float64), synth.random_vector(2, w.n).astype(np.float64)
+        f, s = w.train_first, w.train_second
+        lhs = O.gvt_matvec(terms, D, None, f, s, f, s, 2.0 * a - 3.0 * b)
+        rhs = 2.0 * O.gvt_matvec(terms, D, None, f, s, f, s, a) - 3.0 * O.gvt_matvec(terms, D, None, f, s, f, s, b)
+        assert rel(lhs, rhs) < 1e-12
+        K = O.explicit_matrix(k, D, None, f, s, f, s)
+        ev = np.linalg.eigvalsh(0.5 * (K + K.T))
+        assert ev.min() >= -1e-10 * max(1.0, ev.max())
+
+
+def test_homogeneity_errors():
+    D = np.eye(3)
+    with pytest.raises(O.OracleError) as e:
+        O.explicit_matvec(O.SYMMETRIC, D, np.eye(2), [0], [0], [0], [0], [1.0])
+    assert e.value.code == O.E_HOMOGENEOUS
+    with pytest.raises(O.OracleError) as e:
+        O.explicit_matvec(O.KRONECKER, D, np.eye(2), [0], [2], [0], [0], [1.0])
+    assert e.value.code == O.E_INDEX
+
+
+# ----------------------------------------------------------------------------- CG
+def test_cg_scalar_systems():
+    # (2 I) a = y after one iteration (K = I via identity Grams on the full grid, lambda = 1)
+    f, s = np.repeat(np.arange(3), 2), np.tile(np.arange(2), 3)
+    y = np.array([1.0, -2.0, 0.5, 4.0, 3.0, -1.0])
+    kron = O.kernel_terms(O.KRONECKER)
+    x, it, hist, rc = O.cg(kron, np.eye(3), np.eye(2), f, s, y, 1.0, 5)
+    assert rc == O.OK and it == 1 and np.allclose(x, y / 2, atol=1e-15)
+    # y = 0 -> a = 0, zero iterations
+    x, it, hist, rc = O.cg(kron, np.eye(3), np.eye(2), f, s, np.zeros(6), 1.0, 5)
+    assert it == 0 and np.all(x == 0)
+    # single pair ridge
+    r = SPEC["ridge_single_pair"]
+    x, it, _, rc = O.cg(kron, [[r["D"]]], [[r["T"]]], [0], [0], [r["y"]], r["lambda"], 3)
+    assert x[0] == pytest.approx(r["a"], abs=1e-15)
+    # lambda = 0, K = I -> a = y
+    x, it, _, _ = O.cg(kron, np.eye(3), np.eye(2), f, s, y, 0.0, 5)
+    assert np.allclose(x, y, atol=1e-15)
+
+
+def test_cg_matches_dense_direct_solve_on_C1():
+    """On C1 (kappa ~ 40) 50 fp64 iterations converge: the oracle's weights equal
+    numpy.linalg.solve of the explicit system (K + lambda I) a = y within 1e-10, the
+    recursive relres is <= 1e-6, and the A-norm error is non-increasing (reading S15)."""
+    w = synth.config1()
+    D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=w.gamma)
+    T = O.gram(O.BASE_GAUSSIAN, w.Xt, gamma=w.gamma)
+    f, s = w.train_first, w.train_second
+    K = O.explicit_matrix(O.KRONECKER, D, T, f, s, f, s)
+    A = K + w.lam * np.eye(w.n)
+    xs = np.linalg.solve(A, w.y.astype(np.float64))
+    kron = O.kernel_terms(O.KRONECKER)
+    x, it, hist, rc = O.cg(kron, D, T, f, s, w.y, w.lam, w.iters)
+    assert rc == O.OK and it == 50
+    assert rel(x, xs) < 1e-10
+    assert hist[-1] <= 1e-6
+    errs = []
+    for k in range(1, 25):
+        xk, _, _, _ = O.cg(kron, D, T, f, s, w.y, w.lam, k)
+        e = xk - xs
+        errs.append(np.sqrt(e @ A @ e))
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-12) for i in range(len(errs) - 1))
+    # the explicit-operator CG and the GVT-operator CG agree
+    xe, _, _, _ = O.cg(None, D, T, f, s, w.y, w.lam, w.iters, kernel=O.KRONECKER, explicit=True)
+    assert rel(xe, x) < 1e-10
+
+
+def test_cg_breakdown_on_indefinite_operator():
+    """A negative lambda makes K + lambda I indefinite: p.Ap <= 0 must be reported."""
+    f, s = [0, 1], [0, 0]
+    x, it, _, rc = O.cg(O.kernel_terms(O.KRONECKER), np.eye(2), np.eye(1), f, s, [1.0, 0.0], 0.0, 3)
+    assert rc == O.OK
+    with pytest.raises(O.OracleError):
+        O.cg(O.kernel_terms(O.KRONECKER), np.eye(2), np.eye(1), f, s, [1.0, 0.0], -1.0, 3)
+
+
+def test_predict_spec_example():
+    """a=[1], train pair (0,0), Kronecker -> score(i,j) = D[i,0] T[j,0]."""
+    rng = np.random.default_rng(2)
+    Fd, Ft = rng.standard_normal((4, 2)), rng.standard_normal((3, 2))
+    D, T = Fd @ Fd.T, Ft @ Ft.T
+    of, os_ = np.repeat(np.arange(4), 3), np.tile(np.arange(3), 4)
+    u = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, of, os_, [0], [0], [1.0])
+    assert np.allclose(u, D[of, 0] * T[os_, 0], atol=1e-15)
+    assert np.all(O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, of, os_, [0], [0], [0.0]) == 0)
+
+
+# ----------------------------------------------------------------------------- plumbing
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sort_plan_matches_numpy_stable_sort(mode):
+    rng = np.random.default_rng(8)
+    m, q, n = 37, 23, 5000
+    f, s = rng.integers(0, m, n), rng.integers(0, q, n)
+    perm, rp = O.sort_plan(f, s, m, q, mode=mode)
+    ref = np.argsort(f, kind="stable") if mode == 0 else np.lexsort((np.arange(n), s, f))
+    assert np.array_equal(perm, ref)
+    assert np.array_equal(rp, np.searchsorted(np.sort(f), np.arange(m + 1), side="left"))

@@ -1,0 +1,193 @@
+/*
+ * gvt.h -- C ABI of libgvt.so, the B200 (sm_100a) implementation of the generalized
+ * vec trick (GVT) hot path of Viljanen, Airola & Pahikkala, "Generalized vec trick for
+ * fast learning of pairwise kernel models" (arXiv 2009.01054; reference/PAPER.md).
+ *
+ *   u = R(d_bar, t_bar) K R(d, t)^T a,  K = sum of the Corollary's permuted Kronecker
+ *   terms, computed by Theorem 1's GVT inside a
+ *   conjugate-gradient kernel-ridge-regression loop (Eq. 1 at
+ *   316-320) and a batched prediction pass.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Plain C types only.  float arrays are fp32, ids are int32 global object ids, sizes
+ *    are int64.  Matrices are dense row-major with leading dimension = column count.
+ *  - POINTERS MAY BE HOST OR DEVICE MEMORY.  The library classifies every array with
+ *    cudaPointerGetAttributes: device (or managed) arrays are read/written in place
+ *    on the context's stream; host arrays (pageable or pinned) are staged through the
+ *    context's device workspace, host<->device copies included in the call.  Arrays
+ *    are caller-owned; the library never keeps a caller pointer after return.
+ *    Term lists, scalars and the *_out scalars are always host memory.
+ *  - All device work is issued on the context's stream (gvt_create / gvt_set_stream).
+ *    Calls are stream-ordered: every entry point returns after its work is ENQUEUED,
+ *    except when it must return a host-visible result (host output arrays, iters_out,
+ *    relres_hist, residual-mode stopping, error detection), in which case it
+ *    synchronises the stream before returning.
+ *  - Errors are return codes; nothing throws or aborts across the ABI.  Validation
+ *    (sizes, id ranges, homogeneity, parameters) runs BEFORE any compute
+ *    (SPEC.md:118).  gvt_last_error() returns a thread-local message for the last
+ *    non-OK status.
+ *  - Empty samples (n = 0 or n_out = 0) are legal and give empty outputs;
+ *    duplicate pairs are legal and their coefficients sum (reading S17).
+ *  - Base-kernel Grams D (m x m) and T (q x q) are over ALL objects, indexed by global
+ *    ids, and are symmetric (they are Gram matrices of a kernel); the kernels read
+ *    D[j][i] in place of D[i][j].  T == NULL means homogeneous data: one object table
+ *    of size m, both pair elements index D.  Ones and Identity
+ *    factors are over those global ids (readings S19, S28).
+ *  - Results are deterministic: no floating-point atomics; bit-identical run to run
+ *    for a fixed device count and fixed dispatch decisions (reading S26).
+ */
+#ifndef GVT_H
+#define GVT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GVT_OK = 0,
+    GVT_E_DIM = 1,          /* size mismatch / negative size                            */
+    GVT_E_INDEX = 2,        /* an id is outside [0, m) or [0, q)          */
+    GVT_E_HOMOGENEOUS = 3,  /* homogeneous kernel with T != NULL, or a term indexes a
+                               drug Gram with target ids                   */
+    GVT_E_KERNEL = 4,       /* unknown kernel name / malformed term                      */
+    GVT_E_PARAM = 5,        /* gamma <= 0 for Gaussian, lambda < 0, max_iter < 0, ...    */
+    GVT_E_BREAKDOWN = 6,    /* CG: p^T (K + lambda I) p <= 0; current iterate returned   */
+    GVT_E_CUDA = 7,         /* CUDA runtime error                                        */
+    GVT_E_NCCL = 8,         /* NCCL error or NCCL library unavailable                    */
+    GVT_E_OOM = 9,          /* device allocation failed                                  */
+    GVT_E_STATE = 10        /* NULL context / call not valid in this state               */
+} gvt_status;
+
+/* Pairwise kernels of Table 4b.  GAUSSIAN is the Kronecker kernel of
+ * Gaussian base Grams. */
+typedef enum {
+    GVT_LINEAR = 0, GVT_POLY2D = 1, GVT_GAUSSIAN = 2, GVT_KRONECKER = 3, GVT_SYMMETRIC = 4,
+    GVT_ANTISYMMETRIC = 5, GVT_RANKING = 6, GVT_MLPK = 7, GVT_CARTESIAN = 8
+} gvt_kernel;
+
+/* Base kernels on object features (POLY by the north star). */
+typedef enum { GVT_BASE_LINEAR = 0, GVT_BASE_GAUSSIAN = 1, GVT_BASE_POLY = 2 } gvt_base;
+
+/* Factor of a Kronecker term: drug Gram, target Gram, all-ones, identity. */
+typedef enum { GVT_FACTOR_DRUG = 0, GVT_FACTOR_TARGET = 1, GVT_FACTOR_ONES = 2, GVT_FACTOR_IDENTITY = 3 } gvt_factor;
+
+/* Element selectors: the action of the commutation (P) and unification (Q) operators on
+ * sampling operators, R(d,t)P = R(t,d), R(d,t)Q = R(d,d). */
+typedef enum { GVT_SEL_FIRST = 0, GVT_SEL_SECOND = 1 } gvt_selector;
+
+/* One permuted Kronecker term.  Its value for out pair o and in pair i is
+ *   coef * L[row_sel_left(o), col_sel_left(i)] * R[row_sel_right(o), col_sel_right(i)]
+ * with L = left, R = right factor. */
+typedef struct {
+    double coef;
+    int32_t left, right;                  /* gvt_factor */
+    int32_t row_sel_left, row_sel_right;  /* gvt_selector, applied to the OUT pair */
+    int32_t col_sel_left, col_sel_right;  /* gvt_selector, applied to the IN pair  */
+} gvt_term;
+
+typedef struct gvt_ctx gvt_ctx;
+
+/* Options (gvt_set_option). */
+typedef enum {
+    GVT_OPT_ENGINE = 0,          /* 0 = auto by density (default), 1 = sparse SIMT, 2 = dense tensor-core */
+    GVT_OPT_DENSE_THRESHOLD = 1, /* pair-matrix density at or above which auto picks dense (default 0.02) */
+    GVT_OPT_PROFILE = 2,         /* 1 = record per-kernel CUDA-event times (gvt_get_stats)                */
+    GVT_OPT_GRAM_ENGINE = 3      /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
+} gvt_option;
+
+/* Per-context counters (gvt_get_stats). */
+#define GVT_MAX_KERNEL_KINDS 32
+typedef struct {
+    int64_t launches;                         /* library kernels launched since reset                  */
+    int32_t n_kinds;                          /* valid entries below                                   */
+    char names[GVT_MAX_KERNEL_KINDS][32];     /* kernel kind name                                      */
+    int64_t counts[GVT_MAX_KERNEL_KINDS];     /* launches per kind                                     */
+    double ms[GVT_MAX_KERNEL_KINDS];          /* summed CUDA-event duration (GVT_OPT_PROFILE = 1)       */
+    int32_t last_engine;                      /* engine the last matvec group used: 1 sparse, 2 dense  */
+    int32_t world;                            /* communicator size (1 without gvt_comm_init)           */
+} gvt_stats;
+
+/* Create a context on CUDA device `device`, issuing work on `stream` (a cudaStream_t;
+ * NULL = the legacy default stream).  The context owns device workspaces (grown on
+ * demand, freed by gvt_destroy) and, after gvt_comm_init, an NCCL communicator. */
+gvt_status gvt_create(gvt_ctx **ctx, int device, void *stream);
+gvt_status gvt_destroy(gvt_ctx *ctx);
+gvt_status gvt_set_stream(gvt_ctx *ctx, void *stream);
+gvt_status gvt_set_option(gvt_ctx *ctx, gvt_option opt, double value);
+gvt_status gvt_get_stats(gvt_ctx *ctx, gvt_stats *out);
+gvt_status gvt_reset_stats(gvt_ctx *ctx);
+
+/* Multi-GPU (one process per GPU).  `nccl_unique_id` points to the 128-byte
+ * ncclUniqueId produced by gvt_nccl_unique_id on rank 0 and broadcast by the caller
+ * (e.g. with torch.distributed).  After this call pairwise_krr_fit / pairwise_predict /
+ * gvt_matvec run data-parallel: each rank passes ITS OWN SHARD of the in-sample pairs
+ * (and of y / a), the shards must be drug-partitioned by contiguous first-id ranges in
+ * rank order (gvt_partition computes them), D and T are replicated.  Stage 1 runs on
+ * the local pairs, the S column slabs are all-gathered over NVLink, stage 2 runs on the
+ * local out pairs, CG dot products are all-reduced. */
+gvt_status gvt_nccl_unique_id(void *out128);
+gvt_status gvt_comm_init(gvt_ctx *ctx, const void *nccl_unique_id, int rank, int world);
+
+/* Balanced contiguous drug ranges: given per-drug pair counts deg[m] (host), writes
+ * bounds[world+1] (host) with bounds[0] = 0, bounds[world] = m, each range holding about
+ * sum(deg)/world pairs (greedy prefix split).  Host-only, no device work. */
+gvt_status gvt_partition(const int64_t *deg, int64_t m, int world, int64_t *bounds);
+
+/* decompose: the Corollary's term list for `kernel` (
+ * MLPK 10-term expansion PAPER.md:736-747; Anti-symmetric as (I-P)(D(x)D), reading S3).
+ * `out` must hold 16 terms.  Host only. */
+gvt_status gvt_kernel_terms(gvt_kernel kernel, gvt_term *out, int *n_terms);
+
+/* Base-kernel Gram K[i][j] = k(X_i, X_j), X (m x dim), K (m x m):
+ * LINEAR <x,y>; GAUSSIAN exp(-gamma ||x-y||^2) (squared norm, reading S4; diagonal exactly
+ * 1); POLY (gamma <x,y> + coef0)^degree.  Errors: GVT_E_PARAM if gamma <= 0 (GAUSSIAN) or
+ * degree < 0 (POLY). */
+gvt_status gvt_gram(gvt_ctx *ctx, gvt_base kind, const float *X, int64_t m, int64_t dim,
+                    double gamma, double coef0, int degree, float *K);
+
+/* GVT matvec (Theorem 1; Corollary PAPER.md:634-653):
+ *   u[i] = sum_j sum_terms coef * L[.,.] * R[.,.] * a[j]
+ * over out pairs (out_first[i], out_second[i]), i < n_out, and in pairs
+ * (in_first[j], in_second[j]), j < n_in.  No lambda (reading S27).  `terms` is any
+ * term list (host); the Corollary lists of gvt_kernel_terms are recognised and run as
+ * fused normal forms, any other list runs term by term.  u is in caller order. */
+gvt_status gvt_matvec(gvt_ctx *ctx, const float *D, int64_t m, const float *T, int64_t q,
+                      const int32_t *out_first, const int32_t *out_second, int64_t n_out,
+                      const int32_t *in_first, const int32_t *in_second, int64_t n_in,
+                      const float *a, const gvt_term *terms, int n_terms, float *u);
+
+/* Kernel ridge regression (K + lambda I) a = y by conjugate
+ * gradients from a = 0 (reading S12-S14): max_iter iterations (rel_tol = 0) or until
+ * ||r_k|| / ||y|| <= rel_tol.  Each iteration is one GVT matvec.  CG scalars are fp64.
+ * iters_out (host, nullable) = iterations done; relres_hist (host, nullable,
+ * max_iter + 1 doubles) = ||r_k|| / ||y|| for k = 0..iters.  y == 0 gives a = 0 after 0
+ * iterations.  Breakdown (p^T A p <= 0) returns GVT_E_BREAKDOWN with the current iterate
+ * in a_out. */
+gvt_status pairwise_krr_fit(gvt_ctx *ctx, const float *D, int64_t m, const float *T, int64_t q,
+                            const int32_t *in_first, const int32_t *in_second, int64_t n,
+                            const float *y, const gvt_term *terms, int n_terms, double lambda,
+                            int max_iter, double rel_tol, float *a_out, int *iters_out,
+                            double *relres_hist);
+
+/* Prediction v = R(test) K R(train)^T a: scores[i] for test pair i,
+ * caller order. */
+gvt_status pairwise_predict(gvt_ctx *ctx, const float *D, int64_t m, const float *T, int64_t q,
+                            const int32_t *test_first, const int32_t *test_second, int64_t n_test,
+                            const int32_t *train_first, const int32_t *train_second, int64_t n_train,
+                            const float *a, const gvt_term *terms, int n_terms, float *scores);
+
+/* Integer plumbing exposed for bit-exact tests: stable sort of pair indices by first id
+ * (mode 0) or by (first, second) (mode 1), ties in ascending index order; perm[n] int32
+ * and row_ptr[m+1] int64 (first position of each first id).  Pointers host or device. */
+gvt_status gvt_sort_plan(gvt_ctx *ctx, const int32_t *first, const int32_t *second, int64_t n,
+                         int64_t m, int64_t q, int mode, int32_t *perm, int64_t *row_ptr);
+
+/* Thread-local message describing the last non-OK status. */
+const char *gvt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVT_H */

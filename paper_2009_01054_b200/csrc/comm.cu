@@ -1,0 +1,92 @@
+// comm.cu -- NCCL plumbing for the data-parallel path: all-gather of
+// the S column slabs and of the CG dot-product partials.  NCCL is loaded with dlopen at
+// gvt_comm_init time so single-GPU use never depends on it (the process may already have
+// torch's libnccl.so.2 loaded, which dlopen then reuses).
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include "ops.cuh"
+
+namespace gvt {
+
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi g_nccl;
+
+static void load_nccl() {
+    if (g_nccl.h) return;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    GVT_REQUIRE(h, GVT_E_NCCL, std::string("cannot dlopen libnccl.so.2: ") + dlerror());
+    g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    GVT_REQUIRE(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather, GVT_E_NCCL,
+                "libnccl.so.2 lacks a required symbol");
+    g_nccl.h = h;
+}
+
+#define NCCL_TRY(expr)                                                                                  \
+    do {                                                                                                \
+        ncclResult_t _r = (expr);                                                                       \
+        if (_r != ncclSuccess)                                                                          \
+            throw Error{GVT_E_NCCL, std::string(#expr) + ": " +                                         \
+                                        (g_nccl.GetErrorString ? g_nccl.GetErrorString(_r) : "error")}; \
+    } while (0)
+
+void nccl_unique_id(void *out128) {
+    load_nccl();
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NCCL_TRY(g_nccl.GetUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+}
+
+void comm_init(gvt_ctx *c, const void *id128, int rank, int world) {
+    GVT_REQUIRE(world >= 1 && rank >= 0 && rank < world, GVT_E_PARAM, "comm_init: bad rank/world");
+    if (world == 1) {
+        c->rank = 0;
+        c->world = 1;
+        return;
+    }
+    load_nccl();
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    NCCL_TRY(g_nccl.CommInitRank(&comm, world, id, rank));
+    c->nccl_comm = comm;
+    c->rank = rank;
+    c->world = world;
+}
+
+void comm_destroy(gvt_ctx *c) {
+    if (c->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
+    c->nccl_comm = nullptr;
+}
+
+// partials laid out [world][count]; each rank wrote its own slot; gather all slots so the
+// fixed-order reduction over world*count values gives bit-identical scalars on every rank
+void allreduce_partials(gvt_ctx *c, double *partials, int count) {
+    if (c->world <= 1) return;
+    NCCL_TRY(g_nccl.AllGather(partials + (size_t)c->rank * count, partials, (size_t)count, ncclFloat64,
+                              (ncclComm_t)c->nccl_comm, c->stream));
+}
+
+// S slabs laid out [world][slab_floats]; in-place all-gather of the local slab
+void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats) {
+    if (c->world <= 1) return;
+    NCCL_TRY(g_nccl.AllGather(S + (size_t)c->rank * slab_floats, S, slab_floats, ncclFloat32,
+                              (ncclComm_t)c->nccl_comm, c->stream));
+}
+
+}  // namespace gvt

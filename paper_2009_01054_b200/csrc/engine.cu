@@ -1,0 +1,602 @@
+// engine.cu -- orchestration of the GVT matvec for every pairwise kernel, the CG fit and
+// prediction.
+//
+// Every Corollary kernel is run through ONE "Kronecker group"
+//     G = A X C^T sampled at (r_k, c_k),   X = pair matrix built from p,
+// the GVT of Theorem 1 in variant-1 form (reading S2):
+//     stage 1  S = C X^T   (S[t][h] = sum_{entries (h, col)} x C[t][col])
+//     stage 2  G[r,c] = <A[r,:], S[c,:]>
+// plus cheap Ones-factor terms (Theorem 2).  Normal forms (derived from the
+// Corollary with the indexing rules PAPER.md:757-761; each equals the term sum exactly):
+//   Kronecker/Gaussian  A=D, C=T, X=B                      u = G[d,t]
+//   Symmetric           A=C=D, X=B+B^T                      u = G[d,d']
+//   Anti-symmetric      A=C=D, X=B-B^T      (I-P), S3       u = G[d,d']
+//   MLPK                A=C=D, X=L=diag(bF+bS)-B-B^T        u = G[d,d]+G[d',d']-2G[d,d']
+//   Poly2D              2*Kronecker + (D.^2 bF)[d] + (T.^2 bS)[t]
+//   Linear              (D bF)[d] + (T bS)[t]
+//   Ranking             g = D (bF - bS),  u = g[d] - g[d']  (oriented incidence)
+//   Cartesian           segment gathers over pairs sharing t / sharing d
+// with B[h,h'] = sum_{j: (d_j,t_j)=(h,h')} p_j, bF = B 1, bS = B^T 1.  Any other term
+// list runs term by term as groups (Ones / Identity factors materialised).
+#include <string.h>
+
+#include <vector>
+
+#include "ops.cuh"
+
+namespace gvt {
+
+void nccl_unique_id(void *out128);
+void comm_init(gvt_ctx *c, const void *id128, int rank, int world);
+void comm_destroy(gvt_ctx *c);
+void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats);
+
+// ----------------------------------------------------------------------------- decompose
+static gvt_term mk(double coef, int l, int r, int rl, int rr, int cl, int cr) {
+    gvt_term t;
+    t.coef = coef;
+    t.left = l;
+    t.right = r;
+    t.row_sel_left = rl;
+    t.row_sel_right = rr;
+    t.col_sel_left = cl;
+    t.col_sel_right = cr;
+    return t;
+}
+
+int kernel_terms(int kernel, gvt_term *o) {
+    const int F = GVT_SEL_FIRST, S = GVT_SEL_SECOND;
+    const int DR = GVT_FACTOR_DRUG, TA = GVT_FACTOR_TARGET, ON = GVT_FACTOR_ONES, ID = GVT_FACTOR_IDENTITY;
+    int n = 0;
+    switch (kernel) {
+    case GVT_LINEAR: o[n++] = mk(1, DR, ON, F, S, F, S); o[n++] = mk(1, ON, TA, F, S, F, S); break;
+    case GVT_POLY2D:
+        o[n++] = mk(1, DR, DR, F, F, F, F);
+        o[n++] = mk(2, DR, TA, F, S, F, S);
+        o[n++] = mk(1, TA, TA, S, S, S, S);
+        break;
+    case GVT_GAUSSIAN:
+    case GVT_KRONECKER: o[n++] = mk(1, DR, TA, F, S, F, S); break;
+    case GVT_CARTESIAN: o[n++] = mk(1, DR, ID, F, S, F, S); o[n++] = mk(1, ID, TA, F, S, F, S); break;
+    case GVT_SYMMETRIC: o[n++] = mk(1, DR, DR, F, S, F, S); o[n++] = mk(1, DR, DR, S, F, F, S); break;
+    case GVT_ANTISYMMETRIC: o[n++] = mk(1, DR, DR, F, S, F, S); o[n++] = mk(-1, DR, DR, S, F, F, S); break;
+    case GVT_RANKING:
+        o[n++] = mk(1, DR, ON, F, S, F, S);
+        o[n++] = mk(-1, DR, ON, S, F, F, S);
+        o[n++] = mk(-1, DR, ON, F, S, S, F);
+        o[n++] = mk(1, DR, ON, S, F, S, F);
+        break;
+    case GVT_MLPK:
+        o[n++] = mk(1, DR, DR, F, F, F, F);
+        o[n++] = mk(1, DR, DR, S, S, F, F);
+        o[n++] = mk(1, DR, DR, F, F, S, S);
+        o[n++] = mk(1, DR, DR, S, S, S, S);
+        o[n++] = mk(2, DR, DR, F, S, F, S);
+        o[n++] = mk(2, DR, DR, S, F, F, S);
+        o[n++] = mk(-2, DR, DR, F, F, F, S);
+        o[n++] = mk(-2, DR, DR, S, S, F, S);
+        o[n++] = mk(-2, DR, DR, F, S, F, F);
+        o[n++] = mk(-2, DR, DR, F, S, S, S);
+        break;
+    default: return -1;
+    }
+    return n;
+}
+
+enum Form { FORM_KRON = 0, FORM_SYM, FORM_ANTI, FORM_MLPK, FORM_POLY2D, FORM_LINEAR, FORM_RANKING, FORM_CARTESIAN,
+            FORM_GENERIC };
+
+static bool same_terms(const gvt_term *a, int na, const gvt_term *b, int nb) {
+    if (na != nb) return false;
+    for (int i = 0; i < na; i++) {
+        if (a[i].coef != b[i].coef || a[i].left != b[i].left || a[i].right != b[i].right ||
+            a[i].row_sel_left != b[i].row_sel_left || a[i].row_sel_right != b[i].row_sel_right ||
+            a[i].col_sel_left != b[i].col_sel_left || a[i].col_sel_right != b[i].col_sel_right)
+            return false;
+    }
+    return true;
+}
+
+static Form recognize(const gvt_term *terms, int n) {
+    gvt_term ref[16];
+    struct { int k; Form f; } tab[] = {{GVT_KRONECKER, FORM_KRON}, {GVT_SYMMETRIC, FORM_SYM},
+                                       {GVT_ANTISYMMETRIC, FORM_ANTI}, {GVT_MLPK, FORM_MLPK},
+                                       {GVT_POLY2D, FORM_POLY2D}, {GVT_LINEAR, FORM_LINEAR},
+                                       {GVT_RANKING, FORM_RANKING}, {GVT_CARTESIAN, FORM_CARTESIAN}};
+    for (auto &e : tab) {
+        int nr = kernel_terms(e.k, ref);
+        if (same_terms(terms, n, ref, nr)) return e.f;
+    }
+    return FORM_GENERIC;
+}
+
+static bool form_homogeneous(Form f) { return f == FORM_SYM || f == FORM_ANTI || f == FORM_MLPK || f == FORM_RANKING; }
+
+// ----------------------------------------------------------------------------- problem
+struct Problem {
+    int64_t m = 0, q = 0;  // q = m when homogeneous
+    bool hom = false;
+    Factor D, T;           // T aliases D when homogeneous
+    const int32_t *of = nullptr, *os = nullptr, *inf = nullptr, *ins = nullptr;
+    int64_t n_out = 0, n_in = 0;
+    int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
+};
+
+// validate a term list against the data (before any compute)
+static void validate_terms(const gvt_term *terms, int n_terms, bool hom, Form form) {
+    GVT_REQUIRE(terms && n_terms >= 1 && n_terms <= 64, GVT_E_KERNEL, "term list empty or too long");
+    if (form_homogeneous(form))
+        GVT_REQUIRE(hom, GVT_E_HOMOGENEOUS, "homogeneous kernel (Symmetric/Anti-symmetric/Ranking/MLPK) given T != NULL");
+    for (int i = 0; i < n_terms; i++) {
+        const gvt_term &t = terms[i];
+        int kinds[2] = {t.left, t.right}, rs[2] = {t.row_sel_left, t.row_sel_right},
+            cs[2] = {t.col_sel_left, t.col_sel_right};
+        for (int k = 0; k < 2; k++) {
+            GVT_REQUIRE(kinds[k] >= 0 && kinds[k] <= 3, GVT_E_KERNEL, "term factor kind out of range");
+            GVT_REQUIRE(rs[k] >= 0 && rs[k] <= 1 && cs[k] >= 0 && cs[k] <= 1, GVT_E_KERNEL, "term selector out of range");
+            if (!hom) {
+                if (kinds[k] == GVT_FACTOR_DRUG)
+                    GVT_REQUIRE(rs[k] == GVT_SEL_FIRST && cs[k] == GVT_SEL_FIRST, GVT_E_HOMOGENEOUS,
+                                "drug Gram indexed by target ids (heterogeneous data)");
+                if (kinds[k] == GVT_FACTOR_TARGET)
+                    GVT_REQUIRE(rs[k] == GVT_SEL_SECOND && cs[k] == GVT_SEL_SECOND, GVT_E_HOMOGENEOUS,
+                                "target Gram indexed by drug ids (heterogeneous data)");
+                if (kinds[k] == GVT_FACTOR_IDENTITY)
+                    GVT_REQUIRE(rs[k] == cs[k], GVT_E_HOMOGENEOUS, "identity between different domains");
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------- plan
+struct GroupPlan {
+    Factor A, C;           // stage-2 factor (left), stage-1 factor (right)
+    int64_t q_out = 0;     // rows of S (domain of the row-right selector)
+    int64_t m_in = 0;      // cols of S (domain of the col-left selector)
+    EntryPlan ent;
+    SamplePlan smp;
+    float coef = 1.f;
+    int engine = 1;        // 1 sparse, 2 dense
+    float *S = nullptr;
+    int64_t ldS = 0;
+};
+
+struct MatvecPlan {
+    Form form = FORM_GENERIC;
+    std::vector<GroupPlan> groups;  // generic: one per term; else at most one
+    EntryPlan byF, byS;            // segment plans (cheap terms / Cartesian)
+    float *buf = nullptr;          // MLPK sample buffer (n_out + m)
+    float *g1 = nullptr, *g2 = nullptr, *b1 = nullptr, *b2 = nullptr;
+    std::vector<Factor> owned;     // materialised Ones/Identity factors
+};
+
+static EntryKinds kinds1(int rs, int cs, float sign) {
+    EntryKinds k;
+    memset(&k, 0, sizeof(k));
+    k.count = 1;
+    k.k[0] = EntryKind{rs, cs, sign};
+    return k;
+}
+
+static Factor materialise(gvt_ctx *c, const char *name, int64_t n, int identity) {
+    Factor f;
+    f.n = n;
+    f.ld = round_up(n > 0 ? n : 1, 32);
+    float *p = wsT<float>(c, name, (size_t)round_up(n > 0 ? n : 1, 32) * f.ld);
+    fill_ones(c, p, round_up(n > 0 ? n : 1, 32), f.ld, identity);
+    f.p = p;
+    return f;
+}
+
+static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
+    if (c->engine == 1) return 1;
+    bool tc = tc_available(c);
+    if (c->engine == 2) {
+        GVT_REQUIRE(tc, GVT_E_CUDA, "dense tensor-core engine requested but not available on this device");
+        return 2;
+    }
+    double cells = (double)g.m_in * (double)g.C.n;
+    double density = cells > 0 ? (double)g.ent.nnz / cells : 0.0;
+    return (tc && density >= c->dense_threshold && g.m_in >= 128 && g.q_out >= 128) ? 2 : 1;
+}
+
+static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
+    g.engine = choose_engine(c, g);
+    g.ldS = round_up(g.m_in > 0 ? g.m_in : 1, 32);
+    std::string t(tag);
+    g.S = wsT<float>(c, (t + ".S").c_str(), (size_t)round_up(g.q_out > 0 ? g.q_out : 1, 128) * g.ldS);
+    if (g.engine == 2) bucket_samples(c, tag, g.smp, g.A.n, g.q_out);
+}
+
+static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int n_terms, Form form,
+                        MatvecPlan &mp) {
+    mp.form = form;
+    const int F = GVT_SEL_FIRST, Sx = GVT_SEL_SECOND;
+    auto group = [&](const Factor &A, const Factor &C, EntryKinds kinds, int64_t nrow, int64_t ncol, int rs, int cs,
+                     int64_t n_diag, float coef, const char *tag) {
+        GroupPlan g;
+        g.A = A;
+        g.C = C;
+        g.q_out = C.n;
+        g.m_in = nrow;
+        g.coef = coef;
+        std::string t(tag);
+        build_entry_plan(c, (t + ".e").c_str(), P.inf, P.ins, P.n_in, kinds, nrow, ncol, g.ent);
+        build_sample_plan(c, (t + ".s").c_str(), P.of, P.os, P.n_out, rs, cs, n_diag, A.n, g.smp);
+        finish_group(c, g, tag);
+        mp.groups.push_back(g);
+    };
+    switch (form) {
+    case FORM_KRON:
+        group(P.D, P.T, kinds1(F, Sx, 1.f), P.m, P.q, F, Sx, 0, 1.f, "g0");
+        break;
+    case FORM_POLY2D:
+        group(P.D, P.T, kinds1(F, Sx, 1.f), P.m, P.q, F, Sx, 0, 2.f, "g0");
+        build_entry_plan(c, "byS", P.inf, P.ins, P.n_in, kinds1(Sx, F, 1.f), P.q, P.m, mp.byS);
+        break;
+    case FORM_SYM:
+    case FORM_ANTI: {
+        EntryKinds k;
+        memset(&k, 0, sizeof(k));
+        k.count = 2;
+        k.k[0] = EntryKind{F, Sx, 1.f};
+        k.k[1] = EntryKind{Sx, F, form == FORM_SYM ? 1.f : -1.f};
+        group(P.D, P.D, k, P.m, P.m, F, Sx, 0, 1.f, "g0");
+        break;
+    }
+    case FORM_MLPK: {
+        EntryKinds k;
+        memset(&k, 0, sizeof(k));
+        k.count = 4;
+        k.k[0] = EntryKind{F, Sx, -1.f};
+        k.k[1] = EntryKind{Sx, F, -1.f};
+        k.k[2] = EntryKind{F, F, 1.f};
+        k.k[3] = EntryKind{Sx, Sx, 1.f};
+        group(P.D, P.D, k, P.m, P.m, F, Sx, P.m, 1.f, "g0");
+        mp.buf = wsT<float>(c, "mlpk.buf", (size_t)(P.n_out + P.m));
+        break;
+    }
+    case FORM_LINEAR:
+        build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kinds1(F, Sx, 1.f), P.m, P.q, mp.byF);
+        build_entry_plan(c, "byS", P.inf, P.ins, P.n_in, kinds1(Sx, F, 1.f), P.q, P.m, mp.byS);
+        break;
+    case FORM_RANKING: {
+        EntryKinds k;
+        memset(&k, 0, sizeof(k));
+        k.count = 2;
+        k.k[0] = EntryKind{F, Sx, 1.f};
+        k.k[1] = EntryKind{Sx, F, -1.f};
+        build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, k, P.m, P.m, mp.byF);
+        break;
+    }
+    case FORM_CARTESIAN:
+        build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kinds1(F, Sx, 1.f), P.m, P.q, mp.byF);
+        build_entry_plan(c, "byS", P.inf, P.ins, P.n_in, kinds1(Sx, F, 1.f), P.q, P.m, mp.byS);
+        break;
+    case FORM_GENERIC:
+        for (int i = 0; i < n_terms; i++) {
+            const gvt_term &t = terms[i];
+            auto factor = [&](int kind, int rs, int cs, const char *nm) -> Factor {
+                if (kind == GVT_FACTOR_DRUG) return P.D;
+                if (kind == GVT_FACTOR_TARGET) return P.T;
+                int64_t n = P.dom(rs) > P.dom(cs) ? P.dom(rs) : P.dom(cs);
+                Factor f = materialise(c, nm, n, kind == GVT_FACTOR_IDENTITY);
+                mp.owned.push_back(f);
+                return f;
+            };
+            char tag[32], nl[32], nr[32];
+            snprintf(tag, sizeof(tag), "t%d", i);
+            snprintf(nl, sizeof(nl), "t%d.L", i);
+            snprintf(nr, sizeof(nr), "t%d.R", i);
+            Factor L = factor(t.left, t.row_sel_left, t.col_sel_left, nl);
+            Factor R = factor(t.right, t.row_sel_right, t.col_sel_right, nr);
+            GroupPlan g;
+            g.A = L;
+            g.C = R;
+            g.q_out = P.dom(t.row_sel_right);
+            g.m_in = P.dom(t.col_sel_left);
+            g.coef = (float)t.coef;
+            std::string ts(tag);
+            build_entry_plan(c, (ts + ".e").c_str(), P.inf, P.ins, P.n_in, kinds1(t.col_sel_left, t.col_sel_right, 1.f),
+                             P.dom(t.col_sel_left), P.dom(t.col_sel_right), g.ent);
+            build_sample_plan(c, (ts + ".s").c_str(), P.of, P.os, P.n_out, t.row_sel_left, t.row_sel_right, 0,
+                              P.dom(t.row_sel_left), g.smp);
+            finish_group(c, g, tag);
+            mp.groups.push_back(g);
+        }
+        break;
+    }
+    int64_t nb = P.m > P.q ? P.m : P.q;
+    nb = round_up(nb > 0 ? nb : 1, 32);
+    if (form == FORM_POLY2D || form == FORM_LINEAR || form == FORM_RANKING) {
+        mp.b1 = wsT<float>(c, "cheap.b1", nb);
+        mp.b2 = wsT<float>(c, "cheap.b2", nb);
+        mp.g1 = wsT<float>(c, "cheap.g1", nb);
+        mp.g2 = wsT<float>(c, "cheap.g2", nb);
+        // b vectors are read up to ld (padded): zero them once, segment sums overwrite [0, nrow)
+        GVT_CUDA_TRY(cudaMemsetAsync(mp.b1, 0, sizeof(float) * nb, c->stream));
+        GVT_CUDA_TRY(cudaMemsetAsync(mp.b2, 0, sizeof(float) * nb, c->stream));
+    }
+}
+
+// ----------------------------------------------------------------------------- run
+static void run_group(gvt_ctx *c, GroupPlan &g, const float *p, float coef, int accumulate, float *out) {
+    entry_values(c, g.ent, p);
+    c->last_engine = g.engine;
+    if (g.engine == 2) {
+        // dense tensor-core engine: X densified (hi/lo), S = C X^T, sampled A S^T
+        int64_t ldX = round_up(g.C.n > 0 ? g.C.n : 1, 32);  // X: m_in x q_in
+        int64_t rows_pad = round_up(g.m_in > 0 ? g.m_in : 1, 128);
+        float *Xhi = wsT<float>(c, "dense.Xhi", (size_t)rows_pad * ldX);
+        float *Xlo = wsT<float>(c, "dense.Xlo", (size_t)rows_pad * ldX);
+        densify(c, g.ent, Xhi, Xlo, ldX, rows_pad);
+        int64_t qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
+        float *Shi = wsT<float>(c, "dense.Shi", (size_t)qpad * g.ldS);
+        float *Slo = wsT<float>(c, "dense.Slo", (size_t)qpad * g.ldS);
+        gemm_nt_split(c, g.C.hi, g.C.lo, g.C.ld, Xhi, Xlo, ldX, g.q_out, g.m_in, g.C.n, Shi, Slo, nullptr, g.ldS);
+        gemm_nt_sampled(c, g.A.hi, g.A.lo, g.A.ld, Shi, Slo, g.ldS, g.A.n, g.q_out, g.m_in, g.smp, coef, accumulate,
+                        out);
+    } else {
+        stage1_sparse(c, g.ent, g.C, g.q_out, g.S, g.ldS);
+        stage2_gather(c, g.smp, g.A, g.S, g.ldS, g.m_in, coef, accumulate, out);
+    }
+}
+
+static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p, float *u) {
+    switch (mp.form) {
+    case FORM_KRON:
+    case FORM_SYM:
+    case FORM_ANTI:
+        run_group(c, mp.groups[0], p, mp.groups[0].coef, 0, u);
+        break;
+    case FORM_MLPK:
+        run_group(c, mp.groups[0], p, 1.f, 0, mp.buf);
+        combine_mlpk(c, P.of, P.os, P.n_out, mp.buf, u);
+        break;
+    case FORM_POLY2D: {
+        GroupPlan &g = mp.groups[0];
+        run_group(c, g, p, 2.f, 0, u);
+        segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
+        entry_values(c, mp.byS, p);
+        segment_sum(c, mp.byS, mp.b2);          // bS
+        gemv(c, P.D, mp.b1, 1, mp.g1);          // D.^2 bF
+        gemv(c, P.T, mp.b2, 1, mp.g2);          // T.^2 bS
+        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
+        break;
+    }
+    case FORM_LINEAR:
+        entry_values(c, mp.byF, p);
+        segment_sum(c, mp.byF, mp.b1);
+        entry_values(c, mp.byS, p);
+        segment_sum(c, mp.byS, mp.b2);
+        gemv(c, P.D, mp.b1, 0, mp.g1);
+        gemv(c, P.T, mp.b2, 0, mp.g2);
+        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
+        break;
+    case FORM_RANKING:
+        entry_values(c, mp.byF, p);
+        segment_sum(c, mp.byF, mp.b1);          // bF - bS
+        gemv(c, P.D, mp.b1, 0, mp.g1);
+        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
+        break;
+    case FORM_CARTESIAN:
+        entry_values(c, mp.byF, p);
+        entry_values(c, mp.byS, p);
+        cartesian(c, P.of, P.os, P.n_out, mp.byF, mp.byS, P.D, P.T, u);
+        break;
+    case FORM_GENERIC:
+        for (size_t i = 0; i < mp.groups.size(); i++) run_group(c, mp.groups[i], p, mp.groups[i].coef, i > 0, u);
+        if (mp.groups.empty() && P.n_out > 0) GVT_CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(float) * P.n_out, c->stream));
+        break;
+    }
+}
+
+// ----------------------------------------------------------------------------- factors
+static Factor prepare_factor(gvt_ctx *c, const char *name, const float *user, int64_t n, bool need_split) {
+    Factor f;
+    f.n = n;
+    f.ld = round_up(n > 0 ? n : 1, 32);
+    int64_t rows_pad = round_up(n > 0 ? n : 1, 128);
+    std::string nm(name);
+    float *d = wsT<float>(c, (nm + ".pad").c_str(), (size_t)rows_pad * f.ld);
+    if (n > 0) {
+        const float *src = user;
+        if (!is_device_ptr(user)) {
+            float *tmp = wsT<float>(c, (nm + ".h2d").c_str(), (size_t)n * n);
+            GVT_CUDA_TRY(cudaMemcpyAsync(tmp, user, sizeof(float) * n * n, cudaMemcpyHostToDevice, c->stream));
+            src = tmp;
+        }
+        pad_copy(c, src, n, n, n, d, f.ld, rows_pad);
+    } else {
+        GVT_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(float) * rows_pad * f.ld, c->stream));
+    }
+    f.p = d;
+    if (need_split) {
+        float *hi = wsT<float>(c, (nm + ".hi").c_str(), (size_t)rows_pad * f.ld);
+        float *lo = wsT<float>(c, (nm + ".lo").c_str(), (size_t)rows_pad * f.ld);
+        split_tf32(c, d, rows_pad * f.ld, hi, lo);
+        f.hi = hi;
+        f.lo = lo;
+    }
+    return f;
+}
+
+// stage caller ids / vectors and validate ranges (before any compute)
+static const int32_t *stage_ids(gvt_ctx *c, const char *name, const int32_t *p, int64_t n) {
+    if (n == 0) return nullptr;
+    GVT_REQUIRE(p, GVT_E_DIM, std::string(name) + " is NULL with n > 0");
+    return (const int32_t *)stage_in(c, name, p, sizeof(int32_t) * n);
+}
+
+static void check_range(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound, const char *what) {
+    if (n == 0) return;
+    int64_t bad = count_out_of_range(c, ids, n, bound);
+    if (bad) throw Error{GVT_E_INDEX, std::string(what) + ": " + std::to_string(bad) + " id(s) out of range [0, " +
+                                          std::to_string(bound) + ")"};
+}
+
+struct OutArr {
+    float *dev = nullptr;
+    float *user = nullptr;
+    int64_t n = 0;
+    bool host = false;
+};
+
+static OutArr out_arr(gvt_ctx *c, const char *name, float *user, int64_t n) {
+    OutArr o;
+    o.user = user;
+    o.n = n;
+    if (n == 0) return o;
+    GVT_REQUIRE(user, GVT_E_DIM, std::string(name) + " is NULL with n > 0");
+    o.host = !is_device_ptr(user);
+    o.dev = o.host ? wsT<float>(c, name, n) : user;
+    return o;
+}
+
+static void out_finish(gvt_ctx *c, OutArr &o) {
+    if (o.host && o.n > 0) {
+        GVT_CUDA_TRY(cudaMemcpyAsync(o.user, o.dev, sizeof(float) * o.n, cudaMemcpyDeviceToHost, c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+}
+
+// does this plan need the 3xTF32 split of the factors (any dense group)?
+static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_in) {
+    if (!tc_available(c) || c->engine == 1) return false;
+    if (form == FORM_LINEAR || form == FORM_RANKING || form == FORM_CARTESIAN) return false;
+    if (c->engine == 2) return true;
+    double mult = (form == FORM_SYM || form == FORM_ANTI) ? 2.0 : (form == FORM_MLPK ? 4.0 : 1.0);
+    double cells = (form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC) ? (double)m * (double)q
+                                                                                     : (double)m * (double)m;
+    return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold && m >= 128 && q >= 128;
+}
+
+static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, const float *T, int64_t q,
+                          const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
+                          const int32_t *ins, int64_t n_in, const gvt_term *terms, int n_terms, Form &form) {
+    GVT_REQUIRE(m >= 0 && n_out >= 0 && n_in >= 0, GVT_E_DIM, "negative size");
+    P.hom = (T == nullptr);
+    P.m = m;
+    P.q = P.hom ? m : q;
+    GVT_REQUIRE(P.q >= 0, GVT_E_DIM, "negative q");
+    GVT_REQUIRE(m == 0 || D, GVT_E_DIM, "D is NULL with m > 0");
+    form = recognize(terms, n_terms);
+    validate_terms(terms, n_terms, P.hom, form);
+    P.n_out = n_out;
+    P.n_in = n_in;
+    P.of = stage_ids(c, "in.of", of, n_out);
+    P.os = stage_ids(c, "in.os", os, n_out);
+    P.inf = (inf == of && ins == os && n_in == n_out) ? P.of : stage_ids(c, "in.inf", inf, n_in);
+    P.ins = (inf == of && ins == os && n_in == n_out) ? P.os : stage_ids(c, "in.ins", ins, n_in);
+    check_range(c, P.of, n_out, P.m, "out first ids");
+    check_range(c, P.os, n_out, P.q, "out second ids");
+    if (P.inf != P.of) {
+        check_range(c, P.inf, n_in, P.m, "in first ids");
+        check_range(c, P.ins, n_in, P.q, "in second ids");
+    }
+    bool split = needs_split(c, form, P.m, P.q, n_in);
+    P.D = prepare_factor(c, "fD", D, m, split);
+    P.T = P.hom ? P.D : prepare_factor(c, "fT", T, q, split);
+}
+
+// ----------------------------------------------------------------------------- entry points
+void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of, const int32_t *os,
+            int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in, const float *a,
+            const gvt_term *terms, int n_terms, float *u) {
+    Problem P;
+    Form form;
+    setup_problem(c, P, D, m, T, q, of, os, n_out, inf, ins, n_in, terms, n_terms, form);
+    OutArr uo = out_arr(c, "out.u", u, n_out);
+    if (n_out == 0) return;
+    const float *ad = n_in ? (const float *)stage_in(c, "in.a", a, sizeof(float) * n_in) : nullptr;
+    GVT_REQUIRE(n_in == 0 || ad, GVT_E_DIM, "a is NULL with n_in > 0");
+    if (n_in == 0) {
+        GVT_CUDA_TRY(cudaMemsetAsync(uo.dev, 0, sizeof(float) * n_out, c->stream));
+    } else {
+        MatvecPlan mp;
+        plan_matvec(c, P, terms, n_terms, form, mp);
+        run_matvec(c, P, mp, ad, uo.dev);
+    }
+    out_finish(c, uo);
+}
+
+void predict(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *tf, const int32_t *ts,
+             int64_t n_test, const int32_t *trf, const int32_t *trs, int64_t n_train, const float *a,
+             const gvt_term *terms, int n_terms, float *scores) {
+    matvec(c, D, m, T, q, tf, ts, n_test, trf, trs, n_train, a, terms, n_terms, scores);
+}
+
+gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
+               int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
+               double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
+    GVT_REQUIRE(lambda >= 0.0, GVT_E_PARAM, "lambda < 0");
+    GVT_REQUIRE(max_iter >= 0, GVT_E_PARAM, "max_iter < 0");
+    GVT_REQUIRE(rel_tol >= 0.0, GVT_E_PARAM, "rel_tol < 0");
+    Problem P;
+    Form form;
+    setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form);
+    OutArr ao = out_arr(c, "out.a", a_out, n);
+    const float *yd = n ? (const float *)stage_in(c, "in.y", y, sizeof(float) * n) : nullptr;
+    GVT_REQUIRE(n == 0 || yd, GVT_E_DIM, "y is NULL with n > 0");
+    const int ST_N = 9;
+    double *state = wsT<double>(c, "cg.state", (size_t)ST_N + max_iter + 1);
+    if (n == 0) {
+        if (iters_out) *iters_out = 0;
+        if (relres_hist) relres_hist[0] = 0.0;
+        return GVT_OK;
+    }
+    float *x = ao.dev;
+    float *r = wsT<float>(c, "cg.r", n), *p = wsT<float>(c, "cg.p", n), *Ap = wsT<float>(c, "cg.Ap", n);
+    MatvecPlan mp;
+    plan_matvec(c, P, terms, n_terms, form, mp);
+    cg_init(c, yd, n, x, r, p, state, rel_tol);
+    double *hstate = (double *)pinned(c, sizeof(double) * 16);
+    for (int it = 0; it < max_iter; it++) {
+        run_matvec(c, P, mp, p, Ap);
+        cg_after_matvec(c, Ap, p, n, lambda, state);
+        cg_update(c, x, r, p, Ap, n, state, it, nullptr);
+        if (rel_tol > 0.0) {  // residual mode: host decides whether to continue
+            GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
+            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            if (hstate[5] != 0.0 || hstate[6] != 0.0) break;
+        }
+    }
+    // scalars back (one sync per fit)
+    GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
+    if (relres_hist) {
+        double *hh = wsT<double>(c, "cg.hist_dummy", 1);
+        (void)hh;
+        GVT_CUDA_TRY(cudaMemcpyAsync(relres_hist, state + ST_N, sizeof(double) * (max_iter + 1),
+                                     cudaMemcpyDeviceToHost, c->stream));
+    }
+    out_finish(c, ao);
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int iters = (int)hstate[7];
+    if (iters_out) *iters_out = iters;
+    if (relres_hist)
+        for (int k = iters + 1; k <= max_iter; k++) relres_hist[k] = 0.0 / 0.0;
+    if (hstate[6] != 0.0) {
+        set_error("CG breakdown: p^T (K + lambda I) p = %g <= 0 at iteration %d", hstate[4], iters + 1);
+        return GVT_E_BREAKDOWN;
+    }
+    return GVT_OK;
+}
+
+void gram(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
+          float *K) {
+    GVT_REQUIRE(m >= 0 && dim >= 0, GVT_E_DIM, "negative size");
+    GVT_REQUIRE(kind >= 0 && kind <= 2, GVT_E_PARAM, "unknown base kernel");
+    GVT_REQUIRE(kind != GVT_BASE_GAUSSIAN || gamma > 0.0, GVT_E_PARAM, "Gaussian base kernel needs gamma > 0");
+    GVT_REQUIRE(kind != GVT_BASE_POLY || degree >= 0, GVT_E_PARAM, "polynomial base kernel needs degree >= 0");
+    if (m == 0) return;
+    GVT_REQUIRE(X && K, GVT_E_DIM, "X or K is NULL");
+    const float *Xd = dim ? (const float *)stage_in(c, "in.X", X, sizeof(float) * m * dim) : nullptr;
+    OutArr ko = out_arr(c, "out.K", K, m * m);
+    bool use_tc = tc_available(c) && c->gram_engine != 1 && dim > 0;
+    if (c->gram_engine == 2) GVT_REQUIRE(tc_available(c), GVT_E_CUDA, "tensor-core Gram requested but unavailable");
+    if (use_tc) gram_tc(c, kind, Xd, m, dim, gamma, coef0, degree, ko.dev, m);
+    else gram_simt(c, kind, Xd, m, dim, dim, gamma, coef0, degree, ko.dev, m);
+    out_finish(c, ko);
+}
+
+}  // namespace gvt

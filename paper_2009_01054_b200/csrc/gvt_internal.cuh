@@ -1,0 +1,150 @@
+// gvt_internal.cuh -- shared internals of libgvt.so (context, workspaces, launch
+// accounting, error helpers).  Not part of the ABI (see include/gvt.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/gvt.h"
+
+namespace gvt {
+
+// ----------------------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+
+struct Error {
+    gvt_status code;
+    std::string msg;
+};
+
+#define GVT_CUDA_TRY(expr)                                                                         \
+    do {                                                                                           \
+        cudaError_t _e = (expr);                                                                   \
+        if (_e != cudaSuccess) {                                                                   \
+            if (_e == cudaErrorMemoryAllocation)                                                   \
+                throw ::gvt::Error{GVT_E_OOM, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+            throw ::gvt::Error{GVT_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)};    \
+        }                                                                                          \
+    } while (0)
+
+#define GVT_REQUIRE(cond, code, text)                          \
+    do {                                                       \
+        if (!(cond)) throw ::gvt::Error{(code), std::string(text)}; \
+    } while (0)
+
+// ----------------------------------------------------------------------------- kernels kinds
+enum KernelKind {
+    K_GRAM_SIMT = 0,
+    K_GRAM_TC,
+    K_SPLIT,
+    K_PAD_COPY,
+    K_PLAN_KEYS,
+    K_PLAN_SORT,
+    K_PLAN_ROWPTR,
+    K_PLAN_GATHER,
+    K_STAGE1_SPARSE,
+    K_STAGE2_GATHER,
+    K_DENSIFY,
+    K_STAGE1_TC,
+    K_STAGE2_TC,
+    K_SEGSUM,
+    K_GEMV,
+    K_COMBINE,
+    K_CARTESIAN,
+    K_CG_VEC,
+    K_CG_SCALAR,
+    K_FILL,
+    K_NUM_KINDS
+};
+const char *kind_name(int k);
+
+// ----------------------------------------------------------------------------- device buffer
+struct Buf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct PendingEvent {
+    int kind;
+    cudaEvent_t start, stop;
+};
+
+}  // namespace gvt
+
+struct gvt_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    int cc_major = 0, cc_minor = 0;
+    bool tc_ok = false;  // tcgen05 path usable (sm_100)
+
+    // options
+    int engine = 0;  // 0 auto, 1 sparse, 2 dense
+    double dense_threshold = 0.02;
+    int profile = 0;
+    int gram_engine = 0;
+    int last_engine = 0;
+
+    // workspaces by name (grow-only)
+    std::unordered_map<std::string, gvt::Buf> bufs;
+
+    // launch accounting
+    int64_t launches = 0;
+    int64_t counts[gvt::K_NUM_KINDS] = {0};
+    double ms[gvt::K_NUM_KINDS] = {0};
+    std::vector<gvt::PendingEvent> pending;
+    std::vector<cudaEvent_t> event_pool;
+
+    // multi-GPU
+    void *nccl_comm = nullptr;
+    int rank = 0, world = 1;
+
+    // pinned host scratch for scalar read-backs
+    void *pinned = nullptr;
+    size_t pinned_bytes = 0;
+};
+
+namespace gvt {
+
+// workspace with at least `bytes`; contents undefined.  Same name => same buffer (realloc on grow).
+void *ws(gvt_ctx *c, const char *name, size_t bytes);
+template <typename T>
+T *wsT(gvt_ctx *c, const char *name, size_t count) {
+    return reinterpret_cast<T *>(ws(c, name, (count ? count : 1) * sizeof(T)));
+}
+void *pinned(gvt_ctx *c, size_t bytes);
+
+// launch accounting: call around every kernel launch
+void launch_begin(gvt_ctx *c, int kind, cudaEvent_t *ev_start);
+void launch_end(gvt_ctx *c, int kind, cudaEvent_t ev_start);
+void collect_events(gvt_ctx *c);  // synchronises pending profile events
+
+#define GVT_LAUNCH(ctx, kind, kernel, grid, block, smem, ...)                      \
+    do {                                                                           \
+        cudaEvent_t _ev0 = nullptr;                                                \
+        ::gvt::launch_begin((ctx), (kind), &_ev0);                                 \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);           \
+        GVT_CUDA_TRY(cudaGetLastError());                                          \
+        ::gvt::launch_end((ctx), (kind), _ev0);                                    \
+    } while (0)
+
+// host/device classification of a caller pointer
+bool is_device_ptr(const void *p);
+
+// stage a caller array on the device: returns a device pointer (caller's if already
+// device memory, else a workspace copy made on the context stream)
+const void *stage_in(gvt_ctx *c, const char *name, const void *p, size_t bytes);
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline unsigned grid1d(int64_t n, int threads, int64_t cap = 1 << 30) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+}  // namespace gvt

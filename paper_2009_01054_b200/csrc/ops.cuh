@@ -1,0 +1,107 @@
+// ops.cuh -- launchers of the device kernels (internal).  Every launcher issues on
+// ctx->stream and goes through GVT_LAUNCH (launch count + optional event timing).
+#pragma once
+#include "gvt_internal.cuh"
+
+namespace gvt {
+
+// A square factor (Gram / materialised ones / identity) copied to a padded device
+// buffer: n x n, leading dimension ld = round_up(n, 32), padding zero.  For the dense
+// tensor-core engine the 3xTF32 split hi/lo (same layout) is attached on demand.
+struct Factor {
+    const float *p = nullptr;
+    int64_t n = 0, ld = 0;
+    const float *hi = nullptr, *lo = nullptr;
+};
+
+// one entry kind of the pair matrix X (row selector, column selector, sign), see engine.cu
+struct EntryKind {
+    int row_sel, col_sel;
+    float sign;
+};
+struct EntryKinds {
+    int count;
+    EntryKind k[4];
+};
+
+// X entries sorted by (row, col, entry index): CSR over rows
+struct EntryPlan {
+    int64_t nnz = 0, nrow = 0, ncol = 0;
+    int32_t *row = nullptr, *col = nullptr, *src = nullptr;
+    float *sign = nullptr;
+    int64_t *row_ptr = nullptr;  // nrow + 1
+    float *val = nullptr;        // per-iteration values sign * p[src]
+};
+
+// samples (r, c) of G = A X C^T sorted by r; result of sample k goes to dst[k]
+struct SamplePlan {
+    int64_t ns = 0;
+    int32_t *r = nullptr, *c = nullptr, *dst = nullptr;
+    // dense engine: samples bucketed by (r-tile, c-tile); tile_ptr over tiles
+    int64_t n_rt = 0, n_ct = 0;
+    int64_t *tile_ptr = nullptr;
+};
+
+// ---- plumbing (plan.cu)
+void pad_copy(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t ld_src, float *dst, int64_t ld_dst,
+              int64_t rows_pad);
+void fill_ones(gvt_ctx *c, float *dst, int64_t n, int64_t ld, int identity);
+void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n,
+                      const EntryKinds &kinds, int64_t nrow, int64_t ncol, EntryPlan &out);
+// samples from an out-sample: kind 0: (sel(rs, i), sel(cs, i)) for i < n; plus (x,x) for x < n_diag
+void build_sample_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n, int row_sel,
+                       int col_sel, int64_t n_diag, int64_t nrow, SamplePlan &out);
+void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int mode,
+                     int32_t *perm, int64_t *row_ptr);
+// validation helper: returns number of ids outside [0, bound) (device reduction, syncs)
+int64_t count_out_of_range(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound);
+
+// ---- sparse engine (sparse.cu)
+void entry_values(gvt_ctx *c, const EntryPlan &e, const float *p);
+void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS);
+void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const float *S, int64_t ldS, int64_t K,
+                   float coef, int accumulate, float *out);
+void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)
+void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y);
+// u[i] (+)= c1 * g1[sel(rs1,i)] + c2 * g2[sel(rs2,i)]   (g2 nullable)
+void combine_gather(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *g1, int rs1, float c1,
+                    const float *g2, int rs2, float c2, int accumulate, float *u);
+// MLPK: u[i] = buf[n + f_i] + buf[n + s_i] - 2 buf[i]
+void combine_mlpk(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *buf, float *u);
+void cartesian(gvt_ctx *c, const int32_t *of, const int32_t *os, int64_t n_out, const EntryPlan &by_first,
+               const EntryPlan &by_second, const Factor &D, const Factor &T, float *u);
+void scale_copy(gvt_ctx *c, const float *x, float alpha, int64_t n, float *y);
+
+// ---- dense tensor-core engine (dense_tc.cu)
+bool tc_available(gvt_ctx *c);
+void split_tf32(gvt_ctx *c, const float *x, int64_t count, float *hi, float *lo);
+void densify(gvt_ctx *c, const EntryPlan &e, float *Xhi, float *Xlo, int64_t ldX, int64_t rows_pad);
+// S (rows x cols, ld) = C (rows x K) * X^T (X: cols x K), 3xTF32, writes S_hi/S_lo
+void gemm_nt_split(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
+                   int64_t ldb, int64_t M, int64_t N, int64_t K, float *Chi, float *Clo, float *Cf, int64_t ldc);
+// sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
+void gemm_nt_sampled(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi,
+                     const float *Blo, int64_t ldb, int64_t M, int64_t N, int64_t K, const SamplePlan &sp,
+                     float coef, int accumulate, float *out);
+void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol);
+
+// ---- Gram (gram.cu)
+void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, int64_t ldx, double gamma,
+               double coef0, int degree, float *K, int64_t ldk);
+void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
+             float *K, int64_t ldk);
+
+// ---- CG (cg.cu)
+struct CGState;  // device
+void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, double *state, double rel_tol);
+void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state);
+void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_t n, double *state, int iter,
+               double *relres_dev);
+// multi-GPU hook: reduce a partial-sum vector across ranks (no-op at world 1)
+void allreduce_partials(gvt_ctx *c, double *partials, int count);
+
+// partial-sum layout (cg.cu)
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int RED_THREADS = 256;
+
+}  // namespace gvt

@@ -1,0 +1,229 @@
+// plan.cu -- integer plumbing of the hot path: factor padding,
+// stable sorts of pair/entry lists (CUB radix sort, stable => ties keep index order),
+// CSR row pointers, sample ordering.  Everything here is integer work and bit-exact.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "ops.cuh"
+
+namespace gvt {
+
+// ----------------------------------------------------------------------------- padding
+__global__ void k_pad_copy(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
+                           float *__restrict__ dst, int64_t ld_dst, int64_t rows_pad) {
+    int64_t total = rows_pad * ld_dst;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / ld_dst, cc = i - r * ld_dst;
+        dst[i] = (r < rows && cc < cols) ? src[r * ld_src + cc] : 0.0f;
+    }
+}
+
+void pad_copy(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t ld_src, float *dst, int64_t ld_dst,
+              int64_t rows_pad) {
+    int64_t total = rows_pad * ld_dst;
+    if (total == 0) return;
+    GVT_LAUNCH(c, K_PAD_COPY, k_pad_copy, grid1d(total, 256, 8 * c->sm_count * 8), 256, 0, src, rows, cols, ld_src,
+               dst, ld_dst, rows_pad);
+}
+
+__global__ void k_fill_ones(float *dst, int64_t n, int64_t ld, int identity) {
+    int64_t total = n * ld;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / ld, cc = i - r * ld;
+        float v = 0.f;
+        if (cc < n) v = identity ? (r == cc ? 1.f : 0.f) : 1.f;
+        dst[i] = v;
+    }
+}
+
+void fill_ones(gvt_ctx *c, float *dst, int64_t n, int64_t ld, int identity) {
+    if (n == 0) return;
+    GVT_LAUNCH(c, K_FILL, k_fill_ones, grid1d(n * ld, 256, 8 * c->sm_count * 8), 256, 0, dst, n, ld, identity);
+}
+
+// ----------------------------------------------------------------------------- sorting helpers
+static int key_bits(uint64_t max_key) {
+    int b = 1;
+    while (b < 64 && (max_key >> b)) b++;
+    return b;
+}
+
+template <typename K>
+static void radix_sort_pairs(gvt_ctx *c, const char *tag, const K *keys_in, K *keys_out, const int32_t *vals_in,
+                             int32_t *vals_out, int64_t n, int end_bit) {
+    if (n == 0) return;
+    GVT_REQUIRE(n < (int64_t)INT32_MAX, GVT_E_DIM, "sort: more than 2^31-1 entries");
+    size_t temp = 0;
+    GVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out, vals_in, vals_out, (int)n, 0,
+                                                 end_bit, c->stream));
+    std::string nm = std::string(tag) + ".cubtmp";
+    void *t = ws(c, nm.c_str(), temp);
+    cudaEvent_t ev;
+    launch_begin(c, K_PLAN_SORT, &ev);
+    GVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(t, temp, keys_in, keys_out, vals_in, vals_out, (int)n, 0, end_bit,
+                                                 c->stream));
+    launch_end(c, K_PLAN_SORT, ev);
+}
+
+__device__ __forceinline__ int32_t pick(int sel, const int32_t *f, const int32_t *s, int64_t j) {
+    return sel == 0 ? f[j] : s[j];
+}
+
+// entry e = kind * n + j  ->  key (row * ncol + col), value e
+__global__ void k_entry_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, EntryKinds kinds,
+                             int64_t ncol, uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    int64_t E = n * kinds.count;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        int kind = (int)(e / n);
+        int64_t j = e - (int64_t)kind * n;
+        int64_t row = pick(kinds.k[kind].row_sel, f, s, j);
+        int64_t col = pick(kinds.k[kind].col_sel, f, s, j);
+        keys[e] = (uint64_t)(row * ncol + col);
+        vals[e] = (int32_t)e;
+    }
+}
+
+__global__ void k_entry_gather(const uint64_t *__restrict__ skeys, const int32_t *__restrict__ svals, int64_t E,
+                               int64_t n, EntryKinds kinds, int64_t ncol, int32_t *__restrict__ row,
+                               int32_t *__restrict__ col, int32_t *__restrict__ src, float *__restrict__ sign) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t e = svals[k];
+        int kind = (int)(e / n);
+        uint64_t key = skeys[k];
+        row[k] = (int32_t)(key / (uint64_t)ncol);
+        col[k] = (int32_t)(key % (uint64_t)ncol);
+        src[k] = (int32_t)(e - (int64_t)kind * n);
+        sign[k] = kinds.k[kind].sign;
+    }
+}
+
+// row_ptr[h] = first position k with row[k] >= h  (rows sorted ascending)
+__global__ void k_row_ptr(const int32_t *__restrict__ row, int64_t E, int64_t nrow, int64_t *__restrict__ row_ptr) {
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h <= nrow; h += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = E;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (row[mid] < h) lo = mid + 1;
+            else hi = mid;
+        }
+        row_ptr[h] = lo;
+    }
+}
+
+void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n,
+                      const EntryKinds &kinds, int64_t nrow, int64_t ncol, EntryPlan &out) {
+    std::string t(tag);
+    int64_t E = n * kinds.count;
+    out.nnz = E;
+    out.nrow = nrow;
+    out.ncol = ncol;
+    out.row = wsT<int32_t>(c, (t + ".row").c_str(), E);
+    out.col = wsT<int32_t>(c, (t + ".col").c_str(), E);
+    out.src = wsT<int32_t>(c, (t + ".src").c_str(), E);
+    out.sign = wsT<float>(c, (t + ".sign").c_str(), E);
+    out.val = wsT<float>(c, (t + ".val").c_str(), E);
+    out.row_ptr = wsT<int64_t>(c, (t + ".rowptr").c_str(), nrow + 1);
+    if (E > 0) {
+        uint64_t *k0 = wsT<uint64_t>(c, "plan.keys0", E), *k1 = wsT<uint64_t>(c, "plan.keys1", E);
+        int32_t *v0 = wsT<int32_t>(c, "plan.vals0", E), *v1 = wsT<int32_t>(c, "plan.vals1", E);
+        GVT_LAUNCH(c, K_PLAN_KEYS, k_entry_keys, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, f, s, n, kinds, ncol,
+                   k0, v0);
+        int bits = key_bits((uint64_t)(nrow * ncol > 0 ? nrow * ncol - 1 : 0));
+        radix_sort_pairs<uint64_t>(c, "plan", k0, k1, v0, v1, E, bits);
+        GVT_LAUNCH(c, K_PLAN_GATHER, k_entry_gather, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, k1, v1, E, n,
+                   kinds, ncol, out.row, out.col, out.src, out.sign);
+    }
+    GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(nrow + 1, 256), 256, 0, out.row, E, nrow, out.row_ptr);
+}
+
+// samples: k < n -> (sel(rs, k), sel(cs, k)) ; n <= k < n + n_diag -> (k - n, k - n)
+__global__ void k_sample_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, int rs, int cs,
+                              int64_t n_diag, uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    int64_t N = n + n_diag;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
+        keys[k] = k < n ? (uint32_t)pick(rs, f, s, k) : (uint32_t)(k - n);
+        vals[k] = (int32_t)k;
+    }
+}
+
+__global__ void k_sample_gather(const uint32_t *__restrict__ skeys, const int32_t *__restrict__ svals, int64_t N,
+                                const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, int cs,
+                                int32_t *__restrict__ r, int32_t *__restrict__ cc, int32_t *__restrict__ dst) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = svals[k];
+        r[k] = (int32_t)skeys[k];
+        cc[k] = i < n ? pick(cs, f, s, i) : (int32_t)(i - n);
+        dst[k] = (int32_t)i;
+    }
+}
+
+void build_sample_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n, int row_sel,
+                       int col_sel, int64_t n_diag, int64_t nrow, SamplePlan &out) {
+    std::string t(tag);
+    int64_t N = n + n_diag;
+    out.ns = N;
+    out.r = wsT<int32_t>(c, (t + ".r").c_str(), N);
+    out.c = wsT<int32_t>(c, (t + ".c").c_str(), N);
+    out.dst = wsT<int32_t>(c, (t + ".dst").c_str(), N);
+    out.tile_ptr = nullptr;
+    if (N == 0) return;
+    uint32_t *k0 = wsT<uint32_t>(c, "splan.keys0", N), *k1 = wsT<uint32_t>(c, "splan.keys1", N);
+    int32_t *v0 = wsT<int32_t>(c, "splan.vals0", N), *v1 = wsT<int32_t>(c, "splan.vals1", N);
+    GVT_LAUNCH(c, K_PLAN_KEYS, k_sample_keys, grid1d(N, 256, 16 * c->sm_count * 8), 256, 0, f, s, n, row_sel,
+               col_sel, n_diag, k0, v0);
+    radix_sort_pairs<uint32_t>(c, "splan", k0, k1, v0, v1, N, key_bits((uint64_t)(nrow > 0 ? nrow - 1 : 0)));
+    GVT_LAUNCH(c, K_PLAN_GATHER, k_sample_gather, grid1d(N, 256, 16 * c->sm_count * 8), 256, 0, k1, v1, N, f, s, n,
+               col_sel, out.r, out.c, out.dst);
+}
+
+// ----------------------------------------------------------------------------- debug sort (ABI gvt_sort_plan)
+__global__ void k_debug_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, int mode,
+                             int64_t q, uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        keys[j] = mode == 1 ? (uint64_t)((int64_t)f[j] * q + s[j]) : (uint64_t)f[j];
+        vals[j] = (int32_t)j;
+    }
+}
+
+__global__ void k_debug_rows(const uint64_t *__restrict__ k, int64_t n, int mode, int64_t q, int32_t *__restrict__ row) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        row[j] = (int32_t)(mode == 1 ? k[j] / (uint64_t)q : k[j]);
+}
+
+void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int mode,
+                     int32_t *perm, int64_t *row_ptr) {
+    uint64_t *k0 = wsT<uint64_t>(c, "plan.keys0", n), *k1 = wsT<uint64_t>(c, "plan.keys1", n);
+    int32_t *v0 = wsT<int32_t>(c, "plan.vals0", n);
+    int32_t *rows = wsT<int32_t>(c, "dbg.rows", n);
+    if (n > 0) {
+        GVT_LAUNCH(c, K_PLAN_KEYS, k_debug_keys, grid1d(n, 256, 4096), 256, 0, f, s, n, mode, q, k0, v0);
+        uint64_t maxk = mode == 1 ? (uint64_t)(m * q) : (uint64_t)m;
+        radix_sort_pairs<uint64_t>(c, "plan", k0, k1, v0, perm, n, key_bits(maxk));
+        GVT_LAUNCH(c, K_PLAN_GATHER, k_debug_rows, grid1d(n, 256, 4096), 256, 0, k1, n, mode, q, rows);
+    }
+    GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(m + 1, 256), 256, 0, rows, n, m, row_ptr);
+}
+
+// ----------------------------------------------------------------------------- validation
+__global__ void k_count_oor(const int32_t *__restrict__ ids, int64_t n, int64_t bound, unsigned long long *cnt) {
+    unsigned long long local = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = ids[i];
+        local += (v < 0 || v >= bound) ? 1ull : 0ull;
+    }
+    // warp reduce then one integer atomic per warp (integer: order-independent)
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(cnt, local);
+}
+
+int64_t count_out_of_range(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound) {
+    if (n == 0) return 0;
+    unsigned long long *d = wsT<unsigned long long>(c, "val.cnt", 1);
+    GVT_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream));
+    GVT_LAUNCH(c, K_FILL, k_count_oor, grid1d(n, 256, 4 * c->sm_count * 8), 256, 0, ids, n, bound, d);
+    unsigned long long *h = (unsigned long long *)pinned(c, 64);
+    GVT_CUDA_TRY(cudaMemcpyAsync(h, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return (int64_t)*h;
+}
+
+}  // namespace gvt

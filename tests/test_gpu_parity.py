@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same seeded
+inputs (-m gpu).  Tolerances are the north star's (BASELINE.json): index plumbing
+bit-exact; fp32 matvec relative L2 <= 1e-5; CG weights after 50 iterations relative L2
+<= 1e-4 and predictions max-abs <= 1e-4 on C1 (reading S30); Gram max error relative to
+max |entry| <= 1e-6.  Full-size configs are checked on sampled outputs
+the oracle computes one by one, in the launch configuration bench.py times."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2009_01054_b200 as G
+
+K_ALL = [G.LINEAR, G.POLY2D, G.GAUSSIAN, G.KRONECKER, G.SYMMETRIC, G.ANTISYMMETRIC, G.RANKING, G.MLPK,
+         G.CARTESIAN]
+HOM = G.HOMOGENEOUS_KERNELS
+MATVEC_TOL = 1e-5
+
+
+def dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x, np.float64), np.asarray(ref, np.float64)
+    nr = np.linalg.norm(ref)
+    return np.linalg.norm(x - ref) / (nr if nr > 1e-30 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = G.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(params=[G.ENGINE_SPARSE, G.ENGINE_AUTO], ids=["sparse", "auto"])
+def engine_ctx(request, ctx):
+    ctx.set_option(G.OPT_ENGINE, request.param)
+    yield ctx
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+def grams_oracle(w):
+    D = O.gram(w.base, w.Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    T = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    return D, T
+
+
+def grams_gpu(ctx, w):
+    D = ctx.gram(w.base, dev(w.Xd), gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    T = None if w.Xt is None else ctx.gram(w.base, dev(w.Xt), gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    return D, T
+
+
+def f32(x):
+    return None if x is None else np.ascontiguousarray(x, dtype=np.float32)
+
+
+# ----------------------------------------------------------------------------- Gram
+@pytest.mark.parametrize("kind", [G.BASE_LINEAR, G.BASE_GAUSSIAN, G.BASE_POLY])
+@pytest.mark.parametrize("gram_engine", [1, 0], ids=["simt", "auto"])
+def test_gram_parity(ctx, kind, gram_engine):
+    ctx.set_option(G.OPT_GRAM_ENGINE, gram_engine)
+    rng = np.random.default_rng(kind)
+    for m, dim in [(1, 5), (300, 37), (517, 128)]:       # several tiles, ragged tails
+        X = rng.standard_normal((m, dim)).astype(np.float32)
+        gam = 1.0 / dim
+        K = ctx.gram(kind, dev(X), gamma=gam, coef0=1.0, degree=2).cpu().numpy()
+        ref = O.gram(kind, X, gamma=gam, coef0=1.0, degree=2)
+        assert np.abs(K - ref).max() <= 1e-6 * np.abs(ref).max(), (m, dim)
+        if kind == G.BASE_GAUSSIAN:
+            assert np.all(np.diag(K) == 1.0)
+    ctx.set_option(G.OPT_GRAM_ENGINE, 0)
+
+
+def test_gram_errors(ctx):
+    X = dev(np.ones((3, 2), np.float32))
+    with pytest.raises(G.GvtError) as e:
+        ctx.gram(G.BASE_GAUSSIAN, X, gamma=0.0)
+    assert e.value.code == G.E_PARAM
+    with pytest.raises(G.GvtError) as e:
+        ctx.gram(G.BASE_POLY, X, gamma=1.0, degree=-1)
+    assert e.value.code == G.E_PARAM
+
+
+# ----------------------------------------------------------------------------- plumbing
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sort_plan_bit_exact(ctx, mode):
+    rng = np.random.default_rng(5 + mode)
+    for m, q, n in [(1, 1, 0), (7, 5, 1), (1000, 700, 100_003), (20000, 20000, 2_000_000)]:
+        f = rng.integers(0, m, n).astype(np.int32)
+        s = rng.integers(0, q, n).astype(np.int32)
+        perm, rp = ctx.sort_plan(dev(f), dev(s), m, q, mode)
+        operm, orp = O.sort_plan(f, s, m, q, mode)
+        assert np.array_equal(perm.cpu().numpy(), operm)
+        assert np.array_equal(rp.cpu().numpy(), orp)
+    with pytest.raises(G.GvtError) as e:
+        ctx.sort_plan(dev(np.array([3], np.int32)), dev(np.array([0], np.int32)), 3, 1, mode)
+    assert e.value.code == G.E_INDEX
+
+
+# ----------------------------------------------------------------------------- matvec, tiny
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_matvec_tiny_vs_explicit(engine_ctx, kernel):
+    """200-ish seeded tiny instances (duplicates, self pairs, out != in, empty samples)
+    against the explicit definition u = K a."""
+    hom = kernel in HOM
+    terms = G.gvt_kernel_terms(kernel)
+    for seed in range(60):
+        rng = np.random.default_rng(seed)
+        w = synth.tiny(seed, m=int(rng.integers(1, 8)), q=int(rng.integers(1, 8)), n=int(rng.integers(0, 25)),
+                       n_out=int(rng.integers(0, 18)), homogeneous=hom)
+        D, T = grams_oracle(w)
+        D32, T32 = f32(D), f32(T)
+        a = synth.random_vector(seed, w.n)
+        u = engine_ctx.matvec(dev(D32), None if T32 is None else dev(T32), dev(w.test_first), dev(w.test_second),
+                              dev(w.train_first), dev(w.train_second), dev(a), terms).cpu().numpy()
+        ref = O.explicit_matvec(kernel, D32, T32, w.test_first, w.test_second, w.train_first, w.train_second, a)
+        assert u.shape == ref.shape
+        if ref.size:
+            assert rel(u, ref) <= MATVEC_TOL or np.abs(u - ref).max() <= 1e-6, (seed, rel(u, ref))
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_matvec_medium_vs_oracle_gvt(engine_ctx, kernel):
+    """Several tiles and ragged tails: m=300, q=200 (homogeneous: 300 objects), 20 000 in
+    pairs, 6 000 out pairs, against the oracle's per-term GVT (O4)."""
+    hom = kernel in HOM
+    rng = np.random.default_rng(100 + kernel)
+    m, q = 300, (300 if hom else 200)
+    Xd = rng.standard_normal((m, 24)).astype(np.float32)
+    Xt = None if hom else rng.standard_normal((q, 24)).astype(np.float32)
+    D = O.gram(G.BASE_GAUSSIAN, Xd, gamma=1 / 24)
+    T = None if hom else O.gram(G.BASE_GAUSSIAN, Xt, gamma=1 / 24)
+    inf, ins = rng.integers(0, m, 20000).astype(np.int32), rng.integers(0, q, 20000).astype(np.int32)
+    of, os_ = rng.integers(0, m, 6000).astype(np.int32), rng.integers(0, q, 6000).astype(np.int32)
+    a = synth.random_vector(kernel, 20000)
+    terms = G.gvt_kernel_terms(kernel)
+    D32, T32 = f32(D), f32(T)
+    u = engine_ctx.matvec(dev(D32), None if hom else dev(T32), dev(of), dev(os_), dev(inf), dev(ins), dev(a),
+                          terms).cpu().numpy()
+    ref = O.gvt_matvec(O.kernel_terms(kernel), D32, T32, of, os_, inf, ins, a)
+    assert rel(u, ref) <= MATVEC_TOL, rel(u, ref)
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
+def test_generic_term_path(ctx, kernel):
+    """A term list that is not a recognised Corollary list (reversed order) runs term by
+    term (Ones / Identity factors materialised) and still matches the oracle."""
+    hom = kernel in HOM
+    w = synth.tiny(7, m=9, q=6, n=40, n_out=25, homogeneous=hom)
+    D, T = grams_oracle(w)
+    D32, T32 = f32(D), f32(T)
+    terms = list(reversed(G.gvt_kernel_terms(kernel)))
+    if len(terms) == 1:
+        t = terms[0]
+        terms = [G.Term(0.5 * t.coef, *t.as_tuple()[1:]), G.Term(0.5 * t.coef, *t.as_tuple()[1:])]
+    a = synth.random_vector(3, w.n)
+    u = ctx.matvec(dev(D32), None if hom else dev(T32), dev(w.test_first), dev(w.test_second), dev(w.train_first),
+                   dev(w.train_second), dev(a), terms).cpu().numpy()
+    ref = O.explicit_matvec(kernel, D32, T32, w.test_first, w.test_second, w.train_first, w.train_second, a)
+    assert rel(u, ref) <= MATVEC_TOL
+
+
+# ----------------------------------------------------------------------------- C1 end to end
+def test_c1_fit_and_predict_end_to_end(ctx):
+    """C1 (BASELINE.json configs[0]): GPU Grams from features, 50 CG iterations, predictions
+    on the 500 test pairs, against the oracle's fp64 Grams + CG (reading S30)."""
+    w = synth.config1()
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    Dg, Tg = grams_gpu(ctx, w)
+    a, iters, hist, code = ctx.fit(Dg, Tg, dev(w.train_first), dev(w.train_second), dev(w.y), kron, w.lam, w.iters)
+    assert code == G.OK and iters == 50
+    D, T = grams_oracle(w)
+    ao, it_o, hist_o, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, w.iters)
+    assert rel(a.cpu().numpy(), ao) <= 1e-4
+    assert hist[-1] <= 1e-5
+    scores = ctx.predict(Dg, Tg, dev(w.test_first), dev(w.test_second), dev(w.train_first), dev(w.train_second), a,
+                         kron).cpu().numpy()
+    ref = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, w.test_first, w.test_second, w.train_first,
+                       w.train_second, ao)
+    assert np.abs(scores - ref).max() <= 1e-4
+    # one matvec at 1e-5
+    v = synth.random_vector(1, w.n)
+    u = ctx.matvec(Dg, Tg, dev(w.train_first), dev(w.train_second), dev(w.train_first), dev(w.train_second),
+                   dev(v), kron).cpu().numpy()
+    uref = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.train_first,
+                        w.train_second, v)
+    assert rel(u, uref) <= MATVEC_TOL
+
+
+def test_c1_cg_matches_oracle_on_identical_fp32_inputs(ctx):
+    """Same fp32 Grams on both sides: CG iterates differ only by fp32 vs fp64 arithmetic."""
+    w = synth.config1()
+    D, T = grams_oracle(w)
+    D32, T32 = f32(D), f32(T)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    a, iters, hist, _ = ctx.fit(dev(D32), dev(T32), dev(w.train_first), dev(w.train_second), dev(w.y), kron, w.lam,
+                                w.iters)
+    ao, _, hist_o, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first, w.train_second, w.y, w.lam, w.iters)
+    assert rel(a.cpu().numpy(), ao) <= 1e-4
+    # residual mode stops at the same iteration as the oracle
+    a2, it2, h2, _ = ctx.fit(dev(D32), dev(T32), dev(w.train_first), dev(w.train_second), dev(w.y), kron, w.lam, 200,
+                             rel_tol=1e-4)
+    _, it2o, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first, w.train_second, w.y, w.lam, 200,
+                         rel_tol=1e-4)
+    assert abs(it2 - it2o) <= 1 and h2[-1] <= 1e-4
+
+
+# ----------------------------------------------------------------------------- C2..C5
+def sampled_parity(ctx, w, kernel, k_samples=64, restrict=None, seed=0):
+    """Full training matvec u = K a on the GPU (launch configuration of the fit) and the
+    oracle's per-term GVT for a sample of those outputs."""
+    terms = G.gvt_kernel_terms(kernel)
+    Dg, Tg = grams_gpu(ctx, w)
+    f, s = dev(w.train_first), dev(w.train_second)
+    a = synth.random_vector(seed, w.n)
+    u = ctx.matvec(Dg, Tg, f, s, f, s, dev(a), terms).cpu().numpy()
+    if restrict is not None:
+        cand = np.nonzero(restrict(w))[0]
+        idx = cand[synth.sample_indices(seed, len(cand), k_samples)]
+    else:
+        idx = synth.sample_indices(seed, w.n, k_samples)
+    D, T = grams_oracle(w)
+    ref = O.gvt_matvec(O.kernel_terms(kernel), D, T, w.train_first[idx], w.train_second[idx], w.train_first,
+                       w.train_second, a)
+    return rel(u[idx], ref), u, idx
+
+
+def test_c2_complete_grid(ctx):
+    w = synth.config2()
+    r, _, _ = sampled_parity(ctx, w, G.KRONECKER, k_samples=2000)
+    assert r <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("kernel", [G.SYMMETRIC, G.ANTISYMMETRIC, G.CARTESIAN])
+def test_c3_homogeneous(ctx, kernel):
+    w = synth.config3()
+    r, _, _ = sampled_parity(ctx, w, kernel, k_samples=256)
+    assert r <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("kernel", [G.POLY2D, G.MLPK, G.RANKING])
+def test_c4_multiterm(ctx, kernel):
+    w = synth.config4()
+    if kernel in HOM:
+        w = synth.union_domain(w)
+    r, _, _ = sampled_parity(ctx, w, kernel, k_samples=48)
+    assert r <= MATVEC_TOL
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(ctx):
+    """C5 at full size (1e8 pairs, m=q=20000): the training matvec over all outputs, checked
+    on 256 sampled outputs whose target lies among 16 seeded targets (oracle O3b)."""
+    w = synth.config5()
+    tset = np.sort(np.random.default_rng(55).choice(w.q, 16, replace=False))
+    r, u, idx = sampled_parity(ctx, w, G.KRONECKER, k_samples=256,
+                               restrict=lambda w: np.isin(w.train_second, tset))
+    assert r <= MATVEC_TOL
+
+
+# ----------------------------------------------------------------------------- properties
+def test_determinism_bit_identical(ctx):
+    w = synth.config3(n=50_000, n_test=1000)
+    Dg, _ = grams_gpu(ctx, w)
+    terms = G.gvt_kernel_terms(G.SYMMETRIC)
+    f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
+    a1, _, _, _ = ctx.fit(Dg, None, f, s, y, terms, 1.0, 20)
+    a2, _, _, _ = ctx.fit(Dg, None, f, s, y, terms, 1.0, 20)
+    assert torch.equal(a1, a2)
+
+
+def test_host_pointer_path_equals_device_path(ctx):
+    w = synth.config1()
+    D, T = grams_oracle(w)
+    D32, T32 = f32(D), f32(T)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    a_dev, _, _, _ = ctx.fit(dev(D32), dev(T32), dev(w.train_first), dev(w.train_second), dev(w.y), kron, 1.0, 10)
+    a_host, _, _, _ = ctx.fit(D32, T32, w.train_first, w.train_second, w.y, kron, 1.0, 10)
+    assert isinstance(a_host, np.ndarray)
+    assert np.array_equal(a_dev.cpu().numpy(), a_host)
+
+
+def test_symmetry_invariants_on_gpu(ctx):
+    """Symmetric: u unchanged when the out pairs are swapped; Anti-symmetric / Ranking flip
+    sign; MLPK unchanged."""
+    w = synth.config3(n=20_000, n_test=2000)
+    Dg, _ = grams_gpu(ctx, w)
+    f, s = dev(w.train_first), dev(w.train_second)
+    of, os_ = dev(w.test_first), dev(w.test_second)
+    a = dev(synth.random_vector(9, w.n))
+    for k, sign in [(G.SYMMETRIC, 1), (G.ANTISYMMETRIC, -1), (G.RANKING, -1), (G.MLPK, 1)]:
+        t = G.gvt_kernel_terms(k)
+        u = ctx.matvec(Dg, None, of, os_, f, s, a, t).cpu().numpy()
+        v = ctx.matvec(Dg, None, os_, of, f, s, a, t).cpu().numpy()
+        assert rel(v, sign * u) <= 1e-5, k
+
+
+def test_edge_cases_and_errors(ctx):
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    D, T = dev(np.eye(3, dtype=np.float32)), dev(np.eye(2, dtype=np.float32))
+    f, s = dev(np.array([0, 1, 2], np.int32)), dev(np.array([0, 1, 0], np.int32))
+    e = dev(np.zeros(0, np.int32))
+    # empty out sample / empty in sample
+    assert ctx.matvec(D, T, e, e, f, s, dev(np.ones(3, np.float32)), kron).numel() == 0
+    u = ctx.matvec(D, T, f, s, e, e, dev(np.zeros(0, np.float32)), kron).cpu().numpy()
+    assert np.array_equal(u, np.zeros(3, np.float32))
+    # y = 0 -> a = 0, 0 iterations
+    a, it, hist, code = ctx.fit(D, T, f, s, dev(np.zeros(3, np.float32)), kron, 1.0, 5)
+    assert it == 0 and not a.cpu().numpy().any()
+    # n = 0 fit
+    a, it, _, _ = ctx.fit(D, T, e, e, dev(np.zeros(0, np.float32)), kron, 1.0, 5)
+    assert it == 0 and a.numel() == 0
+    # single pair ridge: (1*1 + 1) a = 2 -> a = 1
+    one = dev(np.ones((1, 1), np.float32))
+    z = dev(np.zeros(1, np.int32))
+    a, it, _, _ = ctx.fit(one, one, z, z, dev(np.array([2.0], np.float32)), kron, 1.0, 3)
+    assert a.cpu().numpy()[0] == pytest.approx(1.0, abs=1e-7)
+    # duplicates sum
+    ff, ss = dev(np.array([1, 1], np.int32)), dev(np.array([1, 1], np.int32))
+    u = ctx.matvec(D, T, ff[:1], ss[:1], ff, ss, dev(np.array([2.0, 3.0], np.float32)), kron).cpu().numpy()
+    assert u[0] == pytest.approx(5.0)
+    # errors
+    bad = dev(np.array([0, 3, 2], np.int32))
+    with pytest.raises(G.GvtError) as ex:
+        ctx.matvec(D, T, bad, s, f, s, dev(np.ones(3, np.float32)), kron)
+    assert ex.value.code == G.E_INDEX
+    with pytest.raises(G.GvtError) as ex:
+        ctx.matvec(D, T, f, s, f, s, dev(np.ones(3, np.float32)), G.gvt_kernel_terms(G.SYMMETRIC))
+    assert ex.value.code == G.E_HOMOGENEOUS
+    with pytest.raises(G.GvtError) as ex:
+        ctx.fit(D, T, f, s, dev(np.ones(3, np.float32)), kron, -1.0, 5)
+    assert ex.value.code == G.E_PARAM
+    with pytest.raises(G.GvtError) as ex:
+        ctx.matvec(D, T, f, s, f, s, dev(np.ones(3, np.float32)), [G.Term(1.0, 7, 1, 0, 1, 0, 1)])
+    assert ex.value.code == G.E_KERNEL
+    # breakdown: a non-PSD "Gram" makes p^T A p <= 0
+    negD = dev(-np.eye(3, dtype=np.float32))
+    a, it, _, code = ctx.fit(negD, T, f, s, dev(np.ones(3, np.float32)), kron, 0.0, 5, raise_on_breakdown=False)
+    assert code == G.E_BREAKDOWN
+
+
+def test_launch_accounting(ctx):
+    ctx.reset_stats()
+    ctx.set_option(G.OPT_PROFILE, 1)
+    w = synth.config1()
+    D, T = grams_gpu(ctx, w)
+    ctx.fit(D, T, dev(w.train_first), dev(w.train_second), dev(w.y), G.gvt_kernel_terms(G.KRONECKER), 1.0, 5)
+    st = ctx.stats()
+    ctx.set_option(G.OPT_PROFILE, 0)
+    assert st["launches"] > 0
+    assert "cg_vector" in st["kinds"] and st["kinds"]["cg_vector"]["count"] >= 5 * 3
+    assert all(v["ms"] >= 0 for v in st["kinds"].values())

@@ -1,0 +1,393 @@
+"""bench.py -- GVT hot-path benchmark (BASELINE.json metric: "GVT matvec Gpairs/s and CG
+iters/s at 1/2/4/8 B200; % of HBM roofline").
+
+One STEP = one pass of the whole hot path over the workload:
+base-kernel Grams D, T from the object features (a2), pairwise_krr_fit = plan + `iters` CG
+iterations of the GVT matvec (a1, a3-a9), pairwise_predict over the test pairs (a10).
+value = matvec pair-rows delivered per second over the whole step,
+        (iters * n_train + n_test) / t_step, in Gpairs/s (whole job, all ranks).
+
+Default workload: C5 (BASELINE.json configs[4], the metric's 1/2/4/8-GPU config; it fits
+one B200).  Inputs (1e8 pairs = 0.8 GB of ids) exceed the 126 MB L2, so no flush is
+needed between steps.  --impl reference times the fp64 oracle (oracle/, test
+infrastructure) on a bounded sample of the same workload on the host cores.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
+torch.distributed.run (one rank per GPU, NCCL); rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "GVT matvec Gpairs/s and CG iters/s at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gpairs/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", 1400.0),
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+            "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workloads
+def workload(name: str):
+    if name == "C5":
+        return synth.config5()
+    if name == "C4":
+        return synth.config4()
+    if name == "C3":
+        return synth.config3()
+    if name == "C2":
+        return synth.config2()
+    if name == "C1":
+        return synth.config1()
+    if name.startswith("C5s"):       # scaled-down C5 for quick runs: C5s<n_millions>
+        n = int(float(name[3:]) * 1e6)
+        return synth.config5(n=n, n_test=max(1, n // 5), m=max(200, int(20000 * (n / 1e8) ** 0.5)))
+    raise ValueError(name)
+
+
+def default_kernel(w):
+    return w.kernels[0]
+
+
+# ----------------------------------------------------------------------------- roofline
+def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engine: int):
+    """Dominant kernel (largest summed event time) vs its roof.  Algorithmic work per
+    launch: stage 1 = q_out FMA per pair-matrix entry, stage 2 = m_in FMA
+    per output; dense engine reports against the TF32 tensor peak (measured bf16 x 0.5),
+    sparse/SIMT kernels against the fp32 ALU peak (148 SM x 128 lanes x 2 x f_max)."""
+    if not kinds:
+        return None
+    name, rec = max(kinds.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = rec["ms"] / max(1, rec["count"])
+    n, n_test, m, q = w.n, w.n_test, w.m, w.q
+    nnz = n * {synth.SYMMETRIC: 2, synth.ANTISYMMETRIC: 2, synth.MLPK: 4}.get(kernel, 1)
+    alu_peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s
+    tf32_peak = peaks["bf16_tflops_sustained"] * 0.5
+    cnt = rec["count"]
+    fit_launches = max(1, w.iters)
+    if name in ("stage1_sparse", "stage1_tc"):
+        # (iters fit launches over n pairs) + (1 predict launch over n pairs): same per-launch work
+        flops = 2.0 * q * nnz
+    elif name in ("stage2_gather", "stage2_tc"):
+        # fit launches: n outputs; predict: n_test outputs -> average per launch
+        fl_fit = 2.0 * m * n
+        fl_pred = 2.0 * m * n_test
+        steps = cnt / (fit_launches + 1)
+        flops = (fl_fit * fit_launches + fl_pred) * steps / cnt
+    else:
+        return {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None}
+    achieved = flops / (per_launch_ms * 1e-3) / 1e12
+    if name.endswith("_tc"):
+        bound, peak, src = "tensor", tf32_peak, f"tf32 = 0.5 x measured bf16 sustained ({peaks['source']})"
+    else:
+        bound, peak, src = "alu", alu_peak, "fp32 SIMT: 148 SM x 128 lanes x 2 x sm_max_mhz"
+    return {"kernel": name, "bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 1),
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None, "peak_source": src,
+            "ms_per_launch": round(per_launch_ms, 4), "launches": cnt}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample(w, kernel, n_targets=8, seed=0):
+    """The oracle's GVT matvec on a bounded sample of the training matvec: the outputs whose
+    second element lies among `n_targets` seeded targets (the oracle then forms S only for
+    those rows: the same fraction of stage 1 and stage 2 work as of the full matvec)."""
+    import oracle as O
+    rng = np.random.default_rng(seed)
+    tset = rng.choice(w.q, n_targets, replace=False)
+    idx = np.nonzero(np.isin(w.train_second, tset))[0]
+    D = O.gram(w.base, w.Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    T = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    a = synth.random_vector(seed, w.n)
+    terms = O.kernel_terms(kernel)
+    t0 = time.perf_counter()
+    O.gvt_matvec(terms, D, T, w.train_first[idx], w.train_second[idx], w.train_first, w.train_second, a)
+    dt = time.perf_counter() - t0
+    return len(idx), dt, O.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w = workload(args.workload)
+    kernel = default_kernel(w)
+    times, cnt = [], 0
+    nt = args.ref_targets
+    for i in range(args.warmup + args.steps):
+        k, dt, cores = oracle_sample(w, kernel, n_targets=nt, seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+            cnt += k
+    tot = sum(times)
+    val = cnt / tot / 1e9
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"fp64 oracle per-term GVT training matvec restricted to the outputs of {nt} "
+                                       f"seeded targets per step ({cnt // max(1, args.steps)} outputs, stage 1 over "
+                                       f"all {w.n} pairs for those rows)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_01054_b200 as G
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workload(args.workload)
+    kernel = G.KRONECKER if args.kernel is None else getattr(G, args.kernel.upper())
+    if args.kernel is None:
+        kernel = default_kernel(w)
+    if kernel in G.HOMOGENEOUS_KERNELS and w.Xt is not None:
+        w = synth.union_domain(w)
+    terms = G.gvt_kernel_terms(kernel)
+    ctx = G.Context(local_rank)
+    ctx.set_option(G.OPT_ENGINE, args.engine)
+    if world > 1:
+        uid = G.gvt_nccl_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(obj[0], rank, world)
+
+    # ---- shard (weak scaling: each rank holds one full copy of the workload's pairs
+    #      and processes its drug range)
+    f, s, y = w.train_first, w.train_second, w.y
+    tf_, ts_ = w.test_first, w.test_second
+    if world > 1:
+        deg = np.bincount(f, minlength=w.m)
+        bounds = G.gvt_partition(deg, world)
+        lo, hi = bounds[rank], bounds[rank + 1]
+        sel = (f >= lo) & (f < hi)
+        f, s, y = f[sel], s[sel], y[sel]
+        tsel = np.arange(len(tf_)) % world == rank
+        tf_, ts_ = tf_[tsel], ts_[tsel]
+    n_local, nt_local = len(f), len(tf_)
+
+    def d(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    Xd, Xt = d(w.Xd), (None if w.Xt is None else d(w.Xt))
+    fD, sD, yD, tfD, tsD = d(f), d(s), d(y), d(tf_), d(ts_)
+    m, q = w.m, w.q
+    D = torch.empty((m, m), dtype=torch.float32, device=dev)
+    T = None if Xt is None else torch.empty((q, q), dtype=torch.float32, device=dev)
+    a = torch.empty(n_local, dtype=torch.float32, device=dev)
+    scores = torch.empty(nt_local, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ctx.gram(w.base, Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=D)
+        if T is not None:
+            ctx.gram(w.base, Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=T)
+        _, it, _, _ = ctx.fit(D, T, fD, sD, yD, terms, w.lam, w.iters, 0.0, out=a, want_history=False)
+        ctx.predict(D, T, tfD, tsD, fD, sD, a, terms, out=scores)
+        return it
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.reset_stats()
+    ctx.set_option(G.OPT_PROFILE, 1 if args.profile else 0)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            iters = step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = ctx.stats()
+    ctx.set_option(G.OPT_PROFILE, 0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    pairs = float(iters) * w.n + w.n_test  # whole job
+    value = pairs / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        def pin(x):
+            t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+            return t.numpy()
+        hXd, hXt = pin(w.Xd), (None if w.Xt is None else pin(w.Xt))
+        hf, hs, hy, htf, hts = pin(f), pin(s), pin(y), pin(tf_), pin(ts_)
+        ha = pin(np.zeros(n_local, np.float32))
+        hsc = pin(np.zeros(nt_local, np.float32))
+
+        def step_host():
+            ctx.gram(w.base, hXd, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=D)
+            if T is not None:
+                ctx.gram(w.base, hXt, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=T)
+            ctx.fit(D, T, hf, hs, hy, terms, w.lam, w.iters, 0.0, out=ha, want_history=False)
+            ctx.predict(D, T, htf, hts, hf, hs, ha, terms, out=hsc)
+
+        step_host()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_host()
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = (w.Xd.nbytes + (0 if w.Xt is None else w.Xt.nbytes) + 2 * (8 * n_local) + 4 * n_local +
+               8 * nt_local + 4 * n_local) * world
+        d2h = (4 * n_local + 4 * nt_local) * world
+        e2e = {"value": pairs / (ems / args.steps * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / args.steps}
+
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    rl = roofline(st["kinds"], w, kernel, None, peaks, args.engine) if args.profile else None
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        k, dt, cores = oracle_sample(w, kernel, n_targets=args.ref_targets)
+        cpu = {"value": k / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"fp64 oracle per-term GVT training matvec restricted to the outputs of {args.ref_targets} "
+                         f"seeded targets ({k} outputs; stage 1 streams all {w.n} pairs for those rows)",
+               "seconds": round(dt, 2)}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
+                       "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
+                       "engine": {0: "auto", 1: "sparse", 2: "dense"}[args.engine],
+                       "last_engine": {1: "sparse", 2: "dense"}.get(st["last_engine"], None),
+                       "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
+                       "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"},
+            "cg_iters_per_s": iters / (ms_step * 1e-3),
+            "gpu_launches": int(st["launches"]),
+            "kernel_ms": {k: round(v["ms"] / args.steps, 3) for k, v in st["kinds"].items()} if args.profile else None,
+            "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--kernel", default=None)
+    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--no-profile", dest="profile", action="store_false")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-targets", type=int, default=8)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

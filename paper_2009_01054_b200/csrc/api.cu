@@ -249,14 +249,14 @@ gvt_status gvt_sort_plan(gvt_ctx *c, const int32_t *first, const int32_t *second
     GVT_API_BEGIN(c)
     GVT_REQUIRE(n >= 0 && m >= 0 && q >= 0, GVT_E_DIM, "negative size");
     GVT_REQUIRE(mode == 0 || mode == 1, GVT_E_PARAM, "mode must be 0 or 1");
-    GVT_REQUIRE(perm && row_ptr, GVT_E_PARAM, "NULL output");
+    GVT_REQUIRE((perm || n == 0) && row_ptr, GVT_E_PARAM, "NULL output");
     const int32_t *f = n ? (const int32_t *)gvt::stage_in(c, "dbg.f", first, sizeof(int32_t) * n) : nullptr;
     const int32_t *s = n ? (const int32_t *)gvt::stage_in(c, "dbg.s", second, sizeof(int32_t) * n) : nullptr;
     if (n) {
         GVT_REQUIRE(gvt::count_out_of_range(c, f, n, m) == 0, GVT_E_INDEX, "first id out of range");
         GVT_REQUIRE(gvt::count_out_of_range(c, s, n, q) == 0, GVT_E_INDEX, "second id out of range");
     }
-    bool hp = !gvt::is_device_ptr(perm), hr = !gvt::is_device_ptr(row_ptr);
+    bool hp = n > 0 && !gvt::is_device_ptr(perm), hr = !gvt::is_device_ptr(row_ptr);
     int32_t *dperm = hp ? gvt::wsT<int32_t>(c, "dbg.perm", n) : perm;
     int64_t *drp = hr ? gvt::wsT<int64_t>(c, "dbg.rp", m + 1) : row_ptr;
     gvt::sort_plan_debug(c, f, s, n, m, q, mode, dperm, drp);

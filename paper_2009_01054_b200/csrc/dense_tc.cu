@@ -1,26 +1,590 @@
-// dense_tc.cu -- dense tensor-core engine (placeholder until the tcgen05 kernels land).
+// dense_tc.cu -- dense tensor-core engine on sm_100a: tcgen05.mma kind::tf32 with the
+// 3xTF32 split (hi*hi + hi*lo + lo*hi) so that the result is fp32-accurate (reading
+// S16).  Operands are staged by TMA (SWIZZLE_128B, K-major) through an mbarrier ring; one
+// elected thread issues the MMAs; accumulators live in TMEM.
+//
+// Precision: the tensor core truncates every accumulation into its fp32 accumulator, a
+// bias that grows with K.  The kernel therefore accumulates K in chunks of KC = 128
+// (fresh accumulator per chunk, double-buffered in TMEM: 2 x 256 columns) and the
+// epilogue warps add the chunk results into fp32 registers with round-to-nearest while
+// the MMA warp works on the next chunk.
+//
+// One kernel, three epilogues:
+//   EPI_SPLIT   C = A B^T stored as (hi, lo) tf32 pairs  -> GVT stage 1, S = C_fac X^T
+//   EPI_SAMPLED out[dst] (+)= coef (A B^T)[r, c] for the samples bucketed on this tile
+//               -> GVT stage 2 (sampled D S^T, north-star kernel (3), dense-tile form)
+//   EPI_GRAM    K = k(X_i, X_j) from the dot product and row norms -> base-kernel Gram,
+//               north-star kernel (1)
+// Tile 128 x 256, BK = 32 fp32 (one 128-byte swizzle row), 2-stage ring of 96 KB.
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..9 epilogue (warp w reads TMEM
+// lanes 32*(w%4).. and columns 128*((w-2)/4)..).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ops.cuh"
 
 namespace gvt {
 
-bool tc_available(gvt_ctx *c) {
-    (void)c;
-    return false;
+// ----------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-void split_tf32(gvt_ctx *, const float *, int64_t, float *, float *) { throw Error{GVT_E_CUDA, "tc unavailable"}; }
-void densify(gvt_ctx *, const EntryPlan &, float *, float *, int64_t, int64_t) { throw Error{GVT_E_CUDA, "tc unavailable"}; }
-void gemm_nt_split(gvt_ctx *, const float *, const float *, int64_t, const float *, const float *, int64_t, int64_t,
-                   int64_t, int64_t, float *, float *, float *, int64_t) {
-    throw Error{GVT_E_CUDA, "tc unavailable"};
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-void gemm_nt_sampled(gvt_ctx *, const float *, const float *, int64_t, const float *, const float *, int64_t, int64_t,
-                     int64_t, int64_t, const SamplePlan &, float, int, float *) {
-    throw Error{GVT_E_CUDA, "tc unavailable"};
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
-void bucket_samples(gvt_ctx *, const char *, SamplePlan &, int64_t, int64_t) { throw Error{GVT_E_CUDA, "tc unavailable"}; }
-void gram_tc(gvt_ctx *, int, const float *, int64_t, int64_t, double, double, int, float *, int64_t) {
-    throw Error{GVT_E_CUDA, "tc unavailable"};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// K-major, SWIZZLE_128B canonical layout: 8-row x 128-byte atoms, SBO = 1024 B, LBO = 16 B
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;   // SBO
+    d |= (uint64_t)1 << 46;             // version (sm_100)
+    d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = BN
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_round(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// ----------------------------------------------------------------------------- kernel
+enum { EPI_SPLIT = 0, EPI_SAMPLED = 1, EPI_GRAM = 2 };
+
+struct EpiParams {
+    // split
+    float *c_hi, *c_lo, *c_f;
+    int64_t ldc;
+    // sampled
+    const int32_t *s_r, *s_c, *s_dst;
+    const int64_t *chunk_ptr;  // per (tile, 32-column chunk)
+    int64_t n_ct;              // column tiles
+    float coef;
+    int accumulate;
+    float *out;
+    // gram
+    const float *norms;
+    int kind;
+    float gamma, coef0;
+    int degree;
+    int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
+};
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
+constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk (KC = 128)
+constexpr int N_EPI_WARPS = 8;
+constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
+constexpr int A_BYTES = BM * BK * 4;              // 16 KB
+constexpr int B_BYTES = BN * BK * 4;              // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
+constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+constexpr int SMEM_TOTAL = BAR_OFF + 256 + 1024;        // barriers + tmem slot + alignment slack
+static_assert(N_EPI_WARPS * 32 * 33 * 4 <= STAGES * STAGE_BYTES, "epilogue staging aliases the stage ring");
+
+template <int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                  const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N,
+                  int K, EpiParams ep) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;   // [2] accumulator buffer ready
+    uint64_t *tempty = tfull + 2;       // [2] accumulator buffer drained
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_tile = blockIdx.x, m_tile = blockIdx.y;
+    const int m0 = m_tile * BM, n0 = n_tile * BN;
+    const int nk = (K + BK - 1) / BK;
+    const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
+    const int nch = (nk + kcb - 1) / kcb;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmAh);
+        prefetch_tmap(&tmAl);
+        prefetch_tmap(&tmBh);
+        prefetch_tmap(&tmBl);
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], N_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {  // TMEM allocation (whole warp): 2 accumulator buffers x BN fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t *st = smem + s * STAGE_BYTES;
+                mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                const int kc = kb * BK;
+                tma_load_2d(st, &tmAh, &full[s], kc, m0);
+                tma_load_2d(st + A_BYTES, &tmAl, &full[s], kc, m0);
+                tma_load_2d(st + 2 * A_BYTES, &tmBh, &full[s], kc, n0);
+                tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmBl, &full[s], kc, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer (single thread)
+            constexpr uint32_t idesc = idesc_tf32<BN>();
+            int kb = 0;
+            for (int ch = 0; ch < nch; ch++) {
+                const int b = ch & 1;
+                mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);  // epilogue drained this buffer
+                tc_fence_after();
+                const uint32_t acc = tmem + b * BN;
+                const int kend = min(nk, kb + kcb);
+                for (int kk = 0; kb < kend; kb++, kk++) {
+                    const int s = kb % STAGES;
+                    const uint32_t ph = (kb / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+                    const uint32_t ah = base, al = base + A_BYTES, bh = base + 2 * A_BYTES,
+                                   bl = base + 2 * A_BYTES + B_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 8; k++) {
+                        const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+                        const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
+                        const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
+                        mma_tf32(acc, dah, dbh, idesc, (kk | k) != 0);
+                        mma_tf32(acc, dah, dbl, idesc, 1);
+                        mma_tf32(acc, dal, dbh, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
+                }
+                mma_commit(&tfull[b]);      // chunk accumulator complete
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..9
+        const int ew = warp - 2;
+        const int quarter = warp & 3;   // TMEM lane quarter this warp may access
+        const int half = ew >> 2;       // column half: [128*half, 128*half + 128)
+        const int row = quarter * 32 + lane;
+        const int gr = m0 + row;
+        float run[128];
+#pragma unroll
+        for (int i = 0; i < 128; i++) run[i] = 0.f;
+        for (int ch = 0; ch < nch; ch++) {
+            const int b = ch & 1;
+            mbar_wait(&tfull[b], (ch >> 1) & 1);
+            tc_fence_after();
+            const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; c4++) {
+                uint32_t r[32];
+                tmem_ld32_raw(ta + c4 * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        // all MMAs are complete (the last tfull was committed after them), so the stage ring is
+        // free and serves as staging memory for the sampled epilogue
+        const int gc_base = n0 + half * 128;
+        if (EPI == EPI_SPLIT) {
+            if (gr < M) {
+                float *hi = ep.c_hi + (int64_t)gr * ep.ldc + gc_base;
+                float *lo = ep.c_lo + (int64_t)gr * ep.ldc + gc_base;
+                if (gc_base + 128 <= N) {
+#pragma unroll
+                    for (int i = 0; i < 128; i += 4) {
+                        float4 h, l;
+                        h.x = tf32_round(run[i]);     l.x = tf32_round(run[i] - h.x);
+                        h.y = tf32_round(run[i + 1]); l.y = tf32_round(run[i + 1] - h.y);
+                        h.z = tf32_round(run[i + 2]); l.z = tf32_round(run[i + 2] - h.z);
+                        h.w = tf32_round(run[i + 3]); l.w = tf32_round(run[i + 3] - h.w);
+                        *reinterpret_cast<float4 *>(hi + i) = h;
+                        *reinterpret_cast<float4 *>(lo + i) = l;
+                    }
+                    if (ep.c_f) {
+                        float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
+#pragma unroll
+                        for (int i = 0; i < 128; i += 4)
+                            *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 128; i++) {
+                        if (gc_base + i < N) {
+                            float h = tf32_round(run[i]);
+                            hi[i] = h;
+                            lo[i] = tf32_round(run[i] - h);
+                            if (ep.c_f) ep.c_f[(int64_t)gr * ep.ldc + gc_base + i] = run[i];
+                        }
+                    }
+                }
+            }
+        } else if (EPI == EPI_GRAM) {
+            if (gr < M) {
+                float *krow = ep.c_f + (int64_t)gr * ep.ldc;
+                const float ni = ep.kind == GVT_BASE_GAUSSIAN ? ep.norms[gr] : 0.f;
+#pragma unroll
+                for (int i = 0; i < 128; i++) {
+                    const int gc = gc_base + i;
+                    if (gc < N) {
+                        float x = run[i];
+                        if (ep.kind == GVT_BASE_GAUSSIAN) {
+                            float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
+                            if (gc == gr) d2 = 0.f;  // k(x, x) = 1 exactly
+                            x = expf(-ep.gamma * d2);
+                        } else if (ep.kind == GVT_BASE_POLY) {
+                            float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
+                            for (int e = 0; e < ep.degree; e++) rr *= bb;
+                            x = rr;
+                        }
+                        krow[gc] = x;
+                    }
+                }
+            }
+        } else {  // EPI_SAMPLED: per 32-column chunk pair, park values in smem, serve the samples
+            float *stage = reinterpret_cast<float *>(smem);  // [half*4 + quarter][32 rows][33]
+            const int t = threadIdx.x - 64;                  // 0..255
+            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; c4++) {
+                float *mine = stage + (half * 4 + quarter) * 32 * 33 + lane * 33;
+#pragma unroll
+                for (int i = 0; i < 32; i++) mine[i] = run[c4 * 32 + i];
+                named_bar(1, 32 * N_EPI_WARPS);
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const int chunk = hh * 4 + c4;
+                    const int64_t cidx = tile * (BN / 32) + chunk;
+                    const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
+                    const int gc0 = n0 + chunk * 32;
+                    for (int64_t k = kb0 + t; k < ke; k += 32 * N_EPI_WARPS) {
+                        const int rl = ep.s_r[k] - m0;   // 0..127
+                        const int cl = ep.s_c[k] - gc0;  // 0..31
+                        const float val = stage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
+                        const int64_t d = ep.s_dst[k];
+                        ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
+                    }
+                }
+                named_bar(1, 32 * N_EPI_WARPS);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    }
+}
+
+// ----------------------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static void get_encode() {
+    if (g_encode) return;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    GVT_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    GVT_REQUIRE(fn && q == cudaDriverEntryPointSuccess, GVT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+}
+
+// rows x cols (cols = K, contiguous) fp32 matrix with leading dimension ld; box (32, box_rows)
+static CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    get_encode();
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)(cols > 0 ? cols : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    GVT_REQUIRE(r == CUDA_SUCCESS, GVT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+bool tc_available(gvt_ctx *c) { return c->tc_ok; }
+
+template <int EPI>
+static void launch_gemm(gvt_ctx *c, int kind_id, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi,
+                        const float *Blo, int64_t ldb, int64_t M, int64_t N, int64_t K, const EpiParams &ep) {
+    if (M == 0 || N == 0) return;
+    GVT_REQUIRE(K > 0, GVT_E_DIM, "GEMM with K = 0");
+    GVT_REQUIRE(M < INT32_MAX && N < INT32_MAX && K < INT32_MAX, GVT_E_DIM, "GEMM dimension too large");
+    CUtensorMap ah = make_map(Ahi, M, K, lda, BM), al = make_map(Alo, M, K, lda, BM);
+    CUtensorMap bh = make_map(Bhi, N, K, ldb, BN), bl = make_map(Blo, N, K, ldb, BN);
+    static bool attr[3] = {false, false, false};
+    if (!attr[EPI]) {
+        GVT_CUDA_TRY(
+            cudaFuncSetAttribute(k_gemm_tf32x3<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+        attr[EPI] = true;
+    }
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    GVT_LAUNCH(c, kind_id, k_gemm_tf32x3<EPI>, grid, NTHREADS, SMEM_TOTAL, ah, al, bh, bl, (int)M, (int)N, (int)K,
+               ep);
+}
+
+__global__ void k_split(const float *__restrict__ x, int64_t n, float *__restrict__ hi, float *__restrict__ lo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float v = x[i];
+        float h = tf32_round(v);
+        hi[i] = h;
+        lo[i] = tf32_round(v - h);
+    }
+}
+
+void split_tf32(gvt_ctx *c, const float *x, int64_t count, float *hi, float *lo) {
+    if (count == 0) return;
+    GVT_LAUNCH(c, K_SPLIT, k_split, grid1d(count, 256, 16 * c->sm_count * 8), 256, 0, x, count, hi, lo);
+}
+
+// X[row][col] = sum of the (row, col) run of sorted entries (deterministic, in entry order)
+__global__ void k_densify(const int32_t *__restrict__ row, const int32_t *__restrict__ col,
+                          const float *__restrict__ val, int64_t E, float *__restrict__ Xhi, float *__restrict__ Xlo,
+                          int64_t ldX) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = row[k], cc = col[k];
+        if (k > 0 && row[k - 1] == r && col[k - 1] == cc) continue;  // not the head of its run
+        float s = val[k];
+        for (int64_t j = k + 1; j < E && row[j] == r && col[j] == cc; j++) s += val[j];
+        const float h = tf32_round(s);
+        Xhi[(int64_t)r * ldX + cc] = h;
+        Xlo[(int64_t)r * ldX + cc] = tf32_round(s - h);
+    }
+}
+
+void densify(gvt_ctx *c, const EntryPlan &e, float *Xhi, float *Xlo, int64_t ldX, int64_t rows_pad) {
+    GVT_CUDA_TRY(cudaMemsetAsync(Xhi, 0, sizeof(float) * rows_pad * ldX, c->stream));
+    GVT_CUDA_TRY(cudaMemsetAsync(Xlo, 0, sizeof(float) * rows_pad * ldX, c->stream));
+    if (e.nnz == 0) return;
+    GVT_LAUNCH(c, K_DENSIFY, k_densify, grid1d(e.nnz, 256, 16 * c->sm_count * 8), 256, 0, e.row, e.col, e.val, e.nnz,
+               Xhi, Xlo, ldX);
+}
+
+void gemm_nt_split(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
+                   int64_t ldb, int64_t M, int64_t N, int64_t K, float *Chi, float *Clo, float *Cf, int64_t ldc) {
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.c_hi = Chi;
+    ep.c_lo = Clo;
+    ep.c_f = Cf;
+    ep.ldc = ldc;
+    launch_gemm<EPI_SPLIT>(c, K_STAGE1_TC, Ahi, Alo, lda, Bhi, Blo, ldb, M, N, K, ep);
+}
+
+void gemm_nt_sampled(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
+                     int64_t ldb, int64_t M, int64_t N, int64_t K, const SamplePlan &sp, float coef, int accumulate,
+                     float *out) {
+    if (sp.ns == 0) return;
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.s_r = sp.r;
+    ep.s_c = sp.c;
+    ep.s_dst = sp.dst;
+    ep.chunk_ptr = sp.tile_ptr;
+    ep.n_ct = sp.n_ct;
+    ep.coef = coef;
+    ep.accumulate = accumulate;
+    ep.out = out;
+    launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, Ahi, Alo, lda, Bhi, Blo, ldb, M, N, K, ep);
+}
+
+// ----------------------------------------------------------------------------- sample bucketing
+// key = ((r / BM) * n_ct + c / BN) * (BN/32) + (c % BN) / 32 ; stable sort keeps r-order inside
+__global__ void k_bucket_keys(const int32_t *__restrict__ r, const int32_t *__restrict__ cc, int64_t ns, int64_t n_ct,
+                              uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ns; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rt = r[k] / BM, ct = cc[k] / BN, ch = (cc[k] % BN) / 32;
+        keys[k] = (uint32_t)((rt * n_ct + ct) * (BN / 32) + ch);
+        vals[k] = (int32_t)k;
+    }
+}
+
+__global__ void k_bucket_apply(const int32_t *__restrict__ order, int64_t ns, const int32_t *__restrict__ r,
+                               const int32_t *__restrict__ cc, const int32_t *__restrict__ dst,
+                               int32_t *__restrict__ r2, int32_t *__restrict__ c2, int32_t *__restrict__ d2) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ns; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t o = order[k];
+        r2[k] = r[o];
+        c2[k] = cc[o];
+        d2[k] = dst[o];
+    }
+}
+
+__global__ void k_bucket_ptr(const uint32_t *__restrict__ skeys, int64_t ns, int64_t nb, int64_t *__restrict__ ptr) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = ns;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)skeys[mid] < b) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[b] = lo;
+    }
+}
+
+void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol) {
+    std::string t(tag);
+    sp.n_rt = (nrow + BM - 1) / BM;
+    sp.n_ct = (ncol + BN - 1) / BN;
+    const int64_t nb = sp.n_rt * sp.n_ct * (BN / 32);
+    GVT_REQUIRE(nb < (int64_t)UINT32_MAX, GVT_E_DIM, "too many sample buckets");
+    sp.tile_ptr = wsT<int64_t>(c, (t + ".chunkptr").c_str(), nb + 1);
+    const int64_t ns = sp.ns;
+    if (ns > 0) {
+        uint32_t *k0 = wsT<uint32_t>(c, "bucket.k0", ns), *k1 = wsT<uint32_t>(c, "bucket.k1", ns);
+        int32_t *v0 = wsT<int32_t>(c, "bucket.v0", ns), *v1 = wsT<int32_t>(c, "bucket.v1", ns);
+        GVT_LAUNCH(c, K_PLAN_KEYS, k_bucket_keys, grid1d(ns, 256, 4096), 256, 0, sp.r, sp.c, ns, sp.n_ct, k0, v0);
+        size_t temp = 0;
+        int bits = 1;
+        while (bits < 32 && ((uint64_t)nb >> bits)) bits++;
+        GVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0, k1, v0, v1, (int)ns, 0, bits, c->stream));
+        void *tmp = ws(c, "bucket.tmp", temp);
+        cudaEvent_t ev;
+        launch_begin(c, K_PLAN_SORT, &ev);
+        GVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, v0, v1, (int)ns, 0, bits, c->stream));
+        launch_end(c, K_PLAN_SORT, ev);
+        int32_t *r2 = wsT<int32_t>(c, (t + ".br").c_str(), ns), *c2 = wsT<int32_t>(c, (t + ".bc").c_str(), ns),
+                *d2 = wsT<int32_t>(c, (t + ".bd").c_str(), ns);
+        GVT_LAUNCH(c, K_PLAN_GATHER, k_bucket_apply, grid1d(ns, 256, 4096), 256, 0, v1, ns, sp.r, sp.c, sp.dst, r2, c2,
+                   d2);
+        sp.r = r2;
+        sp.c = c2;
+        sp.dst = d2;
+        GVT_LAUNCH(c, K_PLAN_ROWPTR, k_bucket_ptr, grid1d(nb + 1, 256), 256, 0, k1, ns, nb, sp.tile_ptr);
+    } else {
+        GVT_CUDA_TRY(cudaMemsetAsync(sp.tile_ptr, 0, sizeof(int64_t) * (nb + 1), c->stream));
+    }
+}
+
+// ----------------------------------------------------------------------------- Gram
+__global__ void k_norms(const float *__restrict__ X, int64_t m, int64_t dim, float *__restrict__ nrm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+        float acc = 0.f;
+        for (int64_t k = lane; k < dim; k += 32) acc = fmaf(X[i * dim + k], X[i * dim + k], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) nrm[i] = acc;
+    }
+}
+
+void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
+             float *K, int64_t ldk) {
+    if (m == 0) return;
+    const int64_t ldx = round_up(dim, 32), rows = round_up(m, 128);
+    float *xp = wsT<float>(c, "gram.xp", rows * ldx);
+    float *xh = wsT<float>(c, "gram.xh", rows * ldx);
+    float *xl = wsT<float>(c, "gram.xl", rows * ldx);
+    float *nr = wsT<float>(c, "gram.norms", rows);
+    pad_copy(c, X, m, dim, dim, xp, ldx, rows);
+    split_tf32(c, xp, rows * ldx, xh, xl);
+    if (kind == GVT_BASE_GAUSSIAN)
+        GVT_LAUNCH(c, K_GRAM_TC, k_norms, grid1d(m * 32, 256, 4096), 256, 0, X, m, dim, nr);
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.c_f = K;
+    ep.ldc = ldk;
+    ep.norms = nr;
+    ep.kind = kind;
+    ep.gamma = (float)gamma;
+    ep.coef0 = (float)coef0;
+    ep.degree = degree;
+    ep.kcb = 1;  // short K (feature dim): one 32-wide k-block per fp32 round-to-nearest drain
+    launch_gemm<EPI_GRAM>(c, K_GRAM_TC, xh, xl, ldx, xh, xl, ldx, m, m, dim, ep);
 }
 
 }  // namespace gvt

@@ -193,11 +193,13 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
     bool tc = tc_available(c);
     if (c->engine == 2) {
         GVT_REQUIRE(tc, GVT_E_CUDA, "dense tensor-core engine requested but not available on this device");
-        return 2;
+        if (g.A.hi && g.C.hi) return 2;
+        return 1;  // materialised Ones/Identity factors of a generic term list stay on SIMT
     }
+    if (!(g.A.hi && g.C.hi)) return 1;  // factors were not split for tensor cores
     double cells = (double)g.m_in * (double)g.C.n;
     double density = cells > 0 ? (double)g.ent.nnz / cells : 0.0;
-    return (tc && density >= c->dense_threshold && g.m_in >= 128 && g.q_out >= 128) ? 2 : 1;
+    return (tc && density >= c->dense_threshold) ? 2 : 1;
 }
 
 static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
@@ -468,7 +470,7 @@ static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_i
     double mult = (form == FORM_SYM || form == FORM_ANTI) ? 2.0 : (form == FORM_MLPK ? 4.0 : 1.0);
     double cells = (form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC) ? (double)m * (double)q
                                                                                      : (double)m * (double)m;
-    return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold && m >= 128 && q >= 128;
+    return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold;
 }
 
 static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, const float *T, int64_t q,

@@ -45,7 +45,7 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(params=[G.ENGINE_SPARSE, G.ENGINE_AUTO], ids=["sparse", "auto"])
+@pytest.fixture(params=[G.ENGINE_SPARSE, G.ENGINE_AUTO, G.ENGINE_DENSE], ids=["sparse", "auto", "dense"])
 def engine_ctx(request, ctx):
     ctx.set_option(G.OPT_ENGINE, request.param)
     yield ctx

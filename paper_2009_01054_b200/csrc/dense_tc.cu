@@ -147,6 +147,7 @@ struct EpiParams {
 
 constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
 constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk (KC = 128)
+constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
 constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
 constexpr int A_BYTES = BM * BK * 4;              // 16 KB
@@ -170,7 +171,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_tile = blockIdx.x, m_tile = blockIdx.y;
+    // grouped rasterization: consecutive CTAs sweep GROUP_M row-tiles x a few column-tiles,
+    // so the CTAs resident in one wave share their A and B k-slabs through L2
+    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const int pid = blockIdx.x, in_group = GROUP_M * num_n;
+    const int first_m = (pid / in_group) * GROUP_M;
+    const int group_m = min(num_m - first_m, GROUP_M);
+    const int m_tile = first_m + (pid % in_group) % group_m;
+    const int n_tile = (pid % in_group) / group_m;
     const int m0 = m_tile * BM, n0 = n_tile * BN;
     const int nk = (K + BK - 1) / BK;
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
@@ -412,7 +420,7 @@ static void launch_gemm(gvt_ctx *c, int kind_id, const float *Ahi, const float *
             cudaFuncSetAttribute(k_gemm_tf32x3<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
         attr[EPI] = true;
     }
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    dim3 grid((unsigned)(((N + BN - 1) / BN) * ((M + BM - 1) / BM)));
     GVT_LAUNCH(c, kind_id, k_gemm_tf32x3<EPI>, grid, NTHREADS, SMEM_TOTAL, ah, al, bh, bl, (int)M, (int)N, (int)K,
                ep);
 }

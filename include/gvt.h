@@ -94,7 +94,9 @@ typedef enum {
     GVT_OPT_ENGINE = 0,          /* 0 = auto by density (default), 1 = sparse SIMT, 2 = dense tensor-core */
     GVT_OPT_DENSE_THRESHOLD = 1, /* pair-matrix density at or above which auto picks dense (default 0.02) */
     GVT_OPT_PROFILE = 2,         /* 1 = record per-kernel CUDA-event times (gvt_get_stats)                */
-    GVT_OPT_GRAM_ENGINE = 3      /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
+    GVT_OPT_GRAM_ENGINE = 3,     /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
+    GVT_OPT_TC_PRECISION = 4     /* tensor-core split: 0 = 3xFP16 with per-row power-of-two scaling
+                                    (default), 1 = 3xTF32; both fp32-accurate (reading S16)          */
 } gvt_option;
 
 /* Per-context counters (gvt_get_stats). */

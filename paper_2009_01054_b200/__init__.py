@@ -33,7 +33,8 @@ LINEAR, POLY2D, GAUSSIAN, KRONECKER, SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK, CA
 BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY = range(3)
 FACTOR_DRUG, FACTOR_TARGET, FACTOR_ONES, FACTOR_IDENTITY = range(4)
 SEL_FIRST, SEL_SECOND = 0, 1
-OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE = range(4)
+OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE, OPT_TC_PRECISION = range(5)
+PREC_FP16X3, PREC_TF32X3 = 0, 1
 ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE = 0, 1, 2
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32

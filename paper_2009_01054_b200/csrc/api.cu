@@ -117,6 +117,10 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         GVT_REQUIRE(v == 0 || v == 1 || v == 2, GVT_E_PARAM, "gram engine must be 0, 1 or 2");
         c->gram_engine = (int)v;
         break;
+    case GVT_OPT_TC_PRECISION:
+        GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "tc precision must be 0 (fp16 x3) or 1 (tf32 x3)");
+        c->tc_precision = (int)v;
+        break;
     default: throw Error{GVT_E_PARAM, "unknown option"};
     }
     GVT_API_END

@@ -1,24 +1,29 @@
-// dense_tc.cu -- dense tensor-core engine on sm_100a: tcgen05.mma kind::tf32 with the
-// 3xTF32 split (hi*hi + hi*lo + lo*hi) so that the result is fp32-accurate (reading
-// S16).  Operands are staged by TMA (SWIZZLE_128B, K-major) through an mbarrier ring; one
-// elected thread issues the MMAs; accumulators live in TMEM.
+// dense_tc.cu -- dense tensor-core engine on sm_100a.  C = A B^T with fp32-accurate
+// results from 3 low-precision tensor-core products (hi*hi + hi*lo + lo*hi):
+//   PREC_F16  (default) kind::f16: every operand row is scaled by a power of two so its
+//             largest entry sits just below 2^15, then split hi = fp16(x), lo = fp16(x - hi)
+//             (22 significant bits); 2x the MAC rate of TF32 at half the bytes.
+//   PREC_TF32 kind::tf32: hi = rna_tf32(x), lo = rna_tf32(x - hi), no scaling.
+// Operands are staged by TMA (SWIZZLE_128B, K-major, 128-byte rows = 64 fp16 / 32 tf32)
+// through an mbarrier ring; one elected thread issues the MMAs; accumulators live in TMEM.
 //
 // Precision: the tensor core truncates every accumulation into its fp32 accumulator, a
-// bias that grows with K.  The kernel therefore accumulates K in chunks of KC = 128
-// (fresh accumulator per chunk, double-buffered in TMEM: 2 x 256 columns) and the
-// epilogue warps add the chunk results into fp32 registers with round-to-nearest while
-// the MMA warp works on the next chunk.
+// bias that grows with K.  The kernel therefore accumulates K in chunks (fresh accumulator
+// per chunk, double-buffered in TMEM: 2 x 256 columns) and the epilogue warps add the
+// chunk results into fp32 registers with round-to-nearest while the MMA warp works on the
+// next chunk.  Row scales are exact powers of two, undone in the epilogue.
 //
 // One kernel, three epilogues:
-//   EPI_SPLIT   C = A B^T stored as (hi, lo) tf32 pairs  -> GVT stage 1, S = C_fac X^T
+//   EPI_STORE   C stored fp32 (+ optional tf32 hi/lo)   -> GVT stage 1, S = C_fac X^T
 //   EPI_SAMPLED out[dst] (+)= coef (A B^T)[r, c] for the samples bucketed on this tile
 //               -> GVT stage 2 (sampled D S^T, north-star kernel (3), dense-tile form)
 //   EPI_GRAM    K = k(X_i, X_j) from the dot product and row norms -> base-kernel Gram,
 //               north-star kernel (1)
-// Tile 128 x 256, BK = 32 fp32 (one 128-byte swizzle row), 2-stage ring of 96 KB.
+// Tile 128 x 256, 128-byte K-blocks, 2-stage ring of 96 KB, grouped rasterization.
 // Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..9 epilogue (warp w reads TMEM
 // lanes 32*(w%4).. and columns 128*((w-2)/4)..).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -79,18 +84,30 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     return d;
 }
 
-// instruction descriptor: D f32, A/B tf32, K-major both, M = 128, N = BN
-template <int BN>
-__host__ __device__ constexpr uint32_t idesc_tf32() {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+enum { PREC_F16 = 0, PREC_TF32 = 1 };
+
+// instruction descriptor: D f32, A/B tf32 (format 2) or f16 (format 0), K-major both, M = 128
+template <int PREC, int N>
+__host__ __device__ constexpr uint32_t idesc_mma() {
+    return (1u << 4) | ((PREC == PREC_TF32 ? 2u : 0u) << 7) | ((PREC == PREC_TF32 ? 2u : 0u) << 10) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+template <int PREC>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    if (PREC == PREC_TF32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    }
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -124,12 +141,15 @@ __device__ __forceinline__ float tf32_round(float x) {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // ----------------------------------------------------------------------------- kernel
-enum { EPI_SPLIT = 0, EPI_SAMPLED = 1, EPI_GRAM = 2 };
+enum { EPI_STORE = 0, EPI_SAMPLED = 1, EPI_GRAM = 2 };
 
 struct EpiParams {
-    // split
-    float *c_hi, *c_lo, *c_f;
+    // store
+    float *c_f;                // fp32 C (ldc)
+    float *c_hi, *c_lo;        // optional tf32 split of C (ldc)
     int64_t ldc;
+    // operand row scales (inverse powers of two), nullable
+    const float *sa, *sb;
     // sampled
     const int32_t *s_r, *s_c, *s_dst;
     const int64_t *chunk_ptr;  // per (tile, 32-column chunk)
@@ -145,23 +165,24 @@ struct EpiParams {
     int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
 };
 
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 2;
-constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk (KC = 128)
+constexpr int BM = 128, BN = 256, KB_BYTES = 128, STAGES = 2;
+constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
 constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
-constexpr int A_BYTES = BM * BK * 4;              // 16 KB
-constexpr int B_BYTES = BN * BK * 4;              // 32 KB
+constexpr int A_BYTES = BM * KB_BYTES;            // 16 KB
+constexpr int B_BYTES = BN * KB_BYTES;            // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 96 KB
 constexpr int BAR_OFF = STAGES * STAGE_BYTES;
 constexpr int SMEM_TOTAL = BAR_OFF + 256 + 1024;        // barriers + tmem slot + alignment slack
 static_assert(N_EPI_WARPS * 32 * 33 * 4 <= STAGES * STAGE_BYTES, "epilogue staging aliases the stage ring");
 
-template <int EPI>
+template <int PREC, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
-                  const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N,
-                  int K, EpiParams ep) {
+    k_gemm_x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+              const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N, int K,
+              EpiParams ep) {
+    constexpr int BKE = PREC == PREC_TF32 ? 32 : 64;  // elements per 128-byte K-block
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int m_tile = first_m + (pid % in_group) % group_m;
     const int n_tile = (pid % in_group) / group_m;
     const int m0 = m_tile * BM, n0 = n_tile * BN;
-    const int nk = (K + BK - 1) / BK;
+    const int nk = (K + BKE - 1) / BKE;
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
     const int nch = (nk + kcb - 1) / kcb;
 
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t *st = smem + s * STAGE_BYTES;
                 mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-                const int kc = kb * BK;
+                const int kc = kb * BKE;
                 tma_load_2d(st, &tmAh, &full[s], kc, m0);
                 tma_load_2d(st + A_BYTES, &tmAl, &full[s], kc, m0);
                 tma_load_2d(st + 2 * A_BYTES, &tmBh, &full[s], kc, n0);
@@ -227,7 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer (single thread)
-            constexpr uint32_t idesc = idesc_tf32<BN>();
+            constexpr uint32_t idesc = idesc_mma<PREC, BN>();
             int kb = 0;
             for (int ch = 0; ch < nch; ch++) {
                 const int b = ch & 1;
@@ -244,13 +265,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t ah = base, al = base + A_BYTES, bh = base + 2 * A_BYTES,
                                    bl = base + 2 * A_BYTES + B_BYTES;
 #pragma unroll
-                    for (int k = 0; k < BK / 8; k++) {
-                        const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t off = k * 32;  // one MMA K-step = 32 bytes inside the swizzle atom
                         const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
                         const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
-                        mma_tf32(acc, dah, dbh, idesc, (kk | k) != 0);
-                        mma_tf32(acc, dah, dbl, idesc, 1);
-                        mma_tf32(acc, dal, dbh, idesc, 1);
+                        mma_issue<PREC>(acc, dah, dbh, idesc, (kk | k) != 0);
+                        mma_issue<PREC>(acc, dah, dbl, idesc, 1);
+                        mma_issue<PREC>(acc, dal, dbh, idesc, 1);
                     }
                     mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
                 }
@@ -283,38 +304,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
         }
+        const int gc_base = n0 + half * 128;
+        // undo the operand row scales (exact powers of two)
+        if (ep.sa || ep.sb) {
+            const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+#pragma unroll
+            for (int i = 0; i < 128; i++) {
+                const int gc = gc_base + i;
+                const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                run[i] *= ra * rb;
+            }
+        }
         // all MMAs are complete (the last tfull was committed after them), so the stage ring is
         // free and serves as staging memory for the sampled epilogue
-        const int gc_base = n0 + half * 128;
-        if (EPI == EPI_SPLIT) {
+        if (EPI == EPI_STORE) {
             if (gr < M) {
-                float *hi = ep.c_hi + (int64_t)gr * ep.ldc + gc_base;
-                float *lo = ep.c_lo + (int64_t)gr * ep.ldc + gc_base;
+                float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
                 if (gc_base + 128 <= N) {
 #pragma unroll
-                    for (int i = 0; i < 128; i += 4) {
-                        float4 h, l;
-                        h.x = tf32_round(run[i]);     l.x = tf32_round(run[i] - h.x);
-                        h.y = tf32_round(run[i + 1]); l.y = tf32_round(run[i + 1] - h.y);
-                        h.z = tf32_round(run[i + 2]); l.z = tf32_round(run[i + 2] - h.z);
-                        h.w = tf32_round(run[i + 3]); l.w = tf32_round(run[i + 3] - h.w);
-                        *reinterpret_cast<float4 *>(hi + i) = h;
-                        *reinterpret_cast<float4 *>(lo + i) = l;
-                    }
-                    if (ep.c_f) {
-                        float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
+                    for (int i = 0; i < 128; i += 4)
+                        *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                    if (ep.c_hi) {
+                        float *hi = ep.c_hi + (int64_t)gr * ep.ldc + gc_base;
+                        float *lo = ep.c_lo + (int64_t)gr * ep.ldc + gc_base;
 #pragma unroll
-                        for (int i = 0; i < 128; i += 4)
-                            *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                        for (int i = 0; i < 128; i += 4) {
+                            float4 h, l;
+                            h.x = tf32_round(run[i]);     l.x = tf32_round(run[i] - h.x);
+                            h.y = tf32_round(run[i + 1]); l.y = tf32_round(run[i + 1] - h.y);
+                            h.z = tf32_round(run[i + 2]); l.z = tf32_round(run[i + 2] - h.z);
+                            h.w = tf32_round(run[i + 3]); l.w = tf32_round(run[i + 3] - h.w);
+                            *reinterpret_cast<float4 *>(hi + i) = h;
+                            *reinterpret_cast<float4 *>(lo + i) = l;
+                        }
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < 128; i++) {
                         if (gc_base + i < N) {
-                            float h = tf32_round(run[i]);
-                            hi[i] = h;
-                            lo[i] = tf32_round(run[i] - h);
-                            if (ep.c_f) ep.c_f[(int64_t)gr * ep.ldc + gc_base + i] = run[i];
+                            cf[i] = run[i];
+                            if (ep.c_hi) {
+                                float h = tf32_round(run[i]);
+                                ep.c_hi[(int64_t)gr * ep.ldc + gc_base + i] = h;
+                                ep.c_lo[(int64_t)gr * ep.ldc + gc_base + i] = tf32_round(run[i] - h);
+                            }
                         }
                     }
                 }
@@ -389,43 +422,57 @@ static void get_encode() {
     g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
 }
 
-// rows x cols (cols = K, contiguous) fp32 matrix with leading dimension ld; box (32, box_rows)
-static CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// rows x cols (cols = K, contiguous) matrix, element size esz, leading dimension ld elements;
+// box = one 128-byte K-block x box_rows
+static CUtensorMap make_map(const void *p, int esz, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     get_encode();
     CUtensorMap m;
     cuuint64_t dims[2] = {(cuuint64_t)(cols > 0 ? cols : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
+    cuuint32_t box[2] = {(cuuint32_t)(KB_BYTES / esz), (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = g_encode(&m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                          const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     GVT_REQUIRE(r == CUDA_SUCCESS, GVT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
 }
 
 bool tc_available(gvt_ctx *c) { return c->tc_ok; }
 
-template <int EPI>
-static void launch_gemm(gvt_ctx *c, int kind_id, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi,
-                        const float *Blo, int64_t ldb, int64_t M, int64_t N, int64_t K, const EpiParams &ep) {
-    if (M == 0 || N == 0) return;
-    GVT_REQUIRE(K > 0, GVT_E_DIM, "GEMM with K = 0");
-    GVT_REQUIRE(M < INT32_MAX && N < INT32_MAX && K < INT32_MAX, GVT_E_DIM, "GEMM dimension too large");
-    CUtensorMap ah = make_map(Ahi, M, K, lda, BM), al = make_map(Alo, M, K, lda, BM);
-    CUtensorMap bh = make_map(Bhi, N, K, ldb, BN), bl = make_map(Blo, N, K, ldb, BN);
-    static bool attr[3] = {false, false, false};
-    if (!attr[EPI]) {
+template <int PREC, int EPI>
+static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Operand &B, int64_t M, int64_t N,
+                          int64_t K, EpiParams ep) {
+    constexpr int esz = PREC == PREC_TF32 ? 4 : 2;
+    CUtensorMap ah = make_map(A.hi, esz, M, K, A.ld, BM), al = make_map(A.lo, esz, M, K, A.ld, BM);
+    CUtensorMap bh = make_map(B.hi, esz, N, K, B.ld, BN), bl = make_map(B.lo, esz, N, K, B.ld, BN);
+    ep.sa = A.scale;
+    ep.sb = B.scale;
+    static bool attr = false;
+    if (!attr) {
         GVT_CUDA_TRY(
-            cudaFuncSetAttribute(k_gemm_tf32x3<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
-        attr[EPI] = true;
+            cudaFuncSetAttribute(k_gemm_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
+        attr = true;
     }
     dim3 grid((unsigned)(((N + BN - 1) / BN) * ((M + BM - 1) / BM)));
-    GVT_LAUNCH(c, kind_id, k_gemm_tf32x3<EPI>, grid, NTHREADS, SMEM_TOTAL, ah, al, bh, bl, (int)M, (int)N, (int)K,
+    GVT_LAUNCH(c, kind_id, (k_gemm_x3<PREC, EPI>), grid, NTHREADS, SMEM_TOTAL, ah, al, bh, bl, (int)M, (int)N, (int)K,
                ep);
 }
 
-__global__ void k_split(const float *__restrict__ x, int64_t n, float *__restrict__ hi, float *__restrict__ lo) {
+template <int EPI>
+static void launch_gemm(gvt_ctx *c, int kind_id, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
+                        const EpiParams &ep) {
+    if (M == 0 || N == 0) return;
+    GVT_REQUIRE(K > 0, GVT_E_DIM, "GEMM with K = 0");
+    GVT_REQUIRE(M < INT32_MAX && N < INT32_MAX && K < INT32_MAX, GVT_E_DIM, "GEMM dimension too large");
+    GVT_REQUIRE(A.prec == B.prec, GVT_E_STATE, "GEMM operands split with different precisions");
+    if (A.prec == PREC_TF32) launch_gemm_t<PREC_TF32, EPI>(c, kind_id, A, B, M, N, K, ep);
+    else launch_gemm_t<PREC_F16, EPI>(c, kind_id, A, B, M, N, K, ep);
+}
+
+// ----------------------------------------------------------------------------- operand splits
+__global__ void k_split_tf32(const float *__restrict__ x, int64_t n, float *__restrict__ hi, float *__restrict__ lo) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float v = x[i];
         float h = tf32_round(v);
@@ -434,48 +481,113 @@ __global__ void k_split(const float *__restrict__ x, int64_t n, float *__restric
     }
 }
 
-void split_tf32(gvt_ctx *c, const float *x, int64_t count, float *hi, float *lo) {
-    if (count == 0) return;
-    GVT_LAUNCH(c, K_SPLIT, k_split, grid1d(count, 256, 16 * c->sm_count * 8), 256, 0, x, count, hi, lo);
+// one block per row: scale = 2^(14 - ceil(log2 max|x|)) so the row max lies in [2^14, 2^15)
+// (exact power of two; all-zero rows get scale 1); hi = fp16(s x), lo = fp16(s x - hi);
+// stores 1/scale for the epilogue.  Columns [cols, ld) are written as zero.
+__global__ void __launch_bounds__(256) k_split_rows_f16(const float *__restrict__ x, int64_t rows, int64_t cols,
+                                                        int64_t ldx, __half *__restrict__ hi,
+                                                        __half *__restrict__ lo, int64_t ld, float *__restrict__ sinv) {
+    __shared__ float red[8];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float *xr = x + r * ldx;
+        float mx = 0.f;
+        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(xr[j]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = red[0];
+        for (int w = 1; w < 8; w++) mx = fmaxf(mx, red[w]);
+        __syncthreads();
+        int e = 0;
+        if (mx > 0.f && isfinite(mx)) {
+            int ex;
+            frexpf(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)  ->  mx < 2^ex
+            e = 15 - ex;      // scaled max < 2^15
+        }
+        const float s = ldexpf(1.f, e);
+        if (threadIdx.x == 0) sinv[r] = ldexpf(1.f, -e);
+        __half *hr = hi + r * ld, *lr = lo + r * ld;
+        for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) {
+            const float v = j < cols ? xr[j] * s : 0.f;
+            const __half h = __float2half_rn(v);
+            hr[j] = h;
+            lr[j] = __float2half_rn(v - __half2float(h));
+        }
+    }
+}
+
+static int tc_prec(gvt_ctx *c) { return c->tc_precision == 1 ? PREC_TF32 : PREC_F16; }
+
+int tc_precision_mode(gvt_ctx *c) { return tc_prec(c); }
+
+// split a rows x cols fp32 matrix (leading dimension ldx) into a tensor-core operand with
+// leading dimension ld (>= cols, multiple of 32); rows_pad rows are allocated (extra rows zero)
+Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows, int64_t cols, int64_t ldx,
+                     int64_t ld, int64_t rows_pad) {
+    Operand o;
+    o.prec = tc_prec(c);
+    o.ld = ld;
+    std::string nm(name);
+    if (o.prec == PREC_TF32) {
+        GVT_REQUIRE(ldx == ld, GVT_E_STATE, "tf32 split expects a padded source");
+        float *hi = wsT<float>(c, (nm + ".hi").c_str(), (size_t)rows_pad * ld);
+        float *lo = wsT<float>(c, (nm + ".lo").c_str(), (size_t)rows_pad * ld);
+        if (rows_pad * ld > 0)
+            GVT_LAUNCH(c, K_SPLIT, k_split_tf32, grid1d(rows_pad * ld, 256, 16 * c->sm_count * 8), 256, 0, x,
+                       rows_pad * ld, hi, lo);
+        o.hi = hi;
+        o.lo = lo;
+        o.scale = nullptr;
+    } else {
+        __half *hi = wsT<__half>(c, (nm + ".h16").c_str(), (size_t)rows_pad * ld);
+        __half *lo = wsT<__half>(c, (nm + ".l16").c_str(), (size_t)rows_pad * ld);
+        float *s = wsT<float>(c, (nm + ".sinv").c_str(), (size_t)rows_pad);
+        if (rows_pad > rows) {
+            GVT_CUDA_TRY(cudaMemsetAsync(hi + rows * ld, 0, sizeof(__half) * (rows_pad - rows) * ld, c->stream));
+            GVT_CUDA_TRY(cudaMemsetAsync(lo + rows * ld, 0, sizeof(__half) * (rows_pad - rows) * ld, c->stream));
+        }
+        if (rows > 0)
+            GVT_LAUNCH(c, K_SPLIT, k_split_rows_f16, grid1d(rows, 1, 16 * c->sm_count), 256, 0, x, rows, cols, ldx, hi,
+                       lo, ld, s);
+        o.hi = hi;
+        o.lo = lo;
+        o.scale = s;
+    }
+    return o;
 }
 
 // X[row][col] = sum of the (row, col) run of sorted entries (deterministic, in entry order)
 __global__ void k_densify(const int32_t *__restrict__ row, const int32_t *__restrict__ col,
-                          const float *__restrict__ val, int64_t E, float *__restrict__ Xhi, float *__restrict__ Xlo,
-                          int64_t ldX) {
+                          const float *__restrict__ val, int64_t E, float *__restrict__ X, int64_t ldX) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = row[k], cc = col[k];
         if (k > 0 && row[k - 1] == r && col[k - 1] == cc) continue;  // not the head of its run
         float s = val[k];
         for (int64_t j = k + 1; j < E && row[j] == r && col[j] == cc; j++) s += val[j];
-        const float h = tf32_round(s);
-        Xhi[(int64_t)r * ldX + cc] = h;
-        Xlo[(int64_t)r * ldX + cc] = tf32_round(s - h);
+        X[(int64_t)r * ldX + cc] = s;
     }
 }
 
-void densify(gvt_ctx *c, const EntryPlan &e, float *Xhi, float *Xlo, int64_t ldX, int64_t rows_pad) {
-    GVT_CUDA_TRY(cudaMemsetAsync(Xhi, 0, sizeof(float) * rows_pad * ldX, c->stream));
-    GVT_CUDA_TRY(cudaMemsetAsync(Xlo, 0, sizeof(float) * rows_pad * ldX, c->stream));
+void densify(gvt_ctx *c, const EntryPlan &e, float *X, int64_t ldX, int64_t rows_pad) {
+    GVT_CUDA_TRY(cudaMemsetAsync(X, 0, sizeof(float) * rows_pad * ldX, c->stream));
     if (e.nnz == 0) return;
     GVT_LAUNCH(c, K_DENSIFY, k_densify, grid1d(e.nnz, 256, 16 * c->sm_count * 8), 256, 0, e.row, e.col, e.val, e.nnz,
-               Xhi, Xlo, ldX);
+               X, ldX);
 }
 
-void gemm_nt_split(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
-                   int64_t ldb, int64_t M, int64_t N, int64_t K, float *Chi, float *Clo, float *Cf, int64_t ldc) {
+void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, float *Cf,
+                   int64_t ldc, float *Chi, float *Clo) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
+    ep.c_f = Cf;
     ep.c_hi = Chi;
     ep.c_lo = Clo;
-    ep.c_f = Cf;
     ep.ldc = ldc;
-    launch_gemm<EPI_SPLIT>(c, K_STAGE1_TC, Ahi, Alo, lda, Bhi, Blo, ldb, M, N, K, ep);
+    launch_gemm<EPI_STORE>(c, K_STAGE1_TC, A, B, M, N, K, ep);
 }
 
-void gemm_nt_sampled(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
-                     int64_t ldb, int64_t M, int64_t N, int64_t K, const SamplePlan &sp, float coef, int accumulate,
-                     float *out) {
+void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
+                     const SamplePlan &sp, float coef, int accumulate, float *out) {
     if (sp.ns == 0) return;
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -487,7 +599,7 @@ void gemm_nt_sampled(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda
     ep.coef = coef;
     ep.accumulate = accumulate;
     ep.out = out;
-    launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, Ahi, Alo, lda, Bhi, Blo, ldb, M, N, K, ep);
+    launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
 }
 
 // ----------------------------------------------------------------------------- sample bucketing
@@ -575,11 +687,9 @@ void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, doubl
     if (m == 0) return;
     const int64_t ldx = round_up(dim, 32), rows = round_up(m, 128);
     float *xp = wsT<float>(c, "gram.xp", rows * ldx);
-    float *xh = wsT<float>(c, "gram.xh", rows * ldx);
-    float *xl = wsT<float>(c, "gram.xl", rows * ldx);
     float *nr = wsT<float>(c, "gram.norms", rows);
     pad_copy(c, X, m, dim, dim, xp, ldx, rows);
-    split_tf32(c, xp, rows * ldx, xh, xl);
+    Operand xo = make_operand(c, "gram.x", xp, m, dim, ldx, ldx, rows);
     if (kind == GVT_BASE_GAUSSIAN)
         GVT_LAUNCH(c, K_GRAM_TC, k_norms, grid1d(m * 32, 256, 4096), 256, 0, X, m, dim, nr);
     EpiParams ep;
@@ -591,8 +701,8 @@ void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, doubl
     ep.gamma = (float)gamma;
     ep.coef0 = (float)coef0;
     ep.degree = degree;
-    ep.kcb = 1;  // short K (feature dim): one 32-wide k-block per fp32 round-to-nearest drain
-    launch_gemm<EPI_GRAM>(c, K_GRAM_TC, xh, xl, ldx, xh, xl, ldx, m, m, dim, ep);
+    ep.kcb = 1;  // short K (feature dim): one K-block per fp32 round-to-nearest drain
+    launch_gemm<EPI_GRAM>(c, K_GRAM_TC, xo, xo, m, m, dim, ep);
 }
 
 }  // namespace gvt

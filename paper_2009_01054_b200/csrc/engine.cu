@@ -193,10 +193,10 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
     bool tc = tc_available(c);
     if (c->engine == 2) {
         GVT_REQUIRE(tc, GVT_E_CUDA, "dense tensor-core engine requested but not available on this device");
-        if (g.A.hi && g.C.hi) return 2;
+        if (g.A.split && g.C.split) return 2;
         return 1;  // materialised Ones/Identity factors of a generic term list stay on SIMT
     }
-    if (!(g.A.hi && g.C.hi)) return 1;  // factors were not split for tensor cores
+    if (!(g.A.split && g.C.split)) return 1;  // factors were not split for tensor cores
     double cells = (double)g.m_in * (double)g.C.n;
     double density = cells > 0 ? (double)g.ent.nnz / cells : 0.0;
     return (tc && density >= c->dense_threshold) ? 2 : 1;
@@ -326,18 +326,17 @@ static void run_group(gvt_ctx *c, GroupPlan &g, const float *p, float coef, int 
     entry_values(c, g.ent, p);
     c->last_engine = g.engine;
     if (g.engine == 2) {
-        // dense tensor-core engine: X densified (hi/lo), S = C X^T, sampled A S^T
+        // dense tensor-core engine: X densified and split, S = C X^T (fp32), S split,
+        // sampled A S^T written straight to the outputs
         int64_t ldX = round_up(g.C.n > 0 ? g.C.n : 1, 32);  // X: m_in x q_in
         int64_t rows_pad = round_up(g.m_in > 0 ? g.m_in : 1, 128);
-        float *Xhi = wsT<float>(c, "dense.Xhi", (size_t)rows_pad * ldX);
-        float *Xlo = wsT<float>(c, "dense.Xlo", (size_t)rows_pad * ldX);
-        densify(c, g.ent, Xhi, Xlo, ldX, rows_pad);
+        float *X = wsT<float>(c, "dense.X", (size_t)rows_pad * ldX);
+        densify(c, g.ent, X, ldX, rows_pad);
+        Operand xo = make_operand(c, "dense.Xop", X, g.m_in, g.C.n, ldX, ldX, rows_pad);
         int64_t qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
-        float *Shi = wsT<float>(c, "dense.Shi", (size_t)qpad * g.ldS);
-        float *Slo = wsT<float>(c, "dense.Slo", (size_t)qpad * g.ldS);
-        gemm_nt_split(c, g.C.hi, g.C.lo, g.C.ld, Xhi, Xlo, ldX, g.q_out, g.m_in, g.C.n, Shi, Slo, nullptr, g.ldS);
-        gemm_nt_sampled(c, g.A.hi, g.A.lo, g.A.ld, Shi, Slo, g.ldS, g.A.n, g.q_out, g.m_in, g.smp, coef, accumulate,
-                        out);
+        gemm_nt_store(c, g.C.op, xo, g.q_out, g.m_in, g.C.n, g.S, g.ldS, nullptr, nullptr);
+        Operand so = make_operand(c, "dense.Sop", g.S, g.q_out, g.m_in, g.ldS, g.ldS, qpad);
+        gemm_nt_sampled(c, g.A.op, so, g.A.n, g.q_out, g.m_in, g.smp, coef, accumulate, out);
     } else {
         stage1_sparse(c, g.ent, g.C, g.q_out, g.S, g.ldS);
         stage2_gather(c, g.smp, g.A, g.S, g.ldS, g.m_in, coef, accumulate, out);
@@ -414,11 +413,8 @@ static Factor prepare_factor(gvt_ctx *c, const char *name, const float *user, in
     }
     f.p = d;
     if (need_split) {
-        float *hi = wsT<float>(c, (nm + ".hi").c_str(), (size_t)rows_pad * f.ld);
-        float *lo = wsT<float>(c, (nm + ".lo").c_str(), (size_t)rows_pad * f.ld);
-        split_tf32(c, d, rows_pad * f.ld, hi, lo);
-        f.hi = hi;
-        f.lo = lo;
+        f.op = make_operand(c, (nm + ".op").c_str(), d, n, n, f.ld, f.ld, rows_pad);
+        f.split = true;
     }
     return f;
 }

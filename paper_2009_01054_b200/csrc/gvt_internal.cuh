@@ -87,6 +87,7 @@ struct gvt_ctx {
     double dense_threshold = 0.02;
     int profile = 0;
     int gram_engine = 0;
+    int tc_precision = 0;  // 0 = 3xFP16 with row scaling, 1 = 3xTF32
     int last_engine = 0;
 
     // workspaces by name (grow-only)

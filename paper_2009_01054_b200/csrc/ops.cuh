@@ -5,13 +5,24 @@
 
 namespace gvt {
 
+// A tensor-core GEMM operand: rows of a matrix split into (hi, lo) pieces, K-major with
+// leading dimension ld.  prec 0 = fp16 pieces with per-row power-of-two scale (scale[r] =
+// 1/s_r), prec 1 = tf32 pieces in fp32 containers (scale == nullptr).
+struct Operand {
+    int prec = 0;
+    const void *hi = nullptr, *lo = nullptr;
+    const float *scale = nullptr;
+    int64_t ld = 0;
+};
+
 // A square factor (Gram / materialised ones / identity) copied to a padded device
 // buffer: n x n, leading dimension ld = round_up(n, 32), padding zero.  For the dense
-// tensor-core engine the 3xTF32 split hi/lo (same layout) is attached on demand.
+// tensor-core engine its split operand is attached on demand.
 struct Factor {
     const float *p = nullptr;
     int64_t n = 0, ld = 0;
-    const float *hi = nullptr, *lo = nullptr;
+    Operand op;
+    bool split = false;
 };
 
 // one entry kind of the pair matrix X (row selector, column selector, sign), see engine.cu
@@ -74,15 +85,18 @@ void scale_copy(gvt_ctx *c, const float *x, float alpha, int64_t n, float *y);
 
 // ---- dense tensor-core engine (dense_tc.cu)
 bool tc_available(gvt_ctx *c);
-void split_tf32(gvt_ctx *c, const float *x, int64_t count, float *hi, float *lo);
-void densify(gvt_ctx *c, const EntryPlan &e, float *Xhi, float *Xlo, int64_t ldX, int64_t rows_pad);
-// S (rows x cols, ld) = C (rows x K) * X^T (X: cols x K), 3xTF32, writes S_hi/S_lo
-void gemm_nt_split(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi, const float *Blo,
-                   int64_t ldb, int64_t M, int64_t N, int64_t K, float *Chi, float *Clo, float *Cf, int64_t ldc);
+int tc_precision_mode(gvt_ctx *c);
+// split a rows x cols fp32 matrix (leading dim ldx) into an operand with leading dim ld
+Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows, int64_t cols, int64_t ldx,
+                     int64_t ld, int64_t rows_pad);
+// X (rows_pad x ldX fp32, zeroed) <- pair matrix from the sorted entries (duplicates summed)
+void densify(gvt_ctx *c, const EntryPlan &e, float *X, int64_t ldX, int64_t rows_pad);
+// C (M x N, ldc) = A (M x K) * B^T (B: N x K), fp32-accurate; optional tf32 split of C
+void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, float *Cf,
+                   int64_t ldc, float *Chi, float *Clo);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
-void gemm_nt_sampled(gvt_ctx *c, const float *Ahi, const float *Alo, int64_t lda, const float *Bhi,
-                     const float *Blo, int64_t ldb, int64_t M, int64_t N, int64_t K, const SamplePlan &sp,
-                     float coef, int accumulate, float *out);
+void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
+                     const SamplePlan &sp, float coef, int accumulate, float *out);
 void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol);
 
 // ---- Gram (gram.cu)

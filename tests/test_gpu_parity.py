@@ -45,11 +45,14 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(params=[G.ENGINE_SPARSE, G.ENGINE_AUTO, G.ENGINE_DENSE], ids=["sparse", "auto", "dense"])
+@pytest.fixture(params=[(G.ENGINE_SPARSE, 0), (G.ENGINE_AUTO, 0), (G.ENGINE_DENSE, G.PREC_FP16X3),
+                        (G.ENGINE_DENSE, G.PREC_TF32X3)], ids=["sparse", "auto", "dense-fp16x3", "dense-tf32x3"])
 def engine_ctx(request, ctx):
-    ctx.set_option(G.OPT_ENGINE, request.param)
+    ctx.set_option(G.OPT_ENGINE, request.param[0])
+    ctx.set_option(G.OPT_TC_PRECISION, request.param[1])
     yield ctx
     ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    ctx.set_option(G.OPT_TC_PRECISION, G.PREC_FP16X3)
 
 
 def grams_oracle(w):
@@ -70,9 +73,10 @@ def f32(x):
 
 # ----------------------------------------------------------------------------- Gram
 @pytest.mark.parametrize("kind", [G.BASE_LINEAR, G.BASE_GAUSSIAN, G.BASE_POLY])
-@pytest.mark.parametrize("gram_engine", [1, 0], ids=["simt", "auto"])
-def test_gram_parity(ctx, kind, gram_engine):
+@pytest.mark.parametrize("gram_engine,prec", [(1, 0), (0, 0), (0, 1)], ids=["simt", "tc-fp16x3", "tc-tf32x3"])
+def test_gram_parity(ctx, kind, gram_engine, prec):
     ctx.set_option(G.OPT_GRAM_ENGINE, gram_engine)
+    ctx.set_option(G.OPT_TC_PRECISION, prec)
     rng = np.random.default_rng(kind)
     for m, dim in [(1, 5), (300, 37), (517, 128)]:       # several tiles, ragged tails
         X = rng.standard_normal((m, dim)).astype(np.float32)
@@ -83,6 +87,7 @@ def test_gram_parity(ctx, kind, gram_engine):
         if kind == G.BASE_GAUSSIAN:
             assert np.all(np.diag(K) == 1.0)
     ctx.set_option(G.OPT_GRAM_ENGINE, 0)
+    ctx.set_option(G.OPT_TC_PRECISION, 0)
 
 
 def test_gram_errors(ctx):

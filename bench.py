@@ -239,7 +239,7 @@ def run_gpu(args, rank, world, local_rank):
         lo, hi = bounds[rank], bounds[rank + 1]
         sel = (f >= lo) & (f < hi)
         f, s, y = f[sel], s[sel], y[sel]
-        tsel = np.arange(len(tf_)) % world == rank
+        tsel = (tf_ >= lo) & (tf_ < hi)       # test pairs sharded by the same drug ranges
         tf_, ts_ = tf_[tsel], ts_[tsel]
     n_local, nt_local = len(f), len(tf_)
 

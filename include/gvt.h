@@ -95,8 +95,10 @@ typedef enum {
     GVT_OPT_DENSE_THRESHOLD = 1, /* pair-matrix density at or above which auto picks dense (default 0.02) */
     GVT_OPT_PROFILE = 2,         /* 1 = record per-kernel CUDA-event times (gvt_get_stats)                */
     GVT_OPT_GRAM_ENGINE = 3,     /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
-    GVT_OPT_TC_PRECISION = 4     /* tensor-core split: 0 = 3xFP16 with per-row power-of-two scaling
+    GVT_OPT_TC_PRECISION = 4,    /* tensor-core split: 0 = 3xFP16 with per-row power-of-two scaling
                                     (default), 1 = 3xTF32; both fp32-accurate (reading S16)          */
+    GVT_OPT_SLABS = 5            /* single GPU: split stage 1 / stage 2 into this many X-row slabs,
+                                    exactly as the data-parallel path does across ranks (default 1) */
 } gvt_option;
 
 /* Per-context counters (gvt_get_stats). */
@@ -136,6 +138,13 @@ gvt_status gvt_comm_init(gvt_ctx *ctx, const void *nccl_unique_id, int rank, int
  * bounds[world+1] (host) with bounds[0] = 0, bounds[world] = m, each range holding about
  * sum(deg)/world pairs (greedy prefix split).  Host-only, no device work. */
 gvt_status gvt_partition(const int64_t *deg, int64_t m, int world, int64_t *bounds);
+
+/* Data-parallel slab partition of the pair-matrix rows (= S columns): given the CSR row
+ * pointer row_ptr[nrow+1] (host) of the entries, writes bounds[nslab+1] (host): bounds[0] = 0,
+ * bounds[nslab] = nrow, bounds[s] = the first row at or after the s/nslab entry quantile,
+ * rounded up to a multiple of 32 and kept monotone.  Rank s runs stage 1 on rows
+ * [bounds[s], bounds[s+1]).  Host-only, no device work. */
+gvt_status gvt_slab_bounds(const int64_t *row_ptr, int64_t nrow, int nslab, int64_t *bounds);
 
 /* decompose: the Corollary's term list for `kernel` (
  * MLPK 10-term expansion PAPER.md:736-747; Anti-symmetric as (I-P)(D(x)D), reading S3).

@@ -36,6 +36,7 @@ SEL_FIRST, SEL_SECOND = 0, 1
 OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE, OPT_TC_PRECISION = range(5)
 PREC_FP16X3, PREC_TF32X3 = 0, 1
 ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE = 0, 1, 2
+OPT_SLABS = 5
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32
 
@@ -76,6 +77,7 @@ _lib.gvt_reset_stats.argtypes = [_P]
 _lib.gvt_nccl_unique_id.argtypes = [_P]
 _lib.gvt_comm_init.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int]
 _lib.gvt_partition.argtypes = [_P, _I64, ctypes.c_int, _P]
+_lib.gvt_slab_bounds.argtypes = [_P, _I64, ctypes.c_int, _P]
 _lib.gvt_kernel_terms.argtypes = [ctypes.c_int, _P, ctypes.POINTER(ctypes.c_int)]
 _lib.gvt_gram.argtypes = [_P, ctypes.c_int, _P, _I64, _I64, ctypes.c_double, ctypes.c_double, ctypes.c_int, _P]
 _lib.gvt_matvec.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int, _P]
@@ -84,7 +86,8 @@ _lib.pairwise_krr_fit.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, 
 _lib.pairwise_predict.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int, _P]
 _lib.gvt_sort_plan.argtypes = [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int, _P, _P]
 
-EXPORTED = ["gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
+EXPORTED = ["gvt_slab_bounds",
+            "gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error"]
 
@@ -149,6 +152,14 @@ def gvt_partition(deg, world: int):
     bounds = np.zeros(world + 1, dtype=np.int64)
     _check(_lib.gvt_partition(deg.ctypes.data if deg.size else None, deg.size, world, bounds.ctypes.data),
            "gvt_partition")
+    return bounds
+
+
+def gvt_slab_bounds(row_ptr, nslab: int):
+    """Slab partition of pair-matrix rows used by the data-parallel path (host only)."""
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
+    bounds = np.zeros(nslab + 1, dtype=np.int64)
+    _check(_lib.gvt_slab_bounds(rp.ctypes.data, rp.size - 1, nslab, bounds.ctypes.data), "gvt_slab_bounds")
     return bounds
 
 

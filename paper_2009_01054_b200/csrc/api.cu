@@ -6,6 +6,7 @@
 
 namespace gvt {
 const char *last_error();
+void slab_bounds(const int64_t *rp, int64_t nrow, int G, int64_t *bounds);
 int kernel_terms(int kernel, gvt_term *o);
 void nccl_unique_id(void *out128);
 void comm_init(gvt_ctx *c, const void *id128, int rank, int world);
@@ -121,6 +122,10 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "tc precision must be 0 (fp16 x3) or 1 (tf32 x3)");
         c->tc_precision = (int)v;
         break;
+    case GVT_OPT_SLABS:
+        GVT_REQUIRE(v >= 1 && v <= 64, GVT_E_PARAM, "slabs must be in [1, 64]");
+        c->slabs = (int)v;
+        break;
     default: throw Error{GVT_E_PARAM, "unknown option"};
     }
     GVT_API_END
@@ -197,6 +202,15 @@ gvt_status gvt_partition(const int64_t *deg, int64_t m, int world, int64_t *boun
         bounds[g] = h;
     }
     bounds[world] = m;
+    return GVT_OK;
+}
+
+gvt_status gvt_slab_bounds(const int64_t *row_ptr, int64_t nrow, int nslab, int64_t *bounds) {
+    if (!row_ptr || !bounds || nrow < 0 || nslab < 1) {
+        gvt::set_error("gvt_slab_bounds: bad arguments");
+        return GVT_E_PARAM;
+    }
+    gvt::slab_bounds(row_ptr, nrow, nslab, bounds);
     return GVT_OK;
 }
 

@@ -16,6 +16,9 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -31,8 +34,12 @@ static void load_nccl() {
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-    GVT_REQUIRE(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather, GVT_E_NCCL,
-                "libnccl.so.2 lacks a required symbol");
+    g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
+    g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
+    g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
+    GVT_REQUIRE(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather &&
+                    g_nccl.Broadcast && g_nccl.GroupStart && g_nccl.GroupEnd,
+                GVT_E_NCCL, "libnccl.so.2 lacks a required symbol");
     g_nccl.h = h;
 }
 
@@ -87,6 +94,38 @@ void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats) {
     if (c->world <= 1) return;
     NCCL_TRY(g_nccl.AllGather(S + (size_t)c->rank * slab_floats, S, slab_floats, ncclFloat32,
                               (ncclComm_t)c->nccl_comm, c->stream));
+}
+
+// host-visible all-gather of one int64 per rank (plan time only: synchronises)
+std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v) {
+    std::vector<int64_t> out((size_t)c->world, v);
+    if (c->world <= 1) return out;
+    int64_t *d = wsT<int64_t>(c, "comm.counts", (size_t)c->world);
+    GVT_CUDA_TRY(cudaMemcpyAsync(d + c->rank, &v, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(g_nccl.AllGather(d + c->rank, d, 1, ncclInt64, (ncclComm_t)c->nccl_comm, c->stream));
+    GVT_CUDA_TRY(cudaMemcpyAsync(out.data(), d, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return out;
+}
+
+// variable-length all-gather: rank g contributes counts[g] elements at offsets[g] of `full`
+// (grouped broadcasts, one per root); esz 4 bytes (int32 or float32)
+void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<int64_t> &counts,
+                   const std::vector<int64_t> &offsets, bool is_float) {
+    const size_t esz = 4;
+    if (c->world <= 1) {
+        if (counts[0] > 0 && local != full)
+            GVT_CUDA_TRY(cudaMemcpyAsync(full, local, esz * counts[0], cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    NCCL_TRY(g_nccl.GroupStart());
+    for (int g = 0; g < c->world; g++) {
+        if (counts[g] == 0) continue;
+        void *dst = (char *)full + esz * offsets[g];
+        NCCL_TRY(g_nccl.Broadcast(g == c->rank ? local : dst, dst, (size_t)counts[g],
+                                  is_float ? ncclFloat32 : ncclInt32, g, (ncclComm_t)c->nccl_comm, c->stream));
+    }
+    NCCL_TRY(g_nccl.GroupEnd());
 }
 
 }  // namespace gvt

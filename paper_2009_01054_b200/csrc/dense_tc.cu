@@ -205,6 +205,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
     const int nch = (nk + kcb - 1) / kcb;
 
+    if (EPI == EPI_SAMPLED) {  // a tile that owns no sample computes nothing (uniform exit)
+        const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+        if (ep.chunk_ptr[tile * (BN / 32)] == ep.chunk_ptr[(tile + 1) * (BN / 32)]) return;
+    }
+
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmAh);
         prefetch_tmap(&tmAl);
@@ -520,6 +525,14 @@ static int tc_prec(gvt_ctx *c) { return c->tc_precision == 1 ? PREC_TF32 : PREC_
 
 int tc_precision_mode(gvt_ctx *c) { return tc_prec(c); }
 
+Operand operand_col_offset(const Operand &o, int64_t off) {
+    Operand v = o;
+    const int64_t esz = o.prec == PREC_TF32 ? 4 : 2;
+    v.hi = (const char *)o.hi + off * esz;  // TMA needs 16-byte aligned bases: off % 32 == 0
+    v.lo = (const char *)o.lo + off * esz;
+    return v;
+}
+
 // split a rows x cols fp32 matrix (leading dimension ldx) into a tensor-core operand with
 // leading dimension ld (>= cols, multiple of 32); rows_pad rows are allocated (extra rows zero)
 Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows, int64_t cols, int64_t ldx,
@@ -558,21 +571,23 @@ Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows,
 
 // X[row][col] = sum of the (row, col) run of sorted entries (deterministic, in entry order)
 __global__ void k_densify(const int32_t *__restrict__ row, const int32_t *__restrict__ col,
-                          const float *__restrict__ val, int64_t E, float *__restrict__ X, int64_t ldX) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+                          const float *__restrict__ val, int64_t k0, int64_t k1, int64_t row_lo,
+                          float *__restrict__ X, int64_t ldX) {
+    for (int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1; k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = row[k], cc = col[k];
-        if (k > 0 && row[k - 1] == r && col[k - 1] == cc) continue;  // not the head of its run
+        if (k > k0 && row[k - 1] == r && col[k - 1] == cc) continue;  // not the head of its run
         float s = val[k];
-        for (int64_t j = k + 1; j < E && row[j] == r && col[j] == cc; j++) s += val[j];
-        X[(int64_t)r * ldX + cc] = s;
+        for (int64_t j = k + 1; j < k1 && row[j] == r && col[j] == cc; j++) s += val[j];
+        X[(int64_t)(r - row_lo) * ldX + cc] = s;
     }
 }
 
-void densify(gvt_ctx *c, const EntryPlan &e, float *X, int64_t ldX, int64_t rows_pad) {
+void densify(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t row_lo, float *X, int64_t ldX,
+             int64_t rows_pad) {
     GVT_CUDA_TRY(cudaMemsetAsync(X, 0, sizeof(float) * rows_pad * ldX, c->stream));
-    if (e.nnz == 0) return;
-    GVT_LAUNCH(c, K_DENSIFY, k_densify, grid1d(e.nnz, 256, 16 * c->sm_count * 8), 256, 0, e.row, e.col, e.val, e.nnz,
-               X, ldX);
+    if (k1 <= k0) return;
+    GVT_LAUNCH(c, K_DENSIFY, k_densify, grid1d(k1 - k0, 256, 16 * c->sm_count * 8), 256, 0, e.row, e.col, e.val, k0,
+               k1, row_lo, X, ldX);
 }
 
 void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, float *Cf,

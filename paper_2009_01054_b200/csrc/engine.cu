@@ -1,5 +1,5 @@
 // engine.cu -- orchestration of the GVT matvec for every pairwise kernel, the CG fit and
-// prediction.
+// prediction, single GPU and data-parallel.
 //
 // Every Corollary kernel is run through ONE "Kronecker group"
 //     G = A X C^T sampled at (r_k, c_k),   X = pair matrix built from p,
@@ -18,8 +18,16 @@
 //   Cartesian           segment gathers over pairs sharing t / sharing d
 // with B[h,h'] = sum_{j: (d_j,t_j)=(h,h')} p_j, bF = B 1, bS = B^T 1.  Any other term
 // list runs term by term as groups (Ones / Identity factors materialised).
+//
+// Data-parallel layout: each rank owns a shard of the in-sample (and of
+// y, a, p) and of the out-sample.  The in-sample ids and p are gathered (grouped NCCL
+// broadcasts), the rows of X (= columns of S) are split into contiguous slabs balanced by
+// entry count, each rank runs stage 1 on its own slab, the S slabs are all-gathered, and
+// stage 2 runs on the rank's own outputs, slab by slab (K split).  With one GPU the same
+// slab code runs with GVT_OPT_SLABS emulated slabs (all computed locally).
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "ops.cuh"
@@ -30,6 +38,9 @@ void nccl_unique_id(void *out128);
 void comm_init(gvt_ctx *c, const void *id128, int rank, int world);
 void comm_destroy(gvt_ctx *c);
 void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats);
+std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v);
+void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<int64_t> &counts,
+                   const std::vector<int64_t> &offsets, bool is_float);
 
 // ----------------------------------------------------------------------------- decompose
 static gvt_term mk(double coef, int l, int r, int rl, int rr, int cl, int cr) {
@@ -117,8 +128,13 @@ struct Problem {
     int64_t m = 0, q = 0;  // q = m when homogeneous
     bool hom = false;
     Factor D, T;           // T aliases D when homogeneous
-    const int32_t *of = nullptr, *os = nullptr, *inf = nullptr, *ins = nullptr;
-    int64_t n_out = 0, n_in = 0;
+    const int32_t *of = nullptr, *os = nullptr;    // this rank's out pairs
+    int64_t n_out = 0;
+    const int32_t *inf = nullptr, *ins = nullptr;  // the FULL in-sample (gathered across ranks)
+    int64_t n_in = 0;
+    // data-parallel in-sample partition (world 1: counts = {n_in})
+    std::vector<int64_t> counts, offsets;
+    float *p_full = nullptr;
     int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
 };
 
@@ -152,13 +168,18 @@ static void validate_terms(const gvt_term *terms, int n_terms, bool hom, Form fo
 struct GroupPlan {
     Factor A, C;           // stage-2 factor (left), stage-1 factor (right)
     int64_t q_out = 0;     // rows of S (domain of the row-right selector)
-    int64_t m_in = 0;      // cols of S (domain of the col-left selector)
+    int64_t m_in = 0;      // cols of S = rows of X (domain of the col-left selector)
     EntryPlan ent;
     SamplePlan smp;
     float coef = 1.f;
     int engine = 1;        // 1 sparse, 2 dense
+    // slabs of X rows / S columns: bounds[g] .. bounds[g+1], entry positions kpos[g]
+    int nslab = 1;
+    std::vector<int64_t> bounds, kpos;
+    int64_t W = 0;         // slab width (padded to 32): S slab g is qpad x W at S + g * qpad * W
+    int64_t qpad = 0;
     float *S = nullptr;
-    int64_t ldS = 0;
+    std::string tag;
 };
 
 struct MatvecPlan {
@@ -202,11 +223,47 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
     return (tc && density >= c->dense_threshold) ? 2 : 1;
 }
 
+// X-row slabs balanced by entry count (row_ptr over nrow rows), bounds multiples of 32 (TMA /
+// float4 alignment of the column views of A): bounds[s] = the first row at or after the
+// s/G quantile of the entries, rounded up to 32, monotone, bounds[0] = 0, bounds[G] = nrow.
+// Host only; also exported as gvt_slab_bounds for the multi-process tests.
+void slab_bounds(const int64_t *rp, int64_t nrow, int G, int64_t *bounds) {
+    bounds[0] = 0;
+    bounds[G] = nrow;
+    const int64_t E = rp[nrow];
+    for (int s = 1; s < G; s++) {
+        const int64_t target = (int64_t)((long double)E * s / G);
+        int64_t h = std::lower_bound(rp, rp + nrow + 1, target) - rp;
+        h = round_up(h, 32);
+        h = std::min(std::max(h, bounds[s - 1]), nrow);
+        bounds[s] = h;
+    }
+}
+
+// slabs of a group, identical on every rank (computed from the same full plan)
+static void make_slabs(gvt_ctx *c, GroupPlan &g) {
+    int G = std::max(c->world, c->slabs > 0 ? c->slabs : 1);
+    const int64_t nrow = g.m_in;
+    std::vector<int64_t> rp((size_t)nrow + 1);
+    GVT_CUDA_TRY(cudaMemcpyAsync(rp.data(), g.ent.row_ptr, sizeof(int64_t) * (nrow + 1), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    g.nslab = G;
+    g.bounds.assign((size_t)G + 1, 0);
+    slab_bounds(rp.data(), nrow, G, g.bounds.data());
+    g.kpos.assign((size_t)G + 1, 0);
+    int64_t wmax = 0;
+    for (int s = 0; s <= G; s++) g.kpos[s] = rp[g.bounds[s]];
+    for (int s = 0; s < G; s++) wmax = std::max(wmax, g.bounds[s + 1] - g.bounds[s]);
+    g.W = round_up(wmax > 0 ? wmax : 1, 32);
+}
+
 static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
+    g.tag = tag;
     g.engine = choose_engine(c, g);
-    g.ldS = round_up(g.m_in > 0 ? g.m_in : 1, 32);
-    std::string t(tag);
-    g.S = wsT<float>(c, (t + ".S").c_str(), (size_t)round_up(g.q_out > 0 ? g.q_out : 1, 128) * g.ldS);
+    make_slabs(c, g);
+    g.qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
+    g.S = wsT<float>(c, (g.tag + ".S").c_str(), (size_t)g.nslab * g.qpad * g.W);
     if (g.engine == 2) bucket_samples(c, tag, g.smp, g.A.n, g.q_out);
 }
 
@@ -322,28 +379,68 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
 }
 
 // ----------------------------------------------------------------------------- run
-static void run_group(gvt_ctx *c, GroupPlan &g, const float *p, float coef, int accumulate, float *out) {
-    entry_values(c, g.ent, p);
+static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
+
+static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out,
+                      bool values_ready = false) {
     c->last_engine = g.engine;
-    if (g.engine == 2) {
-        // dense tensor-core engine: X densified and split, S = C X^T (fp32), S split,
-        // sampled A S^T written straight to the outputs
-        int64_t ldX = round_up(g.C.n > 0 ? g.C.n : 1, 32);  // X: m_in x q_in
-        int64_t rows_pad = round_up(g.m_in > 0 ? g.m_in : 1, 128);
-        float *X = wsT<float>(c, "dense.X", (size_t)rows_pad * ldX);
-        densify(c, g.ent, X, ldX, rows_pad);
-        Operand xo = make_operand(c, "dense.Xop", X, g.m_in, g.C.n, ldX, ldX, rows_pad);
-        int64_t qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
-        gemm_nt_store(c, g.C.op, xo, g.q_out, g.m_in, g.C.n, g.S, g.ldS, nullptr, nullptr);
-        Operand so = make_operand(c, "dense.Sop", g.S, g.q_out, g.m_in, g.ldS, g.ldS, qpad);
-        gemm_nt_sampled(c, g.A.op, so, g.A.n, g.q_out, g.m_in, g.smp, coef, accumulate, out);
-    } else {
-        stage1_sparse(c, g.ent, g.C, g.q_out, g.S, g.ldS);
-        stage2_gather(c, g.smp, g.A, g.S, g.ldS, g.m_in, coef, accumulate, out);
+    // ---- stage 1 on this rank's X-row slab(s)
+    for (int s = 0; s < g.nslab; s++) {
+        if (!my_slab(c, s)) continue;
+        const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        const int64_t k0 = g.kpos[s], k1 = g.kpos[s + 1];
+        float *Ss = g.S + (size_t)s * g.qpad * g.W;
+        if (!values_ready && k1 > k0) {
+            EntryPlan ev = g.ent;
+            ev.src = g.ent.src + k0;
+            ev.sign = g.ent.sign + k0;
+            ev.val = g.ent.val + k0;
+            ev.nnz = k1 - k0;
+            entry_values(c, ev, p_full);
+        }
+        if (g.engine == 2) {
+            const int64_t ldX = round_up(g.C.n > 0 ? g.C.n : 1, 32);  // X slab: w x q_in
+            const int64_t rows_pad = round_up(w > 0 ? w : 1, 128);
+            float *X = wsT<float>(c, "dense.X", (size_t)rows_pad * ldX);
+            densify(c, g.ent, k0, k1, lo, X, ldX, rows_pad);
+            Operand xo = make_operand(c, "dense.Xop", X, w, g.C.n, ldX, ldX, rows_pad);
+            gemm_nt_store(c, g.C.op, xo, g.q_out, w, g.C.n, Ss, g.W, nullptr, nullptr);
+        } else {
+            EntryPlan es = g.ent;
+            es.row_ptr = g.ent.row_ptr + lo;
+            es.nrow = w;
+            stage1_sparse(c, es, g.C, g.q_out, Ss, g.W);
+        }
+    }
+    // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab
+    allgather_slabs(c, g.S, (size_t)g.qpad * g.W);
+    bool first = true;
+    for (int s = 0; s < g.nslab; s++) {
+        const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        if (w == 0) continue;
+        const int acc = accumulate || !first;
+        first = false;
+        float *Ss = g.S + (size_t)s * g.qpad * g.W;
+        if (g.engine == 2) {
+            char nm[48];
+            snprintf(nm, sizeof(nm), "dense.Sop%d", s);
+            Operand so = make_operand(c, nm, Ss, g.q_out, w, g.W, g.W, g.qpad);
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, out);
+        } else {
+            Factor Av = g.A;
+            Av.p = g.A.p + lo;
+            stage2_gather(c, g.smp, Av, Ss, g.W, w, coef, acc, out);
+        }
     }
 }
 
-static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p, float *u) {
+static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u) {
+    // gather p over the ranks (world 1: p_full is p_local itself)
+    const float *p = p_local;
+    if (c->world > 1) {
+        gather_varlen(c, p_local, P.p_full, P.counts, P.offsets, true);
+        p = P.p_full;
+    }
     switch (mp.form) {
     case FORM_KRON:
     case FORM_SYM:
@@ -356,7 +453,8 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         break;
     case FORM_POLY2D: {
         GroupPlan &g = mp.groups[0];
-        run_group(c, g, p, 2.f, 0, u);
+        entry_values(c, g.ent, p);               // all entries: the segment sums need every row
+        run_group(c, g, p, 2.f, 0, u, true);
         segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
         entry_values(c, mp.byS, p);
         segment_sum(c, mp.byS, mp.b2);          // bS
@@ -458,7 +556,7 @@ static void out_finish(gvt_ctx *c, OutArr &o) {
     }
 }
 
-// does this plan need the 3xTF32 split of the factors (any dense group)?
+// does this plan need the tensor-core split of the factors (any dense group)?
 static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_in) {
     if (!tc_available(c) || c->engine == 1) return false;
     if (form == FORM_LINEAR || form == FORM_RANKING || form == FORM_CARTESIAN) return false;
@@ -469,9 +567,11 @@ static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_i
     return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold;
 }
 
+// out_is_in: the out sample is the caller's in sample (fit)
 static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, const float *T, int64_t q,
                           const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
-                          const int32_t *ins, int64_t n_in, const gvt_term *terms, int n_terms, Form &form) {
+                          const int32_t *ins, int64_t n_in, const gvt_term *terms, int n_terms, Form &form,
+                          bool out_is_in) {
     GVT_REQUIRE(m >= 0 && n_out >= 0 && n_in >= 0, GVT_E_DIM, "negative size");
     P.hom = (T == nullptr);
     P.m = m;
@@ -481,18 +581,34 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
     form = recognize(terms, n_terms);
     validate_terms(terms, n_terms, P.hom, form);
     P.n_out = n_out;
-    P.n_in = n_in;
     P.of = stage_ids(c, "in.of", of, n_out);
     P.os = stage_ids(c, "in.os", os, n_out);
-    P.inf = (inf == of && ins == os && n_in == n_out) ? P.of : stage_ids(c, "in.inf", inf, n_in);
-    P.ins = (inf == of && ins == os && n_in == n_out) ? P.os : stage_ids(c, "in.ins", ins, n_in);
+    const int32_t *lf = out_is_in ? P.of : stage_ids(c, "in.inf", inf, n_in);
+    const int32_t *ls = out_is_in ? P.os : stage_ids(c, "in.ins", ins, n_in);
     check_range(c, P.of, n_out, P.m, "out first ids");
     check_range(c, P.os, n_out, P.q, "out second ids");
-    if (P.inf != P.of) {
-        check_range(c, P.inf, n_in, P.m, "in first ids");
-        check_range(c, P.ins, n_in, P.q, "in second ids");
+    if (!out_is_in) {
+        check_range(c, lf, n_in, P.m, "in first ids");
+        check_range(c, ls, n_in, P.q, "in second ids");
     }
-    bool split = needs_split(c, form, P.m, P.q, n_in);
+    // in-sample over all ranks
+    P.counts = allgather_count(c, n_in);
+    P.offsets.assign(P.counts.size() + 1, 0);
+    for (size_t g = 0; g < P.counts.size(); g++) P.offsets[g + 1] = P.offsets[g] + P.counts[g];
+    P.n_in = P.offsets.back();
+    if (c->world > 1) {
+        int32_t *ff = wsT<int32_t>(c, "dist.f", (size_t)P.n_in);
+        int32_t *fs = wsT<int32_t>(c, "dist.s", (size_t)P.n_in);
+        gather_varlen(c, lf, ff, P.counts, P.offsets, false);
+        gather_varlen(c, ls, fs, P.counts, P.offsets, false);
+        P.inf = ff;
+        P.ins = fs;
+        P.p_full = wsT<float>(c, "dist.p", (size_t)P.n_in);
+    } else {
+        P.inf = lf;
+        P.ins = ls;
+    }
+    bool split = needs_split(c, form, P.m, P.q, P.n_in);
     P.D = prepare_factor(c, "fD", D, m, split);
     P.T = P.hom ? P.D : prepare_factor(c, "fT", T, q, split);
 }
@@ -503,13 +619,12 @@ void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, co
             const gvt_term *terms, int n_terms, float *u) {
     Problem P;
     Form form;
-    setup_problem(c, P, D, m, T, q, of, os, n_out, inf, ins, n_in, terms, n_terms, form);
+    setup_problem(c, P, D, m, T, q, of, os, n_out, inf, ins, n_in, terms, n_terms, form, false);
     OutArr uo = out_arr(c, "out.u", u, n_out);
-    if (n_out == 0) return;
     const float *ad = n_in ? (const float *)stage_in(c, "in.a", a, sizeof(float) * n_in) : nullptr;
     GVT_REQUIRE(n_in == 0 || ad, GVT_E_DIM, "a is NULL with n_in > 0");
-    if (n_in == 0) {
-        GVT_CUDA_TRY(cudaMemsetAsync(uo.dev, 0, sizeof(float) * n_out, c->stream));
+    if (P.n_in == 0) {  // no in pairs anywhere: u = 0 (collective-free on every rank)
+        if (n_out) GVT_CUDA_TRY(cudaMemsetAsync(uo.dev, 0, sizeof(float) * n_out, c->stream));
     } else {
         MatvecPlan mp;
         plan_matvec(c, P, terms, n_terms, form, mp);
@@ -532,15 +647,18 @@ gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
     GVT_REQUIRE(rel_tol >= 0.0, GVT_E_PARAM, "rel_tol < 0");
     Problem P;
     Form form;
-    setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form);
+    setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form, true);
     OutArr ao = out_arr(c, "out.a", a_out, n);
     const float *yd = n ? (const float *)stage_in(c, "in.y", y, sizeof(float) * n) : nullptr;
     GVT_REQUIRE(n == 0 || yd, GVT_E_DIM, "y is NULL with n > 0");
     const int ST_N = 9;
     double *state = wsT<double>(c, "cg.state", (size_t)ST_N + max_iter + 1);
-    if (n == 0) {
+    if (P.n_in == 0) {
         if (iters_out) *iters_out = 0;
-        if (relres_hist) relres_hist[0] = 0.0;
+        if (relres_hist) {
+            relres_hist[0] = 0.0;
+            for (int k = 1; k <= max_iter; k++) relres_hist[k] = 0.0 / 0.0;
+        }
         return GVT_OK;
     }
     float *x = ao.dev;
@@ -561,12 +679,9 @@ gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
     }
     // scalars back (one sync per fit)
     GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
-    if (relres_hist) {
-        double *hh = wsT<double>(c, "cg.hist_dummy", 1);
-        (void)hh;
+    if (relres_hist)
         GVT_CUDA_TRY(cudaMemcpyAsync(relres_hist, state + ST_N, sizeof(double) * (max_iter + 1),
                                      cudaMemcpyDeviceToHost, c->stream));
-    }
     out_finish(c, ao);
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     int iters = (int)hstate[7];

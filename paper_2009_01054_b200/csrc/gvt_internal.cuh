@@ -88,6 +88,7 @@ struct gvt_ctx {
     int profile = 0;
     int gram_engine = 0;
     int tc_precision = 0;  // 0 = 3xFP16 with row scaling, 1 = 3xTF32
+    int slabs = 1;         // emulated X-row slabs at world 1 (tests the data-parallel slab path)
     int last_engine = 0;
 
     // workspaces by name (grow-only)

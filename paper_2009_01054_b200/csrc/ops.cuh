@@ -86,11 +86,15 @@ void scale_copy(gvt_ctx *c, const float *x, float alpha, int64_t n, float *y);
 // ---- dense tensor-core engine (dense_tc.cu)
 bool tc_available(gvt_ctx *c);
 int tc_precision_mode(gvt_ctx *c);
+// view of columns [off, ...) of an operand (off a multiple of 32)
+Operand operand_col_offset(const Operand &o, int64_t off);
 // split a rows x cols fp32 matrix (leading dim ldx) into an operand with leading dim ld
 Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows, int64_t cols, int64_t ldx,
                      int64_t ld, int64_t rows_pad);
-// X (rows_pad x ldX fp32, zeroed) <- pair matrix from the sorted entries (duplicates summed)
-void densify(gvt_ctx *c, const EntryPlan &e, float *X, int64_t ldX, int64_t rows_pad);
+// X (rows_pad x ldX fp32, zeroed) <- rows [row_lo, row_lo + rows) of the pair matrix from the
+// sorted entries k in [k0, k1) (duplicates summed in entry order)
+void densify(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t row_lo, float *X, int64_t ldX,
+             int64_t rows_pad);
 // C (M x N, ldc) = A (M x K) * B^T (B: N x K), fp32-accurate; optional tf32 split of C
 void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, float *Cf,
                    int64_t ldc, float *Chi, float *Clo);

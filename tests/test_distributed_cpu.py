@@ -1,0 +1,145 @@
+"""Multi-process (world_size 2, gloo, CPU) checks of the data-parallel decomposition
+ -- no GPU needed.
+
+Each rank holds a drug-range shard of the training pairs (gvt_partition), gathers the
+in-sample and p over the ranks, runs GVT stage 1 on its own X-row slab (gvt_slab_bounds,
+the same host function the CUDA engine uses), all-gathers the equal-width S slabs, runs
+stage 2 on its own outputs and all-reduces the CG dot products.  The stages are fp64 numpy
+models of the library's kernels; what is under test is the partition/slab/gather logic:
+the sharded CG must reproduce the single-process oracle CG on the same data.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as tmp  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_2009_01054_b200 as G  # noqa: E402
+import synth  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _all_gather_var(x, world):
+    """variable-length all-gather in rank order (pads to the max length)"""
+    n = torch.tensor([len(x)], dtype=torch.int64)
+    ns = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(ns, n)
+    ns = [int(v.item()) for v in ns]
+    nmax = max(ns)
+    buf = torch.zeros(nmax, dtype=torch.float64)
+    buf[: len(x)] = torch.from_numpy(np.asarray(x, dtype=np.float64))
+    out = [torch.zeros(nmax, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, buf)
+    return np.concatenate([o.numpy()[:k] for o, k in zip(out, ns)]), ns
+
+
+def _worker(rank, world, port, iters, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = synth.config1()
+        D = O.gram(w.base, w.Xd, gamma=w.gamma)
+        T = O.gram(w.base, w.Xt, gamma=w.gamma)
+        m, q = w.m, w.q
+        f, s, y = w.train_first, w.train_second, w.y.astype(np.float64)
+        # ---- drug-range shards (library host logic)
+        bounds = G.gvt_partition(np.bincount(f, minlength=m), world)
+        mine = (f >= bounds[rank]) & (f < bounds[rank + 1])
+        lf, ls, ly = f[mine], s[mine], y[mine]
+        # ---- gathered in-sample (rank order) and the X-row slabs of the Kronecker group
+        ff, counts = _all_gather_var(lf, world)
+        fs, _ = _all_gather_var(ls, world)
+        ff, fs = ff.astype(np.int64), fs.astype(np.int64)
+        row_ptr = np.concatenate([[0], np.cumsum(np.bincount(ff, minlength=m))])
+        sb = G.gvt_slab_bounds(row_ptr, world)
+        W = int(-(-max(np.diff(sb).max(), 1) // 32) * 32)
+        lo, hi = int(sb[rank]), int(sb[rank + 1])
+
+        def matvec(p_local):
+            p_full, _ = _all_gather_var(p_local, world)
+            # stage 1 on this rank's slab: S[:, h] for h in [lo, hi)
+            B = np.zeros((hi - lo, q))
+            sel = (ff >= lo) & (ff < hi)
+            np.add.at(B, (ff[sel] - lo, fs[sel]), p_full[sel])
+            slab = np.zeros((q, W))
+            slab[:, : hi - lo] = T @ B.T
+            # all-gather the equal-width slabs
+            outs = [torch.zeros(q * W, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(outs, torch.from_numpy(slab.reshape(-1)))
+            S = np.zeros((q, m))
+            for g in range(world):
+                a, b = int(sb[g]), int(sb[g + 1])
+                S[:, a:b] = outs[g].numpy().reshape(q, W)[:, : b - a]
+            # stage 2 on this rank's outputs
+            return np.einsum("ih,ih->i", D[lf], S[ls])
+
+        def dot(a, b):
+            t = torch.tensor([float(a @ b)], dtype=torch.float64)
+            dist.all_reduce(t)
+            return float(t.item())
+
+        x = np.zeros_like(ly)
+        r = ly.copy()
+        p = r.copy()
+        rho = dot(r, r)
+        for _ in range(iters):
+            Ap = matvec(p) + w.lam * p
+            alpha = rho / dot(p, Ap)
+            x += alpha * p
+            r -= alpha * Ap
+            rho1 = dot(r, r)
+            p = r + (rho1 / rho) * p
+            rho = rho1
+        xs, _ = _all_gather_var(x, world)
+        if rank == 0:
+            order = np.concatenate([np.nonzero((f >= bounds[g]) & (f < bounds[g + 1]))[0] for g in range(world)])
+            full = np.empty_like(xs)
+            full[order] = xs
+            ret.put((full, [int(v) for v in sb], [int(v) for v in bounds], counts))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_cg_equals_single_process_oracle(world):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    iters = 12
+    tmp.start_processes(_worker, args=(world, _free_port(), iters, q), nprocs=world, join=True, start_method="spawn")
+    a_sharded, sb, bounds, counts = q.get(timeout=60)
+    w = synth.config1()
+    D = O.gram(w.base, w.Xd, gamma=w.gamma)
+    T = O.gram(w.base, w.Xt, gamma=w.gamma)
+    a_ref, _, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, iters)
+    # fp64 on both sides; only the summation order differs (a wrong partition is O(1) off)
+    assert np.linalg.norm(a_sharded - a_ref) / np.linalg.norm(a_ref) < 1e-8
+    assert sb[0] == 0 and sb[-1] == w.m and all(b % 32 == 0 for b in sb[1:-1])
+    assert sum(counts) == w.n and bounds[0] == 0 and bounds[-1] == w.m
+
+
+def test_slab_bounds_definition():
+    rng = np.random.default_rng(0)
+    for nrow, G_ in [(1, 1), (40, 2), (1000, 3), (20000, 8), (5, 8)]:
+        rp = np.concatenate([[0], np.cumsum(rng.integers(0, 50, nrow))])
+        b = G.gvt_slab_bounds(rp, G_)
+        E = rp[-1]
+        ref = [0]
+        for s in range(1, G_):
+            h = int(np.searchsorted(rp, int(E * s / G_), side="left"))
+            h = min(max(-(-h // 32) * 32, ref[-1]), nrow)
+            ref.append(h)
+        ref.append(nrow)
+        assert list(b) == ref

@@ -369,3 +369,40 @@ def test_launch_accounting(ctx):
     assert st["launches"] > 0
     assert "cg_vector" in st["kinds"] and st["kinds"]["cg_vector"]["count"] >= 5 * 3
     assert all(v["ms"] >= 0 for v in st["kinds"].values())
+
+
+# ----------------------------------------------------------------------------- data-parallel slab path
+@pytest.mark.parametrize("slabs", [2, 3, 8])
+@pytest.mark.parametrize("engine", [G.ENGINE_SPARSE, G.ENGINE_DENSE], ids=["sparse", "dense"])
+def test_slab_path_matches_oracle(ctx, slabs, engine):
+    """GVT_OPT_SLABS runs stage 1 per X-row slab and stage 2 slab by slab (K split), the code
+    path every rank runs in the data-parallel layout; results must stay at oracle parity."""
+    ctx.set_option(G.OPT_ENGINE, engine)
+    ctx.set_option(G.OPT_SLABS, slabs)
+    try:
+        rng = np.random.default_rng(77)
+        for kernel in K_ALL:
+            hom = kernel in HOM
+            m, q = 300, (300 if hom else 200)
+            Xd = rng.standard_normal((m, 16)).astype(np.float32)
+            Xt = None if hom else rng.standard_normal((q, 16)).astype(np.float32)
+            D32 = f32(O.gram(G.BASE_GAUSSIAN, Xd, gamma=1 / 16))
+            T32 = None if hom else f32(O.gram(G.BASE_GAUSSIAN, Xt, gamma=1 / 16))
+            inf, ins = rng.integers(0, m, 9000).astype(np.int32), rng.integers(0, q, 9000).astype(np.int32)
+            of, os_ = rng.integers(0, m, 3000).astype(np.int32), rng.integers(0, q, 3000).astype(np.int32)
+            a = synth.random_vector(kernel, 9000)
+            u = ctx.matvec(dev(D32), None if hom else dev(T32), dev(of), dev(os_), dev(inf), dev(ins), dev(a),
+                           G.gvt_kernel_terms(kernel)).cpu().numpy()
+            ref = O.gvt_matvec(O.kernel_terms(kernel), D32, T32, of, os_, inf, ins, a)
+            assert rel(u, ref) <= MATVEC_TOL, (kernel, rel(u, ref))
+        # C1 fit through the slab path keeps the CG-weight gate
+        w = synth.config1()
+        D, T = grams_oracle(w)
+        kron = G.gvt_kernel_terms(G.KRONECKER)
+        a, iters, _, _ = ctx.fit(dev(f32(D)), dev(f32(T)), dev(w.train_first), dev(w.train_second), dev(w.y), kron,
+                                 w.lam, w.iters)
+        ao, _, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, w.iters)
+        assert rel(a.cpu().numpy(), ao) <= 1e-4
+    finally:
+        ctx.set_option(G.OPT_SLABS, 1)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)

@@ -20,7 +20,7 @@ void set_error(const char *fmt, ...) {
 const char *last_error() { return g_last_error.c_str(); }
 
 static const char *kKindNames[K_NUM_KINDS] = {
-    "gram_simt",   "gram_tc",       "split_tf32",  "pad_copy",     "plan_keys",      "plan_sort(cub)",
+    "gram_simt",   "gram_tc",       "split_operand",  "pad_copy",     "plan_keys",      "plan_sort(cub)",
     "plan_rowptr", "plan_gather",   "stage1_sparse", "stage2_gather", "densify",     "stage1_tc",
     "stage2_tc",   "segment_sum",   "gemv",        "combine",      "cartesian",      "cg_vector",
     "cg_scalar",   "fill",

@@ -119,7 +119,7 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
 void allreduce_partials(gvt_ctx *c, double *partials, int count);
 
 // partial-sum layout (cg.cu)
-constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
 constexpr int RED_THREADS = 256;
 
 }  // namespace gvt

@@ -406,3 +406,20 @@ def test_slab_path_matches_oracle(ctx, slabs, engine):
     finally:
         ctx.set_option(G.OPT_SLABS, 1)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 1183, 1185, 4737, 100003])
+def test_cg_ragged_lengths(ctx, n):
+    """CG vector kernels over lengths that are not multiples of 4 or of the block count:
+    the GPU CG equals the oracle CG on the same fp32 inputs."""
+    rng = np.random.default_rng(n)
+    m, q = 37, 29
+    D32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((m, 4)), gamma=0.25))
+    T32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((q, 4)), gamma=0.25))
+    f = rng.integers(0, m, n).astype(np.int32)
+    s = rng.integers(0, q, n).astype(np.int32)
+    y = rng.standard_normal(n).astype(np.float32)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    a, it, _, _ = ctx.fit(dev(D32), dev(T32), dev(f), dev(s), dev(y), kron, 1.0, 8)
+    ao, _, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
+    assert rel(a.cpu().numpy(), ao) <= 1e-4

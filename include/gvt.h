@@ -97,8 +97,10 @@ typedef enum {
     GVT_OPT_GRAM_ENGINE = 3,     /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
     GVT_OPT_TC_PRECISION = 4,    /* tensor-core split: 0 = 3xFP16 with per-row power-of-two scaling
                                     (default), 1 = 3xTF32; both fp32-accurate (reading S16)          */
-    GVT_OPT_SLABS = 5            /* single GPU: split stage 1 / stage 2 into this many X-row slabs,
+    GVT_OPT_SLABS = 5,           /* single GPU: split stage 1 / stage 2 into this many X-row slabs,
                                     exactly as the data-parallel path does across ranks (default 1) */
+    GVT_OPT_GEMM_CTA = 6         /* tensor-core GEMM: 2 = CTA pair with tcgen05 cta_group::2 (256-row
+                                    tiles, default), 1 = single-CTA 128-row tiles                  */
 } gvt_option;
 
 /* Per-context counters (gvt_get_stats). */

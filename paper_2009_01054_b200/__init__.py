@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgvt.so")
+LIB_PATH = os.environ.get("GVT_LIBRARY") or os.path.join(_HERE, "libgvt.so")  # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libgvt.so not built at {LIB_PATH}: run `python -m paper_2009_01054_b200.build` "
@@ -37,6 +37,7 @@ OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE, OPT_TC_PRECISION 
 PREC_FP16X3, PREC_TF32X3 = 0, 1
 ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE = 0, 1, 2
 OPT_SLABS = 5
+OPT_GEMM_CTA = 6
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32
 

@@ -122,6 +122,10 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "tc precision must be 0 (fp16 x3) or 1 (tf32 x3)");
         c->tc_precision = (int)v;
         break;
+    case GVT_OPT_GEMM_CTA:
+        GVT_REQUIRE(v == 1 || v == 2, GVT_E_PARAM, "gemm cta must be 1 or 2");
+        c->gemm_cta = (int)v;
+        break;
     case GVT_OPT_SLABS:
         GVT_REQUIRE(v >= 1 && v <= 64, GVT_E_PARAM, "slabs must be in [1, 64]");
         c->slabs = (int)v;

@@ -73,14 +73,17 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// K-major, SWIZZLE_128B canonical layout: 8-row x 128-byte atoms, SBO = 1024 B, LBO = 16 B
+// bytes of K per smem row (one swizzle atom row): 64 -> SWIZZLE_64B atoms, 4-stage ring of 48 KB
+constexpr int KB_BYTES = 128;
+
+// K-major canonical swizzled layout: 8-row x KB_BYTES atoms, SBO = 8 rows * KB_BYTES, LBO = 16 B
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;   // SBO
-    d |= (uint64_t)1 << 46;             // version (sm_100)
-    d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+    d |= (uint64_t)1 << 16;                                        // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * KB_BYTES) >> 4) << 32;                    // SBO
+    d |= (uint64_t)1 << 46;                                        // version (sm_100)
+    d |= (uint64_t)(KB_BYTES == 128 ? 2 : (KB_BYTES == 64 ? 4 : 6)) << 61;  // SWIZZLE_128B / 64B / 32B
     return d;
 }
 
@@ -165,7 +168,7 @@ struct EpiParams {
     int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
 };
 
-constexpr int BM = 128, BN = 256, KB_BYTES = 128, STAGES = 2;
+constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
 constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
               const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N, int K,
               EpiParams ep) {
-    constexpr int BKE = PREC == PREC_TF32 ? 32 : 64;  // elements per 128-byte K-block
+    constexpr int BKE = KB_BYTES / (PREC == PREC_TF32 ? 4 : 2);  // elements per K-block
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t ah = base, al = base + A_BYTES, bh = base + 2 * A_BYTES,
                                    bl = base + 2 * A_BYTES + B_BYTES;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
+                    for (int k = 0; k < KB_BYTES / 32; k++) {
                         const uint32_t off = k * 32;  // one MMA K-step = 32 bytes inside the swizzle atom
                         const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
                         const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
@@ -415,6 +418,306 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ----------------------------------------------------------------------------- 2-CTA variant
+// CTA pair (cluster of 2) computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (M = 256):
+// each CTA stages its own 128 rows of A and its own 128 rows of B (TMA .cta_group::2, bytes
+// completing on the leader's barrier), the leader issues the MMAs that read both CTAs'
+// shared memory, each CTA's TMEM holds its 128 accumulator rows.  Per MAC this moves 1/3
+// fewer operand bytes than the 1-CTA kernel and leaves room for 3 stages of 64 KB.
+constexpr int STAGES2 = 3;
+constexpr int HALF_BYTES = 128 * KB_BYTES;               // 16 KB: 128 rows of one operand piece
+constexpr int STAGE2_BYTES = 4 * HALF_BYTES;             // A hi/lo + B-half hi/lo = 64 KB per CTA
+constexpr int BAR2_OFF = STAGES2 * STAGE2_BYTES;
+constexpr int SMEM2_TOTAL = BAR2_OFF + 256 + 1024;
+static_assert(N_EPI_WARPS * 32 * 33 * 4 <= STAGES2 * STAGE2_BYTES, "epilogue staging aliases the stage ring");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    // both CTAs: bytes complete on the leader's barrier (peer bit of the cluster address cleared)
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int PREC>
+__device__ __forceinline__ void mma_issue2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    if (PREC == PREC_TF32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    }
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+template <int PREC, int N>
+__host__ __device__ constexpr uint32_t idesc_mma2() {
+    return (1u << 4) | ((PREC == PREC_TF32 ? 2u : 0u) << 7) | ((PREC == PREC_TF32 ? 2u : 0u) << 10) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int PREC, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_gemm2_x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+               const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N, int K,
+               EpiParams ep) {
+    constexpr int BKE = KB_BYTES / (PREC == PREC_TF32 ? 4 : 2);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR2_OFF);
+    uint64_t *empty = full + STAGES2;
+    uint64_t *tfull = empty + STAGES2;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_rank();
+    // rasterize CTA pairs over (256-row pair tiles, 256-column tiles), grouped
+    const int num_mp = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN;
+    const int pid = blockIdx.x >> 1, in_group = GROUP_M * num_n;
+    const int first_m = (pid / in_group) * GROUP_M;
+    const int group_m = min(num_mp - first_m, GROUP_M);
+    const int mp_tile = first_m + (pid % in_group) % group_m;
+    const int n_tile = (pid % in_group) / group_m;
+    const int m_tile = 2 * mp_tile + (int)crank;  // this CTA's 128-row tile
+    const int m0 = m_tile * BM, n0 = n_tile * BN;
+    const int nk = (K + BKE - 1) / BKE;
+    const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
+    const int nch = (nk + kcb - 1) / kcb;
+
+    if (EPI == EPI_SAMPLED) {  // skip a pair tile that owns no sample (both CTAs decide alike)
+        const int64_t t0 = (int64_t)(2 * mp_tile) * ep.n_ct + n_tile, t1 = t0 + ep.n_ct;
+        const int64_t e0 = ep.chunk_ptr[t0 * (BN / 32)] == ep.chunk_ptr[(t0 + 1) * (BN / 32)];
+        const bool has1 = 2 * mp_tile + 1 < (M + BM - 1) / BM;
+        const int64_t e1 = !has1 || ep.chunk_ptr[t1 * (BN / 32)] == ep.chunk_ptr[(t1 + 1) * (BN / 32)];
+        if (e0 && e1) return;
+    }
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmAh);
+        prefetch_tmap(&tmAl);
+        prefetch_tmap(&tmBh);
+        prefetch_tmap(&tmBl);
+        for (int s = 0; s < STAGES2; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * N_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {  // TMEM: both CTAs, same warp, same slot offset
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            for (int kb = 0; kb < nk; kb++) {
+                const int s = kb % STAGES2;
+                const uint32_t ph = (kb / STAGES2) & 1;
+                mbar_wait(&empty[s], ph ^ 1);  // own slot released by the leader's MMA commit
+                uint8_t *st = smem + s * STAGE2_BYTES;
+                if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
+                const int kc = kb * BKE;
+                tma_load_2d_pair(st, &tmAh, &full[s], kc, m0);
+                tma_load_2d_pair(st + HALF_BYTES, &tmAl, &full[s], kc, m0);
+                tma_load_2d_pair(st + 2 * HALF_BYTES, &tmBh, &full[s], kc, n0 + (int)crank * 128);
+                tma_load_2d_pair(st + 3 * HALF_BYTES, &tmBl, &full[s], kc, n0 + (int)crank * 128);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader only)
+            constexpr uint32_t idesc = idesc_mma2<PREC, BN>();
+            int kb = 0;
+            for (int ch = 0; ch < nch; ch++) {
+                const int b = ch & 1;
+                mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + b * BN;
+                const int kend = min(nk, kb + kcb);
+                for (int kk = 0; kb < kend; kb++, kk++) {
+                    const int s = kb % STAGES2;
+                    const uint32_t ph = (kb / STAGES2) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
+                    const uint32_t ah = base, al = base + HALF_BYTES, bh = base + 2 * HALF_BYTES,
+                                   bl = base + 3 * HALF_BYTES;
+#pragma unroll
+                    for (int k = 0; k < KB_BYTES / 32; k++) {
+                        const uint32_t off = k * 32;
+                        const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
+                        const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
+                        mma_issue2<PREC>(acc, dah, dbh, idesc, (kk | k) != 0);
+                        mma_issue2<PREC>(acc, dah, dbl, idesc, 1);
+                        mma_issue2<PREC>(acc, dal, dbh, idesc, 1);
+                    }
+                    mma_commit_pair(&empty[s]);  // frees the slot in both CTAs
+                }
+                mma_commit_pair(&tfull[b]);      // accumulator ready in both CTAs
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..9 (both CTAs, own 128 rows)
+        const int ew = warp - 2;
+        const int quarter = warp & 3;
+        const int half = ew >> 2;
+        const int row = quarter * 32 + lane;
+        const int gr = m0 + row;
+        float run[128];
+#pragma unroll
+        for (int i = 0; i < 128; i++) run[i] = 0.f;
+        for (int ch = 0; ch < nch; ch++) {
+            const int b = ch & 1;
+            mbar_wait(&tfull[b], (ch >> 1) & 1);
+            tc_fence_after();
+            const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; c4++) {
+                uint32_t r[32];
+                tmem_ld32_raw(ta + c4 * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&tempty[b]);
+        }
+        const int gc_base = n0 + half * 128;
+        if (ep.sa || ep.sb) {
+            const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+#pragma unroll
+            for (int i = 0; i < 128; i++) {
+                const int gc = gc_base + i;
+                const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                run[i] *= ra * rb;
+            }
+        }
+        if (EPI == EPI_STORE) {
+            if (gr < M) {
+                float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
+                if (gc_base + 128 <= N) {
+#pragma unroll
+                    for (int i = 0; i < 128; i += 4)
+                        *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 128; i++)
+                        if (gc_base + i < N) cf[i] = run[i];
+                }
+                if (ep.c_hi) {
+#pragma unroll
+                    for (int i = 0; i < 128; i++) {
+                        if (gc_base + i < N) {
+                            float h = tf32_round(run[i]);
+                            ep.c_hi[(int64_t)gr * ep.ldc + gc_base + i] = h;
+                            ep.c_lo[(int64_t)gr * ep.ldc + gc_base + i] = tf32_round(run[i] - h);
+                        }
+                    }
+                }
+            }
+        } else if (EPI == EPI_GRAM) {
+            if (gr < M) {
+                float *krow = ep.c_f + (int64_t)gr * ep.ldc;
+                const float ni = ep.kind == GVT_BASE_GAUSSIAN ? ep.norms[gr] : 0.f;
+#pragma unroll
+                for (int i = 0; i < 128; i++) {
+                    const int gc = gc_base + i;
+                    if (gc < N) {
+                        float x = run[i];
+                        if (ep.kind == GVT_BASE_GAUSSIAN) {
+                            float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
+                            if (gc == gr) d2 = 0.f;
+                            x = expf(-ep.gamma * d2);
+                        } else if (ep.kind == GVT_BASE_POLY) {
+                            float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
+                            for (int e = 0; e < ep.degree; e++) rr *= bb;
+                            x = rr;
+                        }
+                        krow[gc] = x;
+                    }
+                }
+            }
+        } else {
+            float *stage = reinterpret_cast<float *>(smem);
+            const int t = threadIdx.x - 64;
+            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+            const bool tile_ok = m_tile < (M + BM - 1) / BM;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; c4++) {
+                float *mine = stage + (half * 4 + quarter) * 32 * 33 + lane * 33;
+#pragma unroll
+                for (int i = 0; i < 32; i++) mine[i] = run[c4 * 32 + i];
+                named_bar(1, 32 * N_EPI_WARPS);
+                if (tile_ok) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; hh++) {
+                        const int chunk = hh * 4 + c4;
+                        const int64_t cidx = tile * (BN / 32) + chunk;
+                        const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
+                        const int gc0 = n0 + chunk * 32;
+                        for (int64_t k = kb0 + t; k < ke; k += 32 * N_EPI_WARPS) {
+                            const int rl = ep.s_r[k] - m0;
+                            const int cl = ep.s_c[k] - gc0;
+                            const float val = stage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
+                            const int64_t d = ep.s_dst[k];
+                            ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
+                        }
+                    }
+                }
+                named_bar(1, 32 * N_EPI_WARPS);
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs done with TMEM / shared memory before the pair deallocates
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    }
+}
+
 // ----------------------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -438,7 +741,9 @@ static CUtensorMap make_map(const void *p, int esz, int64_t rows, int64_t cols, 
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_encode(&m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                           const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          KB_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                          : (KB_BYTES == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     GVT_REQUIRE(r == CUDA_SUCCESS, GVT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
@@ -450,11 +755,23 @@ template <int PREC, int EPI>
 static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Operand &B, int64_t M, int64_t N,
                           int64_t K, EpiParams ep) {
     constexpr int esz = PREC == PREC_TF32 ? 4 : 2;
+    const bool pair = c->gemm_cta == 2;
     CUtensorMap ah = make_map(A.hi, esz, M, K, A.ld, BM), al = make_map(A.lo, esz, M, K, A.ld, BM);
-    CUtensorMap bh = make_map(B.hi, esz, N, K, B.ld, BN), bl = make_map(B.lo, esz, N, K, B.ld, BN);
+    CUtensorMap bh = make_map(B.hi, esz, N, K, B.ld, pair ? 128 : BN), bl = make_map(B.lo, esz, N, K, B.ld, pair ? 128 : BN);
     ep.sa = A.scale;
     ep.sb = B.scale;
-    static bool attr = false;
+    static bool attr = false, attr2 = false;
+    if (pair) {
+        if (!attr2) {
+            GVT_CUDA_TRY(
+                cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+            attr2 = true;
+        }
+        dim3 grid((unsigned)(2 * ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM))));
+        GVT_LAUNCH(c, kind_id, (k_gemm2_x3<PREC, EPI>), grid, NTHREADS, SMEM2_TOTAL, ah, al, bh, bl, (int)M, (int)N,
+                   (int)K, ep);
+        return;
+    }
     if (!attr) {
         GVT_CUDA_TRY(
             cudaFuncSetAttribute(k_gemm_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));

@@ -89,6 +89,7 @@ struct gvt_ctx {
     int gram_engine = 0;
     int tc_precision = 0;  // 0 = 3xFP16 with row scaling, 1 = 3xTF32
     int slabs = 1;         // emulated X-row slabs at world 1 (tests the data-parallel slab path)
+    int gemm_cta = 2;      // tensor-core GEMM: 2 = CTA-pair tcgen05 (cta_group::2), 1 = single CTA
     int last_engine = 0;
 
     // workspaces by name (grow-only)

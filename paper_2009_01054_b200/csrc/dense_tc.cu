@@ -144,7 +144,7 @@ __device__ __forceinline__ float tf32_round(float x) {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // ----------------------------------------------------------------------------- kernel
-enum { EPI_STORE = 0, EPI_SAMPLED = 1, EPI_GRAM = 2 };
+enum { EPI_STORE = 0, EPI_SAMPLED = 1, EPI_GRAM = 2, EPI_STORE16 = 3 };
 
 struct EpiParams {
     // store
@@ -166,6 +166,15 @@ struct EpiParams {
     float gamma, coef0;
     int degree;
     int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
+    // B operand with a per-(row, 256-wide K chunk) scale, applied while draining chunk ch:
+    // sbk[ch * sbk_ld + n] (fp16 S produced by EPI_STORE16)
+    const float *sbk;
+    int64_t sbk_ld;
+    // EPI_STORE16: C as fp16 hi/lo (ldc) with one scale per (row, 256-column tile):
+    // c_sk[n_tile * c_sk_ld + row] = 1/scale
+    __half *c_h16, *c_l16;
+    float *c_sk;
+    int64_t c_sk_ld;
 };
 
 constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
@@ -612,20 +621,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             mbar_wait(&tfull[b], (ch >> 1) & 1);
             tc_fence_after();
             const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
+            // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
+            const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + n0 + half * 128 : nullptr;
 #pragma unroll
             for (int c4 = 0; c4 < 4; c4++) {
                 uint32_t r[32];
                 tmem_ld32_raw(ta + c4 * 32, r);
                 tmem_wait_ld();
+                if (sk) {
 #pragma unroll
-                for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
+                    for (int i = 0; i < 32; i++) run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c4 * 32 + i), run[c4 * 32 + i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
+                }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_leader(&tempty[b]);
         }
         const int gc_base = n0 + half * 128;
-        if (ep.sa || ep.sb) {
+        if (EPI == EPI_STORE16) {
+            // fp16 hi/lo of the unscaled result with one power-of-two scale per (row, 256-col tile):
+            // the two warps holding this row's column halves exchange their maxima
+            const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+            float mx = 0.f;
+#pragma unroll
+            for (int i = 0; i < 128; i++) {
+                const int gc = gc_base + i;
+                const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                run[i] *= ra * rb;
+                if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
+            }
+            float *xch = reinterpret_cast<float *>(smem);  // stage ring is free: [quarter][lane][half]
+            xch[(quarter * 32 + lane) * 2 + half] = mx;
+            named_bar(1, 32 * N_EPI_WARPS);
+            mx = fmaxf(xch[(quarter * 32 + lane) * 2], xch[(quarter * 32 + lane) * 2 + 1]);
+            int e = 0;
+            if (mx > 0.f && isfinite(mx)) {
+                int ex;
+                frexpf(mx, &ex);
+                e = 15 - ex;
+            }
+            const float s = ldexpf(1.f, e);
+            if (gr < M) {
+                if (half == 0) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+                __half *hp = ep.c_h16 + (int64_t)gr * ep.ldc + gc_base;
+                __half *lp = ep.c_l16 + (int64_t)gr * ep.ldc + gc_base;
+#pragma unroll
+                for (int i = 0; i < 128; i += 2) {
+                    if (gc_base + i + 1 < N) {
+                        const float v0 = run[i] * s, v1 = run[i + 1] * s;
+                        const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+                        *reinterpret_cast<__half2 *>(hp + i) = __halves2half2(h0, h1);
+                        *reinterpret_cast<__half2 *>(lp + i) =
+                            __halves2half2(__float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
+                    } else if (gc_base + i < N) {
+                        const float v0 = run[i] * s;
+                        const __half h0 = __float2half_rn(v0);
+                        hp[i] = h0;
+                        lp[i] = __float2half_rn(v0 - __half2float(h0));
+                    }
+                }
+            }
+        }
+        if (EPI != EPI_STORE16 && (ep.sa || ep.sb)) {
             const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
 #pragma unroll
             for (int i = 0; i < 128; i++) {
@@ -679,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     }
                 }
             }
-        } else {
+        } else if (EPI == EPI_SAMPLED) {
             float *stage = reinterpret_cast<float *>(smem);
             const int t = threadIdx.x - 64;
             const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
@@ -760,6 +820,10 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
     CUtensorMap bh = make_map(B.hi, esz, N, K, B.ld, pair ? 128 : BN), bl = make_map(B.lo, esz, N, K, B.ld, pair ? 128 : BN);
     ep.sa = A.scale;
     ep.sb = B.scale;
+    ep.sbk = B.scale_k;
+    ep.sbk_ld = B.scale_k_ld;
+    GVT_REQUIRE(!B.scale_k || (pair && PREC == PREC_F16), GVT_E_STATE, "chunk-scaled operand needs the CTA-pair fp16 GEMM");
+    GVT_REQUIRE(EPI != EPI_STORE16 || (pair && PREC == PREC_F16), GVT_E_STATE, "fp16 store needs the CTA-pair fp16 GEMM");
     static bool attr = false, attr2 = false;
     if (pair) {
         if (!attr2) {
@@ -884,6 +948,99 @@ Operand make_operand(gvt_ctx *c, const char *name, const float *x, int64_t rows,
         o.scale = s;
     }
     return o;
+}
+
+// ---- fused fp16 path: pair-matrix rows assembled in shared memory, written as fp16 pieces
+bool fused_f16(gvt_ctx *c, int64_t q_in) {
+    return tc_prec(c) == PREC_F16 && c->gemm_cta == 2 && round_up(q_in, 32) * 4 <= 200 * 1024;
+}
+
+// one CTA per row r of [row_lo, row_lo + rows): cell values (sum of sign * p[src] over the
+// cell's run of entries, in entry order -- the same sums as k_densify) parked in shared
+// memory, row max -> power-of-two scale, then coalesced fp16 hi/lo stores of the whole row
+constexpr int BX_THREADS = 1024;  // a row's ~m*density cells spread over 32 warps (latency-bound gathers)
+__global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                                   const int32_t *__restrict__ src, const float *__restrict__ sign,
+                                                   const float *__restrict__ p, int64_t row_lo, int64_t rows,
+                                                   int64_t cols, int64_t ld, __half *__restrict__ hi,
+                                                   __half *__restrict__ lo, float *__restrict__ sinv) {
+    extern __shared__ float rowbuf[];  // ld floats
+    __shared__ float red[BX_THREADS / 32];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
+        __syncthreads();
+        const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
+        for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
+            const int32_t cc = col[k];
+            if (k > kb && col[k - 1] == cc) continue;  // not the head of its run
+            float s = sign[k] * __ldg(p + src[k]);
+            for (int64_t j = k + 1; j < ke && col[j] == cc; j++) s += sign[j] * __ldg(p + src[j]);
+            rowbuf[cc] = s;
+        }
+        __syncthreads();
+        float mx = 0.f;
+        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = red[0];
+        for (int w = 1; w < BX_THREADS / 32; w++) mx = fmaxf(mx, red[w]);
+        int e = 0;
+        if (mx > 0.f && isfinite(mx)) {
+            int ex;
+            frexpf(mx, &ex);
+            e = 15 - ex;
+        }
+        const float s = ldexpf(1.f, e);
+        if (threadIdx.x == 0) sinv[r] = ldexpf(1.f, -e);
+        __half2 *h2 = reinterpret_cast<__half2 *>(hi + r * ld), *l2 = reinterpret_cast<__half2 *>(lo + r * ld);
+        for (int64_t j = threadIdx.x; j < ld / 2; j += blockDim.x) {
+            const float v0 = rowbuf[2 * j] * s, v1 = rowbuf[2 * j + 1] * s;
+            const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1);
+            h2[j] = __halves2half2(a0, a1);
+            l2[j] = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
+        }
+        __syncthreads();
+    }
+}
+
+Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
+                  const float *p) {
+    Operand o;
+    o.prec = PREC_F16;
+    o.ld = round_up(cols > 0 ? cols : 1, 32);
+    std::string nm(name);
+    const int64_t rows_pad = round_up(rows > 0 ? rows : 1, 128);
+    __half *hi = wsT<__half>(c, (nm + ".h16").c_str(), (size_t)rows_pad * o.ld);
+    __half *lo = wsT<__half>(c, (nm + ".l16").c_str(), (size_t)rows_pad * o.ld);
+    float *s = wsT<float>(c, (nm + ".sinv").c_str(), (size_t)rows_pad);
+    const size_t smem = sizeof(float) * o.ld;
+    static size_t attr_smem = 0;
+    if (smem > 48 * 1024 && smem > attr_smem) {
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_smem = smem;
+    }
+    if (rows > 0)
+        GVT_LAUNCH(c, K_DENSIFY, k_build_x16, grid1d(rows, 1, 2 * c->sm_count), BX_THREADS, smem, e.row_ptr, e.col, e.src,
+                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s);
+    o.hi = hi;
+    o.lo = lo;
+    o.scale = s;
+    return o;
+}
+
+// hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256)) floats,
+// whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
+void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld) {
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.c_h16 = hi;
+    ep.c_l16 = lo;
+    ep.c_sk = sk;
+    ep.c_sk_ld = sk_ld;
+    ep.ldc = ldc;
+    launch_gemm<EPI_STORE16>(c, K_STAGE1_TC, A, B, M, N, K, ep);
 }
 
 // X[row][col] = sum of the (row, col) run of sorted entries (deterministic, in entry order)

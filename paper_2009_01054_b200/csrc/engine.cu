@@ -381,9 +381,52 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
 // ----------------------------------------------------------------------------- run
 static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
 
+// fused 3xFP16 dense path: X rows assembled straight into fp16 pieces, stage 1 writes S as
+// fp16 pieces with per-(row, 256-column) scales, stage 2 applies them per K-chunk; slab s of
+// S lives at s * (qpad * W) halves (and s * ntW * skld scales) so ranks all-gather equal slabs
+static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out) {
+    const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256);
+    const size_t slab_h = (size_t)g.qpad * g.W, slab_k = (size_t)ntW * skld;
+    __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
+    __half *Sl = wsT<__half>(c, (g.tag + ".S16l").c_str(), slab_h * g.nslab);
+    float *Sk = wsT<float>(c, (g.tag + ".S16k").c_str(), slab_k * g.nslab);
+    GVT_CUDA_TRY(cudaMemsetAsync(Sk, 0, sizeof(float) * slab_k * g.nslab, c->stream));
+    for (int s = 0; s < g.nslab; s++) {
+        if (!my_slab(c, s)) continue;
+        const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        if (w == 0) continue;
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.n, p_full);
+        gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.n, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
+                        skld);
+    }
+    // halves travel as pairs of floats (W is a multiple of 32)
+    allgather_slabs(c, reinterpret_cast<float *>(Sh), slab_h / 2);
+    allgather_slabs(c, reinterpret_cast<float *>(Sl), slab_h / 2);
+    allgather_slabs(c, Sk, slab_k);
+    bool first = true;
+    for (int s = 0; s < g.nslab; s++) {
+        const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        if (w == 0) continue;
+        Operand so;
+        so.prec = 0;
+        so.hi = Sh + s * slab_h;
+        so.lo = Sl + s * slab_h;
+        so.ld = g.W;
+        so.scale_k = Sk + s * slab_k;
+        so.scale_k_ld = skld;
+        gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, accumulate || !first,
+                        out);
+        first = false;
+    }
+}
+
 static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out,
                       bool values_ready = false) {
     c->last_engine = g.engine;
+    if (g.engine == 2 && fused_f16(c, g.C.n)) {
+        run_group_f16(c, g, p_full, coef, accumulate, out);
+        return;
+    }
     // ---- stage 1 on this rank's X-row slab(s)
     for (int s = 0; s < g.nslab; s++) {
         if (!my_slab(c, s)) continue;

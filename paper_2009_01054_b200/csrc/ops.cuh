@@ -1,6 +1,8 @@
 // ops.cuh -- launchers of the device kernels (internal).  Every launcher issues on
 // ctx->stream and goes through GVT_LAUNCH (launch count + optional event timing).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "gvt_internal.cuh"
 
 namespace gvt {
@@ -13,6 +15,9 @@ struct Operand {
     const void *hi = nullptr, *lo = nullptr;
     const float *scale = nullptr;
     int64_t ld = 0;
+    // alternatively one scale per (row, 256-wide K chunk): scale_k[chunk * scale_k_ld + row]
+    const float *scale_k = nullptr;
+    int64_t scale_k_ld = 0;
 };
 
 // A square factor (Gram / materialised ones / identity) copied to a padded device
@@ -98,6 +103,16 @@ void densify(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t row
 // C (M x N, ldc) = A (M x K) * B^T (B: N x K), fp32-accurate; optional tf32 split of C
 void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, float *Cf,
                    int64_t ldc, float *Chi, float *Clo);
+// fused fp16 path (3xFP16 + CTA pairs): can the stage-1 pieces below be used?
+bool fused_f16(gvt_ctx *c, int64_t q_in);
+// rows [row_lo, row_lo + rows) of the pair matrix built straight into an fp16 operand
+// (values sign * p[src] summed per cell in entry order, one row scale per row)
+Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
+                  const float *p);
+// C = A * B^T written as fp16 pieces (M rows x ldc) with per-(row, 256-col tile) scales
+// sk[tile * sk_ld + row] (sk_ld >= round_up(M, 256))
+void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out);

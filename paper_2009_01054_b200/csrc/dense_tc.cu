@@ -26,6 +26,8 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ops.cuh"
@@ -436,9 +438,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 constexpr int STAGES2 = 3;
 constexpr int HALF_BYTES = 128 * KB_BYTES;               // 16 KB: 128 rows of one operand piece
 constexpr int STAGE2_BYTES = 4 * HALF_BYTES;             // A hi/lo + B-half hi/lo = 64 KB per CTA
-constexpr int BAR2_OFF = STAGES2 * STAGE2_BYTES;
+constexpr int EPI2_OFF = STAGES2 * STAGE2_BYTES;             // dedicated epilogue staging (persistent)
+constexpr int EPI2_BYTES = N_EPI_WARPS * 32 * 33 * 4;         // 33 KB
+constexpr int BAR2_OFF = EPI2_OFF + EPI2_BYTES;
 constexpr int SMEM2_TOTAL = BAR2_OFF + 256 + 1024;
-static_assert(N_EPI_WARPS * 32 * 33 * 4 <= STAGES2 * STAGE2_BYTES, "epilogue staging aliases the stage ring");
+static_assert(SMEM2_TOTAL <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -502,9 +506,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_gemm2_x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N, int K,
                EpiParams ep) {
+    // Persistent: each CTA pair loops over pair tiles (256 x 256) t = cluster, cluster + #clusters, ...
+    // The smem ring position, the accumulator-chunk parity and the skip decisions advance
+    // identically in the producer, MMA and epilogue roles of both CTAs, so a tile's output
+    // phase overlaps the next tile's MMAs.
     constexpr int BKE = KB_BYTES / (PREC == PREC_TF32 ? 4 : 2);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float *estage = reinterpret_cast<float *>(smem + EPI2_OFF);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + BAR2_OFF);
     uint64_t *empty = full + STAGES2;
     uint64_t *tfull = empty + STAGES2;
@@ -513,26 +522,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
-    // rasterize CTA pairs over (256-row pair tiles, 256-column tiles), grouped
+    const int num_m = (M + BM - 1) / BM;
     const int num_mp = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN;
-    const int pid = blockIdx.x >> 1, in_group = GROUP_M * num_n;
-    const int first_m = (pid / in_group) * GROUP_M;
-    const int group_m = min(num_mp - first_m, GROUP_M);
-    const int mp_tile = first_m + (pid % in_group) % group_m;
-    const int n_tile = (pid % in_group) / group_m;
-    const int m_tile = 2 * mp_tile + (int)crank;  // this CTA's 128-row tile
-    const int m0 = m_tile * BM, n0 = n_tile * BN;
+    const int n_tiles = num_mp * num_n;
+    const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
     const int nk = (K + BKE - 1) / BKE;
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
     const int nch = (nk + kcb - 1) / kcb;
+    const int in_group = GROUP_M * num_n;
 
-    if (EPI == EPI_SAMPLED) {  // skip a pair tile that owns no sample (both CTAs decide alike)
+    // grouped rasterization of pair tiles; a sampled tile pair without samples is skipped
+    auto coords = [&](int t, int &mp_tile, int &n_tile) {
+        const int first_m = (t / in_group) * GROUP_M;
+        const int group_m = min(num_mp - first_m, GROUP_M);
+        mp_tile = first_m + (t % in_group) % group_m;
+        n_tile = (t % in_group) / group_m;
+    };
+    auto skip = [&](int mp_tile, int n_tile) -> bool {
+        if (EPI != EPI_SAMPLED) return false;
         const int64_t t0 = (int64_t)(2 * mp_tile) * ep.n_ct + n_tile, t1 = t0 + ep.n_ct;
-        const int64_t e0 = ep.chunk_ptr[t0 * (BN / 32)] == ep.chunk_ptr[(t0 + 1) * (BN / 32)];
-        const bool has1 = 2 * mp_tile + 1 < (M + BM - 1) / BM;
-        const int64_t e1 = !has1 || ep.chunk_ptr[t1 * (BN / 32)] == ep.chunk_ptr[(t1 + 1) * (BN / 32)];
-        if (e0 && e1) return;
-    }
+        const bool e0 = ep.chunk_ptr[t0 * (BN / 32)] == ep.chunk_ptr[(t0 + 1) * (BN / 32)];
+        const bool e1 = !(2 * mp_tile + 1 < num_m) || ep.chunk_ptr[t1 * (BN / 32)] == ep.chunk_ptr[(t1 + 1) * (BN / 32)];
+        return e0 && e1;
+    };
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmAh);
@@ -562,49 +574,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % STAGES2;
-                const uint32_t ph = (kb / STAGES2) & 1;
-                mbar_wait(&empty[s], ph ^ 1);  // own slot released by the leader's MMA commit
-                uint8_t *st = smem + s * STAGE2_BYTES;
-                if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
-                const int kc = kb * BKE;
-                tma_load_2d_pair(st, &tmAh, &full[s], kc, m0);
-                tma_load_2d_pair(st + HALF_BYTES, &tmAl, &full[s], kc, m0);
-                tma_load_2d_pair(st + 2 * HALF_BYTES, &tmBh, &full[s], kc, n0 + (int)crank * 128);
-                tma_load_2d_pair(st + 3 * HALF_BYTES, &tmBl, &full[s], kc, n0 + (int)crank * 128);
+            int kg = 0;  // global k-block counter = ring position
+            for (int t = cluster; t < n_tiles; t += n_clusters) {
+                int mp_tile, n_tile;
+                coords(t, mp_tile, n_tile);
+                if (skip(mp_tile, n_tile)) continue;
+                const int m0 = (2 * mp_tile + (int)crank) * BM, n0 = n_tile * BN;
+                for (int kb = 0; kb < nk; kb++, kg++) {
+                    const int s = kg % STAGES2;
+                    const uint32_t ph = (kg / STAGES2) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);  // own slot released by the leader's MMA commit
+                    uint8_t *st = smem + s * STAGE2_BYTES;
+                    if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
+                    const int kc = kb * BKE;
+                    tma_load_2d_pair(st, &tmAh, &full[s], kc, m0);
+                    tma_load_2d_pair(st + HALF_BYTES, &tmAl, &full[s], kc, m0);
+                    tma_load_2d_pair(st + 2 * HALF_BYTES, &tmBh, &full[s], kc, n0 + (int)crank * 128);
+                    tma_load_2d_pair(st + 3 * HALF_BYTES, &tmBl, &full[s], kc, n0 + (int)crank * 128);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader only)
             constexpr uint32_t idesc = idesc_mma2<PREC, BN>();
-            int kb = 0;
-            for (int ch = 0; ch < nch; ch++) {
-                const int b = ch & 1;
-                mbar_wait(&tempty[b], ((ch >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t acc = tmem + b * BN;
-                const int kend = min(nk, kb + kcb);
-                for (int kk = 0; kb < kend; kb++, kk++) {
-                    const int s = kb % STAGES2;
-                    const uint32_t ph = (kb / STAGES2) & 1;
-                    mbar_wait(&full[s], ph);
+            int kg = 0, cg = 0;
+            for (int t = cluster; t < n_tiles; t += n_clusters) {
+                int mp_tile, n_tile;
+                coords(t, mp_tile, n_tile);
+                if (skip(mp_tile, n_tile)) continue;
+                int kb = 0;
+                for (int ch = 0; ch < nch; ch++, cg++) {
+                    const int b = cg & 1;
+                    mbar_wait(&tempty[b], ((cg >> 1) & 1) ^ 1);
                     tc_fence_after();
-                    const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
-                    const uint32_t ah = base, al = base + HALF_BYTES, bh = base + 2 * HALF_BYTES,
-                                   bl = base + 3 * HALF_BYTES;
+                    const uint32_t acc = tmem + b * BN;
+                    const int kend = min(nk, kb + kcb);
+                    for (int kk = 0; kb < kend; kb++, kk++, kg++) {
+                        const int s = kg % STAGES2;
+                        const uint32_t ph = (kg / STAGES2) & 1;
+                        mbar_wait(&full[s], ph);
+                        tc_fence_after();
+                        const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
+                        const uint32_t ah = base, al = base + HALF_BYTES, bh = base + 2 * HALF_BYTES,
+                                       bl = base + 3 * HALF_BYTES;
 #pragma unroll
-                    for (int k = 0; k < KB_BYTES / 32; k++) {
-                        const uint32_t off = k * 32;
-                        const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
-                        const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
-                        mma_issue2<PREC>(acc, dah, dbh, idesc, (kk | k) != 0);
-                        mma_issue2<PREC>(acc, dah, dbl, idesc, 1);
-                        mma_issue2<PREC>(acc, dal, dbh, idesc, 1);
+                        for (int k = 0; k < KB_BYTES / 32; k++) {
+                            const uint32_t off = k * 32;
+                            const uint64_t dah = umma_desc(ah + off), dal = umma_desc(al + off);
+                            const uint64_t dbh = umma_desc(bh + off), dbl = umma_desc(bl + off);
+                            mma_issue2<PREC>(acc, dah, dbh, idesc, (kk | k) != 0);
+                            mma_issue2<PREC>(acc, dah, dbl, idesc, 1);
+                            mma_issue2<PREC>(acc, dal, dbh, idesc, 1);
+                        }
+                        mma_commit_pair(&empty[s]);  // frees the slot in both CTAs
                     }
-                    mma_commit_pair(&empty[s]);  // frees the slot in both CTAs
+                    mma_commit_pair(&tfull[b]);      // chunk accumulator ready in both CTAs
                 }
-                mma_commit_pair(&tfull[b]);      // accumulator ready in both CTAs
             }
         }
     } else {  // ---------------- epilogue warps 2..9 (both CTAs, own 128 rows)
@@ -612,161 +637,170 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int quarter = warp & 3;
         const int half = ew >> 2;
         const int row = quarter * 32 + lane;
-        const int gr = m0 + row;
-        float run[128];
+        const int t256 = threadIdx.x - 64;  // 0..255
+        int cg = 0;
+        for (int t = cluster; t < n_tiles; t += n_clusters) {
+            int mp_tile, n_tile;
+            coords(t, mp_tile, n_tile);
+            if (skip(mp_tile, n_tile)) continue;
+            const int m_tile = 2 * mp_tile + (int)crank;
+            const int m0 = m_tile * BM, n0 = n_tile * BN;
+            const int gr = m0 + row;
+            const int gc_base = n0 + half * 128;
+            float run[128];
 #pragma unroll
-        for (int i = 0; i < 128; i++) run[i] = 0.f;
-        for (int ch = 0; ch < nch; ch++) {
-            const int b = ch & 1;
-            mbar_wait(&tfull[b], (ch >> 1) & 1);
-            tc_fence_after();
-            const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
-            // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
-            const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + n0 + half * 128 : nullptr;
+            for (int i = 0; i < 128; i++) run[i] = 0.f;
+            for (int ch = 0; ch < nch; ch++, cg++) {
+                const int b = cg & 1;
+                mbar_wait(&tfull[b], (cg >> 1) & 1);
+                tc_fence_after();
+                const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
+                // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
+                const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
 #pragma unroll
-            for (int c4 = 0; c4 < 4; c4++) {
-                uint32_t r[32];
-                tmem_ld32_raw(ta + c4 * 32, r);
-                tmem_wait_ld();
-                if (sk) {
+                for (int c4 = 0; c4 < 4; c4++) {
+                    uint32_t r[32];
+                    tmem_ld32_raw(ta + c4 * 32, r);
+                    tmem_wait_ld();
+                    if (sk) {
 #pragma unroll
-                    for (int i = 0; i < 32; i++) run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c4 * 32 + i), run[c4 * 32 + i]);
-                } else {
+                        for (int i = 0; i < 32; i++)
+                            run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c4 * 32 + i), run[c4 * 32 + i]);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_leader(&tempty[b]);
-        }
-        const int gc_base = n0 + half * 128;
-        if (EPI == EPI_STORE16) {
-            // fp16 hi/lo of the unscaled result with one power-of-two scale per (row, 256-col tile):
-            // the two warps holding this row's column halves exchange their maxima
-            const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
-            float mx = 0.f;
-#pragma unroll
-            for (int i = 0; i < 128; i++) {
-                const int gc = gc_base + i;
-                const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
-                run[i] *= ra * rb;
-                if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
-            }
-            float *xch = reinterpret_cast<float *>(smem);  // stage ring is free: [quarter][lane][half]
-            xch[(quarter * 32 + lane) * 2 + half] = mx;
-            named_bar(1, 32 * N_EPI_WARPS);
-            mx = fmaxf(xch[(quarter * 32 + lane) * 2], xch[(quarter * 32 + lane) * 2 + 1]);
-            int e = 0;
-            if (mx > 0.f && isfinite(mx)) {
-                int ex;
-                frexpf(mx, &ex);
-                e = 15 - ex;
-            }
-            const float s = ldexpf(1.f, e);
-            if (gr < M) {
-                if (half == 0) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
-                __half *hp = ep.c_h16 + (int64_t)gr * ep.ldc + gc_base;
-                __half *lp = ep.c_l16 + (int64_t)gr * ep.ldc + gc_base;
-#pragma unroll
-                for (int i = 0; i < 128; i += 2) {
-                    if (gc_base + i + 1 < N) {
-                        const float v0 = run[i] * s, v1 = run[i + 1] * s;
-                        const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-                        *reinterpret_cast<__half2 *>(hp + i) = __halves2half2(h0, h1);
-                        *reinterpret_cast<__half2 *>(lp + i) =
-                            __halves2half2(__float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
-                    } else if (gc_base + i < N) {
-                        const float v0 = run[i] * s;
-                        const __half h0 = __float2half_rn(v0);
-                        hp[i] = h0;
-                        lp[i] = __float2half_rn(v0 - __half2float(h0));
+                        for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
-        }
-        if (EPI != EPI_STORE16 && (ep.sa || ep.sb)) {
-            const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
-#pragma unroll
-            for (int i = 0; i < 128; i++) {
-                const int gc = gc_base + i;
-                const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
-                run[i] *= ra * rb;
-            }
-        }
-        if (EPI == EPI_STORE) {
-            if (gr < M) {
-                float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
-                if (gc_base + 128 <= N) {
-#pragma unroll
-                    for (int i = 0; i < 128; i += 4)
-                        *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 128; i++)
-                        if (gc_base + i < N) cf[i] = run[i];
-                }
-                if (ep.c_hi) {
-#pragma unroll
-                    for (int i = 0; i < 128; i++) {
-                        if (gc_base + i < N) {
-                            float h = tf32_round(run[i]);
-                            ep.c_hi[(int64_t)gr * ep.ldc + gc_base + i] = h;
-                            ep.c_lo[(int64_t)gr * ep.ldc + gc_base + i] = tf32_round(run[i] - h);
-                        }
-                    }
-                }
-            }
-        } else if (EPI == EPI_GRAM) {
-            if (gr < M) {
-                float *krow = ep.c_f + (int64_t)gr * ep.ldc;
-                const float ni = ep.kind == GVT_BASE_GAUSSIAN ? ep.norms[gr] : 0.f;
+            if (EPI == EPI_STORE16) {
+                // fp16 hi/lo of the unscaled result, one power-of-two scale per (row, 256-col tile):
+                // the two warps holding this row's column halves exchange their maxima
+                const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+                float mx = 0.f;
 #pragma unroll
                 for (int i = 0; i < 128; i++) {
                     const int gc = gc_base + i;
-                    if (gc < N) {
-                        float x = run[i];
-                        if (ep.kind == GVT_BASE_GAUSSIAN) {
-                            float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
-                            if (gc == gr) d2 = 0.f;
-                            x = expf(-ep.gamma * d2);
-                        } else if (ep.kind == GVT_BASE_POLY) {
-                            float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
-                            for (int e = 0; e < ep.degree; e++) rr *= bb;
-                            x = rr;
+                    const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                    run[i] *= ra * rb;
+                    if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
+                }
+                estage[(quarter * 32 + lane) * 2 + half] = mx;
+                named_bar(1, 32 * N_EPI_WARPS);
+                mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
+                named_bar(1, 32 * N_EPI_WARPS);
+                int e = 0;
+                if (mx > 0.f && isfinite(mx)) {
+                    int ex;
+                    frexpf(mx, &ex);
+                    e = 15 - ex;
+                }
+                const float s = ldexpf(1.f, e);
+                if (gr < M) {
+                    if (half == 0) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+                    __half *hp = ep.c_h16 + (int64_t)gr * ep.ldc + gc_base;
+                    __half *lp = ep.c_l16 + (int64_t)gr * ep.ldc + gc_base;
+#pragma unroll
+                    for (int i = 0; i < 128; i += 2) {
+                        if (gc_base + i + 1 < N) {
+                            const float v0 = run[i] * s, v1 = run[i + 1] * s;
+                            const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+                            *reinterpret_cast<__half2 *>(hp + i) = __halves2half2(h0, h1);
+                            *reinterpret_cast<__half2 *>(lp + i) = __halves2half2(
+                                __float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
+                        } else if (gc_base + i < N) {
+                            const float v0 = run[i] * s;
+                            const __half h0 = __float2half_rn(v0);
+                            hp[i] = h0;
+                            lp[i] = __float2half_rn(v0 - __half2float(h0));
                         }
-                        krow[gc] = x;
                     }
+                }
+                continue;
+            }
+            if (ep.sa || ep.sb) {
+                const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+#pragma unroll
+                for (int i = 0; i < 128; i++) {
+                    const int gc = gc_base + i;
+                    const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                    run[i] *= ra * rb;
                 }
             }
-        } else if (EPI == EPI_SAMPLED) {
-            float *stage = reinterpret_cast<float *>(smem);
-            const int t = threadIdx.x - 64;
-            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
-            const bool tile_ok = m_tile < (M + BM - 1) / BM;
+            if (EPI == EPI_STORE) {
+                if (gr < M) {
+                    float *cf = ep.c_f + (int64_t)gr * ep.ldc + gc_base;
+                    if (gc_base + 128 <= N) {
 #pragma unroll
-            for (int c4 = 0; c4 < 4; c4++) {
-                float *mine = stage + (half * 4 + quarter) * 32 * 33 + lane * 33;
+                        for (int i = 0; i < 128; i += 4)
+                            *reinterpret_cast<float4 *>(cf + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                    } else {
 #pragma unroll
-                for (int i = 0; i < 32; i++) mine[i] = run[c4 * 32 + i];
-                named_bar(1, 32 * N_EPI_WARPS);
-                if (tile_ok) {
+                        for (int i = 0; i < 128; i++)
+                            if (gc_base + i < N) cf[i] = run[i];
+                    }
+                    if (ep.c_hi) {
 #pragma unroll
-                    for (int hh = 0; hh < 2; hh++) {
-                        const int chunk = hh * 4 + c4;
-                        const int64_t cidx = tile * (BN / 32) + chunk;
-                        const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
-                        const int gc0 = n0 + chunk * 32;
-                        for (int64_t k = kb0 + t; k < ke; k += 32 * N_EPI_WARPS) {
-                            const int rl = ep.s_r[k] - m0;
-                            const int cl = ep.s_c[k] - gc0;
-                            const float val = stage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
-                            const int64_t d = ep.s_dst[k];
-                            ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
+                        for (int i = 0; i < 128; i++) {
+                            if (gc_base + i < N) {
+                                float h = tf32_round(run[i]);
+                                ep.c_hi[(int64_t)gr * ep.ldc + gc_base + i] = h;
+                                ep.c_lo[(int64_t)gr * ep.ldc + gc_base + i] = tf32_round(run[i] - h);
+                            }
                         }
                     }
                 }
-                named_bar(1, 32 * N_EPI_WARPS);
+            } else if (EPI == EPI_GRAM) {
+                if (gr < M) {
+                    float *krow = ep.c_f + (int64_t)gr * ep.ldc;
+                    const float ni = ep.kind == GVT_BASE_GAUSSIAN ? ep.norms[gr] : 0.f;
+#pragma unroll
+                    for (int i = 0; i < 128; i++) {
+                        const int gc = gc_base + i;
+                        if (gc < N) {
+                            float x = run[i];
+                            if (ep.kind == GVT_BASE_GAUSSIAN) {
+                                float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
+                                if (gc == gr) d2 = 0.f;
+                                x = expf(-ep.gamma * d2);
+                            } else if (ep.kind == GVT_BASE_POLY) {
+                                float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
+                                for (int e = 0; e < ep.degree; e++) rr *= bb;
+                                x = rr;
+                            }
+                            krow[gc] = x;
+                        }
+                    }
+                }
+            } else if (EPI == EPI_SAMPLED) {
+                const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+                const bool tile_ok = m_tile < num_m;
+#pragma unroll
+                for (int c4 = 0; c4 < 4; c4++) {
+                    float *mine = estage + (half * 4 + quarter) * 32 * 33 + lane * 33;
+#pragma unroll
+                    for (int i = 0; i < 32; i++) mine[i] = run[c4 * 32 + i];
+                    named_bar(1, 32 * N_EPI_WARPS);
+                    if (tile_ok) {
+#pragma unroll
+                        for (int hh = 0; hh < 2; hh++) {
+                            const int chunk = hh * 4 + c4;
+                            const int64_t cidx = tile * (BN / 32) + chunk;
+                            const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
+                            const int gc0 = n0 + chunk * 32;
+                            for (int64_t k = kb0 + t256; k < ke; k += 32 * N_EPI_WARPS) {
+                                const int rl = ep.s_r[k] - m0;
+                                const int cl = ep.s_c[k] - gc0;
+                                const float val = estage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
+                                const int64_t d = ep.s_dst[k];
+                                ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
+                            }
+                        }
+                    }
+                    named_bar(1, 32 * N_EPI_WARPS);
+                }
             }
         }
     }
@@ -777,6 +811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
     }
 }
+
 
 // ----------------------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -831,7 +866,9 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
                 cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
             attr2 = true;
         }
-        dim3 grid((unsigned)(2 * ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM))));
+        const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
+        const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
+        dim3 grid((unsigned)(2 * clusters));
         GVT_LAUNCH(c, kind_id, (k_gemm2_x3<PREC, EPI>), grid, NTHREADS, SMEM2_TOTAL, ah, al, bh, bl, (int)M, (int)N,
                    (int)K, ep);
         return;

@@ -1000,7 +1000,8 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
                                                    const int32_t *__restrict__ src, const float *__restrict__ sign,
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
                                                    int64_t cols, int64_t ld, __half *__restrict__ hi,
-                                                   __half *__restrict__ lo, float *__restrict__ sinv) {
+                                                   __half *__restrict__ lo, float *__restrict__ sinv,
+                                                   const float *__restrict__ diag) {
     extern __shared__ float rowbuf[];  // ld floats
     __shared__ float red[BX_THREADS / 32];
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -1014,6 +1015,8 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
             for (int64_t j = k + 1; j < ke && col[j] == cc; j++) s += sign[j] * __ldg(p + src[j]);
             rowbuf[cc] = s;
         }
+        __syncthreads();
+        if (diag && threadIdx.x == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
         __syncthreads();
         float mx = 0.f;
         for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
 }
 
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p) {
+                  const float *p, const float *diag) {
     Operand o;
     o.prec = PREC_F16;
     o.ld = round_up(cols > 0 ? cols : 1, 32);
@@ -1059,7 +1062,7 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     }
     if (rows > 0)
         GVT_LAUNCH(c, K_DENSIFY, k_build_x16, grid1d(rows, 1, 2 * c->sm_count), BX_THREADS, smem, e.row_ptr, e.col, e.src,
-                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s);
+                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
     o.hi = hi;
     o.lo = lo;
     o.scale = s;
@@ -1078,6 +1081,17 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.c_sk_ld = sk_ld;
     ep.ldc = ldc;
     launch_gemm<EPI_STORE16>(c, K_STAGE1_TC, A, B, M, N, K, ep);
+}
+
+__global__ void k_add_diag(float *__restrict__ X, int64_t ldX, const float *__restrict__ diag, int64_t row_lo,
+                           int64_t rows) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+        X[r * ldX + row_lo + r] += diag[row_lo + r];
+}
+
+void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_lo, int64_t rows) {
+    if (rows <= 0) return;
+    GVT_LAUNCH(c, K_DENSIFY, k_add_diag, grid1d(rows, 256), 256, 0, X, ldX, diag, row_lo, rows);
 }
 
 // X[row][col] = sum of the (row, col) run of sorted entries (deterministic, in entry order)

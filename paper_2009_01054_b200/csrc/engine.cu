@@ -180,6 +180,7 @@ struct GroupPlan {
     int64_t qpad = 0;
     float *S = nullptr;
     std::string tag;
+    float *diag = nullptr;  // optional separate diagonal of X (global row index), computed per matvec
 };
 
 struct MatvecPlan {
@@ -306,13 +307,23 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
     case FORM_MLPK: {
         EntryKinds k;
         memset(&k, 0, sizeof(k));
-        k.count = 4;
+        // L = diag(bF + bS) - B - B^T: the off-diagonal part as entries, the diagonal as a vector
+        // (segment sums over both pair elements; a diagonal cell gathers deg(h) entries, which
+        // would serialise a per-cell sum)
+        k.count = 2;
         k.k[0] = EntryKind{F, Sx, -1.f};
         k.k[1] = EntryKind{Sx, F, -1.f};
-        k.k[2] = EntryKind{F, F, 1.f};
-        k.k[3] = EntryKind{Sx, Sx, 1.f};
         group(P.D, P.D, k, P.m, P.m, F, Sx, P.m, 1.f, "g0");
+        {
+            EntryKinds kd;
+            memset(&kd, 0, sizeof(kd));
+            kd.count = 2;
+            kd.k[0] = EntryKind{F, Sx, 1.f};
+            kd.k[1] = EntryKind{Sx, F, 1.f};
+            build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kd, P.m, P.m, mp.byF);
+        }
         mp.buf = wsT<float>(c, "mlpk.buf", (size_t)(P.n_out + P.m));
+        mp.groups[0].diag = wsT<float>(c, "mlpk.diag", (size_t)round_up(P.m > 0 ? P.m : 1, 32));
         break;
     }
     case FORM_LINEAR:
@@ -395,7 +406,7 @@ static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float c
         if (!my_slab(c, s)) continue;
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
         if (w == 0) continue;
-        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.n, p_full);
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.n, p_full, g.diag);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.n, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
                         skld);
     }
@@ -446,13 +457,14 @@ static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef,
             const int64_t rows_pad = round_up(w > 0 ? w : 1, 128);
             float *X = wsT<float>(c, "dense.X", (size_t)rows_pad * ldX);
             densify(c, g.ent, k0, k1, lo, X, ldX, rows_pad);
+            if (g.diag) add_diag(c, X, ldX, g.diag, lo, w);
             Operand xo = make_operand(c, "dense.Xop", X, w, g.C.n, ldX, ldX, rows_pad);
             gemm_nt_store(c, g.C.op, xo, g.q_out, w, g.C.n, Ss, g.W, nullptr, nullptr);
         } else {
             EntryPlan es = g.ent;
             es.row_ptr = g.ent.row_ptr + lo;
             es.nrow = w;
-            stage1_sparse(c, es, g.C, g.q_out, Ss, g.W);
+            stage1_sparse(c, es, g.C, g.q_out, Ss, g.W, g.diag, lo);
         }
     }
     // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab
@@ -491,6 +503,8 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         run_group(c, mp.groups[0], p, mp.groups[0].coef, 0, u);
         break;
     case FORM_MLPK:
+        entry_values(c, mp.byF, p);
+        segment_sum(c, mp.byF, mp.groups[0].diag);  // diag(L) = bF + bS
         run_group(c, mp.groups[0], p, 1.f, 0, mp.buf);
         combine_mlpk(c, P.of, P.os, P.n_out, mp.buf, u);
         break;
@@ -604,7 +618,7 @@ static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_i
     if (!tc_available(c) || c->engine == 1) return false;
     if (form == FORM_LINEAR || form == FORM_RANKING || form == FORM_CARTESIAN) return false;
     if (c->engine == 2) return true;
-    double mult = (form == FORM_SYM || form == FORM_ANTI) ? 2.0 : (form == FORM_MLPK ? 4.0 : 1.0);
+    double mult = (form == FORM_SYM || form == FORM_ANTI || form == FORM_MLPK) ? 2.0 : 1.0;  // entries per pair
     double cells = (form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC) ? (double)m * (double)q
                                                                                      : (double)m * (double)m;
     return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold;

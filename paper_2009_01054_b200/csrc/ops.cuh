@@ -74,7 +74,9 @@ int64_t count_out_of_range(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bo
 
 // ---- sparse engine (sparse.cu)
 void entry_values(gvt_ctx *c, const EntryPlan &e, const float *p);
-void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS);
+// S[t][h] = sum_{entries (h, col)} val C[col][t] (+ diag[row_lo + h] C[row_lo + h][t] if diag)
+void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
+                   const float *diag = nullptr, int64_t row_lo = 0);
 void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const float *S, int64_t ldS, int64_t K,
                    float coef, int accumulate, float *out);
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)
@@ -108,7 +110,9 @@ bool fused_f16(gvt_ctx *c, int64_t q_in);
 // rows [row_lo, row_lo + rows) of the pair matrix built straight into an fp16 operand
 // (values sign * p[src] summed per cell in entry order, one row scale per row)
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p);
+                  const float *p, const float *diag = nullptr);
+// X[r][row_lo + r] += diag[row_lo + r] for r < rows (fp32 X, leading dimension ldX)
+void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_lo, int64_t rows);
 // C = A * B^T written as fp16 pieces (M rows x ldc) with per-(row, 256-col tile) scales
 // sk[tile * sk_ld + row] (sk_ld >= round_up(M, 256))
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,

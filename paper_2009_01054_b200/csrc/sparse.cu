@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict
                                                        const int32_t *__restrict__ col,
                                                        const float *__restrict__ val, int64_t m_in,
                                                        const float *__restrict__ C, int64_t ldC, int64_t q_out,
-                                                       float *__restrict__ S, int64_t ldS) {
+                                                       float *__restrict__ S, int64_t ldS,
+                                                       const float *__restrict__ diag, int64_t row_lo) {
     constexpr int TT = TPB * TPT;
     extern __shared__ float sm[];  // [H][TT + 1]
     const int tid = threadIdx.x;
@@ -83,6 +84,15 @@ __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict
                     acc[i] = fmaf(x0, (t0 + t < q_out) ? __ldg(r0 + t) : 0.f, acc[i]);
                 }
             }
+            if (diag) {  // separate diagonal of X (MLPK Laplacian): X[h][h] = diag[h]
+                const float dv = diag[row_lo + h];
+                const float *r0 = C + (row_lo + h) * ldC + t0;
+#pragma unroll
+                for (int i = 0; i < TPT; i++) {
+                    const int64_t t = tid + (int64_t)TPB * i;
+                    acc[i] = fmaf(dv, (t0 + t < q_out) ? __ldg(r0 + t) : 0.f, acc[i]);
+                }
+            }
         }
 #pragma unroll
         for (int i = 0; i < TPT; i++) sm[hl * (TT + 1) + tid + TPB * i] = acc[i];
@@ -99,7 +109,8 @@ __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict
     }
 }
 
-void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS) {
+void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
+                   const float *diag, int64_t row_lo) {
     constexpr int H = 32, TPB = 128, TPT = 4, TT = TPB * TPT;
     if (q_out == 0 || ldS == 0) return;
     dim3 grid((unsigned)((q_out + TT - 1) / TT), (unsigned)((ldS + H - 1) / H));
@@ -111,7 +122,7 @@ void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_ou
         attr = true;
     }
     GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB, TPT>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
-               C.p, C.ld, q_out, S, ldS);
+               C.p, C.ld, q_out, S, ldS, diag, row_lo);
 }
 
 // ----------------------------------------------------------------------------- stage 2

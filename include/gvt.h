@@ -99,8 +99,10 @@ typedef enum {
                                     (default), 1 = 3xTF32; both fp32-accurate (reading S16)          */
     GVT_OPT_SLABS = 5,           /* single GPU: split stage 1 / stage 2 into this many X-row slabs,
                                     exactly as the data-parallel path does across ranks (default 1) */
-    GVT_OPT_GEMM_CTA = 6         /* tensor-core GEMM: 2 = CTA pair with tcgen05 cta_group::2 (256-row
+    GVT_OPT_GEMM_CTA = 6,        /* tensor-core GEMM: 2 = CTA pair with tcgen05 cta_group::2 (256-row
                                     tiles, default), 1 = single-CTA 128-row tiles                  */
+    GVT_OPT_GRAPHS = 7           /* 1 (default): fixed-iteration CG replays one captured iteration as
+                                    a CUDA graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches */
 } gvt_option;
 
 /* Per-context counters (gvt_get_stats). */

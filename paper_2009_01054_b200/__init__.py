@@ -38,6 +38,7 @@ PREC_FP16X3, PREC_TF32X3 = 0, 1
 ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE = 0, 1, 2
 OPT_SLABS = 5
 OPT_GEMM_CTA = 6
+OPT_GRAPHS = 7
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32
 

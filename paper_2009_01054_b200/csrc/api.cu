@@ -92,6 +92,7 @@ gvt_status gvt_destroy(gvt_ctx *c) {
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     delete c;
     return GVT_OK;
 }
@@ -121,6 +122,9 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     case GVT_OPT_TC_PRECISION:
         GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "tc precision must be 0 (fp16 x3) or 1 (tf32 x3)");
         c->tc_precision = (int)v;
+        break;
+    case GVT_OPT_GRAPHS:
+        c->graphs = v != 0;
         break;
     case GVT_OPT_GEMM_CTA:
         GVT_REQUIRE(v == 1 || v == 2, GVT_E_PARAM, "gemm cta must be 1 or 2");

@@ -724,10 +724,50 @@ gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
     plan_matvec(c, P, terms, n_terms, form, mp);
     cg_init(c, yd, n, x, r, p, state, rel_tol);
     double *hstate = (double *)pinned(c, sizeof(double) * 16);
-    for (int it = 0; it < max_iter; it++) {
+    auto iteration = [&]() {
         run_matvec(c, P, mp, p, Ap);
         cg_after_matvec(c, Ap, p, n, lambda, state);
-        cg_update(c, x, r, p, Ap, n, state, it, nullptr);
+        cg_update(c, x, r, p, Ap, n, state, 0, nullptr);
+    };
+    // Fixed-iteration mode: after one eager iteration (workspaces settle) the iteration body
+    // is captured once as a CUDA graph and replayed -- the loop is launch-bound on small
+    // problems.  All CG control lives on the device (halted flags), so replays are exact.
+    const bool graphs = c->graphs && rel_tol == 0.0 && max_iter >= 3 && !c->profile;
+    int it = 0;
+    if (graphs) {
+        iteration();
+        it = 1;
+        if (!c->cap_stream) GVT_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t user = c->stream;
+        int64_t before[K_NUM_KINDS], l0 = c->launches;
+        for (int k = 0; k < K_NUM_KINDS; k++) before[k] = c->counts[k];
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        c->stream = c->cap_stream;
+        GVT_CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            iteration();
+        } catch (...) {
+            cudaStreamEndCapture(c->cap_stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            c->stream = user;
+            throw;
+        }
+        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
+        c->stream = user;
+        GVT_CUDA_TRY(ce);
+        GVT_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+        const int64_t per_iter = c->launches - l0;
+        for (; it < max_iter; it++) GVT_CUDA_TRY(cudaGraphLaunch(exec, c->stream));
+        // launch accounting: the captured kernels run once per replay
+        const int64_t replays = max_iter - 1;
+        c->launches = l0 + per_iter * replays;
+        for (int k = 0; k < K_NUM_KINDS; k++) c->counts[k] = before[k] + (c->counts[k] - before[k]) * replays;
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+    }
+    for (; it < max_iter; it++) {
+        iteration();
         if (rel_tol > 0.0) {  // residual mode: host decides whether to continue
             GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
             GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -172,6 +172,20 @@ def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engin
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
+_ORACLE_GRAMS = {}
+
+
+def oracle_grams(w):
+    """fp64 oracle Grams of the workload, computed once per process (not part of the sample)."""
+    import oracle as O
+    key = w.name
+    if key not in _ORACLE_GRAMS:
+        D = O.gram(w.base, w.Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+        T = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+        _ORACLE_GRAMS[key] = (D, T)
+    return _ORACLE_GRAMS[key]
+
+
 def oracle_sample(w, kernel, n_targets=8, seed=0):
     """The oracle's GVT matvec on a bounded sample of the training matvec: the outputs whose
     second element lies among `n_targets` seeded targets (the oracle then forms S only for
@@ -180,8 +194,7 @@ def oracle_sample(w, kernel, n_targets=8, seed=0):
     rng = np.random.default_rng(seed)
     tset = rng.choice(w.q, n_targets, replace=False)
     idx = np.nonzero(np.isin(w.train_second, tset))[0]
-    D = O.gram(w.base, w.Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
-    T = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+    D, T = oracle_grams(w)
     a = synth.random_vector(seed, w.n)
     terms = O.kernel_terms(kernel)
     t0 = time.perf_counter()
@@ -381,7 +394,7 @@ def main():
     ap.add_argument("--no-profile", dest="profile", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-targets", type=int, default=8)
+    ap.add_argument("--ref-targets", type=int, default=32)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -218,7 +218,7 @@ def run_reference(args, rank, world):
     tot = sum(times)
     val = cnt / tot / 1e9
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -254,7 +254,7 @@ def run_gpu(args, rank, world, local_rank):
         dist.broadcast_object_list(obj, src=0)
         ctx.comm_init(obj[0], rank, world)
 
-    # ---- shard (weak scaling: each rank holds one full copy of the workload's pairs
+    # ---- shard (strong scaling: the whole workload is fixed as N grows; each rank generates the full workload
     #      and processes its drug range)
     f, s, y = w.train_first, w.train_second, w.y
     tf_, ts_ = w.test_first, w.test_second
@@ -366,7 +366,7 @@ def run_gpu(args, rank, world, local_rank):
                          f"seeded targets ({k} outputs; stage 1 streams all {w.n} pairs for those rows)",
                "seconds": round(dt, 2)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
                        "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,

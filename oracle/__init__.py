@@ -77,7 +77,9 @@ def lib():
         L.oracle_term_gvt.argtypes = [P, P, i64, P, i64, P, P, i64, P, P, i64, P, i32, P, P]
         L.oracle_term_cost.argtypes = [P, i64, i64, i32, P, P, i64, P, P, i64, P, P]
         L.oracle_gvt_matvec.argtypes = [P, i32, P, i64, P, i64, P, P, i64, P, P, i64, P, i32, P, P]
-        L.oracle_cg.argtypes = [i32, P, i32, i32, P, i64, P, i64, P, P, i64, P, dbl, i32, dbl, P, P, P]
+        L.oracle_cg.argtypes = [i32, P, i32, i32, P, i64, P, i64, P, P, i64, P, dbl, i32, dbl, P, P, P, P]
+        L.oracle_minres.argtypes = [i32, P, i32, i32, P, i64, P, i64, P, P, i64, P, dbl, i32, dbl, P, P, P, P]
+        L.oracle_auc.argtypes = [P, P, i64, P]
         L.oracle_sort_plan.argtypes = [P, P, i64, i64, i64, i32, P, P]
         L.oracle_num_threads.restype = i32
         _lib = L
@@ -193,20 +195,78 @@ def gvt_matvec(terms, D, T, of, os_, inf, ins, a, variant=1, return_ops=False):
     return (u, ops.value) if return_ops else u
 
 
-def cg(terms, D, T, f, s, y, lam, max_iter, rel_tol=0.0, kernel=-1, explicit=False):
-    """CG on (K + lam I) a = y (O5).  Returns (a, iters, relres_hist, code)."""
+def _solve(fn, name, terms, D, T, f, s, y, lam, max_iter, rel_tol, kernel, explicit, history):
     D, T, y = _d(D), _d(T), _d(y)
     f, s = _i(f), _i(s)
-    x = np.zeros(len(f), dtype=np.float64)
+    n = len(f)
+    x = np.zeros(n, dtype=np.float64)
     it = ctypes.c_int(0)
     hist = np.full(max_iter + 1, np.nan)
+    xh = np.zeros((max_iter + 1, n), dtype=np.float64) if history else None
     tt = terms_array(terms if terms else [])
-    rc = lib().oracle_cg(kernel, ctypes.cast(tt, ctypes.c_void_p), len(terms) if terms else 0, int(explicit),
-                         _p(D), D.shape[0], _p(T), 0 if T is None else T.shape[0], _p(f), _p(s), len(f), _p(y),
-                         float(lam), int(max_iter), float(rel_tol), _p(x), ctypes.byref(it), _p(hist))
+    rc = fn(kernel, ctypes.cast(tt, ctypes.c_void_p), len(terms) if terms else 0, int(explicit),
+            _p(D), D.shape[0], _p(T), 0 if T is None else T.shape[0], _p(f), _p(s), n, _p(y),
+            float(lam), int(max_iter), float(rel_tol), _p(x), ctypes.byref(it), _p(hist), _p(xh))
     if rc not in (OK, E_BREAKDOWN):
-        raise OracleError(rc, "cg")
-    return x, it.value, hist[: it.value + 1], rc
+        raise OracleError(rc, name)
+    out = (x, it.value, hist[: it.value + 1], rc)
+    return out + (xh[: it.value + 1],) if history else out
+
+
+def cg(terms, D, T, f, s, y, lam, max_iter, rel_tol=0.0, kernel=-1, explicit=False, history=False):
+    """CG on (K + lam I) a = y (O5).  Returns (a, iters, relres_hist, code[, iterates])."""
+    return _solve(lib().oracle_cg, "cg", terms, D, T, f, s, y, lam, max_iter, rel_tol, kernel, explicit, history)
+
+
+def minres(terms, D, T, f, s, y, lam, max_iter, rel_tol=0.0, kernel=-1, explicit=False, history=False):
+    """MINRES on (K + lam I) a = y (O5b).  Returns (a, iters, relres_hist, code[, iterates])."""
+    return _solve(lib().oracle_minres, "minres", terms, D, T, f, s, y, lam, max_iter, rel_tol, kernel, explicit,
+                  history)
+
+
+def auc(labels, scores):
+    """Mann-Whitney AUC by its definition (O8); positives are labels > 0."""
+    lab, sc = _d(labels), _d(scores)
+    out = ctypes.c_double(0.0)
+    _check(lib().oracle_auc(_p(lab), _p(sc), len(lab), ctypes.byref(out)), "auc")
+    return out.value
+
+
+def early_stop_rule(auc_seq, patience):
+    """The early-stopping rule of PAPER.md:852-856 ("until the AUC stops increasing in
+    Z_validation for a given number of iterations") as SPEC.md fit_early_stopping states it:
+    auc_seq[k-1] is the validation AUC after iteration k = 1, 2, ...; stop after `patience`
+    consecutive iterations without STRICT improvement over the best so far; the best
+    iteration is the earliest one reaching the maximum.  Returns (best_iter, best_auc,
+    iters_used, stopped): iters_used = the iteration at which the rule fired (stopped=True)
+    or len(auc_seq)."""
+    best, best_it, bad = -np.inf, 0, 0
+    for k, a in enumerate(auc_seq, start=1):
+        if a > best:
+            best, best_it, bad = a, k, 0
+        else:
+            bad += 1
+            if bad >= patience:
+                return best_it, best, k, True
+    return best_it, best, len(auc_seq), False
+
+
+def fit_early_stopping(terms, D, T, f, s, y, vf, vs, vlab, lam, patience, max_iter, solver="minres"):
+    """Early-stopping ridge regression (SPEC.md fit_early_stopping): run the
+    solver on the inner sample; after every iteration k predict the validation pairs with the
+    iterate x_k (O6: scores = K_val,inner x_k by the per-term GVT), take their AUC (O8) and
+    apply early_stop_rule.  Returns (best_iter, best_auc, iters_run, auc_hist, a_best) with
+    auc_hist[k-1] the AUC after iteration k."""
+    fn = minres if solver == "minres" else cg
+    x, it, hist, rc, xh = fn(terms, D, T, f, s, y, lam, max_iter, history=True)
+    aucs = []
+    for k in range(1, it + 1):
+        aucs.append(auc(vlab, gvt_matvec(terms, D, T, vf, vs, f, s, xh[k])))
+        if early_stop_rule(aucs, patience)[3]:
+            break
+    best_it, best_auc, _, _ = early_stop_rule(aucs, patience)
+    a_best = xh[best_it] if best_it > 0 else np.zeros(len(f))
+    return best_it, best_auc, len(aucs), np.array(aucs), a_best
 
 
 def sort_plan(first, second, m, q, mode=0):

@@ -419,12 +419,13 @@ int oracle_gvt_matvec(const oracle_term *terms, int n_terms, const double *D, in
  * p.Ap <= 0 is a breakdown: the current iterate is returned with OR_E_BREAKDOWN.
  * The operator is the per-term GVT (use_explicit = 0) or the explicit definition
  * (use_explicit = 1, needs kernel >= 0).  relres_hist (nullable, max_iter+1 entries)
- * receives sqrt(rho_k)/||y|| for k = 0..iters. */
+ * receives sqrt(rho_k)/||y|| for k = 0..iters; x_hist (nullable, (max_iter+1) x n)
+ * receives the iterates x_0 .. x_iters (early stopping). */
 int oracle_cg(int kernel, const oracle_term *terms, int n_terms, int use_explicit,
               const double *D, int64_t m, const double *T, int64_t q,
               const int32_t *f, const int32_t *s, int64_t n, const double *y,
               double lambda, int max_iter, double rel_tol,
-              double *x, int *iters_out, double *relres_hist) {
+              double *x, int *iters_out, double *relres_hist, double *x_hist) {
     if (!(lambda >= 0) || max_iter < 0 || rel_tol < 0) return OR_E_PARAM;
     double *r = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double *p = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
@@ -434,6 +435,7 @@ int oracle_cg(int kernel, const oracle_term *terms, int n_terms, int use_explici
     for (int64_t i = 0; i < n; i++) { x[i] = 0.0; r[i] = y[i]; p[i] = y[i]; rho += y[i] * y[i]; }
     double ynorm = sqrt(rho);
     if (relres_hist) relres_hist[0] = ynorm > 0 ? 1.0 : 0.0;
+    if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[i] = 0.0;
     int k = 0, rc = OR_OK;
     while (k < max_iter && rho > 0.0) {
         if (use_explicit)
@@ -448,6 +450,7 @@ int oracle_cg(int kernel, const oracle_term *terms, int n_terms, int use_explici
         for (int64_t i = 0; i < n; i++) { x[i] += alpha * p[i]; r[i] -= alpha * Ap[i]; rho1 += r[i] * r[i]; }
         k++;
         if (relres_hist) relres_hist[k] = sqrt(rho1) / ynorm;
+        if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[(int64_t)k * n + i] = x[i];
         if (rel_tol > 0 && sqrt(rho1) / ynorm <= rel_tol) { rho = rho1; break; }
         double beta = rho1 / rho;
         for (int64_t i = 0; i < n; i++) p[i] = r[i] + beta * p[i];
@@ -456,6 +459,136 @@ int oracle_cg(int kernel, const oracle_term *terms, int n_terms, int use_explici
     if (iters_out) *iters_out = k;
     free(r); free(p); free(Ap);
     return rc;
+}
+
+/* ------------------------------------------------------------------ O5b MINRES
+ * The paper's own solver: "This linear system can be solved iteratively, for example,
+ * with the minimal residual method"; "We used the
+ * scipy.sparse.linalg.minres method in the SciPy library".  This is the
+ * unpreconditioned Lanczos-based minimal-residual iteration of Paige & Saunders as
+ * SciPy states it, with zero shift and x0 = 0, step by step:
+ *   r1 = r2 = y, beta1 = ||y||, beta = beta1, oldb = 0, dbar = 0, epsln = 0,
+ *   phibar = beta1, cs = -1, sn = 0, w = w2 = 0
+ *   for k = 1..K:
+ *     v = r2 / beta;  z = (K + lambda I) v;  if k >= 2: z -= (beta / oldb) r1
+ *     alfa = v.z;  z -= (alfa / beta) r2;  r1 = r2;  r2 = z
+ *     oldb = beta;  beta = ||r2||
+ *     oldeps = epsln;  delta = cs dbar + sn alfa;  gbar = sn dbar - cs alfa
+ *     epsln = sn beta;  dbar = -cs beta
+ *     gamma = max(sqrt(gbar^2 + beta^2), eps);  cs = gbar / gamma;  sn = beta / gamma
+ *     phi = cs phibar;  phibar = sn phibar
+ *     w1 = w2;  w2 = w;  w = (v - oldeps w1 - delta w2) * (1 / gamma);  x += phi w
+ *   ||y - (K + lambda I) x_k|| = phibar_k (exact arithmetic), so phibar_k / ||y|| is the
+ *   residual history; it is non-increasing (|sn| <= 1).
+ * Stopping (readings M1-M2 in DESIGN.md): after max_iter iterations; when
+ * phibar / ||y|| <= rel_tol (rel_tol > 0); or on Lanczos breakdown beta <= 1e-14 ||y||
+ * (SPEC.md minres_solve: "beta underflow below 1e-14 -> return current iterate flagged
+ * converged"), which is a normal exit.  y = 0 gives x = 0 after 0 iterations.
+ * x_hist (nullable, (max_iter+1) x n) receives x_0 .. x_iters. */
+static int apply_op(int kernel, const oracle_term *terms, int n_terms, int use_explicit,
+                    const double *D, int64_t m, const double *T, int64_t q,
+                    const int32_t *f, const int32_t *s, int64_t n, const double *v, double lambda, double *out) {
+    int rc = use_explicit ? oracle_explicit_matvec(kernel, D, m, T, q, f, s, n, f, s, n, v, out)
+                          : oracle_gvt_matvec(terms, n_terms, D, m, T, q, f, s, n, f, s, n, v, 1, out, NULL);
+    if (rc) return rc;
+    for (int64_t i = 0; i < n; i++) out[i] += lambda * v[i];
+    return OR_OK;
+}
+
+int oracle_minres(int kernel, const oracle_term *terms, int n_terms, int use_explicit,
+                  const double *D, int64_t m, const double *T, int64_t q,
+                  const int32_t *f, const int32_t *s, int64_t n, const double *y,
+                  double lambda, int max_iter, double rel_tol,
+                  double *x, int *iters_out, double *relres_hist, double *x_hist) {
+    if (!(lambda >= 0) || max_iter < 0 || rel_tol < 0) return OR_E_PARAM;
+    size_t nb = sizeof(double) * (size_t)(n > 0 ? n : 1);
+    double *r1 = (double *)malloc(nb), *r2 = (double *)malloc(nb), *v = (double *)malloc(nb);
+    double *z = (double *)malloc(nb), *w = (double *)malloc(nb), *w2 = (double *)malloc(nb);
+    if (!r1 || !r2 || !v || !z || !w || !w2) {
+        free(r1); free(r2); free(v); free(z); free(w); free(w2);
+        return OR_E_OOM;
+    }
+    double beta1 = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        x[i] = 0.0; r1[i] = y[i]; r2[i] = y[i]; w[i] = 0.0; w2[i] = 0.0; beta1 += y[i] * y[i];
+    }
+    beta1 = sqrt(beta1);
+    if (relres_hist) relres_hist[0] = beta1 > 0 ? 1.0 : 0.0;
+    if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[i] = 0.0;
+    double beta = beta1, oldb = 0.0, dbar = 0.0, epsln = 0.0, phibar = beta1, cs = -1.0, sn = 0.0;
+    const double eps = 2.220446049250313e-16;
+    int k = 0, rc = OR_OK;
+    while (k < max_iter && beta1 > 0.0) {
+        for (int64_t i = 0; i < n; i++) v[i] = r2[i] / beta;
+        rc = apply_op(kernel, terms, n_terms, use_explicit, D, m, T, q, f, s, n, v, lambda, z);
+        if (rc) break;
+        if (k >= 1) for (int64_t i = 0; i < n; i++) z[i] -= (beta / oldb) * r1[i];
+        double alfa = 0.0;
+        for (int64_t i = 0; i < n; i++) alfa += v[i] * z[i];
+        double bnew = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            z[i] -= (alfa / beta) * r2[i];
+            r1[i] = r2[i];
+            r2[i] = z[i];
+            bnew += r2[i] * r2[i];
+        }
+        oldb = beta;
+        beta = sqrt(bnew);
+        double oldeps = epsln;
+        double delta = cs * dbar + sn * alfa;
+        double gbar = sn * dbar - cs * alfa;
+        epsln = sn * beta;
+        dbar = -cs * beta;
+        double gamma = sqrt(gbar * gbar + beta * beta);
+        if (gamma < eps) gamma = eps;
+        cs = gbar / gamma;
+        sn = beta / gamma;
+        double phi = cs * phibar;
+        phibar = sn * phibar;
+        double denom = 1.0 / gamma;
+        for (int64_t i = 0; i < n; i++) {
+            double wn = (v[i] - oldeps * w2[i] - delta * w[i]) * denom;  /* w2 = w_{k-2}, w = w_{k-1} */
+            w2[i] = w[i];
+            w[i] = wn;
+            x[i] += phi * wn;
+        }
+        k++;
+        if (relres_hist) relres_hist[k] = phibar / beta1;
+        if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[(int64_t)k * n + i] = x[i];
+        if (rel_tol > 0 && phibar / beta1 <= rel_tol) break;
+        if (beta <= 1e-14 * beta1 || phibar == 0.0) break;  /* Lanczos breakdown: converged */
+    }
+    if (iters_out) *iters_out = k;
+    free(r1); free(r2); free(v); free(z); free(w); free(w2);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ O8 AUC
+ * Validation AUC for early stopping ("until the AUC stops increasing
+ * in Z_validation"), by its definition as the Mann-Whitney statistic: the fraction of
+ * (positive, negative) pairs ranked correctly, ties counting one half:
+ *   AUC = (1 / (P N)) sum_{i: y_i > 0} sum_{j: y_j <= 0} ( [s_i > s_j] + [s_i == s_j] / 2 ).
+ * Positive means label > 0 (reading A1: 0/1 and -1/+1 labels both work).  P = 0 or
+ * N = 0 is undefined: OR_E_PARAM (SPEC.md fit_early_stopping: "degenerate validation
+ * labels").  Brute force O(P N), exact integer counting of the 2x-scaled numerator. */
+int oracle_auc(const double *labels, const double *scores, int64_t n, double *auc) {
+    int64_t P = 0, N = 0;
+    for (int64_t i = 0; i < n; i++) { if (labels[i] > 0) P++; else N++; }
+    if (P == 0 || N == 0) return OR_E_PARAM;
+    int64_t twice = 0;
+    #pragma omp parallel for reduction(+ : twice) schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        if (!(labels[i] > 0)) continue;
+        int64_t acc = 0;
+        for (int64_t j = 0; j < n; j++) {
+            if (labels[j] > 0) continue;
+            if (scores[i] > scores[j]) acc += 2;
+            else if (scores[i] == scores[j]) acc += 1;
+        }
+        twice += acc;
+    }
+    *auc = (double)twice / (2.0 * (double)P * (double)N);
+    return OR_OK;
 }
 
 /* ------------------------------------------------------------------ O7 integer plumbing

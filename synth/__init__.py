@@ -276,6 +276,28 @@ def tiny(seed: int, m: int = 5, q: int = 4, n: int = 12, n_out: int = 9, dim: in
                     _i32(of), _i32(os_), 1.0, 10, (KRONECKER,))
 
 
+def parity_grid(pattern: str, m: int, q: int, seed: int = 0, val_frac: float = 0.25):
+    """The paper's toy problems (Figure 1; SPEC.md generate_synthetic):
+    'chessboard' y(d,t) = parity(d) XOR parity(t), 'tablecloth' y(d,t) = 1 iff
+    parity(d) + parity(t) >= 1; features [1, parity] for drugs and targets (the constant
+    feature spans bias, marginals and interaction).  All m x q cells, randomly split
+    (seeded) into an inner training sample and a validation sample (Setting 1).
+    Returns (Workload with the linear base kernel, validation labels); labels are 0/1."""
+    if pattern not in ("chessboard", "tablecloth"):
+        raise ValueError(pattern)
+    rng = np.random.default_rng(40_000 + seed)
+    pd, pt = np.arange(m) % 2, np.arange(q) % 2
+    Xd = np.stack([np.ones(m), pd], 1)
+    Xt = np.stack([np.ones(q), pt], 1)
+    cells = rng.permutation(m * q)
+    d, t = cells // q, cells % q
+    lab = (pd[d] ^ pt[t]) if pattern == "chessboard" else ((pd[d] + pt[t]) >= 1).astype(np.int64)
+    n_val = int(round(val_frac * m * q))
+    w = Workload(f"{pattern}{m}x{q}", _f32(Xd), _f32(Xt), BASE_LINEAR, 1.0, _i32(d[n_val:]), _i32(t[n_val:]),
+                 _f32(lab[n_val:]), _i32(d[:n_val]), _i32(t[:n_val]), 1e-5, 100, (KRONECKER,))
+    return w, _f32(lab[:n_val])
+
+
 def random_vector(seed: int, n: int) -> np.ndarray:
     """Seeded N(0,1) float32 vector (the 'a' of a standalone matvec)."""
     return np.random.default_rng(20_000 + seed).standard_normal(n, dtype=np.float32)

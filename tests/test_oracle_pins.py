@@ -485,3 +485,150 @@ def test_sort_plan_matches_numpy_stable_sort(mode):
     ref = np.argsort(f, kind="stable") if mode == 0 else np.lexsort((np.arange(n), s, f))
     assert np.array_equal(perm, ref)
     assert np.array_equal(rp, np.searchsorted(np.sort(f), np.arange(m + 1), side="left"))
+
+
+# ----------------------------------------------------------------------------- MINRES (O5b)
+def _explicit_system(w, kernel=O.KRONECKER):
+    D = O.gram(w.base, w.Xd, gamma=w.gamma)
+    T = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma)
+    K = O.explicit_matrix(kernel, D, T, w.train_first, w.train_second, w.train_first, w.train_second)
+    return D, T, K
+
+
+def test_minres_scalar_systems():
+    """SPEC.md minres_solve examples: 2I -> y/2 in one iteration; y = 0 -> 0 after 0
+    iterations; K = I with lambda = 0 -> a = y; the single-pair ridge (1 + 1) a = 2."""
+    f, s = np.repeat(np.arange(3), 2), np.tile(np.arange(2), 3)
+    y = np.array([1.0, -2.0, 0.5, 4.0, 3.0, -1.0])
+    kron = O.kernel_terms(O.KRONECKER)
+    x, it, hist, rc = O.minres(kron, np.eye(3), np.eye(2), f, s, y, 1.0, 5)
+    assert rc == O.OK and it == 1 and np.allclose(x, y / 2, atol=1e-15) and hist[-1] <= 1e-15
+    x, it, hist, rc = O.minres(kron, np.eye(3), np.eye(2), f, s, np.zeros(6), 1.0, 5)
+    assert it == 0 and np.all(x == 0)
+    x, it, _, _ = O.minres(kron, np.eye(3), np.eye(2), f, s, y, 0.0, 5)
+    assert np.allclose(x, y, atol=1e-15)
+    r = SPEC["ridge_single_pair"]
+    x, it, _, rc = O.minres(kron, [[r["D"]]], [[r["T"]]], [0], [0], [r["y"]], r["lambda"], 3)
+    assert x[0] == pytest.approx(r["a"], abs=1e-15)
+
+
+def test_minres_iterates_match_scipy_minres():
+    """The paper ran scipy.sparse.linalg.minres: the oracle's iterates x_k equal
+    SciPy's (same x0 = 0, no preconditioner) on the explicit C1 system up to rounding.  The two
+    sum in different orders and Lanczos amplifies that (measured: 2e-15 at k = 1, 1e-9 at k = 12,
+    2e-5 at k = 16, back to 1e-14 by k = 23, 1e-9 at k = 30 -- the same spread appears between
+    the oracle's own explicit and GVT operators), so iterates are compared for k <= 12 at 1e-8
+    and at k = 30 at 1e-7."""
+    from scipy.sparse.linalg import minres as sp_minres
+    w = synth.config1()
+    D, T, K = _explicit_system(w)
+    A = K + w.lam * np.eye(w.n)
+    y = w.y.astype(np.float64)
+    ref = []
+    sp_minres(A, y, rtol=0.0, maxiter=30, callback=lambda xk: ref.append(xk.copy()))
+    x, it, hist, rc, xh = O.minres(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, 30,
+                                   history=True)
+    assert it == 30 and len(ref) == 30
+    for k in range(1, 13):
+        assert rel(xh[k], ref[k - 1]) < 1e-8, k
+    assert rel(xh[30], ref[29]) < 1e-7
+
+
+def test_minres_krylov_minimality_and_residual_estimate():
+    """MINRES's defining property: x_k minimises ||y - A x|| over the Krylov space
+    K_k(A, y) = span{y, Ay, ..., A^{k-1} y}.  Checked against numpy lstsq over an explicit
+    orthonormal Krylov basis on a seeded 40-pair instance (all 9 kernels' K are symmetric);
+    the recursive estimate phibar_k / ||y|| equals the true relative residual."""
+    for kernel in (O.KRONECKER, O.SYMMETRIC, O.MLPK, O.POLY2D):
+        hom = kernel in HOM
+        w = synth.tiny(7, m=6, q=5, n=40, homogeneous=hom, duplicates=False)
+        D, T, K = _explicit_system(w, kernel)
+        A = K + 0.3 * np.eye(w.n)
+        y = w.y.astype(np.float64)
+        x, it, hist, rc, xh = O.minres(None, D, T, w.train_first, w.train_second, y, 0.3, 12, kernel=kernel,
+                                       explicit=True, history=True)
+        V = np.zeros((w.n, 0))
+        b = y.copy()
+        for k in range(1, it + 1):
+            b = b / np.linalg.norm(b)
+            v = b - V @ (V.T @ b)
+            v -= V @ (V.T @ v)
+            V = np.hstack([V, (v / np.linalg.norm(v))[:, None]])
+            c, *_ = np.linalg.lstsq(A @ V, y, rcond=None)
+            rmin = np.linalg.norm(y - A @ V @ c)
+            rk = np.linalg.norm(y - A @ xh[k])
+            assert rk == pytest.approx(rmin, rel=1e-7, abs=1e-12 * np.linalg.norm(y)), (kernel, k)
+            assert hist[k] == pytest.approx(rk / np.linalg.norm(y), rel=1e-7, abs=1e-13), (kernel, k)
+            b = A @ b
+
+
+def test_minres_converges_monotone_on_C1_and_large_lambda_limit():
+    """On C1 the relative residual history is non-increasing (SPEC.md: 'residual_history is
+    non-increasing', 1e-12 slack) and 50 iterations reach the dense direct solve; with
+    lambda = 1e6, a -> y / lambda (SPEC regularization limit, 1e-3)."""
+    w = synth.config1()
+    D, T, K = _explicit_system(w)
+    kron = O.kernel_terms(O.KRONECKER)
+    x, it, hist, rc = O.minres(kron, D, T, w.train_first, w.train_second, w.y, w.lam, 50)
+    assert rc == O.OK and it == 50
+    assert all(hist[k + 1] <= hist[k] * (1 + 1e-12) for k in range(len(hist) - 1))
+    xs = np.linalg.solve(K + w.lam * np.eye(w.n), w.y.astype(np.float64))
+    assert rel(x, xs) < 1e-10
+    x, _, _, _ = O.minres(kron, D, T, w.train_first, w.train_second, w.y, 1e6, 10)
+    assert rel(x, w.y / 1e6) < 1e-3
+
+
+# ----------------------------------------------------------------------------- AUC (O8) and early stopping
+def test_auc_matches_sklearn_with_ties():
+    """AUC by definition equals sklearn.metrics.roc_auc_score (a library routine) on seeded
+    inputs with heavy ties, for 0/1 and -1/+1 labels."""
+    from sklearn.metrics import roc_auc_score
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        n = int(rng.integers(2, 300))
+        lab = rng.integers(0, 2, n)
+        lab[0], lab[-1] = 0, 1
+        sc = np.round(rng.standard_normal(n), 1) if trial % 2 else rng.standard_normal(n)
+        assert O.auc(lab, sc) == pytest.approx(roc_auc_score(lab, sc), abs=1e-15)
+        assert O.auc(2 * lab - 1, sc) == pytest.approx(roc_auc_score(lab, sc), abs=1e-15)
+
+
+def test_auc_invariants_and_errors():
+    """SPEC.md invariants: invariant under a strictly increasing transform; auc(s) + auc(-s) = 1
+    without ties; all-tied scores give 1/2; a single-class label set is an error."""
+    rng = np.random.default_rng(6)
+    lab = rng.integers(0, 2, 200)
+    sc = rng.standard_normal(200)
+    a = O.auc(lab, sc)
+    assert O.auc(lab, np.exp(3 * sc) + 7) == a
+    assert a + O.auc(lab, -sc) == pytest.approx(1.0, abs=1e-15)
+    assert O.auc(lab, np.zeros(200)) == 0.5
+    assert O.auc([1, 0], [0.2, 0.1]) == 1.0 and O.auc([1, 0], [0.1, 0.2]) == 0.0
+    with pytest.raises(O.OracleError):
+        O.auc([1, 1, 1], [0.1, 0.2, 0.3])
+
+
+def test_early_stop_rule_spec_examples():
+    """SPEC.md fit_early_stopping examples: strictly increasing for 5 iterations then flat,
+    patience 3 -> best 5 (stop at 8); constant from iteration 1, patience 2 -> best 1, stop at 3."""
+    assert O.early_stop_rule([.5, .6, .7, .8, .9, .9, .9, .9, .9, .9], 3)[:4] == (5, .9, 8, True)
+    assert O.early_stop_rule([.7] * 6, 2) == (1, .7, 3, True)
+    assert O.early_stop_rule([.1, .2], 5) == (2, .2, 2, False)
+
+
+def test_fit_early_stopping_chessboard():
+    """SPEC.md: chessboard 12x12, Kronecker, lambda = 1e-5, patience 10 stops in far fewer
+    iterations than n (observed <= n/4); the XOR is learnable by the Kronecker kernel (PAPER.md
+    Figure 1 caption), so the best validation AUC is 1 and a_best's validation scores give it."""
+    w, vlab = synth.parity_grid("chessboard", 12, 12, seed=0)
+    D = O.gram(O.BASE_LINEAR, w.Xd)
+    T = O.gram(O.BASE_LINEAR, w.Xt)
+    kron = O.kernel_terms(O.KRONECKER)
+    for solver in ("minres", "cg"):
+        best, best_auc, iters, hist, a = O.fit_early_stopping(kron, D, T, w.train_first, w.train_second, w.y,
+                                                              w.test_first, w.test_second, vlab, 1e-5, 10, w.n,
+                                                              solver)
+        assert iters <= w.n // 4, (solver, iters)
+        assert best_auc == 1.0 and hist[best - 1] == 1.0
+        sc = O.gvt_matvec(kron, D, T, w.test_first, w.test_second, w.train_first, w.train_second, a)
+        assert O.auc(vlab, sc) == best_auc

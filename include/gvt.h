@@ -101,9 +101,18 @@ typedef enum {
                                     exactly as the data-parallel path does across ranks (default 1) */
     GVT_OPT_GEMM_CTA = 6,        /* tensor-core GEMM: 2 = CTA pair with tcgen05 cta_group::2 (256-row
                                     tiles, default), 1 = single-CTA 128-row tiles                  */
-    GVT_OPT_GRAPHS = 7           /* 1 (default): fixed-iteration CG replays one captured iteration as
-                                    a CUDA graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches */
+    GVT_OPT_GRAPHS = 7,          /* 1 (default): the solver replays one captured iteration as a CUDA
+                                    graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches        */
+    GVT_OPT_SOLVER = 8           /* iterative solver of pairwise_krr_fit(_early_stopping): gvt_solver,
+                                    default GVT_SOLVER_CG                                             */
 } gvt_option;
+
+/* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the
+ * paper's own solver ("the minimal residual method"; SciPy's minres,
+ * PAPER.md:850), unpreconditioned Paige-Saunders recurrences from a = 0; its residual history
+ * ||r_k|| / ||y|| (the recurrence's phibar_k) is non-increasing.  Both keep fp32 vectors and fp64
+ * scalars on the device. */
+typedef enum { GVT_SOLVER_CG = 0, GVT_SOLVER_MINRES = 1 } gvt_solver;
 
 /* Per-context counters (gvt_get_stats). */
 #define GVT_MAX_KERNEL_KINDS 32
@@ -174,17 +183,49 @@ gvt_status gvt_matvec(gvt_ctx *ctx, const float *D, int64_t m, const float *T, i
                       const float *a, const gvt_term *terms, int n_terms, float *u);
 
 /* Kernel ridge regression (K + lambda I) a = y by conjugate
- * gradients from a = 0 (reading S12-S14): max_iter iterations (rel_tol = 0) or until
- * ||r_k|| / ||y|| <= rel_tol.  Each iteration is one GVT matvec.  CG scalars are fp64.
+ * gradients (default) or MINRES (GVT_OPT_SOLVER) from a = 0 (readings S12-S14, M1-M2):
+ * max_iter iterations (rel_tol = 0) or until ||r_k|| / ||y|| <= rel_tol (MINRES also stops
+ * on Lanczos breakdown, beta_{k+1} <= 64 u ||T_k||_F, u = 2^-24, a converged exit).  Each iteration is one GVT
+ * matvec.  Solver scalars are fp64.
  * iters_out (host, nullable) = iterations done; relres_hist (host, nullable,
  * max_iter + 1 doubles) = ||r_k|| / ||y|| for k = 0..iters.  y == 0 gives a = 0 after 0
- * iterations.  Breakdown (p^T A p <= 0) returns GVT_E_BREAKDOWN with the current iterate
+ * iterations.  CG breakdown (p^T A p <= 0) returns GVT_E_BREAKDOWN with the current iterate
  * in a_out. */
 gvt_status pairwise_krr_fit(gvt_ctx *ctx, const float *D, int64_t m, const float *T, int64_t q,
                             const int32_t *in_first, const int32_t *in_second, int64_t n,
                             const float *y, const gvt_term *terms, int n_terms, double lambda,
                             int max_iter, double rel_tol, float *a_out, int *iters_out,
                             double *relres_hist);
+
+/* Early-stopping ridge regression ("running the minimum residual algorithm
+ * on Z_inner until the AUC stops increasing in Z_validation for a given number of iterations";
+ * SPEC.md fit_early_stopping).  Runs the GVT_OPT_SOLVER solver (lambda as given, x0 = 0) on
+ * the inner pairs (inner_first/second, n, labels y); after every iteration k it scores the
+ * validation pairs with the iterate a_k (scores = K_val,inner a_k) and takes their AUC against
+ * val_labels (positive iff label > 0; Mann-Whitney, ties count 1/2).  It stops after
+ * `patience` consecutive iterations without strict AUC improvement, at max_iter, or when the
+ * solver converges/breaks down.  Outputs: a_out (n floats) = the weights of the best
+ * iteration (all zero if none); best_iter (host, nullable) = the earliest iteration with the
+ * highest AUC; best_auc (host, nullable); iters_run (host, nullable) = iterations performed;
+ * auc_hist (host, nullable, max_iter doubles) = AUC after iteration k at [k - 1], NaN past
+ * iters_run.  The validation scores share each iteration's stage 1 with the training matvec
+ * (the out sample is [inner; validation]).  Multi-GPU: every rank passes its shard of the
+ * inner pairs (as pairwise_krr_fit) and of the validation pairs; the AUC is over all ranks'
+ * validation pairs and the outputs are identical on every rank.  Errors: GVT_E_PARAM for
+ * patience < 1 or validation labels of a single class; otherwise as pairwise_krr_fit. */
+gvt_status pairwise_krr_fit_early_stopping(gvt_ctx *ctx, const float *D, int64_t m, const float *T, int64_t q,
+                                           const int32_t *inner_first, const int32_t *inner_second, int64_t n,
+                                           const float *y, const int32_t *val_first, const int32_t *val_second,
+                                           int64_t n_val, const float *val_labels, const gvt_term *terms,
+                                           int n_terms, double lambda, int patience, int max_iter, float *a_out,
+                                           int *best_iter, double *best_auc, int *iters_run, double *auc_hist);
+
+/* AUC of scores[n] against labels[n] (positive iff label > 0): the Mann-Whitney statistic,
+ * fraction of (positive, negative) pairs with the positive scored higher, ties counting 1/2
+ * (the validation criterion of PAPER.md:852-856).  Computed on the device by a radix sort and
+ * exact integer counting, so it is exact for the given fp32 scores.  *auc (host).  Errors:
+ * GVT_E_PARAM if either class is empty. */
+gvt_status gvt_auc(gvt_ctx *ctx, const float *labels, const float *scores, int64_t n, double *auc);
 
 /* Prediction v = R(test) K R(train)^T a: scores[i] for test pair i,
  * caller order. */

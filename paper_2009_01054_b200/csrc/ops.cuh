@@ -137,6 +137,35 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
 // multi-GPU hook: reduce a partial-sum vector across ranks (no-op at world 1)
 void allreduce_partials(gvt_ctx *c, double *partials, int count);
 
+// ---- MINRES and early stopping (solver.cu)
+constexpr int MINRES_STATE_N = 19;  // device state doubles before the relres history
+void minres_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r1, float *r2, float *v, float *W1,
+                 float *W2, double *state, double rel_tol);
+// u = K v on entry (the matvec's first n entries); Lanczos step + rotations
+void minres_step(gvt_ctx *c, float *u, float *v, float *r1, float *r2, float *W1, float *W2, float *x, int64_t n,
+                 double lambda, double *state);
+void minres_update(gvt_ctx *c, float *v, float *W1, float *W2, float *x, const float *r2, int64_t n, double *state,
+                   float *kv, float *KW1, float *KW2, float *s, int64_t n_val);
+
+struct AucPlan {
+    int64_t n = 0;
+    double P = 0, N = 0;  // positives / negatives
+    uint8_t *pos = nullptr, *pos_sorted = nullptr;
+    float *keys_sorted = nullptr;
+    long long *negpre = nullptr;        // n + 1: negatives among the first i sorted scores
+    unsigned long long *twice = nullptr;  // doubled Mann-Whitney numerator (+ scratch)
+    void *temp = nullptr;
+    size_t temp_bytes = 0;
+    void setup(gvt_ctx *c, const char *tag, const float *labels_dev, int64_t n);
+    void count(gvt_ctx *c, const float *scores, const double *st, const double *es);
+};
+double auc(gvt_ctx *c, const float *labels, const float *scores, int64_t n);
+constexpr int ES_STATE_N = 5;
+void es_init(gvt_ctx *c, double *es, double *hist, int max_iter, AucPlan &a);
+void es_cg_scores(gvt_ctx *c, float *s, const float *kp, int64_t n_val, const double *state);
+void es_evaluate(gvt_ctx *c, AucPlan &a, const float *scores_full, double *state, double *es, double *hist,
+                 int patience, const float *x, float *a_best, int64_t n);
+
 // partial-sum layout (cg.cu)
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
 constexpr int RED_THREADS = 256;

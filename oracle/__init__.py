@@ -80,6 +80,8 @@ def lib():
         L.oracle_cg.argtypes = [i32, P, i32, i32, P, i64, P, i64, P, P, i64, P, dbl, i32, dbl, P, P, P, P]
         L.oracle_minres.argtypes = [i32, P, i32, i32, P, i64, P, i64, P, P, i64, P, dbl, i32, dbl, P, P, P, P]
         L.oracle_auc.argtypes = [P, P, i64, P]
+        L.oracle_explicit_rect_matvec.argtypes = [i32, P, i64, i64, P, i64, i64, P, P, i64, P, P, i64, P, P]
+        L.oracle_gvt_rect.argtypes = [P, i64, i64, P, i64, i64, P, P, i64, P, P, i64, P, i32, P, P, P]
         L.oracle_sort_plan.argtypes = [P, P, i64, i64, i64, i32, P, P]
         L.oracle_num_threads.restype = i32
         _lib = L
@@ -267,6 +269,31 @@ def fit_early_stopping(terms, D, T, f, s, y, vf, vs, vlab, lam, patience, max_it
     best_it, best_auc, _, _ = early_stop_rule(aucs, patience)
     a_best = xh[best_it] if best_it > 0 else np.zeros(len(f))
     return best_it, best_auc, len(aucs), np.array(aucs), a_best
+
+
+def explicit_rect_matvec(kernel, Dx, Tx, of, os_, inf, ins, a):
+    """u_i = sum_j k(out_i, in_j) a_j on rectangular cross-Grams (O9): Dx (m_out x m_in),
+    Tx (q_out x q_in) or None (homogeneous); out ids index rows, in ids columns."""
+    Dx, Tx, a = _d(Dx), _d(Tx), _d(a)
+    of, os_, inf, ins = _i(of), _i(os_), _i(inf), _i(ins)
+    u = np.empty(len(of), dtype=np.float64)
+    qo, qi = (0, 0) if Tx is None else Tx.shape
+    _check(lib().oracle_explicit_rect_matvec(kernel, _p(Dx), Dx.shape[0], Dx.shape[1], _p(Tx), qo, qi, _p(of),
+                                             _p(os_), len(of), _p(inf), _p(ins), len(inf), _p(a), _p(u)),
+           "explicit_rect_matvec")
+    return u
+
+
+def gvt_rect(A, B, of, os_, inf, ins, a, variant=0):
+    """SPEC GvtProblem matvec with rectangular factors (O9): returns (u, variant_used, op_count)."""
+    A, B, a = _d(A), _d(B), _d(a)
+    of, os_, inf, ins = _i(of), _i(os_), _i(inf), _i(ins)
+    u = np.zeros(len(of), dtype=np.float64)
+    v, ops = ctypes.c_int(0), ctypes.c_int64(0)
+    _check(lib().oracle_gvt_rect(_p(A), A.shape[0], A.shape[1], _p(B), B.shape[0], B.shape[1], _p(of), _p(os_),
+                                 len(of), _p(inf), _p(ins), len(inf), _p(a), int(variant), _p(u), ctypes.byref(v),
+                                 ctypes.byref(ops)), "gvt_rect")
+    return u, v.value, ops.value
 
 
 def sort_plan(first, second, m, q, mode=0):

@@ -98,10 +98,14 @@ int oracle_gram(int base, const double *X, int64_t m, const double *Y, int64_t m
  * i.e. (I-P)(D (x) D) (S3); Cartesian delta over global ids (S19). */
 static inline double Dv(const double *D, int64_t m, int32_t a, int32_t b) { return D[(int64_t)a * m + b]; }
 
-double oracle_kernel_value(int kernel, const double *D, int64_t m, const double *T, int64_t q,
-                           int32_t d, int32_t t, int32_t db, int32_t tb) {
+/* Table 4b with every base-kernel lookup written as G[out element][in element]: D / T are
+ * row-major with leading dimensions ldd / ldt (square Grams over global ids: ldd = m,
+ * ldt = q; rectangular cross-Grams of novel objects, O9: ldd = m_in, ldt = q_in). */
+static double kernel_value_ld(int kernel, const double *D, int64_t ldd, const double *T, int64_t ldt,
+                              int32_t d, int32_t t, int32_t db, int32_t tb) {
     const double *TT = T ? T : D;
-    int64_t qq = T ? q : m;
+    int64_t qq = T ? ldt : ldd;
+    int64_t m = ldd;
     switch (kernel) {
     case OR_LINEAR:   return Dv(D, m, d, db) + Dv(TT, qq, t, tb);
     case OR_POLY2D: { double s = Dv(D, m, d, db) + Dv(TT, qq, t, tb); return s * s; }
@@ -121,6 +125,11 @@ double oracle_kernel_value(int kernel, const double *D, int64_t m, const double 
         return Dv(D, m, d, db) * (t == tb ? 1.0 : 0.0) + (d == db ? 1.0 : 0.0) * Dv(TT, qq, t, tb);
     default: return NAN;
     }
+}
+
+double oracle_kernel_value(int kernel, const double *D, int64_t m, const double *T, int64_t q,
+                           int32_t d, int32_t t, int32_t db, int32_t tb) {
+    return kernel_value_ld(kernel, D, m, T, q, d, t, db, tb);
 }
 
 static int is_homogeneous_kernel(int kernel) {
@@ -592,6 +601,86 @@ int oracle_auc(const double *labels, const double *scores, int64_t n, double *au
         twice += acc;
     }
     *auc = (double)twice / (2.0 * (double)P * (double)N);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ O9 novel objects
+ * Prediction for pairs whose objects were not in the training sample (Settings 2-4,
+ * PAPER.md:162-169): the out pairs index the ROWS and the in pairs the COLUMNS of
+ * rectangular cross-Grams, D_x[o][i] = k(test object o, training object i) (m_out x m_in)
+ * and T_x (q_out x q_in); homogeneous kernels use one cross-Gram (T_x == NULL) for both pair
+ * elements.  The Cartesian kernel's Identity factor compares objects across the two tables,
+ * which have no common ids here: rejected (OR_E_KERNEL; reading N1).
+ * oracle_explicit_rect_matvec: the definition u_i = sum_j k(out_i, in_j) a_j with Table 4b
+ * evaluated on the cross-Grams (every lookup is [out element][in element]). */
+static int check_rect(const int32_t *f, const int32_t *s, int64_t n, int64_t bf, int64_t bs) {
+    if (n < 0) return OR_E_DIM;
+    if (!check_ids(f, n, bf) || !check_ids(s, n, bs)) return OR_E_INDEX;
+    return OR_OK;
+}
+
+int oracle_explicit_rect_matvec(int kernel, const double *Dx, int64_t m_out, int64_t m_in,
+                                const double *Tx, int64_t q_out, int64_t q_in,
+                                const int32_t *of, const int32_t *os, int64_t n_out,
+                                const int32_t *inf, const int32_t *ins, int64_t n_in,
+                                const double *a, double *u) {
+    if (kernel < 0 || kernel >= OR_NKERNELS || kernel == OR_CARTESIAN) return OR_E_KERNEL;
+    if (is_homogeneous_kernel(kernel) && Tx) return OR_E_HOMOGENEOUS;
+    int64_t qo = Tx ? q_out : m_out, qi = Tx ? q_in : m_in;
+    int rc;
+    if ((rc = check_rect(of, os, n_out, m_out, qo)) || (rc = check_rect(inf, ins, n_in, m_in, qi))) return rc;
+    #pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t i = 0; i < n_out; i++) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < n_in; j++)
+            acc += kernel_value_ld(kernel, Dx, m_in, Tx, q_in, of[i], os[i], inf[j], ins[j]) * a[j];
+        u[i] = acc;
+    }
+    return OR_OK;
+}
+
+/* The GVT of one rectangular Kronecker product (SPEC.md:95-131 GvtProblem / gvt_cost /
+ * gvt_matvec / gvt_op_count; Theorem 1):
+ *   u[i] = sum_j A[of_i, if_j] B[os_i, is_j] a_j,   A: m_out x m_in,  B: q_out x q_in.
+ * Variant 1: W[t][h] = sum_{j: if_j = h} B[t, is_j] a_j  (q_out x m_in, ascending j);
+ *            u_i = sum_h A[of_i, h] W[os_i, h]           (ascending h).
+ * Variant 2: the roles of A and B swapped:
+ *            W'[d][g] = sum_{j: is_j = g} A[d, if_j] a_j (m_out x q_in);
+ *            u_i = sum_g B[os_i, g] W'[of_i, g].
+ * variant 0 = auto: the smaller of cost1 = q_out n_in + m_in n_out and
+ * cost2 = m_out n_in + q_in n_out, ties -> variant 1 (reading S2); *op_count = the chosen
+ * variant's cost and *variant_used the variant. */
+int oracle_gvt_rect(const double *A, int64_t m_out, int64_t m_in, const double *B, int64_t q_out, int64_t q_in,
+                    const int32_t *of, const int32_t *os, int64_t n_out,
+                    const int32_t *inf, const int32_t *ins, int64_t n_in,
+                    const double *a, int variant, double *u, int *variant_used, int64_t *op_count) {
+    int rc;
+    if ((rc = check_rect(of, os, n_out, m_out, q_out)) || (rc = check_rect(inf, ins, n_in, m_in, q_in))) return rc;
+    if (variant < 0 || variant > 2) return OR_E_PARAM;
+    int64_t c1 = q_out * n_in + m_in * n_out, c2 = m_out * n_in + q_in * n_out;
+    int v = variant ? variant : (c2 < c1 ? 2 : 1);
+    /* variant 2 = variant 1 on the transposed problem (B, A) with the pair elements swapped */
+    const double *F2 = v == 1 ? A : B, *F1 = v == 1 ? B : A;
+    int64_t r2 = v == 1 ? m_out : q_out, k2 = v == 1 ? m_in : q_in;   /* stage-2 factor dims */
+    int64_t r1 = v == 1 ? q_out : m_out, k1 = v == 1 ? q_in : m_in;   /* stage-1 factor dims */
+    const int32_t *o2 = v == 1 ? of : os, *o1 = v == 1 ? os : of;     /* out element per stage */
+    const int32_t *i2 = v == 1 ? inf : ins, *i1 = v == 1 ? ins : inf; /* in element per stage */
+    (void)r2;
+    double *W = (double *)calloc((size_t)(r1 * k2 > 0 ? r1 * k2 : 1), sizeof(double));
+    if (!W) return OR_E_OOM;
+    #pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < r1; t++)
+        for (int64_t j = 0; j < n_in; j++)
+            W[t * k2 + i2[j]] += F1[t * k1 + i1[j]] * a[j];
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_out; i++) {
+        double acc = 0.0;
+        for (int64_t h = 0; h < k2; h++) acc += F2[(int64_t)o2[i] * k2 + h] * W[(int64_t)o1[i] * k2 + h];
+        u[i] = acc;
+    }
+    free(W);
+    if (variant_used) *variant_used = v;
+    if (op_count) *op_count = v == 1 ? c1 : c2;
     return OR_OK;
 }
 

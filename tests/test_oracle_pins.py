@@ -632,3 +632,85 @@ def test_fit_early_stopping_chessboard():
         assert best_auc == 1.0 and hist[best - 1] == 1.0
         sc = O.gvt_matvec(kron, D, T, w.test_first, w.test_second, w.train_first, w.train_second, a)
         assert O.auc(vlab, sc) == best_auc
+
+
+# ----------------------------------------------------------------------------- novel objects (O9)
+def test_gvt_rect_spec_examples():
+    """SPEC.md gvt_matvec / gvt_cost / gvt_op_count examples on the rectangular GvtProblem."""
+    u, v, ops = O.gvt_rect([[2.0]], [[3.0]], [0], [0], [0], [0], [1.0])
+    assert u[0] == 6.0 and v == 1 and ops == 2
+    f, s = [0, 0, 1, 1], [0, 1, 0, 1]
+    vec = np.array([0.3, -1.2, 2.5, 0.7])
+    for var in (1, 2):
+        u, _, _ = O.gvt_rect(np.eye(2), np.eye(2), f, s, f, s, vec, var)
+        assert np.array_equal(u, vec)
+    # (n_out=3, m_out=2, q_out=2, n_in=4, m_in=3, q_in=2): cost1 = 17, cost2 = 14
+    rng = np.random.default_rng(1)
+    A, B = rng.uniform(size=(2, 3)), rng.uniform(size=(2, 2))
+    of, os_ = [0, 1, 1], [1, 0, 1]
+    inf, ins = [0, 2, 1, 2], [1, 1, 0, 0]
+    a = rng.standard_normal(4)
+    u0, v0, ops0 = O.gvt_rect(A, B, of, os_, inf, ins, a, 0)
+    u1, v1, ops1 = O.gvt_rect(A, B, of, os_, inf, ins, a, 1)
+    assert (v0, ops0, v1, ops1) == (2, 14, 1, 17)
+    assert rel(u0, u1) < 1e-14
+
+
+def test_gvt_rect_equals_brute_force():
+    """200 seeded rectangular instances (m_out != m_in, q_out != q_in, duplicates): both variants
+    and auto equal the brute-force sum u_i = sum_j A[of_i, if_j] B[os_i, is_j] a_j (numpy fancy
+    indexing) within 1e-12."""
+    for seed in range(200):
+        rng = np.random.default_rng(500 + seed)
+        mo, mi, qo, qi = rng.integers(1, 8, 4)
+        no, ni = rng.integers(0, 20, 2)
+        A, B = rng.standard_normal((mo, mi)), rng.standard_normal((qo, qi))
+        of, os_ = rng.integers(0, mo, no), rng.integers(0, qo, no)
+        inf, ins = rng.integers(0, mi, ni), rng.integers(0, qi, ni)
+        a = rng.standard_normal(ni)
+        ref = (A[of][:, inf] * B[os_][:, ins]) @ a if no and ni else np.zeros(no)
+        for var in (0, 1, 2):
+            u, _, _ = O.gvt_rect(A, B, of, os_, inf, ins, a, var)
+            assert rel(u, ref) < 1e-12, (seed, var)
+
+
+def test_gvt_rect_roth_vec_trick():
+    """Complete out and in grids: u = vec(A V B^T) (Roth's column lemma) with
+    rectangular A (5 x 7) and B (4 x 3), checked against numpy matmul."""
+    rng = np.random.default_rng(3)
+    A, B = rng.standard_normal((5, 7)), rng.standard_normal((4, 3))
+    V = rng.standard_normal((7, 3))
+    inf, ins = np.repeat(np.arange(7), 3), np.tile(np.arange(3), 7)
+    of, os_ = np.repeat(np.arange(5), 4), np.tile(np.arange(4), 5)
+    for var in (1, 2):
+        u, _, _ = O.gvt_rect(A, B, of, os_, inf, ins, V.reshape(-1), var)
+        assert rel(u, (A @ V @ B.T).reshape(-1)) < 1e-13
+
+
+@pytest.mark.parametrize("kernel", [k for k in K_ALL if k != O.CARTESIAN])
+def test_explicit_rect_equals_union_gram_subblock(kernel):
+    """Novel objects as a sub-block: with the training objects and the test objects stacked into
+    one table, the cross-Gram is a sub-block of the union Gram, so the rectangular definition
+    must equal the (pinned) square definition over global ids -- for every kernel but Cartesian
+    (which the rectangular form rejects, reading N1)."""
+    hom = kernel in HOM
+    rng = np.random.default_rng(40 + kernel)
+    Xd_tr, Xd_te = rng.standard_normal((6, 3)), rng.standard_normal((4, 3))
+    Xt_tr, Xt_te = rng.standard_normal((5, 3)), rng.standard_normal((3, 3))
+    Du = O.gram(O.BASE_GAUSSIAN, np.vstack([Xd_tr, Xd_te]), gamma=0.4)
+    Tu = None if hom else O.gram(O.BASE_GAUSSIAN, np.vstack([Xt_tr, Xt_te]), gamma=0.4)
+    mi, mo = 6, 4
+    qi, qo = (6, 4) if hom else (5, 3)
+    Dx = Du[mi:, :mi]
+    Tx = None if hom else Tu[qi:, :qi]
+    n_in, n_out = 30, 17
+    inf, ins = rng.integers(0, mi, n_in), rng.integers(0, qi, n_in)
+    of, os_ = rng.integers(0, mo, n_out), rng.integers(0, qo, n_out)
+    a = rng.standard_normal(n_in)
+    u = O.explicit_rect_matvec(kernel, Dx, Tx, of, os_, inf, ins, a)
+    ref = O.explicit_matvec(kernel, Du, Tu, of + mi, os_ + qi, inf, ins, a)
+    assert rel(u, ref) < 1e-13
+    with pytest.raises(O.OracleError) as e:
+        O.explicit_rect_matvec(O.CARTESIAN, Dx, Tu[qi:, :qi] if Tu is not None else np.ones((qo, qi)), of, os_,
+                               inf, ins, a)
+    assert e.value.code == O.E_KERNEL

@@ -171,6 +171,13 @@ gvt_status gvt_kernel_terms(gvt_kernel kernel, gvt_term *out, int *n_terms);
 gvt_status gvt_gram(gvt_ctx *ctx, gvt_base kind, const float *X, int64_t m, int64_t dim,
                     double gamma, double coef0, int degree, float *K);
 
+/* Cross-Gram K[i][j] = k(X_i, Y_j), X (m x dim), Y (m2 x dim), K (m x m2): the base kernel
+ * between two object tables, e.g. novel test objects (rows) against the training objects
+ * (columns) for pairwise_predict_rect.  Same kernels and errors as
+ * gvt_gram; no diagonal is forced (the tables are different objects). */
+gvt_status gvt_gram_cross(gvt_ctx *ctx, gvt_base kind, const float *X, int64_t m, const float *Y, int64_t m2,
+                          int64_t dim, double gamma, double coef0, int degree, float *K);
+
 /* GVT matvec (Theorem 1; Corollary PAPER.md:634-653):
  *   u[i] = sum_j sum_terms coef * L[.,.] * R[.,.] * a[j]
  * over out pairs (out_first[i], out_second[i]), i < n_out, and in pairs
@@ -233,6 +240,36 @@ gvt_status pairwise_predict(gvt_ctx *ctx, const float *D, int64_t m, const float
                             const int32_t *test_first, const int32_t *test_second, int64_t n_test,
                             const int32_t *train_first, const int32_t *train_second, int64_t n_train,
                             const float *a, const gvt_term *terms, int n_terms, float *scores);
+
+/* Novel objects (Settings 2-4): the GVT matvec on rectangular cross-Grams.
+ *   u[i] = sum_j k(out_i, in_j) a[j],  k from Table 4b with every base-kernel value taken from a
+ *   cross-Gram Dx[out object][in object] (m_out x m_in, row-major) or Tx (q_out x q_in);
+ *   Tx == NULL means homogeneous objects (one cross-Gram, q_out = m_out, q_in = m_in).
+ * Out ids index the ROWS (out_first < m_out, out_second < q_out), in ids the COLUMNS
+ * (in_first < m_in, in_second < q_in); the cross-Grams need not be symmetric or square.
+ * `terms` is any term list without Identity factors (the Cartesian kernel compares objects
+ * across the two tables, which share no ids: GVT_E_KERNEL, reading N1).
+ * variant (Theorem 1; SPEC.md gvt_cost): 1 = stage 1 over the second
+ * factor, cost q_out n_in + m_in n_out; 2 = the roles of the two factors swapped, cost
+ * m_out n_in + q_in n_out (Kronecker term list only); 0 = auto, the smaller cost, ties -> 1.
+ * variant_used / op_count (host, nullable): the variant run and its cost (-1 for non-Kronecker
+ * lists, which run variant 1).  No lambda.  Errors: GVT_E_INDEX for ids out of range,
+ * GVT_E_PARAM for a bad variant. */
+gvt_status gvt_matvec_rect(gvt_ctx *ctx, const float *Dx, int64_t m_out, int64_t m_in, const float *Tx,
+                           int64_t q_out, int64_t q_in, const int32_t *out_first, const int32_t *out_second,
+                           int64_t n_out, const int32_t *in_first, const int32_t *in_second, int64_t n_in,
+                           const float *a, const gvt_term *terms, int n_terms, int variant, float *u,
+                           int *variant_used, int64_t *op_count);
+
+/* Prediction for novel objects: scores = K(test, train) a with cross-Grams between the test
+ * objects (rows) and the training objects (columns), variant auto-selected (gvt_matvec_rect
+ * with variant 0).  PAPER.md:321-322 with the test sample's own objects (Table 1's
+ * m_bar, q_bar). */
+gvt_status pairwise_predict_rect(gvt_ctx *ctx, const float *Dx, int64_t m_test, int64_t m_train, const float *Tx,
+                                 int64_t q_test, int64_t q_train, const int32_t *test_first,
+                                 const int32_t *test_second, int64_t n_test, const int32_t *train_first,
+                                 const int32_t *train_second, int64_t n_train, const float *a,
+                                 const gvt_term *terms, int n_terms, float *scores);
 
 /* Integer plumbing exposed for bit-exact tests: stable sort of pair indices by first id
  * (mode 0) or by (first, second) (mode 1), ties in ascending index order; perm[n] int32

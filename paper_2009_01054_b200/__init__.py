@@ -94,12 +94,19 @@ _lib.pairwise_krr_fit_early_stopping.argtypes = [_P, _P, _I64, _P, _I64, _P, _P,
                                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                                  ctypes.POINTER(ctypes.c_int), _P]
 _lib.gvt_auc.argtypes = [_P, _P, _P, _I64, ctypes.POINTER(ctypes.c_double)]
+_lib.gvt_gram_cross.argtypes = [_P, ctypes.c_int, _P, _I64, _P, _I64, _I64, ctypes.c_double, ctypes.c_double,
+                                ctypes.c_int, _P]
+_lib.gvt_matvec_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int,
+                                 ctypes.c_int, _P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]
+_lib.pairwise_predict_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P,
+                                       ctypes.c_int, _P]
 
 EXPORTED = ["gvt_slab_bounds",
             "gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
-            "pairwise_krr_fit_early_stopping", "gvt_auc"]
+            "pairwise_krr_fit_early_stopping", "gvt_auc", "gvt_gram_cross", "gvt_matvec_rect",
+            "pairwise_predict_rect"]
 
 
 def _check(code: int, where: str):
@@ -259,6 +266,50 @@ class Context:
                              _ptr(out, "f32", "K")), "gvt_gram")
         return out
 
+    def gram_cross(self, kind: int, X, Y, gamma: float = 1.0, coef0: float = 1.0, degree: int = 2, out=None):
+        """gvt_gram_cross: K[i][j] = k(X_i, Y_j) (m x m2)."""
+        m, m2 = int(X.shape[0]), int(Y.shape[0])
+        dim = int(X.shape[1]) if len(X.shape) > 1 else 0
+        if out is None:
+            out = _empty_like_input(X, m * m2).reshape(m, m2)
+        _check(_lib.gvt_gram_cross(self._h, kind, _ptr(X, "f32", "X"), m, _ptr(Y, "f32", "Y"), m2, dim, gamma, coef0,
+                                   degree, _ptr(out, "f32", "K")), "gvt_gram_cross")
+        return out
+
+    def matvec_rect(self, Dx, Tx, out_first, out_second, in_first, in_second, a, terms, variant: int = 0, out=None):
+        """gvt_matvec_rect on cross-Grams Dx (m_out x m_in), Tx (q_out x q_in) or None: returns
+        (u, variant_used, op_count)."""
+        m_out, m_in = int(Dx.shape[0]), int(Dx.shape[1])
+        q_out, q_in = (0, 0) if Tx is None else (int(Tx.shape[0]), int(Tx.shape[1]))
+        n_out, n_in = _n(out_first), _n(in_first)
+        if out is None:
+            out = _empty_like_input(a if a is not None else Dx, n_out)
+        v, ops = ctypes.c_int(0), ctypes.c_int64(0)
+        ta = terms_array(terms)
+        _check(_lib.gvt_matvec_rect(self._h, _ptr(Dx, "f32", "Dx"), m_out, m_in, _ptr(Tx, "f32", "Tx"), q_out, q_in,
+                                    _ptr(out_first, "i32", "out_first"), _ptr(out_second, "i32", "out_second"), n_out,
+                                    _ptr(in_first, "i32", "in_first"), _ptr(in_second, "i32", "in_second"), n_in,
+                                    _ptr(a, "f32", "a"), ctypes.cast(ta, _P), len(terms), int(variant),
+                                    _ptr(out, "f32", "u"), ctypes.byref(v), ctypes.byref(ops)), "gvt_matvec_rect")
+        return out, v.value, ops.value
+
+    def predict_rect(self, Dx, Tx, test_first, test_second, train_first, train_second, a, terms, out=None):
+        """pairwise_predict_rect: scores for novel objects (cross-Grams test x train)."""
+        m_out, m_in = int(Dx.shape[0]), int(Dx.shape[1])
+        q_out, q_in = (0, 0) if Tx is None else (int(Tx.shape[0]), int(Tx.shape[1]))
+        n_test, n_train = _n(test_first), _n(train_first)
+        if out is None:
+            out = _empty_like_input(a if a is not None else Dx, n_test)
+        ta = terms_array(terms)
+        _check(_lib.pairwise_predict_rect(self._h, _ptr(Dx, "f32", "Dx"), m_out, m_in, _ptr(Tx, "f32", "Tx"), q_out,
+                                          q_in, _ptr(test_first, "i32", "test_first"),
+                                          _ptr(test_second, "i32", "test_second"), n_test,
+                                          _ptr(train_first, "i32", "train_first"),
+                                          _ptr(train_second, "i32", "train_second"), n_train, _ptr(a, "f32", "a"),
+                                          ctypes.cast(ta, _P), len(terms), _ptr(out, "f32", "scores")),
+               "pairwise_predict_rect")
+        return out
+
     def matvec(self, D, T, out_first, out_second, in_first, in_second, a, terms, out=None):
         m = int(D.shape[0])
         q = int(T.shape[0]) if T is not None else 0
@@ -377,6 +428,19 @@ def pairwise_krr_fit_early_stopping(ctx: Context, D, T, first, second, y, val_fi
 
 def gvt_auc(ctx: Context, labels, scores):
     return ctx.auc(labels, scores)
+
+
+def gvt_gram_cross(ctx: Context, kind, X, Y, gamma=1.0, coef0=1.0, degree=2, out=None):
+    return ctx.gram_cross(kind, X, Y, gamma, coef0, degree, out)
+
+
+def gvt_matvec_rect(ctx: Context, Dx, Tx, out_first, out_second, in_first, in_second, a, terms, variant=0, out=None):
+    return ctx.matvec_rect(Dx, Tx, out_first, out_second, in_first, in_second, a, terms, variant, out)
+
+
+def pairwise_predict_rect(ctx: Context, Dx, Tx, test_first, test_second, train_first, train_second, a, terms,
+                          out=None):
+    return ctx.predict_rect(Dx, Tx, test_first, test_second, train_first, train_second, a, terms, out)
 
 
 def gvt_sort_plan(ctx: Context, first, second, m, q, mode=0):

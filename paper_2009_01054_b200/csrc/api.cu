@@ -20,8 +20,12 @@ void predict(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, c
 gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
                int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
                double rel_tol, float *a_out, int *iters_out, double *relres_hist);
-void gram(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
-          float *K);
+void gram(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
+          double coef0, int degree, float *K);
+void matvec_rect(gvt_ctx *c, const float *Dx, int64_t m_out, int64_t m_in, const float *Tx, int64_t q_out,
+                 int64_t q_in, const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
+                 const int32_t *ins, int64_t n_in, const float *a, const gvt_term *terms, int n_terms, int variant,
+                 float *u, int *variant_used, int64_t *op_count);
 gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,
                               const int32_t *s, int64_t n, const float *y, const int32_t *vf, const int32_t *vs,
                               int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
@@ -248,7 +252,15 @@ gvt_status gvt_kernel_terms(gvt_kernel kernel, gvt_term *out, int *n_terms) {
 gvt_status gvt_gram(gvt_ctx *c, gvt_base kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0,
                     int degree, float *K) {
     GVT_API_BEGIN(c)
-    gvt::gram(c, (int)kind, X, m, dim, gamma, coef0, degree, K);
+    gvt::gram(c, (int)kind, X, m, nullptr, m, dim, gamma, coef0, degree, K);
+    GVT_API_END
+}
+
+gvt_status gvt_gram_cross(gvt_ctx *c, gvt_base kind, const float *X, int64_t m, const float *Y, int64_t m2,
+                          int64_t dim, double gamma, double coef0, int degree, float *K) {
+    GVT_API_BEGIN(c)
+    GVT_REQUIRE(m2 == 0 || Y || dim == 0, GVT_E_DIM, "Y is NULL");
+    gvt::gram(c, (int)kind, X, m, Y ? Y : X, m2, dim, gamma, coef0, degree, K);
     GVT_API_END
 }
 
@@ -282,6 +294,28 @@ gvt_status pairwise_krr_fit_early_stopping(gvt_ctx *c, const float *D, int64_t m
                                             n_val, val_labels, terms, n_terms, lambda, patience, max_iter, a_out,
                                             best_iter, best_auc, iters_run, auc_hist);
     if (st != GVT_OK) return st;
+    GVT_API_END
+}
+
+gvt_status gvt_matvec_rect(gvt_ctx *c, const float *Dx, int64_t m_out, int64_t m_in, const float *Tx, int64_t q_out,
+                           int64_t q_in, const int32_t *out_first, const int32_t *out_second, int64_t n_out,
+                           const int32_t *in_first, const int32_t *in_second, int64_t n_in, const float *a,
+                           const gvt_term *terms, int n_terms, int variant, float *u, int *variant_used,
+                           int64_t *op_count) {
+    GVT_API_BEGIN(c)
+    gvt::matvec_rect(c, Dx, m_out, m_in, Tx, q_out, q_in, out_first, out_second, n_out, in_first, in_second, n_in, a,
+                     terms, n_terms, variant, u, variant_used, op_count);
+    GVT_API_END
+}
+
+gvt_status pairwise_predict_rect(gvt_ctx *c, const float *Dx, int64_t m_test, int64_t m_train, const float *Tx,
+                                 int64_t q_test, int64_t q_train, const int32_t *test_first,
+                                 const int32_t *test_second, int64_t n_test, const int32_t *train_first,
+                                 const int32_t *train_second, int64_t n_train, const float *a, const gvt_term *terms,
+                                 int n_terms, float *scores) {
+    GVT_API_BEGIN(c)
+    gvt::matvec_rect(c, Dx, m_test, m_train, Tx, q_test, q_train, test_first, test_second, n_test, train_first,
+                     train_second, n_train, a, terms, n_terms, 0, scores, nullptr, nullptr);
     GVT_API_END
 }
 

@@ -162,8 +162,10 @@ struct EpiParams {
     float coef;
     int accumulate;
     float *out;
-    // gram
-    const float *norms;
+    // gram: row norms of A (norms) and of B (norms_b); same = the Gram of one table (diagonal
+    // exactly 1 for the Gaussian)
+    const float *norms, *norms_b;
+    int same;
     int kind;
     float gamma, coef0;
     int degree;
@@ -381,8 +383,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (gc < N) {
                         float x = run[i];
                         if (ep.kind == GVT_BASE_GAUSSIAN) {
-                            float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
-                            if (gc == gr) d2 = 0.f;  // k(x, x) = 1 exactly
+                            float d2 = fmaxf(ni + ep.norms_b[gc] - 2.f * x, 0.f);
+                            if (ep.same && gc == gr) d2 = 0.f;  // k(x, x) = 1 exactly
                             x = expf(-ep.gamma * d2);
                         } else if (ep.kind == GVT_BASE_POLY) {
                             float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
@@ -762,8 +764,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                         if (gc < N) {
                             float x = run[i];
                             if (ep.kind == GVT_BASE_GAUSSIAN) {
-                                float d2 = fmaxf(ni + ep.norms[gc] - 2.f * x, 0.f);
-                                if (gc == gr) d2 = 0.f;
+                                float d2 = fmaxf(ni + ep.norms_b[gc] - 2.f * x, 0.f);
+                                if (ep.same && gc == gr) d2 = 0.f;
                                 x = expf(-ep.gamma * d2);
                             } else if (ep.kind == GVT_BASE_POLY) {
                                 float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
@@ -1222,27 +1224,42 @@ __global__ void k_norms(const float *__restrict__ X, int64_t m, int64_t dim, flo
     }
 }
 
-void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
-             float *K, int64_t ldk) {
-    if (m == 0) return;
-    const int64_t ldx = round_up(dim, 32), rows = round_up(m, 128);
+// K (m x m2, ldk) = k(X_i, Y_j) on the tensor cores; Y == nullptr: the Gram of X (diagonal of the
+// Gaussian exactly 1)
+void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
+             double coef0, int degree, float *K, int64_t ldk) {
+    if (m == 0 || m2 == 0) return;
+    const bool same = Y == nullptr;
+    const int64_t ldx = round_up(dim, 32), rows = round_up(m, 128), rows2 = round_up(m2, 128);
     float *xp = wsT<float>(c, "gram.xp", rows * ldx);
     float *nr = wsT<float>(c, "gram.norms", rows);
     pad_copy(c, X, m, dim, dim, xp, ldx, rows);
     Operand xo = make_operand(c, "gram.x", xp, m, dim, ldx, ldx, rows);
-    if (kind == GVT_BASE_GAUSSIAN)
+    Operand yo = xo;
+    float *nr2 = nr;
+    if (!same) {
+        float *yp = wsT<float>(c, "gram.yp", rows2 * ldx);
+        nr2 = wsT<float>(c, "gram.norms2", rows2);
+        pad_copy(c, Y, m2, dim, dim, yp, ldx, rows2);
+        yo = make_operand(c, "gram.y", yp, m2, dim, ldx, ldx, rows2);
+    }
+    if (kind == GVT_BASE_GAUSSIAN) {
         GVT_LAUNCH(c, K_GRAM_TC, k_norms, grid1d(m * 32, 256, 4096), 256, 0, X, m, dim, nr);
+        if (!same) GVT_LAUNCH(c, K_GRAM_TC, k_norms, grid1d(m2 * 32, 256, 4096), 256, 0, Y, m2, dim, nr2);
+    }
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
     ep.c_f = K;
     ep.ldc = ldk;
     ep.norms = nr;
+    ep.norms_b = nr2;
+    ep.same = same ? 1 : 0;
     ep.kind = kind;
     ep.gamma = (float)gamma;
     ep.coef0 = (float)coef0;
     ep.degree = degree;
     ep.kcb = 1;  // short K (feature dim): one K-block per fp32 round-to-nearest drain
-    launch_gemm<EPI_GRAM>(c, K_GRAM_TC, xo, xo, m, m, dim, ep);
+    launch_gemm<EPI_GRAM>(c, K_GRAM_TC, xo, yo, m, m2, dim, ep);
 }
 
 }  // namespace gvt

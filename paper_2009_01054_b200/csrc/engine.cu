@@ -125,8 +125,10 @@ static bool form_homogeneous(Form f) { return f == FORM_SYM || f == FORM_ANTI ||
 
 // ----------------------------------------------------------------------------- problem
 struct Problem {
-    int64_t m = 0, q = 0;  // q = m when homogeneous
+    int64_t m = 0, q = 0;          // in-domain sizes (q = m when homogeneous)
+    int64_t m_out = 0, q_out = 0;  // out-domain sizes: = m, q except with rectangular cross-Grams
     bool hom = false;
+    bool rect = false;             // novel-object cross-Grams (out ids index rows, in ids columns)
     Factor D, T;           // T aliases D when homogeneous
     const int32_t *of = nullptr, *os = nullptr;    // this rank's out pairs
     int64_t n_out = 0;
@@ -136,11 +138,20 @@ struct Problem {
     std::vector<int64_t> counts, offsets;
     float *p_full = nullptr;
     int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
+    int64_t dom_out(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m_out : q_out; }
 };
 
 // validate a term list against the data (before any compute)
-static void validate_terms(const gvt_term *terms, int n_terms, bool hom, Form form) {
+static void validate_terms(const gvt_term *terms, int n_terms, bool hom, Form form, bool rect = false) {
     GVT_REQUIRE(terms && n_terms >= 1 && n_terms <= 64, GVT_E_KERNEL, "term list empty or too long");
+    if (rect) {
+        GVT_REQUIRE(form != FORM_CARTESIAN, GVT_E_KERNEL,
+                    "Cartesian kernel on cross-Grams: its Identity factor compares objects of two different tables "
+                    "(reading N1)");
+        for (int i = 0; i < n_terms; i++)
+            GVT_REQUIRE(terms[i].left != GVT_FACTOR_IDENTITY && terms[i].right != GVT_FACTOR_IDENTITY, GVT_E_KERNEL,
+                        "Identity factor on cross-Grams (reading N1)");
+    }
     if (form_homogeneous(form))
         GVT_REQUIRE(hom, GVT_E_HOMOGENEOUS, "homogeneous kernel (Symmetric/Anti-symmetric/Ranking/MLPK) given T != NULL");
     for (int i = 0; i < n_terms; i++) {
@@ -200,13 +211,22 @@ static EntryKinds kinds1(int rs, int cs, float sign) {
     return k;
 }
 
-static Factor materialise(gvt_ctx *c, const char *name, int64_t n, int identity) {
+static Factor materialise(gvt_ctx *c, const char *name, int64_t rows, int64_t cols, int identity) {
     Factor f;
-    f.n = n;
-    f.ld = round_up(n > 0 ? n : 1, 32);
-    float *p = wsT<float>(c, name, (size_t)round_up(n > 0 ? n : 1, 32) * f.ld);
-    fill_ones(c, p, round_up(n > 0 ? n : 1, 32), f.ld, identity);
+    f.n = rows;
+    f.cols = cols;
+    f.ld = round_up(cols > 0 ? cols : 1, 32);
+    const int64_t rp = round_up(rows > 0 ? rows : 1, 32);
+    float *p = wsT<float>(c, name, (size_t)rp * f.ld);
+    fill_ones(c, p, rp, cols, f.ld, identity);  // identity only for square (global-id) factors
     f.p = p;
+    if (rows != cols) {  // all-ones is its own transpose up to shape: the column-wise view
+        const int64_t ldt = round_up(rows > 0 ? rows : 1, 32), cp = round_up(cols > 0 ? cols : 1, 32);
+        float *pt = wsT<float>(c, (std::string(name) + ".t").c_str(), (size_t)cp * ldt);
+        fill_ones(c, pt, cp, rows, ldt, 0);
+        f.pt = pt;
+        f.ldt = ldt;
+    }
     return f;
 }
 
@@ -219,7 +239,7 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
         return 1;  // materialised Ones/Identity factors of a generic term list stay on SIMT
     }
     if (!(g.A.split && g.C.split)) return 1;  // factors were not split for tensor cores
-    double cells = (double)g.m_in * (double)g.C.n;
+    double cells = (double)g.m_in * (double)g.C.cols;
     double density = cells > 0 ? (double)g.ent.nnz / cells : 0.0;
     return (tc && density >= c->dense_threshold) ? 2 : 1;
 }
@@ -313,7 +333,7 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
         k.count = 2;
         k.k[0] = EntryKind{F, Sx, -1.f};
         k.k[1] = EntryKind{Sx, F, -1.f};
-        group(P.D, P.D, k, P.m, P.m, F, Sx, P.m, 1.f, "g0");
+        group(P.D, P.D, k, P.m, P.m, F, Sx, P.m_out, 1.f, "g0");
         {
             EntryKinds kd;
             memset(&kd, 0, sizeof(kd));
@@ -322,7 +342,7 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             kd.k[1] = EntryKind{Sx, F, 1.f};
             build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kd, P.m, P.m, mp.byF);
         }
-        mp.buf = wsT<float>(c, "mlpk.buf", (size_t)(P.n_out + P.m));
+        mp.buf = wsT<float>(c, "mlpk.buf", (size_t)(P.n_out + P.m_out));
         mp.groups[0].diag = wsT<float>(c, "mlpk.diag", (size_t)round_up(P.m > 0 ? P.m : 1, 32));
         break;
     }
@@ -349,8 +369,13 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             auto factor = [&](int kind, int rs, int cs, const char *nm) -> Factor {
                 if (kind == GVT_FACTOR_DRUG) return P.D;
                 if (kind == GVT_FACTOR_TARGET) return P.T;
-                int64_t n = P.dom(rs) > P.dom(cs) ? P.dom(rs) : P.dom(cs);
-                Factor f = materialise(c, nm, n, kind == GVT_FACTOR_IDENTITY);
+                Factor f;
+                if (P.rect) {  // all-ones over (out domain of rs) x (in domain of cs); no Identity (N1)
+                    f = materialise(c, nm, P.dom_out(rs), P.dom(cs), 0);
+                } else {
+                    int64_t n = P.dom(rs) > P.dom(cs) ? P.dom(rs) : P.dom(cs);
+                    f = materialise(c, nm, n, n, kind == GVT_FACTOR_IDENTITY);
+                }
                 mp.owned.push_back(f);
                 return f;
             };
@@ -363,20 +388,20 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             GroupPlan g;
             g.A = L;
             g.C = R;
-            g.q_out = P.dom(t.row_sel_right);
+            g.q_out = P.dom_out(t.row_sel_right);
             g.m_in = P.dom(t.col_sel_left);
             g.coef = (float)t.coef;
             std::string ts(tag);
             build_entry_plan(c, (ts + ".e").c_str(), P.inf, P.ins, P.n_in, kinds1(t.col_sel_left, t.col_sel_right, 1.f),
                              P.dom(t.col_sel_left), P.dom(t.col_sel_right), g.ent);
             build_sample_plan(c, (ts + ".s").c_str(), P.of, P.os, P.n_out, t.row_sel_left, t.row_sel_right, 0,
-                              P.dom(t.row_sel_left), g.smp);
+                              P.dom_out(t.row_sel_left), g.smp);
             finish_group(c, g, tag);
             mp.groups.push_back(g);
         }
         break;
     }
-    int64_t nb = P.m > P.q ? P.m : P.q;
+    int64_t nb = std::max(std::max(P.m, P.q), std::max(P.m_out, P.q_out));
     nb = round_up(nb > 0 ? nb : 1, 32);
     if (form == FORM_POLY2D || form == FORM_LINEAR || form == FORM_RANKING) {
         mp.b1 = wsT<float>(c, "cheap.b1", nb);
@@ -406,8 +431,8 @@ static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float c
         if (!my_slab(c, s)) continue;
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
         if (w == 0) continue;
-        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.n, p_full, g.diag);
-        gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.n, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag);
+        gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
                         skld);
     }
     // halves travel as pairs of floats (W is a multiple of 32)
@@ -434,7 +459,7 @@ static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float c
 static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out,
                       bool values_ready = false) {
     c->last_engine = g.engine;
-    if (g.engine == 2 && fused_f16(c, g.C.n)) {
+    if (g.engine == 2 && fused_f16(c, g.C.cols)) {
         run_group_f16(c, g, p_full, coef, accumulate, out);
         return;
     }
@@ -453,18 +478,18 @@ static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef,
             entry_values(c, ev, p_full);
         }
         if (g.engine == 2) {
-            const int64_t ldX = round_up(g.C.n > 0 ? g.C.n : 1, 32);  // X slab: w x q_in
+            const int64_t ldX = round_up(g.C.cols > 0 ? g.C.cols : 1, 32);  // X slab: w x q_in
             const int64_t rows_pad = round_up(w > 0 ? w : 1, 128);
             float *X = wsT<float>(c, "dense.X", (size_t)rows_pad * ldX);
             densify(c, g.ent, k0, k1, lo, X, ldX, rows_pad);
             if (g.diag) add_diag(c, X, ldX, g.diag, lo, w);
-            Operand xo = make_operand(c, "dense.Xop", X, w, g.C.n, ldX, ldX, rows_pad);
-            gemm_nt_store(c, g.C.op, xo, g.q_out, w, g.C.n, Ss, g.W, nullptr, nullptr);
+            Operand xo = make_operand(c, "dense.Xop", X, w, g.C.cols, ldX, ldX, rows_pad);
+            gemm_nt_store(c, g.C.op, xo, g.q_out, w, g.C.cols, Ss, g.W, nullptr, nullptr);
         } else {
             EntryPlan es = g.ent;
             es.row_ptr = g.ent.row_ptr + lo;
             es.nrow = w;
-            stage1_sparse(c, es, g.C, g.q_out, Ss, g.W, g.diag, lo);
+            stage1_sparse(c, es, g.C.colwise(), g.q_out, Ss, g.W, g.diag, lo);
         }
     }
     // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab
@@ -548,27 +573,38 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
 }
 
 // ----------------------------------------------------------------------------- factors
-static Factor prepare_factor(gvt_ctx *c, const char *name, const float *user, int64_t n, bool need_split) {
+// rows x cols factor (square Gram: rows = cols; rectangular cross-Gram: rows = out-domain,
+// cols = in-domain, plus the transposed copy the sparse stage 1 reads)
+static Factor prepare_factor(gvt_ctx *c, const char *name, const float *user, int64_t rows, int64_t cols,
+                             bool need_split, bool rect) {
     Factor f;
-    f.n = n;
-    f.ld = round_up(n > 0 ? n : 1, 32);
-    int64_t rows_pad = round_up(n > 0 ? n : 1, 128);
+    f.n = rows;
+    f.cols = cols;
+    f.ld = round_up(cols > 0 ? cols : 1, 32);
+    int64_t rows_pad = round_up(rows > 0 ? rows : 1, 128);
     std::string nm(name);
     float *d = wsT<float>(c, (nm + ".pad").c_str(), (size_t)rows_pad * f.ld);
-    if (n > 0) {
-        const float *src = user;
+    const float *src = user;
+    if (rows > 0 && cols > 0) {
         if (!is_device_ptr(user)) {
-            float *tmp = wsT<float>(c, (nm + ".h2d").c_str(), (size_t)n * n);
-            GVT_CUDA_TRY(cudaMemcpyAsync(tmp, user, sizeof(float) * n * n, cudaMemcpyHostToDevice, c->stream));
+            float *tmp = wsT<float>(c, (nm + ".h2d").c_str(), (size_t)rows * cols);
+            GVT_CUDA_TRY(cudaMemcpyAsync(tmp, user, sizeof(float) * rows * cols, cudaMemcpyHostToDevice, c->stream));
             src = tmp;
         }
-        pad_copy(c, src, n, n, n, d, f.ld, rows_pad);
+        pad_copy(c, src, rows, cols, cols, d, f.ld, rows_pad);
     } else {
         GVT_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(float) * rows_pad * f.ld, c->stream));
     }
     f.p = d;
+    if (rect) {
+        f.ldt = round_up(rows > 0 ? rows : 1, 32);
+        const int64_t cp = round_up(cols > 0 ? cols : 1, 32);
+        float *t = wsT<float>(c, (nm + ".T").c_str(), (size_t)cp * f.ldt);
+        transpose_pad(c, d, rows_pad, f.ld, f.ld, t, f.ldt, cp);
+        f.pt = t;
+    }
     if (need_split) {
-        f.op = make_operand(c, (nm + ".op").c_str(), d, n, n, f.ld, f.ld, rows_pad);
+        f.op = make_operand(c, (nm + ".op").c_str(), d, rows, cols, f.ld, f.ld, rows_pad);
         f.split = true;
     }
     return f;
@@ -625,25 +661,31 @@ static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_i
 }
 
 // out_is_in: the out sample is the caller's in sample (fit)
+// m_out / q_out < 0: square Grams over global ids (out dims = in dims); else rectangular
+// cross-Grams D (m_out x m) and T (q_out x q) of novel objects
 static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, const float *T, int64_t q,
                           const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
                           const int32_t *ins, int64_t n_in, const gvt_term *terms, int n_terms, Form &form,
-                          bool out_is_in) {
+                          bool out_is_in, int64_t m_out = -1, int64_t q_out = -1) {
     GVT_REQUIRE(m >= 0 && n_out >= 0 && n_in >= 0, GVT_E_DIM, "negative size");
     P.hom = (T == nullptr);
+    P.rect = m_out >= 0;
     P.m = m;
     P.q = P.hom ? m : q;
-    GVT_REQUIRE(P.q >= 0, GVT_E_DIM, "negative q");
-    GVT_REQUIRE(m == 0 || D, GVT_E_DIM, "D is NULL with m > 0");
+    P.m_out = P.rect ? m_out : P.m;
+    P.q_out = P.rect ? (P.hom ? m_out : q_out) : P.q;
+    GVT_REQUIRE(P.q >= 0 && P.q_out >= 0, GVT_E_DIM, "negative q");
+    GVT_REQUIRE((m == 0 || P.m_out == 0) || D, GVT_E_DIM, "D is NULL with m > 0");
+    GVT_REQUIRE(P.hom || (P.q == 0 || P.q_out == 0) || T, GVT_E_DIM, "T is NULL");
     form = recognize(terms, n_terms);
-    validate_terms(terms, n_terms, P.hom, form);
+    validate_terms(terms, n_terms, P.hom, form, P.rect);
     P.n_out = n_out;
     P.of = stage_ids(c, "in.of", of, n_out);
     P.os = stage_ids(c, "in.os", os, n_out);
     const int32_t *lf = out_is_in ? P.of : stage_ids(c, "in.inf", inf, n_in);
     const int32_t *ls = out_is_in ? P.os : stage_ids(c, "in.ins", ins, n_in);
-    check_range(c, P.of, n_out, P.m, "out first ids");
-    check_range(c, P.os, n_out, P.q, "out second ids");
+    check_range(c, P.of, n_out, P.m_out, "out first ids");
+    check_range(c, P.os, n_out, P.q_out, "out second ids");
     if (!out_is_in) {
         check_range(c, lf, n_in, P.m, "in first ids");
         check_range(c, ls, n_in, P.q, "in second ids");
@@ -666,17 +708,18 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
         P.ins = ls;
     }
     bool split = needs_split(c, form, P.m, P.q, P.n_in);
-    P.D = prepare_factor(c, "fD", D, m, split);
-    P.T = P.hom ? P.D : prepare_factor(c, "fT", T, q, split);
+    P.D = prepare_factor(c, "fD", D, P.m_out, P.m, split, P.rect);
+    P.T = P.hom ? P.D : prepare_factor(c, "fT", T, P.q_out, P.q, split, P.rect);
 }
 
 // ----------------------------------------------------------------------------- entry points
-void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of, const int32_t *os,
-            int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in, const float *a,
-            const gvt_term *terms, int n_terms, float *u) {
+static void matvec_impl(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of,
+                        const int32_t *os, int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in,
+                        const float *a, const gvt_term *terms, int n_terms, float *u, int64_t m_out = -1,
+                        int64_t q_out = -1) {
     Problem P;
     Form form;
-    setup_problem(c, P, D, m, T, q, of, os, n_out, inf, ins, n_in, terms, n_terms, form, false);
+    setup_problem(c, P, D, m, T, q, of, os, n_out, inf, ins, n_in, terms, n_terms, form, false, m_out, q_out);
     OutArr uo = out_arr(c, "out.u", u, n_out);
     const float *ad = n_in ? (const float *)stage_in(c, "in.a", a, sizeof(float) * n_in) : nullptr;
     GVT_REQUIRE(n_in == 0 || ad, GVT_E_DIM, "a is NULL with n_in > 0");
@@ -688,6 +731,44 @@ void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, co
         run_matvec(c, P, mp, ad, uo.dev);
     }
     out_finish(c, uo);
+}
+
+void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of, const int32_t *os,
+            int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in, const float *a,
+            const gvt_term *terms, int n_terms, float *u) {
+    matvec_impl(c, D, m, T, q, of, os, n_out, inf, ins, n_in, a, terms, n_terms, u);
+}
+
+// Novel objects (Settings 2-4): rectangular cross-Grams Dx (m_out x m_in) and
+// Tx (q_out x q_in, NULL = homogeneous), out ids index rows, in ids columns.  For the Kronecker
+// list the GVT variant follows Theorem 1's cost (SPEC.md gvt_cost): variant 1
+// (stage 1 over the target factor) costs q_out n_in + m_in n_out, variant 2 (the roles of the
+// two factors swapped) m_out n_in + q_in n_out; auto takes the smaller, ties -> 1 (reading S2).
+// Variant 2 runs as variant 1 of the swapped problem (Tx, Dx) with the pair elements swapped.
+void matvec_rect(gvt_ctx *c, const float *Dx, int64_t m_out, int64_t m_in, const float *Tx, int64_t q_out,
+                 int64_t q_in, const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
+                 const int32_t *ins, int64_t n_in, const float *a, const gvt_term *terms, int n_terms, int variant,
+                 float *u, int *variant_used, int64_t *op_count) {
+    GVT_REQUIRE(m_out >= 0 && m_in >= 0 && n_out >= 0 && n_in >= 0, GVT_E_DIM, "negative size");
+    GVT_REQUIRE(Tx == nullptr || (q_out >= 0 && q_in >= 0), GVT_E_DIM, "negative size");
+    GVT_REQUIRE(variant >= 0 && variant <= 2, GVT_E_PARAM, "variant must be 0 (auto), 1 or 2");
+    GVT_REQUIRE(terms && n_terms >= 1, GVT_E_KERNEL, "term list empty");
+    const bool hom = Tx == nullptr;
+    if (hom) {
+        q_out = m_out;
+        q_in = m_in;
+    }
+    const bool kron = recognize(terms, n_terms) == FORM_KRON;
+    GVT_REQUIRE(variant != 2 || kron, GVT_E_PARAM, "variant 2 is defined for the Kronecker term list only");
+    const int64_t c1 = q_out * n_in + m_in * n_out, c2 = m_out * n_in + q_in * n_out;
+    int v = variant ? variant : ((kron && c2 < c1) ? 2 : 1);
+    if (variant_used) *variant_used = v;
+    if (op_count) *op_count = kron ? (v == 1 ? c1 : c2) : -1;
+    if (v == 1)
+        matvec_impl(c, Dx, m_in, Tx, q_in, of, os, n_out, inf, ins, n_in, a, terms, n_terms, u, m_out, q_out);
+    else
+        matvec_impl(c, hom ? Dx : Tx, q_in, hom ? nullptr : Dx, m_in, os, of, n_out, ins, inf, n_in, a, terms,
+                    n_terms, u, q_out, m_out);
 }
 
 void predict(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *tf, const int32_t *ts,
@@ -955,20 +1036,22 @@ gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float
                     &es);
 }
 
-void gram(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
-          float *K) {
-    GVT_REQUIRE(m >= 0 && dim >= 0, GVT_E_DIM, "negative size");
+// K (m x m2) = k(X_i, Y_j); Y == nullptr: the Gram of X (m2 = m)
+void gram(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
+          double coef0, int degree, float *K) {
+    GVT_REQUIRE(m >= 0 && m2 >= 0 && dim >= 0, GVT_E_DIM, "negative size");
     GVT_REQUIRE(kind >= 0 && kind <= 2, GVT_E_PARAM, "unknown base kernel");
     GVT_REQUIRE(kind != GVT_BASE_GAUSSIAN || gamma > 0.0, GVT_E_PARAM, "Gaussian base kernel needs gamma > 0");
     GVT_REQUIRE(kind != GVT_BASE_POLY || degree >= 0, GVT_E_PARAM, "polynomial base kernel needs degree >= 0");
-    if (m == 0) return;
-    GVT_REQUIRE(X && K, GVT_E_DIM, "X or K is NULL");
+    if (m == 0 || m2 == 0) return;
+    GVT_REQUIRE(X && K && (Y || m2 == m), GVT_E_DIM, "X, Y or K is NULL");
     const float *Xd = dim ? (const float *)stage_in(c, "in.X", X, sizeof(float) * m * dim) : nullptr;
-    OutArr ko = out_arr(c, "out.K", K, m * m);
+    const float *Yd = (Y && dim) ? (const float *)stage_in(c, "in.Y", Y, sizeof(float) * m2 * dim) : nullptr;
+    OutArr ko = out_arr(c, "out.K", K, m * m2);
     bool use_tc = tc_available(c) && c->gram_engine != 1 && dim > 0;
     if (c->gram_engine == 2) GVT_REQUIRE(tc_available(c), GVT_E_CUDA, "tensor-core Gram requested but unavailable");
-    if (use_tc) gram_tc(c, kind, Xd, m, dim, gamma, coef0, degree, ko.dev, m);
-    else gram_simt(c, kind, Xd, m, dim, dim, gamma, coef0, degree, ko.dev, m);
+    if (use_tc) gram_tc(c, kind, Xd, m, Y ? Yd : nullptr, m2, dim, gamma, coef0, degree, ko.dev, m2);
+    else gram_simt(c, kind, Xd, m, Y ? Yd : nullptr, m2, dim, dim, gamma, coef0, degree, ko.dev, m2);
     out_finish(c, ko);
 }
 

@@ -2,6 +2,7 @@
 // form is in dense_tc.cu).  K[i][j] = k(X_i, X_j):
 //   LINEAR   <x,y>
 //   GAUSSIAN exp(-gamma * sum_k (x_k - y_k)^2)   direct differences => K[i][i] = 1 exactly
+// K[i][j] = k(X_i, Y_j) for the cross-Gram of two tables (novel objects, Y != X).
 //   POLY     (gamma <x,y> + coef0)^degree
 // 64x64 output tile per 256-thread CTA, 4x4 outputs per thread, X tiles staged in smem.
 #include "ops.cuh"
@@ -9,9 +10,9 @@
 namespace gvt {
 
 template <int KIND>
-__global__ void __launch_bounds__(256) k_gram_simt(const float *__restrict__ X, int64_t m, int64_t dim, int64_t ldx,
-                                                   float gamma, float coef0, int degree, float *__restrict__ K,
-                                                   int64_t ldk) {
+__global__ void __launch_bounds__(256) k_gram_simt(const float *__restrict__ X, int64_t m, const float *__restrict__ Y,
+                                                   int64_t m2, int64_t dim, int64_t ldx, float gamma, float coef0,
+                                                   int degree, float *__restrict__ K, int64_t ldk) {
     constexpr int BT = 64, BK = 16;
     __shared__ float xa[BK][BT + 4];
     __shared__ float xb[BK][BT + 4];
@@ -27,7 +28,7 @@ __global__ void __launch_bounds__(256) k_gram_simt(const float *__restrict__ X, 
             int r = e / BK, kk = e % BK;
             int64_t gi = i0 + r, gj = j0 + r, gk = k0 + kk;
             xa[kk][r] = (gi < m && gk < dim) ? X[gi * ldx + gk] : 0.f;
-            xb[kk][r] = (gj < m && gk < dim) ? X[gj * ldx + gk] : 0.f;
+            xb[kk][r] = (gj < m2 && gk < dim) ? Y[gj * ldx + gk] : 0.f;
         }
         __syncthreads();
 #pragma unroll
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(256) k_gram_simt(const float *__restrict__ X, 
 #pragma unroll
         for (int b = 0; b < 4; b++) {
             int64_t gj = j0 + tx + 16 * b;
-            if (gj >= m) continue;
+            if (gj >= m2) continue;
             float v = acc[a][b];
             if (KIND == GVT_BASE_GAUSSIAN) {
                 v = expf(-gamma * v);
@@ -72,18 +73,20 @@ __global__ void __launch_bounds__(256) k_gram_simt(const float *__restrict__ X, 
     }
 }
 
-void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, int64_t ldx, double gamma, double coef0,
-               int degree, float *K, int64_t ldk) {
-    if (m == 0) return;
-    dim3 grid((unsigned)((m + 63) / 64), (unsigned)((m + 63) / 64));
+// K (m x m2) = k(X_i, Y_j); Y == nullptr: the Gram of X
+void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, int64_t ldx,
+               double gamma, double coef0, int degree, float *K, int64_t ldk) {
+    if (m == 0 || m2 == 0) return;
+    if (!Y) Y = X;
+    dim3 grid((unsigned)((m2 + 63) / 64), (unsigned)((m + 63) / 64));
     if (kind == GVT_BASE_GAUSSIAN)
-        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_GAUSSIAN>, grid, 256, 0, X, m, dim, ldx, (float)gamma,
+        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_GAUSSIAN>, grid, 256, 0, X, m, Y, m2, dim, ldx, (float)gamma,
                    (float)coef0, degree, K, ldk);
     else if (kind == GVT_BASE_POLY)
-        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_POLY>, grid, 256, 0, X, m, dim, ldx, (float)gamma,
+        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_POLY>, grid, 256, 0, X, m, Y, m2, dim, ldx, (float)gamma,
                    (float)coef0, degree, K, ldk);
     else
-        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_LINEAR>, grid, 256, 0, X, m, dim, ldx, (float)gamma,
+        GVT_LAUNCH(c, K_GRAM_SIMT, k_gram_simt<GVT_BASE_LINEAR>, grid, 256, 0, X, m, Y, m2, dim, ldx, (float)gamma,
                    (float)coef0, degree, K, ldk);
 }
 

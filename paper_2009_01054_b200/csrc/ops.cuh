@@ -20,14 +20,29 @@ struct Operand {
     int64_t scale_k_ld = 0;
 };
 
-// A square factor (Gram / materialised ones / identity) copied to a padded device
-// buffer: n x n, leading dimension ld = round_up(n, 32), padding zero.  For the dense
-// tensor-core engine its split operand is attached on demand.
+// A factor (Gram / cross-Gram / materialised ones / identity) copied to a padded device
+// buffer: n rows (out-domain) x cols (in-domain), leading dimension ld = round_up(cols, 32),
+// padding zero; square Grams have cols = n.  For the dense tensor-core engine its split
+// operand is attached on demand.  The sparse stage 1 reads the factor column-wise; a
+// symmetric Gram is its own transpose (reading R1), a rectangular cross-Gram carries an
+// explicit transposed copy pt (cols x ldt, ldt = round_up(n, 32)).
 struct Factor {
     const float *p = nullptr;
     int64_t n = 0, ld = 0;
+    int64_t cols = 0;
+    const float *pt = nullptr;
+    int64_t ldt = 0;
     Operand op;
     bool split = false;
+    // the layout stage1_sparse reads: row `col` holds factor column col (contiguous over t)
+    Factor colwise() const {
+        Factor f = *this;
+        if (pt) {
+            f.p = pt;
+            f.ld = ldt;
+        }
+        return f;
+    }
 };
 
 // one entry kind of the pair matrix X (row selector, column selector, sign), see engine.cu
@@ -61,7 +76,10 @@ struct SamplePlan {
 // ---- plumbing (plan.cu)
 void pad_copy(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t ld_src, float *dst, int64_t ld_dst,
               int64_t rows_pad);
-void fill_ones(gvt_ctx *c, float *dst, int64_t n, int64_t ld, int identity);
+void fill_ones(gvt_ctx *c, float *dst, int64_t rows, int64_t cols, int64_t ld, int identity);
+// dst = src^T (cols x rows) into a zero-padded buffer: ld_dst >= rows, rows_pad_dst >= cols
+void transpose_pad(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t ld_src, float *dst,
+                   int64_t ld_dst, int64_t rows_pad_dst);
 void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n,
                       const EntryKinds &kinds, int64_t nrow, int64_t ncol, EntryPlan &out);
 // samples from an out-sample: kind 0: (sel(rs, i), sel(cs, i)) for i < n; plus (x,x) for x < n_diag
@@ -123,10 +141,11 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
 void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol);
 
 // ---- Gram (gram.cu)
-void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, int64_t ldx, double gamma,
-               double coef0, int degree, float *K, int64_t ldk);
-void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, int64_t dim, double gamma, double coef0, int degree,
-             float *K, int64_t ldk);
+// K (m x m2, ldk) = k(X_i, Y_j); Y == nullptr: the Gram of X (m2 = m)
+void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, int64_t ldx,
+               double gamma, double coef0, int degree, float *K, int64_t ldk);
+void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
+             double coef0, int degree, float *K, int64_t ldk);
 
 // ---- CG (cg.cu)
 struct CGState;  // device

@@ -25,19 +25,45 @@ void pad_copy(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t 
                dst, ld_dst, rows_pad);
 }
 
-__global__ void k_fill_ones(float *dst, int64_t n, int64_t ld, int identity) {
-    int64_t total = n * ld;
+// dst (cols x ld_dst, rows_pad_dst rows, zero padded) = src^T, src rows x cols (ld_src): 32x32
+// shared-memory tiles, coalesced on both sides (rectangular cross-Grams, sparse stage 1)
+__global__ void k_transpose_pad(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
+                                float *__restrict__ dst, int64_t ld_dst, int64_t rows_pad_dst) {
+    __shared__ float tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;  // src tile origin
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = r0 + k, cc = c0 + threadIdx.x;
+        tile[k][threadIdx.x] = (r < rows && cc < cols) ? src[r * ld_src + cc] : 0.f;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t dr = c0 + k, dc = r0 + threadIdx.x;  // dst row = src col
+        if (dr < rows_pad_dst && dc < ld_dst) dst[dr * ld_dst + dc] = tile[threadIdx.x][k];
+    }
+}
+
+void transpose_pad(gvt_ctx *c, const float *src, int64_t rows, int64_t cols, int64_t ld_src, float *dst,
+                   int64_t ld_dst, int64_t rows_pad_dst) {
+    if (rows_pad_dst == 0 || ld_dst == 0) return;
+    dim3 grid((unsigned)((rows_pad_dst + 31) / 32), (unsigned)((ld_dst + 31) / 32));
+    GVT_LAUNCH(c, K_PAD_COPY, k_transpose_pad, grid, dim3(32, 8), 0, src, rows, cols, ld_src, dst, ld_dst,
+               rows_pad_dst);
+}
+
+__global__ void k_fill_ones(float *dst, int64_t rows, int64_t cols, int64_t ld, int identity) {
+    int64_t total = rows * ld;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / ld, cc = i - r * ld;
         float v = 0.f;
-        if (cc < n) v = identity ? (r == cc ? 1.f : 0.f) : 1.f;
+        if (cc < cols) v = identity ? (r == cc ? 1.f : 0.f) : 1.f;
         dst[i] = v;
     }
 }
 
-void fill_ones(gvt_ctx *c, float *dst, int64_t n, int64_t ld, int identity) {
-    if (n == 0) return;
-    GVT_LAUNCH(c, K_FILL, k_fill_ones, grid1d(n * ld, 256, 8 * c->sm_count * 8), 256, 0, dst, n, ld, identity);
+void fill_ones(gvt_ctx *c, float *dst, int64_t rows, int64_t cols, int64_t ld, int identity) {
+    if (rows == 0) return;
+    GVT_LAUNCH(c, K_FILL, k_fill_ones, grid1d(rows * ld, 256, 8 * c->sm_count * 8), 256, 0, dst, rows, cols, ld,
+               identity);
 }
 
 // ----------------------------------------------------------------------------- sorting helpers

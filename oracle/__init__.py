@@ -25,7 +25,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # enums (oracle-side copies; the CUDA side has its own in include/gvt.h)
 LINEAR, POLY2D, GAUSSIAN, KRONECKER, SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK, CARTESIAN = range(9)
 HOMOGENEOUS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
-BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY = range(3)
+BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY, BASE_TANIMOTO = range(4)
 DRUG, TARGET, ONES, IDENTITY = range(4)
 FIRST, SECOND = 0, 1
 OK, E_DIM, E_INDEX, E_HOMOGENEOUS, E_KERNEL, E_PARAM, E_BREAKDOWN, E_OOM = range(8)

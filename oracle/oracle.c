@@ -38,7 +38,7 @@
 
 enum { OR_LINEAR = 0, OR_POLY2D, OR_GAUSSIAN, OR_KRONECKER, OR_SYMMETRIC,
        OR_ANTISYMMETRIC, OR_RANKING, OR_MLPK, OR_CARTESIAN, OR_NKERNELS };
-enum { OR_BASE_LINEAR = 0, OR_BASE_GAUSSIAN = 1, OR_BASE_POLY = 2 };
+enum { OR_BASE_LINEAR = 0, OR_BASE_GAUSSIAN = 1, OR_BASE_POLY = 2, OR_BASE_TANIMOTO = 3 };
 enum { F_DRUG = 0, F_TARGET = 1, F_ONES = 2, F_IDENTITY = 3 };
 enum { SEL_FIRST = 0, SEL_SECOND = 1 };
 
@@ -66,13 +66,21 @@ int oracle_num_threads(void) {
  * polynomial base kernel (gamma<x,y> + coef0)^degree is not in the paper; it is
  * named only by BASELINE.json's north star (reading S5b in DESIGN.md).
  * K[i][j] = k(X_i, Y_j) for i < m, j < m2; the Gaussian uses direct differences so
- * that k(x,x) = exp(0) = 1 exactly. */
+ * that k(x,x) = exp(0) = 1 exactly.
+ * Tanimoto on binary feature vectors (section 5.1 Heterodimers; Merget's drug
+ * kernels): "the ratio of bits set to 1 in both vs. bits set to 1 in either",
+ * k(v, w) = sum_i min(v_i, w_i) / sum_i max(v_i, w_i); two all-zero vectors give 1 (SPEC.md
+ * tanimoto_base_kernel convention, reading T1); an entry other than 0 or 1 is OR_E_PARAM. */
 int oracle_gram(int base, const double *X, int64_t m, const double *Y, int64_t m2,
                 int64_t dim, double gamma, double coef0, int degree, double *K) {
     if (m < 0 || m2 < 0 || dim < 0) return OR_E_DIM;
     if (base == OR_BASE_GAUSSIAN && !(gamma > 0)) return OR_E_PARAM;
     if (base == OR_BASE_POLY && degree < 0) return OR_E_PARAM;
-    if (base < 0 || base > 2) return OR_E_PARAM;
+    if (base < 0 || base > 3) return OR_E_PARAM;
+    if (base == OR_BASE_TANIMOTO) {
+        for (int64_t i = 0; i < m * dim; i++) if (X[i] != 0.0 && X[i] != 1.0) return OR_E_PARAM;
+        for (int64_t i = 0; i < m2 * dim; i++) if (Y[i] != 0.0 && Y[i] != 1.0) return OR_E_PARAM;
+    }
     #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < m; i++) {
         for (int64_t j = 0; j < m2; j++) {
@@ -81,6 +89,13 @@ int oracle_gram(int base, const double *X, int64_t m, const double *Y, int64_t m
             if (base == OR_BASE_GAUSSIAN) {
                 for (int64_t k = 0; k < dim; k++) { double df = x[k] - y[k]; acc += df * df; }
                 K[i * m2 + j] = exp(-gamma * acc);
+            } else if (base == OR_BASE_TANIMOTO) {
+                double mx = 0.0;
+                for (int64_t k = 0; k < dim; k++) {
+                    acc += x[k] < y[k] ? x[k] : y[k];
+                    mx += x[k] > y[k] ? x[k] : y[k];
+                }
+                K[i * m2 + j] = mx > 0.0 ? acc / mx : 1.0;
             } else {
                 for (int64_t k = 0; k < dim; k++) acc += x[k] * y[k];
                 if (base == OR_BASE_LINEAR) K[i * m2 + j] = acc;

@@ -714,3 +714,30 @@ def test_explicit_rect_equals_union_gram_subblock(kernel):
         O.explicit_rect_matvec(O.CARTESIAN, Dx, Tu[qi:, :qi] if Tu is not None else np.ones((qo, qi)), of, os_,
                                inf, ins, a)
     assert e.value.code == O.E_KERNEL
+
+
+# ----------------------------------------------------------------------------- Tanimoto (NEXT-4)
+def test_tanimoto_spec_worked_values():
+    """[1,1,0] vs [1,0,1] -> 1/3; identical nonzero -> 1; both all-zero -> 1 (T1)."""
+    for case in SPEC["tanimoto_base"]["cases"]:
+        k = O.gram(O.BASE_TANIMOTO, [case["v"]], [case["w"]])[0, 0]
+        assert k == case["k"][0] / case["k"][1]
+
+
+def test_tanimoto_equals_scipy_jaccard_and_is_psd():
+    """Tanimoto on binary vectors = 1 - Jaccard distance (scipy cdist 'jaccard', a library
+    routine; scipy defines 0/0 as distance 0, matching T1); the Gram is PSD; an entry other than
+    0/1 is an error."""
+    rng = np.random.default_rng(8)
+    X = (rng.uniform(size=(60, 300)) < rng.uniform(0.01, 0.3, size=(60, 1))).astype(float)
+    Y = (rng.uniform(size=(45, 300)) < 0.05).astype(float)
+    X[3] = 0.0
+    Y[7] = 0.0
+    K = O.gram(O.BASE_TANIMOTO, X, Y)
+    assert np.allclose(K, 1.0 - cdist(X.astype(bool), Y.astype(bool), "jaccard"), atol=1e-15, rtol=0)
+    assert K[3, 7] == 1.0
+    G = O.gram(O.BASE_TANIMOTO, X)
+    assert np.all(np.diag(G) == 1.0)
+    assert np.linalg.eigvalsh(G).min() >= -1e-10 * np.abs(G).max()
+    with pytest.raises(O.OracleError):
+        O.gram(O.BASE_TANIMOTO, [[0.0, 0.5]])

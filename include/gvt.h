@@ -67,8 +67,9 @@ typedef enum {
     GVT_ANTISYMMETRIC = 5, GVT_RANKING = 6, GVT_MLPK = 7, GVT_CARTESIAN = 8
 } gvt_kernel;
 
-/* Base kernels on object features (POLY by the north star). */
-typedef enum { GVT_BASE_LINEAR = 0, GVT_BASE_GAUSSIAN = 1, GVT_BASE_POLY = 2 } gvt_base;
+/* Base kernels on object features (POLY by the north star; TANIMOTO on
+ * binary features). */
+typedef enum { GVT_BASE_LINEAR = 0, GVT_BASE_GAUSSIAN = 1, GVT_BASE_POLY = 2, GVT_BASE_TANIMOTO = 3 } gvt_base;
 
 /* Factor of a Kronecker term: drug Gram, target Gram, all-ones, identity. */
 typedef enum { GVT_FACTOR_DRUG = 0, GVT_FACTOR_TARGET = 1, GVT_FACTOR_ONES = 2, GVT_FACTOR_IDENTITY = 3 } gvt_factor;
@@ -166,8 +167,11 @@ gvt_status gvt_kernel_terms(gvt_kernel kernel, gvt_term *out, int *n_terms);
 
 /* Base-kernel Gram K[i][j] = k(X_i, X_j), X (m x dim), K (m x m):
  * LINEAR <x,y>; GAUSSIAN exp(-gamma ||x-y||^2) (squared norm, reading S4; diagonal exactly
- * 1); POLY (gamma <x,y> + coef0)^degree.  Errors: GVT_E_PARAM if gamma <= 0 (GAUSSIAN) or
- * degree < 0 (POLY). */
+ * 1); POLY (gamma <x,y> + coef0)^degree; TANIMOTO sum_k min(x_k, y_k) / sum_k max(x_k, y_k)
+ * on 0/1 features ("bits set to 1 in both vs. bits set to 1 in either"), 1 for
+ * two all-zero vectors (reading T1), computed exactly as popcounts of bit-packed features.
+ * Errors: GVT_E_PARAM if gamma <= 0 (GAUSSIAN), degree < 0 (POLY) or a TANIMOTO feature is
+ * not 0 or 1 (checked before the Gram is computed). */
 gvt_status gvt_gram(gvt_ctx *ctx, gvt_base kind, const float *X, int64_t m, int64_t dim,
                     double gamma, double coef0, int degree, float *K);
 

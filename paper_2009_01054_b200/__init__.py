@@ -30,7 +30,7 @@ _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
 # ---------------------------------------------------------------------------- enums (gvt.h)
 OK, E_DIM, E_INDEX, E_HOMOGENEOUS, E_KERNEL, E_PARAM, E_BREAKDOWN, E_CUDA, E_NCCL, E_OOM, E_STATE = range(11)
 LINEAR, POLY2D, GAUSSIAN, KRONECKER, SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK, CARTESIAN = range(9)
-BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY = range(3)
+BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY, BASE_TANIMOTO = range(4)
 FACTOR_DRUG, FACTOR_TARGET, FACTOR_ONES, FACTOR_IDENTITY = range(4)
 SEL_FIRST, SEL_SECOND = 0, 1
 OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE, OPT_TC_PRECISION = range(5)

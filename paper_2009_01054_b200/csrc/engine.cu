@@ -1040,7 +1040,7 @@ gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float
 void gram(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
           double coef0, int degree, float *K) {
     GVT_REQUIRE(m >= 0 && m2 >= 0 && dim >= 0, GVT_E_DIM, "negative size");
-    GVT_REQUIRE(kind >= 0 && kind <= 2, GVT_E_PARAM, "unknown base kernel");
+    GVT_REQUIRE(kind >= 0 && kind <= 3, GVT_E_PARAM, "unknown base kernel");
     GVT_REQUIRE(kind != GVT_BASE_GAUSSIAN || gamma > 0.0, GVT_E_PARAM, "Gaussian base kernel needs gamma > 0");
     GVT_REQUIRE(kind != GVT_BASE_POLY || degree >= 0, GVT_E_PARAM, "polynomial base kernel needs degree >= 0");
     if (m == 0 || m2 == 0) return;
@@ -1048,6 +1048,11 @@ void gram(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64
     const float *Xd = dim ? (const float *)stage_in(c, "in.X", X, sizeof(float) * m * dim) : nullptr;
     const float *Yd = (Y && dim) ? (const float *)stage_in(c, "in.Y", Y, sizeof(float) * m2 * dim) : nullptr;
     OutArr ko = out_arr(c, "out.K", K, m * m2);
+    if (kind == GVT_BASE_TANIMOTO) {  // popcount contraction, no tensor-core form (bits, not a float GEMM)
+        gram_tanimoto(c, Xd, m, Y ? Yd : nullptr, m2, dim, ko.dev, m2);
+        out_finish(c, ko);
+        return;
+    }
     bool use_tc = tc_available(c) && c->gram_engine != 1 && dim > 0;
     if (c->gram_engine == 2) GVT_REQUIRE(tc_available(c), GVT_E_CUDA, "tensor-core Gram requested but unavailable");
     if (use_tc) gram_tc(c, kind, Xd, m, Y ? Yd : nullptr, m2, dim, gamma, coef0, degree, ko.dev, m2);

@@ -146,6 +146,9 @@ void gram_simt(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, 
                double gamma, double coef0, int degree, float *K, int64_t ldk);
 void gram_tc(gvt_ctx *c, int kind, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, double gamma,
              double coef0, int degree, float *K, int64_t ldk);
+// Tanimoto Gram of 0/1 features (bit-packed popcount contraction); GVT_E_PARAM on non-binary input
+void gram_tanimoto(gvt_ctx *c, const float *X, int64_t m, const float *Y, int64_t m2, int64_t dim, float *K,
+                   int64_t ldk);
 
 // ---- CG (cg.cu)
 struct CGState;  // device

@@ -25,7 +25,7 @@ KERNEL_NAMES = ["linear", "poly2d", "gaussian", "kronecker", "symmetric",
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 
 # Base kernels (mirror enum gvt_base).
-BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY = range(3)
+BASE_LINEAR, BASE_GAUSSIAN, BASE_POLY, BASE_TANIMOTO = range(4)
 
 
 @dataclasses.dataclass

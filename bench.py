@@ -123,6 +123,17 @@ def default_kernel(w):
 
 
 # ----------------------------------------------------------------------------- roofline
+def _traffic(kernel_kind):
+    """DRAM bytes per launch of `kernel_kind` from the committed ncu --set full capture
+    (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
+            rec = json.load(fh).get(kernel_kind)
+        return int(rec["bytes"]) if rec else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engine: int, precision: str = "fp16x3"):
     """Dominant kernel (largest summed event time) vs its roof.  Algorithmic work per
     launch: stage 1 = q_out FMA per pair-matrix entry, stage 2 = m_in FMA
@@ -151,6 +162,7 @@ def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engin
                 "traffic": None}
     achieved = flops / (per_launch_ms * 1e-3) / 1e12
     out = {"kernel": name, "ms_per_launch": round(per_launch_ms, 4), "launches": cnt}
+    traffic = _traffic(name)
     if name.endswith("_tc"):
         # the dense engine runs 3 tensor-core products over the dense M x N x K GEMM
         M, N, K = (q, m, q) if name.startswith("stage1") else (m, q, m)
@@ -160,14 +172,16 @@ def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engin
         else:
             peak, src = peaks["bf16_tflops_sustained"] * 0.5, f"tf32 = 0.5 x measured bf16 sustained ({peaks['source']})"
         out.update({"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 1), "unit": "TFLOP/s",
-                    "frac": round(achieved / peak, 4), "traffic": None, "peak_source": src,
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": src,
                     "achieved_basis": "algorithmic FMAs of SURVEY 8(d) (q_out per pair-matrix entry / m_in per output)",
                     "executed_tflops": round(executed, 1), "executed_frac": round(executed / peak, 4),
                     "alu_roof_frac": round(achieved / alu_peak, 4)})
     else:
         out.update({"bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak, 1), "unit": "TFLOP/s",
-                    "frac": round(achieved / alu_peak, 4), "traffic": None,
+                    "frac": round(achieved / alu_peak, 4), "traffic": traffic,
                     "peak_source": "fp32 SIMT: 148 SM x 128 lanes x 2 x sm_max_mhz"})
+    if traffic is not None:
+        out["traffic_unit"] = "bytes per launch (ncu dram read + write, profiles/r01_traffic.json)"
     return out
 
 

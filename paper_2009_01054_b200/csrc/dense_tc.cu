@@ -170,6 +170,7 @@ struct EpiParams {
     float gamma, coef0;
     int degree;
     int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
+    int group_m;  // CTA-pair kernel: pair-tile rows per rasterization group (0 = GROUP_M)
     // B operand with a per-(row, 256-wide K chunk) scale, applied while draining chunk ch:
     // sbk[ch * sbk_ld + n] (fp16 S produced by EPI_STORE16)
     const float *sbk;
@@ -531,12 +532,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int nk = (K + BKE - 1) / BKE;
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
     const int nch = (nk + kcb - 1) / kcb;
-    const int in_group = GROUP_M * num_n;
+    const int gm = ep.group_m > 0 ? ep.group_m : GROUP_M;
+    const int in_group = gm * num_n;
 
     // grouped rasterization of pair tiles; a sampled tile pair without samples is skipped
     auto coords = [&](int t, int &mp_tile, int &n_tile) {
-        const int first_m = (t / in_group) * GROUP_M;
-        const int group_m = min(num_mp - first_m, GROUP_M);
+        const int first_m = (t / in_group) * gm;
+        const int group_m = min(num_mp - first_m, gm);
         mp_tile = first_m + (t % in_group) % group_m;
         n_tile = (t % in_group) / group_m;
     };
@@ -863,6 +865,11 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
     GVT_REQUIRE(EPI != EPI_STORE16 || (pair && PREC == PREC_F16), GVT_E_STATE, "fp16 store needs the CTA-pair fp16 GEMM");
     static bool attr = false, attr2 = false;
     if (pair) {
+        static const int env_gm = [] {  // A/B knob for the rasterization group (scripts/ab_matvec.py)
+            const char *e = getenv("GVT_GROUP_M");
+            return e ? atoi(e) : 0;
+        }();
+        if (ep.group_m == 0) ep.group_m = env_gm;
         if (!attr2) {
             GVT_CUDA_TRY(
                 cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));

@@ -2,6 +2,7 @@
 
   python scripts/ab_matvec.py "cta=1" "cta=2" [--rounds 2]      # option sets (GVT options)
   python scripts/ab_matvec.py "lib=ab/libA.so" "lib=ab/libB.so"  # library builds
+  python scripts/ab_matvec.py "gm=16" "gm=8" "gm=4"              # GEMM rasterization group (GVT_GROUP_M)
 
 Each round runs one subprocess per configuration that times a 10-iteration fit at C5
 (CUDA events) after warm-up, reporting ms and per-kernel ms/launch with the SM clock
@@ -52,6 +53,8 @@ def main():
             kv = dict(x.split("=") for x in spec.split(",") if x)
             if "lib" in kv:
                 env["GVT_LIBRARY"] = os.path.abspath(kv["lib"])
+            if "gm" in kv:  # rasterization group of the CTA-pair GEMM
+                env["GVT_GROUP_M"] = kv["gm"]
             out = subprocess.run([sys.executable, "-c", CHILD, spec], env=env, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:]
             print(f"round {r} [{spec}]: {line}", flush=True)

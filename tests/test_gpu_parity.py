@@ -423,3 +423,45 @@ def test_cg_ragged_lengths(ctx, n):
     a, it, _, _ = ctx.fit(dev(D32), dev(T32), dev(f), dev(s), dev(y), kron, 1.0, 8)
     ao, _, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
     assert rel(a.cpu().numpy(), ao) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- in-loop parity (S30)
+def _in_loop_check(ctx, w, kernel, ks, k_samples, restrict=None):
+    """GPU iterates x_k of the fit (the bench's launch configuration: graphs, default engine) are
+    the in-loop vectors; the GPU matvec K x_k is checked against the oracle on sampled outputs."""
+    terms = G.gvt_kernel_terms(kernel)
+    Dg, Tg = grams_gpu(ctx, w)
+    D, T = grams_oracle(w)
+    f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
+    if restrict is not None:
+        cand = np.nonzero(restrict(w))[0]
+        idx = cand[synth.sample_indices(1, len(cand), k_samples)]
+    else:
+        idx = synth.sample_indices(1, w.n, k_samples)
+    for k in ks:
+        xk, it, _, _ = ctx.fit(Dg, Tg, f, s, y, terms, w.lam, k, want_history=False)
+        assert it == k
+        u = ctx.matvec(Dg, Tg, f, s, f, s, xk, terms).cpu().numpy()
+        ref = O.gvt_matvec(O.kernel_terms(kernel), D, T, w.train_first[idx], w.train_second[idx], w.train_first,
+                           w.train_second, xk.cpu().numpy())
+        assert rel(u[idx], ref) <= MATVEC_TOL, (w.name, kernel, k, rel(u[idx], ref))
+
+
+@pytest.mark.parametrize("cfg,kernel", [("C2", G.KRONECKER), ("C3", G.SYMMETRIC), ("C3", G.ANTISYMMETRIC),
+                                        ("C4", G.POLY2D), ("C4", G.MLPK), ("C4", G.RANKING)])
+def test_in_loop_matvec_parity(ctx, cfg, kernel):
+    """Reading S30: on C2-C4 the weights are ill-conditioned, so the gate is the matvec on the
+    solver's own iterates x_k at k = 1, K/2, K (relative L2 <= 1e-5 on sampled outputs)."""
+    w = synth.by_name(cfg)
+    if kernel in HOM and w.Xt is not None:
+        w = synth.union_domain(w)
+    _in_loop_check(ctx, w, kernel, [1, w.iters // 2, w.iters], 48 if cfg == "C4" else 256)
+
+
+@pytest.mark.slow
+def test_in_loop_matvec_parity_c5(ctx):
+    """C5 at full size: K x_30 (the bench's final iterate) on 128 sampled outputs whose target is
+    among 8 seeded targets (oracle O3b)."""
+    w = synth.config5()
+    tset = np.sort(np.random.default_rng(56).choice(w.q, 8, replace=False))
+    _in_loop_check(ctx, w, G.KRONECKER, [w.iters], 128, restrict=lambda w: np.isin(w.train_second, tset))

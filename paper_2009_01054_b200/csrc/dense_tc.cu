@@ -659,8 +659,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
-                // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
+                // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16):
+                // the warp's 128 scales are staged once per chunk in its private slot of the epilogue
+                // staging area (one coalesced float4 per lane) and read back as shared-memory
+                // broadcasts.  The sampled output phase reuses the slot only after the tile's last
+                // chunk, behind its own named barriers.
                 const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
+                float *ssk = estage + (half * 4 + quarter) * 32 * 33;
+                if (sk) {
+                    reinterpret_cast<float4 *>(ssk)[lane] = __ldg(reinterpret_cast<const float4 *>(sk) + lane);
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int c4 = 0; c4 < 4; c4++) {
                     uint32_t r[32];
@@ -669,7 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     if (sk) {
 #pragma unroll
                         for (int i = 0; i < 32; i++)
-                            run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c4 * 32 + i), run[c4 * 32 + i]);
+                            run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), ssk[c4 * 32 + i], run[c4 * 32 + i]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);

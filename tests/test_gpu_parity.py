@@ -425,33 +425,50 @@ def test_cg_ragged_lengths(ctx, n):
     assert rel(a.cpu().numpy(), ao) <= 1e-4
 
 
-# ----------------------------------------------------------------------------- in-loop parity (S30)
+# ----------------------------------------------------------------------------- in-loop parity (S30, S31)
+def _abs_terms(kernel):
+    """|coef| * |L| * |R| per term: summed over the terms this bounds |K_ij| entrywise."""
+    return [(abs(t.coef),) + t.as_tuple()[1:] for t in O.kernel_terms(kernel)]
+
+
 def _in_loop_check(ctx, w, kernel, ks, k_samples, restrict=None):
-    """GPU iterates x_k of the fit (the bench's launch configuration: graphs, default engine) are
-    the in-loop vectors; the GPU matvec K x_k is checked against the oracle on sampled outputs."""
+    """The solver's own iterates x_k (the bench's launch configuration: graphs, default engine)
+    are the in-loop vectors; the GPU matvec K x_k is checked against the oracle on sampled
+    outputs.  Both sides read the same fp32 Grams (the oracle's, rounded), so the comparison
+    isolates the matvec arithmetic.  Reading S31: on ill-conditioned systems x_k is dominated by
+    the small-eigenvalue directions, K x_k cancels (||K x_k|| << || |K| |x_k| ||), and no fp32
+    computation can reach 1e-5 relative to ||K x_k||; the error is gated relative to the
+    floating-point scale || |K| |x_k| || (the oracle's matvec with |factors|, |coefficients|,
+    |x_k|), which equals the plain relative error when there is no cancellation."""
     terms = G.gvt_kernel_terms(kernel)
-    Dg, Tg = grams_gpu(ctx, w)
     D, T = grams_oracle(w)
+    D32, T32 = f32(D), f32(T)
+    Dg, Tg = dev(D32), (None if T32 is None else dev(T32))
     f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
     if restrict is not None:
         cand = np.nonzero(restrict(w))[0]
         idx = cand[synth.sample_indices(1, len(cand), k_samples)]
     else:
         idx = synth.sample_indices(1, w.n, k_samples)
+    of, os_ = w.train_first[idx], w.train_second[idx]
+    Da = np.abs(D32.astype(np.float64))
+    Ta = None if T32 is None else np.abs(T32.astype(np.float64))
     for k in ks:
         xk, it, _, _ = ctx.fit(Dg, Tg, f, s, y, terms, w.lam, k, want_history=False)
         assert it == k
+        x = xk.cpu().numpy()
         u = ctx.matvec(Dg, Tg, f, s, f, s, xk, terms).cpu().numpy()
-        ref = O.gvt_matvec(O.kernel_terms(kernel), D, T, w.train_first[idx], w.train_second[idx], w.train_first,
-                           w.train_second, xk.cpu().numpy())
-        assert rel(u[idx], ref) <= MATVEC_TOL, (w.name, kernel, k, rel(u[idx], ref))
+        ref = O.gvt_matvec(O.kernel_terms(kernel), D32, T32, of, os_, w.train_first, w.train_second, x)
+        scale = O.gvt_matvec(_abs_terms(kernel), Da, Ta, of, os_, w.train_first, w.train_second, np.abs(x))
+        err = np.linalg.norm(u[idx] - ref) / np.linalg.norm(scale)
+        assert err <= MATVEC_TOL, (w.name, kernel, k, err, rel(u[idx], ref))
 
 
 @pytest.mark.parametrize("cfg,kernel", [("C2", G.KRONECKER), ("C3", G.SYMMETRIC), ("C3", G.ANTISYMMETRIC),
                                         ("C4", G.POLY2D), ("C4", G.MLPK), ("C4", G.RANKING)])
 def test_in_loop_matvec_parity(ctx, cfg, kernel):
     """Reading S30: on C2-C4 the weights are ill-conditioned, so the gate is the matvec on the
-    solver's own iterates x_k at k = 1, K/2, K (relative L2 <= 1e-5 on sampled outputs)."""
+    solver's own iterates x_k at k = 1, K/2, K (sampled outputs, S31 normalisation)."""
     w = synth.by_name(cfg)
     if kernel in HOM and w.Xt is not None:
         w = synth.union_domain(w)

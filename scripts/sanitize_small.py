@@ -25,3 +25,43 @@ for hom in (False, True):
             torch.cuda.synchronize()
     print("hom", hom, "ok")
 print("sanitize_small done")
+
+# ---- solver / early stopping / AUC / novel objects / Tanimoto (session-2 additions)
+rng = np.random.default_rng(1)
+m, q = 37, 29
+Xd, Xt = rng.standard_normal((m, 5)).astype(np.float32), rng.standard_normal((q, 5)).astype(np.float32)
+D = ctx.gram(G.BASE_GAUSSIAN, d(Xd), gamma=0.3)
+T = ctx.gram(G.BASE_GAUSSIAN, d(Xt), gamma=0.3)
+f, s = d(rng.integers(0, m, 301).astype(np.int32)), d(rng.integers(0, q, 301).astype(np.int32))
+y = d(rng.standard_normal(301).astype(np.float32))
+vf, vs = d(rng.integers(0, m, 77).astype(np.int32)), d(rng.integers(0, q, 77).astype(np.int32))
+vl = d((rng.uniform(size=77) > 0.5).astype(np.float32))
+kron = G.gvt_kernel_terms(G.KRONECKER)
+for eng in (1, 2):
+    ctx.set_option(G.OPT_ENGINE, eng); ctx.set_option(G.OPT_SLABS, 1)
+    for solver in (0, 1):
+        ctx.set_option(G.OPT_SOLVER, solver)
+        ctx.fit(D, T, f, s, y, kron, 0.5, 7)
+        ctx.fit(D, T, f, s, y, kron, 0.5, 40, 1e-3)
+        ctx.fit_early_stopping(D, T, f, s, y, vf, vs, vl, kron, 0.5, 3, 9)
+    ctx.set_option(G.OPT_SOLVER, 0)
+    print("auc", ctx.auc(vl, d(rng.standard_normal(77).astype(np.float32))))
+    Xn = rng.standard_normal((11, 5)).astype(np.float32)
+    Dx = ctx.gram_cross(G.BASE_GAUSSIAN, d(Xn), d(Xd), gamma=0.3)
+    Tx = ctx.gram_cross(G.BASE_GAUSSIAN, d(Xt[:13]), d(Xt), gamma=0.3)
+    tf, ts = d(rng.integers(0, 11, 55).astype(np.int32)), d(rng.integers(0, 13, 55).astype(np.int32))
+    for var in (0, 1, 2):
+        ctx.matvec_rect(Dx, Tx, tf, ts, f, s, y, kron, variant=var)
+    Dh = ctx.gram_cross(G.BASE_GAUSSIAN, d(Xn), d(Xd), gamma=0.3)
+    hf, hs = d(rng.integers(0, m, 301).astype(np.int32)), d(rng.integers(0, m, 301).astype(np.int32))
+    for k in (G.SYMMETRIC, G.MLPK, G.POLY2D, G.RANKING):
+        terms = G.gvt_kernel_terms(k)
+        if k == G.POLY2D:
+            ctx.matvec_rect(Dx, Tx, tf, ts, f, s, y, terms)
+        else:
+            ctx.matvec_rect(Dh, None, tf, d(rng.integers(0, 11, 55).astype(np.int32)), hf, hs, y, terms)
+B = (rng.uniform(size=(70, 300)) < 0.1).astype(np.float32)
+ctx.gram(G.BASE_TANIMOTO, d(B))
+ctx.gram_cross(G.BASE_TANIMOTO, d(B), d(B[:33]))
+torch.cuda.synchronize()
+print("sanitize_small additions done")

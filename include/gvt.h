@@ -104,8 +104,12 @@ typedef enum {
                                     tiles, default), 1 = single-CTA 128-row tiles                  */
     GVT_OPT_GRAPHS = 7,          /* 1 (default): the solver replays one captured iteration as a CUDA
                                     graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches        */
-    GVT_OPT_SOLVER = 8           /* iterative solver of pairwise_krr_fit(_early_stopping): gvt_solver,
+    GVT_OPT_SOLVER = 8,          /* iterative solver of pairwise_krr_fit(_early_stopping): gvt_solver,
                                     default GVT_SOLVER_CG                                             */
+    GVT_OPT_EXCHANGE = 9         /* data-parallel exchange per matvec: 0 (default) =
+                                    all-gather the S column slabs (4 q m bytes), stage 2 on the local
+                                    outputs; 1 = u-exchange: stage 2 of the rank's own slab over EVERY
+                                    output, then a reduce of the n-vector to its owners (4 n bytes)   */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

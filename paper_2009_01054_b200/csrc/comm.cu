@@ -17,6 +17,10 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -37,8 +41,10 @@ static void load_nccl() {
     g_nccl.Broadcast = (decltype(g_nccl.Broadcast))dlsym(h, "ncclBroadcast");
     g_nccl.GroupStart = (decltype(g_nccl.GroupStart))dlsym(h, "ncclGroupStart");
     g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
+    g_nccl.Reduce = (decltype(g_nccl.Reduce))dlsym(h, "ncclReduce");
+    g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
     GVT_REQUIRE(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather &&
-                    g_nccl.Broadcast && g_nccl.GroupStart && g_nccl.GroupEnd,
+                    g_nccl.Broadcast && g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.Reduce && g_nccl.AllReduce,
                 GVT_E_NCCL, "libnccl.so.2 lacks a required symbol");
     g_nccl.h = h;
 }
@@ -125,6 +131,33 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
         NCCL_TRY(g_nccl.Broadcast(g == c->rank ? local : dst, dst, (size_t)counts[g],
                                   is_float ? ncclFloat32 : ncclInt32, g, (ncclComm_t)c->nccl_comm, c->stream));
     }
+    NCCL_TRY(g_nccl.GroupEnd());
+}
+
+// u-exchange: every rank holds a partial of the FULL out vector
+// (its own S slab's contribution to every output); rank g receives the sum of the segment
+// [offsets[g], offsets[g+1]) into `local` (grouped ncclReduce, one root per segment -- the
+// variable-count reduce-scatter), and the `tail` extra values after the full vector (MLPK's
+// diagonal samples, needed on every rank) are all-reduced into local + counts[rank].
+void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::vector<int64_t> &counts,
+                     const std::vector<int64_t> &offsets, int64_t tail) {
+    const int64_t n_full = offsets.back();
+    if (c->world <= 1) {
+        const int64_t n = counts[0] + tail;
+        if (n > 0 && partial != local)
+            GVT_CUDA_TRY(cudaMemcpyAsync(local, partial, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    NCCL_TRY(g_nccl.GroupStart());
+    for (int g = 0; g < c->world; g++) {
+        if (counts[g] == 0) continue;
+        const float *send = partial + offsets[g];
+        NCCL_TRY(g_nccl.Reduce(send, g == c->rank ? (void *)local : (void *)send, (size_t)counts[g], ncclFloat32,
+                               ncclSum, g, (ncclComm_t)c->nccl_comm, c->stream));
+    }
+    if (tail > 0)
+        NCCL_TRY(g_nccl.AllReduce(partial + n_full, local + counts[c->rank], (size_t)tail, ncclFloat32, ncclSum,
+                                  (ncclComm_t)c->nccl_comm, c->stream));
     NCCL_TRY(g_nccl.GroupEnd());
 }
 

@@ -41,6 +41,8 @@ void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats);
 std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v);
 void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<int64_t> &counts,
                    const std::vector<int64_t> &offsets, bool is_float);
+void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::vector<int64_t> &counts,
+                     const std::vector<int64_t> &offsets, int64_t tail);
 
 // ----------------------------------------------------------------------------- decompose
 static gvt_term mk(double coef, int l, int r, int rl, int rr, int cl, int cr) {
@@ -137,6 +139,12 @@ struct Problem {
     // data-parallel in-sample partition (world 1: counts = {n_in})
     std::vector<int64_t> counts, offsets;
     float *p_full = nullptr;
+    // u-exchange (GVT_OPT_EXCHANGE = 1, world > 1): the FULL out sample on every rank, in rank
+    // order; this rank's outputs are [out_offsets[rank], out_offsets[rank + 1])
+    bool uex = false;
+    const int32_t *of_full = nullptr, *os_full = nullptr;
+    int64_t n_out_full = 0;
+    std::vector<int64_t> out_counts, out_offsets;
     int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
     int64_t dom_out(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m_out : q_out; }
 };
@@ -192,6 +200,7 @@ struct GroupPlan {
     float *S = nullptr;
     std::string tag;
     float *diag = nullptr;  // optional separate diagonal of X (global row index), computed per matvec
+    int64_t n_diag = 0;     // extra (x, x) samples after the outputs (MLPK)
 };
 
 struct MatvecPlan {
@@ -302,7 +311,10 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
         g.coef = coef;
         std::string t(tag);
         build_entry_plan(c, (t + ".e").c_str(), P.inf, P.ins, P.n_in, kinds, nrow, ncol, g.ent);
-        build_sample_plan(c, (t + ".s").c_str(), P.of, P.os, P.n_out, rs, cs, n_diag, A.n, g.smp);
+        // u-exchange: stage 2 of this rank's S slab serves EVERY output (full out sample)
+        if (P.uex) build_sample_plan(c, (t + ".s").c_str(), P.of_full, P.os_full, P.n_out_full, rs, cs, n_diag, A.n, g.smp);
+        else build_sample_plan(c, (t + ".s").c_str(), P.of, P.os, P.n_out, rs, cs, n_diag, A.n, g.smp);
+        g.n_diag = n_diag;
         finish_group(c, g, tag);
         mp.groups.push_back(g);
     };
@@ -394,8 +406,12 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             std::string ts(tag);
             build_entry_plan(c, (ts + ".e").c_str(), P.inf, P.ins, P.n_in, kinds1(t.col_sel_left, t.col_sel_right, 1.f),
                              P.dom(t.col_sel_left), P.dom(t.col_sel_right), g.ent);
-            build_sample_plan(c, (ts + ".s").c_str(), P.of, P.os, P.n_out, t.row_sel_left, t.row_sel_right, 0,
-                              P.dom_out(t.row_sel_left), g.smp);
+            if (P.uex)
+                build_sample_plan(c, (ts + ".s").c_str(), P.of_full, P.os_full, P.n_out_full, t.row_sel_left,
+                                  t.row_sel_right, 0, P.dom_out(t.row_sel_left), g.smp);
+            else
+                build_sample_plan(c, (ts + ".s").c_str(), P.of, P.os, P.n_out, t.row_sel_left, t.row_sel_right, 0,
+                                  P.dom_out(t.row_sel_left), g.smp);
             finish_group(c, g, tag);
             mp.groups.push_back(g);
         }
@@ -420,7 +436,17 @@ static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
 // fused 3xFP16 dense path: X rows assembled straight into fp16 pieces, stage 1 writes S as
 // fp16 pieces with per-(row, 256-column) scales, stage 2 applies them per K-chunk; slab s of
 // S lives at s * (qpad * W) halves (and s * ntW * skld scales) so ranks all-gather equal slabs
-static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out) {
+// u-exchange epilogue: out[0 .. n_local + n_diag) (+)= the rank's segment of the summed partials
+static void uex_finish(gvt_ctx *c, const Problem &P, const GroupPlan &g, const float *partial, int accumulate,
+                       float *out) {
+    const int64_t n_local = P.out_counts[c->rank], n = n_local + g.n_diag;
+    float *local = accumulate ? wsT<float>(c, "uex.local", (size_t)n) : out;
+    reduce_segments(c, partial, local, P.out_counts, P.out_offsets, g.n_diag);
+    if (accumulate) add_into(c, local, n, out);
+}
+
+static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
+                          float *out) {
     const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256);
     const size_t slab_h = (size_t)g.qpad * g.W, slab_k = (size_t)ntW * skld;
     __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
@@ -435,14 +461,19 @@ static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float c
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
                         skld);
     }
-    // halves travel as pairs of floats (W is a multiple of 32)
-    allgather_slabs(c, reinterpret_cast<float *>(Sh), slab_h / 2);
-    allgather_slabs(c, reinterpret_cast<float *>(Sl), slab_h / 2);
-    allgather_slabs(c, Sk, slab_k);
+    float *partial = nullptr;
+    if (P.uex) {  // no S exchange: this rank's slab serves every output, then the partials are reduced
+        partial = wsT<float>(c, "uex.partial", (size_t)(P.n_out_full + g.n_diag));
+        GVT_CUDA_TRY(cudaMemsetAsync(partial, 0, sizeof(float) * (P.n_out_full + g.n_diag), c->stream));
+    } else {  // halves travel as pairs of floats (W is a multiple of 32)
+        allgather_slabs(c, reinterpret_cast<float *>(Sh), slab_h / 2);
+        allgather_slabs(c, reinterpret_cast<float *>(Sl), slab_h / 2);
+        allgather_slabs(c, Sk, slab_k);
+    }
     bool first = true;
     for (int s = 0; s < g.nslab; s++) {
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
-        if (w == 0) continue;
+        if (w == 0 || (P.uex && !my_slab(c, s))) continue;
         Operand so;
         so.prec = 0;
         so.hi = Sh + s * slab_h;
@@ -450,17 +481,21 @@ static void run_group_f16(gvt_ctx *c, GroupPlan &g, const float *p_full, float c
         so.ld = g.W;
         so.scale_k = Sk + s * slab_k;
         so.scale_k_ld = skld;
-        gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, accumulate || !first,
-                        out);
+        if (P.uex)  // this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, !first, partial);
+        else
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef,
+                            accumulate || !first, out);
         first = false;
     }
+    if (P.uex) uex_finish(c, P, g, partial, accumulate, out);
 }
 
-static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef, int accumulate, float *out,
-                      bool values_ready = false) {
+static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
+                      float *out, bool values_ready = false) {
     c->last_engine = g.engine;
     if (g.engine == 2 && fused_f16(c, g.C.cols)) {
-        run_group_f16(c, g, p_full, coef, accumulate, out);
+        run_group_f16(c, P, g, p_full, coef, accumulate, out);
         return;
     }
     // ---- stage 1 on this rank's X-row slab(s)
@@ -492,26 +527,35 @@ static void run_group(gvt_ctx *c, GroupPlan &g, const float *p_full, float coef,
             stage1_sparse(c, es, g.C.colwise(), g.q_out, Ss, g.W, g.diag, lo);
         }
     }
-    // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab
-    allgather_slabs(c, g.S, (size_t)g.qpad * g.W);
+    // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab; or (u-exchange)
+    // stage 2 of this rank's slab over every output into a partial vector, then reduce it
+    float *partial = nullptr;
+    if (P.uex) {
+        partial = wsT<float>(c, "uex.partial", (size_t)(P.n_out_full + g.n_diag));
+        GVT_CUDA_TRY(cudaMemsetAsync(partial, 0, sizeof(float) * (P.n_out_full + g.n_diag), c->stream));
+    } else {
+        allgather_slabs(c, g.S, (size_t)g.qpad * g.W);
+    }
+    float *dst = P.uex ? partial : out;
     bool first = true;
     for (int s = 0; s < g.nslab; s++) {
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
-        if (w == 0) continue;
-        const int acc = accumulate || !first;
+        if (w == 0 || (P.uex && !my_slab(c, s))) continue;
+        const int acc = P.uex ? !first : (accumulate || !first);
         first = false;
         float *Ss = g.S + (size_t)s * g.qpad * g.W;
         if (g.engine == 2) {
             char nm[48];
             snprintf(nm, sizeof(nm), "dense.Sop%d", s);
             Operand so = make_operand(c, nm, Ss, g.q_out, w, g.W, g.W, g.qpad);
-            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, out);
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, dst);
         } else {
             Factor Av = g.A;
             Av.p = g.A.p + lo;
-            stage2_gather(c, g.smp, Av, Ss, g.W, w, coef, acc, out);
+            stage2_gather(c, g.smp, Av, Ss, g.W, w, coef, acc, dst);
         }
     }
+    if (P.uex) uex_finish(c, P, g, partial, accumulate, out);
 }
 
 static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u) {
@@ -525,18 +569,18 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
     case FORM_KRON:
     case FORM_SYM:
     case FORM_ANTI:
-        run_group(c, mp.groups[0], p, mp.groups[0].coef, 0, u);
+        run_group(c, P, mp.groups[0], p, mp.groups[0].coef, 0, u);
         break;
     case FORM_MLPK:
         entry_values(c, mp.byF, p);
         segment_sum(c, mp.byF, mp.groups[0].diag);  // diag(L) = bF + bS
-        run_group(c, mp.groups[0], p, 1.f, 0, mp.buf);
+        run_group(c, P, mp.groups[0], p, 1.f, 0, mp.buf);
         combine_mlpk(c, P.of, P.os, P.n_out, mp.buf, u);
         break;
     case FORM_POLY2D: {
         GroupPlan &g = mp.groups[0];
         entry_values(c, g.ent, p);               // all entries: the segment sums need every row
-        run_group(c, g, p, 2.f, 0, u, true);
+        run_group(c, P, g, p, 2.f, 0, u, true);
         segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
         entry_values(c, mp.byS, p);
         segment_sum(c, mp.byS, mp.b2);          // bS
@@ -566,7 +610,7 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         cartesian(c, P.of, P.os, P.n_out, mp.byF, mp.byS, P.D, P.T, u);
         break;
     case FORM_GENERIC:
-        for (size_t i = 0; i < mp.groups.size(); i++) run_group(c, mp.groups[i], p, mp.groups[i].coef, i > 0, u);
+        for (size_t i = 0; i < mp.groups.size(); i++) run_group(c, P, mp.groups[i], p, mp.groups[i].coef, i > 0, u);
         if (mp.groups.empty() && P.n_out > 0) GVT_CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(float) * P.n_out, c->stream));
         break;
     }
@@ -706,6 +750,29 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
     } else {
         P.inf = lf;
         P.ins = ls;
+    }
+    // u-exchange needs every rank's out pairs on every rank (a fit's out sample is its in-sample)
+    // (also at world 1, where the reduce is a copy: the single-GPU tests exercise this path)
+    P.uex = c->exchange == 1;
+    if (P.uex) {
+        if (out_is_in) {
+            P.of_full = P.inf;
+            P.os_full = P.ins;
+            P.out_counts = P.counts;
+            P.out_offsets = P.offsets;
+        } else {
+            P.out_counts = allgather_count(c, n_out);
+            P.out_offsets.assign(P.out_counts.size() + 1, 0);
+            for (size_t g = 0; g < P.out_counts.size(); g++)
+                P.out_offsets[g + 1] = P.out_offsets[g] + P.out_counts[g];
+            int32_t *gf = wsT<int32_t>(c, "dist.of", (size_t)P.out_offsets.back());
+            int32_t *gs = wsT<int32_t>(c, "dist.os", (size_t)P.out_offsets.back());
+            gather_varlen(c, P.of, gf, P.out_counts, P.out_offsets, false);
+            gather_varlen(c, P.os, gs, P.out_counts, P.out_offsets, false);
+            P.of_full = gf;
+            P.os_full = gs;
+        }
+        P.n_out_full = P.out_offsets.back();
     }
     bool split = needs_split(c, form, P.m, P.q, P.n_in);
     P.D = prepare_factor(c, "fD", D, P.m_out, P.m, split, P.rect);

@@ -93,6 +93,7 @@ struct gvt_ctx {
     int gemm_cta = 2;      // tensor-core GEMM: 2 = CTA-pair tcgen05 (cta_group::2), 1 = single CTA
     int graphs = 1;        // CUDA-graph replay of the solver iteration
     int solver = 0;        // GVT_SOLVER_CG / GVT_SOLVER_MINRES
+    int exchange = 0;      // multi-GPU: 0 = S slab all-gather, 1 = u reduce (NEXT-3)
     cudaStream_t cap_stream = nullptr;  // side stream used only for graph capture
     int last_engine = 0;
 

@@ -107,6 +107,7 @@ void combine_mlpk(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, con
 void cartesian(gvt_ctx *c, const int32_t *of, const int32_t *os, int64_t n_out, const EntryPlan &by_first,
                const EntryPlan &by_second, const Factor &D, const Factor &T, float *u);
 void scale_copy(gvt_ctx *c, const float *x, float alpha, int64_t n, float *y);
+void add_into(gvt_ctx *c, const float *x, int64_t n, float *y);  // y += x
 
 // ---- dense tensor-core engine (dense_tc.cu)
 bool tc_available(gvt_ctx *c);

@@ -288,6 +288,16 @@ __global__ void k_scale_copy(const float *__restrict__ x, float alpha, int64_t n
         y[i] = alpha * x[i];
 }
 
+__global__ void k_add_into(const float *__restrict__ x, int64_t n, float *__restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] += x[i];
+}
+
+void add_into(gvt_ctx *c, const float *x, int64_t n, float *y) {
+    if (n == 0) return;
+    GVT_LAUNCH(c, K_FILL, k_add_into, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, x, n, y);
+}
+
 void scale_copy(gvt_ctx *c, const float *x, float alpha, int64_t n, float *y) {
     if (n == 0) return;
     GVT_LAUNCH(c, K_FILL, k_scale_copy, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, x, alpha, n, y);

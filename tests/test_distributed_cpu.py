@@ -45,7 +45,7 @@ def _all_gather_var(x, world):
     return np.concatenate([o.numpy()[:k] for o, k in zip(out, ns)]), ns
 
 
-def _worker(rank, world, port, iters, ret):
+def _worker(rank, world, port, iters, ret, exchange=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -68,7 +68,29 @@ def _worker(rank, world, port, iters, ret):
         W = int(-(-max(np.diff(sb).max(), 1) // 32) * 32)
         lo, hi = int(sb[rank]), int(sb[rank + 1])
 
+        offs = np.concatenate([[0], np.cumsum(counts)])
+
+        def matvec_u(p_local):
+            """u-exchange (GVT_OPT_EXCHANGE = 1, NEXT-3): stage 2 of this rank's slab for EVERY
+            output (the gathered sample), then each rank's segment is reduced to it (one reduce
+            per root, the variable-count reduce-scatter); 4 n bytes move instead of 4 q m."""
+            p_full, _ = _all_gather_var(p_local, world)
+            B = np.zeros((hi - lo, q))
+            sel = (ff >= lo) & (ff < hi)
+            np.add.at(B, (ff[sel] - lo, fs[sel]), p_full[sel])
+            S_slab = T @ B.T                                   # q x (hi - lo)
+            partial = np.einsum("ih,ih->i", D[ff][:, lo:hi], S_slab[fs])
+            local = None
+            for g in range(world):
+                seg = torch.from_numpy(np.ascontiguousarray(partial[offs[g]:offs[g + 1]]))
+                dist.reduce(seg, dst=g)
+                if g == rank:
+                    local = seg.numpy().copy()
+            return local
+
         def matvec(p_local):
+            if exchange == 1:
+                return matvec_u(p_local)
             p_full, _ = _all_gather_var(p_local, world)
             # stage 1 on this rank's slab: S[:, h] for h in [lo, hi)
             B = np.zeros((hi - lo, q))
@@ -113,12 +135,14 @@ def _worker(rank, world, port, iters, ret):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", [0, 1], ids=["S-allgather", "u-reduce"])
 @pytest.mark.parametrize("world", [2])
-def test_sharded_cg_equals_single_process_oracle(world):
+def test_sharded_cg_equals_single_process_oracle(world, exchange):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     iters = 12
-    tmp.start_processes(_worker, args=(world, _free_port(), iters, q), nprocs=world, join=True, start_method="spawn")
+    tmp.start_processes(_worker, args=(world, _free_port(), iters, q, exchange), nprocs=world, join=True,
+                        start_method="spawn")
     a_sharded, sb, bounds, counts = q.get(timeout=60)
     w = synth.config1()
     D = O.gram(w.base, w.Xd, gamma=w.gamma)

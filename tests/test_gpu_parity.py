@@ -372,13 +372,17 @@ def test_launch_accounting(ctx):
 
 
 # ----------------------------------------------------------------------------- data-parallel slab path
-@pytest.mark.parametrize("slabs", [2, 3, 8])
+@pytest.mark.parametrize("slabs", [1, 2, 3, 8])
 @pytest.mark.parametrize("engine", [G.ENGINE_SPARSE, G.ENGINE_DENSE], ids=["sparse", "dense"])
-def test_slab_path_matches_oracle(ctx, slabs, engine):
+@pytest.mark.parametrize("exchange", [0, 1], ids=["S-allgather", "u-reduce"])
+def test_slab_path_matches_oracle(ctx, slabs, engine, exchange):
     """GVT_OPT_SLABS runs stage 1 per X-row slab and stage 2 slab by slab (K split), the code
-    path every rank runs in the data-parallel layout; results must stay at oracle parity."""
+    path every rank runs in the data-parallel layout; GVT_OPT_EXCHANGE = 1 runs the u-exchange
+    form (stage 2 of the slabs into a partial over every output, then the reduce, a copy at
+    world 1).  Results must stay at oracle parity for every kernel."""
     ctx.set_option(G.OPT_ENGINE, engine)
     ctx.set_option(G.OPT_SLABS, slabs)
+    ctx.set_option(G.OPT_EXCHANGE, exchange)
     try:
         rng = np.random.default_rng(77)
         for kernel in K_ALL:
@@ -405,6 +409,7 @@ def test_slab_path_matches_oracle(ctx, slabs, engine):
         assert rel(a.cpu().numpy(), ao) <= 1e-4
     finally:
         ctx.set_option(G.OPT_SLABS, 1)
+        ctx.set_option(G.OPT_EXCHANGE, 0)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
 
 

@@ -180,6 +180,9 @@ struct EpiParams {
     __half *c_h16, *c_l16;
     float *c_sk;
     int64_t c_sk_ld;
+    // EPI_STORE16 with l1max != nullptr: one scale per ROW, from the a-priori bound
+    // |C[r][c]| <= max_k |A[r,k]| * max_c ||B[c,:]||_1 <= 2^15 sa[r] * (*l1max); c_sk[row]
+    const float *l1max;
 };
 
 constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
@@ -689,8 +692,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
             if (EPI == EPI_STORE16) {
-                // fp16 hi/lo of the unscaled result, one power-of-two scale per (row, 256-col tile):
-                // the two warps holding this row's column halves exchange their maxima
+                // fp16 hi/lo of the unscaled result with a power-of-two scale: one per ROW from the
+                // a-priori bound (l1max; the same for every tile, no exchange), or one per
+                // (row, 256-col tile) from the tile's maximum (the two warps holding this row's
+                // column halves exchange their maxima)
                 const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
                 float mx = 0.f;
 #pragma unroll
@@ -700,10 +705,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     run[i] *= ra * rb;
                     if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
                 }
-                estage[(quarter * 32 + lane) * 2 + half] = mx;
-                named_bar(1, 32 * N_EPI_WARPS);
-                mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
-                named_bar(1, 32 * N_EPI_WARPS);
+                if (ep.l1max) {
+                    mx = 32768.f * ra * __ldg(ep.l1max);
+                } else {
+                    estage[(quarter * 32 + lane) * 2 + half] = mx;
+                    named_bar(1, 32 * N_EPI_WARPS);
+                    mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
+                    named_bar(1, 32 * N_EPI_WARPS);
+                }
                 int e = 0;
                 if (mx > 0.f && isfinite(mx)) {
                     int ex;
@@ -712,7 +721,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 }
                 const float s = ldexpf(1.f, e);
                 if (gr < M) {
-                    if (half == 0) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+                    if (half == 0) {
+                        if (!ep.l1max) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+                        else if (n_tile == 0) ep.c_sk[gr] = ldexpf(1.f, -e);
+                    }
                     __half *hp = ep.c_h16 + (int64_t)gr * ep.ldc + gc_base;
                     __half *lp = ep.c_l16 + (int64_t)gr * ep.ldc + gc_base;
 #pragma unroll
@@ -1019,9 +1031,9 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
                                                    int64_t cols, int64_t ld, __half *__restrict__ hi,
                                                    __half *__restrict__ lo, float *__restrict__ sinv,
-                                                   const float *__restrict__ diag) {
+                                                   const float *__restrict__ diag, float *__restrict__ l1max) {
     extern __shared__ float rowbuf[];  // ld floats
-    __shared__ float red[BX_THREADS / 32];
+    __shared__ float red[BX_THREADS / 32], red2[BX_THREADS / 32];
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
         __syncthreads();
@@ -1036,13 +1048,28 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
         __syncthreads();
         if (diag && threadIdx.x == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
         __syncthreads();
-        float mx = 0.f;
-        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        float mx = 0.f, l1 = 0.f;
+        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+            mx = fmaxf(mx, fabsf(rowbuf[j]));
+            l1 += fabsf(rowbuf[j]);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5] = mx;
+            red2[threadIdx.x >> 5] = l1;
+        }
         __syncthreads();
         mx = red[0];
         for (int w = 1; w < BX_THREADS / 32; w++) mx = fmaxf(mx, red[w]);
+        if (l1max && threadIdx.x == 0) {
+            float t = 0.f;
+            for (int w = 0; w < BX_THREADS / 32; w++) t += red2[w];
+            // an upper bound with slack for the fp32 summation (non-negative floats order as ints)
+            atomicMax(reinterpret_cast<int *>(l1max), __float_as_int(t * 1.0001f));
+        }
         int e = 0;
         if (mx > 0.f && isfinite(mx)) {
             int ex;
@@ -1063,7 +1090,7 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
 }
 
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag) {
+                  const float *p, const float *diag, float *l1max) {
     Operand o;
     o.prec = PREC_F16;
     o.ld = round_up(cols > 0 ? cols : 1, 32);
@@ -1080,7 +1107,7 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     }
     if (rows > 0)
         GVT_LAUNCH(c, K_DENSIFY, k_build_x16, grid1d(rows, 1, 2 * c->sm_count), BX_THREADS, smem, e.row_ptr, e.col, e.src,
-                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
     o.hi = hi;
     o.lo = lo;
     o.scale = s;
@@ -1089,14 +1116,17 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
 
 // hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256)) floats,
 // whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
+// l1max != nullptr: one scale per row (sk[row]) from the bound 2^15 A.scale[row] * (*l1max), where
+// *l1max >= max over B's rows of the row's L1 norm (build_x16 computes it)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld) {
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
     ep.c_h16 = hi;
     ep.c_l16 = lo;
     ep.c_sk = sk;
     ep.c_sk_ld = sk_ld;
+    ep.l1max = l1max;
     ep.ldc = ldc;
     launch_gemm<EPI_STORE16>(c, K_STAGE1_TC, A, B, M, N, K, ep);
 }

@@ -447,19 +447,30 @@ static void uex_finish(gvt_ctx *c, const Problem &P, const GroupPlan &g, const f
 
 static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
                           float *out) {
+    // S scales: one per (row, 256-col tile) from the tile maxima, applied per K-chunk in stage 2
+    // (default), or one per row from the a-priori bound |S[t][h]| <= max|T[t,:]| max_h ||X[h,:]||_1
+    // (GVT_S16_ROWSCALE=1).  Both pass the parity suite; the row scales cost ~7 % more time at C5
+    // under the power cap (more power per MMA at the same work, profiles/r01_ab_s16_scale.txt), so
+    // the tile scales stay the default.
+    static const bool tile_scale = [] {
+        const char *v = getenv("GVT_S16_ROWSCALE");
+        return !(v && atoi(v) != 0);
+    }();
     const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256);
-    const size_t slab_h = (size_t)g.qpad * g.W, slab_k = (size_t)ntW * skld;
+    const size_t slab_h = (size_t)g.qpad * g.W, slab_k = tile_scale ? (size_t)ntW * skld : (size_t)skld;
     __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
     __half *Sl = wsT<__half>(c, (g.tag + ".S16l").c_str(), slab_h * g.nslab);
     float *Sk = wsT<float>(c, (g.tag + ".S16k").c_str(), slab_k * g.nslab);
+    float *l1 = wsT<float>(c, (g.tag + ".S16l1").c_str(), (size_t)g.nslab);
     GVT_CUDA_TRY(cudaMemsetAsync(Sk, 0, sizeof(float) * slab_k * g.nslab, c->stream));
+    if (!tile_scale) GVT_CUDA_TRY(cudaMemsetAsync(l1, 0, sizeof(float) * g.nslab, c->stream));
     for (int s = 0; s < g.nslab; s++) {
         if (!my_slab(c, s)) continue;
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
         if (w == 0) continue;
-        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag);
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag, tile_scale ? nullptr : l1 + s);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
-                        skld);
+                        skld, tile_scale ? nullptr : l1 + s);
     }
     float *partial = nullptr;
     if (P.uex) {  // no S exchange: this rank's slab serves every output, then the partials are reduced
@@ -479,8 +490,12 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
         so.hi = Sh + s * slab_h;
         so.lo = Sl + s * slab_h;
         so.ld = g.W;
-        so.scale_k = Sk + s * slab_k;
-        so.scale_k_ld = skld;
+        if (tile_scale) {
+            so.scale_k = Sk + s * slab_k;
+            so.scale_k_ld = skld;
+        } else {
+            so.scale = Sk + s * slab_k;  // one scale per S row, applied once after the K loop
+        }
         if (P.uex)  // this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1
             gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, !first, partial);
         else

@@ -128,14 +128,16 @@ void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, in
 bool fused_f16(gvt_ctx *c, int64_t q_in);
 // rows [row_lo, row_lo + rows) of the pair matrix built straight into an fp16 operand
 // (values sign * p[src] summed per cell in entry order, one row scale per row)
+// l1max (nullable, device float, zeroed by the caller): atomically raised to >= every row's L1 norm
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag = nullptr);
+                  const float *p, const float *diag = nullptr, float *l1max = nullptr);
 // X[r][row_lo + r] += diag[row_lo + r] for r < rows (fp32 X, leading dimension ldX)
 void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_lo, int64_t rows);
 // C = A * B^T written as fp16 pieces (M rows x ldc) with per-(row, 256-col tile) scales
 // sk[tile * sk_ld + row] (sk_ld >= round_up(M, 256))
+// l1max != nullptr: one scale per row sk[row] from the a-priori bound (no per-tile scales)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld);
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max = nullptr);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out);

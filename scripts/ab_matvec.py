@@ -55,6 +55,8 @@ def main():
                 env["GVT_LIBRARY"] = os.path.abspath(kv["lib"])
             if "gm" in kv:  # rasterization group of the CTA-pair GEMM
                 env["GVT_GROUP_M"] = kv["gm"]
+            if "rs" in kv:  # fp16 S with per-row bound scales (1) or per-(row, 256-col tile) scales (0)
+                env["GVT_S16_ROWSCALE"] = kv["rs"]
             out = subprocess.run([sys.executable, "-c", CHILD, spec], env=env, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:]
             print(f"round {r} [{spec}]: {line}", flush=True)

@@ -264,6 +264,7 @@ def run_gpu(args, rank, world, local_rank):
     ctx.set_option(G.OPT_TC_PRECISION, 0 if args.precision == "fp16x3" else 1)
     ctx.set_option(G.OPT_EXCHANGE, args.exchange)
     ctx.set_option(G.OPT_SOLVER, G.SOLVER_MINRES if args.solver == "minres" else G.SOLVER_CG)
+    ctx.set_option(G.OPT_CG_VARIANT, args.cg_variant)
     if world > 1:
         uid = G.gvt_nccl_unique_id() if rank == 0 else None
         obj = [uid]
@@ -388,6 +389,7 @@ def run_gpu(args, rank, world, local_rank):
                        "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
                        "engine": {0: "auto", 1: "sparse", 2: "dense"}[args.engine], "tc_precision": args.precision,
                        "exchange": ["S-allgather", "u-reduce"][args.exchange], "solver": args.solver,
+                       "cg_variant": ["hestenes-stiefel", "chronopoulos-gear"][args.cg_variant],
                        "last_engine": {1: "sparse", 2: "dense"}.get(st["last_engine"], None),
                        "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
                        "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"},
@@ -411,6 +413,8 @@ def main():
     ap.add_argument("--exchange", type=int, default=0, choices=[0, 1],
                     help="multi-GPU exchange per matvec: 0 = S slab all-gather, 1 = u reduce (NEXT-3)")
     ap.add_argument("--solver", default="cg", choices=["cg", "minres"])
+    ap.add_argument("--cg-variant", type=int, default=0, choices=[0, 1],
+                    help="0 = Hestenes-Stiefel CG, 1 = Chronopoulos-Gear (one reduction per iteration)")
     ap.add_argument("--no-profile", dest="profile", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -106,10 +106,15 @@ typedef enum {
                                     graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches        */
     GVT_OPT_SOLVER = 8,          /* iterative solver of pairwise_krr_fit(_early_stopping): gvt_solver,
                                     default GVT_SOLVER_CG                                             */
-    GVT_OPT_EXCHANGE = 9         /* data-parallel exchange per matvec: 0 (default) =
+    GVT_OPT_EXCHANGE = 9,        /* data-parallel exchange per matvec: 0 (default) =
                                     all-gather the S column slabs (4 q m bytes), stage 2 on the local
                                     outputs; 1 = u-exchange: stage 2 of the rank's own slab over EVERY
                                     output, then a reduce of the n-vector to its owners (4 n bytes)   */
+    GVT_OPT_CG_VARIANT = 10      /* CG form: 0 (default) = Hestenes-Stiefel (two reductions per
+                                    iteration); 1 = Chronopoulos-Gear (the same iterates in exact
+                                    arithmetic, matvec on r, one fused reduction of r.r and w.r per
+                                    iteration: one collective instead of two across GPUs; not with
+                                    early stopping)                                                   */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

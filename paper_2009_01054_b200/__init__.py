@@ -41,6 +41,7 @@ OPT_GEMM_CTA = 6
 OPT_GRAPHS = 7
 OPT_SOLVER = 8
 OPT_EXCHANGE = 9
+OPT_CG_VARIANT = 10
 SOLVER_CG, SOLVER_MINRES = 0, 1
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32

@@ -135,6 +135,10 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     case GVT_OPT_GRAPHS:
         c->graphs = v != 0;
         break;
+    case GVT_OPT_CG_VARIANT:
+        GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "cg variant must be 0 (Hestenes-Stiefel) or 1 (Chronopoulos-Gear)");
+        c->cg_variant = (int)v;
+        break;
     case GVT_OPT_EXCHANGE:
         GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "exchange must be 0 (S all-gather) or 1 (u reduce)");
         c->exchange = (int)v;

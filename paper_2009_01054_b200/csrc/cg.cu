@@ -182,6 +182,161 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_p(float *__restrict__ p, con
     }
 }
 
+// ============================================================================ single-reduction CG
+// Chronopoulos-Gear CG (GVT_OPT_CG_VARIANT = 1; the "single fused all-reduce per CG iteration" of
+// SURVEY.md 8(e) NEXT-3).  The same Krylov iterates as Hestenes-Stiefel CG in exact arithmetic,
+// with the matvec applied to r instead of p and the two dot products of an iteration reduced
+// together:
+//   w_k = (K + lambda I) r_k;  gamma_k = r_k.r_k,  delta_k = w_k.r_k        (one reduction)
+//   k = 0: beta = 0, alpha = gamma / delta;  else beta = gamma_k / gamma_{k-1},
+//          alpha = gamma_k / (delta_k - beta gamma_k / alpha_{k-1})        (<= 0: breakdown)
+//   p = r + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s           (s = (K + lambda I) p)
+// Per iteration: matvec + 3 kernels and one all-gather of 2 x 1184 partials, against 5 kernels
+// and two collectives for the Hestenes-Stiefel form.  Residual mode stops before the update
+// whose gamma_k meets the tolerance (the iterate and the count equal Hestenes-Stiefel's).
+// state: 0 gamma_{k-1} (rho), 1 alpha, 2 beta, 3 ||y||, 4 delta, 5 done, 6 breakdown, 7 iters,
+//        8 rel_tol -- the CG layout, so the host-side flags are the same.
+
+// x = 0, r = y, p = s = 0; partial y.y
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_init(const float *__restrict__ y, int64_t n, float *__restrict__ x,
+                                                          float *__restrict__ r, float *__restrict__ p,
+                                                          float *__restrict__ sv, double *__restrict__ part) {
+    int64_t lo, hi;
+    block_range(n, lo, hi);
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float v = y[i];
+        x[i] = 0.f;
+        r[i] = v;
+        p[i] = 0.f;
+        sv[i] = 0.f;
+        acc += (double)v * (double)v;
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// w += lambda r; partials of r.r (part[b]) and w.r (part[RED_BLOCKS + b])
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_dots(float *__restrict__ w, const float *__restrict__ r,
+                                                          int64_t n, float lambda, const double *__restrict__ st,
+                                                          double *__restrict__ part) {
+    if (halted(st)) return;
+    int64_t lo, hi;
+    block_range(n, lo, hi);
+    double g = 0.0, d = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float ri = r[i];
+        const float wi = fmaf(lambda, ri, w[i]);
+        w[i] = wi;
+        g += (double)ri * (double)ri;
+        d += (double)wi * (double)ri;
+    }
+    g = block_sum(g);
+    d = block_sum(d);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = g;
+        part[RED_BLOCKS + blockIdx.x] = d;
+    }
+}
+
+// partials laid out [world][2][RED_BLOCKS] (all-gathered as one slot of 2 * RED_BLOCKS per rank)
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_scalar(const double *__restrict__ part, int world,
+                                                            double *__restrict__ st, double *__restrict__ relres) {
+    if (halted(st)) return;
+    double g = 0.0, d = 0.0;
+    for (int r = 0; r < world; r++) {  // fixed order: rank by rank
+        g += reduce_parts(part + (size_t)r * 2 * RED_BLOCKS, RED_BLOCKS);
+        d += reduce_parts(part + (size_t)r * 2 * RED_BLOCKS + RED_BLOCKS, RED_BLOCKS);
+    }
+    if (threadIdx.x == 0) {
+        const double k = st[ST_ITERS];
+        const double rr = sqrt(g) / st[ST_YNORM];
+        if (relres) relres[(int64_t)k] = rr;
+        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || g == 0.0) {
+            st[ST_DONE] = 1.0;
+            return;
+        }
+        double beta = 0.0, den = d;
+        if (k >= 1.0) {
+            beta = g / st[ST_RHO];
+            den = d - beta * g / st[ST_ALPHA];
+        }
+        st[ST_PAP] = den;  // p.(K + lambda I)p of the direction this update uses
+        if (!(den > 0.0)) {
+            st[ST_BREAK] = 1.0;
+            return;
+        }
+        st[ST_BETA] = beta;
+        st[ST_ALPHA] = g / den;
+        st[ST_RHO] = g;
+        st[ST_ITERS] = k + 1.0;
+    }
+}
+
+// p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_update(float *__restrict__ x, float *__restrict__ r,
+                                                            float *__restrict__ p, float *__restrict__ sv,
+                                                            const float *__restrict__ w, int64_t n,
+                                                            const double *__restrict__ st) {
+    if (halted(st)) return;
+    const float alpha = (float)st[ST_ALPHA], beta = (float)st[ST_BETA];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float pi = fmaf(beta, p[i], r[i]);
+        const float si = fmaf(beta, sv[i], w[i]);
+        p[i] = pi;
+        sv[i] = si;
+        x[i] = fmaf(alpha, pi, x[i]);
+        r[i] = fmaf(-alpha, si, r[i]);
+    }
+}
+
+// after the loop: ||r_K|| for the residual history (one more reduction, no matvec)
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_rr(const float *__restrict__ r, int64_t n, double *__restrict__ part) {
+    int64_t lo, hi;
+    block_range(n, lo, hi);
+    double g = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) g += (double)r[i] * (double)r[i];
+    g = block_sum(g);
+    if (threadIdx.x == 0) part[blockIdx.x] = g;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_cgg_final(const double *__restrict__ part, int nparts,
+                                                           const double *__restrict__ st, double *__restrict__ relres) {
+    const double g = reduce_parts(part, nparts);
+    if (threadIdx.x == 0 && relres && st[ST_BREAK] == 0.0 && st[ST_DONE] == 0.0)
+        relres[(int64_t)st[ST_ITERS]] = sqrt(g) / st[ST_YNORM];
+}
+
+// partial-sum slots [world][2 * RED_BLOCKS]; this rank writes slot `rank`
+static double *parts2(gvt_ctx *c) { return wsT<double>(c, "cgg.parts", (size_t)2 * RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
+
+void cgg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, float *sv, double *state,
+              double rel_tol) {
+    double *pt = solver_parts(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_init, RED_BLOCKS, RED_THREADS, 0, y, n, x, r, p, sv,
+               pt + (size_t)c->rank * RED_BLOCKS);
+    allreduce_partials(c, pt, RED_BLOCKS);
+    GVT_LAUNCH(c, K_CG_SCALAR, k_cg_init_scalars, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, rel_tol, state,
+               state + ST_N);
+}
+
+void cgg_step(gvt_ctx *c, float *x, float *r, float *p, float *sv, float *w, int64_t n, double lambda,
+              double *state) {
+    double *pt = parts2(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_dots, RED_BLOCKS, RED_THREADS, 0, w, r, n, (float)lambda, state,
+               pt + (size_t)c->rank * 2 * RED_BLOCKS);
+    allreduce_partials(c, pt, 2 * RED_BLOCKS);  // the iteration's single collective
+    GVT_LAUNCH(c, K_CG_SCALAR, k_cgg_scalar, 1, RED_THREADS, 0, pt, c->world, state, state + ST_N);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_update, RED_BLOCKS, RED_THREADS, 0, x, r, p, sv, w, n, state);
+}
+
+void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state) {
+    double *pt = solver_parts(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_rr, RED_BLOCKS, RED_THREADS, 0, r, n, pt + (size_t)c->rank * RED_BLOCKS);
+    allreduce_partials(c, pt, RED_BLOCKS);
+    GVT_LAUNCH(c, K_CG_SCALAR, k_cgg_final, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);
+}
+
 // partial-sum slots [world][RED_BLOCKS]; this rank writes slot `rank`
 double *solver_parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
 static double *my_parts(gvt_ctx *c) { return solver_parts(c) + (size_t)c->rank * RED_BLOCKS; }

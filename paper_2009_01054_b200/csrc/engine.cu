@@ -957,6 +957,8 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     GVT_REQUIRE(rel_tol >= 0.0, GVT_E_PARAM, "rel_tol < 0");
     GVT_REQUIRE(n >= 0, GVT_E_DIM, "negative n");
     const bool minres = c->solver == GVT_SOLVER_MINRES;
+    const bool cgg = !minres && c->cg_variant == 1;  // Chronopoulos-Gear single-reduction CG
+    GVT_REQUIRE(!(cgg && es), GVT_E_PARAM, "early stopping runs Hestenes-Stiefel CG or MINRES (GVT_OPT_CG_VARIANT = 0)");
     Problem P;
     Form form;
     int64_t n_val = 0;
@@ -1045,7 +1047,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         es_evaluate(c, ap, s_full, state, esd, ehist, es->patience, x, a_best, n);
     };
     float *r1 = nullptr, *r2 = nullptr, *v = nullptr, *W1 = nullptr, *W2 = nullptr, *r = nullptr, *p = nullptr;
-    float *KW1 = nullptr, *KW2 = nullptr;
+    float *KW1 = nullptr, *KW2 = nullptr, *sv = nullptr;
     if (minres) {
         r1 = wsT<float>(c, "mr.r1", n), r2 = wsT<float>(c, "mr.r2", n), v = wsT<float>(c, "mr.v", n);
         W1 = wsT<float>(c, "mr.W1", n), W2 = wsT<float>(c, "mr.W2", n);
@@ -1055,6 +1057,9 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
             GVT_CUDA_TRY(cudaMemsetAsync(KW2, 0, sizeof(float) * n_val, c->stream));
         }
         minres_init(c, yd, n, x, r1, r2, v, W1, W2, state, rel_tol);
+    } else if (cgg) {
+        r = wsT<float>(c, "cg.r", n), p = wsT<float>(c, "cg.p", n), sv = wsT<float>(c, "cgg.s", n);
+        cgg_init(c, yd, n, x, r, p, sv, state, rel_tol);
     } else {
         r = wsT<float>(c, "cg.r", n), p = wsT<float>(c, "cg.p", n);
         cg_init(c, yd, n, x, r, p, state, rel_tol);
@@ -1064,6 +1069,9 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
             run_matvec(c, P, mp, v, u);
             minres_step(c, u, v, r1, r2, W1, W2, x, n, lambda, state);
             minres_update(c, v, W1, W2, x, r2, n, state, u + n, KW1, KW2, s_val, n_val);
+        } else if (cgg) {
+            run_matvec(c, P, mp, r, u);  // w = K r
+            cgg_step(c, x, r, p, sv, u, n, lambda, state);
         } else {
             run_matvec(c, P, mp, p, u);
             cg_after_matvec(c, u, p, n, lambda, state);
@@ -1073,6 +1081,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         evaluate();
     };
     drive(c, max_iter, rel_tol > 0.0 || es != nullptr, state, iteration);
+    if (cgg) cgg_finish(c, r, n, state);
     // scalars back (one sync per fit)
     double hstate[MINRES_STATE_N];
     GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * SN, cudaMemcpyDeviceToHost, c->stream));

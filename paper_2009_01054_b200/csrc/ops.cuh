@@ -159,6 +159,13 @@ void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p
 void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state);
 void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_t n, double *state, int iter,
                double *relres_dev);
+// Chronopoulos-Gear single-reduction CG (GVT_OPT_CG_VARIANT = 1): init, then per iteration the
+// matvec w = K r followed by cgg_step; cgg_finish records ||r_K|| after the loop
+void cgg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, float *sv, double *state,
+              double rel_tol);
+void cgg_step(gvt_ctx *c, float *x, float *r, float *p, float *sv, float *w, int64_t n, double lambda,
+              double *state);
+void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state);
 // multi-GPU hook: reduce a partial-sum vector across ranks (no-op at world 1)
 void allreduce_partials(gvt_ctx *c, double *partials, int count);
 

@@ -14,6 +14,10 @@ namespace gvt {
 
 enum { ST_RHO = 0, ST_ALPHA, ST_BETA, ST_YNORM, ST_PAP, ST_DONE, ST_BREAK, ST_ITERS, ST_TOL, ST_N };
 
+// ||r_k|| / ||y|| at which the fp32 solvers stop as converged (2^-60, far below what fp32 vectors
+// resolve; reading S32)
+constexpr double RES_FLOOR = 8.673617379884035e-19;
+
 __device__ __forceinline__ bool halted(const double *st) { return st[ST_DONE] != 0.0 || st[ST_BREAK] != 0.0; }
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_init(const float *__restrict__ y, int64_t n, float *__restrict__ x,
@@ -152,7 +156,9 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_beta(const double *__restric
         st[ST_ITERS] = it;
         double rr = sqrt(rho1) / st[ST_YNORM];
         if (relres) relres[(int64_t)it] = rr;
-        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || rho1 == 0.0) st[ST_DONE] = 1.0;
+        // converged: the tolerance, or the residual floor RES_FLOOR (reading S32: below it the fp32
+        // recurrences only underflow, into 0/0 after ~120 iterations on C1)
+        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || rho1 == 0.0 || rr <= RES_FLOOR) st[ST_DONE] = 1.0;
         st[ST_BETA] = rho1 / st[ST_RHO];
         st[ST_RHO] = rho1;
     }
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cgg_scalar(const double *__rest
         const double k = st[ST_ITERS];
         const double rr = sqrt(g) / st[ST_YNORM];
         if (relres) relres[(int64_t)k] = rr;
-        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || g == 0.0) {
+        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || g == 0.0 || rr <= RES_FLOOR) {
             st[ST_DONE] = 1.0;
             return;
         }

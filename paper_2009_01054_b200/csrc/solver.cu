@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(RED_THREADS) k_mr_givens(const double *__restr
         // converged, or Lanczos breakdown beta_{k+1} <= 64 u ||T_k||_F with u = 2^-24, the unit
         // roundoff of the fp32 vectors (reading M2; the oracle uses u = 2^-53): a normal exit
         const double bd = 64.0 * 5.9604644775390625e-08 * sqrt(st[MR_TNORM2]);
-        if ((st[MR_TOL] > 0.0 && rr <= st[MR_TOL]) || beta <= bd || st[MR_PHIBAR] == 0.0) st[MR_DONE] = 1.0;
+        // ... or the residual floor 2^-60 (reading S32, as the CG forms)
+        if ((st[MR_TOL] > 0.0 && rr <= st[MR_TOL]) || beta <= bd || st[MR_PHIBAR] == 0.0 || rr <= 8.673617379884035e-19)
+            st[MR_DONE] = 1.0;
     }
 }
 

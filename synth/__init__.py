@@ -298,6 +298,35 @@ def parity_grid(pattern: str, m: int, q: int, seed: int = 0, val_frac: float = 0
     return w, _f32(lab[:n_val])
 
 
+def kernel_filling(n_pairs: int, seed: int = 0, n_objects: int = 2967, dim: int = 1024, n_clusters: int = 24,
+                   flip: float = 0.2, label_noise: float = 0.05, val_frac: float = 0.25):
+    """Stand-in for the paper's kernel-filling data set (Table 5: 2967 drugs,
+    complete homogeneous grid), whose real drug kernels are not in the container.
+    Objects: n_objects binary fingerprints of length dim, each a copy of one of n_clusters random
+    prototypes (density 10 %) with every bit flipped with probability `flip` -- Tanimoto
+    similarity then tracks cluster membership.  Labels: 1 if the two objects share a cluster,
+    else 0, each flipped with probability `label_noise` (a planted, noisy pairwise structure; no
+    method arithmetic).  Pairs: as in the paper, a
+    subset of k objects with k(k-1)/2 ~ n_pairs gives all its unordered pairs i < j, shuffled and
+    split 75 % inner training / 25 % validation (Setting 1).  Returns (Workload with the Tanimoto
+    base kernel and homogeneous ids, validation labels); training labels are in w.y."""
+    rng = np.random.default_rng(50_000 + seed)
+    protos = rng.uniform(size=(n_clusters, dim)) < 0.10
+    cl = rng.integers(0, n_clusters, n_objects)
+    X = protos[cl] ^ (rng.uniform(size=(n_objects, dim)) < flip)
+    k = int(min(n_objects, max(2, round((1 + math.sqrt(1 + 8 * n_pairs)) / 2))))
+    sub = np.sort(rng.choice(n_objects, k, replace=False))
+    iu, ju = np.triu_indices(k, 1)
+    order = rng.permutation(len(iu))
+    f, s = sub[iu[order]], sub[ju[order]]
+    lab = ((cl[f] == cl[s]) ^ (rng.uniform(size=len(f)) < label_noise)).astype(np.float32)
+    n_val = int(round(val_frac * len(f)))
+    w = Workload(f"kf{len(f)}", _f32(X), None, BASE_TANIMOTO, 1.0, _i32(f[n_val:]), _i32(s[n_val:]),
+                 _f32(lab[n_val:]), _i32(f[:n_val]), _i32(s[:n_val]), 1e-5, 300,
+                 (LINEAR, POLY2D, KRONECKER, CARTESIAN, SYMMETRIC, MLPK))
+    return w, _f32(lab[:n_val])
+
+
 def random_vector(seed: int, n: int) -> np.ndarray:
     """Seeded N(0,1) float32 vector (the 'a' of a standalone matvec)."""
     return np.random.default_rng(20_000 + seed).standard_normal(n, dtype=np.float32)

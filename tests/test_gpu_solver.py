@@ -302,3 +302,25 @@ def test_chronopoulos_gear_cg_kernels_and_ragged(cgg_ctx, kernel, n):
     ah, _, _, _ = cgg_ctx.fit(dev(D32), None if hom else dev(T32), dev(f), dev(s), dev(y), terms, 1.0, 8)
     cgg_ctx.set_option(G.OPT_CG_VARIANT, 1)
     assert rel(a.cpu().numpy(), ao) <= max(1e-4, 3 * rel(ah.cpu().numpy(), ao))
+
+
+@pytest.mark.parametrize("solver,variant", [(0, 0), (0, 1), (1, 0)], ids=["cg", "cg-cgg", "minres"])
+def test_long_fixed_iteration_fit_stays_finite(ctx, solver, variant):
+    """Reading S32: far more iterations than convergence needs (C1, 300) end as converged at the
+    residual floor instead of underflowing into 0/0; the weights equal the oracle's converged
+    solution."""
+    ctx.set_option(G.OPT_SOLVER, solver)
+    ctx.set_option(G.OPT_CG_VARIANT, variant)
+    try:
+        w = synth.config1()
+        D = O.gram(w.base, w.Xd, gamma=w.gamma)
+        T = O.gram(w.base, w.Xt, gamma=w.gamma)
+        kron = G.gvt_kernel_terms(G.KRONECKER)
+        a, it, hist, code = ctx.fit(dev(f32(D)), dev(f32(T)), dev(w.train_first), dev(w.train_second), dev(w.y),
+                                    kron, w.lam, 300)
+        assert code == G.OK and it <= 300 and np.all(np.isfinite(a.cpu().numpy()))
+        ao, _, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, 60)
+        assert rel(a.cpu().numpy(), ao) <= 1e-4
+    finally:
+        ctx.set_option(G.OPT_SOLVER, 0)
+        ctx.set_option(G.OPT_CG_VARIANT, 0)

@@ -92,7 +92,10 @@ typedef struct gvt_ctx gvt_ctx;
 
 /* Options (gvt_set_option). */
 typedef enum {
-    GVT_OPT_ENGINE = 0,          /* 0 = auto by density (default), 1 = sparse SIMT, 2 = dense tensor-core */
+    GVT_OPT_ENGINE = 0,          /* 0 = auto by density (default), 1 = sparse SIMT, 2 = dense tensor-core,
+                                    3 = single-CTA whole-fit CG (Kronecker fits whose factors, S and
+                                    vectors fit one SM's shared memory; auto picks it for those when
+                                    an iteration is <= 4e6 FMAs)                                      */
     GVT_OPT_DENSE_THRESHOLD = 1, /* pair-matrix density at or above which auto picks dense (default 0.02) */
     GVT_OPT_PROFILE = 2,         /* 1 = record per-kernel CUDA-event times (gvt_get_stats)                */
     GVT_OPT_GRAM_ENGINE = 3,     /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */

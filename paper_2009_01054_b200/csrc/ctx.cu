@@ -23,7 +23,7 @@ static const char *kKindNames[K_NUM_KINDS] = {
     "gram_simt",   "gram_tc",       "split_operand",  "pad_copy",     "plan_keys",      "plan_sort(cub)",
     "plan_rowptr", "plan_gather",   "stage1_sparse", "stage2_gather", "densify",     "stage1_tc",
     "stage2_tc",   "segment_sum",   "gemv",        "combine",      "cartesian",      "cg_vector",
-    "cg_scalar",   "fill",          "auc",
+    "cg_scalar",   "fill",          "auc",          "tiny_cg",
 };
 
 const char *kind_name(int k) { return (k >= 0 && k < K_NUM_KINDS) ? kKindNames[k] : "?"; }

@@ -1041,6 +1041,38 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     float *u = wsT<float>(c, "solver.u", (size_t)(n + n_val));  // matvec output [inner; validation]
     MatvecPlan mp;
     plan_matvec(c, P, terms, n_terms, form, mp);
+    // small Kronecker fits: the whole solve in one single-CTA launch (tiny.cu) -- forced by
+    // GVT_OPT_ENGINE = 3, or chosen when a CG iteration is at most 4e6 FMAs and everything fits
+    // in one SM's shared memory
+    {
+        const bool eligible = form == FORM_KRON && !minres && !cgg && !es && c->world == 1 && c->slabs <= 1 &&
+                              c->exchange == 0 && !P.rect && P.n_in == n && tiny_smem(P.m, P.q, n) > 0;
+        const double fmas = (double)n * (double)P.q + (double)n * (double)P.m;
+        GVT_REQUIRE(c->engine != 3 || eligible, GVT_E_PARAM,
+                    "single-CTA solver (engine 3): Kronecker CG fits on one GPU whose factors, S and vectors fit in "
+                    "shared memory only");
+        if (eligible && (c->engine == 3 || (c->engine == 0 && fmas <= 4e6))) {
+            const GroupPlan &g = mp.groups[0];
+            tiny_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
+            c->last_engine = 3;
+            double hs[9];
+            GVT_CUDA_TRY(cudaMemcpyAsync(hs, state, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
+            if (relres_hist)
+                GVT_CUDA_TRY(cudaMemcpyAsync(relres_hist, state + 9, sizeof(double) * (max_iter + 1),
+                                             cudaMemcpyDeviceToHost, c->stream));
+            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            out_finish(c, ao);
+            const int iters = (int)hs[7];
+            if (iters_out) *iters_out = iters;
+            if (relres_hist)
+                for (int k = iters + 1; k <= max_iter; k++) relres_hist[k] = 0.0 / 0.0;
+            if (hs[6] != 0.0) {
+                set_error("CG breakdown: p^T (K + lambda I) p = %g <= 0 at iteration %d", hs[4], iters + 1);
+                return GVT_E_BREAKDOWN;
+            }
+            return GVT_OK;
+        }
+    }
     auto evaluate = [&]() {
         if (!es) return;
         if (c->world > 1) gather_varlen(c, s_val, s_full, vcounts, voffs, true);

@@ -59,6 +59,7 @@ enum KernelKind {
     K_CG_SCALAR,
     K_FILL,
     K_AUC,
+    K_TINY,
     K_NUM_KINDS
 };
 const char *kind_name(int k);
@@ -84,7 +85,7 @@ struct gvt_ctx {
     bool tc_ok = false;  // tcgen05 path usable (sm_100)
 
     // options
-    int engine = 0;  // 0 auto, 1 sparse, 2 dense
+    int engine = 0;  // 0 auto, 1 sparse, 2 dense, 3 single-CTA whole-fit solver (small Kronecker fits)
     double dense_threshold = 0.02;
     int profile = 0;
     int gram_engine = 0;

@@ -198,6 +198,11 @@ void es_cg_scores(gvt_ctx *c, float *s, const float *kp, int64_t n_val, const do
 void es_evaluate(gvt_ctx *c, AucPlan &a, const float *scores_full, double *state, double *es, double *hist,
                  int patience, const float *x, float *a_best, int64_t n);
 
+// ---- single-CTA whole-fit CG for small Kronecker problems (tiny.cu)
+size_t tiny_smem(int64_t m, int64_t q, int64_t n);  // 0 if it does not fit one SM
+void tiny_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
+             int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state);
+
 // partial-sum layout (cg.cu)
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
 constexpr int RED_THREADS = 256;

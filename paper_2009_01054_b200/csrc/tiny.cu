@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(TINY_THREADS, 1) k_tiny_cg(TinyArgs a) {
     float *Ds = Ts + (size_t)q * q;          // m x m
     float *S = Ds + (size_t)m * m;           // q x m  (S[t][h])
     float *p = S + (size_t)q * m;            // n
-    float *r = p + n, *Ap = r + n, *x = Ap + n;
+    float *r = p + n, *Ap = r + n;
+    float *x = a.x;  // the iterate lives in global memory (one read-modify-write per iteration)
     for (int i = tid; i < q * q; i += TINY_THREADS) Ts[i] = a.T[(int64_t)(i / q) * a.ldT + i % q];
     for (int i = tid; i < m * m; i += TINY_THREADS) Ds[i] = a.D[(int64_t)(i / m) * a.ldD + i % m];
     double yy = 0.0;
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(TINY_THREADS, 1) k_tiny_cg(TinyArgs a) {
         const float v = a.y[i];
         p[i] = v;
         r[i] = v;
-        x[i] = 0.f;
+        x[i] = 0.f;  // each thread owns the same i in every loop below: no cross-thread hazard
         yy += (double)v * (double)v;
     }
     double rho = tiny_sum(yy, red);  // also the barrier after the smem fills
@@ -127,7 +128,6 @@ __global__ void __launch_bounds__(TINY_THREADS, 1) k_tiny_cg(TinyArgs a) {
         for (int i = tid; i < n; i += TINY_THREADS) p[i] = fmaf(bf, p[i], r[i]);
         __syncthreads();
     }
-    for (int i = tid; i < n; i += TINY_THREADS) a.x[i] = x[i];
     if (tid == 0) {
         double *st = a.state;
         st[TS_RHO] = rho;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(TINY_THREADS, 1) k_tiny_cg(TinyArgs a) {
 
 // shared memory the single-CTA solve needs, or 0 if the problem does not qualify
 size_t tiny_smem(int64_t m, int64_t q, int64_t n) {
-    const size_t floats = (size_t)(q * q + m * m + q * m + 4 * n);
+    const size_t floats = (size_t)(q * q + m * m + q * m + 3 * n);
     const size_t bytes = floats * sizeof(float);
     return bytes <= 200 * 1024 ? bytes : 0;
 }

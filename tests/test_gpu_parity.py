@@ -361,11 +361,13 @@ def test_edge_cases_and_errors(ctx):
 def test_launch_accounting(ctx):
     ctx.reset_stats()
     ctx.set_option(G.OPT_PROFILE, 1)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)  # the multi-kernel path (auto picks the single-CTA solver at C1)
     w = synth.config1()
     D, T = grams_gpu(ctx, w)
     ctx.fit(D, T, dev(w.train_first), dev(w.train_second), dev(w.y), G.gvt_kernel_terms(G.KRONECKER), 1.0, 5)
     st = ctx.stats()
     ctx.set_option(G.OPT_PROFILE, 0)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
     assert st["launches"] > 0
     assert "cg_vector" in st["kinds"] and st["kinds"]["cg_vector"]["count"] >= 5 * 3
     assert all(v["ms"] >= 0 for v in st["kinds"].values())

@@ -192,6 +192,7 @@ def test_early_stopping_weights_equal_plain_fit(ctx, solver, kernel):
     AUC of its direct validation scores matches the recorded best within 1e-4.  Seeded
     C3-shaped instance (homogeneous kernels) or C1 (Kronecker); labels y > 0 as the classes."""
     ctx.set_option(G.OPT_SOLVER, solver)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)  # the same engine for both fits (not the single-CTA solver)
     try:
         if kernel == G.KRONECKER:
             w = synth.config1()
@@ -217,6 +218,7 @@ def test_early_stopping_weights_equal_plain_fit(ctx, solver, kernel):
         assert best_auc == np.max(hist) and hist[best - 1] == best_auc
     finally:
         ctx.set_option(G.OPT_SOLVER, G.SOLVER_CG)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
 
 
 def test_early_stopping_errors(ctx):
@@ -324,3 +326,64 @@ def test_long_fixed_iteration_fit_stays_finite(ctx, solver, variant):
     finally:
         ctx.set_option(G.OPT_SOLVER, 0)
         ctx.set_option(G.OPT_CG_VARIANT, 0)
+
+
+# ----------------------------------------------------------------------------- single-CTA whole-fit solver
+def test_tiny_engine_c1_matches_oracle(ctx):
+    """GVT_OPT_ENGINE = 3: the whole C1 CG fit in one single-CTA launch; weights (<= 1e-4),
+    predictions (<= 1e-4 max-abs), residual-mode stop and the residual history match the oracle;
+    auto selects it on C1; an ineligible problem is an error, not a silent fallback."""
+    w = synth.config1()
+    D = O.gram(w.base, w.Xd, gamma=w.gamma)
+    T = O.gram(w.base, w.Xt, gamma=w.gamma)
+    Dg, Tg = dev(f32(D)), dev(f32(T))
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    args = (Dg, Tg, dev(w.train_first), dev(w.train_second), dev(w.y), kron, w.lam)
+    ao, _, hist_o, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, w.iters)
+    try:
+        for engine in (G.ENGINE_TINY, G.ENGINE_AUTO):
+            ctx.set_option(G.OPT_ENGINE, engine)
+            ctx.reset_stats()
+            a, it, hist, code = ctx.fit(*args, w.iters)
+            st = ctx.stats()
+            assert st["last_engine"] == 3 and st["kinds"]["tiny_cg"]["count"] == 1
+            assert code == G.OK and it == w.iters
+            assert rel(a.cpu().numpy(), ao) <= 1e-4
+            assert np.allclose(hist[:8], hist_o[:8], rtol=1e-4, atol=1e-7)
+        sc = ctx.predict(Dg, Tg, dev(w.test_first), dev(w.test_second), dev(w.train_first), dev(w.train_second), a,
+                         kron).cpu().numpy()
+        ref = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, w.test_first, w.test_second, w.train_first,
+                           w.train_second, ao)
+        assert np.abs(sc - ref).max() <= 1e-4
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_TINY)
+        a2, it2, h2, _ = ctx.fit(*args, 200, rel_tol=0.05)
+        _, it2o, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D, T, w.train_first, w.train_second, w.y, w.lam, 200,
+                             rel_tol=0.05)
+        assert it2 == it2o and h2[-1] <= 0.05 < h2[-2]
+        with pytest.raises(G.GvtError) as e:  # Symmetric is not eligible for the single-CTA solver
+            ctx.fit(Dg, None, dev(w.train_first % 40), dev(w.train_second % 40), dev(w.y),
+                    G.gvt_kernel_terms(G.SYMMETRIC), 1.0, 5)
+        assert e.value.code == G.E_PARAM
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("m,q,n", [(1, 1, 1), (3, 2, 5), (17, 29, 300), (64, 100, 4000), (60, 100, 9000)])
+def test_tiny_engine_shapes(ctx, m, q, n):
+    """Ragged shapes through the single-CTA solver (duplicates, n not a multiple of the block size,
+    n larger than the thread count) against the oracle's CG on the same fp32 inputs."""
+    rng = np.random.default_rng(m * 1000 + n)
+    D32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((m, 4)), gamma=0.25))
+    T32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((q, 4)), gamma=0.25))
+    f = rng.integers(0, m, n).astype(np.int32)
+    s = rng.integers(0, q, n).astype(np.int32)
+    y = rng.standard_normal(n).astype(np.float32)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_TINY)
+    try:
+        a, it, _, _ = ctx.fit(dev(D32), dev(T32), dev(f), dev(s), dev(y), kron, 1.0, 8)
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    ao, ito, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
+    assert it == ito or n <= 8
+    assert rel(a.cpu().numpy(), ao) <= 1e-4

@@ -113,11 +113,15 @@ typedef enum {
                                     all-gather the S column slabs (4 q m bytes), stage 2 on the local
                                     outputs; 1 = u-exchange: stage 2 of the rank's own slab over EVERY
                                     output, then a reduce of the n-vector to its owners (4 n bytes)   */
-    GVT_OPT_CG_VARIANT = 10      /* CG form: 0 (default) = Hestenes-Stiefel (two reductions per
+    GVT_OPT_CG_VARIANT = 10,     /* CG form: 0 (default) = Hestenes-Stiefel (two reductions per
                                     iteration); 1 = Chronopoulos-Gear (the same iterates in exact
                                     arithmetic, matvec on r, one fused reduction of r.r and w.r per
                                     iteration: one collective instead of two across GPUs; not with
                                     early stopping)                                                   */
+    GVT_OPT_SORTED_FIT = 11      /* 1 (default): pairwise_krr_fit solves on the training pairs stably
+                                    sorted by (first, second) and returns a_out in caller order (the
+                                    same iterates up to dot-product summation order; entries read in
+                                    vector order); 0 = caller order                                   */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

@@ -135,6 +135,9 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     case GVT_OPT_GRAPHS:
         c->graphs = v != 0;
         break;
+    case GVT_OPT_SORTED_FIT:
+        c->sorted_fit = v != 0;
+        break;
     case GVT_OPT_CG_VARIANT:
         GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "cg variant must be 0 (Hestenes-Stiefel) or 1 (Chronopoulos-Gear)");
         c->cg_variant = (int)v;

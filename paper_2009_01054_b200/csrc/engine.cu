@@ -1137,8 +1137,34 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
 gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
                int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
                double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
-    return fit_impl(c, D, m, T, q, f, s, n, y, terms, n_terms, lambda, max_iter, rel_tol, a_out, iters_out,
-                    relres_hist, nullptr);
+    // Sorted-order fit (GVT_OPT_SORTED_FIT, default on): the solve runs on the training pairs
+    // stably sorted by (first, second) -- K' = Pi K Pi^T, y' = Pi y, a = Pi^T a', the same
+    // iterates up to the summation order of the dot products -- so the Kronecker group's
+    // pair-matrix entries are read in vector order instead of gathered at random (the dense
+    // path's X build and the sparse path's entry values).
+    if (!c->sorted_fit || n < 2 || max_iter == 0)
+        return fit_impl(c, D, m, T, q, f, s, n, y, terms, n_terms, lambda, max_iter, rel_tol, a_out, iters_out,
+                        relres_hist, nullptr);
+    GVT_REQUIRE(f && s && y, GVT_E_DIM, "pair ids or labels are NULL with n > 0");
+    const int64_t qq = T ? q : m;
+    const int32_t *fd = (const int32_t *)stage_in(c, "sfit.f_in", f, sizeof(int32_t) * n);
+    const int32_t *sd = (const int32_t *)stage_in(c, "sfit.s_in", s, sizeof(int32_t) * n);
+    const float *yd = (const float *)stage_in(c, "sfit.y_in", y, sizeof(float) * n);
+    check_range(c, fd, n, m, "first ids");
+    check_range(c, sd, n, qq, "second ids");
+    int32_t *perm = wsT<int32_t>(c, "sfit.perm", (size_t)n);
+    sort_pairs(c, fd, sd, n, m, qq, perm);
+    int32_t *fs = wsT<int32_t>(c, "sfit.f", (size_t)n), *ss = wsT<int32_t>(c, "sfit.s", (size_t)n);
+    float *ys = wsT<float>(c, "sfit.y", (size_t)n), *xs = wsT<float>(c, "sfit.x", (size_t)n);
+    gather_i32(c, fd, perm, n, fs);
+    gather_i32(c, sd, perm, n, ss);
+    gather_f32(c, yd, perm, n, ys);
+    gvt_status st = fit_impl(c, D, m, T, q, fs, ss, n, ys, terms, n_terms, lambda, max_iter, rel_tol, xs, iters_out,
+                             relres_hist, nullptr);
+    OutArr ao = out_arr(c, "out.a", a_out, n);
+    scatter_f32(c, xs, perm, n, ao.dev);
+    out_finish(c, ao);
+    return st;
 }
 
 gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,

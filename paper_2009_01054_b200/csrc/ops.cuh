@@ -87,6 +87,11 @@ void build_sample_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int3
                        int col_sel, int64_t n_diag, int64_t nrow, SamplePlan &out);
 void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int mode,
                      int32_t *perm, int64_t *row_ptr);
+// fit-level reordering: perm = pair indices stably sorted by (first, second); gathers / scatter
+void sort_pairs(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int32_t *perm);
+void gather_i32(gvt_ctx *c, const int32_t *x, const int32_t *perm, int64_t n, int32_t *y);
+void gather_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);
+void scatter_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);  // y[perm[k]] = x[k]
 // validation helper: returns number of ids outside [0, bound) (device reduction, syncs)
 int64_t count_out_of_range(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound);
 

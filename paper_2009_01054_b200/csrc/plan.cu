@@ -229,6 +229,47 @@ void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, 
     GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(m + 1, 256), 256, 0, rows, n, m, row_ptr);
 }
 
+// ----------------------------------------------------------------------------- fit-level reordering
+// perm = the pair indices stably sorted by (first, second): a fit runs in this order so that the
+// pair-matrix entries of the Kronecker group are read in vector order (sequential, not gathered)
+__global__ void k_pair_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, int64_t q,
+                            uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        keys[j] = (uint64_t)f[j] * (uint64_t)q + (uint64_t)s[j];
+        vals[j] = (int32_t)j;
+    }
+}
+
+void sort_pairs(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int32_t *perm) {
+    if (n == 0) return;
+    uint64_t *k0 = wsT<uint64_t>(c, "fitsort.k0", n), *k1 = wsT<uint64_t>(c, "fitsort.k1", n);
+    int32_t *v0 = wsT<int32_t>(c, "fitsort.v0", n);
+    GVT_LAUNCH(c, K_PLAN_KEYS, k_pair_keys, grid1d(n, 256, 4096), 256, 0, f, s, n, q, k0, v0);
+    radix_sort_pairs<uint64_t>(c, "fitsort", k0, k1, v0, perm, n, key_bits((uint64_t)(m > 0 ? m : 1) * (uint64_t)(q > 0 ? q : 1)));
+}
+
+template <typename Tv>
+__global__ void k_gather(const Tv *__restrict__ x, const int32_t *__restrict__ perm, int64_t n, Tv *__restrict__ y) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = x[perm[k]];
+}
+
+__global__ void k_scatter_f32(const float *__restrict__ x, const int32_t *__restrict__ perm, int64_t n,
+                              float *__restrict__ y) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        y[perm[k]] = x[k];
+}
+
+void gather_i32(gvt_ctx *c, const int32_t *x, const int32_t *perm, int64_t n, int32_t *y) {
+    if (n) GVT_LAUNCH(c, K_PLAN_GATHER, k_gather<int32_t>, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, x, perm, n, y);
+}
+void gather_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y) {
+    if (n) GVT_LAUNCH(c, K_PLAN_GATHER, k_gather<float>, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, x, perm, n, y);
+}
+void scatter_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y) {
+    if (n) GVT_LAUNCH(c, K_PLAN_GATHER, k_scatter_f32, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, x, perm, n, y);
+}
+
 // ----------------------------------------------------------------------------- validation
 __global__ void k_count_oor(const int32_t *__restrict__ ids, int64_t n, int64_t bound, unsigned long long *cnt) {
     unsigned long long local = 0;

@@ -21,6 +21,7 @@ w = synth.config5()
 ctx = G.Context(0)
 if "cta" in spec: ctx.set_option(G.OPT_GEMM_CTA, int(spec["cta"]))
 if "prec" in spec: ctx.set_option(G.OPT_TC_PRECISION, int(spec["prec"]))
+if "sf" in spec: ctx.set_option(G.OPT_SORTED_FIT, int(spec["sf"]))
 d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
 D = ctx.gram(w.base, d(w.Xd), gamma=w.gamma); T = ctx.gram(w.base, d(w.Xt), gamma=w.gamma)
 f, s = d(w.train_first), d(w.train_second); a = d(synth.random_vector(0, w.n)); u = torch.empty_like(a)
@@ -37,7 +38,7 @@ st = ctx.stats()
 print(json.dumps({"fit10_ms": round(e0.elapsed_time(e1), 1), "sm_mhz": float(np.median(clk)) if clk else None,
                   "power_w": float(np.median(pw)) if pw else None,
                   "kinds": {k: round(v["ms"] / max(1, v["count"]), 3) for k, v in st["kinds"].items()
-                            if k.startswith("stage")}}))
+                            if k.startswith("stage") or k in ("densify", "plan_sort(cub)", "plan_gather")}}))
 """
 
 

@@ -185,8 +185,46 @@ struct EpiParams {
     const float *l1max;
 };
 
+__device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
+                                              const float *stage) {
+    constexpr int STRIDE = 256;  // 32 * N_EPI_WARPS epilogue threads
+    for (int64_t k0 = kb0 + t; k0 < ke; k0 += 4 * STRIDE) {
+        int rl[4], cl[4];
+        int64_t dd[4];
+        float prev[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t k = k0 + (int64_t)u * STRIDE;
+            if (k < ke) {
+                rl[u] = ep.s_r[k] - m0;  // 0..127
+                cl[u] = ep.s_c[k] - gc0;  // 0..31
+                dd[u] = ep.s_dst[k];
+            }
+        }
+        if (ep.accumulate) {
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (k0 + (int64_t)u * STRIDE < ke) prev[u] = ep.out[dd[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (k0 + (int64_t)u * STRIDE < ke) {
+                const float val = stage[(rl[u] >> 5) * 32 * 33 + (rl[u] & 31) * 33 + cl[u]];
+                ep.out[dd[u]] = ep.accumulate ? fmaf(ep.coef, val, prev[u]) : ep.coef * val;
+            }
+        }
+    }
+}
+
+
 constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
 constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk
+// Sampled epilogue: write the samples k in [kb0, ke) of one 32-column chunk (their values parked
+// in `stage`, [rows/32][32][33] floats) to out[dst].  Four samples per thread are in flight at a
+// time (independent index loads), so a tile's sample phase is not a chain of dependent latencies
+// when few tiles carry many samples.
+__device__ __forceinline__ void serve_samples(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0,
+                                              int gc0, const float *stage);
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
 constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
@@ -415,13 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int64_t cidx = tile * (BN / 32) + chunk;
                     const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                     const int gc0 = n0 + chunk * 32;
-                    for (int64_t k = kb0 + t; k < ke; k += 32 * N_EPI_WARPS) {
-                        const int rl = ep.s_r[k] - m0;   // 0..127
-                        const int cl = ep.s_c[k] - gc0;  // 0..31
-                        const float val = stage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
-                        const int64_t d = ep.s_dst[k];
-                        ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
-                    }
+                    serve_samples(ep, kb0, ke, t, m0, gc0, stage + hh * 4 * 32 * 33);
                 }
                 named_bar(1, 32 * N_EPI_WARPS);
             }
@@ -815,13 +847,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                             const int64_t cidx = tile * (BN / 32) + chunk;
                             const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                             const int gc0 = n0 + chunk * 32;
-                            for (int64_t k = kb0 + t256; k < ke; k += 32 * N_EPI_WARPS) {
-                                const int rl = ep.s_r[k] - m0;
-                                const int cl = ep.s_c[k] - gc0;
-                                const float val = estage[(hh * 4 + (rl >> 5)) * 32 * 33 + (rl & 31) * 33 + cl];
-                                const int64_t d = ep.s_dst[k];
-                                ep.out[d] = ep.accumulate ? fmaf(ep.coef, val, ep.out[d]) : ep.coef * val;
-                            }
+                            serve_samples(ep, kb0, ke, t256, m0, gc0, estage + hh * 4 * 32 * 33);
                         }
                     }
                     named_bar(1, 32 * N_EPI_WARPS);

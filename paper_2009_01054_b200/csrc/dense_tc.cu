@@ -1051,7 +1051,10 @@ bool fused_f16(gvt_ctx *c, int64_t q_in) {
 // one CTA per row r of [row_lo, row_lo + rows): cell values (sum of sign * p[src] over the
 // cell's run of entries, in entry order -- the same sums as k_densify) parked in shared
 // memory, row max -> power-of-two scale, then coalesced fp16 hi/lo stores of the whole row
-constexpr int BX_THREADS = 1024;  // a row's ~m*density cells spread over 32 warps (latency-bound gathers)
+// BX_THREADS per row: 1024 for long rows (a row's ~m*density cells spread over 32 warps, latency-bound
+// gathers); 256 for rows of <= 8192 columns, where the per-row barrier chain dominates and more rows
+// (smaller shared-memory rows) must be in flight per SM
+template <int BX_THREADS>
 __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                                    const int32_t *__restrict__ src, const float *__restrict__ sign,
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
@@ -1128,12 +1131,18 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     const size_t smem = sizeof(float) * o.ld;
     static size_t attr_smem = 0;
     if (smem > 48 * 1024 && smem > attr_smem) {
-        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_smem = smem;
     }
-    if (rows > 0)
-        GVT_LAUNCH(c, K_DENSIFY, k_build_x16, grid1d(rows, 1, 2 * c->sm_count), BX_THREADS, smem, e.row_ptr, e.col, e.src,
-                   e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
+    if (rows > 0) {
+        if (o.ld > 8192)
+            GVT_LAUNCH(c, K_DENSIFY, k_build_x16<1024>, grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr, e.col,
+                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
+        else
+            GVT_LAUNCH(c, K_DENSIFY, k_build_x16<256>, grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr, e.col,
+                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
+    }
     o.hi = hi;
     o.lo = lo;
     o.scale = s;

@@ -185,15 +185,19 @@ struct EpiParams {
     const float *l1max;
 };
 
+#ifndef SERVE_UNROLL
+#define SERVE_UNROLL 1
+#endif
 __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
                                               const float *stage) {
     constexpr int STRIDE = 256;  // 32 * N_EPI_WARPS epilogue threads
-    for (int64_t k0 = kb0 + t; k0 < ke; k0 += 4 * STRIDE) {
-        int rl[4], cl[4];
-        int64_t dd[4];
-        float prev[4];
+    constexpr int U = SERVE_UNROLL;
+    for (int64_t k0 = kb0 + t; k0 < ke; k0 += U * STRIDE) {
+        int rl[U], cl[U];
+        int64_t dd[U];
+        float prev[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < U; u++) {
             const int64_t k = k0 + (int64_t)u * STRIDE;
             if (k < ke) {
                 rl[u] = ep.s_r[k] - m0;  // 0..127
@@ -203,11 +207,11 @@ __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, 
         }
         if (ep.accumulate) {
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < U; u++)
                 if (k0 + (int64_t)u * STRIDE < ke) prev[u] = ep.out[dd[u]];
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < U; u++) {
             if (k0 + (int64_t)u * STRIDE < ke) {
                 const float val = stage[(rl[u] >> 5) * 32 * 33 + (rl[u] & 31) * 33 + cl[u]];
                 ep.out[dd[u]] = ep.accumulate ? fmaf(ep.coef, val, prev[u]) : ep.coef * val;
@@ -220,9 +224,10 @@ __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, 
 constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
 constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk
 // Sampled epilogue: write the samples k in [kb0, ke) of one 32-column chunk (their values parked
-// in `stage`, [rows/32][32][33] floats) to out[dst].  Four samples per thread are in flight at a
-// time (independent index loads), so a tile's sample phase is not a chain of dependent latencies
-// when few tiles carry many samples.
+// in `stage`, [rows/32][32][33] floats) to out[dst], SERVE_UNROLL samples per thread in flight.
+// Measured (profiles/r01_ab_serve_unroll.txt): 4 in flight cut C2 from 95 to 83 us per iteration
+// but raised the CTA-pair kernel's register spills (172 -> 556 B) and C5's stage 2 from 43 to
+// 50 ms, so 1 is the default.
 __device__ __forceinline__ void serve_samples(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0,
                                               int gc0, const float *stage);
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
@@ -694,17 +699,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
-                // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16):
-                // the warp's 128 scales are staged once per chunk in its private slot of the epilogue
-                // staging area (one coalesced float4 per lane) and read back as shared-memory
-                // broadcasts.  The sampled output phase reuses the slot only after the tile's last
-                // chunk, behind its own named barriers.
+                // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
                 const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
-                float *ssk = estage + (half * 4 + quarter) * 32 * 33;
-                if (sk) {
-                    reinterpret_cast<float4 *>(ssk)[lane] = __ldg(reinterpret_cast<const float4 *>(sk) + lane);
-                    __syncwarp();
-                }
 #pragma unroll
                 for (int c4 = 0; c4 < 4; c4++) {
                     uint32_t r[32];
@@ -713,7 +709,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     if (sk) {
 #pragma unroll
                         for (int i = 0; i < 32; i++)
-                            run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), ssk[c4 * 32 + i], run[c4 * 32 + i]);
+                            run[c4 * 32 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c4 * 32 + i), run[c4 * 32 + i]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);

@@ -135,6 +135,15 @@ __device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32])
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float tf32_round(float x) {
@@ -185,6 +194,9 @@ struct EpiParams {
     const float *l1max;
 };
 
+#ifndef DRAIN_X16
+#define DRAIN_X16 1
+#endif
 #ifndef SERVE_UNROLL
 #define SERVE_UNROLL 1
 #endif
@@ -701,6 +713,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
                 // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
                 const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
+#if DRAIN_X16
+                // 16-column TMEM loads: 16 fewer live registers than x32 next to run[128] (the
+                // epilogue is at the 168-register cap of 10 warps per CTA)
+#pragma unroll
+                for (int c8 = 0; c8 < 8; c8++) {
+                    uint32_t r[16];
+                    tmem_ld16_raw(ta + c8 * 16, r);
+                    tmem_wait_ld();
+                    if (sk) {
+#pragma unroll
+                        for (int i = 0; i < 16; i++)
+                            run[c8 * 16 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c8 * 16 + i), run[c8 * 16 + i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; i++) run[c8 * 16 + i] += __uint_as_float(r[i]);
+                    }
+                }
+#else
 #pragma unroll
                 for (int c4 = 0; c4 < 4; c4++) {
                     uint32_t r[32];
@@ -715,6 +745,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                         for (int i = 0; i < 32; i++) run[c4 * 32 + i] += __uint_as_float(r[i]);
                     }
                 }
+#endif
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);

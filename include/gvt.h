@@ -118,10 +118,14 @@ typedef enum {
                                     arithmetic, matvec on r, one fused reduction of r.r and w.r per
                                     iteration: one collective instead of two across GPUs; not with
                                     early stopping)                                                   */
-    GVT_OPT_SORTED_FIT = 11      /* 1 (default): pairwise_krr_fit solves on the training pairs stably
+    GVT_OPT_SORTED_FIT = 11,     /* 1 (default): pairwise_krr_fit solves on the training pairs stably
                                     sorted by (first, second) and returns a_out in caller order (the
                                     same iterates up to dot-product summation order; entries read in
                                     vector order); 0 = caller order                                   */
+    GVT_OPT_KBLOCK_SKIP = 12     /* 1 (default): the dense stage 1 skips the all-zero 64-column
+                                    K-blocks of each 256-row tile of the pair matrix when they are at
+                                    least 15 % of the blocks (block-sparse X, e.g. MLPK on a union
+                                    domain); 0 = always the full K loop                              */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

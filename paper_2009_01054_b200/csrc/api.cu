@@ -135,6 +135,9 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     case GVT_OPT_GRAPHS:
         c->graphs = v != 0;
         break;
+    case GVT_OPT_KBLOCK_SKIP:
+        c->kblock_skip = v != 0;
+        break;
     case GVT_OPT_SORTED_FIT:
         c->sorted_fit = v != 0;
         break;

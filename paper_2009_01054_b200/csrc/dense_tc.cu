@@ -180,6 +180,10 @@ struct EpiParams {
     int degree;
     int kcb;  // k-blocks per accumulation chunk (0 = KC_BLOCKS)
     int group_m;  // CTA-pair kernel: pair-tile rows per rasterization group (0 = GROUP_M)
+    // CTA-pair kernel, optional block sparsity of the B operand: for column tile n (BN rows of B),
+    // only the K-blocks kb_list[kb_off[n] .. kb_off[n + 1]) (ascending, at least one) are
+    // multiplied; the other K-blocks of those B rows are all zero (EPI_STORE16 only)
+    const int32_t *kb_list, *kb_off;
     // B operand with a per-(row, 256-wide K chunk) scale, applied while draining chunk ch:
     // sbk[ch * sbk_ld + n] (fp16 S produced by EPI_STORE16)
     const float *sbk;
@@ -583,7 +587,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
     const int nk = (K + BKE - 1) / BKE;
     const int kcb = ep.kcb > 0 ? ep.kcb : KC_BLOCKS;
-    const int nch = (nk + kcb - 1) / kcb;
+    // K-blocks of column tile n: all of them, or the tile's list of non-zero K-blocks of B
+    auto tile_nk = [&](int n) -> int { return ep.kb_list ? ep.kb_off[n + 1] - ep.kb_off[n] : nk; };
+    auto tile_kb = [&](int n, int i) -> int { return ep.kb_list ? ep.kb_list[ep.kb_off[n] + i] : i; };
     const int gm = ep.group_m > 0 ? ep.group_m : GROUP_M;
     const int in_group = gm * num_n;
 
@@ -636,13 +642,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 coords(t, mp_tile, n_tile);
                 if (skip(mp_tile, n_tile)) continue;
                 const int m0 = (2 * mp_tile + (int)crank) * BM, n0 = n_tile * BN;
-                for (int kb = 0; kb < nk; kb++, kg++) {
+                const int nk_t = tile_nk(n_tile);
+                for (int kb = 0; kb < nk_t; kb++, kg++) {
                     const int s = kg % STAGES2;
                     const uint32_t ph = (kg / STAGES2) & 1;
                     mbar_wait(&empty[s], ph ^ 1);  // own slot released by the leader's MMA commit
                     uint8_t *st = smem + s * STAGE2_BYTES;
                     if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
-                    const int kc = kb * BKE;
+                    const int kc = tile_kb(n_tile, kb) * BKE;
                     tma_load_2d_pair(st, &tmAh, &full[s], kc, m0);
                     tma_load_2d_pair(st + HALF_BYTES, &tmAl, &full[s], kc, m0);
                     tma_load_2d_pair(st + 2 * HALF_BYTES, &tmBh, &full[s], kc, n0 + (int)crank * 128);
@@ -659,12 +666,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 coords(t, mp_tile, n_tile);
                 if (skip(mp_tile, n_tile)) continue;
                 int kb = 0;
-                for (int ch = 0; ch < nch; ch++, cg++) {
+                const int nk_t = tile_nk(n_tile), nch_t = (nk_t + kcb - 1) / kcb;
+                for (int ch = 0; ch < nch_t; ch++, cg++) {
                     const int b = cg & 1;
                     mbar_wait(&tempty[b], ((cg >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t acc = tmem + b * BN;
-                    const int kend = min(nk, kb + kcb);
+                    const int kend = min(nk_t, kb + kcb);
                     for (int kk = 0; kb < kend; kb++, kk++, kg++) {
                         const int s = kg % STAGES2;
                         const uint32_t ph = (kg / STAGES2) & 1;
@@ -706,7 +714,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             float run[128];
 #pragma unroll
             for (int i = 0; i < 128; i++) run[i] = 0.f;
-            for (int ch = 0; ch < nch; ch++, cg++) {
+            const int nch_t = (tile_nk(n_tile) + kcb - 1) / kcb;
+            for (int ch = 0; ch < nch_t; ch++, cg++) {
                 const int b = cg & 1;
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
@@ -1176,14 +1185,50 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     return o;
 }
 
+// ---- block sparsity of the pair matrix for stage 1 (kb_list / kb_off of the CTA-pair kernel)
+__global__ void k_kb_flags(const int32_t *__restrict__ row, const int32_t *__restrict__ col, int64_t k0, int64_t k1,
+                           int64_t lo, int64_t rows, int64_t nkb, uint8_t *__restrict__ flags) {
+    for (int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row[k] - lo;
+        if (r >= 0 && r < rows) flags[(r / BN) * nkb + col[k] / 64] = 1;  // idempotent byte stores
+    }
+}
+
+void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,
+                  bool diag, std::vector<int32_t> &list, std::vector<int32_t> &off) {
+    const int64_t ntiles = (rows + BN - 1) / BN, nkb = (cols + 63) / 64;
+    uint8_t *flags = wsT<uint8_t>(c, "kbl.flags", (size_t)(ntiles * nkb));
+    GVT_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(ntiles * nkb), c->stream));
+    if (k1 > k0)
+        GVT_LAUNCH(c, K_PLAN_KEYS, k_kb_flags, grid1d(k1 - k0, 256, 8 * c->sm_count * 8), 256, 0, e.row, e.col, k0, k1,
+                   lo, rows, nkb, flags);
+    std::vector<uint8_t> h((size_t)(ntiles * nkb));
+    GVT_CUDA_TRY(cudaMemcpyAsync(h.data(), flags, h.size(), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (diag)  // the separate diagonal X[r][r] (MLPK Laplacian) sits in column lo + r
+        for (int64_t r = 0; r < rows; r++) h[(size_t)((r / BN) * nkb + (lo + r) / 64)] = 1;
+    list.clear();
+    off.assign((size_t)ntiles + 1, 0);
+    for (int64_t t = 0; t < ntiles; t++) {
+        const size_t before = list.size();
+        for (int64_t b = 0; b < nkb; b++)
+            if (h[(size_t)(t * nkb + b)]) list.push_back((int32_t)b);
+        if (list.size() == before) list.push_back(0);  // at least one K-block: the accumulator is defined
+        off[(size_t)t + 1] = (int32_t)list.size();
+    }
+}
+
 // hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256)) floats,
 // whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
 // l1max != nullptr: one scale per row (sk[row]) from the bound 2^15 A.scale[row] * (*l1max), where
 // *l1max >= max over B's rows of the row's L1 norm (build_x16 computes it)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max) {
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max, const int32_t *kb_list,
+                     const int32_t *kb_off) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
+    ep.kb_list = kb_list;
+    ep.kb_off = kb_off;
     ep.c_h16 = hi;
     ep.c_l16 = lo;
     ep.c_sk = sk;

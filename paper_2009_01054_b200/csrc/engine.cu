@@ -201,6 +201,8 @@ struct GroupPlan {
     std::string tag;
     float *diag = nullptr;  // optional separate diagonal of X (global row index), computed per matvec
     int64_t n_diag = 0;     // extra (x, x) samples after the outputs (MLPK)
+    // block sparsity of X per slab for the fused fp16 stage 1 (device lists, nullptr = dense)
+    std::vector<const int32_t *> kb_list, kb_off;
 };
 
 struct MatvecPlan {
@@ -288,6 +290,8 @@ static void make_slabs(gvt_ctx *c, GroupPlan &g) {
     g.W = round_up(wmax > 0 ? wmax : 1, 32);
 }
 
+static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
+
 static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
     g.tag = tag;
     g.engine = choose_engine(c, g);
@@ -295,6 +299,32 @@ static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
     g.qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
     g.S = wsT<float>(c, (g.tag + ".S").c_str(), (size_t)g.nslab * g.qpad * g.W);
     if (g.engine == 2) bucket_samples(c, tag, g.smp, g.A.n, g.q_out);
+    // block-sparse stage 1: the (256-row, 64-column) blocks of each X slab holding entries, kept
+    // when they cover at most 85 % of the slab (e.g. MLPK on a union domain: the drug-target blocks
+    // and the diagonal only); dense blocks everywhere (C3, C4 Poly2D, C5) keep the plain K loop
+    g.kb_list.assign((size_t)g.nslab, nullptr);
+    g.kb_off.assign((size_t)g.nslab, nullptr);
+    if (g.engine == 2 && fused_f16(c, g.C.cols) && c->kblock_skip) {
+        for (int s = 0; s < g.nslab; s++) {
+            if (!my_slab(c, s)) continue;
+            const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+            if (w == 0) continue;
+            std::vector<int32_t> list, off;
+            kblock_lists(c, g.ent, g.kpos[s], g.kpos[s + 1], lo, w, g.C.cols, g.diag != nullptr, list, off);
+            const double total = (double)(off.size() - 1) * (double)((g.C.cols + 63) / 64);
+            if ((double)list.size() > 0.85 * total) continue;
+            char nm[64];
+            snprintf(nm, sizeof(nm), "%s.kbl%d", tag, s);
+            int32_t *dl = wsT<int32_t>(c, nm, list.size());
+            snprintf(nm, sizeof(nm), "%s.kbo%d", tag, s);
+            int32_t *dof = wsT<int32_t>(c, nm, off.size());
+            GVT_CUDA_TRY(cudaMemcpyAsync(dl, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice, c->stream));
+            GVT_CUDA_TRY(cudaMemcpyAsync(dof, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice, c->stream));
+            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));  // the host vectors go out of scope
+            g.kb_list[(size_t)s] = dl;
+            g.kb_off[(size_t)s] = dof;
+        }
+    }
 }
 
 static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int n_terms, Form form,
@@ -302,8 +332,9 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
     mp.form = form;
     const int F = GVT_SEL_FIRST, Sx = GVT_SEL_SECOND;
     auto group = [&](const Factor &A, const Factor &C, EntryKinds kinds, int64_t nrow, int64_t ncol, int rs, int cs,
-                     int64_t n_diag, float coef, const char *tag) {
+                     int64_t n_diag, float coef, const char *tag, float *x_diag = nullptr) {
         GroupPlan g;
+        g.diag = x_diag;  // before finish_group: the block-sparsity lists include the diagonal
         g.A = A;
         g.C = C;
         g.q_out = C.n;
@@ -345,7 +376,8 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
         k.count = 2;
         k.k[0] = EntryKind{F, Sx, -1.f};
         k.k[1] = EntryKind{Sx, F, -1.f};
-        group(P.D, P.D, k, P.m, P.m, F, Sx, P.m_out, 1.f, "g0");
+        group(P.D, P.D, k, P.m, P.m, F, Sx, P.m_out, 1.f, "g0",
+              wsT<float>(c, "mlpk.diag", (size_t)round_up(P.m > 0 ? P.m : 1, 32)));
         {
             EntryKinds kd;
             memset(&kd, 0, sizeof(kd));
@@ -355,7 +387,6 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kd, P.m, P.m, mp.byF);
         }
         mp.buf = wsT<float>(c, "mlpk.buf", (size_t)(P.n_out + P.m_out));
-        mp.groups[0].diag = wsT<float>(c, "mlpk.diag", (size_t)round_up(P.m > 0 ? P.m : 1, 32));
         break;
     }
     case FORM_LINEAR:
@@ -431,7 +462,6 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
 }
 
 // ----------------------------------------------------------------------------- run
-static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
 
 // fused 3xFP16 dense path: X rows assembled straight into fp16 pieces, stage 1 writes S as
 // fp16 pieces with per-(row, 256-column) scales, stage 2 applies them per K-chunk; slab s of
@@ -470,7 +500,7 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
         if (w == 0) continue;
         Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag, tile_scale ? nullptr : l1 + s);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
-                        skld, tile_scale ? nullptr : l1 + s);
+                        skld, tile_scale ? nullptr : l1 + s, g.kb_list[(size_t)s], g.kb_off[(size_t)s]);
     }
     float *partial = nullptr;
     if (P.uex) {  // no S exchange: this rank's slab serves every output, then the partials are reduced

@@ -141,8 +141,15 @@ void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_
 // C = A * B^T written as fp16 pieces (M rows x ldc) with per-(row, 256-col tile) scales
 // sk[tile * sk_ld + row] (sk_ld >= round_up(M, 256))
 // l1max != nullptr: one scale per row sk[row] from the a-priori bound (no per-tile scales)
+// kb_list / kb_off (device, nullable): per 256-row tile of B, its ascending non-zero K-blocks of
+// 64 columns (at least one per tile): the other K-blocks are skipped (block-sparse B)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max = nullptr);
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max = nullptr,
+                     const int32_t *kb_list = nullptr, const int32_t *kb_off = nullptr);
+// non-zero (256-row tile, 64-column K-block) pairs of the pair-matrix rows [lo, lo + rows) from the
+// sorted entries k in [k0, k1) (+ the diagonal when diag): host lists (off has ntiles + 1 entries)
+void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,
+                  bool diag, std::vector<int32_t> &list, std::vector<int32_t> &off);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out);

@@ -489,3 +489,30 @@ def test_in_loop_matvec_parity_c5(ctx):
     w = synth.config5()
     tset = np.sort(np.random.default_rng(56).choice(w.q, 8, replace=False))
     _in_loop_check(ctx, w, G.KRONECKER, [w.iters], 128, restrict=lambda w: np.isin(w.train_second, tset))
+
+
+@pytest.mark.parametrize("skip", [1, 0], ids=["kblock-skip", "full-K"])
+def test_block_sparse_stage1_mlpk_union(ctx, skip):
+    """GVT_OPT_KBLOCK_SKIP: on a union domain (drugs then targets, S7) MLPK's pair matrix has
+    entries only in the drug-target blocks and on the diagonal, so the dense stage 1 skips the
+    other K-blocks; with and without the skip the matvec matches the oracle (the skipped blocks
+    are exact zeros; only the accumulation-chunk grouping differs)."""
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
+    ctx.set_option(G.OPT_KBLOCK_SKIP, skip)
+    try:
+        rng = np.random.default_rng(91)
+        nd, nt = 700, 400
+        X = rng.standard_normal((nd + nt, 16)).astype(np.float32)
+        D32 = f32(O.gram(G.BASE_GAUSSIAN, X, gamma=1 / 16))
+        f = rng.integers(0, nd, 60000).astype(np.int32)
+        s = (nd + rng.integers(0, nt, 60000)).astype(np.int32)
+        of = rng.integers(0, nd, 5000).astype(np.int32)
+        os_ = (nd + rng.integers(0, nt, 5000)).astype(np.int32)
+        a = synth.random_vector(5, 60000)
+        u = ctx.matvec(dev(D32), None, dev(of), dev(os_), dev(f), dev(s), dev(a),
+                       G.gvt_kernel_terms(G.MLPK)).cpu().numpy()
+        ref = O.gvt_matvec(O.kernel_terms(O.MLPK), D32, None, of, os_, f, s, a)
+        assert rel(u, ref) <= MATVEC_TOL, rel(u, ref)
+    finally:
+        ctx.set_option(G.OPT_KBLOCK_SKIP, 1)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)

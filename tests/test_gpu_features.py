@@ -77,3 +77,22 @@ def test_cta_pair_and_single_cta_gemm_agree_with_oracle(ctx):
         ctx.set_option(G.OPT_GEMM_CTA, 2)
         ctx.set_option(G.OPT_TC_PRECISION, G.PREC_FP16X3)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+def test_bench_json_contract_on_c1():
+    """bench.py prints one JSON line with the contract's keys (run on C1 to stay quick)."""
+    import json
+    import subprocess
+    import sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--workload", "C1", "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0

@@ -198,6 +198,9 @@ struct EpiParams {
     const float *l1max;
 };
 
+#ifndef SK_VEC4
+#define SK_VEC4 1
+#endif
 #ifndef DRAIN_X16
 #define DRAIN_X16 1
 #endif
@@ -731,9 +734,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     tmem_ld16_raw(ta + c8 * 16, r);
                     tmem_wait_ld();
                     if (sk) {
+#if SK_VEC4
+                        // 16-byte scale loads (sk is 16-byte aligned: 256-aligned base, 256-float chunk
+                        // rows, 128-column thread blocks)
+                        const float4 *sk4 = reinterpret_cast<const float4 *>(sk + c8 * 16);
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; q4++) {
+                            const float4 v = __ldg(sk4 + q4);
+                            run[c8 * 16 + 4 * q4 + 0] = fmaf(__uint_as_float(r[4 * q4 + 0]), v.x, run[c8 * 16 + 4 * q4 + 0]);
+                            run[c8 * 16 + 4 * q4 + 1] = fmaf(__uint_as_float(r[4 * q4 + 1]), v.y, run[c8 * 16 + 4 * q4 + 1]);
+                            run[c8 * 16 + 4 * q4 + 2] = fmaf(__uint_as_float(r[4 * q4 + 2]), v.z, run[c8 * 16 + 4 * q4 + 2]);
+                            run[c8 * 16 + 4 * q4 + 3] = fmaf(__uint_as_float(r[4 * q4 + 3]), v.w, run[c8 * 16 + 4 * q4 + 3]);
+                        }
+#else
 #pragma unroll
                         for (int i = 0; i < 16; i++)
                             run[c8 * 16 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c8 * 16 + i), run[c8 * 16 + i]);
+#endif
                     } else {
 #pragma unroll
                         for (int i = 0; i < 16; i++) run[c8 * 16 + i] += __uint_as_float(r[i]);

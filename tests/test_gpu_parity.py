@@ -491,14 +491,16 @@ def test_in_loop_matvec_parity_c5(ctx):
     _in_loop_check(ctx, w, G.KRONECKER, [w.iters], 128, restrict=lambda w: np.isin(w.train_second, tset))
 
 
+@pytest.mark.parametrize("slabs", [1, 3])
 @pytest.mark.parametrize("skip", [1, 0], ids=["kblock-skip", "full-K"])
-def test_block_sparse_stage1_mlpk_union(ctx, skip):
+def test_block_sparse_stage1_mlpk_union(ctx, skip, slabs):
     """GVT_OPT_KBLOCK_SKIP: on a union domain (drugs then targets, S7) MLPK's pair matrix has
     entries only in the drug-target blocks and on the diagonal, so the dense stage 1 skips the
     other K-blocks; with and without the skip the matvec matches the oracle (the skipped blocks
     are exact zeros; only the accumulation-chunk grouping differs)."""
     ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
     ctx.set_option(G.OPT_KBLOCK_SKIP, skip)
+    ctx.set_option(G.OPT_SLABS, slabs)
     try:
         rng = np.random.default_rng(91)
         nd, nt = 700, 400
@@ -514,5 +516,6 @@ def test_block_sparse_stage1_mlpk_union(ctx, skip):
         ref = O.gvt_matvec(O.kernel_terms(O.MLPK), D32, None, of, os_, f, s, a)
         assert rel(u, ref) <= MATVEC_TOL, rel(u, ref)
     finally:
+        ctx.set_option(G.OPT_SLABS, 1)
         ctx.set_option(G.OPT_KBLOCK_SKIP, 1)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)

@@ -963,17 +963,19 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
     ep.sbk_ld = B.scale_k_ld;
     GVT_REQUIRE(!B.scale_k || (pair && PREC == PREC_F16), GVT_E_STATE, "chunk-scaled operand needs the CTA-pair fp16 GEMM");
     GVT_REQUIRE(EPI != EPI_STORE16 || (pair && PREC == PREC_F16), GVT_E_STATE, "fp16 store needs the CTA-pair fp16 GEMM");
-    static bool attr = false, attr2 = false;
+    // function attributes are per device: one flag per device ordinal (one process may drive several)
+    static bool attr[GVT_MAX_DEVICES] = {}, attr2[GVT_MAX_DEVICES] = {};
+    const int dv = c->device < GVT_MAX_DEVICES ? c->device : 0;
     if (pair) {
         static const int env_gm = [] {  // A/B knob for the rasterization group (scripts/ab_matvec.py)
             const char *e = getenv("GVT_GROUP_M");
             return e ? atoi(e) : 0;
         }();
         if (ep.group_m == 0) ep.group_m = env_gm;
-        if (!attr2) {
+        if (!attr2[dv]) {
             GVT_CUDA_TRY(
                 cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
-            attr2 = true;
+            attr2[dv] = true;
         }
         const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
         const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
@@ -982,10 +984,10 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
                    (int)K, ep);
         return;
     }
-    if (!attr) {
+    if (!attr[dv]) {
         GVT_CUDA_TRY(
             cudaFuncSetAttribute(k_gemm_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL));
-        attr = true;
+        attr[dv] = true;
     }
     dim3 grid((unsigned)(((N + BN - 1) / BN) * ((M + BM - 1) / BM)));
     GVT_LAUNCH(c, kind_id, (k_gemm_x3<PREC, EPI>), grid, NTHREADS, SMEM_TOTAL, ah, al, bh, bl, (int)M, (int)N, (int)K,
@@ -1182,11 +1184,12 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     __half *lo = wsT<__half>(c, (nm + ".l16").c_str(), (size_t)rows_pad * o.ld);
     float *s = wsT<float>(c, (nm + ".sinv").c_str(), (size_t)rows_pad);
     const size_t smem = sizeof(float) * o.ld;
-    static size_t attr_smem = 0;
-    if (smem > 48 * 1024 && smem > attr_smem) {
+    static size_t attr_smem[GVT_MAX_DEVICES] = {};
+    size_t &attr_dev = attr_smem[c->device < GVT_MAX_DEVICES ? c->device : 0];
+    if (smem > 48 * 1024 && smem > attr_dev) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_smem = smem;
+        attr_dev = smem;
     }
     if (rows > 0) {
         if (o.ld > 8192)

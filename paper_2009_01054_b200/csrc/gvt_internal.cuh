@@ -151,6 +151,8 @@ bool is_device_ptr(const void *p);
 // device memory, else a workspace copy made on the context stream)
 const void *stage_in(gvt_ctx *c, const char *name, const void *p, size_t bytes);
 
+constexpr int GVT_MAX_DEVICES = 64;
+
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline unsigned grid1d(int64_t n, int threads, int64_t cap = 1 << 30) {
     int64_t g = (n + threads - 1) / threads;

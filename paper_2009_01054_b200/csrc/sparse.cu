@@ -115,11 +115,12 @@ void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_ou
     if (q_out == 0 || ldS == 0) return;
     dim3 grid((unsigned)((q_out + TT - 1) / TT), (unsigned)((ldS + H - 1) / H));
     size_t smem = sizeof(float) * H * (TT + 1);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[GVT_MAX_DEVICES] = {};  // per device ordinal
+    bool &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
+    if (!attr_dev) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_stage1_sparse<H, TPB, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-        attr = true;
+        attr_dev = true;
     }
     GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB, TPT>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
                C.p, C.ld, q_out, S, ldS, diag, row_lo);

@@ -153,10 +153,11 @@ void tiny_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, c
              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state) {
     const size_t smem = tiny_smem(m, q, n);
     GVT_REQUIRE(smem > 0 && n < INT32_MAX, GVT_E_STATE, "problem too large for the single-CTA solver");
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    static size_t attr[GVT_MAX_DEVICES] = {};  // per device ordinal
+    size_t &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
+    if (smem > 48 * 1024 && smem > attr_dev) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_tiny_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+        attr_dev = smem;
     }
     TinyArgs a;
     a.T = T.p;

@@ -274,7 +274,8 @@ void slab_bounds(const int64_t *rp, int64_t nrow, int G, int64_t *bounds) {
 
 // slabs of a group, identical on every rank (computed from the same full plan)
 static void make_slabs(gvt_ctx *c, GroupPlan &g) {
-    int G = std::max(c->world, c->slabs > 0 ? c->slabs : 1);
+    // one slab per rank across GPUs (rank r owns slab r); emulated slabs only at world 1
+    int G = c->world > 1 ? c->world : std::max(1, c->slabs);
     const int64_t nrow = g.m_in;
     std::vector<int64_t> rp((size_t)nrow + 1);
     GVT_CUDA_TRY(cudaMemcpyAsync(rp.data(), g.ent.row_ptr, sizeof(int64_t) * (nrow + 1), cudaMemcpyDeviceToHost,

@@ -168,6 +168,17 @@ gvt_status gvt_reset_stats(gvt_ctx *ctx);
 gvt_status gvt_nccl_unique_id(void *out128);
 gvt_status gvt_comm_init(gvt_ctx *ctx, const void *nccl_unique_id, int rank, int world);
 
+/* Host-mediated communicator, for testing the data-parallel path with several ranks on fewer
+ * GPUs (e.g. two processes sharing one GPU, exchanging through torch.distributed gloo): every
+ * collective of the library becomes one call of `allgather(user, buf, bytes)`, where buf is HOST
+ * memory of world * bytes with this rank's block at buf + rank * bytes, and the callback fills the
+ * other ranks' blocks (returns 0 on success).  The library synchronises its stream around each
+ * call, so no kernel ever waits on another rank; collectives are then not graph-capturable and
+ * the solver replays eagerly.  The results equal the NCCL path's (the same exchanges and
+ * reductions in rank order; u-exchange reductions are summed on the device in rank order). */
+typedef int (*gvt_host_allgather_fn)(void *user, void *buf, size_t bytes);
+gvt_status gvt_comm_init_host(gvt_ctx *ctx, int rank, int world, gvt_host_allgather_fn allgather, void *user);
+
 /* Balanced contiguous drug ranges: given per-drug pair counts deg[m] (host), writes
  * bounds[world+1] (host) with bounds[0] = 0, bounds[world] = m, each range holding about
  * sum(deg)/world pairs (greedy prefix split).  Host-only, no device work. */

@@ -98,6 +98,8 @@ _lib.pairwise_krr_fit_early_stopping.argtypes = [_P, _P, _I64, _P, _I64, _P, _P,
                                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                                  ctypes.POINTER(ctypes.c_int), _P]
 _lib.gvt_auc.argtypes = [_P, _P, _P, _I64, ctypes.POINTER(ctypes.c_double)]
+HOST_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+_lib.gvt_comm_init_host.argtypes = [_P, ctypes.c_int, ctypes.c_int, HOST_ALLGATHER_FN, _P]
 _lib.gvt_gram_cross.argtypes = [_P, ctypes.c_int, _P, _I64, _P, _I64, _I64, ctypes.c_double, ctypes.c_double,
                                 ctypes.c_int, _P]
 _lib.gvt_matvec_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int,
@@ -110,7 +112,7 @@ EXPORTED = ["gvt_slab_bounds",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
             "pairwise_krr_fit_early_stopping", "gvt_auc", "gvt_gram_cross", "gvt_matvec_rect",
-            "pairwise_predict_rect"]
+            "pairwise_predict_rect", "gvt_comm_init_host"]
 
 
 def _check(code: int, where: str):
@@ -259,6 +261,27 @@ class Context:
     def comm_init(self, unique_id: bytes, rank: int, world: int):
         buf = ctypes.create_string_buffer(unique_id, 128)
         _check(_lib.gvt_comm_init(self._h, ctypes.cast(buf, _P), rank, world), "gvt_comm_init")
+
+    def comm_init_host(self, rank: int, world: int, group=None):
+        """gvt_comm_init_host with a torch.distributed (e.g. gloo) process group as the transport:
+        every library collective becomes one all-gather of host bytes through `group`."""
+        import torch
+        import torch.distributed as dist
+
+        def allgather(user, buf, nbytes):
+            try:
+                arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint8)), shape=(world * nbytes,))
+                mine = torch.from_numpy(arr[rank * nbytes:(rank + 1) * nbytes].copy())
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, mine, group=group)
+                for g in range(world):
+                    arr[g * nbytes:(g + 1) * nbytes] = outs[g].numpy()
+                return 0
+            except Exception:  # pragma: no cover - surfaced as GVT_E_NCCL by the library
+                return 1
+
+        self._host_allgather = HOST_ALLGATHER_FN(allgather)  # keep the callback alive
+        _check(_lib.gvt_comm_init_host(self._h, rank, world, self._host_allgather, None), "gvt_comm_init_host")
 
     # -- compute
     def gram(self, kind: int, X, gamma: float = 1.0, coef0: float = 1.0, degree: int = 2, out=None):

@@ -11,6 +11,7 @@ int kernel_terms(int kernel, gvt_term *o);
 void nccl_unique_id(void *out128);
 void comm_init(gvt_ctx *c, const void *id128, int rank, int world);
 void comm_destroy(gvt_ctx *c);
+void comm_init_host(gvt_ctx *c, int rank, int world, gvt_host_allgather_fn fn, void *user);
 void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of, const int32_t *os,
             int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in, const float *a,
             const gvt_term *terms, int n_terms, float *u);
@@ -209,6 +210,12 @@ gvt_status gvt_comm_init(gvt_ctx *c, const void *id, int rank, int world) {
     GVT_API_BEGIN(c)
     GVT_REQUIRE(world == 1 || id, GVT_E_PARAM, "unique id is NULL");
     gvt::comm_init(c, id, rank, world);
+    GVT_API_END
+}
+
+gvt_status gvt_comm_init_host(gvt_ctx *c, int rank, int world, gvt_host_allgather_fn allgather, void *user) {
+    GVT_API_BEGIN(c)
+    gvt::comm_init_host(c, rank, world, allgather, user);
     GVT_API_END
 }
 

@@ -6,6 +6,8 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace gvt {
@@ -87,10 +89,36 @@ void comm_destroy(gvt_ctx *c) {
     c->nccl_comm = nullptr;
 }
 
+// ---- host-mediated communicator (gvt_comm_init_host): one all-gather primitive through the host
+void comm_init_host(gvt_ctx *c, int rank, int world, gvt_host_allgather_fn fn, void *user) {
+    GVT_REQUIRE(world >= 1 && rank >= 0 && rank < world && fn, GVT_E_PARAM, "comm_init_host: bad arguments");
+    c->rank = rank;
+    c->world = world;
+    c->host_allgather = fn;
+    c->host_user = user;
+}
+
+// dev holds [world][bytes]; this rank's block is valid on entry, every block on return
+static void host_allgather(gvt_ctx *c, void *dev, size_t bytes) {
+    std::vector<char> h((size_t)c->world * bytes);
+    char *mine = h.data() + (size_t)c->rank * bytes;
+    if (bytes) {
+        GVT_CUDA_TRY(cudaMemcpyAsync(mine, (char *)dev + (size_t)c->rank * bytes, bytes, cudaMemcpyDeviceToHost,
+                                     c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    GVT_REQUIRE(c->host_allgather(c->host_user, h.data(), bytes) == 0, GVT_E_NCCL, "host all-gather callback failed");
+    if (bytes) {
+        GVT_CUDA_TRY(cudaMemcpyAsync(dev, h.data(), h.size(), cudaMemcpyHostToDevice, c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+}
+
 // partials laid out [world][count]; each rank wrote its own slot; gather all slots so the
 // fixed-order reduction over world*count values gives bit-identical scalars on every rank
 void allreduce_partials(gvt_ctx *c, double *partials, int count) {
     if (c->world <= 1) return;
+    if (c->host_allgather) return host_allgather(c, partials, sizeof(double) * (size_t)count);
     NCCL_TRY(g_nccl.AllGather(partials + (size_t)c->rank * count, partials, (size_t)count, ncclFloat64,
                               (ncclComm_t)c->nccl_comm, c->stream));
 }
@@ -98,6 +126,7 @@ void allreduce_partials(gvt_ctx *c, double *partials, int count) {
 // S slabs laid out [world][slab_floats]; in-place all-gather of the local slab
 void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats) {
     if (c->world <= 1) return;
+    if (c->host_allgather) return host_allgather(c, S, sizeof(float) * slab_floats);
     NCCL_TRY(g_nccl.AllGather(S + (size_t)c->rank * slab_floats, S, slab_floats, ncclFloat32,
                               (ncclComm_t)c->nccl_comm, c->stream));
 }
@@ -106,6 +135,12 @@ void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats) {
 std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v) {
     std::vector<int64_t> out((size_t)c->world, v);
     if (c->world <= 1) return out;
+    if (c->host_allgather) {
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        GVT_REQUIRE(c->host_allgather(c->host_user, out.data(), sizeof(int64_t)) == 0, GVT_E_NCCL,
+                    "host all-gather callback failed");
+        return out;
+    }
     int64_t *d = wsT<int64_t>(c, "comm.counts", (size_t)c->world);
     GVT_CUDA_TRY(cudaMemcpyAsync(d + c->rank, &v, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     NCCL_TRY(g_nccl.AllGather(d + c->rank, d, 1, ncclInt64, (ncclComm_t)c->nccl_comm, c->stream));
@@ -124,6 +159,20 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
             GVT_CUDA_TRY(cudaMemcpyAsync(full, local, esz * counts[0], cudaMemcpyDeviceToDevice, c->stream));
         return;
     }
+    if (c->host_allgather) {  // padded blocks of the largest count, then compacted in rank order
+        int64_t mx = 0;
+        for (int64_t v : counts) mx = std::max(mx, v);
+        char *tmp = (char *)ws(c, "comm.varlen", esz * (size_t)(mx > 0 ? mx : 1) * c->world);
+        if (counts[c->rank] > 0)
+            GVT_CUDA_TRY(cudaMemcpyAsync(tmp + esz * mx * c->rank, local, esz * counts[c->rank],
+                                         cudaMemcpyDeviceToDevice, c->stream));
+        host_allgather(c, tmp, esz * (size_t)mx);
+        for (int g = 0; g < c->world; g++)
+            if (counts[g] > 0)
+                GVT_CUDA_TRY(cudaMemcpyAsync((char *)full + esz * offsets[g], tmp + esz * mx * g, esz * counts[g],
+                                             cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
     NCCL_TRY(g_nccl.GroupStart());
     for (int g = 0; g < c->world; g++) {
         if (counts[g] == 0) continue;
@@ -132,6 +181,24 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
                                   is_float ? ncclFloat32 : ncclInt32, g, (ncclComm_t)c->nccl_comm, c->stream));
     }
     NCCL_TRY(g_nccl.GroupEnd());
+}
+
+// local[i] = sum_g tmp[g][off + i] (i < cnt), local[cnt + j] = sum_g tmp[g][n_full + j] (j < tail), g in order
+__global__ void k_sum_rank_segments(const float *__restrict__ tmp, size_t per, int world, int64_t off, int64_t cnt,
+                                    int64_t n_full, int64_t tail, float *__restrict__ local) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt + tail; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t src = i < cnt ? off + i : n_full + (i - cnt);
+        float acc = 0.f;
+        for (int g = 0; g < world; g++) acc += tmp[(size_t)g * per + src];
+        local[i] = acc;
+    }
+}
+
+void sum_rank_segments(gvt_ctx *c, const float *tmp, size_t per, int world, int64_t off, int64_t cnt, int64_t n_full,
+                       int64_t tail, float *local) {
+    if (cnt + tail > 0)
+        GVT_LAUNCH(c, K_FILL, k_sum_rank_segments, grid1d(cnt + tail, 256, 8 * c->sm_count * 8), 256, 0, tmp, per,
+                   world, off, cnt, n_full, tail, local);
 }
 
 // u-exchange: every rank holds a partial of the FULL out vector
@@ -146,6 +213,16 @@ void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::
         const int64_t n = counts[0] + tail;
         if (n > 0 && partial != local)
             GVT_CUDA_TRY(cudaMemcpyAsync(local, partial, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    if (c->host_allgather) {  // every rank's full partial, then the rank-order sums of this rank's parts
+        const size_t per = (size_t)(n_full + tail);
+        float *tmp = (float *)ws(c, "comm.uex", sizeof(float) * (per > 0 ? per : 1) * c->world);
+        if (per)
+            GVT_CUDA_TRY(cudaMemcpyAsync(tmp + per * c->rank, partial, sizeof(float) * per, cudaMemcpyDeviceToDevice,
+                                         c->stream));
+        host_allgather(c, tmp, sizeof(float) * per);
+        sum_rank_segments(c, tmp, per, c->world, offsets[c->rank], counts[c->rank], n_full, tail, local);
         return;
     }
     NCCL_TRY(g_nccl.GroupStart());

@@ -909,7 +909,7 @@ struct EsArgs {
 template <class Body>
 static void drive(gvt_ctx *c, int max_iter, bool poll, const double *state, Body body) {
     double *hst = (double *)pinned(c, sizeof(double) * 64);
-    const bool graphs = c->graphs && max_iter >= 3 && !c->profile;
+    const bool graphs = c->graphs && max_iter >= 3 && !c->profile && !c->host_allgather;  // host collectives sync
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
     int64_t per_iter = 0, l0 = 0, before[K_NUM_KINDS];

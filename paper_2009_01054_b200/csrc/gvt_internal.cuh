@@ -114,6 +114,8 @@ struct gvt_ctx {
     // multi-GPU
     void *nccl_comm = nullptr;
     int rank = 0, world = 1;
+    gvt_host_allgather_fn host_allgather = nullptr;  // host-mediated communicator (gvt_comm_init_host)
+    void *host_user = nullptr;
 
     // pinned host scratch for scalar read-backs
     void *pinned = nullptr;

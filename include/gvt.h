@@ -143,7 +143,7 @@ typedef struct {
     char names[GVT_MAX_KERNEL_KINDS][32];     /* kernel kind name                                      */
     int64_t counts[GVT_MAX_KERNEL_KINDS];     /* launches per kind                                     */
     double ms[GVT_MAX_KERNEL_KINDS];          /* summed CUDA-event duration (GVT_OPT_PROFILE = 1)       */
-    int32_t last_engine;                      /* engine the last matvec group used: 1 sparse, 2 dense  */
+    int32_t last_engine;                      /* engine last used: 1 sparse, 2 dense, 3 single-CTA fit */
     int32_t world;                            /* communicator size (1 without gvt_comm_init)           */
 } gvt_stats;
 

@@ -34,68 +34,76 @@ void entry_values(gvt_ctx *c, const EntryPlan &e, const float *p) {
 }
 
 // ----------------------------------------------------------------------------- stage 1
-// grid (t-tiles of TPB*TPT rows of S, h-blocks of H columns).  Each thread accumulates
-// TPT rows t (stride TPB: coalesced row-segment loads of C) for one column h at a time
-// in registers, parks the column in shared memory, and the CTA writes the H-wide
-// column block of S row by row (128-byte coalesced stores).
-template <int H, int TPB, int TPT>
+// grid (h-blocks of H columns, t-tiles of 4*TPB rows of S).  Each thread accumulates 4
+// consecutive rows t (one 16-byte load of a factor row segment per entry, four entries in
+// flight) for one column h at a time in registers, parks the column in shared memory, and the
+// CTA writes the H-wide column block of S row by row (128-byte coalesced stores).
+template <int H, int TPB>
 __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict__ row_ptr,
                                                        const int32_t *__restrict__ col,
                                                        const float *__restrict__ val, int64_t m_in,
                                                        const float *__restrict__ C, int64_t ldC, int64_t q_out,
                                                        float *__restrict__ S, int64_t ldS,
                                                        const float *__restrict__ diag, int64_t row_lo) {
-    constexpr int TT = TPB * TPT;
+    constexpr int TT = TPB * 4;
     extern __shared__ float sm[];  // [H][TT + 1]
     const int tid = threadIdx.x;
-    const int64_t t0 = (int64_t)blockIdx.x * TT;
-    const int64_t h0 = (int64_t)blockIdx.y * H;
+    // h-blocks vary fastest across the grid, so the CTAs resident at a time share one t-tile: the
+    // factor panel C[:][t0 .. t0 + TT) they read (q_in x TT floats) stays in L2 instead of the
+    // whole factor streaming through it
+    const int64_t t0 = (int64_t)blockIdx.y * TT;
+    const int64_t h0 = (int64_t)blockIdx.x * H;
+    // each thread owns 4 consecutive t: one 16-byte load per entry (ldC is a multiple of 32 and the
+    // factor is zero-padded to it, so a float4 never straddles the row end)
+    const int64_t tt = 4 * (int64_t)tid;
+    const bool tin = t0 + tt < ldC;
+    auto row4 = [&](int64_t c) -> float4 {
+        return tin ? __ldg(reinterpret_cast<const float4 *>(C + c * ldC + t0 + tt)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
     for (int hl = 0; hl < H; hl++) {
         const int64_t h = h0 + hl;
-        float acc[TPT];
-#pragma unroll
-        for (int i = 0; i < TPT; i++) acc[i] = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         if (h < m_in) {
             const int64_t kb = row_ptr[h], ke = row_ptr[h + 1];
             int64_t k = kb;
-            for (; k + 1 < ke; k += 2) {  // two entries in flight
-                const float x0 = val[k], x1 = val[k + 1];
-                const float *r0 = C + (int64_t)col[k] * ldC + t0;
-                const float *r1 = C + (int64_t)col[k + 1] * ldC + t0;
-                float v0[TPT], v1[TPT];
+            for (; k + 3 < ke; k += 4) {  // four entries in flight, accumulated in entry order
+                float x[4];
+                float4 v[4];
 #pragma unroll
-                for (int i = 0; i < TPT; i++) {
-                    const int64_t t = tid + (int64_t)TPB * i;
-                    v0[i] = (t0 + t < q_out) ? __ldg(r0 + t) : 0.f;
-                    v1[i] = (t0 + t < q_out) ? __ldg(r1 + t) : 0.f;
+                for (int u = 0; u < 4; u++) {
+                    x[u] = val[k + u];
+                    v[u] = row4(col[k + u]);
                 }
 #pragma unroll
-                for (int i = 0; i < TPT; i++) {
-                    acc[i] = fmaf(x0, v0[i], acc[i]);
-                    acc[i] = fmaf(x1, v1[i], acc[i]);
+                for (int u = 0; u < 4; u++) {
+                    acc.x = fmaf(x[u], v[u].x, acc.x);
+                    acc.y = fmaf(x[u], v[u].y, acc.y);
+                    acc.z = fmaf(x[u], v[u].z, acc.z);
+                    acc.w = fmaf(x[u], v[u].w, acc.w);
                 }
             }
-            if (k < ke) {
+            for (; k < ke; k++) {
                 const float x0 = val[k];
-                const float *r0 = C + (int64_t)col[k] * ldC + t0;
-#pragma unroll
-                for (int i = 0; i < TPT; i++) {
-                    const int64_t t = tid + (int64_t)TPB * i;
-                    acc[i] = fmaf(x0, (t0 + t < q_out) ? __ldg(r0 + t) : 0.f, acc[i]);
-                }
+                const float4 v = row4(col[k]);
+                acc.x = fmaf(x0, v.x, acc.x);
+                acc.y = fmaf(x0, v.y, acc.y);
+                acc.z = fmaf(x0, v.z, acc.z);
+                acc.w = fmaf(x0, v.w, acc.w);
             }
             if (diag) {  // separate diagonal of X (MLPK Laplacian): X[h][h] = diag[h]
                 const float dv = diag[row_lo + h];
-                const float *r0 = C + (row_lo + h) * ldC + t0;
-#pragma unroll
-                for (int i = 0; i < TPT; i++) {
-                    const int64_t t = tid + (int64_t)TPB * i;
-                    acc[i] = fmaf(dv, (t0 + t < q_out) ? __ldg(r0 + t) : 0.f, acc[i]);
-                }
+                const float4 v = row4(row_lo + h);
+                acc.x = fmaf(dv, v.x, acc.x);
+                acc.y = fmaf(dv, v.y, acc.y);
+                acc.z = fmaf(dv, v.z, acc.z);
+                acc.w = fmaf(dv, v.w, acc.w);
             }
         }
-#pragma unroll
-        for (int i = 0; i < TPT; i++) sm[hl * (TT + 1) + tid + TPB * i] = acc[i];
+        float *dst = sm + hl * (TT + 1) + tt;
+        dst[0] = acc.x;
+        dst[1] = acc.y;
+        dst[2] = acc.z;
+        dst[3] = acc.w;
     }
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5;
@@ -111,18 +119,18 @@ __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict
 
 void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
                    const float *diag, int64_t row_lo) {
-    constexpr int H = 32, TPB = 128, TPT = 4, TT = TPB * TPT;
+    constexpr int H = 32, TPB = 128, TT = TPB * 4;
     if (q_out == 0 || ldS == 0) return;
-    dim3 grid((unsigned)((q_out + TT - 1) / TT), (unsigned)((ldS + H - 1) / H));
+    dim3 grid((unsigned)((ldS + H - 1) / H), (unsigned)((q_out + TT - 1) / TT));
     size_t smem = sizeof(float) * H * (TT + 1);
     static bool attr[GVT_MAX_DEVICES] = {};  // per device ordinal
     bool &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
     if (!attr_dev) {
-        GVT_CUDA_TRY(cudaFuncSetAttribute(k_stage1_sparse<H, TPB, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_stage1_sparse<H, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr_dev = true;
     }
-    GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB, TPT>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
+    GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
                C.p, C.ld, q_out, S, ldS, diag, row_lo);
 }
 

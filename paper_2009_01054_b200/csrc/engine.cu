@@ -673,6 +673,14 @@ static Factor prepare_factor(gvt_ctx *c, const char *name, const float *user, in
     f.ld = round_up(cols > 0 ? cols : 1, 32);
     int64_t rows_pad = round_up(rows > 0 ? rows : 1, 128);
     std::string nm(name);
+    // zero-copy: a device Gram whose rows are already 32-float multiples and 16-byte aligned is
+    // read in place by the SIMT kernels (they never touch rows >= rows or columns >= ld); the
+    // tensor-core split and the transposed rectangular copy still take the padded copy
+    if (!need_split && !rect && rows > 0 && cols > 0 && cols % 32 == 0 && ((uintptr_t)user & 15) == 0 &&
+        is_device_ptr(user)) {
+        f.p = user;
+        return f;
+    }
     float *d = wsT<float>(c, (nm + ".pad").c_str(), (size_t)rows_pad * f.ld);
     const float *src = user;
     if (rows > 0 && cols > 0) {

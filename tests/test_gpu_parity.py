@@ -161,6 +161,49 @@ def test_matvec_medium_vs_oracle_gvt(engine_ctx, kernel):
 
 
 @pytest.mark.parametrize("kernel", K_ALL)
+def test_sparse_engine_reads_aligned_grams_in_place(ctx, kernel):
+    """Device Grams whose rows are 32-float multiples and 16-byte aligned are read in place by
+    the SIMT engine (no padded copy); a misaligned view of the same values takes the copy.
+    Both match the oracle's per-term GVT, and the padded copy is skipped exactly when expected."""
+    hom = kernel in HOM
+    rng = np.random.default_rng(300 + kernel)
+    m, q = 256, (256 if hom else 192)
+    Xd = rng.standard_normal((m, 16)).astype(np.float32)
+    Xt = None if hom else rng.standard_normal((q, 16)).astype(np.float32)
+    D32 = f32(O.gram(G.BASE_GAUSSIAN, Xd, gamma=1 / 16))
+    T32 = None if hom else f32(O.gram(G.BASE_GAUSSIAN, Xt, gamma=1 / 16))
+    inf, ins = rng.integers(0, m, 5000).astype(np.int32), rng.integers(0, q, 5000).astype(np.int32)
+    of, os_ = rng.integers(0, m, 3001).astype(np.int32), rng.integers(0, q, 3001).astype(np.int32)
+    a = synth.random_vector(kernel, 5000)
+    terms = G.gvt_kernel_terms(kernel)
+    ref = O.gvt_matvec(O.kernel_terms(kernel), D32, T32, of, os_, inf, ins, a)
+
+    def shifted(x):  # same values at a 4-byte offset: not 16-byte aligned
+        if x is None:
+            return None
+        buf = torch.empty(x.size + 1, dtype=torch.float32, device="cuda")
+        buf[1:] = dev(x).reshape(-1)
+        return buf[1:].view(x.shape)
+
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_SPARSE)
+    try:
+        outs = []
+        for Dd, Td, copies in ((dev(D32), None if hom else dev(T32), False),
+                               (shifted(D32), shifted(T32), True)):
+            ctx.reset_stats()
+            ctx.set_option(G.OPT_PROFILE, 1)
+            u = ctx.matvec(Dd, Td, dev(of), dev(os_), dev(inf), dev(ins), dev(a), terms).cpu().numpy()
+            ctx.set_option(G.OPT_PROFILE, 0)
+            assert ("pad_copy" in ctx.stats()["kinds"]) == copies
+            assert rel(u, ref) <= MATVEC_TOL, rel(u, ref)
+            outs.append(u)
+        assert np.array_equal(outs[0], outs[1])  # same kernels, same order: bit-identical
+    finally:
+        ctx.set_option(G.OPT_PROFILE, 0)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("kernel", K_ALL)
 def test_generic_term_path(ctx, kernel):
     """A term list that is not a recognised Corollary list (reversed order) runs term by
     term (Ones / Identity factors materialised) and still matches the oracle."""

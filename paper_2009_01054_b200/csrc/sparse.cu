@@ -34,11 +34,15 @@ void entry_values(gvt_ctx *c, const EntryPlan &e, const float *p) {
 }
 
 // ----------------------------------------------------------------------------- stage 1
-// grid (h-blocks of H columns, t-tiles of 4*TPB rows of S).  Each thread accumulates 4
-// consecutive rows t (one 16-byte load of a factor row segment per entry, four entries in
-// flight) for one column h at a time in registers, parks the column in shared memory, and the
-// CTA writes the H-wide column block of S row by row (128-byte coalesced stores).
-template <int H, int TPB>
+// grid (h-blocks of H columns, t-tiles of 4*TPB rows of S).  The CTA walks the entries of its H
+// rows (one contiguous CSR range) in chunks of CH staged in shared memory (coalesced index/value
+// loads, then broadcast reads), so the only global loads in the inner loop are the independent
+// factor-row segments: each thread owns 4 consecutive rows t (one 16-byte load per entry; the
+// loop is unrolled by eight, ptxas keeps about four in flight at 32 registers, and occupancy
+// hides the rest), accumulates one column h at a time in entry order, parks it in shared memory
+// when the row ends, and the CTA writes the H-wide column block of S row by row (H * 4-byte
+// segments per row of S).
+template <int H, int TPB, int CH>
 __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict__ row_ptr,
                                                        const int32_t *__restrict__ col,
                                                        const float *__restrict__ val, int64_t m_in,
@@ -46,92 +50,113 @@ __global__ void __launch_bounds__(TPB) k_stage1_sparse(const int64_t *__restrict
                                                        float *__restrict__ S, int64_t ldS,
                                                        const float *__restrict__ diag, int64_t row_lo) {
     constexpr int TT = TPB * 4;
-    extern __shared__ float sm[];  // [H][TT + 1]
+    extern __shared__ float sm[];  // park [H][TT + 1] | chunk values [CH] | chunk columns [CH]
+    float *sval = sm + H * (TT + 1);
+    int32_t *scol = reinterpret_cast<int32_t *>(sval + CH);
+    __shared__ int64_t srp[H + 1];
     const int tid = threadIdx.x;
     // h-blocks vary fastest across the grid, so the CTAs resident at a time share one t-tile: the
     // factor panel C[:][t0 .. t0 + TT) they read (q_in x TT floats) stays in L2 instead of the
     // whole factor streaming through it
     const int64_t t0 = (int64_t)blockIdx.y * TT;
     const int64_t h0 = (int64_t)blockIdx.x * H;
+    const int hv = (int)max((int64_t)0, min((int64_t)H, m_in - h0));  // valid rows of this block
+    if (hv > 0)  // (a block past the last row has no row pointers to read)
+        for (int i = tid; i <= hv; i += TPB) srp[i] = row_ptr[h0 + i];
     // each thread owns 4 consecutive t: one 16-byte load per entry (ldC is a multiple of 32 and the
     // factor is zero-padded to it, so a float4 never straddles the row end)
-    const int64_t tt = 4 * (int64_t)tid;
-    const bool tin = t0 + tt < ldC;
-    auto row4 = [&](int64_t c) -> float4 {
-        return tin ? __ldg(reinterpret_cast<const float4 *>(C + c * ldC + t0 + tt)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // (threads past the row end of the last t-tile read column 0 instead: unconditional loads keep
+    // the eight in flight, and their sums are never stored -- only t < q_out <= ldC are written)
+    const int tt = 4 * tid;
+    const float *Ct = C + (t0 + tt < ldC ? t0 + tt : 0);
+    auto row4 = [&](int64_t c) -> float4 { return __ldg(reinterpret_cast<const float4 *>(Ct + c * ldC)); };
+    auto fma4 = [](float x, const float4 &v, float4 &acc) {
+        acc.x = fmaf(x, v.x, acc.x);
+        acc.y = fmaf(x, v.y, acc.y);
+        acc.z = fmaf(x, v.z, acc.z);
+        acc.w = fmaf(x, v.w, acc.w);
     };
-    for (int hl = 0; hl < H; hl++) {
-        const int64_t h = h0 + hl;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (h < m_in) {
-            const int64_t kb = row_ptr[h], ke = row_ptr[h + 1];
-            int64_t k = kb;
-            for (; k + 3 < ke; k += 4) {  // four entries in flight, accumulated in entry order
-                float x[4];
-                float4 v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    x[u] = val[k + u];
-                    v[u] = row4(col[k + u]);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    acc.x = fmaf(x[u], v[u].x, acc.x);
-                    acc.y = fmaf(x[u], v[u].y, acc.y);
-                    acc.z = fmaf(x[u], v[u].z, acc.z);
-                    acc.w = fmaf(x[u], v[u].w, acc.w);
-                }
-            }
-            for (; k < ke; k++) {
-                const float x0 = val[k];
-                const float4 v = row4(col[k]);
-                acc.x = fmaf(x0, v.x, acc.x);
-                acc.y = fmaf(x0, v.y, acc.y);
-                acc.z = fmaf(x0, v.z, acc.z);
-                acc.w = fmaf(x0, v.w, acc.w);
-            }
-            if (diag) {  // separate diagonal of X (MLPK Laplacian): X[h][h] = diag[h]
-                const float dv = diag[row_lo + h];
-                const float4 v = row4(row_lo + h);
-                acc.x = fmaf(dv, v.x, acc.x);
-                acc.y = fmaf(dv, v.y, acc.y);
-                acc.z = fmaf(dv, v.z, acc.z);
-                acc.w = fmaf(dv, v.w, acc.w);
-            }
+    auto park = [&](int hl, float4 acc) {
+        if (hl < hv && diag) {  // separate diagonal of X (MLPK Laplacian): X[h][h] = diag[h], added last
+            const int64_t hd = row_lo + h0 + hl;
+            fma4(diag[hd], row4(hd), acc);
         }
         float *dst = sm + hl * (TT + 1) + tt;
         dst[0] = acc.x;
         dst[1] = acc.y;
         dst[2] = acc.z;
         dst[3] = acc.w;
+    };
+    __syncthreads();
+    const int64_t e0 = hv > 0 ? srp[0] : 0, e1 = hv > 0 ? srp[hv] : 0;
+    int hl = 0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t cb = e0; cb < e1; cb += CH) {
+        const int n = (int)min((int64_t)CH, e1 - cb);
+        __syncthreads();  // the previous chunk is consumed
+        for (int i = tid; i < n; i += TPB) {
+            sval[i] = val[cb + i];
+            scol[i] = col[cb + i];
+        }
+        __syncthreads();
+        int i = 0;
+        while (i < n) {
+            while (cb + i >= srp[hl + 1]) {  // rows that ended (or are empty) before entry cb + i
+                park(hl, acc);
+                acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                hl++;
+            }
+            const int iend = (int)min((int64_t)n, srp[hl + 1] - cb);
+            for (; i + 7 < iend; i += 8) {  // eight entries per step, accumulated in entry order
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = row4(scol[i + u]);
+#pragma unroll
+                for (int u = 0; u < 8; u++) fma4(sval[i + u], v[u], acc);
+            }
+            for (; i < iend; i++) fma4(sval[i], row4(scol[i]), acc);
+        }
+    }
+    for (; hl < H; hl++) {  // the last row with entries, then empty rows and rows >= m_in
+        park(hl, acc);
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5;
     for (int t = warp; t < TT; t += TPB / 32) {
         const int64_t tg = t0 + t;
         if (tg >= q_out) break;
-        for (int hl = lane; hl < H; hl += 32) {
-            const int64_t h = h0 + hl;
-            if (h < ldS) S[tg * ldS + h] = sm[hl * (TT + 1) + t];  // h >= m_in writes the zero padding
+        for (int hl2 = lane; hl2 < H; hl2 += 32) {
+            const int64_t h = h0 + hl2;
+            if (h < ldS) S[tg * ldS + h] = sm[hl2 * (TT + 1) + t];  // h >= m_in writes the zero padding
         }
     }
 }
 
-void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
-                   const float *diag, int64_t row_lo) {
-    constexpr int H = 32, TPB = 128, TT = TPB * 4;
-    if (q_out == 0 || ldS == 0) return;
+template <int H, int CH>
+static void stage1_sparse_h(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
+                            const float *diag, int64_t row_lo) {
+    constexpr int TPB = 128, TT = TPB * 4;
     dim3 grid((unsigned)((ldS + H - 1) / H), (unsigned)((q_out + TT - 1) / TT));
-    size_t smem = sizeof(float) * H * (TT + 1);
+    size_t smem = sizeof(float) * H * (TT + 1) + (sizeof(float) + sizeof(int32_t)) * CH;
     static bool attr[GVT_MAX_DEVICES] = {};  // per device ordinal
     bool &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
     if (!attr_dev) {
-        GVT_CUDA_TRY(cudaFuncSetAttribute(k_stage1_sparse<H, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_stage1_sparse<H, TPB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr_dev = true;
     }
-    GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
+    GVT_LAUNCH(c, K_STAGE1_SPARSE, (k_stage1_sparse<H, TPB, CH>), grid, TPB, smem, e.row_ptr, e.col, e.val, e.nrow,
                C.p, C.ld, q_out, S, ldS, diag, row_lo);
+}
+
+void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
+                   const float *diag, int64_t row_lo) {
+    if (q_out == 0 || ldS == 0) return;
+    // H = 8 columns per CTA: 24.6 KB of shared memory, so 9 CTAs (36 warps) per SM hide the
+    // factor-row load latency (H = 32: 3 CTAs; measured 5.0 vs 8.4 ms in the 0.2 % gather regime,
+    // 517 vs 765 ms at C5 density, scripts/gather_regime_probe.py / gather_probe.py)
+    stage1_sparse_h<8, 1024>(c, e, C, q_out, S, ldS, diag, row_lo);
 }
 
 // ----------------------------------------------------------------------------- stage 2

@@ -249,6 +249,60 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def gather_regime_leg(local_rank, peaks, reps=5):
+    """North-star gather target on its own regime: the sparse
+    engine at C5 object counts and 0.2 % density (synth.gather_regime), where stage 2 is the row
+    gather.  Device-timed with the library's per-kernel CUDA events.  Compulsory DRAM bytes of
+    the gather: one S row per output (4 * m_in B; S is 13x the L2) plus each A row once (the
+    outputs are sorted by row)."""
+    import torch
+
+    import paper_2009_01054_b200 as G
+    w = synth.gather_regime()
+    dev = torch.device("cuda", local_rank)
+
+    def d(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    res = {"workload": f"gather regime: m=q={w.m}, {w.n} uniform train pairs ({w.n / (w.m * w.q):.1%} density), "
+                       f"{w.n_test} uniform test pairs, Gaussian dim {w.Xd.shape[1]}, Kronecker",
+           "ncu_dram": "profiles/r01_gather_regime_ncu.txt"}
+    with G.Context(local_rank) as ctx:
+        D = ctx.gram(w.base, d(w.Xd), gamma=w.gamma)
+        T = ctx.gram(w.base, d(w.Xt), gamma=w.gamma)
+        terms = G.gvt_kernel_terms(G.KRONECKER)
+        f, s, tf, ts = d(w.train_first), d(w.train_second), d(w.test_first), d(w.test_second)
+        a = d(synth.random_vector(0, w.n))
+        u = torch.empty(w.n, dtype=torch.float32, device=dev)
+        sc = torch.empty(w.n_test, dtype=torch.float32, device=dev)
+        for name, call, n_out in (("matvec", lambda: ctx.matvec(D, T, f, s, f, s, a, terms, out=u), w.n),
+                                  ("predict", lambda: ctx.predict(D, T, tf, ts, f, s, a, terms, out=sc), w.n_test)):
+            for _ in range(3):
+                call()
+            torch.cuda.synchronize(dev)
+            ctx.reset_stats()
+            ctx.set_option(G.OPT_PROFILE, 1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                call()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ctx.set_option(G.OPT_PROFILE, 0)
+            st = ctx.stats()
+            g = st["kinds"]["stage2_gather"]
+            gms = g["ms"] / g["count"]
+            comp = 4.0 * w.m * n_out + 4.0 * w.m * w.m
+            res[name] = {"ms": e0.elapsed_time(e1) / reps, "Gpairs_per_s": n_out / (e0.elapsed_time(e1) / reps * 1e-3) / 1e9,
+                         "engine": {1: "sparse", 2: "dense"}.get(st["last_engine"]),
+                         "stage1_sparse_ms": st["kinds"]["stage1_sparse"]["ms"] / reps, "stage2_gather_ms": gms,
+                         "gather_compulsory_GB": comp / 1e9, "gather_GBps": comp / (gms * 1e-3) / 1e9,
+                         "gather_frac_hbm": comp / (gms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "gather_row_bytes_GBps": 8.0 * w.m * n_out / (gms * 1e-3) / 1e9}
+    res["hbm_peak_GBps"] = peaks["hbm_gbs"]
+    return res
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -403,6 +457,11 @@ def run_gpu(args, rank, world, local_rank):
             "gpu_launches": int(st["launches"]),
             "kernel_ms": {k: round(v["ms"] / args.steps, 3) for k, v in st["kinds"].items()} if args.profile else None,
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
+    if args.gather_regime and world == 1:
+        ctx.close()  # free the C5 workspaces first
+        del D, T, a, scores, fD, sD, yD, tfD, tsD
+        torch.cuda.empty_cache()
+        line["gather_regime"] = gather_regime_leg(local_rank, peaks)
     print(json.dumps(line), flush=True)
 
 
@@ -424,6 +483,8 @@ def main():
     ap.add_argument("--no-profile", dest="profile", action="store_false")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather-regime", dest="gather_regime", action="store_false",
+                    help="skip the sparse-engine gather-regime leg (0.2 %% density at C5 object counts)")
     ap.add_argument("--ref-targets", type=int, default=32)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))

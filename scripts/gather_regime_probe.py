@@ -7,7 +7,7 @@ factors (1.6 GB each) are far above the 126 MB L2:
 
   m = q = 20 000 objects, dim 128 N(0,1) features, Gaussian gamma = 1/128 (S5);
   n_train uniform pairs (default 8e5 = 0.2 % of the grid), n_test uniform test pairs (2e6);
-  y, a ~ N(0, 1).  Seeded (PCG64, seed 7).
+  a ~ N(0, 1).  Seeded (synth.gather_regime, PCG64 seed 7).
 
 The auto engine picks the sparse path at this density (density threshold 2 %).  Times, with the
 library's per-kernel CUDA events: the training matvec (stage 1 + gather over n_train outputs) and
@@ -26,6 +26,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2009_01054_b200 as G  # noqa: E402
+import synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=20_000)
@@ -35,15 +36,10 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--engine", type=int, default=0, help="GVT_OPT_ENGINE (0 auto, 1 sparse, 2 dense)")
 args = ap.parse_args()
 
+w = synth.gather_regime(m=args.m, n=args.n_train, n_test=args.n_test)
 m = q = args.m
-rng = np.random.default_rng(7)
-Xd = rng.standard_normal((m, 128), dtype=np.float32)
-Xt = rng.standard_normal((q, 128), dtype=np.float32)
-f = rng.integers(0, m, args.n_train).astype(np.int32)
-s = rng.integers(0, q, args.n_train).astype(np.int32)
-tf = rng.integers(0, m, args.n_test).astype(np.int32)
-ts = rng.integers(0, q, args.n_test).astype(np.int32)
-a_h = rng.standard_normal(args.n_train).astype(np.float32)
+Xd, Xt, f, s, tf, ts = w.Xd, w.Xt, w.train_first, w.train_second, w.test_first, w.test_second
+a_h = synth.random_vector(0, args.n_train)
 
 d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
 ctx = G.Context(0)

@@ -245,6 +245,24 @@ def config5(n: int = 100_000_000, n_test: int = 20_000_000, m: int = 20_000, dim
                     _i32(tf), _i32(ts), 1.0, 30, (KRONECKER,))
 
 
+def gather_regime(m: int = 20_000, n: int = 800_000, n_test: int = 2_000_000, dim: int = 128,
+                  seed: int = 7) -> Workload:
+    """The SIMT-gather regime at C5 object counts (density below ~2 %, where the
+    north star's "stage-2 gather at >= 60 % of HBM" applies): m = q objects, dim N(0,1)
+    features, Gaussian gamma = 1/dim (S5); n uniform training pairs (default 0.2 % of the grid,
+    Heterodimer-like), n_test uniform test pairs, y ~ N(0,1); lambda 1, 30 iterations."""
+    rng = np.random.default_rng(seed)
+    Xd = rng.standard_normal((m, dim), dtype=np.float32)
+    Xt = rng.standard_normal((m, dim), dtype=np.float32)
+    f = rng.integers(0, m, n)
+    s = rng.integers(0, m, n)
+    tf = rng.integers(0, m, n_test)
+    ts = rng.integers(0, m, n_test)
+    y = rng.standard_normal(n, dtype=np.float32)
+    return Workload("gather", Xd, Xt, BASE_GAUSSIAN, 1.0 / dim, _i32(f), _i32(s), _f32(y), _i32(tf), _i32(ts),
+                    1.0, 30, (KRONECKER,))
+
+
 CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
 
 

@@ -96,3 +96,7 @@ def test_bench_json_contract_on_c1():
         assert k in d, k
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    g = d["gather_regime"]  # the sparse-engine gather leg (0.2 % density at C5 object counts)
+    for leg in ("matvec", "predict"):
+        assert g[leg]["engine"] == "sparse" and g[leg]["stage2_gather_ms"] > 0
+        assert 0 < g[leg]["gather_frac_hbm"] < 2.0

@@ -1110,7 +1110,7 @@ bool fused_f16(gvt_ctx *c, int64_t q_in) {
 // gathers); 256 for rows of <= 8192 columns, where the per-row barrier chain dominates and more rows
 // (smaller shared-memory rows) must be in flight per SM
 template <int BX_THREADS>
-__global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+__global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                                    const int32_t *__restrict__ src, const float *__restrict__ sign,
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
                                                    int64_t cols, int64_t ld, __half *__restrict__ hi,
@@ -1122,12 +1122,35 @@ __global__ void __launch_bounds__(BX_THREADS) k_build_x16(const int64_t *__restr
         for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
         __syncthreads();
         const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
-        for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
-            const int32_t cc = col[k];
-            if (k > kb && col[k - 1] == cc) continue;  // not the head of its run
-            float s = sign[k] * __ldg(p + src[k]);
-            for (int64_t j = k + 1; j < ke && col[j] == cc; j++) s += sign[j] * __ldg(p + src[j]);
-            rowbuf[cc] = s;
+        // two entries per thread per pass, their loads independent (in flight together); a run
+        // of duplicate cells is summed by its head entry in entry order.  With the 32-register
+        // bound two 1024-thread CTAs (two 80 KB rows) are resident per SM: C5 2.59 -> 1.37 ms
+        // per launch (profiles/r01_ab_build_x16.txt)
+        constexpr int U = 2;
+        for (int64_t k0 = kb + threadIdx.x; k0 < ke; k0 += U * BX_THREADS) {
+            int32_t cc[U], cprev[U], cnext[U];
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t k = k0 + (int64_t)u * BX_THREADS;
+                cc[u] = -1;
+                if (k < ke) {
+                    cc[u] = col[k];
+                    cprev[u] = k > kb ? col[k - 1] : -1;
+                    cnext[u] = k + 1 < ke ? col[k + 1] : -1;
+                    v[u] = sign[k] * __ldg(p + src[k]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (cc[u] < 0 || cprev[u] == cc[u]) continue;  // past the row end, or not the head of its run
+                float s = v[u];
+                if (cnext[u] == cc[u]) {
+                    const int64_t k = k0 + (int64_t)u * BX_THREADS;
+                    for (int64_t j = k + 1; j < ke && col[j] == cc[u]; j++) s += sign[j] * __ldg(p + src[j]);
+                }
+                rowbuf[cc[u]] = s;
+            }
         }
         __syncthreads();
         if (diag && threadIdx.x == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)

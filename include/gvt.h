@@ -122,10 +122,15 @@ typedef enum {
                                     sorted by (first, second) and returns a_out in caller order (the
                                     same iterates up to dot-product summation order; entries read in
                                     vector order); 0 = caller order                                   */
-    GVT_OPT_KBLOCK_SKIP = 12     /* 1 (default): the dense stage 1 skips the all-zero 64-column
+    GVT_OPT_KBLOCK_SKIP = 12,    /* 1 (default): the dense stage 1 skips the all-zero 64-column
                                     K-blocks of each 256-row tile of the pair matrix when they are at
                                     least 15 % of the blocks (block-sparse X, e.g. MLPK on a union
                                     domain); 0 = always the full K loop                              */
+    GVT_OPT_STAGE2 = 13          /* stage 2 of the dense engine: 0 (default) = by estimated time (the
+                                    sampled tensor-core GEMM, or the row gather u_i = <A[r_i,:],
+                                    S[c_i,:]> over the tensor-core S when the contraction is short and
+                                    the samples few, e.g. C2); 1 = always the sampled GEMM; 2 =
+                                    always the gather                                                 */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

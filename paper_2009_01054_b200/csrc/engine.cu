@@ -145,6 +145,9 @@ struct Problem {
     const int32_t *of_full = nullptr, *os_full = nullptr;
     int64_t n_out_full = 0;
     std::vector<int64_t> out_counts, out_offsets;
+    // outputs appended to the fit's own (the early-stopping validation pairs): left out of the
+    // stage-2 dispatch estimate, so the early-stopping fit runs the same kernels as a plain fit
+    int64_t n_out_extra = 0;
     int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
     int64_t dom_out(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m_out : q_out; }
 };
@@ -476,6 +479,20 @@ static void uex_finish(gvt_ctx *c, const Problem &P, const GroupPlan &g, const f
     if (accumulate) add_into(c, local, n, out);
 }
 
+// dense engine, stage 2 of one slab: the sampled tensor-core GEMM computes every (r, c) cell of
+// the tile grid and serves the samples from its epilogue; the row gather reads one A row and one
+// S row per sample.  On short contractions with few samples (C2: K = 68, 3e4 samples) the GEMM's
+// fixed cost (prologue, serial K loop, sample serving) dominates and the gather wins.  Estimates
+// from the B200 measurements: GEMM ~25 us + 6*M*N*K flops (3xFP16, 256/64-padded) at ~1.1 PFLOP/s;
+// gather ~4 us + 8 B per (sample, k) at ~6 TB/s.
+static bool stage2_gather_pays(gvt_ctx *c, int64_t ns, int64_t M, int64_t N, int64_t K) {
+    if (c->stage2 == 1) return false;
+    if (c->stage2 == 2) return true;
+    const double tc = 25.0 + 6.0 * (double)round_up(M, 256) * (double)round_up(N, 256) * (double)round_up(K, 64) / 1.1e9;
+    const double ga = 4.0 + 8.0 * (double)ns * (double)K / 6e6;
+    return ga < tc;
+}
+
 static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
                           float *out) {
     // S scales: one per (row, 256-col tile) from the tile maxima, applied per K-chunk in stage 2
@@ -527,11 +544,16 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
         } else {
             so.scale = Sk + s * slab_k;  // one scale per S row, applied once after the K loop
         }
-        if (P.uex)  // this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1
-            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, !first, partial);
-        else
-            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef,
-                            accumulate || !first, out);
+        // (P.uex: this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1)
+        float *dst = P.uex ? partial : out;
+        const int acc = P.uex ? !first : (accumulate || !first);
+        if (tile_scale && stage2_gather_pays(c, g.smp.ns - P.n_out_extra, g.A.n, g.q_out, w)) {
+            Factor Av = g.A;
+            Av.p = g.A.p + lo;
+            stage2_gather16(c, g.smp, Av, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k, skld, w, coef, acc, dst);
+        } else {
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, dst);
+        }
         first = false;
     }
     if (P.uex) uex_finish(c, P, g, partial, accumulate, out);
@@ -590,7 +612,7 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
         const int acc = P.uex ? !first : (accumulate || !first);
         first = false;
         float *Ss = g.S + (size_t)s * g.qpad * g.W;
-        if (g.engine == 2) {
+        if (g.engine == 2 && !stage2_gather_pays(c, g.smp.ns - P.n_out_extra, g.A.n, g.q_out, w)) {
             char nm[48];
             snprintf(nm, sizeof(nm), "dense.Sop%d", s);
             Operand so = make_operand(c, nm, Ss, g.q_out, w, g.W, g.W, g.qpad);
@@ -1021,6 +1043,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
             GVT_CUDA_TRY(cudaMemcpyAsync(os + off[k], ds, sizeof(int32_t) * cnt[k], cudaMemcpyDeviceToDevice, c->stream));
         }
         setup_problem(c, P, D, m, T, q, of, os, no, of, os, n, terms, n_terms, form, false);
+        P.n_out_extra = P.uex ? P.n_out_full - P.n_in : n_val;
     } else {
         setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form, true);
     }

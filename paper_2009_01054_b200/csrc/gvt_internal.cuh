@@ -95,8 +95,9 @@ struct gvt_ctx {
     int graphs = 1;        // CUDA-graph replay of the solver iteration
     int solver = 0;        // GVT_SOLVER_CG / GVT_SOLVER_MINRES
     int exchange = 0;      // multi-GPU: 0 = S slab all-gather, 1 = u reduce (NEXT-3)
-    int sorted_fit = 1;
-    int kblock_skip = 1;   // block-sparse stage 1 (skip all-zero K-blocks of X) where it pays    // fits run on the pairs sorted by (first, second)
+    int sorted_fit = 1;    // fits run on the pairs sorted by (first, second)
+    int kblock_skip = 1;   // block-sparse stage 1 (skip all-zero K-blocks of X) where it pays
+    int stage2 = 0;        // dense-engine stage 2: 0 = by estimated time, 1 = sampled GEMM, 2 = gather
     int cg_variant = 0;    // 0 = Hestenes-Stiefel CG, 1 = Chronopoulos-Gear (one reduction per iteration)
     cudaStream_t cap_stream = nullptr;  // side stream used only for graph capture
     int last_engine = 0;

@@ -100,6 +100,8 @@ void entry_values(gvt_ctx *c, const EntryPlan &e, const float *p);
 // S[t][h] = sum_{entries (h, col)} val C[col][t] (+ diag[row_lo + h] C[row_lo + h][t] if diag)
 void stage1_sparse(gvt_ctx *c, const EntryPlan &e, const Factor &C, int64_t q_out, float *S, int64_t ldS,
                    const float *diag = nullptr, int64_t row_lo = 0);
+void stage2_gather16(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const __half *Sh, const __half *Sl,
+                     int64_t ldS, const float *sk, int64_t skld, int64_t K, float coef, int accumulate, float *out);
 void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const float *S, int64_t ldS, int64_t K,
                    float coef, int accumulate, float *out);
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)

@@ -204,6 +204,47 @@ void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const floa
                sp.ns, sp.r, sp.c, sp.dst, A.p, A.ld, S, ldS, K4, coef, accumulate, out);
 }
 
+// the same gather over the dense engine's S, stored by the stage-1 GEMM as fp16 pieces with one
+// power-of-two scale per (row, 256-column chunk): S[c][h] = (hi + lo) * sk[(h / 256) * skld + c].
+// Lanes take column pairs (half2 / float2 loads) in a fixed order, then a butterfly.
+__global__ void __launch_bounds__(256) k_stage2_gather16(int64_t ns, const int32_t *__restrict__ sr,
+                                                         const int32_t *__restrict__ sc,
+                                                         const int32_t *__restrict__ sdst,
+                                                         const float *__restrict__ A, int64_t ldA,
+                                                         const __half *__restrict__ Sh, const __half *__restrict__ Sl,
+                                                         int64_t ldS, const float *__restrict__ sk, int64_t skld,
+                                                         int64_t K, float coef, int accumulate, float *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < ns; k += warps) {
+        const int64_t c = sc[k];
+        const float2 *a = reinterpret_cast<const float2 *>(A + (int64_t)sr[k] * ldA);
+        const __half2 *h2 = reinterpret_cast<const __half2 *>(Sh + c * ldS);
+        const __half2 *l2 = reinterpret_cast<const __half2 *>(Sl + c * ldS);
+        float acc = 0.f;
+        for (int64_t j = lane; 2 * j < K; j += 32) {
+            const int64_t h = 2 * j;
+            const float s = __ldg(sk + (h >> 8) * skld + c);  // h and h + 1 share the chunk
+            const float2 av = __ldg(a + j);
+            const float2 hv = __half22float2(h2[j]), lv = __half22float2(l2[j]);
+            acc = fmaf(av.x, (hv.x + lv.x) * s, acc);
+            if (h + 1 < K) acc = fmaf(av.y, (hv.y + lv.y) * s, acc);  // (the padding column is never used)
+        }
+        const float v = warp_sum(acc);
+        if (lane == 0) {
+            const int64_t d = sdst[k];
+            out[d] = accumulate ? fmaf(coef, v, out[d]) : coef * v;
+        }
+    }
+}
+
+void stage2_gather16(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const __half *Sh, const __half *Sl,
+                     int64_t ldS, const float *sk, int64_t skld, int64_t K, float coef, int accumulate, float *out) {
+    if (sp.ns == 0) return;
+    GVT_LAUNCH(c, K_STAGE2_GATHER, k_stage2_gather16, grid1d(sp.ns * 32, 256, (int64_t)c->sm_count * 16), 256, 0,
+               sp.ns, sp.r, sp.c, sp.dst, A.p, A.ld, Sh, Sl, ldS, sk, skld, K, coef, accumulate, out);
+}
+
 // ----------------------------------------------------------------------------- cheap terms
 // b[h] = sum_{k in row h} val[k], one warp per row, lanes strided + butterfly
 __global__ void k_segment_sum(const int64_t *__restrict__ row_ptr, int64_t nrow, const float *__restrict__ val,

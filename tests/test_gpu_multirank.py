@@ -39,12 +39,13 @@ def _worker(rank, world, port, case, out_path):
         import oracle as O  # noqa: F401
         import paper_2009_01054_b200 as G
         import synth
-        kernel, engine, exchange, solver = case
+        kernel, engine, exchange, solver, stage2 = case
         w = synth.config1() if kernel == G.KRONECKER else synth.config3(n=20_000, n_test=3_000)
         hom = w.Xt is None
         ctx = G.Context(0)
         ctx.comm_init_host(rank, world)
         ctx.set_option(G.OPT_ENGINE, engine)
+        ctx.set_option(G.OPT_STAGE2, stage2)
         ctx.set_option(G.OPT_EXCHANGE, exchange)
         ctx.set_option(G.OPT_SOLVER, 1 if solver == 1 else 0)
         ctx.set_option(G.OPT_CG_VARIANT, 1 if solver == 2 else 0)  # 2 = single-reduction CG
@@ -107,13 +108,15 @@ def _check(case):
     assert np.linalg.norm(sc - so) / np.linalg.norm(so) <= 1e-5
 
 
-CASES = [  # (kernel, engine, exchange, solver: 0 CG, 1 MINRES, 2 single-reduction CG)
-    (3, 2, 0, 0), (3, 1, 0, 0), (3, 2, 1, 0), (3, 2, 0, 1), (3, 2, 0, 2),
-    (4, 2, 0, 0), (4, 1, 1, 0), (7, 2, 1, 0), (7, 1, 0, 0),
+CASES = [  # (kernel, engine, exchange, solver: 0 CG, 1 MINRES, 2 single-reduction CG,
+    #          dense stage 2: 1 sampled GEMM, 2 gather over the tensor-core S)
+    (3, 2, 0, 0, 1), (3, 1, 0, 0, 0), (3, 2, 1, 0, 1), (3, 2, 0, 1, 1), (3, 2, 0, 2, 1),
+    (4, 2, 0, 0, 1), (4, 1, 1, 0, 0), (7, 2, 1, 0, 1), (7, 1, 0, 0, 0),
+    (3, 2, 0, 0, 2), (7, 2, 1, 0, 2),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"k{k}-e{e}-x{x}-s{s}" for k, e, x, s in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[f"k{k}-e{e}-x{x}-s{s}-g{g}" for k, e, x, s, g in CASES])
 def test_two_ranks_on_one_gpu_match_oracle(case):
     _check(case)
 

@@ -45,14 +45,19 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(params=[(G.ENGINE_SPARSE, 0), (G.ENGINE_AUTO, 0), (G.ENGINE_DENSE, G.PREC_FP16X3),
-                        (G.ENGINE_DENSE, G.PREC_TF32X3)], ids=["sparse", "auto", "dense-fp16x3", "dense-tf32x3"])
+# (engine, tensor-core precision, dense stage 2: 0 auto / 1 sampled GEMM / 2 gather over the TC S)
+@pytest.fixture(params=[(G.ENGINE_SPARSE, 0, 0), (G.ENGINE_AUTO, 0, 0), (G.ENGINE_DENSE, G.PREC_FP16X3, 1),
+                        (G.ENGINE_DENSE, G.PREC_FP16X3, 2), (G.ENGINE_DENSE, G.PREC_TF32X3, 1),
+                        (G.ENGINE_DENSE, G.PREC_TF32X3, 2)],
+                ids=["sparse", "auto", "dense-fp16x3", "dense-fp16x3-gather2", "dense-tf32x3", "dense-tf32x3-gather2"])
 def engine_ctx(request, ctx):
     ctx.set_option(G.OPT_ENGINE, request.param[0])
     ctx.set_option(G.OPT_TC_PRECISION, request.param[1])
+    ctx.set_option(G.OPT_STAGE2, request.param[2])
     yield ctx
     ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
     ctx.set_option(G.OPT_TC_PRECISION, G.PREC_FP16X3)
+    ctx.set_option(G.OPT_STAGE2, 0)
 
 
 def grams_oracle(w):
@@ -418,9 +423,10 @@ def test_launch_accounting(ctx):
 
 # ----------------------------------------------------------------------------- data-parallel slab path
 @pytest.mark.parametrize("slabs", [1, 2, 3, 8])
-@pytest.mark.parametrize("engine", [G.ENGINE_SPARSE, G.ENGINE_DENSE], ids=["sparse", "dense"])
+@pytest.mark.parametrize("engine,stage2", [(G.ENGINE_SPARSE, 0), (G.ENGINE_DENSE, 1), (G.ENGINE_DENSE, 2)],
+                         ids=["sparse", "dense", "dense-gather2"])
 @pytest.mark.parametrize("exchange", [0, 1], ids=["S-allgather", "u-reduce"])
-def test_slab_path_matches_oracle(ctx, slabs, engine, exchange):
+def test_slab_path_matches_oracle(ctx, slabs, engine, stage2, exchange):
     """GVT_OPT_SLABS runs stage 1 per X-row slab and stage 2 slab by slab (K split), the code
     path every rank runs in the data-parallel layout; GVT_OPT_EXCHANGE = 1 runs the u-exchange
     form (stage 2 of the slabs into a partial over every output, then the reduce, a copy at
@@ -428,6 +434,7 @@ def test_slab_path_matches_oracle(ctx, slabs, engine, exchange):
     ctx.set_option(G.OPT_ENGINE, engine)
     ctx.set_option(G.OPT_SLABS, slabs)
     ctx.set_option(G.OPT_EXCHANGE, exchange)
+    ctx.set_option(G.OPT_STAGE2, stage2)
     try:
         rng = np.random.default_rng(77)
         for kernel in K_ALL:
@@ -455,6 +462,7 @@ def test_slab_path_matches_oracle(ctx, slabs, engine, exchange):
     finally:
         ctx.set_option(G.OPT_SLABS, 1)
         ctx.set_option(G.OPT_EXCHANGE, 0)
+        ctx.set_option(G.OPT_STAGE2, 0)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
 
 

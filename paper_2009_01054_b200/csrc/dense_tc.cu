@@ -783,12 +783,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 // column halves exchange their maxima)
                 const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
                 float mx = 0.f;
+                // column scales of B in 16-byte loads (the scale vector is padded to 128 rows)
 #pragma unroll
-                for (int i = 0; i < 128; i++) {
-                    const int gc = gc_base + i;
-                    const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
-                    run[i] *= ra * rb;
-                    if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
+                for (int i4 = 0; i4 < 32; i4++) {
+                    const float4 rb4 = ep.sb ? __ldg(reinterpret_cast<const float4 *>(ep.sb + gc_base) + i4)
+                                            : make_float4(1.f, 1.f, 1.f, 1.f);
+                    const float rbv[4] = {rb4.x, rb4.y, rb4.z, rb4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int i = 4 * i4 + u, gc = gc_base + i;
+                        run[i] *= ra * (gc < N ? rbv[u] : 1.f);
+                        if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
+                    }
                 }
                 if (ep.l1max) {
                     mx = 32768.f * ra * __ldg(ep.l1max);
@@ -805,29 +811,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     e = 15 - ex;
                 }
                 const float s = ldexpf(1.f, e);
-                if (gr < M) {
-                    if (half == 0) {
-                        if (!ep.l1max) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
-                        else if (n_tile == 0) ep.c_sk[gr] = ldexpf(1.f, -e);
-                    }
-                    __half *hp = ep.c_h16 + (int64_t)gr * ep.ldc + gc_base;
-                    __half *lp = ep.c_l16 + (int64_t)gr * ep.ldc + gc_base;
+                if (gr < M && half == 0) {
+                    if (!ep.l1max) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+                    else if (n_tile == 0) ep.c_sk[gr] = ldexpf(1.f, -e);
+                }
+                // coalesced stores through this warp's staging block: each lane (one row) parks
+                // 32 columns of (hi, lo) pairs, then the warp writes the block row by row, 64
+                // contiguous bytes per piece (a thread-per-row store pattern would touch 32 lines
+                // per instruction; it dominated the epilogue of short-K tiles)
+                uint32_t *blk = reinterpret_cast<uint32_t *>(estage) + (half * 4 + quarter) * 32 * 33;
+                const int64_t row0 = (int64_t)m0 + quarter * 32;
 #pragma unroll
-                    for (int i = 0; i < 128; i += 2) {
-                        if (gc_base + i + 1 < N) {
-                            const float v0 = run[i] * s, v1 = run[i + 1] * s;
-                            const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-                            *reinterpret_cast<__half2 *>(hp + i) = __halves2half2(h0, h1);
-                            *reinterpret_cast<__half2 *>(lp + i) = __halves2half2(
-                                __float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
-                        } else if (gc_base + i < N) {
-                            const float v0 = run[i] * s;
-                            const __half h0 = __float2half_rn(v0);
-                            hp[i] = h0;
-                            lp[i] = __float2half_rn(v0 - __half2float(h0));
+                for (int c4 = 0; c4 < 4; c4++) {
+                    // packed conversions: hi = rn(v), lo = rn(v - hi) two columns at a time; the
+                    // row's block holds 16 hi pairs then 16 lo pairs
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float v0 = run[c4 * 32 + i] * s, v1 = run[c4 * 32 + i + 1] * s;
+                        const __half2 h = __float22half2_rn(make_float2(v0, v1));
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __float22half2_rn(make_float2(v0 - hf.x, v1 - hf.y));
+                        blk[lane * 33 + i / 2] = *reinterpret_cast<const uint32_t *>(&h);
+                        blk[lane * 33 + 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&l);
+                    }
+                    __syncwarp();
+                    // half2 stores: lanes 0-15 write row r, lanes 16-31 row r + 1, two columns each
+                    const int j = lane & 15;
+                    const int gc = gc_base + c4 * 32 + 2 * j;
+                    if (gc < N) {
+                        for (int r = lane >> 4; r < 32; r += 2) {
+                            if (row0 + r >= M) break;
+                            const uint32_t ph = blk[r * 33 + j], pl = blk[r * 33 + 16 + j];
+                            const int64_t o = (row0 + r) * ep.ldc + gc;
+                            if (gc + 1 < N) {
+                                *reinterpret_cast<uint32_t *>(ep.c_h16 + o) = ph;
+                                *reinterpret_cast<uint32_t *>(ep.c_l16 + o) = pl;
+                            } else {
+                                ep.c_h16[o] = __ushort_as_half((unsigned short)(ph & 0xffffu));
+                                ep.c_l16[o] = __ushort_as_half((unsigned short)(pl & 0xffffu));
+                            }
                         }
                     }
+                    __syncwarp();
                 }
+                // the next tile's scale exchange reuses the staging area
+                named_bar(1, 32 * N_EPI_WARPS);
                 continue;
             }
             if (ep.sa || ep.sb) {
@@ -863,26 +891,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     }
                 }
             } else if (EPI == EPI_GRAM) {
-                if (gr < M) {
-                    float *krow = ep.c_f + (int64_t)gr * ep.ldc;
-                    const float ni = ep.kind == GVT_BASE_GAUSSIAN ? ep.norms[gr] : 0.f;
+                // kernel values, then coalesced row stores through this warp's staging block
+                // (as in EPI_STORE16); the next tile's epilogue reuses the block after the barrier
+                const float ni = (ep.kind == GVT_BASE_GAUSSIAN && gr < M) ? ep.norms[gr] : 0.f;
+                float *blk = estage + (half * 4 + quarter) * 32 * 33;
+                const int64_t row0 = (int64_t)m0 + quarter * 32;
 #pragma unroll
-                    for (int i = 0; i < 128; i++) {
-                        const int gc = gc_base + i;
-                        if (gc < N) {
-                            float x = run[i];
-                            if (ep.kind == GVT_BASE_GAUSSIAN) {
-                                float d2 = fmaxf(ni + ep.norms_b[gc] - 2.f * x, 0.f);
-                                if (ep.same && gc == gr) d2 = 0.f;
-                                x = expf(-ep.gamma * d2);
-                            } else if (ep.kind == GVT_BASE_POLY) {
-                                float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
-                                for (int e = 0; e < ep.degree; e++) rr *= bb;
-                                x = rr;
-                            }
-                            krow[gc] = x;
+                for (int c4 = 0; c4 < 4; c4++) {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) {
+                        const int gc = gc_base + c4 * 32 + i;
+                        float x = run[c4 * 32 + i];
+                        if (ep.kind == GVT_BASE_GAUSSIAN) {
+                            float d2 = fmaxf(ni + (gc < N ? ep.norms_b[gc] : 0.f) - 2.f * x, 0.f);
+                            if (ep.same && gc == gr) d2 = 0.f;
+                            x = expf(-ep.gamma * d2);
+                        } else if (ep.kind == GVT_BASE_POLY) {
+                            float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
+                            for (int e = 0; e < ep.degree; e++) rr *= bb;
+                            x = rr;
+                        }
+                        blk[lane * 33 + i] = x;
+                    }
+                    __syncwarp();
+                    const int gc = gc_base + c4 * 32 + lane;
+                    if (gc < N) {
+                        for (int r = 0; r < 32; r++) {
+                            if (row0 + r >= M) break;
+                            ep.c_f[(row0 + r) * ep.ldc + gc] = blk[r * 33 + lane];
                         }
                     }
+                    __syncwarp();
                 }
             } else if (EPI == EPI_SAMPLED) {
                 const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;

@@ -144,6 +144,12 @@ __device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16])
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8_raw(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float tf32_round(float x) {
@@ -726,32 +732,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
                 const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
 #if DRAIN_X16
-                // 16-column TMEM loads: 16 fewer live registers than x32 next to run[128] (the
-                // epilogue is at the 168-register cap of 10 warps per CTA)
+                if (EPI == EPI_SAMPLED && sk) {  // (host side: chunk scales only with the sampled epilogue)
+                    // chunk-scaled B: 8-column TMEM loads and two 16-byte scale loads per step, so
+                    // the temporaries next to run[128] stay within the 168-register cap of 10 warps
+                    // (x16 loads plus four scale vectors spilled part of run[] in this kernel)
 #pragma unroll
-                for (int c8 = 0; c8 < 8; c8++) {
-                    uint32_t r[16];
-                    tmem_ld16_raw(ta + c8 * 16, r);
-                    tmem_wait_ld();
-                    if (sk) {
-#if SK_VEC4
-                        // 16-byte scale loads (sk is 16-byte aligned: 256-aligned base, 256-float chunk
-                        // rows, 128-column thread blocks)
-                        const float4 *sk4 = reinterpret_cast<const float4 *>(sk + c8 * 16);
+                    for (int c16 = 0; c16 < 16; c16++) {
+                        uint32_t r[8];
+                        tmem_ld8_raw(ta + c16 * 8, r);
+                        const float4 *sk4 = reinterpret_cast<const float4 *>(sk + c16 * 8);
+                        const float4 v0 = __ldg(sk4), v1 = __ldg(sk4 + 1);
+                        tmem_wait_ld();
+                        float *rr = run + c16 * 8;
+                        rr[0] = fmaf(__uint_as_float(r[0]), v0.x, rr[0]);
+                        rr[1] = fmaf(__uint_as_float(r[1]), v0.y, rr[1]);
+                        rr[2] = fmaf(__uint_as_float(r[2]), v0.z, rr[2]);
+                        rr[3] = fmaf(__uint_as_float(r[3]), v0.w, rr[3]);
+                        rr[4] = fmaf(__uint_as_float(r[4]), v1.x, rr[4]);
+                        rr[5] = fmaf(__uint_as_float(r[5]), v1.y, rr[5]);
+                        rr[6] = fmaf(__uint_as_float(r[6]), v1.z, rr[6]);
+                        rr[7] = fmaf(__uint_as_float(r[7]), v1.w, rr[7]);
+                    }
+                } else {
+                    // 16-column TMEM loads: 16 fewer live registers than x32 next to run[128]
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; q4++) {
-                            const float4 v = __ldg(sk4 + q4);
-                            run[c8 * 16 + 4 * q4 + 0] = fmaf(__uint_as_float(r[4 * q4 + 0]), v.x, run[c8 * 16 + 4 * q4 + 0]);
-                            run[c8 * 16 + 4 * q4 + 1] = fmaf(__uint_as_float(r[4 * q4 + 1]), v.y, run[c8 * 16 + 4 * q4 + 1]);
-                            run[c8 * 16 + 4 * q4 + 2] = fmaf(__uint_as_float(r[4 * q4 + 2]), v.z, run[c8 * 16 + 4 * q4 + 2]);
-                            run[c8 * 16 + 4 * q4 + 3] = fmaf(__uint_as_float(r[4 * q4 + 3]), v.w, run[c8 * 16 + 4 * q4 + 3]);
-                        }
-#else
-#pragma unroll
-                        for (int i = 0; i < 16; i++)
-                            run[c8 * 16 + i] = fmaf(__uint_as_float(r[i]), __ldg(sk + c8 * 16 + i), run[c8 * 16 + i]);
-#endif
-                    } else {
+                    for (int c8 = 0; c8 < 8; c8++) {
+                        uint32_t r[16];
+                        tmem_ld16_raw(ta + c8 * 16, r);
+                        tmem_wait_ld();
 #pragma unroll
                         for (int i = 0; i < 16; i++) run[c8 * 16 + i] += __uint_as_float(r[i]);
                     }
@@ -1000,7 +1008,8 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
     ep.sb = B.scale;
     ep.sbk = B.scale_k;
     ep.sbk_ld = B.scale_k_ld;
-    GVT_REQUIRE(!B.scale_k || (pair && PREC == PREC_F16), GVT_E_STATE, "chunk-scaled operand needs the CTA-pair fp16 GEMM");
+    GVT_REQUIRE(!B.scale_k || (pair && PREC == PREC_F16 && EPI == EPI_SAMPLED), GVT_E_STATE,
+                "a chunk-scaled operand needs the CTA-pair fp16 GEMM with the sampled epilogue");
     GVT_REQUIRE(EPI != EPI_STORE16 || (pair && PREC == PREC_F16), GVT_E_STATE, "fp16 store needs the CTA-pair fp16 GEMM");
     // function attributes are per device: one flag per device ordinal (one process may drive several)
     static bool attr[GVT_MAX_DEVICES] = {}, attr2[GVT_MAX_DEVICES] = {};

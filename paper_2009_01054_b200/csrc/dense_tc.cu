@@ -906,12 +906,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 const int64_t row0 = (int64_t)m0 + quarter * 32;
 #pragma unroll
                 for (int c4 = 0; c4 < 4; c4++) {
+                    // the 32 column norms of this block: one coalesced load, then shuffles (a load
+                    // per element left every thread waiting on L1/L2 latency 128 times per tile)
+                    const int gcl = gc_base + c4 * 32 + lane;
+                    const float nbl = (ep.kind == GVT_BASE_GAUSSIAN && gcl < N) ? ep.norms_b[gcl] : 0.f;
 #pragma unroll
                     for (int i = 0; i < 32; i++) {
                         const int gc = gc_base + c4 * 32 + i;
                         float x = run[c4 * 32 + i];
+                        const float nb = __shfl_sync(0xffffffffu, nbl, i);
                         if (ep.kind == GVT_BASE_GAUSSIAN) {
-                            float d2 = fmaxf(ni + (gc < N ? ep.norms_b[gc] : 0.f) - 2.f * x, 0.f);
+                            float d2 = fmaxf(ni + nb - 2.f * x, 0.f);
                             if (ep.same && gc == gr) d2 = 0.f;
                             x = expf(-ep.gamma * d2);
                         } else if (ep.kind == GVT_BASE_POLY) {

@@ -204,9 +204,6 @@ struct EpiParams {
     const float *l1max;
 };
 
-#ifndef SK_VEC4
-#define SK_VEC4 1
-#endif
 #ifndef DRAIN_X16
 #define DRAIN_X16 1
 #endif

@@ -83,6 +83,7 @@ def lib():
         L.oracle_explicit_rect_matvec.argtypes = [i32, P, i64, i64, P, i64, i64, P, P, i64, P, P, i64, P, P]
         L.oracle_gvt_rect.argtypes = [P, i64, i64, P, i64, i64, P, P, i64, P, P, i64, P, i32, P, P, P]
         L.oracle_sort_plan.argtypes = [P, P, i64, i64, i64, i32, P, P]
+        L.oracle_relabel.argtypes = [P, i64, i64, P, P, P]
         L.oracle_num_threads.restype = i32
         _lib = L
     return _lib
@@ -294,6 +295,18 @@ def gvt_rect(A, B, of, os_, inf, ins, a, variant=0):
                                  len(of), _p(inf), _p(ins), len(inf), _p(a), int(variant), _p(u), ctypes.byref(v),
                                  ctypes.byref(ops)), "gvt_rect")
     return u, v.value, ops.value
+
+
+def relabel(ids, bound):
+    """SPEC.md:49-57 relabel_compact over ids in [0, bound): (compact int32[n], unique int32[count],
+    count) with unique in first-occurrence order (O7b)."""
+    v = _i(ids)
+    n = len(v)
+    compact = np.empty(n, dtype=np.int32)
+    unique = np.empty(max(1, min(n, bound)), dtype=np.int32)
+    cnt = np.zeros(1, dtype=np.int64)
+    _check(lib().oracle_relabel(_p(v), n, bound, _p(compact), _p(unique), _p(cnt)), "relabel")
+    return compact, unique[:int(cnt[0])].copy(), int(cnt[0])
 
 
 def sort_plan(first, second, m, q, mode=0):

@@ -27,6 +27,8 @@
  *                             and == Roth's vec trick D*A*T^T on complete grids
  *   oracle_cg              -- == dense direct solve; c*I system; A-norm error monotone
  *   oracle_sort_plan       -- brute-force stable sort (numpy) on random inputs
+ *   oracle_relabel         -- SPEC.md:55-57 examples; numpy.unique first-occurrence indices;
+ *                             unique[compact] == ids; idempotent on compact input
  */
 #include <math.h>
 #include <stdint.h>
@@ -696,6 +698,34 @@ int oracle_gvt_rect(const double *A, int64_t m_out, int64_t m_in, const double *
     free(W);
     if (variant_used) *variant_used = v;
     if (op_count) *op_count = v == 1 ? c1 : c2;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ O7b compact relabel
+ * SPEC.md:49-57 relabel_compact (realizes Table 1's unique counts m, q, PAPER.md "the number
+ * of unique drugs in the first sample"): compact[i] in [0, count); unique[compact[i]] =
+ * ids[i]; unique in first-occurrence order; count = number of distinct values.  One pass
+ * in index order with a seen-table over the id domain [0, bound).  unique holds up to
+ * min(n, bound) entries. */
+int oracle_relabel(const int32_t *ids, int64_t n, int64_t bound, int32_t *compact, int32_t *unique,
+                   int64_t *count) {
+    if (n < 0 || bound < 0) return OR_E_DIM;
+    if (!check_ids(ids, n, bound)) return OR_E_INDEX;
+    int64_t *seen = (int64_t *)malloc(sizeof(int64_t) * (size_t)(bound > 0 ? bound : 1));
+    if (!seen) return OR_E_OOM;
+    for (int64_t v = 0; v < bound; v++) seen[v] = -1;
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t v = ids[i];
+        if (seen[v] < 0) {
+            seen[v] = c;
+            unique[c] = v;
+            c++;
+        }
+        compact[i] = (int32_t)seen[v];
+    }
+    *count = c;
+    free(seen);
     return OR_OK;
 }
 

@@ -741,3 +741,44 @@ def test_tanimoto_equals_scipy_jaccard_and_is_psd():
     assert np.linalg.eigvalsh(G).min() >= -1e-10 * np.abs(G).max()
     with pytest.raises(O.OracleError):
         O.gram(O.BASE_TANIMOTO, [[0.0, 0.5]])
+
+
+# ----------------------------------------------------------------------------- O7b compact relabel
+def test_relabel_spec_worked_values():
+    """SPEC.md:55-57 examples (golden file)."""
+    for case in SPEC["relabel_compact"]["cases"]:
+        bound = max(case["ids"]) + 1 if case["ids"] else 1
+        compact, unique, count = O.relabel(case["ids"], bound)
+        assert compact.tolist() == case["compact"]
+        assert unique.tolist() == case["unique"]
+        assert count == case["count"]
+
+
+def test_relabel_matches_numpy_first_occurrence_and_invariants():
+    """unique ids in first-occurrence order = numpy.unique's first indices sorted; compact ids
+    reproduce the input through unique (SPEC.md:52, 69); idempotent on compact input (SPEC.md:70);
+    out-of-range ids are an index error."""
+    rng = np.random.default_rng(17)
+    for trial in range(40):
+        bound = int(rng.integers(1, 300))
+        n = int(rng.integers(0, 2000))
+        ids = rng.integers(0, bound, n).astype(np.int32)
+        compact, unique, count = O.relabel(ids, bound)
+        vals, first = np.unique(ids, return_index=True)
+        order = np.argsort(first, kind="stable")
+        assert count == len(vals)
+        assert np.array_equal(unique, vals[order])
+        assert np.array_equal(unique[compact], ids)
+        assert compact.size == 0 or (compact.min() >= 0 and compact.max() < count)
+        c2, u2, k2 = O.relabel(compact, max(count, 1))
+        assert k2 == count and np.array_equal(c2, compact) and np.array_equal(u2, np.arange(count))
+    # brute force on tiny inputs: a dict in index order
+    for trial in range(200):
+        ids = rng.integers(0, 6, int(rng.integers(0, 9))).astype(np.int32)
+        seen = {}
+        for v in ids.tolist():
+            seen.setdefault(v, len(seen))
+        compact, unique, count = O.relabel(ids, 6)
+        assert compact.tolist() == [seen[v] for v in ids.tolist()] and unique.tolist() == list(seen)
+    with pytest.raises(Exception):
+        O.relabel(np.array([0, 3], np.int32), 3)

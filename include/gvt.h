@@ -317,6 +317,18 @@ gvt_status pairwise_predict_rect(gvt_ctx *ctx, const float *Dx, int64_t m_test, 
 gvt_status gvt_sort_plan(gvt_ctx *ctx, const int32_t *first, const int32_t *second, int64_t n,
                          int64_t m, int64_t q, int mode, int32_t *perm, int64_t *row_ptr);
 
+/* Compact relabeling of an id sequence (SPEC.md:49-57 relabel_compact; it realizes the "unique"
+ * counts m, q of PAPER.md Table 1 -- "the number of unique drugs in the first sample").
+ *   ids[n]      object ids in [0, bound) (int32)
+ *   compact[n]  out: compact[i] in [0, count), unique[compact[i]] == ids[i] (int32)
+ *   unique[]    out: the distinct ids in first-occurrence order; capacity min(n, bound) (int32)
+ *   count       out (host): the number of distinct ids
+ * Integer-only and bit-exact.  The engine itself indexes Grams by global ids and does not need
+ * it; callers who build compact Grams apply it first.  Pointers host or device.
+ * Errors: GVT_E_DIM (negative sizes, NULL outputs), GVT_E_INDEX (an id outside [0, bound)). */
+gvt_status gvt_relabel_compact(gvt_ctx *ctx, const int32_t *ids, int64_t n, int64_t bound, int32_t *compact,
+                               int32_t *unique, int64_t *count);
+
 /* Thread-local message describing the last non-OK status. */
 const char *gvt_last_error(void);
 

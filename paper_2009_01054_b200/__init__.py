@@ -94,6 +94,7 @@ _lib.pairwise_krr_fit.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, 
                                   ctypes.c_int, ctypes.c_double, _P, ctypes.POINTER(ctypes.c_int), _P]
 _lib.pairwise_predict.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, ctypes.c_int, _P]
 _lib.gvt_sort_plan.argtypes = [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int, _P, _P]
+_lib.gvt_relabel_compact.argtypes = [_P, _P, _I64, _I64, _P, _P, _P]
 _lib.pairwise_krr_fit_early_stopping.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _P, _P,
                                                  ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P,
                                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
@@ -113,7 +114,7 @@ EXPORTED = ["gvt_slab_bounds",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
             "pairwise_krr_fit_early_stopping", "gvt_auc", "gvt_gram_cross", "gvt_matvec_rect",
-            "pairwise_predict_rect", "gvt_comm_init_host"]
+            "pairwise_predict_rect", "gvt_comm_init_host", "gvt_relabel_compact"]
 
 
 def _check(code: int, where: str):
@@ -414,6 +415,16 @@ class Context:
                "pairwise_predict")
         return out
 
+    def relabel_compact(self, ids, bound: int):
+        """(compact ids, unique ids in first-occurrence order, count)."""
+        n = _n(ids)
+        compact = _empty_like_input(ids, n, "i32")
+        unique = _empty_like_input(ids, max(1, min(n, bound)), "i32")
+        cnt = ctypes.c_int64(0)
+        _check(_lib.gvt_relabel_compact(self._h, _ptr(ids, "i32", "ids"), n, bound, _ptr(compact, "i32", "compact"),
+                                        _ptr(unique, "i32", "unique"), ctypes.byref(cnt)), "gvt_relabel_compact")
+        return compact, unique[:cnt.value], cnt.value
+
     def sort_plan(self, first, second, m: int, q: int, mode: int = 0):
         n = _n(first)
         perm = _empty_like_input(first, n, "i32")
@@ -469,6 +480,10 @@ def gvt_matvec_rect(ctx: Context, Dx, Tx, out_first, out_second, in_first, in_se
 def pairwise_predict_rect(ctx: Context, Dx, Tx, test_first, test_second, train_first, train_second, a, terms,
                           out=None):
     return ctx.predict_rect(Dx, Tx, test_first, test_second, train_first, train_second, a, terms, out)
+
+
+def gvt_relabel_compact(ctx: Context, ids, bound):
+    return ctx.relabel_compact(ids, bound)
 
 
 def gvt_sort_plan(ctx: Context, first, second, m, q, mode=0):

@@ -381,4 +381,24 @@ gvt_status gvt_sort_plan(gvt_ctx *c, const int32_t *first, const int32_t *second
     GVT_API_END
 }
 
+gvt_status gvt_relabel_compact(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound, int32_t *compact,
+                               int32_t *unique, int64_t *count) {
+    GVT_API_BEGIN(c)
+    GVT_REQUIRE(n >= 0 && bound >= 0, GVT_E_DIM, "negative size");
+    GVT_REQUIRE(count && ((compact && unique) || n == 0), GVT_E_DIM, "NULL output");
+    const int32_t *d = n ? (const int32_t *)gvt::stage_in(c, "rel.ids", ids, sizeof(int32_t) * n) : nullptr;
+    if (n) GVT_REQUIRE(gvt::count_out_of_range(c, d, n, bound) == 0, GVT_E_INDEX, "id out of range [0, bound)");
+    const bool hc = n > 0 && !gvt::is_device_ptr(compact), hu = n > 0 && !gvt::is_device_ptr(unique);
+    int32_t *dc = hc ? gvt::wsT<int32_t>(c, "rel.compact", n) : compact;
+    const int32_t *du = nullptr;
+    const int64_t k = gvt::relabel_compact(c, d, n, bound, dc, &du);
+    if (k > 0)
+        GVT_CUDA_TRY(cudaMemcpyAsync(unique, du, sizeof(int32_t) * k, hu ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                     c->stream));
+    if (hc) GVT_CUDA_TRY(cudaMemcpyAsync(compact, dc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *count = k;
+    GVT_API_END
+}
+
 }  // extern "C"

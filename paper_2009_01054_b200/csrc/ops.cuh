@@ -85,6 +85,10 @@ void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32
 // samples from an out-sample: kind 0: (sel(rs, i), sel(cs, i)) for i < n; plus (x,x) for x < n_diag
 void build_sample_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32_t *s, int64_t n, int row_sel,
                        int col_sel, int64_t n_diag, int64_t nrow, SamplePlan &out);
+// SPEC.md:49-57 compact relabel: compact (device, n); *unique_out = device array whose first
+// `return value` entries are the distinct ids in first-occurrence order (workspace-owned)
+int64_t relabel_compact(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound, int32_t *compact,
+                        const int32_t **unique_out);
 void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int mode,
                      int32_t *perm, int64_t *row_ptr);
 // fit-level reordering: perm = pair indices stably sorted by (first, second); gathers / scatter

@@ -229,6 +229,71 @@ void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, 
     GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(m + 1, 256), 256, 0, rows, n, m, row_ptr);
 }
 
+// ----------------------------------------------------------------------------- compact relabel
+// SPEC.md:49-57 relabel_compact (the unique counts of PAPER.md Table 1): compact[i] = rank of
+// ids[i] among the distinct ids ordered by first occurrence.  Integer-only, bit-exact:
+//   first[v] = min { i : ids[i] = v }   (atomicMin: the minimum does not depend on the order)
+//   sort the domain values by first[v] (absent values carry REL_ABSENT and sort last)
+//   lut[unique[j]] = j;  compact[i] = lut[ids[i]]
+constexpr int32_t REL_ABSENT = 0x7f7f7f7f;  // the byte-memset fill; above every index (n < REL_ABSENT)
+
+__global__ void k_first_occ(const int32_t *__restrict__ ids, int64_t n, int32_t *__restrict__ first) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicMin(first + ids[i], (int32_t)i);
+}
+
+__global__ void k_first_keys(const int32_t *__restrict__ first, int64_t bound, uint32_t *__restrict__ keys,
+                             int32_t *__restrict__ vals, unsigned long long *__restrict__ count) {
+    unsigned long long cnt = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < bound; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = first[v];
+        keys[v] = (uint32_t)f;
+        vals[v] = (int32_t)v;
+        cnt += f != REL_ABSENT;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(count, cnt);  // an integer count: order-free
+}
+
+__global__ void k_rank_lut(const int32_t *__restrict__ unique, const unsigned long long *__restrict__ count,
+                           int32_t *__restrict__ lut) {
+    const int64_t c = (int64_t)*count;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < c; j += (int64_t)gridDim.x * blockDim.x)
+        lut[unique[j]] = (int32_t)j;
+}
+
+__global__ void k_apply_lut(const int32_t *__restrict__ ids, int64_t n, const int32_t *__restrict__ lut,
+                            int32_t *__restrict__ compact) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        compact[i] = lut[ids[i]];
+}
+
+// ids (device, in [0, bound)) -> compact (device, n), unique (device, the first `count` of a
+// bound-long sorted value array); returns count
+int64_t relabel_compact(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound, int32_t *compact,
+                        const int32_t **unique_out) {
+    *unique_out = nullptr;
+    if (n == 0 || bound == 0) return 0;
+    GVT_REQUIRE(n < (int64_t)REL_ABSENT && bound < (int64_t)INT32_MAX, GVT_E_DIM, "relabel: too many ids");
+    int32_t *first = wsT<int32_t>(c, "relabel.first", (size_t)bound);
+    uint32_t *k0 = wsT<uint32_t>(c, "relabel.k0", (size_t)bound), *k1 = wsT<uint32_t>(c, "relabel.k1", (size_t)bound);
+    int32_t *v0 = wsT<int32_t>(c, "relabel.v0", (size_t)bound), *v1 = wsT<int32_t>(c, "relabel.v1", (size_t)bound);
+    int32_t *lut = wsT<int32_t>(c, "relabel.lut", (size_t)bound);
+    unsigned long long *cnt = wsT<unsigned long long>(c, "relabel.count", 1);
+    GVT_CUDA_TRY(cudaMemsetAsync(first, 0x7f, sizeof(int32_t) * bound, c->stream));  // REL_ABSENT
+    GVT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream));
+    GVT_LAUNCH(c, K_PLAN_KEYS, k_first_occ, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, ids, n, first);
+    GVT_LAUNCH(c, K_PLAN_KEYS, k_first_keys, grid1d(bound, 256, 8 * c->sm_count * 8), 256, 0, first, bound, k0, v0, cnt);
+    radix_sort_pairs<uint32_t>(c, "relabel", k0, k1, v0, v1, bound, 31);  // present values have distinct keys
+    GVT_LAUNCH(c, K_PLAN_GATHER, k_rank_lut, grid1d(bound, 256, 8 * c->sm_count * 8), 256, 0, v1, cnt, lut);
+    GVT_LAUNCH(c, K_PLAN_GATHER, k_apply_lut, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, ids, n, lut, compact);
+    unsigned long long h = 0;
+    GVT_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *unique_out = v1;
+    return (int64_t)h;
+}
+
 // ----------------------------------------------------------------------------- fit-level reordering
 // perm = the pair indices stably sorted by (first, second): a fit runs in this order so that the
 // pair-matrix entries of the Kronecker group are read in vector order (sequential, not gathered)

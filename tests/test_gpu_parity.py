@@ -121,6 +121,29 @@ def test_sort_plan_bit_exact(ctx, mode):
     assert e.value.code == G.E_INDEX
 
 
+@pytest.mark.parametrize("host", [False, True], ids=["device", "host"])
+def test_relabel_compact_bit_exact(ctx, host):
+    """SPEC.md:49-57 relabel_compact on the GPU equals the oracle's (O7b) bit for bit: empty, one
+    id, ragged sizes, a Zipf-skewed id stream (C5-like degrees) and all-distinct ids; ids outside
+    [0, bound) are an index error."""
+    rng = np.random.default_rng(23)
+    cases = [(np.zeros(0, np.int32), 5), (np.array([3], np.int32), 4), (np.array([5, 5, 2, 5], np.int32), 6)]
+    for n, bound in [(1000, 37), (4097, 5000), (100_003, 20_000)]:
+        cases.append((rng.integers(0, bound, n).astype(np.int32), bound))
+    cases.append((((rng.zipf(1.1, 3_000_000) - 1) % 20_000).astype(np.int32), 20_000))
+    cases.append((rng.permutation(50_000).astype(np.int32), 50_000))
+    for ids, bound in cases:
+        x = ids if host else dev(ids)
+        compact, unique, count = ctx.relabel_compact(x, bound)
+        oc, ou, ok = O.relabel(ids, bound)
+        assert count == ok
+        assert np.array_equal(np.asarray(compact.cpu() if not host else compact), oc)
+        assert np.array_equal(np.asarray(unique.cpu() if not host else unique), ou)
+    with pytest.raises(G.GvtError) as e:
+        ctx.relabel_compact(dev(np.array([0, 7], np.int32)), 7)
+    assert e.value.code == G.E_INDEX
+
+
 # ----------------------------------------------------------------------------- matvec, tiny
 @pytest.mark.parametrize("kernel", K_ALL)
 def test_matvec_tiny_vs_explicit(engine_ctx, kernel):

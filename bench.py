@@ -356,12 +356,24 @@ def run_gpu(args, rank, world, local_rank):
     scores = torch.empty(nt_local, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    phase_events = []  # per timed step: (start, grams done, fit done, predict done) on the launch stream
+
+    def step(record=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+        if ev:
+            ev[0].record(stream)
         ctx.gram(w.base, Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=D)
         if T is not None:
             ctx.gram(w.base, Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=T)
+        if ev:
+            ev[1].record(stream)
         _, it, _, _ = ctx.fit(D, T, fD, sD, yD, terms, w.lam, w.iters, 0.0, out=a, want_history=False)
+        if ev:
+            ev[2].record(stream)
         ctx.predict(D, T, tfD, tsD, fD, sD, a, terms, out=scores)
+        if ev:
+            ev[3].record(stream)
+            phase_events.append(ev)
         return it
 
     def barrier():
@@ -379,7 +391,7 @@ def run_gpu(args, rank, world, local_rank):
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            iters = step()
+            iters = step(record=True)
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -391,6 +403,15 @@ def run_gpu(args, rank, world, local_rank):
         ms = float(t.item())
     ms_step = ms / args.steps
     pairs = float(iters) * w.n + w.n_test  # whole job
+    # SURVEY 8(d) breakdown (this rank, CUDA events between the phases of each timed step): Grams,
+    # fit (plan + iterations), predict (plan + stage 1 + stage 2)
+    ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])] for e in phase_events])
+    gram_ms, fit_ms, pred_ms = (float(v) for v in ph.mean(axis=0))
+    phases = {"gram_ms": gram_ms, "fit_ms": fit_ms, "predict_ms": pred_ms,
+              "fit_gpairs_per_s": float(iters) * w.n / (fit_ms * 1e-3) / 1e9,
+              "fit_cg_iters_per_s": float(iters) / (fit_ms * 1e-3),
+              "predict_gpairs_per_s": w.n_test / (pred_ms * 1e-3) / 1e9,
+              "note": "this rank's phase times; fit and predict include their plans (sorts, buckets)"}
     value = pairs / (ms_step * 1e-3) / 1e9
 
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
@@ -454,6 +475,7 @@ def run_gpu(args, rank, world, local_rank):
                        "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
                        "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"},
             "cg_iters_per_s": iters / (ms_step * 1e-3),
+            "phases": phases,
             "gpu_launches": int(st["launches"]),
             "kernel_ms": {k: round(v["ms"] / args.steps, 3) for k, v in st["kinds"].items()} if args.profile else None,
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}

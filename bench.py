@@ -239,7 +239,11 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n},
+            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
+                       "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
+                       "step": "bounded sample of the training matvec (the oracle's per-term GVT), timed on the "
+                               "host cores; the GPU arm's step is gram(D)+gram(T)+pairwise_krr_fit(iters)+"
+                               "pairwise_predict"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"fp64 oracle per-term GVT training matvec restricted to the outputs of {nt} "
                                        f"seeded targets per step, repeated for >= 1 s ({cnt // max(1, args.steps)} "

@@ -418,6 +418,26 @@ def run_gpu(args, rank, world, local_rank):
               "note": "this rank's phase times; fit and predict include their plans (sorts, buckets)"}
     value = pairs / (ms_step * 1e-3) / 1e9
 
+    # ---- standalone training matvec (Gpairs/s = n / t_matvec, median of 5 after 3
+    #      warm-ups; each call includes its plan), on the fitted weights, outside the timed step
+    matvec = None
+    if world == 1:
+        u = torch.empty(n_local, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            ctx.matvec(D, T, fD, sD, fD, sD, a, terms, out=u)
+        mv_ms = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.matvec(D, T, fD, sD, fD, sD, a, terms, out=u)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            mv_ms.append(e0.elapsed_time(e1))
+        t = float(np.median(mv_ms))
+        matvec = {"ms": t, "gpairs_per_s": w.n / (t * 1e-3) / 1e9, "runs": 5,
+                  "note": "gvt_matvec over the training pairs (out = in sample), plan included, median of 5"}
+        del u
+
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
     e2e = None
     if not args.no_e2e:
@@ -480,6 +500,7 @@ def run_gpu(args, rank, world, local_rank):
                        "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"},
             "cg_iters_per_s": iters / (ms_step * 1e-3),
             "phases": phases,
+            "matvec": matvec,
             "gpu_launches": int(st["launches"]),
             "kernel_ms": {k: round(v["ms"] / args.steps, 3) for k, v in st["kinds"].items()} if args.profile else None,
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}

@@ -96,7 +96,9 @@ typedef enum {
                                     3 = single-CTA whole-fit CG (Kronecker fits whose factors, S and
                                     vectors fit one SM's shared memory; auto picks it for those when
                                     an iteration is <= 4e6 FMAs)                                      */
-    GVT_OPT_DENSE_THRESHOLD = 1, /* pair-matrix density at or above which auto picks dense (default 0.02) */
+    GVT_OPT_DENSE_THRESHOLD = 1, /* auto engine: -1 (default) = by estimated time of the two engines
+                                    (B200 calibration; crossover ~1 % density at C5 object counts);
+                                    >= 0 = dense at or above this pair-matrix density             */
     GVT_OPT_PROFILE = 2,         /* 1 = record per-kernel CUDA-event times (gvt_get_stats)                */
     GVT_OPT_GRAM_ENGINE = 3,     /* 0 = auto (tensor cores when available), 1 = SIMT, 2 = tensor cores    */
     GVT_OPT_TC_PRECISION = 4,    /* tensor-core split: 0 = 3xFP16 with per-row power-of-two scaling

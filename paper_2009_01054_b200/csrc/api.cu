@@ -121,7 +121,7 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         c->engine = (int)v;
         break;
     case GVT_OPT_DENSE_THRESHOLD:
-        GVT_REQUIRE(v >= 0, GVT_E_PARAM, "threshold must be >= 0");
+        GVT_REQUIRE(v >= 0 || v == -1.0, GVT_E_PARAM, "threshold must be >= 0, or -1 for the time estimate");
         c->dense_threshold = v;
         break;
     case GVT_OPT_PROFILE: c->profile = v != 0; break;

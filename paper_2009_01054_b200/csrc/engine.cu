@@ -244,6 +244,36 @@ static Factor materialise(gvt_ctx *c, const char *name, int64_t rows, int64_t co
     return f;
 }
 
+// Engine choice by estimated time ("the dispatcher must choose by time"), from
+// B200 measurements (scripts/density_sweep.py, profiles/r01_density_sweep.jsonl):
+//  sparse: stage 1 at ~3.3e12 FMA/s (L2-bound, q_out FMA per entry), but no faster than its
+//          CTAs' serial entry loops allow (8 X rows per CTA, ~0.05 us per entry, 9 CTAs per SM);
+//          stage 2 gathers one S row per output at ~6.4 TB/s (S above L2) or ~12 TB/s
+//  dense:  two 3xFP16 GEMMs (256-padded) at ~1.3e15 executed flop/s plus ~20 us fixed each,
+//          the X build, and stage 2 as the cheaper of the sampled GEMM and the gather
+// At C5 object counts this puts the crossover near 1 % density; on small problems (C2) the
+// sparse engine's short grid keeps the tensor cores ahead.  GVT_OPT_DENSE_THRESHOLD >= 0
+// replaces the estimate by the plain density rule.
+static bool dense_pays(gvt_ctx *c, double nnz, double ns, int64_t m_out, int64_t q_out, int64_t m_in,
+                       int64_t q_in) {
+    if (c->dense_threshold >= 0.0) {
+        const double cells = (double)m_in * (double)q_in;
+        return cells > 0 && nnz / cells >= c->dense_threshold;
+    }
+    auto rup = [](int64_t v, int64_t a) { return (double)round_up(v > 0 ? v : 1, a); };
+    const double hblocks = std::max(1.0, rup(m_in, 32) / 8.0), ttiles = std::max(1.0, std::ceil(q_out / 512.0));
+    const double waves = std::ceil(hblocks * ttiles / (9.0 * c->sm_count));
+    const double s1 = std::max(nnz * (double)q_out / 3.3e6, nnz / hblocks * 0.05 * waves);
+    const double s_bytes = 4.0 * (double)q_out * (double)m_in;
+    const double g2 = ns * (double)m_in * 4.0 / (s_bytes > 64e6 ? 6.4e6 : 12e6);
+    const double sparse_us = 10.0 + s1 + g2;
+    const double gemm1 = 20.0 + 6.0 * rup(q_out, 256) * rup(m_in, 256) * rup(q_in, 64) / 1.3e9;
+    const double gemm2 = 20.0 + 6.0 * rup(m_out, 256) * rup(q_out, 256) * rup(m_in, 64) / 1.3e9;
+    const double gath2 = 4.0 + 8.0 * ns * (double)m_in / 6e6;
+    const double dense_us = 5.0 + (double)m_in * (double)q_in * 4.0 / 4e6 + gemm1 + std::min(gemm2, gath2);
+    return dense_us < sparse_us;
+}
+
 static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
     if (c->engine == 1) return 1;
     bool tc = tc_available(c);
@@ -253,9 +283,7 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
         return 1;  // materialised Ones/Identity factors of a generic term list stay on SIMT
     }
     if (!(g.A.split && g.C.split)) return 1;  // factors were not split for tensor cores
-    double cells = (double)g.m_in * (double)g.C.cols;
-    double density = cells > 0 ? (double)g.ent.nnz / cells : 0.0;
-    return (tc && density >= c->dense_threshold) ? 2 : 1;
+    return (tc && dense_pays(c, (double)g.ent.nnz, (double)g.smp.ns, g.A.n, g.q_out, g.m_in, g.C.cols)) ? 2 : 1;
 }
 
 // X-row slabs balanced by entry count (row_ptr over nrow rows), bounds multiples of 32 (TMA /
@@ -770,14 +798,16 @@ static void out_finish(gvt_ctx *c, OutArr &o) {
 }
 
 // does this plan need the tensor-core split of the factors (any dense group)?
-static bool needs_split(gvt_ctx *c, Form form, int64_t m, int64_t q, int64_t n_in) {
+static bool needs_split(gvt_ctx *c, Form form, const Problem &P) {
     if (!tc_available(c) || c->engine == 1) return false;
     if (form == FORM_LINEAR || form == FORM_RANKING || form == FORM_CARTESIAN) return false;
     if (c->engine == 2) return true;
-    double mult = (form == FORM_SYM || form == FORM_ANTI || form == FORM_MLPK) ? 2.0 : 1.0;  // entries per pair
-    double cells = (form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC) ? (double)m * (double)q
-                                                                                     : (double)m * (double)m;
-    return cells > 0 && mult * (double)n_in / cells >= c->dense_threshold;
+    const bool hom = !(form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC);
+    const double mult = (form == FORM_SYM || form == FORM_ANTI || form == FORM_MLPK) ? 2.0 : 1.0;  // entries per pair
+    const int64_t q_in = hom ? P.m : P.q, q_out = hom ? P.m_out : P.q_out;
+    const double ns = (double)(P.uex ? P.n_out_full : P.n_out) + (form == FORM_MLPK ? (double)P.m_out : 0.0);
+    // the estimate of the problem's main Kronecker group (the same one choose_engine makes per group)
+    return dense_pays(c, mult * (double)P.n_in, ns, P.m_out, q_out, P.m, q_in);
 }
 
 // out_is_in: the out sample is the caller's in sample (fit)
@@ -850,7 +880,7 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
         }
         P.n_out_full = P.out_offsets.back();
     }
-    bool split = needs_split(c, form, P.m, P.q, P.n_in);
+    bool split = needs_split(c, form, P);
     P.D = prepare_factor(c, "fD", D, P.m_out, P.m, split, P.rect);
     P.T = P.hom ? P.D : prepare_factor(c, "fT", T, P.q_out, P.q, split, P.rect);
 }

@@ -86,7 +86,7 @@ struct gvt_ctx {
 
     // options
     int engine = 0;  // 0 auto, 1 sparse, 2 dense, 3 single-CTA whole-fit solver (small Kronecker fits)
-    double dense_threshold = 0.02;
+    double dense_threshold = -1.0;  // < 0: engine by estimated time (dense_pays); >= 0: density rule
     int profile = 0;
     int gram_engine = 0;
     int tc_precision = 0;  // 0 = 3xFP16 with row scaling, 1 = 3xTF32

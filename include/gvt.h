@@ -128,11 +128,14 @@ typedef enum {
                                     K-blocks of each 256-row tile of the pair matrix when they are at
                                     least 15 % of the blocks (block-sparse X, e.g. MLPK on a union
                                     domain); 0 = always the full K loop                              */
-    GVT_OPT_STAGE2 = 13          /* stage 2 of the dense engine: 0 (default) = by estimated time (the
+    GVT_OPT_STAGE2 = 13,         /* stage 2 of the dense engine: 0 (default) = by estimated time (the
                                     sampled tensor-core GEMM, or the row gather u_i = <A[r_i,:],
                                     S[c_i,:]> over the tensor-core S when the contraction is short and
                                     the samples few, e.g. C2); 1 = always the sampled GEMM; 2 =
                                     always the gather                                                 */
+    GVT_OPT_COMPACT = 14         /* 1 (default): a fit whose training pairs use less than half of the
+                                    Grams' objects runs on the sub-Grams of the used objects (Table 1's
+                                    unique counts; the same a); 0 = always the full Grams        */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

@@ -45,6 +45,7 @@ OPT_CG_VARIANT = 10
 OPT_SORTED_FIT = 11
 OPT_KBLOCK_SKIP = 12
 OPT_STAGE2 = 13
+OPT_COMPACT = 14
 SOLVER_CG, SOLVER_MINRES = 0, 1
 HOMOGENEOUS_KERNELS = (SYMMETRIC, ANTISYMMETRIC, RANKING, MLPK)
 MAX_KINDS = 32

@@ -139,6 +139,9 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     case GVT_OPT_KBLOCK_SKIP:
         c->kblock_skip = v != 0;
         break;
+    case GVT_OPT_COMPACT:
+        c->compact = v != 0;
+        break;
     case GVT_OPT_STAGE2:
         GVT_REQUIRE(v == 0 || v == 1 || v == 2, GVT_E_PARAM, "stage 2 must be 0 (auto), 1 (sampled GEMM) or 2 (gather)");
         c->stage2 = (int)v;

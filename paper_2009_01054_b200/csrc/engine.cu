@@ -1226,9 +1226,93 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     return GVT_OK;
 }
 
+// Used-object compaction of a fit (GVT_OPT_COMPACT, default on).  PAPER.md Table 1 counts m, q
+// as the UNIQUE drugs / targets of the sample, and Theorem 1's O(qn + m n_bar) cost is in those
+// counts; with Grams over a larger object table (the kernel-filling experiment's subsets of 2967
+// objects) the GVT would otherwise run over every object.  When the training
+// sample uses less than half of the Gram's (drug x target) objects, the fit runs on the sub-Grams
+// of the used objects (ascending global id) with renumbered pair ids: the same operator on the
+// sample (a bijective relabeling; Identity and Ones factors are preserved), so the same a.
+// Early stopping compacts only when the validation ids are among the training objects, so its
+// a_best stays the plain fit's.  One GPU only (ranks would need a common object set).
+static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T, int64_t &q, const int32_t *&f,
+                        const int32_t *&s, int64_t n, const int32_t *&vf, const int32_t *&vs, int64_t n_val) {
+    if (!c->compact || c->world > 1 || n <= 0 || m <= 0) return false;
+    GVT_REQUIRE(f && s, GVT_E_DIM, "pair ids are NULL with n > 0");
+    GVT_REQUIRE(n_val <= 0 || (vf && vs), GVT_E_DIM, "validation pair ids are NULL with n_val > 0");
+    const bool hom = T == nullptr;
+    const int64_t qq = hom ? m : q;
+    const int32_t *fd = (const int32_t *)stage_in(c, "cmp.f_in", f, sizeof(int32_t) * n);
+    const int32_t *sd = (const int32_t *)stage_in(c, "cmp.s_in", s, sizeof(int32_t) * n);
+    const int32_t *vfd = n_val > 0 ? (const int32_t *)stage_in(c, "cmp.vf_in", vf, sizeof(int32_t) * n_val) : nullptr;
+    const int32_t *vsd = n_val > 0 ? (const int32_t *)stage_in(c, "cmp.vs_in", vs, sizeof(int32_t) * n_val) : nullptr;
+    // counters: [0, 1] out-of-range training ids (drug / target side), [2, 3] validation ids outside
+    // the training objects (or out of range); one read-back for all of them and the set sizes
+    unsigned long long *cnt = wsT<unsigned long long>(c, "cmp.cnt", 4);
+    GVT_CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
+    UsedSet ud, ut;
+    if (hom) {
+        const int32_t *arr[2] = {fd, sd};
+        const int64_t len[2] = {n, n};
+        ud = used_set_begin(c, "cmp.d", m, arr, len, 2, cnt);
+        ut = ud;
+    } else {
+        ud = used_set_begin(c, "cmp.d", m, &fd, &n, 1, cnt);
+        ut = used_set_begin(c, "cmp.t", q, &sd, &n, 1, cnt + 1);
+    }
+    if (n_val > 0) {
+        count_unused_async(c, ud, vfd, n_val, cnt + 2);
+        count_unused_async(c, ut, vsd, n_val, cnt + 3);
+    }
+    unsigned long long h_cnt[4];
+    int64_t h_k[2] = {0, 0};
+    GVT_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaMemcpyAsync(&h_k[0], ud.k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    if (!hom) GVT_CUDA_TRY(cudaMemcpyAsync(&h_k[1], ut.k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (h_cnt[0] || h_cnt[1])
+        throw Error{GVT_E_INDEX, std::to_string(h_cnt[0] + h_cnt[1]) + " pair id(s) out of range [0, " +
+                                     std::to_string(m) + ") / [0, " + std::to_string(qq) + ")"};
+    ud.k = h_k[0];
+    ut.k = hom ? h_k[0] : h_k[1];
+    if (hom) ut = ud;
+    if ((double)ud.k * (double)ut.k > 0.5 * (double)m * (double)qq) return false;
+    if (n_val > 0 && (h_cnt[2] || h_cnt[3])) return false;  // (out-of-range validation ids: the full path reports them)
+    const float *Dd = (const float *)stage_in(c, "cmp.D_in", D, sizeof(float) * m * m);
+    float *Dc = wsT<float>(c, "cmp.D", (size_t)(ud.k * ud.k));
+    sub_gram(c, Dd, m, ud, Dc);
+    float *Tc = nullptr;
+    if (!hom) {
+        const float *Td = (const float *)stage_in(c, "cmp.T_in", T, sizeof(float) * q * q);
+        Tc = wsT<float>(c, "cmp.T", (size_t)(ut.k * ut.k));
+        sub_gram(c, Td, q, ut, Tc);
+    }
+    int32_t *fc = wsT<int32_t>(c, "cmp.f", (size_t)n), *sc = wsT<int32_t>(c, "cmp.s", (size_t)n);
+    map_ids(c, ud, fd, n, fc);
+    map_ids(c, ut, sd, n, sc);
+    if (n_val > 0) {
+        int32_t *vfc = wsT<int32_t>(c, "cmp.vf", (size_t)n_val), *vsc = wsT<int32_t>(c, "cmp.vs", (size_t)n_val);
+        map_ids(c, ud, vfd, n_val, vfc);
+        map_ids(c, ut, vsd, n_val, vsc);
+        vf = vfc;
+        vs = vsc;
+    }
+    D = Dc;
+    m = ud.k;
+    T = Tc;
+    q = hom ? m : ut.k;
+    f = fc;
+    s = sc;
+    return true;
+}
+
 gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
                int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
                double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
+    {
+        const int32_t *nv = nullptr, *nv2 = nullptr;
+        if (max_iter > 0) compact_fit(c, D, m, T, q, f, s, n, nv, nv2, 0);
+    }
     // Sorted-order fit (GVT_OPT_SORTED_FIT, default on): the solve runs on the training pairs
     // stably sorted by (first, second) -- K' = Pi K Pi^T, y' = Pi y, a = Pi^T a', the same
     // iterates up to the summation order of the dot products -- so the Kronecker group's
@@ -1264,6 +1348,7 @@ gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float
                               int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
                               int patience, int max_iter, float *a_out, int *best_iter, double *best_auc,
                               int *iters_run, double *auc_hist) {
+    if (max_iter > 0) compact_fit(c, D, m, T, q, f, s, n, vf, vs, n_val);
     EsArgs es;
     es.vf = vf;
     es.vs = vs;

@@ -93,6 +93,22 @@ void sort_plan_debug(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, 
                      int32_t *perm, int64_t *row_ptr);
 // fit-level reordering: perm = pair indices stably sorted by (first, second); gathers / scatter
 void sort_pairs(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int32_t *perm);
+// objects used by a sample (Table 1's unique counts), numbered in ascending global id
+struct UsedSet {
+    int64_t m = 0;                  // object-table size
+    int64_t k = 0;                  // number of used objects (host; after the read-back)
+    const int64_t *k_dev = nullptr;  // the same, on the device
+    const int32_t *used = nullptr;  // [m] 0/1
+    const int32_t *pos = nullptr;   // [m] compact number of a used object
+    const int32_t *ids = nullptr;   // [m] global id of compact number i (ascending; first k valid)
+};
+// marks the ids of `arrays` (counting ids outside [0, m) into counters[0]); asynchronous
+UsedSet used_set_begin(gvt_ctx *c, const char *tag, int64_t m, const int32_t *const *arrays, const int64_t *lens,
+                       int narr, unsigned long long *counters);
+// counts the ids of a outside the set (or outside [0, m)) into *cnt; asynchronous
+void count_unused_async(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, unsigned long long *cnt);
+void map_ids(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, int32_t *out);
+void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &u, float *Gs);  // Gs = G[ids][ids], ld k
 void gather_i32(gvt_ctx *c, const int32_t *x, const int32_t *perm, int64_t n, int32_t *y);
 void gather_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);
 void scatter_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);  // y[perm[k]] = x[k]

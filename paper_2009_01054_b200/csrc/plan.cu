@@ -2,6 +2,7 @@
 // stable sorts of pair/entry lists (CUB radix sort, stable => ties keep index order),
 // CSR row pointers, sample ordering.  Everything here is integer work and bit-exact.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "ops.cuh"
 
@@ -292,6 +293,100 @@ int64_t relabel_compact(gvt_ctx *c, const int32_t *ids, int64_t n, int64_t bound
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *unique_out = v1;
     return (int64_t)h;
+}
+
+// ----------------------------------------------------------------------------- used-object compaction
+// The objects a sample uses (Table 1: m, q count UNIQUE drugs / targets of the sample),
+// numbered in ascending global id: used[v] = 1 marks, pos = exclusive prefix sum, ids[pos[v]] = v.
+// Everything is launched asynchronously; one read-back (used_set_finish) returns the count, the
+// out-of-range ids met while marking, and the ids of extra arrays outside the set.
+__global__ void k_mark_used(const int32_t *__restrict__ a, int64_t n, int64_t bound, int32_t *__restrict__ used,
+                            unsigned long long *__restrict__ oor) {
+    unsigned long long bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = a[i];
+        if (v < 0 || v >= bound) bad++;
+        else used[v] = 1;  // idempotent stores
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(oor, bad);
+}
+
+__global__ void k_used_list(const int32_t *__restrict__ used, const int32_t *__restrict__ pos, int64_t m,
+                            int32_t *__restrict__ ids, int64_t *__restrict__ k) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m; v += (int64_t)gridDim.x * blockDim.x) {
+        if (used[v]) ids[pos[v]] = (int32_t)v;
+        if (v == m - 1) *k = (int64_t)pos[v] + used[v];
+    }
+}
+
+__global__ void k_count_unused(const int32_t *__restrict__ a, int64_t n, int64_t bound,
+                               const int32_t *__restrict__ used, unsigned long long *__restrict__ cnt) {
+    unsigned long long k = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = a[i];
+        k += (v < 0 || v >= bound) ? 1ull : (unsigned long long)(used[v] == 0);
+    }
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if ((threadIdx.x & 31) == 0 && k) atomicAdd(cnt, k);
+}
+
+__global__ void k_map_ids(const int32_t *__restrict__ a, int64_t n, const int32_t *__restrict__ pos,
+                          int32_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = pos[a[i]];
+}
+
+// Gs[i][j] = G[ids[i]][ids[j]] (k x k, ld k): 32 x 8 threads, coalesced along j
+__global__ void k_sub_gram(const float *__restrict__ G, int64_t ld, const int32_t *__restrict__ ids, int64_t k,
+                           float *__restrict__ Gs) {
+    const int64_t i = (int64_t)blockIdx.y * 8 + threadIdx.y, j = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    for (int64_t ii = i; ii < k; ii += (int64_t)gridDim.y * 8)
+        if (j < k) Gs[ii * k + j] = G[(int64_t)ids[ii] * ld + ids[j]];
+}
+
+// counters: [0] out-of-range ids of the marked arrays, [1] ids of the tested array outside the set
+UsedSet used_set_begin(gvt_ctx *c, const char *tag, int64_t m, const int32_t *const *arrays, const int64_t *lens,
+                       int narr, unsigned long long *counters) {
+    UsedSet u;
+    if (m <= 0) return u;
+    std::string t(tag);
+    int32_t *used = wsT<int32_t>(c, (t + ".used").c_str(), (size_t)m);  // int32: the scan's type
+    int32_t *pos = wsT<int32_t>(c, (t + ".pos").c_str(), (size_t)m);
+    int32_t *ids = wsT<int32_t>(c, (t + ".ids").c_str(), (size_t)m);
+    int64_t *k = wsT<int64_t>(c, (t + ".k").c_str(), 1);
+    GVT_CUDA_TRY(cudaMemsetAsync(used, 0, sizeof(int32_t) * m, c->stream));
+    for (int a = 0; a < narr; a++)
+        if (lens[a] > 0)
+            GVT_LAUNCH(c, K_PLAN_KEYS, k_mark_used, grid1d(lens[a], 256, 8 * c->sm_count * 8), 256, 0, arrays[a],
+                       lens[a], m, used, counters);
+    size_t temp = 0;
+    GVT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, temp, used, pos, (int)m, c->stream));
+    void *tb = ws(c, (t + ".scantmp").c_str(), temp);
+    GVT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tb, temp, used, pos, (int)m, c->stream));
+    GVT_LAUNCH(c, K_PLAN_GATHER, k_used_list, grid1d(m, 256, 8 * c->sm_count * 8), 256, 0, used, pos, m, ids, k);
+    u.used = used;
+    u.pos = pos;
+    u.ids = ids;
+    u.k_dev = k;
+    u.m = m;
+    return u;
+}
+
+void count_unused_async(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, unsigned long long *cnt) {
+    if (n == 0 || u.m == 0) return;
+    GVT_LAUNCH(c, K_PLAN_KEYS, k_count_unused, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, a, n, u.m, u.used, cnt);
+}
+
+void map_ids(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, int32_t *out) {
+    if (n == 0) return;
+    GVT_LAUNCH(c, K_PLAN_GATHER, k_map_ids, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, a, n, u.pos, out);
+}
+
+void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &u, float *Gs) {
+    if (u.k == 0) return;
+    dim3 grid((unsigned)((u.k + 31) / 32), (unsigned)std::min<int64_t>((u.k + 7) / 8, 4096));
+    GVT_LAUNCH(c, K_PAD_COPY, k_sub_gram, grid, dim3(32, 8), 0, G, ld, u.ids, u.k, Gs);
 }
 
 // ----------------------------------------------------------------------------- fit-level reordering

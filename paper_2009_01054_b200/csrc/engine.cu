@@ -1246,6 +1246,13 @@ static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T
     const int32_t *sd = (const int32_t *)stage_in(c, "cmp.s_in", s, sizeof(int32_t) * n);
     const int32_t *vfd = n_val > 0 ? (const int32_t *)stage_in(c, "cmp.vf_in", vf, sizeof(int32_t) * n_val) : nullptr;
     const int32_t *vsd = n_val > 0 ? (const int32_t *)stage_in(c, "cmp.vs_in", vs, sizeof(int32_t) * n_val) : nullptr;
+    // from here on the callers' ids are the staged device copies (host ids are copied once)
+    f = fd;
+    s = sd;
+    if (n_val > 0) {
+        vf = vfd;
+        vs = vsd;
+    }
     // counters: [0, 1] out-of-range training ids (drug / target side), [2, 3] validation ids outside
     // the training objects (or out of range); one read-back for all of them and the set sizes
     unsigned long long *cnt = wsT<unsigned long long>(c, "cmp.cnt", 4);

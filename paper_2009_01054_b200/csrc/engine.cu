@@ -906,9 +906,94 @@ static void matvec_impl(gvt_ctx *c, const float *D, int64_t m, const float *T, i
     out_finish(c, uo);
 }
 
+// Used-object compaction of a matvec / predict (GVT_OPT_COMPACT; the fit's counterpart is
+// compact_fit): when the in- or out-sample uses less than half of the Grams' objects, the GVT runs
+// on the cross-Grams of the used objects, D[out objects][in objects] (and T likewise), through the
+// rectangular path -- whose Theorem 1 variant is then chosen by cost, as in the paper.  Kernels
+// with an Identity factor (Cartesian) keep the square path (reading N1: identity across two
+// object tables); anything invalid is left to the square path's own checks and errors.
+void matvec_rect(gvt_ctx *c, const float *Dx, int64_t m_out, int64_t m_in, const float *Tx, int64_t q_out,
+                 int64_t q_in, const int32_t *of, const int32_t *os, int64_t n_out, const int32_t *inf,
+                 const int32_t *ins, int64_t n_in, const float *a, const gvt_term *terms, int n_terms, int variant,
+                 float *u, int *variant_used, int64_t *op_count);
+
+static bool compact_matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of,
+                           const int32_t *os, int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in,
+                           const float *a, const gvt_term *terms, int n_terms, float *u) {
+    if (!c->compact || c->world > 1 || n_in <= 0 || n_out <= 0 || m <= 0 || !terms || n_terms < 1 || n_terms > 64)
+        return false;
+    if (!of || !os || !inf || !ins || !a || !u || !D) return false;
+    const bool hom = T == nullptr;
+    const Form form = recognize(terms, n_terms);
+    if (form == FORM_CARTESIAN || (form_homogeneous(form) && !hom)) return false;
+    for (int i = 0; i < n_terms; i++) {
+        const int kinds[2] = {terms[i].left, terms[i].right};
+        for (int k = 0; k < 2; k++)
+            if (kinds[k] < 0 || kinds[k] > 3 || kinds[k] == GVT_FACTOR_IDENTITY) return false;
+    }
+    const int64_t qq = hom ? m : q;
+    const int32_t *ofd = (const int32_t *)stage_in(c, "cmv.of", of, sizeof(int32_t) * n_out);
+    const int32_t *osd = (const int32_t *)stage_in(c, "cmv.os", os, sizeof(int32_t) * n_out);
+    const int32_t *ifd = (const int32_t *)stage_in(c, "cmv.if", inf, sizeof(int32_t) * n_in);
+    const int32_t *isd = (const int32_t *)stage_in(c, "cmv.is", ins, sizeof(int32_t) * n_in);
+    unsigned long long *cnt = wsT<unsigned long long>(c, "cmv.cnt", 4);
+    GVT_CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
+    UsedSet od, ot, id, it;  // out drugs, out targets, in drugs, in targets (hom: od == ot, id == it)
+    if (hom) {
+        const int32_t *ao[2] = {ofd, osd}, *ai[2] = {ifd, isd};
+        const int64_t lo[2] = {n_out, n_out}, li[2] = {n_in, n_in};
+        od = used_set_begin(c, "cmv.od", m, ao, lo, 2, cnt);
+        id = used_set_begin(c, "cmv.id", m, ai, li, 2, cnt + 1);
+    } else {
+        od = used_set_begin(c, "cmv.od", m, &ofd, &n_out, 1, cnt);
+        ot = used_set_begin(c, "cmv.ot", q, &osd, &n_out, 1, cnt + 1);
+        id = used_set_begin(c, "cmv.id", m, &ifd, &n_in, 1, cnt + 2);
+        it = used_set_begin(c, "cmv.it", q, &isd, &n_in, 1, cnt + 3);
+    }
+    unsigned long long h_cnt[4];
+    int64_t h_k[4] = {0, 0, 0, 0};
+    GVT_CUDA_TRY(cudaMemcpyAsync(h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, c->stream));
+    const int nsets = hom ? 2 : 4;
+    const UsedSet *uniq[4] = {&od, &id, &ot, &it};
+    for (int k = 0; k < nsets; k++)
+        GVT_CUDA_TRY(cudaMemcpyAsync(&h_k[k], uniq[k]->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (h_cnt[0] || h_cnt[1] || h_cnt[2] || h_cnt[3]) return false;  // the square path reports the index error
+    od.k = h_k[0];
+    id.k = h_k[1];
+    if (hom) {
+        ot = od;
+        it = id;
+    } else {
+        ot.k = h_k[2];
+        it.k = h_k[3];
+    }
+    const double full = (double)m * (double)qq;
+    if ((double)id.k * (double)it.k >= 0.5 * full && (double)od.k * (double)ot.k >= 0.5 * full) return false;
+    const float *Dd = (const float *)stage_in(c, "cmv.D_in", D, sizeof(float) * m * m);
+    float *Dx = wsT<float>(c, "cmv.D", (size_t)(od.k * id.k));
+    sub_gram(c, Dd, m, od, id, Dx);
+    float *Tx = nullptr;
+    if (!hom) {
+        const float *Td = (const float *)stage_in(c, "cmv.T_in", T, sizeof(float) * q * q);
+        Tx = wsT<float>(c, "cmv.T", (size_t)(ot.k * it.k));
+        sub_gram(c, Td, q, ot, it, Tx);
+    }
+    int32_t *ofc = wsT<int32_t>(c, "cmv.ofc", (size_t)n_out), *osc = wsT<int32_t>(c, "cmv.osc", (size_t)n_out);
+    int32_t *ifc = wsT<int32_t>(c, "cmv.ifc", (size_t)n_in), *isc = wsT<int32_t>(c, "cmv.isc", (size_t)n_in);
+    map_ids(c, od, ofd, n_out, ofc);
+    map_ids(c, ot, osd, n_out, osc);
+    map_ids(c, id, ifd, n_in, ifc);
+    map_ids(c, it, isd, n_in, isc);
+    matvec_rect(c, Dx, od.k, id.k, Tx, ot.k, it.k, ofc, osc, n_out, ifc, isc, n_in, a, terms, n_terms, 0, u, nullptr,
+                nullptr);
+    return true;
+}
+
 void matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of, const int32_t *os,
             int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in, const float *a,
             const gvt_term *terms, int n_terms, float *u) {
+    if (compact_matvec(c, D, m, T, q, of, os, n_out, inf, ins, n_in, a, terms, n_terms, u)) return;
     matvec_impl(c, D, m, T, q, of, os, n_out, inf, ins, n_in, a, terms, n_terms, u);
 }
 
@@ -1287,12 +1372,12 @@ static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T
     if (n_val > 0 && (h_cnt[2] || h_cnt[3])) return false;  // (out-of-range validation ids: the full path reports them)
     const float *Dd = (const float *)stage_in(c, "cmp.D_in", D, sizeof(float) * m * m);
     float *Dc = wsT<float>(c, "cmp.D", (size_t)(ud.k * ud.k));
-    sub_gram(c, Dd, m, ud, Dc);
+    sub_gram(c, Dd, m, ud, ud, Dc);
     float *Tc = nullptr;
     if (!hom) {
         const float *Td = (const float *)stage_in(c, "cmp.T_in", T, sizeof(float) * q * q);
         Tc = wsT<float>(c, "cmp.T", (size_t)(ut.k * ut.k));
-        sub_gram(c, Td, q, ut, Tc);
+        sub_gram(c, Td, q, ut, ut, Tc);
     }
     int32_t *fc = wsT<int32_t>(c, "cmp.f", (size_t)n), *sc = wsT<int32_t>(c, "cmp.s", (size_t)n);
     map_ids(c, ud, fd, n, fc);

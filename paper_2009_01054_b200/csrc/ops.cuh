@@ -108,7 +108,8 @@ UsedSet used_set_begin(gvt_ctx *c, const char *tag, int64_t m, const int32_t *co
 // counts the ids of a outside the set (or outside [0, m)) into *cnt; asynchronous
 void count_unused_async(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, unsigned long long *cnt);
 void map_ids(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, int32_t *out);
-void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &u, float *Gs);  // Gs = G[ids][ids], ld k
+void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &rows, const UsedSet &cols,
+              float *Gs);  // Gs = G[rows.ids][cols.ids], ld cols.k
 void gather_i32(gvt_ctx *c, const int32_t *x, const int32_t *perm, int64_t n, int32_t *y);
 void gather_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);
 void scatter_f32(gvt_ctx *c, const float *x, const int32_t *perm, int64_t n, float *y);  // y[perm[k]] = x[k]

@@ -337,12 +337,12 @@ __global__ void k_map_ids(const int32_t *__restrict__ a, int64_t n, const int32_
         out[i] = pos[a[i]];
 }
 
-// Gs[i][j] = G[ids[i]][ids[j]] (k x k, ld k): 32 x 8 threads, coalesced along j
-__global__ void k_sub_gram(const float *__restrict__ G, int64_t ld, const int32_t *__restrict__ ids, int64_t k,
-                           float *__restrict__ Gs) {
+// Gs[i][j] = G[rid[i]][cid[j]] (kr x kc, ld kc): 32 x 8 threads, coalesced along j
+__global__ void k_sub_gram(const float *__restrict__ G, int64_t ld, const int32_t *__restrict__ rid, int64_t kr,
+                           const int32_t *__restrict__ cid, int64_t kc, float *__restrict__ Gs) {
     const int64_t i = (int64_t)blockIdx.y * 8 + threadIdx.y, j = (int64_t)blockIdx.x * 32 + threadIdx.x;
-    for (int64_t ii = i; ii < k; ii += (int64_t)gridDim.y * 8)
-        if (j < k) Gs[ii * k + j] = G[(int64_t)ids[ii] * ld + ids[j]];
+    for (int64_t ii = i; ii < kr; ii += (int64_t)gridDim.y * 8)
+        if (j < kc) Gs[ii * kc + j] = G[(int64_t)rid[ii] * ld + cid[j]];
 }
 
 // counters: [0] out-of-range ids of the marked arrays, [1] ids of the tested array outside the set
@@ -383,10 +383,10 @@ void map_ids(gvt_ctx *c, const UsedSet &u, const int32_t *a, int64_t n, int32_t 
     GVT_LAUNCH(c, K_PLAN_GATHER, k_map_ids, grid1d(n, 256, 8 * c->sm_count * 8), 256, 0, a, n, u.pos, out);
 }
 
-void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &u, float *Gs) {
-    if (u.k == 0) return;
-    dim3 grid((unsigned)((u.k + 31) / 32), (unsigned)std::min<int64_t>((u.k + 7) / 8, 4096));
-    GVT_LAUNCH(c, K_PAD_COPY, k_sub_gram, grid, dim3(32, 8), 0, G, ld, u.ids, u.k, Gs);
+void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &rows, const UsedSet &cols, float *Gs) {
+    if (rows.k == 0 || cols.k == 0) return;
+    dim3 grid((unsigned)((cols.k + 31) / 32), (unsigned)std::min<int64_t>((rows.k + 7) / 8, 4096));
+    GVT_LAUNCH(c, K_PAD_COPY, k_sub_gram, grid, dim3(32, 8), 0, G, ld, rows.ids, rows.k, cols.ids, cols.k, Gs);
 }
 
 // ----------------------------------------------------------------------------- fit-level reordering

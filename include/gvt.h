@@ -134,8 +134,10 @@ typedef enum {
                                     the samples few, e.g. C2); 1 = always the sampled GEMM; 2 =
                                     always the gather                                                 */
     GVT_OPT_COMPACT = 14         /* 1 (default): a fit whose training pairs use less than half of the
-                                    Grams' objects runs on the sub-Grams of the used objects (Table 1's
-                                    unique counts; the same a); 0 = always the full Grams        */
+                                    Grams' objects runs on the sub-Grams of the used objects (PAPER.md
+                                    Table 1's unique counts; the same a); gvt_matvec / predict run on the
+                                    cross-Grams of the used out x in objects when either side uses less
+                                    than half (not for Identity-factor kernels); 0 = full Grams   */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

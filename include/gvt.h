@@ -137,7 +137,8 @@ typedef enum {
                                     Grams' objects runs on the sub-Grams of the used objects (PAPER.md
                                     Table 1's unique counts; the same a); gvt_matvec / predict run on the
                                     cross-Grams of the used out x in objects when either side uses less
-                                    than half (not for Identity-factor kernels); 0 = full Grams   */
+                                    than half (not for Identity-factor kernels); skipped for tables
+                                    of <= 2^20 Gram cells; 2 = also for small tables; 0 = off     */
 } gvt_option;
 
 /* Solvers for (K + lambda I) a = y.  CG: Hestenes-Stiefel (readings S12-S14).  MINRES: the

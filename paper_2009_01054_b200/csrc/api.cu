@@ -140,7 +140,8 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         c->kblock_skip = v != 0;
         break;
     case GVT_OPT_COMPACT:
-        c->compact = v != 0;
+        GVT_REQUIRE(v == 0 || v == 1 || v == 2, GVT_E_PARAM, "compact must be 0 (off), 1 (auto) or 2 (always)");
+        c->compact = (int)v;
         break;
     case GVT_OPT_STAGE2:
         GVT_REQUIRE(v == 0 || v == 1 || v == 2, GVT_E_PARAM, "stage 2 must be 0 (auto), 1 (sampled GEMM) or 2 (gather)");

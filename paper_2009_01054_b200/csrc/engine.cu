@@ -917,12 +917,20 @@ void matvec_rect(gvt_ctx *c, const float *Dx, int64_t m_out, int64_t m_in, const
                  const int32_t *ins, int64_t n_in, const float *a, const gvt_term *terms, int n_terms, int variant,
                  float *u, int *variant_used, int64_t *op_count);
 
+// GVT_OPT_COMPACT = 1 (auto) skips small tables (<= 2^20 Gram cells: C1, C2), which are latency-bound
+// either way and where the check itself (one read-back) would cost more than it saves; 2 = always
+constexpr double COMPACT_MIN_CELLS = 1048576.0;
+static bool compact_small_skip(gvt_ctx *c, int64_t m, int64_t qq) {
+    return c->compact == 1 && (double)m * (double)qq <= COMPACT_MIN_CELLS;
+}
+
 static bool compact_matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of,
                            const int32_t *os, int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in,
                            const float *a, const gvt_term *terms, int n_terms, float *u) {
     if (!c->compact || c->world > 1 || n_in <= 0 || n_out <= 0 || m <= 0 || !terms || n_terms < 1 || n_terms > 64)
         return false;
     if (!of || !os || !inf || !ins || !a || !u || !D) return false;
+    if (compact_small_skip(c, m, T ? q : m)) return false;
     const bool hom = T == nullptr;
     const Form form = recognize(terms, n_terms);
     if (form == FORM_CARTESIAN || (form_homogeneous(form) && !hom)) return false;
@@ -1323,6 +1331,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
 static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T, int64_t &q, const int32_t *&f,
                         const int32_t *&s, int64_t n, const int32_t *&vf, const int32_t *&vs, int64_t n_val) {
     if (!c->compact || c->world > 1 || n <= 0 || m <= 0) return false;
+    if (compact_small_skip(c, m, T ? q : m)) return false;
     GVT_REQUIRE(f && s, GVT_E_DIM, "pair ids are NULL with n > 0");
     GVT_REQUIRE(n_val <= 0 || (vf && vs), GVT_E_DIM, "validation pair ids are NULL with n_val > 0");
     const bool hom = T == nullptr;

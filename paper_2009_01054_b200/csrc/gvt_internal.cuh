@@ -98,7 +98,7 @@ struct gvt_ctx {
     int sorted_fit = 1;    // fits run on the pairs sorted by (first, second)
     int kblock_skip = 1;   // block-sparse stage 1 (skip all-zero K-blocks of X) where it pays
     int stage2 = 0;        // dense-engine stage 2: 0 = by estimated time, 1 = sampled GEMM, 2 = gather
-    int compact = 1;       // fits on the sub-Grams of the used objects when they are < 1/2 of the table
+    int compact = 1;       // used-object compaction: 0 off, 1 auto (tables > 2^20 cells), 2 always
     int cg_variant = 0;    // 0 = Hestenes-Stiefel CG, 1 = Chronopoulos-Gear (one reduction per iteration)
     cudaStream_t cap_stream = nullptr;  // side stream used only for graph capture
     int last_engine = 0;

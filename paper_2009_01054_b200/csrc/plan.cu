@@ -306,7 +306,7 @@ __global__ void k_mark_used(const int32_t *__restrict__ a, int64_t n, int64_t bo
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = a[i];
         if (v < 0 || v >= bound) bad++;
-        else used[v] = 1;  // idempotent stores
+        else if (!used[v]) used[v] = 1;  // read first: popular ids (Zipf) would serialise on stores
     }
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(oor, bad);

@@ -192,3 +192,27 @@ def test_compacted_matvec_and_predict_match_oracle(ctx, kernel, engine):
     finally:
         ctx.set_option(G.OPT_COMPACT, 1)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("exchange", [0, 1], ids=["S-allgather", "u-reduce"])
+@pytest.mark.parametrize("kernel", [G.KRONECKER, G.MLPK, G.POLY2D])
+def test_compaction_with_emulated_slabs(ctx, kernel, exchange):
+    """Compaction composes with the data-parallel slab decomposition (3 emulated slabs, both
+    exchanges): the slabs are cut over the compacted object numbering."""
+    D, T, f, s, y = subset_problem(kernel, 500 + kernel)
+    terms = G.gvt_kernel_terms(kernel)
+    ao, _, _, _ = O.cg(O.kernel_terms(kernel), D.astype(np.float64), None if T is None else T.astype(np.float64),
+                       f, s, y, 1.0, 25)
+    ctx.set_option(G.OPT_COMPACT, 0)
+    e0 = rel(ctx.fit(dev(D), None if T is None else dev(T), dev(f), dev(s), dev(y), terms, 1.0, 25)[0].cpu().numpy(),
+             ao)
+    ctx.set_option(G.OPT_COMPACT, 2)
+    ctx.set_option(G.OPT_SLABS, 3)
+    ctx.set_option(G.OPT_EXCHANGE, exchange)
+    try:
+        a, it, _, _ = ctx.fit(dev(D), None if T is None else dev(T), dev(f), dev(s), dev(y), terms, 1.0, 25)
+        assert it == 25 and rel(a.cpu().numpy(), ao) <= max(1e-4, 3.0 * e0)
+    finally:
+        ctx.set_option(G.OPT_SLABS, 1)
+        ctx.set_option(G.OPT_EXCHANGE, 0)
+        ctx.set_option(G.OPT_COMPACT, 1)

@@ -1,3 +1,5 @@
+"""Gram GEMM throughput at C5 size: 20 000 x 20 000 Gaussian and linear Grams of dim-128 features
+(CUDA events, mean of 5 after 2 warm-ups).  usage: python scripts/gram_probe.py"""
 import sys, os, torch, numpy as np, json
 sys.path.insert(0, os.getcwd())
 import paper_2009_01054_b200 as G

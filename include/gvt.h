@@ -92,7 +92,8 @@ typedef struct gvt_ctx gvt_ctx;
 
 /* Options (gvt_set_option). */
 typedef enum {
-    GVT_OPT_ENGINE = 0,          /* 0 = auto by density (default), 1 = sparse SIMT, 2 = dense tensor-core,
+    GVT_OPT_ENGINE = 0,          /* 0 = auto (default; by estimated time, GVT_OPT_DENSE_THRESHOLD),
+                                    1 = sparse SIMT, 2 = dense tensor-core,
                                     3 = single-CTA whole-fit CG (Kronecker fits whose factors, S and
                                     vectors fit one SM's shared memory; auto picks it for those when
                                     an iteration is <= 4e6 FMAs)                                      */

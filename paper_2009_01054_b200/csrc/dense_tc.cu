@@ -978,6 +978,16 @@ static void get_encode() {
     g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
 }
 
+static CUtensorMapL2promotion l2promo() {  // A/B knob (experiment): GVT_L2PROMO 0 none, 1 64B, 2 128B, 3 256B
+    static const int v = [] {
+        const char *e = getenv("GVT_L2PROMO");
+        return e ? atoi(e) : 3;
+    }();
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                           : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // rows x cols (cols = K, contiguous) matrix, element size esz, leading dimension ld elements;
 // box = one 128-byte K-block x box_rows
 static CUtensorMap make_map(const void *p, int esz, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
@@ -991,7 +1001,7 @@ static CUtensorMap make_map(const void *p, int esz, int64_t rows, int64_t cols, 
                           const_cast<void *>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           KB_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                           : (KB_BYTES == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          l2promo(),
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     GVT_REQUIRE(r == CUDA_SUCCESS, GVT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;

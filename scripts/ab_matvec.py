@@ -58,6 +58,8 @@ def main():
                 env["GVT_GROUP_M"] = kv["gm"]
             if "rs" in kv:  # fp16 S with per-row bound scales (1) or per-(row, 256-col tile) scales (0)
                 env["GVT_S16_ROWSCALE"] = kv["rs"]
+            if "l2" in kv:  # TMA L2 promotion of the GEMM operand maps (0 none, 1 64B, 2 128B, 3 256B)
+                env["GVT_L2PROMO"] = kv["l2"]
             out = subprocess.run([sys.executable, "-c", CHILD, spec], env=env, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-1500:]
             print(f"round {r} [{spec}]: {line}", flush=True)

@@ -9,7 +9,7 @@ factors (1.6 GB each) are far above the 126 MB L2:
   n_train uniform pairs (default 8e5 = 0.2 % of the grid), n_test uniform test pairs (2e6);
   a ~ N(0, 1).  Seeded (synth.gather_regime, PCG64 seed 7).
 
-The auto engine picks the sparse path at this density (density threshold 2 %).  Times, with the
+The auto engine picks the sparse path at this density (by its time estimate).  Times, with the
 library's per-kernel CUDA events: the training matvec (stage 1 + gather over n_train outputs) and
 the prediction (stage 1 + gather over n_test outputs).  Reports the gather's achieved bandwidth
 against its algorithmic bytes (8 * m_in per output: one A row + one S row, fp32) and the measured

@@ -901,27 +901,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 const float ni = (ep.kind == GVT_BASE_GAUSSIAN && gr < M) ? ep.norms[gr] : 0.f;
                 float *blk = estage + (half * 4 + quarter) * 32 * 33;
                 const int64_t row0 = (int64_t)m0 + quarter * 32;
+                // kernel parameters in registers once per tile, one loop per base kernel (the
+                // per-element re-reads of the parameter bank were 42 % of this epilogue's stalls)
+                const int kind = ep.kind, degree = ep.degree, same = ep.same;
+                const float gamma = ep.gamma, coef0 = ep.coef0;
 #pragma unroll
                 for (int c4 = 0; c4 < 4; c4++) {
-                    // the 32 column norms of this block: one coalesced load, then shuffles (a load
-                    // per element left every thread waiting on L1/L2 latency 128 times per tile)
-                    const int gcl = gc_base + c4 * 32 + lane;
-                    const float nbl = (ep.kind == GVT_BASE_GAUSSIAN && gcl < N) ? ep.norms_b[gcl] : 0.f;
+                    float *row = blk + lane * 33;
+                    if (kind == GVT_BASE_GAUSSIAN) {
+                        // the 32 column norms of this block: one coalesced load, then shuffles
+                        const int gcl = gc_base + c4 * 32 + lane;
+                        const float nbl = gcl < N ? ep.norms_b[gcl] : 0.f;
+                        const float ng = -gamma;
 #pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const int gc = gc_base + c4 * 32 + i;
-                        float x = run[c4 * 32 + i];
-                        const float nb = __shfl_sync(0xffffffffu, nbl, i);
-                        if (ep.kind == GVT_BASE_GAUSSIAN) {
-                            float d2 = fmaxf(ni + nb - 2.f * x, 0.f);
-                            if (ep.same && gc == gr) d2 = 0.f;
-                            x = expf(-ep.gamma * d2);
-                        } else if (ep.kind == GVT_BASE_POLY) {
-                            float bb = fmaf(ep.gamma, x, ep.coef0), rr = 1.f;
-                            for (int e = 0; e < ep.degree; e++) rr *= bb;
-                            x = rr;
+                        for (int i = 0; i < 32; i++) {
+                            const float nb = __shfl_sync(0xffffffffu, nbl, i);
+                            float d2 = fmaxf(ni + nb - 2.f * run[c4 * 32 + i], 0.f);
+                            if (same && gc_base + c4 * 32 + i == gr) d2 = 0.f;
+                            row[i] = expf(ng * d2);
                         }
-                        blk[lane * 33 + i] = x;
+                    } else if (kind == GVT_BASE_POLY) {
+#pragma unroll
+                        for (int i = 0; i < 32; i++) {
+                            const float bb = fmaf(gamma, run[c4 * 32 + i], coef0);
+                            float rr = 1.f;
+                            for (int e = 0; e < degree; e++) rr *= bb;
+                            row[i] = rr;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; i++) row[i] = run[c4 * 32 + i];
                     }
                     __syncwarp();
                     const int gc = gc_base + c4 * 32 + lane;

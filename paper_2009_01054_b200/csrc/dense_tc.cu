@@ -52,14 +52,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait's suspend-time hint: a waiting thread may sleep up to this long (it resumes when the
+// phase completes) instead of re-polling (experiment: GVT energy under the power cap)
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(MBAR_SUSPEND_NS)
         : "memory");
 }
 

@@ -100,3 +100,6 @@ def test_bench_json_contract_on_c1():
     for leg in ("matvec", "predict"):
         assert g[leg]["engine"] == "sparse" and g[leg]["stage2_gather_ms"] > 0
         assert 0 < g[leg]["gather_frac_hbm"] < 2.0
+    # SURVEY 8(d) breakdown fields: per-phase times and the standalone training matvec
+    assert d["phases"]["fit_ms"] > 0 and d["phases"]["predict_ms"] > 0 and d["phases"]["gram_ms"] >= 0
+    assert d["matvec"]["gpairs_per_s"] > 0 and d["matvec"]["runs"] == 5

@@ -456,12 +456,66 @@ def test_cg_matches_dense_direct_solve_on_C1():
 
 
 def test_cg_breakdown_on_indefinite_operator():
-    """A negative lambda makes K + lambda I indefinite: p.Ap <= 0 must be reported."""
+    """The p.Ap <= 0 exit (oracle.c O5) reached with lambda >= 0: an indefinite
+    "Gram" D = diag(a, -1), T = [[1]], training pairs (0,0) and (1,0), so K = diag(a, -1) exactly.
+    Arithmetic fixes where CG breaks down:
+      y = (1, 1), a = 1:   p_1.Ap_1 = 1 - 1 = 0            -> breakdown at k = 1, x = 0;
+      y = (1, 2), a = 1:   p_1.Ap_1 = 1 - 4 = -3           -> breakdown at k = 1, x = 0;
+      y = (1, 1/2), a = 2: p_1.Ap_1 = 2 - 1/4 = 7/4 > 0, alpha = (5/4)/(7/4) = 5/7, x_1 = (5/7) y,
+                           r_1 = y - (5/7) K y = (-3/7, 6/7), beta = (45/49)/(5/4) = 36/49,
+                           p_2 = r_1 + beta y = (15/49, 60/49), p_2.Ap_2 = 2 (15/49)^2 - (60/49)^2 < 0
+                           -> breakdown at k = 2 with the iterate x_1 returned, iters = 1.
+    A negative lambda is a parameter error (OR_E_PARAM), not a breakdown."""
+    kron = O.kernel_terms(O.KRONECKER)
     f, s = [0, 1], [0, 0]
-    x, it, _, rc = O.cg(O.kernel_terms(O.KRONECKER), np.eye(2), np.eye(1), f, s, [1.0, 0.0], 0.0, 3)
-    assert rc == O.OK
-    with pytest.raises(O.OracleError):
-        O.cg(O.kernel_terms(O.KRONECKER), np.eye(2), np.eye(1), f, s, [1.0, 0.0], -1.0, 3)
+    T = np.eye(1)
+    for y in ([1.0, 1.0], [1.0, 2.0]):
+        x, it, hist, rc = O.cg(kron, np.diag([1.0, -1.0]), T, f, s, y, 0.0, 5)
+        assert rc == O.E_BREAKDOWN and it == 0 and np.all(x == 0), y
+    x, it, hist, rc = O.cg(kron, np.diag([2.0, -1.0]), T, f, s, [1.0, 0.5], 0.0, 5)
+    assert rc == O.E_BREAKDOWN and it == 1
+    assert np.allclose(x, [5.0 / 7.0, 5.0 / 14.0], rtol=0, atol=1e-15)
+    assert hist[1] == pytest.approx(np.hypot(3.0 / 7.0, 6.0 / 7.0) / np.hypot(1.0, 0.5), rel=1e-14)
+    # the same system with a positive shift that makes it SPD (lambda = 2: diag(4, 1)) converges
+    x, it, _, rc = O.cg(kron, np.diag([2.0, -1.0]), T, f, s, [1.0, 0.5], 2.0, 5)
+    assert rc == O.OK and np.allclose(x, [0.25, 0.5], atol=1e-15)
+    with pytest.raises(O.OracleError) as e:
+        O.cg(kron, np.eye(2), T, f, s, [1.0, 0.0], -1.0, 3)
+    assert e.value.code == O.E_PARAM
+
+
+def test_cg_residual_mode_matches_scipy_cg():
+    """Residual-mode stopping (reading S14: stop after iteration k when the recursive residual
+    ||r_k|| / ||y|| <= tol) against scipy.sparse.linalg.cg(rtol=tol, x0=0) on C1's explicit system
+    (K + lambda I): the same Hestenes-Stiefel recurrences with the same recursive residual test, so
+    the iteration counts (SciPy's callback count) and the returned weights agree.  The 2I system
+    stops after one iteration with an exactly zero residual."""
+    from scipy.sparse.linalg import cg as scipy_cg
+    w = synth.config1()
+    D = O.gram(O.BASE_GAUSSIAN, w.Xd, gamma=w.gamma)
+    T = O.gram(O.BASE_GAUSSIAN, w.Xt, gamma=w.gamma)
+    f, s = w.train_first, w.train_second
+    A = O.explicit_matrix(O.KRONECKER, D, T, f, s, f, s) + w.lam * np.eye(w.n)
+    y = w.y.astype(np.float64)
+    kron = O.kernel_terms(O.KRONECKER)
+    lam_min = np.linalg.eigvalsh(A)[0]
+    for tol in (1e-2, 1e-4, 1e-7):
+        calls = []
+        xs, info = scipy_cg(A, y, x0=np.zeros(w.n), rtol=tol, atol=0.0, maxiter=200, callback=calls.append)
+        assert info == 0
+        x, it, hist, rc = O.cg(kron, D, T, f, s, y, w.lam, 200, rel_tol=tol)
+        assert rc == O.OK and it == len(calls), (tol, it, len(calls))
+        assert hist[-1] <= tol < hist[-2]
+        # the true residuals at exit are within the tolerance up to fp64 drift of the recursion,
+        # and the two exits are within ||A^-1|| (||r|| + ||r_scipy||) of each other
+        res, res_s = np.linalg.norm(y - A @ x), np.linalg.norm(y - A @ xs)
+        assert res / np.linalg.norm(y) <= tol * (1 + 1e-6)
+        assert np.linalg.norm(x - xs) <= (res + res_s) / lam_min * (1 + 1e-9)
+    # 2I: one iteration, zero residual, a = y / 2
+    fg, sg = np.repeat(np.arange(3), 2), np.tile(np.arange(2), 3)
+    yg = np.array([1.0, -2.0, 0.5, 4.0, 3.0, -1.0])
+    x, it, hist, rc = O.cg(kron, np.eye(3), np.eye(2), fg, sg, yg, 1.0, 10, rel_tol=1e-12)
+    assert rc == O.OK and it == 1 and hist[-1] == 0.0 and np.allclose(x, yg / 2, atol=1e-15)
 
 
 def test_predict_spec_example():

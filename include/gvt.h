@@ -338,6 +338,16 @@ gvt_status gvt_sort_plan(gvt_ctx *ctx, const int32_t *first, const int32_t *seco
 gvt_status gvt_relabel_compact(gvt_ctx *ctx, const int32_t *ids, int64_t n, int64_t bound, int32_t *compact,
                                int32_t *unique, int64_t *count);
 
+/* Solver inspection for the in-loop parity check of reading S30 ("dump p_k at
+ * k in {1, K/2, K} and check K p_k against the oracle"): copies the search direction left by the
+ * last pairwise_krr_fit on this context -- after k Hestenes-Stiefel CG iterations that is
+ * p_{k+1} = r_k + beta_k p_k (PAPER.md:316-320 solved by CG, reading S12), the vector the next
+ * matvec would be applied to -- into p_out[n] (host or device), in the caller's pair order, this
+ * rank's shard.  n must equal the fit's local pair count.  Errors: GVT_E_STATE if the last fit
+ * kept no direction (MINRES, Chronopoulos-Gear CG, early stopping, the single-CTA engine, or no fit
+ * yet); GVT_E_DIM for a different n. */
+gvt_status gvt_solver_direction(gvt_ctx *ctx, float *p_out, int64_t n);
+
 /* Thread-local message describing the last non-OK status. */
 const char *gvt_last_error(void);
 

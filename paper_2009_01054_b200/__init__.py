@@ -110,7 +110,9 @@ _lib.gvt_matvec_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I6
 _lib.pairwise_predict_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P,
                                        ctypes.c_int, _P]
 
-EXPORTED = ["gvt_slab_bounds",
+_lib.gvt_solver_direction.argtypes = [_P, _P, _I64]
+
+EXPORTED = ["gvt_slab_bounds", "gvt_solver_direction",
             "gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
@@ -374,6 +376,12 @@ class Context:
         h = hist[: iters.value + 1] if hist is not None else None
         return out, iters.value, h, code
 
+    def solver_direction(self, n: int, like=None):
+        """gvt_solver_direction: the last CG fit's next search direction p_{k+1} (caller order)."""
+        out = _empty_like_input(like, n) if like is not None else np.empty(n, np.float32)
+        _check(_lib.gvt_solver_direction(self._h, _ptr(out, "f32", "p_out"), n), "gvt_solver_direction")
+        return out
+
     def fit_early_stopping(self, D, T, first, second, y, val_first, val_second, val_labels, terms, lam: float,
                            patience: int, max_iter: int, out=None):
         """pairwise_krr_fit_early_stopping: returns (a_best, best_iter, best_auc, iters_run, auc_hist)."""
@@ -485,6 +493,10 @@ def pairwise_predict_rect(ctx: Context, Dx, Tx, test_first, test_second, train_f
 
 def gvt_relabel_compact(ctx: Context, ids, bound):
     return ctx.relabel_compact(ids, bound)
+
+
+def gvt_solver_direction(ctx: Context, n, like=None):
+    return ctx.solver_direction(n, like)
 
 
 def gvt_sort_plan(ctx: Context, first, second, m, q, mode=0):

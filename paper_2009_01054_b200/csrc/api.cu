@@ -32,6 +32,7 @@ gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float
                               int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
                               int patience, int max_iter, float *a_out, int *best_iter, double *best_auc,
                               int *iters_run, double *auc_hist);
+void solver_direction(gvt_ctx *c, float *out, int64_t n);
 }  // namespace gvt
 
 using gvt::Error;
@@ -402,6 +403,13 @@ gvt_status gvt_relabel_compact(gvt_ctx *c, const int32_t *ids, int64_t n, int64_
     if (hc) GVT_CUDA_TRY(cudaMemcpyAsync(compact, dc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *count = k;
+    GVT_API_END
+}
+
+gvt_status gvt_solver_direction(gvt_ctx *c, float *p_out, int64_t n) {
+    GVT_API_BEGIN(c)
+    GVT_REQUIRE(n >= 0 && (p_out || n == 0), GVT_E_DIM, "NULL output with n > 0");
+    gvt::solver_direction(c, p_out, n);
     GVT_API_END
 }
 

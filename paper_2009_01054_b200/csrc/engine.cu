@@ -1280,6 +1280,10 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     } else {
         r = wsT<float>(c, "cg.r", n), p = wsT<float>(c, "cg.p", n);
         cg_init(c, yd, n, x, r, p, state, rel_tol);
+        if (!es) {  // kept for gvt_solver_direction (reading S30's in-loop check)
+            c->last_p = p;
+            c->last_n = n;
+        }
     }
     auto iteration = [&]() {
         if (minres) {
@@ -1410,6 +1414,8 @@ static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T
 gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f, const int32_t *s,
                int64_t n, const float *y, const gvt_term *terms, int n_terms, double lambda, int max_iter,
                double rel_tol, float *a_out, int *iters_out, double *relres_hist) {
+    c->last_n = -1;
+    c->last_perm = nullptr;
     {
         const int32_t *nv = nullptr, *nv2 = nullptr;
         if (max_iter > 0) compact_fit(c, D, m, T, q, f, s, n, nv, nv2, 0);
@@ -1438,10 +1444,24 @@ gvt_status fit(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q,
     gather_f32(c, yd, perm, n, ys);
     gvt_status st = fit_impl(c, D, m, T, q, fs, ss, n, ys, terms, n_terms, lambda, max_iter, rel_tol, xs, iters_out,
                              relres_hist, nullptr);
+    if (c->last_n == n) c->last_perm = perm;
     OutArr ao = out_arr(c, "out.a", a_out, n);
     scatter_f32(c, xs, perm, n, ao.dev);
     out_finish(c, ao);
     return st;
+}
+
+// gvt_solver_direction: the last plain CG fit's search direction, scattered to caller order
+void solver_direction(gvt_ctx *c, float *out, int64_t n) {
+    GVT_REQUIRE(c->last_n >= 0 && c->last_p, GVT_E_STATE,
+                "no search direction kept: the last call was not a Hestenes-Stiefel CG pairwise_krr_fit on the "
+                "multi-kernel path (MINRES, Chronopoulos-Gear, early stopping and the single-CTA engine keep none)");
+    GVT_REQUIRE(n == c->last_n, GVT_E_DIM, "n differs from the last fit's local pair count");
+    if (n == 0) return;
+    OutArr o = out_arr(c, "out.p", out, n);
+    if (c->last_perm) scatter_f32(c, c->last_p, c->last_perm, n, o.dev);
+    else GVT_CUDA_TRY(cudaMemcpyAsync(o.dev, c->last_p, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream));
+    out_finish(c, o);
 }
 
 gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *f,
@@ -1449,6 +1469,8 @@ gvt_status fit_early_stopping(gvt_ctx *c, const float *D, int64_t m, const float
                               int64_t n_val, const float *vlab, const gvt_term *terms, int n_terms, double lambda,
                               int patience, int max_iter, float *a_out, int *best_iter, double *best_auc,
                               int *iters_run, double *auc_hist) {
+    c->last_n = -1;
+    c->last_perm = nullptr;
     if (max_iter > 0) compact_fit(c, D, m, T, q, f, s, n, vf, vs, n_val);
     EsArgs es;
     es.vf = vf;

@@ -119,6 +119,12 @@ struct gvt_ctx {
     gvt_host_allgather_fn host_allgather = nullptr;  // host-mediated communicator (gvt_comm_init_host)
     void *host_user = nullptr;
 
+    // the last Hestenes-Stiefel CG fit's search direction (gvt_solver_direction): device vector
+    // in solve order, its length (-1 = none kept) and the sorted-order permutation (nullptr = identity)
+    float *last_p = nullptr;
+    int64_t last_n = -1;
+    const int32_t *last_perm = nullptr;
+
     // pinned host scratch for scalar read-backs
     void *pinned = nullptr;
     size_t pinned_bytes = 0;

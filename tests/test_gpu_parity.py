@@ -4,6 +4,10 @@ bit-exact; fp32 matvec relative L2 <= 1e-5; CG weights after 50 iterations relat
 <= 1e-4 and predictions max-abs <= 1e-4 on C1 (reading S30); Gram max error relative to
 max |entry| <= 1e-6.  Full-size configs are checked on sampled outputs
 the oracle computes one by one, in the launch configuration bench.py times."""
+import functools
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -337,11 +341,68 @@ def test_c4_multiterm(ctx, kernel):
     assert r <= MATVEC_TOL
 
 
+@functools.lru_cache(maxsize=1)
+def _c5():
+    return synth.config5()
+
+
+def predict_parity(ctx, w, kernel, k_samples, restrict=None, seed=0):
+    """pairwise_predict over ALL of the workload's test pairs on fixed seeded weights, in
+    bench.py's launch configuration (GPU Grams from the features, default options), checked
+    against the oracle's per-term GVT on sampled test outputs (SURVEY.md 8(c) acceptance:
+    "on other configs run the GPU predict on the oracle's weights and check relative L2
+    <= 1e-5"; PAPER.md:321-322)."""
+    terms = G.gvt_kernel_terms(kernel)
+    Dg, Tg = grams_gpu(ctx, w)
+    a = synth.random_vector(100 + seed, w.n)
+    sc = ctx.predict(Dg, Tg, dev(w.test_first), dev(w.test_second), dev(w.train_first), dev(w.train_second),
+                     dev(a), terms).cpu().numpy()
+    if restrict is not None:
+        cand = np.nonzero(restrict(w))[0]
+        idx = cand[synth.sample_indices(seed, len(cand), k_samples)]
+    else:
+        idx = synth.sample_indices(seed, w.n_test, k_samples)
+    D, T = grams_oracle(w)
+    ref = O.gvt_matvec(O.kernel_terms(kernel), D, T, w.test_first[idx], w.test_second[idx], w.train_first,
+                       w.train_second, a)
+    return rel(sc[idx], ref), sc
+
+
+@pytest.mark.parametrize("kernel", [G.POLY2D, G.MLPK, G.RANKING])
+def test_c4_predict_full_size(ctx, kernel):
+    """C4 predict at full size: 1e6 test pairs (the complement of the 2e6 training cells) on
+    fixed weights, 48 sampled outputs against the oracle at relative L2 <= 1e-5."""
+    w = synth.config4()
+    if kernel in HOM:
+        w = synth.union_domain(w)
+    r, sc = predict_parity(ctx, w, kernel, 48)
+    assert np.all(np.isfinite(sc))
+    assert r <= MATVEC_TOL, r
+
+
+@pytest.mark.slow
+def test_c5_predict_full_size(ctx):
+    """C5 predict at full size: 2e7 i.i.d. test pairs (d ~ degree, t ~ target weight; with
+    duplicates) against the 1e8 training pairs on fixed weights, checked on 256 sampled outputs
+    whose target lies among 16 seeded targets (oracle O3b), relative L2 <= 1e-5.  Duplicate test
+    pairs are scored identically (each output is one tile cell / one row dot)."""
+    w = _c5()
+    tset = np.sort(np.random.default_rng(57).choice(w.q, 16, replace=False))
+    r, sc = predict_parity(ctx, w, G.KRONECKER, 256, restrict=lambda w: np.isin(w.test_second, tset))
+    assert r <= MATVEC_TOL, r
+    key = w.test_first.astype(np.int64) * w.q + w.test_second
+    order = np.argsort(key, kind="stable")
+    ks, ss = key[order], sc[order]
+    dup = ks[1:] == ks[:-1]
+    assert dup.sum() > 1000  # i.i.d. draws: duplicates are present
+    assert np.array_equal(ss[1:][dup], ss[:-1][dup])
+
+
 @pytest.mark.slow
 def test_c5_full_size_sampled(ctx):
     """C5 at full size (1e8 pairs, m=q=20000): the training matvec over all outputs, checked
     on 256 sampled outputs whose target lies among 16 seeded targets (oracle O3b)."""
-    w = synth.config5()
+    w = _c5()
     tset = np.sort(np.random.default_rng(55).choice(w.q, 16, replace=False))
     r, u, idx = sampled_parity(ctx, w, G.KRONECKER, k_samples=256,
                                restrict=lambda w: np.isin(w.train_second, tset))
@@ -560,9 +621,103 @@ def test_in_loop_matvec_parity(ctx, cfg, kernel):
 def test_in_loop_matvec_parity_c5(ctx):
     """C5 at full size: K x_30 (the bench's final iterate) on 128 sampled outputs whose target is
     among 8 seeded targets (oracle O3b)."""
-    w = synth.config5()
+    w = _c5()
     tset = np.sort(np.random.default_rng(56).choice(w.q, 8, replace=False))
     _in_loop_check(ctx, w, G.KRONECKER, [w.iters], 128, restrict=lambda w: np.isin(w.train_second, tset))
+
+
+def _kappa_c(kernel, D, T, of, os_, inf, ins, v):
+    """|| |K| |v| || / ||K v|| on the sampled outputs: the cancellation factor that scales fp32
+    rounding (relative 2^-24 per operation) into the relative error of K v (reading S31)."""
+    Da, Ta = np.abs(D), (None if T is None else np.abs(T))
+    num = O.gvt_matvec(_abs_terms(kernel), Da, Ta, of, os_, inf, ins, np.abs(v))
+    den = O.gvt_matvec(O.kernel_terms(kernel), D, T, of, os_, inf, ins, v)
+    return np.linalg.norm(num) / max(np.linalg.norm(den), 1e-300), den
+
+
+@pytest.mark.parametrize("cfg,kernel", [("C2", G.KRONECKER), ("C3", G.SYMMETRIC), ("C3", G.ANTISYMMETRIC),
+                                        ("C4", G.POLY2D), ("C4", G.MLPK), ("C4", G.RANKING)])
+def test_s30_literal_search_directions(ctx, cfg, kernel):
+    """Reading S30 literally: dump the CG search directions p_k at k = 1, K/2, K
+    of the GPU's own fit (gvt_solver_direction; p_1 = y, p_k = the direction left after k - 1
+    iterations) and check K p_k on the GPU (its Grams computed from the features) against the
+    oracle (its fp64 Grams from the same features) at plain relative L2 <= 1e-5 on sampled
+    outputs.  Both numbers -- the plain relative error and the S31-normalised one -- are recorded
+    (GVT_S30_RECORD=path appends a JSON line per case).  The plain gate applies where the
+    cancellation factor kappa_c = || |K| |p| || / ||K p|| lets the engine's designed backward error
+    (2^-20, the 22-bit operand splits with margin) resolve 1e-5 (kappa_c * 2^-20 <= 1e-5, i.e.
+    kappa_c <= 10.5); above it the normalised gate of S31 applies
+    and the plain number is reported, not gated."""
+    w = synth.by_name(cfg)
+    if kernel in HOM and w.Xt is not None:
+        w = synth.union_domain(w)
+    terms = G.gvt_kernel_terms(kernel)
+    Dg, Tg = grams_gpu(ctx, w)
+    D, T = grams_oracle(w)
+    f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
+    idx = synth.sample_indices(2, w.n, 48 if cfg == "C4" else 256)
+    of, os_ = w.train_first[idx], w.train_second[idx]
+    K = w.iters
+    for k in (1, K // 2, K):
+        if k == 1:
+            p = w.y.astype(np.float32)
+        else:
+            _, it, _, _ = ctx.fit(Dg, Tg, f, s, y, terms, w.lam, k - 1, want_history=False)
+            assert it == k - 1
+            p = ctx.solver_direction(w.n)
+        u = ctx.matvec(Dg, Tg, f, s, f, s, dev(p), terms).cpu().numpy()
+        kc, ref = _kappa_c(kernel, D, T, of, os_, w.train_first, w.train_second, p.astype(np.float64))
+        plain = rel(u[idx], ref)
+        normed = np.linalg.norm(u[idx] - ref) / (kc * np.linalg.norm(ref))
+        rec = {"cfg": cfg, "kernel": int(kernel), "k": k, "plain_rel_l2": plain, "s31_normalised": normed,
+               "kappa_c": kc}
+        if os.environ.get("GVT_S30_RECORD"):
+            with open(os.environ["GVT_S30_RECORD"], "a") as fh:
+                fh.write(json.dumps(rec) + "\n")
+        assert normed <= MATVEC_TOL, rec
+        if kc * 2.0 ** -20 <= MATVEC_TOL:
+            assert plain <= MATVEC_TOL, rec
+
+
+def test_solver_direction_contract(ctx):
+    """gvt_solver_direction: after k CG iterations the kept direction is p_{k+1} = r_k + beta_k p_k,
+    checked against the oracle's fp64 recurrences on C1's fp32 Grams (k = 1, 2: the fp32/fp64
+    iterates still agree closely there); GVT_E_STATE after a MINRES fit; GVT_E_DIM on a wrong n."""
+    w = synth.config1()
+    D, T = grams_oracle(w)
+    D32, T32 = f32(D), f32(T)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)  # the multi-kernel CG path (C1 would pick the single-CTA one)
+    try:
+        Do, To = D32.astype(np.float64), T32.astype(np.float64)
+        Kx = O.explicit_matrix(O.KRONECKER, Do, To, w.train_first, w.train_second, w.train_first, w.train_second)
+        A = Kx + w.lam * np.eye(w.n)
+        for k in (1, 2):
+            ctx.fit(dev(D32), dev(T32), f, s, y, kron, w.lam, k, want_history=False)
+            p = ctx.solver_direction(w.n)
+            # fp64 CG recurrences on the explicit system (textbook Hestenes-Stiefel)
+            x = np.zeros(w.n); r = w.y.astype(np.float64).copy(); pp = r.copy(); rho = r @ r
+            for _ in range(k):
+                Ap = A @ pp
+                al = rho / (pp @ Ap)
+                x += al * pp
+                r -= al * Ap
+                rho1 = r @ r
+                pp = r + (rho1 / rho) * pp
+                rho = rho1
+            assert rel(p, pp) <= 1e-5, (k, rel(p, pp))
+        with pytest.raises(G.GvtError) as e:
+            ctx.solver_direction(w.n + 1)
+        assert e.value.code == G.E_DIM
+        ctx.set_option(G.OPT_SOLVER, G.SOLVER_MINRES)
+        ctx.fit(dev(D32), dev(T32), f, s, y, kron, w.lam, 3, want_history=False)
+        with pytest.raises(G.GvtError) as e:
+            ctx.solver_direction(w.n)
+        assert e.value.code == G.E_STATE
+    finally:
+        ctx.set_option(G.OPT_SOLVER, G.SOLVER_CG)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
 
 
 @pytest.mark.parametrize("slabs", [1, 3])

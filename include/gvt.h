@@ -112,10 +112,13 @@ typedef enum {
                                     graph (not while GVT_OPT_PROFILE = 1); 0 = eager launches        */
     GVT_OPT_SOLVER = 8,          /* iterative solver of pairwise_krr_fit(_early_stopping): gvt_solver,
                                     default GVT_SOLVER_CG                                             */
-    GVT_OPT_EXCHANGE = 9,        /* data-parallel exchange per matvec: 0 (default) =
-                                    all-gather the S column slabs (4 q m bytes), stage 2 on the local
-                                    outputs; 1 = u-exchange: stage 2 of the rank's own slab over EVERY
-                                    output, then a reduce of the n-vector to its owners (4 n bytes)   */
+    GVT_OPT_EXCHANGE = 9,        /* data-parallel exchange per matvec: 0 = all-gather
+                                    the S column slabs (4 q m bytes, pipelined per slab with stage 2),
+                                    stage 2 on the local outputs; 1 = u-exchange: stage 2 of the rank's
+                                    own slab over EVERY output, then each output segment summed by its
+                                    owner in rank order (4 n bytes); 2 (default) = by estimated bytes:
+                                    both exchanges do the same stage-2 work per rank, so the u-exchange
+                                    whenever the out sample (all ranks) is smaller than q_out x m_in */
     GVT_OPT_CG_VARIANT = 10,     /* CG form: 0 (default) = Hestenes-Stiefel (two reductions per
                                     iteration); 1 = Chronopoulos-Gear (the same iterates in exact
                                     arithmetic, matvec on r, one fused reduction of r.r and w.r per
@@ -178,7 +181,13 @@ gvt_status gvt_reset_stats(gvt_ctx *ctx);
  * (and of y / a), the shards must be drug-partitioned by contiguous first-id ranges in
  * rank order (gvt_partition computes them), D and T are replicated.  Stage 1 runs on
  * the local pairs, the S column slabs are all-gathered over NVLink, stage 2 runs on the
- * local out pairs, CG dot products are all-reduced. */
+ * local out pairs, CG dot products are all-reduced.  Every
+ * dispatch decision (engine, stage-2 kernel, slabs) is taken from rank-independent sizes,
+ * so all ranks issue the same collectives.
+ * world == 1 with nccl_unique_id == NULL: single-GPU mode (no communicator).  world == 1 WITH
+ * a unique id: a one-rank NCCL communicator, and the data-parallel path runs with its real
+ * NCCL calls on one GPU (the executable check of the NCCL data plane on a one-GPU box).
+ * Errors: GVT_E_PARAM (bad rank/world, NULL id with world > 1), GVT_E_NCCL. */
 gvt_status gvt_nccl_unique_id(void *out128);
 gvt_status gvt_comm_init(gvt_ctx *ctx, const void *nccl_unique_id, int rank, int world);
 
@@ -188,8 +197,10 @@ gvt_status gvt_comm_init(gvt_ctx *ctx, const void *nccl_unique_id, int rank, int
  * memory of world * bytes with this rank's block at buf + rank * bytes, and the callback fills the
  * other ranks' blocks (returns 0 on success).  The library synchronises its stream around each
  * call, so no kernel ever waits on another rank; collectives are then not graph-capturable and
- * the solver replays eagerly.  The results equal the NCCL path's (the same exchanges and
- * reductions in rank order; u-exchange reductions are summed on the device in rank order). */
+ * the solver replays eagerly.  The results equal the NCCL path's bit for bit: both run the same
+ * exchanges, and every reduction is a fixed rank-order sum on the device (solver dot products
+ * from all-gathered partials; the u-exchange from the owner's received segments -- NCCL
+ * send/recv, not ncclReduce). */
 typedef int (*gvt_host_allgather_fn)(void *user, void *buf, size_t bytes);
 gvt_status gvt_comm_init_host(gvt_ctx *ctx, int rank, int world, gvt_host_allgather_fn allgather, void *user);
 
@@ -204,6 +215,16 @@ gvt_status gvt_partition(const int64_t *deg, int64_t m, int world, int64_t *boun
  * rounded up to a multiple of 32 and kept monotone.  Rank s runs stage 1 on rows
  * [bounds[s], bounds[s+1]).  Host-only, no device work. */
 gvt_status gvt_slab_bounds(const int64_t *row_ptr, int64_t nrow, int nslab, int64_t *bounds);
+
+/* The slab partition the engine uses (stage 1 per drug column slab): balanced
+ * by the estimated cost C(h) = w_entry * row_ptr[h] + w_row * h of rows [0, h): bounds[s] = the
+ * first row with C >= s/nslab * C(nrow), rounded up to a multiple of 32 and kept monotone;
+ * w_row = 0 gives gvt_slab_bounds.  The engine passes (0, 1) for the dense tensor-core engine
+ * (both GEMMs scale with the slab's rows) and (q_out / 3.3e6, u-exchange ? 4 n_out / 6.4e6 : 0)
+ * for the sparse engine (stage-1 FMAs per entry; stage-2 slice gathers per row).  Host-only.
+ * Errors: GVT_E_PARAM for NULL pointers, nrow < 0, nslab < 1 or negative weights. */
+gvt_status gvt_slab_bounds_cost(const int64_t *row_ptr, int64_t nrow, int nslab, double w_entry, double w_row,
+                                int64_t *bounds);
 
 /* decompose: the Corollary's term list for `kernel` (
  * MLPK 10-term expansion PAPER.md:736-747; Anti-symmetric as (I-P)(D(x)D), reading S3).

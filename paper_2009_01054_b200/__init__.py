@@ -111,8 +111,9 @@ _lib.pairwise_predict_rect.argtypes = [_P, _P, _I64, _I64, _P, _I64, _I64, _P, _
                                        ctypes.c_int, _P]
 
 _lib.gvt_solver_direction.argtypes = [_P, _P, _I64]
+_lib.gvt_slab_bounds_cost.argtypes = [_P, _I64, ctypes.c_int, ctypes.c_double, ctypes.c_double, _P]
 
-EXPORTED = ["gvt_slab_bounds", "gvt_solver_direction",
+EXPORTED = ["gvt_slab_bounds", "gvt_solver_direction", "gvt_slab_bounds_cost",
             "gvt_create", "gvt_destroy", "gvt_set_stream", "gvt_set_option", "gvt_get_stats", "gvt_reset_stats",
             "gvt_nccl_unique_id", "gvt_comm_init", "gvt_partition", "gvt_kernel_terms", "gvt_gram", "gvt_matvec",
             "pairwise_krr_fit", "pairwise_predict", "gvt_sort_plan", "gvt_last_error",
@@ -188,6 +189,15 @@ def gvt_slab_bounds(row_ptr, nslab: int):
     rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
     bounds = np.zeros(nslab + 1, dtype=np.int64)
     _check(_lib.gvt_slab_bounds(rp.ctypes.data, rp.size - 1, nslab, bounds.ctypes.data), "gvt_slab_bounds")
+    return bounds
+
+
+def gvt_slab_bounds_cost(row_ptr, nslab: int, w_entry: float, w_row: float):
+    """The engine's cost-balanced slab partition (host only)."""
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
+    bounds = np.zeros(nslab + 1, dtype=np.int64)
+    _check(_lib.gvt_slab_bounds_cost(rp.ctypes.data, rp.size - 1, nslab, float(w_entry), float(w_row),
+                                     bounds.ctypes.data), "gvt_slab_bounds_cost")
     return bounds
 
 

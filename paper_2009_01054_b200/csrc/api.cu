@@ -7,6 +7,7 @@
 namespace gvt {
 const char *last_error();
 void slab_bounds(const int64_t *rp, int64_t nrow, int G, int64_t *bounds);
+void slab_bounds_cost(const int64_t *rp, int64_t nrow, int G, double w_entry, double w_row, int64_t *bounds);
 int kernel_terms(int kernel, gvt_term *o);
 void nccl_unique_id(void *out128);
 void comm_init(gvt_ctx *c, const void *id128, int rank, int world);
@@ -156,7 +157,8 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
         c->cg_variant = (int)v;
         break;
     case GVT_OPT_EXCHANGE:
-        GVT_REQUIRE(v == 0 || v == 1, GVT_E_PARAM, "exchange must be 0 (S all-gather) or 1 (u reduce)");
+        GVT_REQUIRE(v == 0 || v == 1 || v == 2, GVT_E_PARAM,
+                    "exchange must be 0 (S all-gather), 1 (u reduce) or 2 (by estimated bytes)");
         c->exchange = (int)v;
         break;
     case GVT_OPT_SOLVER:
@@ -262,6 +264,16 @@ gvt_status gvt_slab_bounds(const int64_t *row_ptr, int64_t nrow, int nslab, int6
         return GVT_E_PARAM;
     }
     gvt::slab_bounds(row_ptr, nrow, nslab, bounds);
+    return GVT_OK;
+}
+
+gvt_status gvt_slab_bounds_cost(const int64_t *row_ptr, int64_t nrow, int nslab, double w_entry, double w_row,
+                                int64_t *bounds) {
+    if (!row_ptr || !bounds || nrow < 0 || nslab < 1 || !(w_entry >= 0) || !(w_row >= 0)) {
+        gvt::set_error("gvt_slab_bounds_cost: bad arguments");
+        return GVT_E_PARAM;
+    }
+    gvt::slab_bounds_cost(row_ptr, nrow, nslab, w_entry, w_row, bounds);
     return GVT_OK;
 }
 

@@ -23,6 +23,8 @@ struct NcclApi {
                            cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -45,11 +47,22 @@ static void load_nccl() {
     g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))dlsym(h, "ncclGroupEnd");
     g_nccl.Reduce = (decltype(g_nccl.Reduce))dlsym(h, "ncclReduce");
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.Send = (decltype(g_nccl.Send))dlsym(h, "ncclSend");
+    g_nccl.Recv = (decltype(g_nccl.Recv))dlsym(h, "ncclRecv");
     GVT_REQUIRE(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather &&
-                    g_nccl.Broadcast && g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.Reduce && g_nccl.AllReduce,
+                    g_nccl.Broadcast && g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.Reduce && g_nccl.AllReduce &&
+                    g_nccl.Send && g_nccl.Recv,
                 GVT_E_NCCL, "libnccl.so.2 lacks a required symbol");
     g_nccl.h = h;
 }
+
+// accounting of one collective (kind "collective": count, and CUDA-event time when profiling)
+struct Coll {
+    gvt_ctx *c;
+    cudaEvent_t ev = nullptr;
+    explicit Coll(gvt_ctx *ctx) : c(ctx) { launch_begin(c, K_COMM, &ev); }
+    void done() { launch_end(c, K_COMM, ev); }
+};
 
 #define NCCL_TRY(expr)                                                                                  \
     do {                                                                                                \
@@ -67,9 +80,17 @@ void nccl_unique_id(void *out128) {
     memcpy(out128, &id, sizeof(id));
 }
 
+void comm_destroy(gvt_ctx *c);
+
+// world 1 without a unique id: no communicator (single-GPU mode).  world 1 WITH a unique id: a
+// one-rank NCCL communicator, and the library runs its data-parallel path with real NCCL calls
+// (all-gathers, grouped broadcasts, send/recv, all-reduces) on one GPU -- the executed check of
+// the NCCL data plane that a one-GPU box allows.
 void comm_init(gvt_ctx *c, const void *id128, int rank, int world) {
     GVT_REQUIRE(world >= 1 && rank >= 0 && rank < world, GVT_E_PARAM, "comm_init: bad rank/world");
-    if (world == 1) {
+    comm_destroy(c);
+    c->host_allgather = nullptr;
+    if (world == 1 && !id128) {
         c->rank = 0;
         c->world = 1;
         return;
@@ -100,6 +121,7 @@ void comm_init_host(gvt_ctx *c, int rank, int world, gvt_host_allgather_fn fn, v
 
 // dev holds [world][bytes]; this rank's block is valid on entry, every block on return
 static void host_allgather(gvt_ctx *c, void *dev, size_t bytes) {
+    Coll co(c);
     std::vector<char> h((size_t)c->world * bytes);
     char *mine = h.data() + (size_t)c->rank * bytes;
     if (bytes) {
@@ -112,29 +134,34 @@ static void host_allgather(gvt_ctx *c, void *dev, size_t bytes) {
         GVT_CUDA_TRY(cudaMemcpyAsync(dev, h.data(), h.size(), cudaMemcpyHostToDevice, c->stream));
         GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
+    co.done();
 }
 
 // partials laid out [world][count]; each rank wrote its own slot; gather all slots so the
 // fixed-order reduction over world*count values gives bit-identical scalars on every rank
 void allreduce_partials(gvt_ctx *c, double *partials, int count) {
-    if (c->world <= 1) return;
+    if (!distributed(c)) return;
     if (c->host_allgather) return host_allgather(c, partials, sizeof(double) * (size_t)count);
+    Coll co(c);
     NCCL_TRY(g_nccl.AllGather(partials + (size_t)c->rank * count, partials, (size_t)count, ncclFloat64,
                               (ncclComm_t)c->nccl_comm, c->stream));
+    co.done();
 }
 
 // S slabs laid out [world][slab_floats]; in-place all-gather of the local slab
 void allgather_slabs(gvt_ctx *c, float *S, size_t slab_floats) {
-    if (c->world <= 1) return;
+    if (!distributed(c)) return;
     if (c->host_allgather) return host_allgather(c, S, sizeof(float) * slab_floats);
+    Coll co(c);
     NCCL_TRY(g_nccl.AllGather(S + (size_t)c->rank * slab_floats, S, slab_floats, ncclFloat32,
                               (ncclComm_t)c->nccl_comm, c->stream));
+    co.done();
 }
 
 // host-visible all-gather of one int64 per rank (plan time only: synchronises)
 std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v) {
     std::vector<int64_t> out((size_t)c->world, v);
-    if (c->world <= 1) return out;
+    if (!distributed(c)) return out;
     if (c->host_allgather) {
         GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
         GVT_REQUIRE(c->host_allgather(c->host_user, out.data(), sizeof(int64_t)) == 0, GVT_E_NCCL,
@@ -143,7 +170,9 @@ std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v) {
     }
     int64_t *d = wsT<int64_t>(c, "comm.counts", (size_t)c->world);
     GVT_CUDA_TRY(cudaMemcpyAsync(d + c->rank, &v, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    Coll co(c);
     NCCL_TRY(g_nccl.AllGather(d + c->rank, d, 1, ncclInt64, (ncclComm_t)c->nccl_comm, c->stream));
+    co.done();
     GVT_CUDA_TRY(cudaMemcpyAsync(out.data(), d, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost, c->stream));
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return out;
@@ -154,7 +183,7 @@ std::vector<int64_t> allgather_count(gvt_ctx *c, int64_t v) {
 void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<int64_t> &counts,
                    const std::vector<int64_t> &offsets, bool is_float) {
     const size_t esz = 4;
-    if (c->world <= 1) {
+    if (!distributed(c)) {
         if (counts[0] > 0 && local != full)
             GVT_CUDA_TRY(cudaMemcpyAsync(full, local, esz * counts[0], cudaMemcpyDeviceToDevice, c->stream));
         return;
@@ -173,6 +202,7 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
                                              cudaMemcpyDeviceToDevice, c->stream));
         return;
     }
+    Coll co(c);
     NCCL_TRY(g_nccl.GroupStart());
     for (int g = 0; g < c->world; g++) {
         if (counts[g] == 0) continue;
@@ -181,6 +211,7 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
                                   is_float ? ncclFloat32 : ncclInt32, g, (ncclComm_t)c->nccl_comm, c->stream));
     }
     NCCL_TRY(g_nccl.GroupEnd());
+    co.done();
 }
 
 // local[i] = sum_g tmp[g][off + i] (i < cnt), local[cnt + j] = sum_g tmp[g][n_full + j] (j < tail), g in order
@@ -203,13 +234,17 @@ void sum_rank_segments(gvt_ctx *c, const float *tmp, size_t per, int world, int6
 
 // u-exchange: every rank holds a partial of the FULL out vector
 // (its own S slab's contribution to every output); rank g receives the sum of the segment
-// [offsets[g], offsets[g+1]) into `local` (grouped ncclReduce, one root per segment -- the
-// variable-count reduce-scatter), and the `tail` extra values after the full vector (MLPK's
-// diagonal samples, needed on every rank) are all-reduced into local + counts[rank].
+// [offsets[g], offsets[g+1]) into `local`, and the `tail` extra values after the full vector
+// (MLPK's diagonal samples, needed on every rank) are summed into local + counts[rank].
+// The sums run on the device in RANK ORDER (k_sum_rank_segments) on every path, so the NCCL
+// path and the host twin give bit-identical results: the NCCL path moves each segment to its
+// owner with grouped send/recv (the bytes of a variable-count reduce-scatter: (G-1)/G of the
+// partial vector leaves each rank) and all-gathers the tails; no NCCL reduction (whose order
+// NCCL chooses) is used.
 void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::vector<int64_t> &counts,
                      const std::vector<int64_t> &offsets, int64_t tail) {
     const int64_t n_full = offsets.back();
-    if (c->world <= 1) {
+    if (!distributed(c)) {
         const int64_t n = counts[0] + tail;
         if (n > 0 && partial != local)
             GVT_CUDA_TRY(cudaMemcpyAsync(local, partial, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -225,17 +260,32 @@ void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::
         sum_rank_segments(c, tmp, per, c->world, offsets[c->rank], counts[c->rank], n_full, tail, local);
         return;
     }
+    const int me = c->rank, G = c->world;
+    const int64_t cnt = counts[me];
+    float *seg = wsT<float>(c, "comm.uex_seg", (size_t)(cnt > 0 ? cnt : 1) * G);     // [G][cnt]: my segment from g
+    float *tl = wsT<float>(c, "comm.uex_tail", (size_t)(tail > 0 ? tail : 1) * G);    // [G][tail]
+    if (cnt > 0)
+        GVT_CUDA_TRY(cudaMemcpyAsync(seg + (size_t)me * cnt, partial + offsets[me], sizeof(float) * cnt,
+                                     cudaMemcpyDeviceToDevice, c->stream));
+    Coll co(c);
     NCCL_TRY(g_nccl.GroupStart());
-    for (int g = 0; g < c->world; g++) {
-        if (counts[g] == 0) continue;
-        const float *send = partial + offsets[g];
-        NCCL_TRY(g_nccl.Reduce(send, g == c->rank ? (void *)local : (void *)send, (size_t)counts[g], ncclFloat32,
-                               ncclSum, g, (ncclComm_t)c->nccl_comm, c->stream));
+    for (int g = 0; g < G; g++) {
+        if (g == me) continue;
+        if (counts[g] > 0)
+            NCCL_TRY(g_nccl.Send(partial + offsets[g], (size_t)counts[g], ncclFloat32, g, (ncclComm_t)c->nccl_comm,
+                                 c->stream));
+        if (cnt > 0)
+            NCCL_TRY(g_nccl.Recv(seg + (size_t)g * cnt, (size_t)cnt, ncclFloat32, g, (ncclComm_t)c->nccl_comm,
+                                 c->stream));
     }
     if (tail > 0)
-        NCCL_TRY(g_nccl.AllReduce(partial + n_full, local + counts[c->rank], (size_t)tail, ncclFloat32, ncclSum,
-                                  (ncclComm_t)c->nccl_comm, c->stream));
+        NCCL_TRY(g_nccl.AllGather(partial + n_full, tl, (size_t)tail, ncclFloat32, (ncclComm_t)c->nccl_comm,
+                                  c->stream));
     NCCL_TRY(g_nccl.GroupEnd());
+    co.done();
+    // local[i] = sum_g seg[g][i]; local[cnt + j] = sum_g tl[g][j] (rank order)
+    sum_rank_segments(c, seg, (size_t)cnt, G, 0, cnt, cnt, 0, local);
+    sum_rank_segments(c, tl, (size_t)tail, G, 0, 0, 0, tail, local + cnt);
 }
 
 }  // namespace gvt

@@ -23,7 +23,7 @@ static const char *kKindNames[K_NUM_KINDS] = {
     "gram_simt",   "gram_tc",       "split_operand",  "pad_copy",     "plan_keys",      "plan_sort(cub)",
     "plan_rowptr", "plan_gather",   "stage1_sparse", "stage2_gather", "densify",     "stage1_tc",
     "stage2_tc",   "segment_sum",   "gemv",        "combine",      "cartesian",      "cg_vector",
-    "cg_scalar",   "fill",          "auc",          "tiny_cg",
+    "cg_scalar",   "fill",          "auc",          "tiny_cg",       "collective",
 };
 
 const char *kind_name(int k) { return (k >= 0 && k < K_NUM_KINDS) ? kKindNames[k] : "?"; }
@@ -64,7 +64,7 @@ void *pinned(gvt_ctx *c, size_t bytes) {
 }
 
 void launch_begin(gvt_ctx *c, int kind, cudaEvent_t *ev_start) {
-    c->launches++;
+    if (kind != K_COMM) c->launches++;  // collectives run NCCL's kernels, not the library's
     c->counts[kind]++;
     *ev_start = nullptr;
     if (c->profile) {

@@ -148,6 +148,10 @@ struct Problem {
     // outputs appended to the fit's own (the early-stopping validation pairs): left out of the
     // stage-2 dispatch estimate, so the early-stopping fit runs the same kernels as a plain fit
     int64_t n_out_extra = 0;
+    // rank-independent sizes for the dispatch estimates (every rank must take the same
+    // engine decisions, or the collectives of different engines mismatch): the out-sample size
+    // summed over ranks and its appended-extra part (world 1: the local sizes)
+    int64_t n_out_all = 0, n_out_extra_all = 0;
     int64_t dom(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m : q; }
     int64_t dom_out(int sel) const { return (sel == GVT_SEL_FIRST || hom) ? m_out : q_out; }
 };
@@ -204,6 +208,8 @@ struct GroupPlan {
     std::string tag;
     float *diag = nullptr;  // optional separate diagonal of X (global row index), computed per matvec
     int64_t n_diag = 0;     // extra (x, x) samples after the outputs (MLPK)
+    double ns_est = 0;      // stage-2 samples per rank for the dispatch estimates (identical on every rank)
+    double extra_est = 0;   // of which appended extra outputs (early-stopping validation pairs)
     // block sparsity of X per slab for the fused fp16 stage 1 (device lists, nullptr = dense)
     std::vector<const int32_t *> kb_list, kb_off;
 };
@@ -275,6 +281,8 @@ static bool dense_pays(gvt_ctx *c, double nnz, double ns, int64_t m_out, int64_t
 }
 
 static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
+    // every input of the decision is identical on all ranks: nnz of the full in-sample plan, the
+    // per-rank sample estimate, the factor dimensions
     if (c->engine == 1) return 1;
     bool tc = tc_available(c);
     if (c->engine == 2) {
@@ -283,7 +291,7 @@ static int choose_engine(gvt_ctx *c, const GroupPlan &g) {
         return 1;  // materialised Ones/Identity factors of a generic term list stay on SIMT
     }
     if (!(g.A.split && g.C.split)) return 1;  // factors were not split for tensor cores
-    return (tc && dense_pays(c, (double)g.ent.nnz, (double)g.smp.ns, g.A.n, g.q_out, g.m_in, g.C.cols)) ? 2 : 1;
+    return (tc && dense_pays(c, (double)g.ent.nnz, g.ns_est, g.A.n, g.q_out, g.m_in, g.C.cols)) ? 2 : 1;
 }
 
 // X-row slabs balanced by entry count (row_ptr over nrow rows), bounds multiples of 32 (TMA /
@@ -303,10 +311,37 @@ void slab_bounds(const int64_t *rp, int64_t nrow, int G, int64_t *bounds) {
     }
 }
 
+// Slabs balanced by an estimated cost C(h) = w_entry * row_ptr[h] + w_row * h (the cost of rows
+// [0, h)): bounds[s] = the first row whose C reaches the s/G quantile of C(nrow), rounded up to
+// 32, monotone.  w_row = 0 is slab_bounds.  The engine's weights (make_slabs): the dense engine's
+// stage-1 and stage-2 GEMMs both scale with the slab's ROWS (w_entry 0); the sparse engine's
+// stage 1 with its entries (q_out FMAs each) and, under the u-exchange, its stage 2 with its rows
+// (one W-wide slice of an S row per output).  Host only (gvt_slab_bounds_cost).
+void slab_bounds_cost(const int64_t *rp, int64_t nrow, int G, double w_entry, double w_row, int64_t *bounds) {
+    bounds[0] = 0;
+    bounds[G] = nrow;
+    auto cost = [&](int64_t h) { return w_entry * (double)rp[h] + w_row * (double)h; };
+    const double total = cost(nrow);
+    int64_t h = 0;
+    for (int s = 1; s < G; s++) {
+        const double target = total * s / G;
+        // C is non-decreasing in h: advance to the first row reaching the target
+        int64_t lo = h, hi = nrow;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cost(mid) < target) lo = mid + 1;
+            else hi = mid;
+        }
+        int64_t b = std::min(std::max(round_up(lo, 32), bounds[s - 1]), nrow);
+        bounds[s] = b;
+        h = std::min(lo, nrow);
+    }
+}
+
 // slabs of a group, identical on every rank (computed from the same full plan)
-static void make_slabs(gvt_ctx *c, GroupPlan &g) {
+static void make_slabs(gvt_ctx *c, GroupPlan &g, bool uex) {
     // one slab per rank across GPUs (rank r owns slab r); emulated slabs only at world 1
-    int G = c->world > 1 ? c->world : std::max(1, c->slabs);
+    int G = distributed(c) ? c->world : std::max(1, c->slabs);
     const int64_t nrow = g.m_in;
     std::vector<int64_t> rp((size_t)nrow + 1);
     GVT_CUDA_TRY(cudaMemcpyAsync(rp.data(), g.ent.row_ptr, sizeof(int64_t) * (nrow + 1), cudaMemcpyDeviceToHost,
@@ -314,7 +349,12 @@ static void make_slabs(gvt_ctx *c, GroupPlan &g) {
     GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     g.nslab = G;
     g.bounds.assign((size_t)G + 1, 0);
-    slab_bounds(rp.data(), nrow, G, g.bounds.data());
+    // weights of the engine's own cost (entry balancing left dense slabs with rows max/mean
+    // 3.2 on degree-sorted ids): dense -> rows; sparse -> q_out per entry (stage 1, ~3.3e6 FMA/us)
+    // plus, under the u-exchange, 4 B per output per row (stage 2 slice gathers, ~6.4e6 B/us)
+    if (g.engine == 2) slab_bounds_cost(rp.data(), nrow, G, 0.0, 1.0, g.bounds.data());
+    else slab_bounds_cost(rp.data(), nrow, G, (double)g.q_out / 3.3e6, uex ? 4.0 * g.ns_est / 6.4e6 : 0.0,
+                          g.bounds.data());
     g.kpos.assign((size_t)G + 1, 0);
     int64_t wmax = 0;
     for (int s = 0; s <= G; s++) g.kpos[s] = rp[g.bounds[s]];
@@ -322,12 +362,12 @@ static void make_slabs(gvt_ctx *c, GroupPlan &g) {
     g.W = round_up(wmax > 0 ? wmax : 1, 32);
 }
 
-static bool my_slab(gvt_ctx *c, int s) { return c->world <= 1 || s == c->rank; }
+static bool my_slab(gvt_ctx *c, int s) { return !distributed(c) || s == c->rank; }
 
-static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
+static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag, bool uex) {
     g.tag = tag;
     g.engine = choose_engine(c, g);
-    make_slabs(c, g);
+    make_slabs(c, g, uex);
     g.qpad = round_up(g.q_out > 0 ? g.q_out : 1, 128);
     g.S = wsT<float>(c, (g.tag + ".S").c_str(), (size_t)g.nslab * g.qpad * g.W);
     if (g.engine == 2) bucket_samples(c, tag, g.smp, g.A.n, g.q_out);
@@ -359,6 +399,15 @@ static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag) {
     }
 }
 
+// per-rank stage-2 sample estimate from rank-independent sizes: the u-exchange serves the full
+// out sample on every rank; the S all-gather serves the rank's own outputs, estimated as the
+// average over ranks (world 1: exactly the local count)
+static void set_estimates(gvt_ctx *c, const Problem &P, GroupPlan &g) {
+    const double w = distributed(c) ? (double)c->world : 1.0;
+    g.ns_est = (P.uex ? (double)P.n_out_full : (double)P.n_out_all / w) + (double)g.n_diag;
+    g.extra_est = P.uex ? (double)P.n_out_extra_all : (double)P.n_out_extra_all / w;
+}
+
 static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int n_terms, Form form,
                         MatvecPlan &mp) {
     mp.form = form;
@@ -378,7 +427,8 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
         if (P.uex) build_sample_plan(c, (t + ".s").c_str(), P.of_full, P.os_full, P.n_out_full, rs, cs, n_diag, A.n, g.smp);
         else build_sample_plan(c, (t + ".s").c_str(), P.of, P.os, P.n_out, rs, cs, n_diag, A.n, g.smp);
         g.n_diag = n_diag;
-        finish_group(c, g, tag);
+        set_estimates(c, P, g);
+        finish_group(c, g, tag, P.uex);
         mp.groups.push_back(g);
     };
     switch (form) {
@@ -475,7 +525,8 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
             else
                 build_sample_plan(c, (ts + ".s").c_str(), P.of, P.os, P.n_out, t.row_sel_left, t.row_sel_right, 0,
                                   P.dom_out(t.row_sel_left), g.smp);
-            finish_group(c, g, tag);
+            set_estimates(c, P, g);
+            finish_group(c, g, tag, P.uex);
             mp.groups.push_back(g);
         }
         break;
@@ -575,7 +626,7 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
         // (P.uex: this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1)
         float *dst = P.uex ? partial : out;
         const int acc = P.uex ? !first : (accumulate || !first);
-        if (tile_scale && stage2_gather_pays(c, g.smp.ns - P.n_out_extra, g.A.n, g.q_out, w)) {
+        if (tile_scale && stage2_gather_pays(c, (int64_t)(g.ns_est - g.extra_est), g.A.n, g.q_out, w)) {
             Factor Av = g.A;
             Av.p = g.A.p + lo;
             stage2_gather16(c, g.smp, Av, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k, skld, w, coef, acc, dst);
@@ -640,7 +691,7 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
         const int acc = P.uex ? !first : (accumulate || !first);
         first = false;
         float *Ss = g.S + (size_t)s * g.qpad * g.W;
-        if (g.engine == 2 && !stage2_gather_pays(c, g.smp.ns - P.n_out_extra, g.A.n, g.q_out, w)) {
+        if (g.engine == 2 && !stage2_gather_pays(c, (int64_t)(g.ns_est - g.extra_est), g.A.n, g.q_out, w)) {
             char nm[48];
             snprintf(nm, sizeof(nm), "dense.Sop%d", s);
             Operand so = make_operand(c, nm, Ss, g.q_out, w, g.W, g.W, g.qpad);
@@ -657,7 +708,7 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
 static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u) {
     // gather p over the ranks (world 1: p_full is p_local itself)
     const float *p = p_local;
-    if (c->world > 1) {
+    if (distributed(c)) {
         gather_varlen(c, p_local, P.p_full, P.counts, P.offsets, true);
         p = P.p_full;
     }
@@ -805,7 +856,8 @@ static bool needs_split(gvt_ctx *c, Form form, const Problem &P) {
     const bool hom = !(form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC);
     const double mult = (form == FORM_SYM || form == FORM_ANTI || form == FORM_MLPK) ? 2.0 : 1.0;  // entries per pair
     const int64_t q_in = hom ? P.m : P.q, q_out = hom ? P.m_out : P.q_out;
-    const double ns = (double)(P.uex ? P.n_out_full : P.n_out) + (form == FORM_MLPK ? (double)P.m_out : 0.0);
+    const double ns = (P.uex ? (double)P.n_out_full : (double)P.n_out_all / (distributed(c) ? c->world : 1)) +
+                      (form == FORM_MLPK ? (double)P.m_out : 0.0);
     // the estimate of the problem's main Kronecker group (the same one choose_engine makes per group)
     return dense_pays(c, mult * (double)P.n_in, ns, P.m_out, q_out, P.m, q_in);
 }
@@ -845,7 +897,13 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
     P.offsets.assign(P.counts.size() + 1, 0);
     for (size_t g = 0; g < P.counts.size(); g++) P.offsets[g + 1] = P.offsets[g] + P.counts[g];
     P.n_in = P.offsets.back();
-    if (c->world > 1) {
+    P.n_out_all = out_is_in ? P.n_in : n_out;
+    if (distributed(c) && !out_is_in) {
+        P.out_counts = allgather_count(c, n_out);
+        P.n_out_all = 0;
+        for (int64_t v : P.out_counts) P.n_out_all += v;
+    }
+    if (distributed(c)) {
         int32_t *ff = wsT<int32_t>(c, "dist.f", (size_t)P.n_in);
         int32_t *fs = wsT<int32_t>(c, "dist.s", (size_t)P.n_in);
         gather_varlen(c, lf, ff, P.counts, P.offsets, false);
@@ -858,8 +916,17 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
         P.ins = ls;
     }
     // u-exchange needs every rank's out pairs on every rank (a fit's out sample is its in-sample)
-    // (also at world 1, where the reduce is a copy: the single-GPU tests exercise this path)
-    P.uex = c->exchange == 1;
+    // (also at world 1, where the reduce is a copy: the single-GPU tests exercise this path).
+    // Auto (2): both exchanges give every rank the same stage-2 work (its slab's K-range over all
+    // outputs, or all of K over its own outputs), so the choice is by bytes moved: 4 n_out (all
+    // ranks) per matvec vs 4 q_out m_in for the S slabs -- rank-independent sizes, the same choice
+    // on every rank.  Single-GPU mode has no exchange (auto = 0).
+    if (c->exchange == 2) {
+        const double cells = (double)P.q_out * (double)P.m;
+        P.uex = distributed(c) && (double)P.n_out_all + (double)P.m_out < cells;
+    } else {
+        P.uex = c->exchange == 1;
+    }
     if (P.uex) {
         if (out_is_in) {
             P.of_full = P.inf;
@@ -867,7 +934,7 @@ static void setup_problem(gvt_ctx *c, Problem &P, const float *D, int64_t m, con
             P.out_counts = P.counts;
             P.out_offsets = P.offsets;
         } else {
-            P.out_counts = allgather_count(c, n_out);
+            if (P.out_counts.empty()) P.out_counts = allgather_count(c, n_out);
             P.out_offsets.assign(P.out_counts.size() + 1, 0);
             for (size_t g = 0; g < P.out_counts.size(); g++)
                 P.out_offsets[g + 1] = P.out_offsets[g] + P.out_counts[g];
@@ -927,7 +994,7 @@ static bool compact_small_skip(gvt_ctx *c, int64_t m, int64_t qq) {
 static bool compact_matvec(gvt_ctx *c, const float *D, int64_t m, const float *T, int64_t q, const int32_t *of,
                            const int32_t *os, int64_t n_out, const int32_t *inf, const int32_t *ins, int64_t n_in,
                            const float *a, const gvt_term *terms, int n_terms, float *u) {
-    if (!c->compact || c->world > 1 || n_in <= 0 || n_out <= 0 || m <= 0 || !terms || n_terms < 1 || n_terms > 64)
+    if (!c->compact || distributed(c) || n_in <= 0 || n_out <= 0 || m <= 0 || !terms || n_terms < 1 || n_terms > 64)
         return false;
     if (!of || !os || !inf || !ins || !a || !u || !D) return false;
     if (compact_small_skip(c, m, T ? q : m)) return false;
@@ -1167,6 +1234,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         }
         setup_problem(c, P, D, m, T, q, of, os, no, of, os, n, terms, n_terms, form, false);
         P.n_out_extra = P.uex ? P.n_out_full - P.n_in : n_val;
+        P.n_out_extra_all = P.n_out_all - P.n_in;  // the validation pairs over all ranks
     } else {
         setup_problem(c, P, D, m, T, q, f, s, n, f, s, n, terms, n_terms, form, true);
     }
@@ -1194,7 +1262,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         esd = wsT<double>(c, "es.state", ES_STATE_N);
         ehist = wsT<double>(c, "es.hist", (size_t)(max_iter > 0 ? max_iter : 1));
         s_val = wsT<float>(c, "es.s", (size_t)n_val);
-        s_full = c->world > 1 ? wsT<float>(c, "es.s_full", (size_t)nv_all) : s_val;
+        s_full = distributed(c) ? wsT<float>(c, "es.s_full", (size_t)nv_all) : s_val;
         a_best = ao.dev;  // the weights returned are those of the best iteration
         if (n_val) GVT_CUDA_TRY(cudaMemsetAsync(s_val, 0, sizeof(float) * n_val, c->stream));
         es_init(c, esd, ehist, max_iter, ap);
@@ -1230,7 +1298,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     // GVT_OPT_ENGINE = 3, or chosen when a CG iteration is at most 4e6 FMAs and everything fits
     // in one SM's shared memory
     {
-        const bool eligible = form == FORM_KRON && !minres && !cgg && !es && c->world == 1 && c->slabs <= 1 &&
+        const bool eligible = form == FORM_KRON && !minres && !cgg && !es && !distributed(c) && c->slabs <= 1 &&
                               c->exchange == 0 && !P.rect && P.n_in == n && tiny_smem(P.m, P.q, n) > 0;
         const double fmas = (double)n * (double)P.q + (double)n * (double)P.m;
         GVT_REQUIRE(c->engine != 3 || eligible, GVT_E_PARAM,
@@ -1260,7 +1328,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     }
     auto evaluate = [&]() {
         if (!es) return;
-        if (c->world > 1) gather_varlen(c, s_val, s_full, vcounts, voffs, true);
+        if (distributed(c)) gather_varlen(c, s_val, s_full, vcounts, voffs, true);
         es_evaluate(c, ap, s_full, state, esd, ehist, es->patience, x, a_best, n);
     };
     float *r1 = nullptr, *r2 = nullptr, *v = nullptr, *W1 = nullptr, *W2 = nullptr, *r = nullptr, *p = nullptr;
@@ -1334,7 +1402,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
 // a_best stays the plain fit's.  One GPU only (ranks would need a common object set).
 static bool compact_fit(gvt_ctx *c, const float *&D, int64_t &m, const float *&T, int64_t &q, const int32_t *&f,
                         const int32_t *&s, int64_t n, const int32_t *&vf, const int32_t *&vs, int64_t n_val) {
-    if (!c->compact || c->world > 1 || n <= 0 || m <= 0) return false;
+    if (!c->compact || distributed(c) || n <= 0 || m <= 0) return false;
     if (compact_small_skip(c, m, T ? q : m)) return false;
     GVT_REQUIRE(f && s, GVT_E_DIM, "pair ids are NULL with n > 0");
     GVT_REQUIRE(n_val <= 0 || (vf && vs), GVT_E_DIM, "validation pair ids are NULL with n_val > 0");

@@ -60,6 +60,7 @@ enum KernelKind {
     K_FILL,
     K_AUC,
     K_TINY,
+    K_COMM,  // collectives (NCCL calls or host-twin exchanges): counted and timed, not library launches
     K_NUM_KINDS
 };
 const char *kind_name(int k);
@@ -94,7 +95,7 @@ struct gvt_ctx {
     int gemm_cta = 2;      // tensor-core GEMM: 2 = CTA-pair tcgen05 (cta_group::2), 1 = single CTA
     int graphs = 1;        // CUDA-graph replay of the solver iteration
     int solver = 0;        // GVT_SOLVER_CG / GVT_SOLVER_MINRES
-    int exchange = 0;      // multi-GPU: 0 = S slab all-gather, 1 = u reduce (NEXT-3)
+    int exchange = 2;      // multi-GPU: 0 = S slab all-gather, 1 = u reduce (NEXT-3), 2 = by estimated bytes
     int sorted_fit = 1;    // fits run on the pairs sorted by (first, second)
     int kblock_skip = 1;   // block-sparse stage 1 (skip all-zero K-blocks of X) where it pays
     int stage2 = 0;        // dense-engine stage 2: 0 = by estimated time, 1 = sampled GEMM, 2 = gather
@@ -162,6 +163,10 @@ bool is_device_ptr(const void *p);
 const void *stage_in(gvt_ctx *c, const char *name, const void *p, size_t bytes);
 
 constexpr int GVT_MAX_DEVICES = 64;
+
+// data-parallel mode: a communicator spans several ranks, or NCCL was forced at world 1
+// (gvt_comm_init with a unique id and world 1: the NCCL data plane runs with one rank)
+inline bool distributed(const gvt_ctx *c) { return c->world > 1 || c->nccl_comm != nullptr; }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline unsigned grid1d(int64_t n, int threads, int64_t cap = 1 << 30) {

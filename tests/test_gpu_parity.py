@@ -643,11 +643,14 @@ def test_s30_literal_search_directions(ctx, cfg, kernel):
     iterations) and check K p_k on the GPU (its Grams computed from the features) against the
     oracle (its fp64 Grams from the same features) at plain relative L2 <= 1e-5 on sampled
     outputs.  Both numbers -- the plain relative error and the S31-normalised one -- are recorded
-    (GVT_S30_RECORD=path appends a JSON line per case).  The plain gate applies where the
-    cancellation factor kappa_c = || |K| |p| || / ||K p|| lets the engine's designed backward error
-    (2^-20, the 22-bit operand splits with margin) resolve 1e-5 (kappa_c * 2^-20 <= 1e-5, i.e.
-    kappa_c <= 10.5); above it the normalised gate of S31 applies
-    and the plain number is reported, not gated."""
+    (GVT_S30_RECORD=path appends a JSON line per case; profiles/r02_s30_literal.jsonl).  The plain
+    gate is 1e-5, widened only where the unavoidable fp32 rounding of the inputs bounds it higher:
+    each side's Grams are its own (fp32 on the GPU, fp64 in the oracle), |dK| <= 2^-24 |K|, so
+    ||dK p|| / ||K p|| <= 2^-24 kappa_c with kappa_c = || |K| |p| || / ||K p|| (the cancellation
+    factor of reading S31); the gate is max(1e-5, 4 * 2^-24 * kappa_c).  Measured on a B200: every
+    C3/C4 case and C2 at k = 1 pass the plain 1e-5 (<= 1.9e-6); C2 at k = 50 / 100 (kappa_c 4.0e3 /
+    1.5e4: K p_k cancels on the rank-deficient complete-grid linear Kronecker operator) reach 4.3e-5
+    / 1.7e-4 plain, 1.1e-8 normalised."""
     w = synth.by_name(cfg)
     if kernel in HOM and w.Xt is not None:
         w = synth.union_domain(w)
@@ -675,8 +678,7 @@ def test_s30_literal_search_directions(ctx, cfg, kernel):
             with open(os.environ["GVT_S30_RECORD"], "a") as fh:
                 fh.write(json.dumps(rec) + "\n")
         assert normed <= MATVEC_TOL, rec
-        if kc * 2.0 ** -20 <= MATVEC_TOL:
-            assert plain <= MATVEC_TOL, rec
+        assert plain <= max(MATVEC_TOL, 4 * 2.0 ** -24 * kc), rec
 
 
 def test_solver_direction_contract(ctx):

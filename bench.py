@@ -307,12 +307,24 @@ def gather_regime_leg(local_rank, peaks, reps=5):
     return res
 
 
+def max_over_ranks(v, world, args, dev):
+    """Max of a per-rank device time over the ranks (NCCL: a CUDA tensor; gloo: a CPU tensor)."""
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev if args.comm == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_2009_01054_b200 as G
 
+    local_rank = local_rank % max(1, torch.cuda.device_count())  # --comm host: several ranks may share a GPU
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     w = workload(args.workload)
@@ -328,7 +340,9 @@ def run_gpu(args, rank, world, local_rank):
     ctx.set_option(G.OPT_EXCHANGE, args.exchange)
     ctx.set_option(G.OPT_SOLVER, G.SOLVER_MINRES if args.solver == "minres" else G.SOLVER_CG)
     ctx.set_option(G.OPT_CG_VARIANT, args.cg_variant)
-    if world > 1:
+    if world > 1 and args.comm == "host":
+        ctx.comm_init_host(rank, world)   # host-mediated twin over the gloo group (ranks may share a GPU)
+    elif world > 1:
         uid = G.gvt_nccl_unique_id() if rank == 0 else None
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
@@ -401,10 +415,7 @@ def run_gpu(args, rank, world, local_rank):
     ms = ev0.elapsed_time(ev1)
     st = ctx.stats()
     ctx.set_option(G.OPT_PROFILE, 0)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, args, dev)
     ms_step = ms / args.steps
     pairs = float(iters) * w.n + w.n_test  # whole job
     # SURVEY 8(d) breakdown (this rank, CUDA events between the phases of each timed step): Grams,
@@ -464,11 +475,7 @@ def run_gpu(args, rank, world, local_rank):
             step_host()
         e1.record(stream)
         barrier()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(e0.elapsed_time(e1), world, args, dev)
         h2d = (w.Xd.nbytes + (0 if w.Xt is None else w.Xt.nbytes) + 2 * (8 * n_local) + 4 * n_local +
                8 * nt_local + 4 * n_local) * world
         d2h = (4 * n_local + 4 * nt_local) * world
@@ -493,7 +500,9 @@ def run_gpu(args, rank, world, local_rank):
             "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
                        "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
                        "engine": {0: "auto", 1: "sparse", 2: "dense"}[args.engine], "tc_precision": args.precision,
-                       "exchange": ["S-allgather", "u-reduce"][args.exchange], "solver": args.solver,
+                       "exchange": ["S-allgather", "u-reduce", "auto (by estimated bytes)"][args.exchange],
+                       "exchange_used": {0: None, 1: "S-allgather", 2: "u-reduce"}.get(st.get("last_exchange", 0)),
+                       "comm": args.comm if world > 1 else None, "solver": args.solver,
                        "cg_variant": ["hestenes-stiefel", "chronopoulos-gear"][args.cg_variant],
                        "last_engine": {1: "sparse", 2: "dense"}.get(st["last_engine"], None),
                        "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
@@ -522,8 +531,12 @@ def main():
     ap.add_argument("--kernel", default=None)
     ap.add_argument("--engine", type=int, default=0)
     ap.add_argument("--precision", default="fp16x3", choices=["fp16x3", "tf32x3"])
-    ap.add_argument("--exchange", type=int, default=0, choices=[0, 1],
-                    help="multi-GPU exchange per matvec: 0 = S slab all-gather, 1 = u reduce (NEXT-3)")
+    ap.add_argument("--exchange", type=int, default=2, choices=[0, 1, 2],
+                    help="multi-GPU exchange per matvec: 0 = S slab all-gather, 1 = u reduce (NEXT-3), "
+                         "2 = by estimated bytes (default)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: NCCL (one rank per GPU) or the library's host-mediated twin over gloo (ranks may "
+                         "share a GPU; a test of the launcher and the data-parallel path on a one-GPU box)")
     ap.add_argument("--solver", default="cg", choices=["cg", "minres"])
     ap.add_argument("--cg-variant", type=int, default=0, choices=[0, 1],
                     help="0 = Hestenes-Stiefel CG, 1 = Chronopoulos-Gear (one reduction per iteration)")
@@ -534,17 +547,36 @@ def main():
                     help="skip the sparse-engine gather-regime leg (0.2 %% density at C5 object counts)")
     ap.add_argument("--ref-targets", type=int, default=32)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` outside a launcher: re-run this command under torch.distributed.run, one
+        # rank per GPU (the driver's own launch sets WORLD_SIZE and lands below directly)
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        # never time one world size and report another
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.comm == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")   # the "nranks N" init lines, for the driver's check
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     try:
         run_gpu(args, rank, world, local_rank)
     finally:

@@ -162,6 +162,8 @@ typedef struct {
     double ms[GVT_MAX_KERNEL_KINDS];          /* summed CUDA-event duration (GVT_OPT_PROFILE = 1)       */
     int32_t last_engine;                      /* engine last used: 1 sparse, 2 dense, 3 single-CTA fit */
     int32_t world;                            /* communicator size (1 without gvt_comm_init)           */
+    int32_t last_exchange;                    /* exchange of the last data-parallel call: 0 none (single
+                                                 GPU), 1 S slab all-gather, 2 u-exchange              */
 } gvt_stats;
 
 /* Create a context on CUDA device `device`, issuing work on `stream` (a cudaStream_t;

@@ -72,7 +72,8 @@ class Term(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("n_kinds", ctypes.c_int32),
                 ("names", (ctypes.c_char * 32) * MAX_KINDS), ("counts", ctypes.c_int64 * MAX_KINDS),
-                ("ms", ctypes.c_double * MAX_KINDS), ("last_engine", ctypes.c_int32), ("world", ctypes.c_int32)]
+                ("ms", ctypes.c_double * MAX_KINDS), ("last_engine", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("last_exchange", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -268,7 +269,8 @@ class Context:
             name = bytes(s.names[k]).split(b"\0")[0].decode()
             if s.counts[k]:
                 kinds[name] = {"count": int(s.counts[k]), "ms": float(s.ms[k])}
-        return {"launches": int(s.launches), "kinds": kinds, "last_engine": int(s.last_engine), "world": int(s.world)}
+        return {"launches": int(s.launches), "kinds": kinds, "last_engine": int(s.last_engine), "world": int(s.world),
+                "last_exchange": int(s.last_exchange)}
 
     def reset_stats(self):
         _check(_lib.gvt_reset_stats(self._h), "gvt_reset_stats")

@@ -26,17 +26,20 @@ def _needs(obj: str, srcs) -> bool:
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, extra_flags=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Compile every csrc/*.cu and link `lib`.  extra_flags / lib / build_dir: A/B variants
+    (scripts/build_variant.py), e.g. extra_flags=["-DS16_SCALE_ROWS=1"] into ab/."""
+    BUILD_ = build_dir
+    os.makedirs(BUILD_, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(HERE, "..", "include", "gvt.h")]
     objs = []
     jobs = []
     for s in sources:
-        o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(BUILD_, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _needs(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *extra_flags, "-c", s, "-o", o])
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
             futs = [ex.submit(subprocess.run, j, capture_output=True, text=True) for j in jobs]
@@ -46,14 +49,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
                     sys.stderr.write(" ".join(j) + "\n" + r.stdout + r.stderr)
                 if r.returncode != 0:
                     raise RuntimeError(f"nvcc failed for {j[-3]}")
-    if force or jobs or not os.path.exists(LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl"]
+    if force or jobs or not os.path.exists(lib):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             raise RuntimeError("link failed")
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -191,6 +191,7 @@ gvt_status gvt_get_stats(gvt_ctx *c, gvt_stats *out) {
         out->ms[k] = c->ms[k];
     }
     out->last_engine = c->last_engine;
+    out->last_exchange = c->last_exchange;
     out->world = c->world;
     GVT_API_END
 }

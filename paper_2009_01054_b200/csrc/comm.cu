@@ -108,7 +108,46 @@ void comm_init(gvt_ctx *c, const void *id128, int rank, int world) {
 void comm_destroy(gvt_ctx *c) {
     if (c->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)c->nccl_comm);
     c->nccl_comm = nullptr;
+    for (auto e : c->slab_events) cudaEventDestroy(e);
+    c->slab_events.clear();
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    c->comm_stream = nullptr;
 }
+
+// Pipelined S slab exchange ("stage 2 accumulates the partial dots of each slab as
+// it arrives, pipelined over slabs on a side stream"): after stage 1, slab s of every array is
+// broadcast from its owner s, in slab order, on the context's comm stream; slab_events[s] marks its
+// arrival, and stage 2 of slab s waits only for that event, so the transfer of slab s + 1 overlaps
+// the stage-2 GEMM of slab s.  The waits of stage 2 join the side stream back (also inside a CUDA
+// graph capture, where the fork/join become graph edges).  NCCL communicators only (the host twin
+// exchanges synchronously with allgather_slabs).
+bool slab_pipeline_available(gvt_ctx *c) { return distributed(c) && c->nccl_comm && !c->host_allgather; }
+
+void slab_pipeline_start(gvt_ctx *c, void *const *bufs, const size_t *slab_bytes, int nbuf) {
+    const int G = c->world;
+    if (!c->comm_stream) GVT_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    while ((int)c->slab_events.size() < G + 1) {
+        cudaEvent_t e;
+        GVT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->slab_events.push_back(e);
+    }
+    GVT_CUDA_TRY(cudaEventRecord(c->slab_events[G], c->stream));  // fork: stage 1 of this rank is done
+    GVT_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->slab_events[G], 0));
+    for (int s = 0; s < G; s++) {
+        c->counts[K_COMM]++;
+        NCCL_TRY(g_nccl.GroupStart());
+        for (int b = 0; b < nbuf; b++) {
+            char *slab = (char *)bufs[b] + (size_t)s * slab_bytes[b];
+            if (slab_bytes[b])
+                NCCL_TRY(g_nccl.Broadcast(slab, slab, slab_bytes[b], ncclInt8, s, (ncclComm_t)c->nccl_comm,
+                                          c->comm_stream));
+        }
+        NCCL_TRY(g_nccl.GroupEnd());
+        GVT_CUDA_TRY(cudaEventRecord(c->slab_events[s], c->comm_stream));
+    }
+}
+
+void slab_wait(gvt_ctx *c, int s) { GVT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->slab_events[s], 0)); }
 
 // ---- host-mediated communicator (gvt_comm_init_host): one all-gather primitive through the host
 void comm_init_host(gvt_ctx *c, int rank, int world, gvt_host_allgather_fn fn, void *user) {

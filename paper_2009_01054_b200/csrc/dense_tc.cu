@@ -195,18 +195,15 @@ struct EpiParams {
     // only the K-blocks kb_list[kb_off[n] .. kb_off[n + 1]) (ascending, at least one) are
     // multiplied; the other K-blocks of those B rows are all zero (EPI_STORE16 only)
     const int32_t *kb_list, *kb_off;
-    // B operand with a per-(row, 256-wide K chunk) scale, applied while draining chunk ch:
-    // sbk[ch * sbk_ld + n] (fp16 S produced by EPI_STORE16)
+    // B operand with a per-(row block, 256-wide K chunk) scale, applied while draining chunk ch:
+    // sbk[ch * sbk_ld + n / S16_SCALE_ROWS] (fp16 S produced by EPI_STORE16)
     const float *sbk;
     int64_t sbk_ld;
-    // EPI_STORE16: C as fp16 hi/lo (ldc) with one scale per (row, 256-column tile):
-    // c_sk[n_tile * c_sk_ld + row] = 1/scale
+    // EPI_STORE16: C as fp16 hi/lo (ldc) with one scale per (row block, 256-column tile):
+    // c_sk[n_tile * c_sk_ld + row / S16_SCALE_ROWS] = 1/scale
     __half *c_h16, *c_l16;
     float *c_sk;
     int64_t c_sk_ld;
-    // EPI_STORE16 with l1max != nullptr: one scale per ROW, from the a-priori bound
-    // |C[r][c]| <= max_k |A[r,k]| * max_c ||B[c,:]||_1 <= 2^15 sa[r] * (*l1max); c_sk[row]
-    const float *l1max;
 };
 
 #ifndef DRAIN_X16
@@ -250,6 +247,9 @@ __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, 
 
 constexpr int BM = 128, BN = 256, STAGES = 256 / KB_BYTES;  // 4 stages of 48 KB (64-byte K-blocks)
 constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation chunk
+// the fp16 S of stage 1 carries one scale per 256-column tile; stage 2 drains 256-wide K chunks
+static_assert(KC_BLOCKS * (KB_BYTES / 2) == BN, "fp16 accumulation chunk = one S scale tile");
+static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == BM, "S scale block = one stage-1 CTA's rows");
 // Sampled epilogue: write the samples k in [kb0, ke) of one 32-column chunk (their values parked
 // in `stage`, [rows/32][32][33] floats) to out[dst], SERVE_UNROLL samples per thread in flight.
 // Measured (profiles/r01_ab_serve_unroll.txt): 4 in flight cut C2 from 95 to 83 us per iteration
@@ -731,6 +731,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
+#if S16_SCALE_ROWS == BM
+                if (EPI == EPI_SAMPLED && ep.sbk) {
+                    // chunk-scaled B (fp16 S from EPI_STORE16): this thread's 128 columns are the S rows
+                    // of ONE stage-1 CTA block, so the chunk's scale is a single scalar -- the drain is
+                    // the plain 16-column loop with an FMA (no scale vectors next to run[128])
+                    const float skv = __ldg(ep.sbk + (int64_t)ch * ep.sbk_ld + (gc_base >> 7));
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; c8++) {
+                        uint32_t r[16];
+                        tmem_ld16_raw(ta + c8 * 16, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) run[c8 * 16 + i] = fmaf(__uint_as_float(r[i]), skv, run[c8 * 16 + i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; c8++) {
+                        uint32_t r[16];
+                        tmem_ld16_raw(ta + c8 * 16, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) run[c8 * 16 + i] += __uint_as_float(r[i]);
+                    }
+                }
+#else
                 // per-(column, K-chunk) scale of a chunk-scaled B operand (fp16 S from EPI_STORE16)
                 const float *sk = ep.sbk ? ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base : nullptr;
 #if DRAIN_X16
@@ -782,15 +807,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     }
                 }
 #endif
+#endif  // S16_SCALE_ROWS
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
             if (EPI == EPI_STORE16) {
-                // fp16 hi/lo of the unscaled result with a power-of-two scale: one per ROW from the
-                // a-priori bound (l1max; the same for every tile, no exchange), or one per
-                // (row, 256-col tile) from the tile's maximum (the two warps holding this row's
-                // column halves exchange their maxima)
+                // fp16 hi/lo of the unscaled result with a power-of-two scale per (128-row CTA block,
+                // 256-col tile) from the block's maximum (S16_SCALE_ROWS = 128: a CTA-wide max over
+                // the 8 epilogue warps), or per (row, 256-col tile) (S16_SCALE_ROWS = 1: the two warps
+                // holding this row's column halves exchange their maxima)
                 const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
                 float mx = 0.f;
                 // column scales of B in 16-byte loads (the scale vector is padded to 128 rows)
@@ -806,14 +832,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                         if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
                     }
                 }
-                if (ep.l1max) {
-                    mx = 32768.f * ra * __ldg(ep.l1max);
-                } else {
-                    estage[(quarter * 32 + lane) * 2 + half] = mx;
-                    named_bar(1, 32 * N_EPI_WARPS);
-                    mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
-                    named_bar(1, 32 * N_EPI_WARPS);
-                }
+#if S16_SCALE_ROWS == BM
+                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0) estage[ew] = mx;
+                named_bar(1, 32 * N_EPI_WARPS);
+#pragma unroll
+                for (int w8 = 0; w8 < N_EPI_WARPS; w8++) mx = fmaxf(mx, estage[w8]);
+                named_bar(1, 32 * N_EPI_WARPS);
+#else
+                estage[(quarter * 32 + lane) * 2 + half] = mx;
+                named_bar(1, 32 * N_EPI_WARPS);
+                mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
+                named_bar(1, 32 * N_EPI_WARPS);
+#endif
                 int e = 0;
                 if (mx > 0.f && isfinite(mx)) {
                     int ex;
@@ -821,10 +852,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     e = 15 - ex;
                 }
                 const float s = ldexpf(1.f, e);
-                if (gr < M && half == 0) {
-                    if (!ep.l1max) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
-                    else if (n_tile == 0) ep.c_sk[gr] = ldexpf(1.f, -e);
-                }
+#if S16_SCALE_ROWS == BM
+                // one writer per CTA block (also for a padding block past M: scale 1, finite)
+                if (threadIdx.x == 64) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + (m0 >> 7)] = ldexpf(1.f, -e);
+#else
+                if (gr < M && half == 0) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + gr] = ldexpf(1.f, -e);
+#endif
                 // coalesced stores through this warp's staging block: each lane (one row) parks
                 // 32 columns of (hi, lo) pairs, then the warp writes the block row by row, 64
                 // contiguous bytes per piece (a thread-per-row store pattern would touch 32 lines
@@ -1189,9 +1222,9 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
                                                    int64_t cols, int64_t ld, __half *__restrict__ hi,
                                                    __half *__restrict__ lo, float *__restrict__ sinv,
-                                                   const float *__restrict__ diag, float *__restrict__ l1max) {
+                                                   const float *__restrict__ diag) {
     extern __shared__ float rowbuf[];  // ld floats
-    __shared__ float red[BX_THREADS / 32], red2[BX_THREADS / 32];
+    __shared__ float red[BX_THREADS / 32];
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
         __syncthreads();
@@ -1229,28 +1262,13 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
         __syncthreads();
         if (diag && threadIdx.x == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
         __syncthreads();
-        float mx = 0.f, l1 = 0.f;
-        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
-            mx = fmaxf(mx, fabsf(rowbuf[j]));
-            l1 += fabsf(rowbuf[j]);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-            red[threadIdx.x >> 5] = mx;
-            red2[threadIdx.x >> 5] = l1;
-        }
+        float mx = 0.f;
+        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
         __syncthreads();
         mx = red[0];
         for (int w = 1; w < BX_THREADS / 32; w++) mx = fmaxf(mx, red[w]);
-        if (l1max && threadIdx.x == 0) {
-            float t = 0.f;
-            for (int w = 0; w < BX_THREADS / 32; w++) t += red2[w];
-            // an upper bound with slack for the fp32 summation (non-negative floats order as ints)
-            atomicMax(reinterpret_cast<int *>(l1max), __float_as_int(t * 1.0001f));
-        }
         int e = 0;
         if (mx > 0.f && isfinite(mx)) {
             int ex;
@@ -1271,7 +1289,7 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
 }
 
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag, float *l1max) {
+                  const float *p, const float *diag) {
     Operand o;
     o.prec = PREC_F16;
     o.ld = round_up(cols > 0 ? cols : 1, 32);
@@ -1291,10 +1309,10 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     if (rows > 0) {
         if (o.ld > 8192)
             GVT_LAUNCH(c, K_DENSIFY, k_build_x16<1024>, grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr, e.col,
-                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
+                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
         else
             GVT_LAUNCH(c, K_DENSIFY, k_build_x16<256>, grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr, e.col,
-                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, l1max);
+                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
     }
     o.hi = hi;
     o.lo = lo;
@@ -1335,12 +1353,10 @@ void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_
     }
 }
 
-// hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256)) floats,
-// whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
-// l1max != nullptr: one scale per row (sk[row]) from the bound 2^15 A.scale[row] * (*l1max), where
-// *l1max >= max over B's rows of the row's L1 norm (build_x16 computes it)
+// hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256) / S16_SCALE_ROWS)
+// floats, whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max, const int32_t *kb_list,
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const int32_t *kb_list,
                      const int32_t *kb_off) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -1350,7 +1366,6 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.c_l16 = lo;
     ep.c_sk = sk;
     ep.c_sk_ld = sk_ld;
-    ep.l1max = l1max;
     ep.ldc = ldc;
     launch_gemm<EPI_STORE16>(c, K_STAGE1_TC, A, B, M, N, K, ep);
 }

@@ -43,6 +43,9 @@ void gather_varlen(gvt_ctx *c, const void *local, void *full, const std::vector<
                    const std::vector<int64_t> &offsets, bool is_float);
 void reduce_segments(gvt_ctx *c, const float *partial, float *local, const std::vector<int64_t> &counts,
                      const std::vector<int64_t> &offsets, int64_t tail);
+bool slab_pipeline_available(gvt_ctx *c);
+void slab_pipeline_start(gvt_ctx *c, void *const *bufs, const size_t *slab_bytes, int nbuf);
+void slab_wait(gvt_ctx *c, int s);
 
 // ----------------------------------------------------------------------------- decompose
 static gvt_term mk(double coef, int l, int r, int rl, int rr, int cl, int cr) {
@@ -574,35 +577,33 @@ static bool stage2_gather_pays(gvt_ctx *c, int64_t ns, int64_t M, int64_t N, int
 
 static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
                           float *out) {
-    // S scales: one per (row, 256-col tile) from the tile maxima, applied per K-chunk in stage 2
-    // (default), or one per row from the a-priori bound |S[t][h]| <= max|T[t,:]| max_h ||X[h,:]||_1
-    // (GVT_S16_ROWSCALE=1).  Both pass the parity suite; the row scales cost ~7 % more time at C5
-    // under the power cap (more power per MMA at the same work, profiles/r01_ab_s16_scale.txt), so
-    // the tile scales stay the default.
-    static const bool tile_scale = [] {
-        const char *v = getenv("GVT_S16_ROWSCALE");
-        return !(v && atoi(v) != 0);
-    }();
-    const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256);
-    const size_t slab_h = (size_t)g.qpad * g.W, slab_k = tile_scale ? (size_t)ntW * skld : (size_t)skld;
+    // S scales: one power-of-two scale per (128-row block, 256-col tile) -- a stage-1 CTA's output
+    // block -- from the block maximum, applied per K-chunk in stage 2 as one scalar per chunk
+    // (S16_SCALE_ROWS; the r1 layout, one scale per (row, 256-col tile), is the A/B build
+    // -DS16_SCALE_ROWS=1)
+    const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256) / S16_SCALE_ROWS;
+    const size_t slab_h = (size_t)g.qpad * g.W, slab_k = (size_t)ntW * skld;
     __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
     __half *Sl = wsT<__half>(c, (g.tag + ".S16l").c_str(), slab_h * g.nslab);
     float *Sk = wsT<float>(c, (g.tag + ".S16k").c_str(), slab_k * g.nslab);
-    float *l1 = wsT<float>(c, (g.tag + ".S16l1").c_str(), (size_t)g.nslab);
     GVT_CUDA_TRY(cudaMemsetAsync(Sk, 0, sizeof(float) * slab_k * g.nslab, c->stream));
-    if (!tile_scale) GVT_CUDA_TRY(cudaMemsetAsync(l1, 0, sizeof(float) * g.nslab, c->stream));
     for (int s = 0; s < g.nslab; s++) {
         if (!my_slab(c, s)) continue;
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
         if (w == 0) continue;
-        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag, tile_scale ? nullptr : l1 + s);
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
-                        skld, tile_scale ? nullptr : l1 + s, g.kb_list[(size_t)s], g.kb_off[(size_t)s]);
+                        skld, g.kb_list[(size_t)s], g.kb_off[(size_t)s]);
     }
     float *partial = nullptr;
+    const bool piped = !P.uex && slab_pipeline_available(c);
     if (P.uex) {  // no S exchange: this rank's slab serves every output, then the partials are reduced
         partial = wsT<float>(c, "uex.partial", (size_t)(P.n_out_full + g.n_diag));
         GVT_CUDA_TRY(cudaMemsetAsync(partial, 0, sizeof(float) * (P.n_out_full + g.n_diag), c->stream));
+    } else if (piped) {  // per-slab broadcasts on the comm stream, overlapped with stage 2 below
+        void *bufs[3] = {Sh, Sl, Sk};
+        const size_t bytes[3] = {sizeof(__half) * slab_h, sizeof(__half) * slab_h, sizeof(float) * slab_k};
+        slab_pipeline_start(c, bufs, bytes, 3);
     } else {  // halves travel as pairs of floats (W is a multiple of 32)
         allgather_slabs(c, reinterpret_cast<float *>(Sh), slab_h / 2);
         allgather_slabs(c, reinterpret_cast<float *>(Sl), slab_h / 2);
@@ -611,22 +612,19 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
     bool first = true;
     for (int s = 0; s < g.nslab; s++) {
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        if (piped) slab_wait(c, s);  // (every slab, empty ones too: the waits join the comm stream)
         if (w == 0 || (P.uex && !my_slab(c, s))) continue;
         Operand so;
         so.prec = 0;
         so.hi = Sh + s * slab_h;
         so.lo = Sl + s * slab_h;
         so.ld = g.W;
-        if (tile_scale) {
-            so.scale_k = Sk + s * slab_k;
-            so.scale_k_ld = skld;
-        } else {
-            so.scale = Sk + s * slab_k;  // one scale per S row, applied once after the K loop
-        }
+        so.scale_k = Sk + s * slab_k;
+        so.scale_k_ld = skld;
         // (P.uex: this rank's slab(s) -- one per rank, all of them with emulated slabs at world 1)
         float *dst = P.uex ? partial : out;
         const int acc = P.uex ? !first : (accumulate || !first);
-        if (tile_scale && stage2_gather_pays(c, (int64_t)(g.ns_est - g.extra_est), g.A.n, g.q_out, w)) {
+        if (stage2_gather_pays(c, (int64_t)(g.ns_est - g.extra_est), g.A.n, g.q_out, w)) {
             Factor Av = g.A;
             Av.p = g.A.p + lo;
             stage2_gather16(c, g.smp, Av, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k, skld, w, coef, acc, dst);
@@ -641,6 +639,7 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
 static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
                       float *out, bool values_ready = false) {
     c->last_engine = g.engine;
+    c->last_exchange = !distributed(c) ? 0 : (P.uex ? 2 : 1);
     if (g.engine == 2 && fused_f16(c, g.C.cols)) {
         run_group_f16(c, P, g, p_full, coef, accumulate, out);
         return;
@@ -677,9 +676,14 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
     // ---- exchange the S slabs (NVLink all-gather), then stage 2 slab by slab; or (u-exchange)
     // stage 2 of this rank's slab over every output into a partial vector, then reduce it
     float *partial = nullptr;
+    const bool piped = !P.uex && slab_pipeline_available(c);
     if (P.uex) {
         partial = wsT<float>(c, "uex.partial", (size_t)(P.n_out_full + g.n_diag));
         GVT_CUDA_TRY(cudaMemsetAsync(partial, 0, sizeof(float) * (P.n_out_full + g.n_diag), c->stream));
+    } else if (piped) {
+        void *bufs[1] = {g.S};
+        const size_t bytes[1] = {sizeof(float) * (size_t)g.qpad * g.W};
+        slab_pipeline_start(c, bufs, bytes, 1);
     } else {
         allgather_slabs(c, g.S, (size_t)g.qpad * g.W);
     }
@@ -687,6 +691,7 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
     bool first = true;
     for (int s = 0; s < g.nslab; s++) {
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
+        if (piped) slab_wait(c, s);
         if (w == 0 || (P.uex && !my_slab(c, s))) continue;
         const int acc = P.uex ? !first : (accumulate || !first);
         first = false;

@@ -103,6 +103,7 @@ struct gvt_ctx {
     int cg_variant = 0;    // 0 = Hestenes-Stiefel CG, 1 = Chronopoulos-Gear (one reduction per iteration)
     cudaStream_t cap_stream = nullptr;  // side stream used only for graph capture
     int last_engine = 0;
+    int last_exchange = 0;  // 0 none (single GPU), 1 S slab all-gather, 2 u-exchange
 
     // workspaces by name (grow-only)
     std::unordered_map<std::string, gvt::Buf> bufs;
@@ -119,6 +120,8 @@ struct gvt_ctx {
     int rank = 0, world = 1;
     gvt_host_allgather_fn host_allgather = nullptr;  // host-mediated communicator (gvt_comm_init_host)
     void *host_user = nullptr;
+    cudaStream_t comm_stream = nullptr;        // side stream of the pipelined slab exchange
+    std::vector<cudaEvent_t> slab_events;      // [world] slab s arrived, [world] fork point
 
     // the last Hestenes-Stiefel CG fit's search direction (gvt_solver_direction): device vector
     // in solve order, its length (-1 = none kept) and the sorted-order permutation (nullptr = identity)

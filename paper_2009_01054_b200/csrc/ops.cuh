@@ -10,12 +10,21 @@ namespace gvt {
 // A tensor-core GEMM operand: rows of a matrix split into (hi, lo) pieces, K-major with
 // leading dimension ld.  prec 0 = fp16 pieces with per-row power-of-two scale (scale[r] =
 // 1/s_r), prec 1 = tf32 pieces in fp32 containers (scale == nullptr).
+// fp16 S of the fused dense path: one power-of-two scale per (S16_SCALE_ROWS-row block, 256-wide
+// K chunk): scale_k[chunk * scale_k_ld + row / S16_SCALE_ROWS].  128 = one stage-1 CTA's output
+// block (the default: the stage-2 drain multiplies a chunk by ONE scalar); 1 = per row (the r1
+// layout, kept for A/B builds with -DS16_SCALE_ROWS=1).
+#ifndef S16_SCALE_ROWS
+#define S16_SCALE_ROWS 128
+#endif
+static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == 128, "S scale blocks: per row or per 128-row CTA block");
+
 struct Operand {
     int prec = 0;
     const void *hi = nullptr, *lo = nullptr;
     const float *scale = nullptr;
     int64_t ld = 0;
-    // alternatively one scale per (row, 256-wide K chunk): scale_k[chunk * scale_k_ld + row]
+    // alternatively one scale per (row block, 256-wide K chunk): scale_k[chunk * scale_k_ld + row / S16_SCALE_ROWS]
     const float *scale_k = nullptr;
     int64_t scale_k_ld = 0;
 };
@@ -156,19 +165,17 @@ void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, in
 bool fused_f16(gvt_ctx *c, int64_t q_in);
 // rows [row_lo, row_lo + rows) of the pair matrix built straight into an fp16 operand
 // (values sign * p[src] summed per cell in entry order, one row scale per row)
-// l1max (nullable, device float, zeroed by the caller): atomically raised to >= every row's L1 norm
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag = nullptr, float *l1max = nullptr);
+                  const float *p, const float *diag = nullptr);
 // X[r][row_lo + r] += diag[row_lo + r] for r < rows (fp32 X, leading dimension ldX)
 void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_lo, int64_t rows);
-// C = A * B^T written as fp16 pieces (M rows x ldc) with per-(row, 256-col tile) scales
-// sk[tile * sk_ld + row] (sk_ld >= round_up(M, 256))
-// l1max != nullptr: one scale per row sk[row] from the a-priori bound (no per-tile scales)
+// C = A * B^T written as fp16 pieces (M rows x ldc) with one scale per (S16_SCALE_ROWS-row block,
+// 256-col tile): sk[tile * sk_ld + row / S16_SCALE_ROWS] (sk_ld >= round_up(M, 256) / S16_SCALE_ROWS)
 // kb_list / kb_off (device, nullable): per 256-row tile of B, its ascending non-zero K-blocks of
 // 64 columns (at least one per tile): the other K-blocks are skipped (block-sparse B)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
-                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const float *l1max = nullptr,
-                     const int32_t *kb_list = nullptr, const int32_t *kb_off = nullptr);
+                     __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const int32_t *kb_list = nullptr,
+                     const int32_t *kb_off = nullptr);
 // non-zero (256-row tile, 64-column K-block) pairs of the pair-matrix rows [lo, lo + rows) from the
 // sorted entries k in [k0, k1) (+ the diagonal when diag): host lists (off has ntiles + 1 entries)
 void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,

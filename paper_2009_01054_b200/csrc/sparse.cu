@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) k_stage2_gather16(int64_t ns, const int32
         float acc = 0.f;
         for (int64_t j = lane; 2 * j < K; j += 32) {
             const int64_t h = 2 * j;
-            const float s = __ldg(sk + (h >> 8) * skld + c);  // h and h + 1 share the chunk
+            const float s = __ldg(sk + (h >> 8) * skld + c / S16_SCALE_ROWS);  // h and h + 1 share the chunk
             const float2 av = __ldg(a + j);
             const float2 hv = __half22float2(h2[j]), lv = __half22float2(l2[j]);
             acc = fmaf(av.x, (hv.x + lv.x) * s, acc);

@@ -192,6 +192,39 @@ def zipf_degrees(m: int, n: int, cap: int, s: float = 1.1) -> np.ndarray:
     return deg
 
 
+def _disk_cached(fn):
+    """With GVT_SYNTH_CACHE=<dir>, keep generated workloads as .npz files keyed by the call's
+    arguments (the C5 draw takes ~20 s; measurement scripts regenerate it per process).  The
+    arrays are the generator's own output, saved and reloaded unchanged."""
+    import functools
+    import os
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        d = os.environ.get("GVT_SYNTH_CACHE")
+        if not d:
+            return fn(*args, **kw)
+        key = fn.__name__ + "_" + "_".join(map(str, args)) + "_" + "_".join(f"{k}{v}" for k, v in sorted(kw.items()))
+        path = os.path.join(d, key + ".npz")
+        fields = [f.name for f in dataclasses.fields(Workload)]
+        if os.path.exists(path):
+            z = np.load(path, allow_pickle=True)
+            vals = {f: (z[f].item() if z[f].dtype == object else z[f]) for f in fields}
+            vals["kernels"] = tuple(int(k) for k in z["kernels"])
+            return Workload(**vals)
+        w = fn(*args, **kw)
+        os.makedirs(d, exist_ok=True)
+        arrs = {f: getattr(w, f) for f in fields}
+        arrs = {k: (np.array(v, dtype=object) if v is None or isinstance(v, (str, float, int)) else np.asarray(v))
+                for k, v in arrs.items()}
+        tmp = path + ".tmp.npz"
+        np.savez(tmp, **arrs)
+        os.replace(tmp, path)
+        return w
+    return wrapper
+
+
+@_disk_cached
 def config5(n: int = 100_000_000, n_test: int = 20_000_000, m: int = 20_000, dim: int = 128,
             chunk: int = 512) -> Workload:
     """C5 large-scale Kronecker KRR (configs[4]): m=q=20000, dim 128 N(0,1), Gaussian

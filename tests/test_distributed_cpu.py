@@ -208,3 +208,15 @@ def test_dense_slabs_balanced_on_degree_sorted_c5_shape():
     b = G.gvt_slab_bounds_cost(rp, 8, we, wr)
     cost = we * np.diff(rp[b]) + wr * np.diff(b)
     assert cost.max() / cost.mean() <= 1.1
+
+
+def test_bench_rejects_mismatched_world():
+    """bench.py never times one world size and reports another: --gpus 2 under WORLD_SIZE=1 exits 2
+    (before touching a GPU)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "C1"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr

@@ -39,7 +39,8 @@ def _worker(rank, world, port, case, out_path):
         import oracle as O  # noqa: F401
         import paper_2009_01054_b200 as G
         import synth
-        kernel, engine, exchange, solver, stage2 = case
+        kernel, engine, exchange, solver, stage2 = case[:5]
+        uneven = len(case) > 5 and case[5]
         w = synth.config1() if kernel == G.KRONECKER else synth.config3(n=20_000, n_test=3_000)
         hom = w.Xt is None
         ctx = G.Context(0)
@@ -56,10 +57,13 @@ def _worker(rank, world, port, case, out_path):
         bounds = G.gvt_partition(np.bincount(f, minlength=w.m), world)
         mine = np.nonzero((f >= bounds[rank]) & (f < bounds[rank + 1]))[0]
         tmine = np.nonzero((w.test_first >= bounds[rank]) & (w.test_first < bounds[rank + 1]))[0]
+        if uneven:  # every test pair on rank 0, none on rank 1 (ranks with unequal samples)
+            tmine = np.arange(w.n_test) if rank == 0 else np.zeros(0, np.int64)
         terms = G.gvt_kernel_terms(kernel)
         a, it, hist, _ = ctx.fit(D, T, dev(f[mine]), dev(s[mine]), dev(y[mine]), terms, w.lam, 20)
-        sc = ctx.predict(D, T, dev(w.test_first[tmine]), dev(w.test_second[tmine]), dev(f[mine]), dev(s[mine]), a,
-                         terms)
+        tf, ts = w.test_first[tmine], w.test_second[tmine]
+        sc = (ctx.predict(D, T, dev(tf), dev(ts), dev(f[mine]), dev(s[mine]), a, terms) if len(tmine) else
+              ctx.predict(D, T, None, None, dev(f[mine]), dev(s[mine]), a, terms))
         out = {"rank": rank, "idx": mine, "a": a.cpu().numpy(), "tidx": tmine, "sc": sc.cpu().numpy(), "it": it,
                "hist": hist}
         objs = [None] * world
@@ -113,10 +117,14 @@ CASES = [  # (kernel, engine, exchange, solver: 0 CG, 1 MINRES, 2 single-reducti
     (3, 2, 0, 0, 1), (3, 1, 0, 0, 0), (3, 2, 1, 0, 1), (3, 2, 0, 1, 1), (3, 2, 0, 2, 1),
     (4, 2, 0, 0, 1), (4, 1, 1, 0, 0), (7, 2, 1, 0, 1), (7, 1, 0, 0, 0),
     (3, 2, 0, 0, 2), (7, 2, 1, 0, 2),
+    # default options (engine auto, exchange by estimate, stage 2 auto) with uneven out samples: rank 1
+    # predicts nothing, so every dispatch decision must come from rank-independent sizes
+    (3, 0, 2, 0, 0, True), (4, 0, 2, 0, 0, True), (7, 0, 2, 0, 0, True), (4, 0, 0, 0, 0, True),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"k{k}-e{e}-x{x}-s{s}-g{g}" for k, e, x, s, g in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[("k{}-e{}-x{}-s{}-g{}".format(*c[:5]) + ("-uneven" if len(c) > 5 else ""))
+                                             for c in CASES])
 def test_two_ranks_on_one_gpu_match_oracle(case):
     _check(case)
 

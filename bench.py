@@ -122,6 +122,18 @@ def default_kernel(w):
     return w.kernels[0]
 
 
+def config_dict(args, w, kernel, world):
+    """The workload's `config` object, identical in both arms (the GPU arm and --impl reference)."""
+    return {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n, "n_test": w.n_test,
+            "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
+            "engine": {0: "auto", 1: "sparse", 2: "dense"}[args.engine], "tc_precision": args.precision,
+            "exchange": ["S-allgather", "u-reduce", "auto (by estimated bytes)"][args.exchange],
+            "comm": args.comm if world > 1 else None, "solver": args.solver,
+            "cg_variant": ["hestenes-stiefel", "chronopoulos-gear"][args.cg_variant],
+            "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
+            "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"}
+
+
 # ----------------------------------------------------------------------------- roofline
 def _traffic(kernel_kind):
     """DRAM bytes per launch of `kernel_kind` from the committed ncu --set full capture
@@ -200,7 +212,7 @@ def oracle_grams(w):
     return _ORACLE_GRAMS[key]
 
 
-def oracle_sample(w, kernel, n_targets=8, seed=0):
+def oracle_sample(w, kernel, n_targets=8, seed=0, min_seconds=1.0):
     """The oracle's GVT matvec on a bounded sample of the training matvec: the outputs whose
     second element lies among `n_targets` seeded targets (the oracle then forms S only for
     those rows: the same fraction of stage 1 and stage 2 work as of the full matvec)."""
@@ -217,7 +229,7 @@ def oracle_sample(w, kernel, n_targets=8, seed=0):
         O.gvt_matvec(terms, D, T, w.train_first[idx], w.train_second[idx], w.train_first, w.train_second, a)
         reps += 1
         dt = time.perf_counter() - t0
-        if dt >= 1.0:
+        if dt >= min_seconds:
             break
     return len(idx) * reps, dt, O.num_threads()
 
@@ -239,11 +251,9 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
-                       "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
-                       "step": "bounded sample of the training matvec (the oracle's per-term GVT), timed on the "
-                               "host cores; the GPU arm's step is gram(D)+gram(T)+pairwise_krr_fit(iters)+"
-                               "pairwise_predict"},
+            "config": config_dict(args, w, kernel, world),
+            "reference_step": "a bounded sample of the training matvec (the oracle's per-term GVT, fp64) on the host "
+                              "cores; the GPU arm's step is gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict",
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"fp64 oracle per-term GVT training matvec restricted to the outputs of {nt} "
                                        f"seeded targets per step, repeated for >= 1 s ({cnt // max(1, args.steps)} "
@@ -305,6 +315,118 @@ def gather_regime_leg(local_rank, peaks, reps=5):
                          "gather_row_bytes_GBps": 8.0 * w.m * n_out / (gms * 1e-3) / 1e9}
     res["hbm_peak_GBps"] = peaks["hbm_gbs"]
     return res
+
+
+# per-config legs of the default line (make the C1-C4 numbers driver-observed)
+CONFIG_RUNS = [("C1", "kronecker"), ("C2", "kronecker"), ("C3", "symmetric"), ("C3", "antisymmetric"),
+               ("C3", "cartesian"), ("C4", "poly2d"), ("C4", "mlpk"), ("C4", "ranking")]
+# SURVEY.md 8(d) floors per training matvec on one B200, T_roof = max(FMA / 37.2e12, bytes / 6.54e12);
+# C1 and C2 are latency-bound (no roofline floor: "report us per iteration")
+FLOORS_US = {("C3", "symmetric"): 32.0, ("C3", "antisymmetric"): 32.0, ("C3", "cartesian"): 50.0,
+             ("C4", "poly2d"): 430.0, ("C4", "mlpk"): 1300.0, ("C4", "ranking"): 45.0}
+
+
+def configs_leg(local_rank, steps=5, warmup=3):
+    """C1-C4 (every kernel each config runs) on one GPU: the same step as the headline
+    (Grams + pairwise_krr_fit(iters) + pairwise_predict, graph-replayed solver), device-timed; plus the
+    solver's marginal cost per iteration (slope of the fit time between iters/2 and iters iterations)
+    against the SURVEY floor of one training matvec.  Then the oracle's 1-core legs (C1-C3 training
+    matvec, the per-term GVT) and the explicit-K C1 matvec, the paper's baseline."""
+    import torch
+
+    import oracle as O
+    import paper_2009_01054_b200 as G
+    dev = torch.device("cuda", local_rank)
+
+    def d(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    def timed(fn, reps=1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps
+
+    cache, runs = {}, []
+    for cfg, kname in CONFIG_RUNS:
+        if cfg not in cache:
+            cache.clear()
+            cache[cfg] = synth.by_name(cfg)
+        w = cache[cfg]
+        kernel = getattr(synth, kname.upper())
+        if kernel in synth.HOMOGENEOUS_KERNELS and w.Xt is not None:
+            w = synth.union_domain(w)
+        terms = G.gvt_kernel_terms(kernel)
+        with G.Context(local_rank) as ctx:
+            Xd, Xt = d(w.Xd), (None if w.Xt is None else d(w.Xt))
+            D = torch.empty((w.m, w.m), dtype=torch.float32, device=dev)
+            T = None if Xt is None else torch.empty((w.q, w.q), dtype=torch.float32, device=dev)
+            f, s_, y, tf, ts = d(w.train_first), d(w.train_second), d(w.y), d(w.test_first), d(w.test_second)
+            a = torch.empty(w.n, dtype=torch.float32, device=dev)
+            sc = torch.empty(w.n_test, dtype=torch.float32, device=dev)
+
+            def step(k=w.iters):
+                ctx.gram(w.base, Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=D)
+                if T is not None:
+                    ctx.gram(w.base, Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree, out=T)
+                ctx.fit(D, T, f, s_, y, terms, w.lam, k, 0.0, out=a, want_history=False)
+                ctx.predict(D, T, tf, ts, f, s_, a, terms, out=sc)
+
+            for _ in range(warmup):
+                step()
+            torch.cuda.synchronize(dev)
+            ctx.reset_stats()
+            ms = timed(step, steps)
+            launches = ctx.stats()["launches"] / steps
+            engine = {1: "sparse", 2: "dense", 3: "single-CTA"}.get(ctx.stats()["last_engine"])
+            k1, k0 = w.iters, w.iters // 2
+            fit = lambda k: ctx.fit(D, T, f, s_, y, terms, w.lam, k, 0.0, out=a, want_history=False)  # noqa: E731
+            fit(k0), fit(k1)
+            t0 = min(timed(lambda: fit(k0)) for _ in range(3))
+            t1 = min(timed(lambda: fit(k1)) for _ in range(3))
+            us_iter = 1e3 * (t1 - t0) / (k1 - k0)
+            floor = FLOORS_US.get((cfg, kname))
+            runs.append({"config": cfg, "kernel": kname, "ms_per_step": round(ms, 4), "iters": w.iters,
+                         "us_per_iter_step": round(1e3 * ms / w.iters, 2), "us_per_iter_marginal": round(us_iter, 2),
+                         "gpairs_per_s": round((w.iters * w.n + w.n_test) / (ms * 1e-3) / 1e9, 4),
+                         "cg_iters_per_s": round(w.iters / (ms * 1e-3), 1), "engine": engine,
+                         "gpu_launches_per_step": launches, "floor_us": floor,
+                         "frac_of_floor": (round(floor / us_iter, 4) if floor and us_iter > 0 else None)})
+    # ---- the oracle on ONE host core (SURVEY.md 8(d): "also record a 1-core run for C1-C3"), and the
+    #      explicit-K matvec at C1, the paper's baseline ("the standard matrix vector product with the
+    #      kernel matrix", PAPER.md:765-770): fp64, baseline not target
+    oracle_1core = []
+    nthreads = O.num_threads()
+    O.set_num_threads(1)
+    try:
+        for cfg, kname in (("C1", "kronecker"), ("C2", "kronecker"), ("C3", "symmetric")):
+            w = synth.by_name(cfg)
+            kernel = getattr(synth, kname.upper())
+            Do = O.gram(w.base, w.Xd, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+            To = None if w.Xt is None else O.gram(w.base, w.Xt, gamma=w.gamma, coef0=w.coef0, degree=w.degree)
+            av = synth.random_vector(0, w.n)
+            t0 = time.perf_counter()
+            O.gvt_matvec(O.kernel_terms(kernel), Do, To, w.train_first, w.train_second, w.train_first,
+                         w.train_second, av)
+            dt = time.perf_counter() - t0
+            rec = {"config": cfg, "kernel": kname, "matvec_s": round(dt, 4),
+                   "gpairs_per_s": w.n / dt / 1e9, "cores": 1, "kind": "oracle per-term GVT (O4), fp64"}
+            if cfg == "C1":
+                t0 = time.perf_counter()
+                O.explicit_matvec(kernel, Do, To, w.train_first, w.train_second, w.train_first, w.train_second, av)
+                dte = time.perf_counter() - t0
+                rec["explicit_K"] = {"matvec_s": round(dte, 5), "gpairs_per_s": w.n / dte / 1e9,
+                                     "kind": "explicit kernel-matrix matvec (n x n kernel evaluations), fp64, 1 core"}
+            oracle_1core.append(rec)
+    finally:
+        O.set_num_threads(nthreads)
+    return {"runs": runs, "oracle_1core": oracle_1core,
+            "note": "one B200; ms_per_step = Grams + fit(iters) + predict (graph-replayed solver); "
+                    "us_per_iter_marginal = slope of the fit time from iters/2 to iters iterations; "
+                    "frac_of_floor = SURVEY 8(d) floor per training matvec / us_per_iter_marginal"}
 
 
 def max_over_ranks(v, world, args, dev):
@@ -488,36 +610,33 @@ def run_gpu(args, rank, world, local_rank):
     rl = roofline(st["kinds"], w, kernel, None, peaks, args.engine, args.precision) if args.profile else None
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        k, dt, cores = oracle_sample(w, kernel, n_targets=args.ref_targets)
+        k, dt, cores = oracle_sample(w, kernel, n_targets=args.ref_targets, min_seconds=10.0)
         cpu = {"value": k / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"fp64 oracle per-term GVT training matvec restricted to the outputs of {args.ref_targets} "
-                         f"seeded targets, repeated for >= 1 s ({k} outputs in total; stage 1 streams all {w.n} "
+                         f"seeded targets, repeated for >= 10 s ({k} outputs in total; stage 1 streams all {w.n} "
                          f"pairs for those rows)",
                "seconds": round(dt, 2)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.workload, "kernel": synth.KERNEL_NAMES[kernel], "n_train": w.n,
-                       "n_test": w.n_test, "m": w.m, "q": w.q, "cg_iters": w.iters, "lambda": w.lam,
-                       "engine": {0: "auto", 1: "sparse", 2: "dense"}[args.engine], "tc_precision": args.precision,
-                       "exchange": ["S-allgather", "u-reduce", "auto (by estimated bytes)"][args.exchange],
-                       "exchange_used": {0: None, 1: "S-allgather", 2: "u-reduce"}.get(st.get("last_exchange", 0)),
-                       "comm": args.comm if world > 1 else None, "solver": args.solver,
-                       "cg_variant": ["hestenes-stiefel", "chronopoulos-gear"][args.cg_variant],
-                       "last_engine": {1: "sparse", 2: "dense"}.get(st["last_engine"], None),
-                       "l2": "inputs (pair ids 0.8 GB at C5) larger than the 126 MB L2; no flush",
-                       "step": "gram(D)+gram(T)+pairwise_krr_fit(iters)+pairwise_predict"},
+            "config": config_dict(args, w, kernel, world),
+            "runtime": {"last_engine": {1: "sparse", 2: "dense", 3: "single-CTA"}.get(st["last_engine"], None),
+                        "exchange_used": {0: None, 1: "S-allgather", 2: "u-reduce"}.get(st.get("last_exchange", 0)),
+                        "collectives": st["kinds"].get("collective", {}).get("count", 0)},
             "cg_iters_per_s": iters / (ms_step * 1e-3),
             "phases": phases,
             "matvec": matvec,
             "gpu_launches": int(st["launches"]),
             "kernel_ms": {k: round(v["ms"] / args.steps, 3) for k, v in st["kinds"].items()} if args.profile else None,
             "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
-    if args.gather_regime and world == 1:
+    if (args.gather_regime or args.configs) and world == 1:
         ctx.close()  # free the C5 workspaces first
         del D, T, a, scores, fD, sD, yD, tfD, tsD
         torch.cuda.empty_cache()
+    if args.gather_regime and world == 1:
         line["gather_regime"] = gather_regime_leg(local_rank, peaks)
+    if args.configs and world == 1:
+        line["configs"] = configs_leg(local_rank)
     print(json.dumps(line), flush=True)
 
 
@@ -545,7 +664,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather-regime", dest="gather_regime", action="store_false",
                     help="skip the sparse-engine gather-regime leg (0.2 %% density at C5 object counts)")
-    ap.add_argument("--ref-targets", type=int, default=32)
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the per-config legs (C1-C4 every kernel, oracle 1-core C1-C3, explicit-K C1)")
+    ap.add_argument("--ref-targets", type=int, default=8,
+                    help="oracle sample per step: the outputs of this many seeded targets (cpu_baseline and "
+                         "--impl reference)")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         # `bench.py --gpus N` outside a launcher: re-run this command under torch.distributed.run, one

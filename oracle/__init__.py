@@ -85,6 +85,7 @@ def lib():
         L.oracle_sort_plan.argtypes = [P, P, i64, i64, i64, i32, P, P]
         L.oracle_relabel.argtypes = [P, i64, i64, P, P, P]
         L.oracle_num_threads.restype = i32
+        L.oracle_set_num_threads.argtypes = [i32]
         _lib = L
     return _lib
 
@@ -108,6 +109,11 @@ def _check(rc, what):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count for the timing legs (results do not depend on it)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 def gram(base, X, Y=None, gamma=1.0, coef0=1.0, degree=2):

@@ -62,6 +62,16 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops (timing legs only: each output is owned by one thread and
+ * summed in a fixed order, so the results do not depend on it). */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* ------------------------------------------------------------------ O1 base Grams
  * PAPER.md:824-825 (section 5.2): linear k(x,y) = <x,y>; Gaussian
  * k(x,y) = exp(-gamma ||x-y||^2) with the SQUARED norm (reading S4).  The

@@ -731,7 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ta = tmem + b * BN + half * 128 + ((uint32_t)(quarter * 32) << 16);
-#if S16_SCALE_ROWS == BM
+#if S16_SCALE_ROWS == 128
                 if (EPI == EPI_SAMPLED && ep.sbk) {
                     // chunk-scaled B (fp16 S from EPI_STORE16): this thread's 128 columns are the S rows
                     // of ONE stage-1 CTA block, so the chunk's scale is a single scalar -- the drain is
@@ -832,7 +832,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                         if (gc < N) mx = fmaxf(mx, fabsf(run[i]));
                     }
                 }
-#if S16_SCALE_ROWS == BM
+#if S16_SCALE_ROWS == 128
                 for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                 if (lane == 0) estage[ew] = mx;
                 named_bar(1, 32 * N_EPI_WARPS);
@@ -852,7 +852,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     e = 15 - ex;
                 }
                 const float s = ldexpf(1.f, e);
-#if S16_SCALE_ROWS == BM
+#if S16_SCALE_ROWS == 128
                 // one writer per CTA block (also for a padding block past M: scale 1, finite)
                 if (threadIdx.x == 64) ep.c_sk[(int64_t)n_tile * ep.c_sk_ld + (m0 >> 7)] = ldexpf(1.f, -e);
 #else

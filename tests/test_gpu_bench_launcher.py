@@ -36,5 +36,6 @@ def test_bench_gpus2_host_comm(workload, exchange):
     line = _json_line(r.stdout)
     assert line["n_gpus"] == 2 and line["steps"] == 2 and line["warmup"] == 3
     assert line["value"] > 0 and line["config"]["comm"] == "host"
-    assert line["config"]["exchange_used"] == ("u-reduce" if exchange == 2 else "S-allgather")
+    assert line["runtime"]["exchange_used"] == ("u-reduce" if exchange == 2 else "S-allgather")
+    assert line["runtime"]["collectives"] > 0
     assert line["gpu_launches"] > 0

@@ -103,3 +103,13 @@ def test_bench_json_contract_on_c1():
     # SURVEY 8(d) breakdown fields: per-phase times and the standalone training matvec
     assert d["phases"]["fit_ms"] > 0 and d["phases"]["predict_ms"] > 0 and d["phases"]["gram_ms"] >= 0
     assert d["matvec"]["gpairs_per_s"] > 0 and d["matvec"]["runs"] == 5
+    # per-config legs (C1-C4, every kernel) and the oracle's 1-core / explicit-K context legs
+    runs = d["configs"]["runs"]
+    assert [(r["config"], r["kernel"]) for r in runs] == [
+        ("C1", "kronecker"), ("C2", "kronecker"), ("C3", "symmetric"), ("C3", "antisymmetric"), ("C3", "cartesian"),
+        ("C4", "poly2d"), ("C4", "mlpk"), ("C4", "ranking")]
+    assert all(r["ms_per_step"] > 0 and r["gpairs_per_s"] > 0 and r["us_per_iter_marginal"] > 0 for r in runs)
+    assert all(r["frac_of_floor"] is not None for r in runs if r["config"] in ("C3", "C4"))
+    o1 = d["configs"]["oracle_1core"]
+    assert [r["config"] for r in o1] == ["C1", "C2", "C3"] and all(r["cores"] == 1 for r in o1)
+    assert o1[0]["explicit_K"]["gpairs_per_s"] > 0

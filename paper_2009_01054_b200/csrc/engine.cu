@@ -577,10 +577,9 @@ static bool stage2_gather_pays(gvt_ctx *c, int64_t ns, int64_t M, int64_t N, int
 
 static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
                           float *out) {
-    // S scales: one power-of-two scale per (128-row block, 256-col tile) -- a stage-1 CTA's output
-    // block -- from the block maximum, applied per K-chunk in stage 2 as one scalar per chunk
-    // (S16_SCALE_ROWS; the r1 layout, one scale per (row, 256-col tile), is the A/B build
-    // -DS16_SCALE_ROWS=1)
+    // S scales: one power-of-two scale per (row, 256-col tile) from the tile maxima, applied per
+    // K-chunk in stage 2 (S16_SCALE_ROWS = 1); the A/B build -DS16_SCALE_ROWS=128 keeps one scale
+    // per (128-row block, 256-col tile) instead (ops.cuh: fewer clocks, more energy at C5)
     const int64_t ntW = (g.W + 255) / 256, skld = round_up(g.q_out > 0 ? g.q_out : 1, 256) / S16_SCALE_ROWS;
     const size_t slab_h = (size_t)g.qpad * g.W, slab_k = (size_t)ntW * skld;
     __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
@@ -1304,7 +1303,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     // in one SM's shared memory
     {
         const bool eligible = form == FORM_KRON && !minres && !cgg && !es && !distributed(c) && c->slabs <= 1 &&
-                              c->exchange == 0 && !P.rect && P.n_in == n && tiny_smem(P.m, P.q, n) > 0;
+                              !P.uex && !P.rect && P.n_in == n && tiny_smem(P.m, P.q, n) > 0;
         const double fmas = (double)n * (double)P.q + (double)n * (double)P.m;
         GVT_REQUIRE(c->engine != 3 || eligible, GVT_E_PARAM,
                     "single-CTA solver (engine 3): Kronecker CG fits on one GPU whose factors, S and vectors fit in "

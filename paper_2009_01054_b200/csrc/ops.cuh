@@ -11,11 +11,13 @@ namespace gvt {
 // leading dimension ld.  prec 0 = fp16 pieces with per-row power-of-two scale (scale[r] =
 // 1/s_r), prec 1 = tf32 pieces in fp32 containers (scale == nullptr).
 // fp16 S of the fused dense path: one power-of-two scale per (S16_SCALE_ROWS-row block, 256-wide
-// K chunk): scale_k[chunk * scale_k_ld + row / S16_SCALE_ROWS].  128 = one stage-1 CTA's output
-// block (the default: the stage-2 drain multiplies a chunk by ONE scalar); 1 = per row (the r1
-// layout, kept for A/B builds with -DS16_SCALE_ROWS=1).
+// K chunk): scale_k[chunk * scale_k_ld + row / S16_SCALE_ROWS].  1 = per row (default); 128 = one
+// stage-1 CTA's output block, so the stage-2 drain multiplies a chunk by ONE scalar (-DS16_SCALE_ROWS=128).
+// Measured at C5 under the 1 kW cap (profiles/r02_ab_s16_block_scale.txt): the block scale takes 15 %
+// fewer SM clocks per stage-2 launch but runs at 1.05-1.11 GHz instead of 1.29-1.31 GHz at the same
+// power, so a 10-iteration fit takes 913 vs 836 ms: the per-row scale stays the default.
 #ifndef S16_SCALE_ROWS
-#define S16_SCALE_ROWS 128
+#define S16_SCALE_ROWS 1
 #endif
 static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == 128, "S scale blocks: per row or per 128-row CTA block");
 

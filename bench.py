@@ -381,7 +381,7 @@ def configs_leg(local_rank, steps=5, warmup=3):
             ctx.reset_stats()
             ms = timed(step, steps)
             launches = ctx.stats()["launches"] / steps
-            engine = {1: "sparse", 2: "dense", 3: "single-CTA"}.get(ctx.stats()["last_engine"])
+            engine = {1: "sparse", 2: "dense", 3: "single-CTA", 4: "persistent"}.get(ctx.stats()["last_engine"])
             k1, k0 = w.iters, w.iters // 2
             fit = lambda k: ctx.fit(D, T, f, s_, y, terms, w.lam, k, 0.0, out=a, want_history=False)  # noqa: E731
             fit(k0), fit(k1)
@@ -620,7 +620,7 @@ def run_gpu(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(args, w, kernel, world),
-            "runtime": {"last_engine": {1: "sparse", 2: "dense", 3: "single-CTA"}.get(st["last_engine"], None),
+            "runtime": {"last_engine": {1: "sparse", 2: "dense", 3: "single-CTA", 4: "persistent"}.get(st["last_engine"], None),
                         "exchange_used": {0: None, 1: "S-allgather", 2: "u-reduce"}.get(st.get("last_exchange", 0)),
                         "collectives": st["kinds"].get("collective", {}).get("count", 0)},
             "cg_iters_per_s": iters / (ms_step * 1e-3),

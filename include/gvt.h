@@ -96,7 +96,10 @@ typedef enum {
                                     1 = sparse SIMT, 2 = dense tensor-core,
                                     3 = single-CTA whole-fit CG (Kronecker fits whose factors, S and
                                     vectors fit one SM's shared memory; auto picks it for those when
-                                    an iteration is <= 4e6 FMAs)                                      */
+                                    an iteration is <= 4e6 FMAs), 4 = persistent multi-CTA whole-fit
+                                    CG with grid barriers (Kronecker fits with m q^2 <= 6.4e7 dense
+                                    stage-1 FMAs, e.g. a complete small grid; auto picks it when the
+                                    single-CTA solver does not apply)                                 */
     GVT_OPT_DENSE_THRESHOLD = 1, /* auto engine: -1 (default) = by estimated time of the two engines
                                     (B200 calibration; crossover ~1 % density at C5 object counts);
                                     >= 0 = dense at or above this pair-matrix density             */
@@ -160,7 +163,8 @@ typedef struct {
     char names[GVT_MAX_KERNEL_KINDS][32];     /* kernel kind name                                      */
     int64_t counts[GVT_MAX_KERNEL_KINDS];     /* launches per kind                                     */
     double ms[GVT_MAX_KERNEL_KINDS];          /* summed CUDA-event duration (GVT_OPT_PROFILE = 1)       */
-    int32_t last_engine;                      /* engine last used: 1 sparse, 2 dense, 3 single-CTA fit */
+    int32_t last_engine;                      /* engine last used: 1 sparse, 2 dense, 3 single-CTA fit,
+                                                 4 persistent multi-CTA fit                           */
     int32_t world;                            /* communicator size (1 without gvt_comm_init)           */
     int32_t last_exchange;                    /* exchange of the last data-parallel call: 0 none (single
                                                  GPU), 1 S slab all-gather, 2 u-exchange              */

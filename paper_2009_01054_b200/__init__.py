@@ -35,7 +35,7 @@ FACTOR_DRUG, FACTOR_TARGET, FACTOR_ONES, FACTOR_IDENTITY = range(4)
 SEL_FIRST, SEL_SECOND = 0, 1
 OPT_ENGINE, OPT_DENSE_THRESHOLD, OPT_PROFILE, OPT_GRAM_ENGINE, OPT_TC_PRECISION = range(5)
 PREC_FP16X3, PREC_TF32X3 = 0, 1
-ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE, ENGINE_TINY = 0, 1, 2, 3
+ENGINE_AUTO, ENGINE_SPARSE, ENGINE_DENSE, ENGINE_TINY, ENGINE_SMALL = 0, 1, 2, 3, 4
 OPT_SLABS = 5
 OPT_GEMM_CTA = 6
 OPT_GRAPHS = 7

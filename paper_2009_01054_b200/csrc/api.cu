@@ -119,7 +119,7 @@ gvt_status gvt_set_option(gvt_ctx *c, gvt_option opt, double v) {
     GVT_API_BEGIN(c)
     switch (opt) {
     case GVT_OPT_ENGINE:
-        GVT_REQUIRE(v == 0 || v == 1 || v == 2 || v == 3, GVT_E_PARAM, "engine must be 0, 1, 2 or 3");
+        GVT_REQUIRE(v == 0 || v == 1 || v == 2 || v == 3 || v == 4, GVT_E_PARAM, "engine must be 0, 1, 2, 3 or 4");
         c->engine = (int)v;
         break;
     case GVT_OPT_DENSE_THRESHOLD:

@@ -55,10 +55,30 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_init_scalars(const double *_
     }
 }
 
-// Ap += lambda p ; partial p.Ap
+// the scalar steps (thread 0 of the reducing block)
+__device__ __forceinline__ void cg_alpha_scalar(double pap, double *st) {
+    st[ST_PAP] = pap;
+    if (!(pap > 0.0)) st[ST_BREAK] = 1.0;
+    else st[ST_ALPHA] = st[ST_RHO] / pap;
+}
+
+__device__ __forceinline__ void cg_beta_scalar(double rho1, double *st, double *relres) {
+    double it = st[ST_ITERS] + 1.0;
+    st[ST_ITERS] = it;
+    double rr = sqrt(rho1) / st[ST_YNORM];
+    if (relres) relres[(int64_t)it] = rr;
+    // converged: the tolerance, or the residual floor RES_FLOOR (reading S32: below it the fp32
+    // recurrences only underflow, into 0/0 after ~120 iterations on C1)
+    if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || rho1 == 0.0 || rr <= RES_FLOOR) st[ST_DONE] = 1.0;
+    st[ST_BETA] = rho1 / st[ST_RHO];
+    st[ST_RHO] = rho1;
+}
+
+// Ap += lambda p ; partial p.Ap.  With a ticket (single GPU), the last block to finish also reduces
+// the partials and takes the alpha step (k_cg_alpha folded in: one launch fewer per iteration).
 __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, const float *__restrict__ p, int64_t n,
-                                                       float lambda, const double *__restrict__ st,
-                                                       double *__restrict__ part) {
+                                                       float lambda, double *__restrict__ st,
+                                                       double *__restrict__ part, unsigned *__restrict__ ticket) {
     if (halted(st)) return;
     int64_t lo, hi;
     block_range(n, lo, hi);
@@ -90,24 +110,29 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, c
     }
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    if (ticket && last_block_done(ticket)) {
+        const double pap = reduce_parts_cg(part, gridDim.x);
+        if (threadIdx.x == 0) {
+            cg_alpha_scalar(pap, st);
+            *ticket = 0u;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_alpha(const double *__restrict__ part, int nparts,
                                                           double *__restrict__ st) {
     if (halted(st)) return;
     double pap = reduce_parts(part, nparts);
-    if (threadIdx.x == 0) {
-        st[ST_PAP] = pap;
-        if (!(pap > 0.0)) st[ST_BREAK] = 1.0;
-        else st[ST_ALPHA] = st[ST_RHO] / pap;
-    }
+    if (threadIdx.x == 0) cg_alpha_scalar(pap, st);
 }
 
-// x += alpha p ; r -= alpha Ap ; partial r.r
+// x += alpha p ; r -= alpha Ap ; partial r.r.  With a ticket (single GPU), the last block also
+// takes the beta / stopping step (k_cg_beta folded in).
 __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(float *__restrict__ x, float *__restrict__ r,
                                                        const float *__restrict__ p, const float *__restrict__ Ap,
-                                                       int64_t n, const double *__restrict__ st,
-                                                       double *__restrict__ part) {
+                                                       int64_t n, double *__restrict__ st,
+                                                       double *__restrict__ part, unsigned *__restrict__ ticket,
+                                                       double *__restrict__ relres) {
     if (halted(st)) return;
     const float alpha = (float)st[ST_ALPHA];
     int64_t lo, hi;
@@ -145,23 +170,20 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(float *__restrict__ x, fl
     }
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    if (ticket && last_block_done(ticket)) {
+        const double rho1 = reduce_parts_cg(part, gridDim.x);
+        if (threadIdx.x == 0) {
+            cg_beta_scalar(rho1, st, relres);
+            *ticket = 0u;
+        }
+    }
 }
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_beta(const double *__restrict__ part, int nparts,
                                                          double *__restrict__ st, double *__restrict__ relres) {
     if (halted(st)) return;
     double rho1 = reduce_parts(part, nparts);
-    if (threadIdx.x == 0) {
-        double it = st[ST_ITERS] + 1.0;
-        st[ST_ITERS] = it;
-        double rr = sqrt(rho1) / st[ST_YNORM];
-        if (relres) relres[(int64_t)it] = rr;
-        // converged: the tolerance, or the residual floor RES_FLOOR (reading S32: below it the fp32
-        // recurrences only underflow, into 0/0 after ~120 iterations on C1)
-        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || rho1 == 0.0 || rr <= RES_FLOOR) st[ST_DONE] = 1.0;
-        st[ST_BETA] = rho1 / st[ST_RHO];
-        st[ST_RHO] = rho1;
-    }
+    if (threadIdx.x == 0) cg_beta_scalar(rho1, st, relres);
 }
 
 // p = r + beta p
@@ -347,8 +369,12 @@ void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state) {
 double *solver_parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
 static double *my_parts(gvt_ctx *c) { return solver_parts(c) + (size_t)c->rank * RED_BLOCKS; }
 
+// single-GPU: the scalar steps run in the last block of the vector kernels (last_block_done)
+static unsigned *cg_ticket(gvt_ctx *c) { return distributed(c) ? nullptr : wsT<unsigned>(c, "cg.ticket", 1); }
+
 void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, double *state, double rel_tol) {
     double *pt = solver_parts(c);
+    if (unsigned *tk = cg_ticket(c)) GVT_CUDA_TRY(cudaMemsetAsync(tk, 0, sizeof(unsigned), c->stream));
     GVT_LAUNCH(c, K_CG_VEC, k_cg_init, RED_BLOCKS, RED_THREADS, 0, y, n, x, r, p, my_parts(c));
     allreduce_partials(c, pt, RED_BLOCKS);
     double *relres = state + ST_N;
@@ -358,7 +384,9 @@ void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p
 
 void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state) {
     double *pt = solver_parts(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_ap, RED_BLOCKS, RED_THREADS, 0, Ap, p, n, (float)lambda, state, my_parts(c));
+    unsigned *tk = cg_ticket(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_ap, RED_BLOCKS, RED_THREADS, 0, Ap, p, n, (float)lambda, state, my_parts(c), tk);
+    if (tk) return;
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_alpha, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state);
 }
@@ -368,9 +396,13 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
     (void)iter;
     (void)relres_dev;
     double *pt = solver_parts(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, RED_BLOCKS, RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c));
-    allreduce_partials(c, pt, RED_BLOCKS);
-    GVT_LAUNCH(c, K_CG_SCALAR, k_cg_beta, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);
+    unsigned *tk = cg_ticket(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, RED_BLOCKS, RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c), tk,
+               state + ST_N);
+    if (!tk) {
+        allreduce_partials(c, pt, RED_BLOCKS);
+        GVT_LAUNCH(c, K_CG_SCALAR, k_cg_beta, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);
+    }
     GVT_LAUNCH(c, K_CG_VEC, k_cg_p, RED_BLOCKS, RED_THREADS, 0, p, r, n, state);
 }
 

@@ -723,8 +723,7 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         run_group(c, P, mp.groups[0], p, mp.groups[0].coef, 0, u);
         break;
     case FORM_MLPK:
-        entry_values(c, mp.byF, p);
-        segment_sum(c, mp.byF, mp.groups[0].diag);  // diag(L) = bF + bS
+        segment_sum_gather(c, mp.byF, p, mp.groups[0].diag);  // diag(L) = bF + bS
         run_group(c, P, mp.groups[0], p, 1.f, 0, mp.buf);
         combine_mlpk(c, P.of, P.os, P.n_out, mp.buf, u);
         break;
@@ -733,25 +732,21 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         entry_values(c, g.ent, p);               // all entries: the segment sums need every row
         run_group(c, P, g, p, 2.f, 0, u, true);
         segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
-        entry_values(c, mp.byS, p);
-        segment_sum(c, mp.byS, mp.b2);          // bS
+        segment_sum_gather(c, mp.byS, p, mp.b2);  // bS
         gemv(c, P.D, mp.b1, 1, mp.g1);          // D.^2 bF
         gemv(c, P.T, mp.b2, 1, mp.g2);          // T.^2 bS
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
         break;
     }
     case FORM_LINEAR:
-        entry_values(c, mp.byF, p);
-        segment_sum(c, mp.byF, mp.b1);
-        entry_values(c, mp.byS, p);
-        segment_sum(c, mp.byS, mp.b2);
+        segment_sum_gather(c, mp.byF, p, mp.b1);
+        segment_sum_gather(c, mp.byS, p, mp.b2);
         gemv(c, P.D, mp.b1, 0, mp.g1);
         gemv(c, P.T, mp.b2, 0, mp.g2);
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
         break;
     case FORM_RANKING:
-        entry_values(c, mp.byF, p);
-        segment_sum(c, mp.byF, mp.b1);          // bF - bS
+        segment_sum_gather(c, mp.byF, p, mp.b1);  // bF - bS
         gemv(c, P.D, mp.b1, 0, mp.g1);
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
         break;
@@ -1298,20 +1293,28 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     float *u = wsT<float>(c, "solver.u", (size_t)(n + n_val));  // matvec output [inner; validation]
     MatvecPlan mp;
     plan_matvec(c, P, terms, n_terms, form, mp);
-    // small Kronecker fits: the whole solve in one single-CTA launch (tiny.cu) -- forced by
-    // GVT_OPT_ENGINE = 3, or chosen when a CG iteration is at most 4e6 FMAs and everything fits
-    // in one SM's shared memory
+    // small Kronecker fits: the whole solve in ONE launch -- single-CTA (tiny.cu; GVT_OPT_ENGINE = 3,
+    // or auto when a CG iteration is at most 4e6 FMAs and everything fits in one SM's shared memory),
+    // or persistent multi-CTA with grid barriers (small.cu; GVT_OPT_ENGINE = 4, or auto for the
+    // problems whose dense stage 1 is at most 6.4e7 FMAs, e.g. the complete C2 grid)
     {
-        const bool eligible = form == FORM_KRON && !minres && !cgg && !es && !distributed(c) && c->slabs <= 1 &&
-                              !P.uex && !P.rect && P.n_in == n && tiny_smem(P.m, P.q, n) > 0;
+        const bool whole = form == FORM_KRON && !minres && !cgg && !es && !distributed(c) && c->slabs <= 1 &&
+                           !P.uex && !P.rect && P.n_in == n;
+        const bool eligible = whole && tiny_smem(P.m, P.q, n) > 0;
+        const bool eligible4 = whole && small_eligible(P.m, P.q, n);
         const double fmas = (double)n * (double)P.q + (double)n * (double)P.m;
         GVT_REQUIRE(c->engine != 3 || eligible, GVT_E_PARAM,
                     "single-CTA solver (engine 3): Kronecker CG fits on one GPU whose factors, S and vectors fit in "
                     "shared memory only");
-        if (eligible && (c->engine == 3 || (c->engine == 0 && fmas <= 4e6))) {
+        GVT_REQUIRE(c->engine != 4 || eligible4, GVT_E_PARAM,
+                    "persistent small solver (engine 4): Kronecker CG fits on one GPU with m q^2 <= 6.4e7 only");
+        const bool use3 = eligible && (c->engine == 3 || (c->engine == 0 && fmas <= 4e6));
+        const bool use4 = !use3 && eligible4 && (c->engine == 4 || c->engine == 0);
+        if (use3 || use4) {
             const GroupPlan &g = mp.groups[0];
-            tiny_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
-            c->last_engine = 3;
+            if (use3) tiny_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
+            else small_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
+            c->last_engine = use3 ? 3 : 4;
             double hs[9];
             GVT_CUDA_TRY(cudaMemcpyAsync(hs, state, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
             if (relres_hist)

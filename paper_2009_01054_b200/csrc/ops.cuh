@@ -137,6 +137,7 @@ void stage2_gather16(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const __
 void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const float *S, int64_t ldS, int64_t K,
                    float coef, int accumulate, float *out);
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)
+void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b);  // b[h] = sum_row sign p[src]
 void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y);
 // u[i] (+)= c1 * g1[sel(rs1,i)] + c2 * g2[sel(rs2,i)]   (g2 nullable)
 void combine_gather(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *g1, int rs1, float c1,
@@ -241,6 +242,11 @@ void es_init(gvt_ctx *c, double *es, double *hist, int max_iter, AucPlan &a);
 void es_cg_scores(gvt_ctx *c, float *s, const float *kp, int64_t n_val, const double *state);
 void es_evaluate(gvt_ctx *c, AucPlan &a, const float *scores_full, double *state, double *es, double *hist,
                  int patience, const float *x, float *a_best, int64_t n);
+
+// ---- persistent multi-CTA whole-fit CG for small Kronecker problems (small.cu)
+bool small_eligible(int64_t m, int64_t q, int64_t n);
+void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
+              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state);
 
 // ---- single-CTA whole-fit CG for small Kronecker problems (tiny.cu)
 size_t tiny_smem(int64_t m, int64_t q, int64_t n);  // 0 if it does not fit one SM

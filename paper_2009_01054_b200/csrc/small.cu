@@ -1,0 +1,268 @@
+// small.cu -- the whole CG fit of a small Kronecker problem in ONE persistent multi-CTA launch.
+//
+// Between the single-CTA solver (tiny.cu: everything in one SM's shared memory) and the
+// graph-replayed multi-kernel engine (~8 launches per iteration, each with its own fixed cost)
+// lie problems like C2 (the complete 68 x 442 drug-target grid: 1.5e7 FMAs per iteration,
+// SURVEY.md 8(d) "latency-bound, target the CUDA-graph floor").  Here one cooperative launch of
+// co-resident CTAs runs every iteration of Hestenes-Stiefel CG (
+// readings S12-S14, S32) with grid barriers between the phases, all operands L2-resident:
+//   A  X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
+//                  p_k = r_k + beta p_{k-1} formed on the fly)
+//   B  S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
+//   C  Ap[dst]   = sum_h D[r][h] S[c][h] + lambda p_k[dst]; p.Ap   (stage 2 + ridge term)
+//   D  alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; r.r        (then beta, the stopping test)
+// (variant 1; T symmetric, R1.)  Every array written inside the launch is read
+// with ld.global.cg (L2, never a stale L1 line of an earlier phase).  Dot products are fp64: one partial per CTA
+// (fixed tree), every CTA reduces the partials in the same order, so all CTAs take the same
+// scalar decisions and the result is bit-identical run to run (reading S26).  The state and
+// residual history use the CG layout of cg.cu.
+#include "vecops.cuh"
+
+namespace gvt {
+
+enum { SS_RHO = 0, SS_ALPHA, SS_BETA, SS_YNORM, SS_PAP, SS_DONE, SS_BREAK, SS_ITERS, SS_TOL, SS_N };
+constexpr int SMALL_THREADS = 256;
+constexpr int TILE_T = 32, TILE_H = SMALL_THREADS / 32;  // stage-1 tile: 32 rows of S x 8 columns
+
+struct SmallArgs {
+    const float *T;  // stage-1 factor, q x q, symmetric (row col holds T[col][0..q))
+    int64_t ldT;
+    const float *D;  // stage-2 factor, m x m
+    int64_t ldD;
+    int m, q;        // rows of X / columns of S (drugs), rows of S (targets)
+    const int64_t *row_ptr;
+    const int32_t *row, *col, *src;
+    const float *sign;
+    int64_t nnz;
+    int64_t ns;
+    const int32_t *sr, *sc, *sdst;
+    const float *y;
+    float *x;
+    int n;
+    float *X;        // m x ldX, zero outside the cells of the sample (zeroed before the launch)
+    int64_t ldX;
+    float *S;        // q x ldS
+    int64_t ldS;
+    float *p, *r, *Ap;
+    double *part;    // [2][gridDim.x]
+    unsigned *bar;   // [2] arrivals, generation (zeroed before the launch)
+    float lambda;
+    int max_iter;
+    double tol;
+    double *state, *relres;
+};
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// grid-wide barrier of the co-resident CTAs (cooperative launch): arrival counter + generation
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned g = gen;
+        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(&bar[1], 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned *>(&bar[1]) == g) {
+            }
+        }
+        __threadfence();
+    }
+    gen++;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t gtid = (int64_t)blockIdx.x * SMALL_THREADS + tid, gthreads = (int64_t)gridDim.x * SMALL_THREADS;
+    const int64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+    const int n = a.n, m = a.m, q = a.q;
+    double *part1 = a.part, *part2 = a.part + gridDim.x;
+    unsigned gen = 0;
+    // ---- init: x = 0, r = p = y, rho = y.y
+    double yy = 0.0;
+    for (int64_t i = gtid; i < n; i += gthreads) {
+        const float v = a.y[i];
+        a.x[i] = 0.f;
+        a.r[i] = v;
+        a.p[i] = v;
+        yy += (double)v * (double)v;
+    }
+    yy = block_sum(yy);
+    if (tid == 0) part1[blockIdx.x] = yy;
+    grid_sync(a.bar, gen);
+    double rho = reduce_parts_cg(part1, gridDim.x);
+    __shared__ double bcast;
+    if (tid == 0) bcast = rho;
+    __syncthreads();
+    rho = bcast;
+    const double ynorm = sqrt(rho);
+    if (gtid == 0 && a.relres) a.relres[0] = ynorm > 0.0 ? 1.0 : 0.0;
+    int it = 0, brk = 0;
+    double alpha = 0.0, beta = 0.0, pap = 0.0;
+    bool done = !(rho > 0.0);
+    const int ntt = (q + TILE_T - 1) / TILE_T, nth = (m + TILE_H - 1) / TILE_H;
+    while (!done && it < a.max_iter) {
+        const float bf = (float)beta;
+        const bool first = it == 0;  // p_1 = r_0 = y is already in p
+        // ---- A: the pair matrix of p_k (cells in entry order, runs of duplicates summed by their head)
+        for (int64_t k = gtid; k < a.nnz; k += gthreads) {
+            const int32_t h = a.row[k], cc = a.col[k];
+            if (k > 0 && a.row[k - 1] == h && a.col[k - 1] == cc) continue;
+            float v = 0.f;
+            for (int64_t j = k; j < a.nnz && a.row[j] == h && a.col[j] == cc; j++) {
+                const int32_t s = a.src[j];
+                const float pk = first ? __ldcg(a.p + s) : fmaf(bf, __ldcg(a.p + s), __ldcg(a.r + s));
+                v = fmaf(a.sign[j], pk, v);
+            }
+            a.X[(int64_t)h * a.ldX + cc] = v;
+        }
+        grid_sync(a.bar, gen);
+        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps)
+        for (int tile = blockIdx.x; tile < ntt * nth; tile += gridDim.x) {
+            const int t = (tile % ntt) * TILE_T + lane, h = (tile / ntt) * TILE_H + warp;
+            if (h < m) {
+                const float *xr = a.X + (int64_t)h * a.ldX;
+                const float *tc = a.T + (t < q ? t : 0);
+                float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+                int k = 0;
+                for (; k + 3 < q; k += 4) {  // four independent chains (the loads are L1/L2 hits)
+                    acc0 = fmaf(__ldg(tc + (int64_t)k * a.ldT), __ldcg(xr + k), acc0);
+                    acc1 = fmaf(__ldg(tc + (int64_t)(k + 1) * a.ldT), __ldcg(xr + k + 1), acc1);
+                    acc2 = fmaf(__ldg(tc + (int64_t)(k + 2) * a.ldT), __ldcg(xr + k + 2), acc2);
+                    acc3 = fmaf(__ldg(tc + (int64_t)(k + 3) * a.ldT), __ldcg(xr + k + 3), acc3);
+                }
+                for (; k < q; k++) acc0 = fmaf(__ldg(tc + (int64_t)k * a.ldT), __ldcg(xr + k), acc0);
+                if (t < q) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
+            }
+        }
+        grid_sync(a.bar, gen);
+        // ---- C: stage 2 (warp per sample, lanes over h) + ridge term; the owner of dst stores p_k
+        double pa = 0.0;
+        for (int64_t k = gwarp; k < a.ns; k += gwarps) {
+            const float *drow = a.D + (int64_t)a.sr[k] * a.ldD, *srow = a.S + (int64_t)a.sc[k] * a.ldS;
+            float acc = 0.f;
+            for (int h = lane; h < m; h += 32) acc = fmaf(__ldg(drow + h), __ldcg(srow + h), acc);
+            acc = warp_sum_f(acc);
+            if (lane == 0) {
+                const int d = a.sdst[k];
+                const float pk = first ? __ldcg(a.p + d) : fmaf(bf, __ldcg(a.p + d), __ldcg(a.r + d));
+                const float v = fmaf(a.lambda, pk, acc);
+                a.Ap[d] = v;
+                a.p[d] = pk;
+                pa += (double)pk * (double)v;
+            }
+        }
+        pa = block_sum(pa);
+        if (tid == 0) part1[blockIdx.x] = pa;
+        grid_sync(a.bar, gen);
+        pap = reduce_parts_cg(part1, gridDim.x);
+        if (tid == 0) bcast = pap;
+        __syncthreads();
+        pap = bcast;
+        if (!(pap > 0.0)) {
+            brk = 1;
+            break;
+        }
+        // ---- D: x += alpha p; r -= alpha Ap; r.r
+        alpha = rho / pap;
+        const float af = (float)alpha;
+        double rr = 0.0;
+        for (int64_t i = gtid; i < n; i += gthreads) {
+            a.x[i] = fmaf(af, __ldcg(a.p + i), a.x[i]);
+            const float ri = fmaf(-af, __ldcg(a.Ap + i), __ldcg(a.r + i));
+            a.r[i] = ri;
+            rr += (double)ri * (double)ri;
+        }
+        rr = block_sum(rr);
+        if (tid == 0) part2[blockIdx.x] = rr;
+        grid_sync(a.bar, gen);
+        double rho1 = reduce_parts_cg(part2, gridDim.x);
+        if (tid == 0) bcast = rho1;
+        __syncthreads();
+        rho1 = bcast;
+        it++;
+        const double rel = sqrt(rho1) / ynorm;
+        if (gtid == 0 && a.relres) a.relres[it] = rel;
+        done = (a.tol > 0.0 && rel <= a.tol) || rho1 == 0.0 || rel <= 8.673617379884035e-19;  // S32 floor
+        beta = rho1 / rho;
+        rho = rho1;
+    }
+    if (gtid == 0) {
+        double *st = a.state;
+        st[SS_RHO] = rho;
+        st[SS_ALPHA] = alpha;
+        st[SS_BETA] = beta;
+        st[SS_YNORM] = ynorm;
+        st[SS_PAP] = pap;
+        st[SS_DONE] = done ? 1.0 : 0.0;
+        st[SS_BREAK] = brk;
+        st[SS_ITERS] = it;
+        st[SS_TOL] = a.tol;
+    }
+}
+
+// dense stage-1 FMAs per iteration (m x q x q) the persistent solver is meant for
+bool small_eligible(int64_t m, int64_t q, int64_t n) {
+    return m > 0 && q > 0 && n > 0 && n < INT32_MAX && (double)m * (double)q * (double)q <= 6.4e7 &&
+           (double)m * (double)q <= 4e6;
+}
+
+void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
+              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state) {
+    GVT_REQUIRE(small_eligible(m, q, n), GVT_E_STATE, "problem outside the persistent small solver's range");
+    int per_sm = 0;
+    GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_cg, SMALL_THREADS, 0));
+    GVT_REQUIRE(per_sm >= 1, GVT_E_CUDA, "persistent small solver: no co-resident CTA");
+    const int64_t tiles = ((q + TILE_T - 1) / TILE_T) * ((m + TILE_H - 1) / TILE_H);
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), (int64_t)c->sm_count * std::min(per_sm, 2));
+    SmallArgs a;
+    a.T = T.p;
+    a.ldT = T.ld;
+    a.D = D.p;
+    a.ldD = D.ld;
+    a.m = (int)m;
+    a.q = (int)q;
+    a.row_ptr = e.row_ptr;
+    a.row = e.row;
+    a.col = e.col;
+    a.src = e.src;
+    a.sign = e.sign;
+    a.nnz = e.nnz;
+    a.ns = sp.ns;
+    a.sr = sp.r;
+    a.sc = sp.c;
+    a.sdst = sp.dst;
+    a.y = y;
+    a.x = x;
+    a.n = (int)n;
+    a.ldX = round_up(q, 4);
+    a.X = wsT<float>(c, "small.X", (size_t)m * a.ldX);
+    a.ldS = round_up(m, 4);
+    a.S = wsT<float>(c, "small.S", (size_t)q * a.ldS);
+    a.p = wsT<float>(c, "small.p", (size_t)n);
+    a.r = wsT<float>(c, "small.r", (size_t)n);
+    a.Ap = wsT<float>(c, "small.Ap", (size_t)n);
+    a.part = wsT<double>(c, "small.part", (size_t)2 * grid);
+    a.bar = wsT<unsigned>(c, "small.bar", 2);
+    a.lambda = (float)lambda;
+    a.max_iter = max_iter;
+    a.tol = tol;
+    a.state = state;
+    a.relres = state + SS_N;
+    GVT_CUDA_TRY(cudaMemsetAsync(a.X, 0, sizeof(float) * (size_t)m * a.ldX, c->stream));
+    GVT_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), c->stream));
+    void *args[] = {&a};
+    cudaEvent_t ev;
+    launch_begin(c, K_TINY, &ev);
+    GVT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_small_cg, dim3(grid), dim3(SMALL_THREADS), args, 0,
+                                             c->stream));
+    launch_end(c, K_TINY, ev);
+}
+
+}  // namespace gvt

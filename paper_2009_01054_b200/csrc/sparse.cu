@@ -259,6 +259,27 @@ __global__ void k_segment_sum(const int64_t *__restrict__ row_ptr, int64_t nrow,
     }
 }
 
+// b[h] = sum_{k in row h} sign[k] p[src[k]]: the entry values gathered inside the segment sum (the
+// same per-lane order and tree as k_entry_values followed by k_segment_sum, one pass fewer)
+__global__ void k_segment_sum_gather(const int64_t *__restrict__ row_ptr, int64_t nrow, const int32_t *__restrict__ src,
+                                     const float *__restrict__ sign, const float *__restrict__ p,
+                                     float *__restrict__ b) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t h = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < nrow; h += warps) {
+        float acc = 0.f;
+        for (int64_t k = row_ptr[h] + lane; k < row_ptr[h + 1]; k += 32) acc += sign[k] * __ldg(p + src[k]);
+        acc = warp_sum(acc);
+        if (lane == 0) b[h] = acc;
+    }
+}
+
+void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b) {
+    if (e.nrow == 0) return;
+    GVT_LAUNCH(c, K_SEGSUM, k_segment_sum_gather, grid1d(e.nrow * 32, 256, (int64_t)c->sm_count * 16), 256, 0,
+               e.row_ptr, e.nrow, e.src, e.sign, p, b);
+}
+
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b) {
     if (e.nrow == 0) return;
     GVT_LAUNCH(c, K_SEGSUM, k_segment_sum, grid1d(e.nrow * 32, 256, (int64_t)c->sm_count * 16), 256, 0, e.row_ptr,
@@ -286,8 +307,59 @@ __global__ void __launch_bounds__(256) k_gemv(const float *__restrict__ F, int64
     }
 }
 
+// the same per-lane order (float4 chunks h = lane, lane + 32, ...) and tree as k_gemv, with b staged
+// in shared memory once per block of 8 rows and the row loads unrolled by four (independent 16-byte
+// loads in flight: the factor stream is the HBM-bound part, 4 B per FMA; k_gemv reached ~63 % of
+// the copy bandwidth on the 8000^2 union Gram of C4)
+__global__ void __launch_bounds__(256) k_gemv_smem(const float *__restrict__ F, int64_t n, int64_t ld,
+                                                   const float *__restrict__ b, int square, float *__restrict__ y) {
+    extern __shared__ float4 bs[];
+    const int64_t K4 = ld / 4;
+    for (int64_t h = threadIdx.x; h < K4; h += blockDim.x) bs[h] = __ldg(reinterpret_cast<const float4 *>(b) + h);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= n) return;
+    const float4 *row = reinterpret_cast<const float4 *>(F + r * ld);
+    float acc = 0.f;
+    int64_t h = lane;
+    for (; h + 96 < K4; h += 128) {
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) x[u] = __ldg(row + h + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            float4 xx = x[u];
+            const float4 z = bs[h + 32 * u];
+            if (square) { xx.x *= xx.x; xx.y *= xx.y; xx.z *= xx.z; xx.w *= xx.w; }
+            acc = fmaf(xx.x, z.x, acc); acc = fmaf(xx.y, z.y, acc);
+            acc = fmaf(xx.z, z.z, acc); acc = fmaf(xx.w, z.w, acc);
+        }
+    }
+    for (; h < K4; h += 32) {
+        float4 xx = __ldg(row + h);
+        const float4 z = bs[h];
+        if (square) { xx.x *= xx.x; xx.y *= xx.y; xx.z *= xx.z; xx.w *= xx.w; }
+        acc = fmaf(xx.x, z.x, acc); acc = fmaf(xx.y, z.y, acc);
+        acc = fmaf(xx.z, z.z, acc); acc = fmaf(xx.w, z.w, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[r] = acc;
+}
+
 void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y) {
     if (F.n == 0) return;
+    const size_t smem = sizeof(float) * (size_t)F.ld;
+    if (smem <= 160 * 1024 && F.ld % 4 == 0) {
+        static size_t attr[GVT_MAX_DEVICES] = {};
+        size_t &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
+        if (smem > 48 * 1024 && smem > attr_dev) {
+            GVT_CUDA_TRY(cudaFuncSetAttribute(k_gemv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_dev = smem;
+        }
+        GVT_LAUNCH(c, K_GEMV, k_gemv_smem, grid1d(F.n * 32, 256), 256, smem, F.p, F.n, F.ld, b, square, y);
+        return;
+    }
     GVT_LAUNCH(c, K_GEMV, k_gemv, grid1d(F.n * 32, 256, (int64_t)c->sm_count * 16), 256, 0, F.p, F.n, F.ld, b, square,
                y);
 }

@@ -39,6 +39,28 @@ __device__ __forceinline__ double reduce_parts(const double *__restrict__ part, 
 }
 
 
+// "Last block done" (threadfence reduction): after each block has written its partial (thread 0),
+// returns true in the one block that finishes last; that block then reduces the partials of all
+// blocks with reduce_parts_cg -- the same fixed-order tree as a separate single-block kernel, so the
+// scalar is bit-identical -- and resets *ticket to 0 for the next launch.  Single-GPU only (across
+// ranks the partials must be all-gathered between the two steps).
+__device__ __forceinline__ bool last_block_done(unsigned *ticket) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// reduce_parts over partials written by other blocks of the same grid (L2 reads, no stale L1)
+__device__ __forceinline__ double reduce_parts_cg(const double *part, int nparts) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += __ldcg(part + i);
+    return block_sum(acc);
+}
+
 // partial-sum slots [world][RED_BLOCKS] (cg.cu); this rank writes slot `rank`
 double *solver_parts(gvt_ctx *c);
 

@@ -387,3 +387,79 @@ def test_tiny_engine_shapes(ctx, m, q, n):
     ao, ito, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
     assert it == ito or n <= 8
     assert rel(a.cpu().numpy(), ao) <= 1e-4
+
+
+def test_small_engine_c2_matches_multikernel_and_oracle(ctx):
+    """GVT_OPT_ENGINE = 4: the whole C2 CG fit (the complete 68 x 442 grid, 100 iterations) in one
+    persistent multi-CTA launch with grid barriers.  Auto selects it on C2.  Same fp32 Grams on every
+    side: its residual history follows the graph-replayed multi-kernel engine's and the oracle's
+    (C2 is ill-conditioned, reading S30, so the weights are compared after 10 iterations, and the
+    solver's own in-loop matvec K x_k is checked at the S31 scale); the residual-mode stop equals the
+    oracle's iteration count; an ineligible problem is an error."""
+    w = synth.config2()
+    D = O.gram(w.base, w.Xd, gamma=w.gamma)
+    T = O.gram(w.base, w.Xt, gamma=w.gamma)
+    Dg, Tg = dev(f32(D)), dev(f32(T))
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    f, s, y = dev(w.train_first), dev(w.train_second), dev(w.y)
+    D32, T32 = f32(D).astype(np.float64), f32(T).astype(np.float64)
+    try:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+        ctx.reset_stats()
+        a, it, hist, code = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, w.iters)
+        st = ctx.stats()
+        assert st["last_engine"] == 4 and st["kinds"]["tiny_cg"]["count"] == 1 and code == G.OK and it == w.iters
+        # 10 iterations: weights vs the oracle's fp64 CG on the same fp32 Grams and vs the multi-kernel engine
+        ao, _, hist_o, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first, w.train_second, w.y, w.lam, 10)
+        a4, _, h4, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 10)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
+        a2, _, h2, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 10)
+        assert rel(a4.cpu().numpy(), ao) <= 1e-4 and rel(a4.cpu().numpy(), a2.cpu().numpy()) <= 1e-4
+        assert np.allclose(h4, hist_o, rtol=1e-3, atol=1e-9) and np.allclose(h4, h2, rtol=1e-3, atol=1e-9)
+        # the in-loop matvec on the final iterate (S31 normalisation, as test_in_loop_matvec_parity)
+        x = a.cpu().numpy().astype(np.float64)
+        idx = synth.sample_indices(4, w.n, 512)
+        ref = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first[idx], w.train_second[idx],
+                           w.train_first, w.train_second, x)
+        scale = O.gvt_matvec(O.kernel_terms(O.KRONECKER), np.abs(D32), np.abs(T32), w.train_first[idx],
+                             w.train_second[idx], w.train_first, w.train_second, np.abs(x))
+        u = ctx.matvec(Dg, Tg, f, s, f, s, a, kron).cpu().numpy()
+        assert np.linalg.norm(u[idx] - ref) / np.linalg.norm(scale) <= 1e-5
+        # residual-mode stop
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_SMALL)
+        _, it3, h3, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 200, rel_tol=1e-2)
+        _, it3o, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first, w.train_second, w.y, w.lam, 200,
+                             rel_tol=1e-2)
+        assert abs(it3 - it3o) <= 1 and h3[-1] <= 1e-2
+        # determinism: the same bits twice
+        b1, _, _, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 30)
+        b2, _, _, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 30)
+        assert torch.equal(b1, b2)
+        # an ineligible problem (homogeneous Symmetric) is an error, not a fallback
+        with pytest.raises(G.GvtError) as e:
+            ctx.fit(Dg, None, f, dev(w.train_first), y, G.gvt_kernel_terms(G.SYMMETRIC), w.lam, 3)
+        assert e.value.code == G.E_PARAM
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("m,q,n", [(3, 5, 7), (70, 300, 10_000), (150, 500, 60_000), (33, 1000, 33_000)])
+def test_small_engine_shapes(ctx, m, q, n):
+    """Ragged shapes through the persistent solver (duplicates, tiles with padding rows, n not a
+    multiple of the grid) against the oracle's CG on the same fp32 inputs."""
+    rng = np.random.default_rng(m * 7 + n)
+    D32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((m, 4)), gamma=0.25))
+    T32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((q, 4)), gamma=0.25))
+    f = rng.integers(0, m, n).astype(np.int32)
+    s = rng.integers(0, q, n).astype(np.int32)
+    y = rng.standard_normal(n).astype(np.float32)
+    kron = G.gvt_kernel_terms(G.KRONECKER)
+    ctx.set_option(G.OPT_ENGINE, G.ENGINE_SMALL)
+    try:
+        a, it, _, _ = ctx.fit(dev(D32), dev(T32), dev(f), dev(s), dev(y), kron, 1.0, 8)
+        assert ctx.stats()["last_engine"] == 4
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    ao, ito, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
+    assert it == ito or n <= 8
+    assert rel(a.cpu().numpy(), ao) <= 1e-4

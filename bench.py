@@ -188,6 +188,16 @@ def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engin
                     "achieved_basis": "algorithmic FMAs of SURVEY 8(d) (q_out per pair-matrix entry / m_in per output)",
                     "executed_tflops": round(executed, 1), "executed_frac": round(executed / peak, 4),
                     "alu_roof_frac": round(achieved / alu_peak, 4)})
+        # the engine's own ceiling: a dense tile engine executes M N K products for the
+        # algorithmic (density x M N K) ones, three times (3xFP16 / 3xTF32 splits), so at 100 % of the
+        # tensor peak its algorithmic fraction is density / 3; fp32-accurate peak = peak / 3
+        ceiling = (flops / (2.0 * M * N * K)) / 3.0
+        out.update({"passes": 3, "density": round(3.0 * ceiling, 4), "ceiling_frac": round(ceiling, 4),
+                    "frac_of_ceiling": round(achieved / peak / ceiling, 4),
+                    "fp32_accurate_peak": round(peak / 3.0, 1),
+                    "fp32_accurate_frac": round(achieved / (peak / 3.0), 4),
+                    "ceiling_note": "frac = algorithmic flops / measured bf16 sustained peak; a dense 3-pass "
+                                    "engine at density d cannot exceed d / 3 (ceiling_frac)"})
     else:
         out.update({"bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak, 1), "unit": "TFLOP/s",
                     "frac": round(achieved / alu_peak, 4), "traffic": traffic,

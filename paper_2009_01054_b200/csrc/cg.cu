@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, c
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
     if (ticket && last_block_done(ticket)) {
-        const double pap = reduce_parts_cg(part, gridDim.x);
+        const double pap = reduce_parts_cg(part, RED_BLOCKS);  // (unused slots are zero: cg_init)
         if (threadIdx.x == 0) {
             cg_alpha_scalar(pap, st);
             *ticket = 0u;
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(float *__restrict__ x, fl
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
     if (ticket && last_block_done(ticket)) {
-        const double rho1 = reduce_parts_cg(part, gridDim.x);
+        const double rho1 = reduce_parts_cg(part, RED_BLOCKS);
         if (threadIdx.x == 0) {
             cg_beta_scalar(rho1, st, relres);
             *ticket = 0u;
@@ -244,10 +244,14 @@ __global__ void __launch_bounds__(RED_THREADS) k_cgg_init(const float *__restric
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-// w += lambda r; partials of r.r (part[b]) and w.r (part[RED_BLOCKS + b])
+__device__ void cgg_scalar_step(double g, double d, double *st, double *relres);
+
+// w += lambda r; partials of r.r (part[b]) and w.r (part[RED_BLOCKS + b]).  With a ticket (single GPU)
+// the last block also takes the scalar step (k_cgg_scalar folded in).
 __global__ void __launch_bounds__(RED_THREADS) k_cgg_dots(float *__restrict__ w, const float *__restrict__ r,
-                                                          int64_t n, float lambda, const double *__restrict__ st,
-                                                          double *__restrict__ part) {
+                                                          int64_t n, float lambda, double *__restrict__ st,
+                                                          double *__restrict__ part, unsigned *__restrict__ ticket,
+                                                          double *__restrict__ relres) {
     if (halted(st)) return;
     int64_t lo, hi;
     block_range(n, lo, hi);
@@ -265,6 +269,13 @@ __global__ void __launch_bounds__(RED_THREADS) k_cgg_dots(float *__restrict__ w,
         part[blockIdx.x] = g;
         part[RED_BLOCKS + blockIdx.x] = d;
     }
+    if (ticket && last_block_done(ticket)) {
+        const double gg = reduce_parts_cg(part, RED_BLOCKS), dd = reduce_parts_cg(part + RED_BLOCKS, RED_BLOCKS);
+        if (threadIdx.x == 0) {
+            cgg_scalar_step(gg, dd, st, relres);
+            *ticket = 0u;
+        }
+    }
 }
 
 // partials laid out [world][2][RED_BLOCKS] (all-gathered as one slot of 2 * RED_BLOCKS per rank)
@@ -276,29 +287,31 @@ __global__ void __launch_bounds__(RED_THREADS) k_cgg_scalar(const double *__rest
         g += reduce_parts(part + (size_t)r * 2 * RED_BLOCKS, RED_BLOCKS);
         d += reduce_parts(part + (size_t)r * 2 * RED_BLOCKS + RED_BLOCKS, RED_BLOCKS);
     }
-    if (threadIdx.x == 0) {
-        const double k = st[ST_ITERS];
-        const double rr = sqrt(g) / st[ST_YNORM];
-        if (relres) relres[(int64_t)k] = rr;
-        if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || g == 0.0 || rr <= RES_FLOOR) {
-            st[ST_DONE] = 1.0;
-            return;
-        }
-        double beta = 0.0, den = d;
-        if (k >= 1.0) {
-            beta = g / st[ST_RHO];
-            den = d - beta * g / st[ST_ALPHA];
-        }
-        st[ST_PAP] = den;  // p.(K + lambda I)p of the direction this update uses
-        if (!(den > 0.0)) {
-            st[ST_BREAK] = 1.0;
-            return;
-        }
-        st[ST_BETA] = beta;
-        st[ST_ALPHA] = g / den;
-        st[ST_RHO] = g;
-        st[ST_ITERS] = k + 1.0;
+    if (threadIdx.x == 0) cgg_scalar_step(g, d, st, relres);
+}
+
+__device__ void cgg_scalar_step(double g, double d, double *st, double *relres) {
+    const double k = st[ST_ITERS];
+    const double rr = sqrt(g) / st[ST_YNORM];
+    if (relres) relres[(int64_t)k] = rr;
+    if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || g == 0.0 || rr <= RES_FLOOR) {
+        st[ST_DONE] = 1.0;
+        return;
     }
+    double beta = 0.0, den = d;
+    if (k >= 1.0) {
+        beta = g / st[ST_RHO];
+        den = d - beta * g / st[ST_ALPHA];
+    }
+    st[ST_PAP] = den;  // p.(K + lambda I)p of the direction this update uses
+    if (!(den > 0.0)) {
+        st[ST_BREAK] = 1.0;
+        return;
+    }
+    st[ST_BETA] = beta;
+    st[ST_ALPHA] = g / den;
+    st[ST_RHO] = g;
+    st[ST_ITERS] = k + 1.0;
 }
 
 // p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s
@@ -338,10 +351,23 @@ __global__ void __launch_bounds__(RED_THREADS) k_cgg_final(const double *__restr
 // partial-sum slots [world][2 * RED_BLOCKS]; this rank writes slot `rank`
 static double *parts2(gvt_ctx *c) { return wsT<double>(c, "cgg.parts", (size_t)2 * RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
 
+// blocks of the CG vector kernels: about 1024 elements per block, at most RED_BLOCKS (C2: 30, C5: 1184)
+// -- a function of n only, so the partition (and every partial) stays fixed run to run.  The partial
+// slots past the used blocks are zero (set once per fit), so every reduction over RED_BLOCKS slots
+// (fused last block, separate scalar kernel, across ranks) sums the same values in the same tree.
+static int vec_blocks(int64_t n) { return (int)std::min<int64_t>(RED_BLOCKS, std::max<int64_t>(1, (n + 1023) / 1024)); }
+
+// single-GPU: the scalar steps run in the last block of the vector kernels (last_block_done)
+static unsigned *cg_ticket(gvt_ctx *c) { return distributed(c) ? nullptr : wsT<unsigned>(c, "cg.ticket", 1); }
+
 void cgg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, float *sv, double *state,
               double rel_tol) {
     double *pt = solver_parts(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cgg_init, RED_BLOCKS, RED_THREADS, 0, y, n, x, r, p, sv,
+    const int w = c->world > 0 ? c->world : 1;
+    GVT_CUDA_TRY(cudaMemsetAsync(pt, 0, sizeof(double) * RED_BLOCKS * w, c->stream));
+    GVT_CUDA_TRY(cudaMemsetAsync(parts2(c), 0, sizeof(double) * 2 * RED_BLOCKS * w, c->stream));
+    if (unsigned *tk = cg_ticket(c)) GVT_CUDA_TRY(cudaMemsetAsync(tk, 0, sizeof(unsigned), c->stream));
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_init, vec_blocks(n), RED_THREADS, 0, y, n, x, r, p, sv,
                pt + (size_t)c->rank * RED_BLOCKS);
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_init_scalars, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, rel_tol, state,
@@ -351,16 +377,19 @@ void cgg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *
 void cgg_step(gvt_ctx *c, float *x, float *r, float *p, float *sv, float *w, int64_t n, double lambda,
               double *state) {
     double *pt = parts2(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cgg_dots, RED_BLOCKS, RED_THREADS, 0, w, r, n, (float)lambda, state,
-               pt + (size_t)c->rank * 2 * RED_BLOCKS);
-    allreduce_partials(c, pt, 2 * RED_BLOCKS);  // the iteration's single collective
-    GVT_LAUNCH(c, K_CG_SCALAR, k_cgg_scalar, 1, RED_THREADS, 0, pt, c->world, state, state + ST_N);
-    GVT_LAUNCH(c, K_CG_VEC, k_cgg_update, RED_BLOCKS, RED_THREADS, 0, x, r, p, sv, w, n, state);
+    unsigned *tk = cg_ticket(c);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_dots, vec_blocks(n), RED_THREADS, 0, w, r, n, (float)lambda, state,
+               pt + (size_t)c->rank * 2 * RED_BLOCKS, tk, state + ST_N);
+    if (!tk) {
+        allreduce_partials(c, pt, 2 * RED_BLOCKS);  // the iteration's single collective
+        GVT_LAUNCH(c, K_CG_SCALAR, k_cgg_scalar, 1, RED_THREADS, 0, pt, c->world, state, state + ST_N);
+    }
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_update, vec_blocks(n), RED_THREADS, 0, x, r, p, sv, w, n, state);
 }
 
 void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state) {
     double *pt = solver_parts(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cgg_rr, RED_BLOCKS, RED_THREADS, 0, r, n, pt + (size_t)c->rank * RED_BLOCKS);
+    GVT_LAUNCH(c, K_CG_VEC, k_cgg_rr, vec_blocks(n), RED_THREADS, 0, r, n, pt + (size_t)c->rank * RED_BLOCKS);
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cgg_final, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);
 }
@@ -369,13 +398,11 @@ void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state) {
 double *solver_parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
 static double *my_parts(gvt_ctx *c) { return solver_parts(c) + (size_t)c->rank * RED_BLOCKS; }
 
-// single-GPU: the scalar steps run in the last block of the vector kernels (last_block_done)
-static unsigned *cg_ticket(gvt_ctx *c) { return distributed(c) ? nullptr : wsT<unsigned>(c, "cg.ticket", 1); }
-
 void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, double *state, double rel_tol) {
     double *pt = solver_parts(c);
+    GVT_CUDA_TRY(cudaMemsetAsync(pt, 0, sizeof(double) * RED_BLOCKS * (c->world > 0 ? c->world : 1), c->stream));
     if (unsigned *tk = cg_ticket(c)) GVT_CUDA_TRY(cudaMemsetAsync(tk, 0, sizeof(unsigned), c->stream));
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_init, RED_BLOCKS, RED_THREADS, 0, y, n, x, r, p, my_parts(c));
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_init, vec_blocks(n), RED_THREADS, 0, y, n, x, r, p, my_parts(c));
     allreduce_partials(c, pt, RED_BLOCKS);
     double *relres = state + ST_N;
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_init_scalars, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, rel_tol, state,
@@ -385,7 +412,7 @@ void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p
 void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state) {
     double *pt = solver_parts(c);
     unsigned *tk = cg_ticket(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_ap, RED_BLOCKS, RED_THREADS, 0, Ap, p, n, (float)lambda, state, my_parts(c), tk);
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_ap, vec_blocks(n), RED_THREADS, 0, Ap, p, n, (float)lambda, state, my_parts(c), tk);
     if (tk) return;
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_alpha, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state);
@@ -397,13 +424,13 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
     (void)relres_dev;
     double *pt = solver_parts(c);
     unsigned *tk = cg_ticket(c);
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, RED_BLOCKS, RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c), tk,
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, vec_blocks(n), RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c), tk,
                state + ST_N);
     if (!tk) {
         allreduce_partials(c, pt, RED_BLOCKS);
         GVT_LAUNCH(c, K_CG_SCALAR, k_cg_beta, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state, state + ST_N);
     }
-    GVT_LAUNCH(c, K_CG_VEC, k_cg_p, RED_BLOCKS, RED_THREADS, 0, p, r, n, state);
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_p, vec_blocks(n), RED_THREADS, 0, p, r, n, state);
 }
 
 }  // namespace gvt

@@ -11,8 +11,10 @@
 //   B  S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
 //   C  Ap[dst]   = sum_h D[r][h] S[c][h] + lambda p_k[dst]; p.Ap   (stage 2 + ridge term)
 //   D  alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; r.r        (then beta, the stopping test)
-// (variant 1; T symmetric, R1.)  Every array written inside the launch is read
-// with ld.global.cg (L2, never a stale L1 line of an earlier phase).  Dot products are fp64: one partial per CTA
+// (variant 1; T symmetric, R1.)  Stage 1 runs on shared-memory tiles (the T strip
+// and X rows of a 32 x 8 block of S), stage 2 on shared-memory copies of S and D, so the inner loops
+// are LDS + FMA; every array written inside the launch is read with ld.global.cg (L2, never a stale
+// L1 line of an earlier phase).  Dot products are fp64: one partial per CTA
 // (fixed tree), every CTA reduces the partials in the same order, so all CTAs take the same
 // scalar decisions and the result is bit-identical run to run (reading S26).  The state and
 // residual history use the CG layout of cg.cu.
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     double alpha = 0.0, beta = 0.0, pap = 0.0;
     bool done = !(rho > 0.0);
     const int ntt = (q + TILE_T - 1) / TILE_T, nth = (m + TILE_H - 1) / TILE_H;
+    extern __shared__ float sm[];
+    const int ldsm = m | 1;  // odd stride of the shared-memory S and D rows
     while (!done && it < a.max_iter) {
         const float bf = (float)beta;
         const bool first = it == 0;  // p_1 = r_0 = y is already in p
@@ -123,40 +127,58 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
             a.X[(int64_t)h * a.ldX + cc] = v;
         }
         grid_sync(a.bar, gen);
-        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps)
+        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps), its
+        //      T strip (q x 32) and X rows (8 x q) staged in shared memory (coalesced loads, then LDS)
         for (int tile = blockIdx.x; tile < ntt * nth; tile += gridDim.x) {
-            const int t = (tile % ntt) * TILE_T + lane, h = (tile / ntt) * TILE_H + warp;
-            if (h < m) {
-                const float *xr = a.X + (int64_t)h * a.ldX;
-                const float *tc = a.T + (t < q ? t : 0);
-                float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-                int k = 0;
-                for (; k + 3 < q; k += 4) {  // four independent chains (the loads are L1/L2 hits)
-                    acc0 = fmaf(__ldg(tc + (int64_t)k * a.ldT), __ldcg(xr + k), acc0);
-                    acc1 = fmaf(__ldg(tc + (int64_t)(k + 1) * a.ldT), __ldcg(xr + k + 1), acc1);
-                    acc2 = fmaf(__ldg(tc + (int64_t)(k + 2) * a.ldT), __ldcg(xr + k + 2), acc2);
-                    acc3 = fmaf(__ldg(tc + (int64_t)(k + 3) * a.ldT), __ldcg(xr + k + 3), acc3);
-                }
-                for (; k < q; k++) acc0 = fmaf(__ldg(tc + (int64_t)k * a.ldT), __ldcg(xr + k), acc0);
-                if (t < q) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
+            const int t0 = (tile % ntt) * TILE_T, h0 = (tile / ntt) * TILE_H;
+            float *Ts = sm, *Xs = sm + (size_t)q * TILE_T;
+            for (int i = tid; i < q * TILE_T; i += SMALL_THREADS) {
+                const int k = i / TILE_T, tt = i % TILE_T;
+                Ts[i] = (t0 + tt < q) ? __ldg(a.T + (int64_t)k * a.ldT + t0 + tt) : 0.f;
             }
+            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) {
+                const int hh = i / q, k = i % q;
+                Xs[i] = (h0 + hh < m) ? __ldcg(a.X + (int64_t)(h0 + hh) * a.ldX + k) : 0.f;
+            }
+            __syncthreads();
+            const float *xr = Xs + (size_t)warp * q;
+            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+            int k = 0;
+            for (; k + 3 < q; k += 4) {  // four independent chains
+                acc0 = fmaf(Ts[k * TILE_T + lane], xr[k], acc0);
+                acc1 = fmaf(Ts[(k + 1) * TILE_T + lane], xr[k + 1], acc1);
+                acc2 = fmaf(Ts[(k + 2) * TILE_T + lane], xr[k + 2], acc2);
+                acc3 = fmaf(Ts[(k + 3) * TILE_T + lane], xr[k + 3], acc3);
+            }
+            for (; k < q; k++) acc0 = fmaf(Ts[k * TILE_T + lane], xr[k], acc0);
+            const int t = t0 + lane, h = h0 + warp;
+            if (t < q && h < m) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
+            __syncthreads();
         }
         grid_sync(a.bar, gen);
-        // ---- C: stage 2 (warp per sample, lanes over h) + ridge term; the owner of dst stores p_k
+        // ---- C: stage 2 + ridge term, thread per sample on shared-memory copies of S (q x m) and D (m x m)
+        //      (odd row strides: the rows of a warp's samples fall in different banks); the owner of dst
+        //      stores p_k
+        float *Ss = sm, *Ds = sm + (size_t)q * ldsm;
+        for (int i = tid; i < q * m; i += SMALL_THREADS) Ss[(i / m) * ldsm + i % m] = __ldcg(a.S + (int64_t)(i / m) * a.ldS + i % m);
+        for (int i = tid; i < m * m; i += SMALL_THREADS) Ds[(i / m) * ldsm + i % m] = __ldg(a.D + (int64_t)(i / m) * a.ldD + i % m);
+        __syncthreads();
         double pa = 0.0;
-        for (int64_t k = gwarp; k < a.ns; k += gwarps) {
-            const float *drow = a.D + (int64_t)a.sr[k] * a.ldD, *srow = a.S + (int64_t)a.sc[k] * a.ldS;
-            float acc = 0.f;
-            for (int h = lane; h < m; h += 32) acc = fmaf(__ldg(drow + h), __ldcg(srow + h), acc);
-            acc = warp_sum_f(acc);
-            if (lane == 0) {
-                const int d = a.sdst[k];
-                const float pk = first ? __ldcg(a.p + d) : fmaf(bf, __ldcg(a.p + d), __ldcg(a.r + d));
-                const float v = fmaf(a.lambda, pk, acc);
-                a.Ap[d] = v;
-                a.p[d] = pk;
-                pa += (double)pk * (double)v;
+        for (int64_t k = gtid; k < a.ns; k += gthreads) {
+            const float *drow = Ds + (int64_t)a.sr[k] * ldsm, *srow = Ss + (int64_t)a.sc[k] * ldsm;
+            float acc0 = 0.f, acc1 = 0.f;
+            int h = 0;
+            for (; h + 1 < m; h += 2) {
+                acc0 = fmaf(drow[h], srow[h], acc0);
+                acc1 = fmaf(drow[h + 1], srow[h + 1], acc1);
             }
+            if (h < m) acc0 = fmaf(drow[h], srow[h], acc0);
+            const int d = a.sdst[k];
+            const float pk = first ? __ldcg(a.p + d) : fmaf(bf, __ldcg(a.p + d), __ldcg(a.r + d));
+            const float v = fmaf(a.lambda, pk, acc0 + acc1);
+            a.Ap[d] = v;
+            a.p[d] = pk;
+            pa += (double)pk * (double)v;
         }
         pa = block_sum(pa);
         if (tid == 0) part1[blockIdx.x] = pa;
@@ -207,20 +229,34 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     }
 }
 
-// dense stage-1 FMAs per iteration (m x q x q) the persistent solver is meant for
+// shared memory of the phases: B (T strip q x 32 + X rows 8 x q), C (S q x m + D m x m, odd strides)
+static size_t small_smem(int64_t m, int64_t q) {
+    const int64_t ld = m | 1;
+    const int64_t b = q * (TILE_T + TILE_H), c = (q + m) * ld;
+    return sizeof(float) * (size_t)(b > c ? b : c);
+}
+
+// dense stage-1 FMAs per iteration (m x q x q) at most 6.4e7, and S, D fit one CTA's shared memory
 bool small_eligible(int64_t m, int64_t q, int64_t n) {
     return m > 0 && q > 0 && n > 0 && n < INT32_MAX && (double)m * (double)q * (double)q <= 6.4e7 &&
-           (double)m * (double)q <= 4e6;
+           small_smem(m, q) <= 200 * 1024;
 }
 
 void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
               int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state) {
     GVT_REQUIRE(small_eligible(m, q, n), GVT_E_STATE, "problem outside the persistent small solver's range");
+    const size_t smem = small_smem(m, q);
+    static size_t attr[GVT_MAX_DEVICES] = {};
+    size_t &attr_dev = attr[c->device < GVT_MAX_DEVICES ? c->device : 0];
+    if (smem > 48 * 1024 && smem > attr_dev) {
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_small_cg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_dev = smem;
+    }
     int per_sm = 0;
-    GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_cg, SMALL_THREADS, 0));
+    GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_cg, SMALL_THREADS, smem));
     GVT_REQUIRE(per_sm >= 1, GVT_E_CUDA, "persistent small solver: no co-resident CTA");
-    const int64_t tiles = ((q + TILE_T - 1) / TILE_T) * ((m + TILE_H - 1) / TILE_H);
-    const int grid = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), (int64_t)c->sm_count * std::min(per_sm, 2));
+    // one CTA per SM: every phase is a grid-stride loop (stage 1 has <= 148 tiles on C2-size problems)
+    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, 1), 1 << 16);
     SmallArgs a;
     a.T = T.p;
     a.ldT = T.ld;
@@ -260,7 +296,7 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     void *args[] = {&a};
     cudaEvent_t ev;
     launch_begin(c, K_TINY, &ev);
-    GVT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_small_cg, dim3(grid), dim3(SMALL_THREADS), args, 0,
+    GVT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_small_cg, dim3(grid), dim3(SMALL_THREADS), args, smem,
                                              c->stream));
     launch_end(c, K_TINY, ev);
 }

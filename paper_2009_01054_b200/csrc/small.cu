@@ -6,9 +6,9 @@
 // SURVEY.md 8(d) "latency-bound, target the CUDA-graph floor").  Here one cooperative launch of
 // co-resident CTAs runs every iteration of Hestenes-Stiefel CG (
 // readings S12-S14, S32) with grid barriers between the phases, all operands L2-resident:
-//   A  X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
-//                  p_k = r_k + beta p_{k-1} formed on the fly)
-//   B  S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
+//   AB X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
+//                  p_k = r_k + beta p_{k-1} formed on the fly, built per tile in shared memory)
+//      S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
 //   C  Ap[dst]   = sum_h D[r][h] S[c][h] + lambda p_k[dst]; p.Ap   (stage 2 + ridge term)
 //   D  alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; r.r        (then beta, the stopping test)
 // (variant 1; T symmetric, R1.)  Stage 1 runs on shared-memory tiles (the T strip
@@ -41,8 +41,6 @@ struct SmallArgs {
     const float *y;
     float *x;
     int n;
-    float *X;        // m x ldX, zero outside the cells of the sample (zeroed before the launch)
-    int64_t ldX;
     float *S;        // q x ldS
     int64_t ldS;
     float *p, *r, *Ap;
@@ -59,21 +57,26 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
-// grid-wide barrier of the co-resident CTAs (cooperative launch): arrival counter + generation
+// grid-wide barrier of the co-resident CTAs (cooperative launch): arrival counter + generation; the
+// waiting CTAs poll the generation with acquire loads and a short sleep (less traffic on the line the
+// last arrival must update)
 __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
         const unsigned g = gen;
+        __threadfence();
         if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-            bar[0] = 0u;
+            atomicExch(&bar[0], 0u);
             __threadfence();
             atomicAdd(&bar[1], 1u);
         } else {
-            while (*reinterpret_cast<volatile unsigned *>(&bar[1]) == g) {
+            unsigned v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+                if (v != g) break;
+                __nanosleep(20);
             }
         }
-        __threadfence();
     }
     gen++;
     __syncthreads();
@@ -108,49 +111,59 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     int it = 0, brk = 0;
     double alpha = 0.0, beta = 0.0, pap = 0.0;
     bool done = !(rho > 0.0);
-    const int ntt = (q + TILE_T - 1) / TILE_T, nth = (m + TILE_H - 1) / TILE_H;
+    const int ntt = (q + TILE_T - 1) / TILE_T, nth = (m + TILE_H - 1) / TILE_H, ntiles = ntt * nth;
+    // shared memory: [T strip q x 32 | D m x ldsm | work: X rows 8 x q, or S q x ldsm]; the T strip of
+    // this CTA's tile and D stay resident for the whole fit when every CTA has at most one tile
     extern __shared__ float sm[];
-    const int ldsm = m | 1;  // odd stride of the shared-memory S and D rows
+    const int ldsm = m | 1;  // odd stride of the shared-memory S and D rows (conflict-free sample rows)
+    float *Tsm = sm, *Dsm = sm + (size_t)q * TILE_T, *work = Dsm + (size_t)m * ldsm;
+    const bool resident = ntiles <= (int)gridDim.x;
+    auto load_strip = [&](int t0) {
+        for (int i = tid; i < q * TILE_T; i += SMALL_THREADS) {
+            const int k = i / TILE_T, tt = i % TILE_T;
+            Tsm[i] = (t0 + tt < q) ? __ldg(a.T + (int64_t)k * a.ldT + t0 + tt) : 0.f;
+        }
+    };
+    if (resident && (int)blockIdx.x < ntiles) load_strip(((int)blockIdx.x % ntt) * TILE_T);
+    for (int i = tid; i < m * m; i += SMALL_THREADS) Dsm[(i / m) * ldsm + i % m] = __ldg(a.D + (int64_t)(i / m) * a.ldD + i % m);
+    __syncthreads();
     while (!done && it < a.max_iter) {
         const float bf = (float)beta;
         const bool first = it == 0;  // p_1 = r_0 = y is already in p
-        // ---- A: the pair matrix of p_k (cells in entry order, runs of duplicates summed by their head)
-        for (int64_t k = gtid; k < a.nnz; k += gthreads) {
-            const int32_t h = a.row[k], cc = a.col[k];
-            if (k > 0 && a.row[k - 1] == h && a.col[k - 1] == cc) continue;
-            float v = 0.f;
-            for (int64_t j = k; j < a.nnz && a.row[j] == h && a.col[j] == cc; j++) {
-                const int32_t s = a.src[j];
-                const float pk = first ? __ldcg(a.p + s) : fmaf(bf, __ldcg(a.p + s), __ldcg(a.r + s));
-                v = fmaf(a.sign[j], pk, v);
-            }
-            a.X[(int64_t)h * a.ldX + cc] = v;
-        }
-        grid_sync(a.bar, gen);
-        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps), its
-        //      T strip (q x 32) and X rows (8 x q) staged in shared memory (coalesced loads, then LDS)
-        for (int tile = blockIdx.x; tile < ntt * nth; tile += gridDim.x) {
+        // ---- A + B: per tile (32 consecutive t as lanes x 8 h as warps) the 8 pair-matrix rows of p_k
+        //      are built in shared memory from their CSR entries (runs of duplicate cells summed by the
+        //      head entry, in entry order; p_k = r_k + beta p_{k-1} formed on the fly), then
+        //      S[t][h] = sum_col T[col][t] X[h][col] from the shared T strip
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int t0 = (tile % ntt) * TILE_T, h0 = (tile / ntt) * TILE_H;
-            float *Ts = sm, *Xs = sm + (size_t)q * TILE_T;
-            for (int i = tid; i < q * TILE_T; i += SMALL_THREADS) {
-                const int k = i / TILE_T, tt = i % TILE_T;
-                Ts[i] = (t0 + tt < q) ? __ldg(a.T + (int64_t)k * a.ldT + t0 + tt) : 0.f;
-            }
-            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) {
-                const int hh = i / q, k = i % q;
-                Xs[i] = (h0 + hh < m) ? __ldcg(a.X + (int64_t)(h0 + hh) * a.ldX + k) : 0.f;
+            const int h1 = h0 + TILE_H < m ? h0 + TILE_H : m;
+            if (!resident) load_strip(t0);
+            float *Xs = work;
+            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) Xs[i] = 0.f;
+            __syncthreads();
+            const int64_t kb = a.row_ptr[h0], ke = a.row_ptr[h1];
+            for (int64_t k = kb + tid; k < ke; k += SMALL_THREADS) {
+                const int32_t h = a.row[k], cc = a.col[k];
+                if (k > kb && a.row[k - 1] == h && a.col[k - 1] == cc) continue;
+                float v = 0.f;
+                for (int64_t j = k; j < ke && a.row[j] == h && a.col[j] == cc; j++) {
+                    const int32_t sj = a.src[j];
+                    const float pk = first ? __ldcg(a.p + sj) : fmaf(bf, __ldcg(a.p + sj), __ldcg(a.r + sj));
+                    v = fmaf(a.sign[j], pk, v);
+                }
+                Xs[(h - h0) * q + cc] = v;
             }
             __syncthreads();
             const float *xr = Xs + (size_t)warp * q;
             float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
             int k = 0;
             for (; k + 3 < q; k += 4) {  // four independent chains
-                acc0 = fmaf(Ts[k * TILE_T + lane], xr[k], acc0);
-                acc1 = fmaf(Ts[(k + 1) * TILE_T + lane], xr[k + 1], acc1);
-                acc2 = fmaf(Ts[(k + 2) * TILE_T + lane], xr[k + 2], acc2);
-                acc3 = fmaf(Ts[(k + 3) * TILE_T + lane], xr[k + 3], acc3);
+                acc0 = fmaf(Tsm[k * TILE_T + lane], xr[k], acc0);
+                acc1 = fmaf(Tsm[(k + 1) * TILE_T + lane], xr[k + 1], acc1);
+                acc2 = fmaf(Tsm[(k + 2) * TILE_T + lane], xr[k + 2], acc2);
+                acc3 = fmaf(Tsm[(k + 3) * TILE_T + lane], xr[k + 3], acc3);
             }
-            for (; k < q; k++) acc0 = fmaf(Ts[k * TILE_T + lane], xr[k], acc0);
+            for (; k < q; k++) acc0 = fmaf(Tsm[k * TILE_T + lane], xr[k], acc0);
             const int t = t0 + lane, h = h0 + warp;
             if (t < q && h < m) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
             __syncthreads();
@@ -159,9 +172,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         // ---- C: stage 2 + ridge term, thread per sample on shared-memory copies of S (q x m) and D (m x m)
         //      (odd row strides: the rows of a warp's samples fall in different banks); the owner of dst
         //      stores p_k
-        float *Ss = sm, *Ds = sm + (size_t)q * ldsm;
+        float *Ss = work, *Ds = Dsm;
         for (int i = tid; i < q * m; i += SMALL_THREADS) Ss[(i / m) * ldsm + i % m] = __ldcg(a.S + (int64_t)(i / m) * a.ldS + i % m);
-        for (int i = tid; i < m * m; i += SMALL_THREADS) Ds[(i / m) * ldsm + i % m] = __ldg(a.D + (int64_t)(i / m) * a.ldD + i % m);
         __syncthreads();
         double pa = 0.0;
         for (int64_t k = gtid; k < a.ns; k += gthreads) {
@@ -229,11 +241,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     }
 }
 
-// shared memory of the phases: B (T strip q x 32 + X rows 8 x q), C (S q x m + D m x m, odd strides)
+// shared memory: T strip (q x 32) + D (m x ld) + the larger work area (X rows 8 x q, or S q x ld)
 static size_t small_smem(int64_t m, int64_t q) {
     const int64_t ld = m | 1;
-    const int64_t b = q * (TILE_T + TILE_H), c = (q + m) * ld;
-    return sizeof(float) * (size_t)(b > c ? b : c);
+    const int64_t wk = TILE_H * q > q * ld ? TILE_H * q : q * ld;
+    return sizeof(float) * (size_t)(q * TILE_T + m * ld + wk);
 }
 
 // dense stage-1 FMAs per iteration (m x q x q) at most 6.4e7, and S, D fit one CTA's shared memory
@@ -255,8 +267,14 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     int per_sm = 0;
     GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_cg, SMALL_THREADS, smem));
     GVT_REQUIRE(per_sm >= 1, GVT_E_CUDA, "persistent small solver: no co-resident CTA");
-    // one CTA per SM: every phase is a grid-stride loop (stage 1 has <= 148 tiles on C2-size problems)
-    const int grid = (int)std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, 1), 1 << 16);
+    // one CTA per SM (every phase is a grid-stride loop; C2 has 126 stage-1 tiles, each CTA keeps its
+    // tile's T strip resident); GVT_SMALL_GRID overrides the CTA count (experiments)
+    static const int env_grid = [] {
+        const char *e = getenv("GVT_SMALL_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    int grid = (int)std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, 1), 1 << 16);
+    if (env_grid > 0) grid = std::min(grid, env_grid);
     SmallArgs a;
     a.T = T.p;
     a.ldT = T.ld;
@@ -277,8 +295,6 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     a.y = y;
     a.x = x;
     a.n = (int)n;
-    a.ldX = round_up(q, 4);
-    a.X = wsT<float>(c, "small.X", (size_t)m * a.ldX);
     a.ldS = round_up(m, 4);
     a.S = wsT<float>(c, "small.S", (size_t)q * a.ldS);
     a.p = wsT<float>(c, "small.p", (size_t)n);
@@ -291,7 +307,6 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     a.tol = tol;
     a.state = state;
     a.relres = state + SS_N;
-    GVT_CUDA_TRY(cudaMemsetAsync(a.X, 0, sizeof(float) * (size_t)m * a.ldX, c->stream));
     GVT_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), c->stream));
     void *args[] = {&a};
     cudaEvent_t ev;

@@ -425,12 +425,14 @@ def test_small_engine_c2_matches_multikernel_and_oracle(ctx):
                              w.train_second[idx], w.train_first, w.train_second, np.abs(x))
         u = ctx.matvec(Dg, Tg, f, s, f, s, a, kron).cpu().numpy()
         assert np.linalg.norm(u[idx] - ref) / np.linalg.norm(scale) <= 1e-5
-        # residual-mode stop
+        # residual-mode stop (a tolerance the oracle's history reaches at iteration 6; C2's residual is
+        # not monotone, reading S15)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_SMALL)
-        _, it3, h3, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 200, rel_tol=1e-2)
+        tol = float(hist_o[6]) * (1 + 1e-9)
+        _, it3, h3, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 200, rel_tol=tol)
         _, it3o, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, w.train_first, w.train_second, w.y, w.lam, 200,
-                             rel_tol=1e-2)
-        assert abs(it3 - it3o) <= 1 and h3[-1] <= 1e-2
+                             rel_tol=tol)
+        assert it3o <= 6 and abs(it3 - it3o) <= 1 and h3[-1] <= tol
         # determinism: the same bits twice
         b1, _, _, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 30)
         b2, _, _, _ = ctx.fit(Dg, Tg, f, s, y, kron, w.lam, 30)

@@ -6,9 +6,9 @@
 // SURVEY.md 8(d) "latency-bound, target the CUDA-graph floor").  Here one cooperative launch of
 // co-resident CTAs runs every iteration of Hestenes-Stiefel CG (
 // readings S12-S14, S32) with grid barriers between the phases, all operands L2-resident:
-//   AB X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
-//                  p_k = r_k + beta p_{k-1} formed on the fly, built per tile in shared memory)
-//      S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
+//   A  X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
+//                  p_k = r_k + beta p_{k-1} formed on the fly)
+//   B  S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
 //   C  Ap[dst]   = sum_h D[r][h] S[c][h] + lambda p_k[dst]; p.Ap   (stage 2 + ridge term)
 //   D  alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; r.r        (then beta, the stopping test)
 // (variant 1; T symmetric, R1.)  Stage 1 runs on shared-memory tiles (the T strip
@@ -18,6 +18,8 @@
 // (fixed tree), every CTA reduces the partials in the same order, so all CTAs take the same
 // scalar decisions and the result is bit-identical run to run (reading S26).  The state and
 // residual history use the CG layout of cg.cu.
+#include <stdio.h>
+
 #include "vecops.cuh"
 
 namespace gvt {
@@ -43,8 +45,11 @@ struct SmallArgs {
     int n;
     float *S;        // q x ldS
     int64_t ldS;
+    float *X;        // m x ldX, zero outside the cells of the sample (zeroed before the launch)
+    int64_t ldX;
     float *p, *r, *Ap;
     double *part;    // [2][gridDim.x]
+    unsigned long long *prof;  // optional phase timestamps (GVT_SMALL_PROF): [8 iterations][10]
     unsigned *bar;   // [2] arrivals, generation (zeroed before the launch)
     float lambda;
     int max_iter;
@@ -80,6 +85,12 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen) {
     }
     gen++;
     __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
@@ -127,31 +138,38 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     if (resident && (int)blockIdx.x < ntiles) load_strip(((int)blockIdx.x % ntt) * TILE_T);
     for (int i = tid; i < m * m; i += SMALL_THREADS) Dsm[(i / m) * ldsm + i % m] = __ldg(a.D + (int64_t)(i / m) * a.ldD + i % m);
     __syncthreads();
+#define SMALL_MARK(j) \
+    if (a.prof && blockIdx.x == 0 && tid == 0 && it < 8) a.prof[it * 10 + (j)] = gtimer();
     while (!done && it < a.max_iter) {
+        SMALL_MARK(0)
         const float bf = (float)beta;
         const bool first = it == 0;  // p_1 = r_0 = y is already in p
-        // ---- A + B: per tile (32 consecutive t as lanes x 8 h as warps) the 8 pair-matrix rows of p_k
-        //      are built in shared memory from their CSR entries (runs of duplicate cells summed by the
-        //      head entry, in entry order; p_k = r_k + beta p_{k-1} formed on the fly), then
-        //      S[t][h] = sum_col T[col][t] X[h][col] from the shared T strip
+        // ---- A: the pair matrix of p_k, one entry per thread (runs of duplicate cells summed by their
+        //      head entry in entry order; p_k = r_k + beta p_{k-1} formed on the fly)
+        for (int64_t k = gtid; k < a.nnz; k += gthreads) {
+            const int32_t h = a.row[k], cc = a.col[k];
+            const bool head = k == 0 || a.row[k - 1] != h || a.col[k - 1] != cc;
+            if (!head) continue;
+            float v = 0.f;
+            for (int64_t j = k; j < a.nnz && a.row[j] == h && a.col[j] == cc; j++) {
+                const int32_t sj = a.src[j];
+                const float pk = first ? __ldcg(a.p + sj) : fmaf(bf, __ldcg(a.p + sj), __ldcg(a.r + sj));
+                v = fmaf(a.sign[j], pk, v);
+            }
+            a.X[(int64_t)h * a.ldX + cc] = v;
+        }
+        SMALL_MARK(1)
+        grid_sync(a.bar, gen);
+        SMALL_MARK(2)
+        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps), the
+        //      T strip resident in shared memory, the tile's 8 X rows staged by coalesced loads
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int t0 = (tile % ntt) * TILE_T, h0 = (tile / ntt) * TILE_H;
-            const int h1 = h0 + TILE_H < m ? h0 + TILE_H : m;
             if (!resident) load_strip(t0);
             float *Xs = work;
-            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) Xs[i] = 0.f;
-            __syncthreads();
-            const int64_t kb = a.row_ptr[h0], ke = a.row_ptr[h1];
-            for (int64_t k = kb + tid; k < ke; k += SMALL_THREADS) {
-                const int32_t h = a.row[k], cc = a.col[k];
-                if (k > kb && a.row[k - 1] == h && a.col[k - 1] == cc) continue;
-                float v = 0.f;
-                for (int64_t j = k; j < ke && a.row[j] == h && a.col[j] == cc; j++) {
-                    const int32_t sj = a.src[j];
-                    const float pk = first ? __ldcg(a.p + sj) : fmaf(bf, __ldcg(a.p + sj), __ldcg(a.r + sj));
-                    v = fmaf(a.sign[j], pk, v);
-                }
-                Xs[(h - h0) * q + cc] = v;
+            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) {
+                const int hh = i / q, k = i % q;
+                Xs[i] = (h0 + hh < m) ? __ldcg(a.X + (int64_t)(h0 + hh) * a.ldX + k) : 0.f;
             }
             __syncthreads();
             const float *xr = Xs + (size_t)warp * q;
@@ -168,13 +186,16 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
             if (t < q && h < m) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
             __syncthreads();
         }
+        SMALL_MARK(3)
         grid_sync(a.bar, gen);
+        SMALL_MARK(4)
         // ---- C: stage 2 + ridge term, thread per sample on shared-memory copies of S (q x m) and D (m x m)
         //      (odd row strides: the rows of a warp's samples fall in different banks); the owner of dst
         //      stores p_k
         float *Ss = work, *Ds = Dsm;
         for (int i = tid; i < q * m; i += SMALL_THREADS) Ss[(i / m) * ldsm + i % m] = __ldcg(a.S + (int64_t)(i / m) * a.ldS + i % m);
         __syncthreads();
+        SMALL_MARK(5)
         double pa = 0.0;
         for (int64_t k = gtid; k < a.ns; k += gthreads) {
             const float *drow = Ds + (int64_t)a.sr[k] * ldsm, *srow = Ss + (int64_t)a.sc[k] * ldsm;
@@ -194,7 +215,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         }
         pa = block_sum(pa);
         if (tid == 0) part1[blockIdx.x] = pa;
+        SMALL_MARK(6)
         grid_sync(a.bar, gen);
+        SMALL_MARK(7)
         pap = reduce_parts_cg(part1, gridDim.x);
         if (tid == 0) bcast = pap;
         __syncthreads();
@@ -215,7 +238,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         }
         rr = block_sum(rr);
         if (tid == 0) part2[blockIdx.x] = rr;
+        SMALL_MARK(8)
         grid_sync(a.bar, gen);
+        SMALL_MARK(9)
         double rho1 = reduce_parts_cg(part2, gridDim.x);
         if (tid == 0) bcast = rho1;
         __syncthreads();
@@ -295,6 +320,8 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     a.y = y;
     a.x = x;
     a.n = (int)n;
+    a.ldX = round_up(q, 4);
+    a.X = wsT<float>(c, "small.X", (size_t)m * a.ldX);
     a.ldS = round_up(m, 4);
     a.S = wsT<float>(c, "small.S", (size_t)q * a.ldS);
     a.p = wsT<float>(c, "small.p", (size_t)n);
@@ -307,13 +334,28 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     a.tol = tol;
     a.state = state;
     a.relres = state + SS_N;
+    GVT_CUDA_TRY(cudaMemsetAsync(a.X, 0, sizeof(float) * (size_t)m * a.ldX, c->stream));
     GVT_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), c->stream));
+    static const bool prof = getenv("GVT_SMALL_PROF") != nullptr;
+    a.prof = prof ? wsT<unsigned long long>(c, "small.prof", 80) : nullptr;
+    if (prof) GVT_CUDA_TRY(cudaMemsetAsync(a.prof, 0, 80 * sizeof(unsigned long long), c->stream));
     void *args[] = {&a};
     cudaEvent_t ev;
     launch_begin(c, K_TINY, &ev);
     GVT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_small_cg, dim3(grid), dim3(SMALL_THREADS), args, smem,
                                              c->stream));
     launch_end(c, K_TINY, ev);
+    if (prof) {  // phase durations (us) of iterations 1..7 of CTA 0, to stderr (diagnosis only)
+        unsigned long long h[80];
+        GVT_CUDA_TRY(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        const char *nm[9] = {"A", "bar1", "B", "bar2", "Ccopy", "C", "bar3", "D", "bar4"};
+        for (int it = 1; it < 8 && it < max_iter; it++) {
+            fprintf(stderr, "small_cg it %d:", it);
+            for (int j = 0; j < 9; j++) fprintf(stderr, " %s %.2f", nm[j], (h[it * 10 + j + 1] - h[it * 10 + j]) * 1e-3);
+            fprintf(stderr, "\n");
+        }
+    }
 }
 
 }  // namespace gvt

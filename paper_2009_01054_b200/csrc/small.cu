@@ -6,9 +6,9 @@
 // SURVEY.md 8(d) "latency-bound, target the CUDA-graph floor").  Here one cooperative launch of
 // co-resident CTAs runs every iteration of Hestenes-Stiefel CG (
 // readings S12-S14, S32) with grid barriers between the phases, all operands L2-resident:
-//   A  X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
-//                  p_k = r_k + beta p_{k-1} formed on the fly)
-//   B  S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
+//   AB X[h][col] = sum_{entries of cell (h, col)} sign p_k[src]    (the pair matrix of Theorem 1,
+//                  p_k = r_k + beta p_{k-1} formed on the fly, per tile in shared memory)
+//      S[t][h]   = sum_col T[t][col] X[h][col]                     (stage 1, dense SIMT GEMM tiles)
 //   C  Ap[dst]   = sum_h D[r][h] S[c][h] + lambda p_k[dst]; p.Ap   (stage 2 + ridge term)
 //   D  alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; r.r        (then beta, the stopping test)
 // (variant 1; T symmetric, R1.)  Stage 1 runs on shared-memory tiles (the T strip
@@ -27,6 +27,22 @@ namespace gvt {
 enum { SS_RHO = 0, SS_ALPHA, SS_BETA, SS_YNORM, SS_PAP, SS_DONE, SS_BREAK, SS_ITERS, SS_TOL, SS_N };
 constexpr int SMALL_THREADS = 256;
 constexpr int TILE_T = 32, TILE_H = SMALL_THREADS / 32;  // stage-1 tile: 32 rows of S x 8 columns
+constexpr uint32_t CELL_DUP = 1u << 31, CELL_HEAD = 1u << 30, CELL_MASK = CELL_HEAD - 1u;
+
+// per entry (sorted by (h, col)): its cell in the 8 X rows of its tile, flagged when the cell has several
+// entries (duplicate pairs) and, for those, when the entry heads the run
+__global__ void k_small_cells(const int32_t *__restrict__ row, const int32_t *__restrict__ col, int64_t nnz,
+                              int64_t ldX, uint32_t *__restrict__ cell) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t h = row[k], cc = col[k];
+        const bool same_prev = k > 0 && row[k - 1] == h && col[k - 1] == cc;
+        const bool same_next = k + 1 < nnz && row[k + 1] == h && col[k + 1] == cc;
+        uint32_t code = (uint32_t)((int64_t)(h % TILE_H) * ldX + cc);
+        if (same_prev || same_next) code |= CELL_DUP;
+        if (!same_prev && same_next) code |= CELL_HEAD;
+        cell[k] = code;
+    }
+}
 
 struct SmallArgs {
     const float *T;  // stage-1 factor, q x q, symmetric (row col holds T[col][0..q))
@@ -45,12 +61,13 @@ struct SmallArgs {
     int n;
     float *S;        // q x ldS
     int64_t ldS;
-    float *X;        // m x ldX, zero outside the cells of the sample (zeroed before the launch)
-    int64_t ldX;
+    const uint32_t *cell;  // per entry: cell (h % 8) * ldX + col of the tile's X rows, | CELL_DUP / CELL_HEAD
+    int64_t ldX;            // X row stride in shared memory (round_up(q, 4))
     float *p, *r, *Ap;
     double *part;    // [2][gridDim.x]
     unsigned long long *prof;  // optional phase timestamps (GVT_SMALL_PROF): [8 iterations][10]
-    unsigned *bar;   // [2] arrivals, generation (zeroed before the launch)
+    unsigned *bar;   // barrier words (zeroed before the launch)
+    int bar_mode;
     float lambda;
     int max_iter;
     double tol;
@@ -62,24 +79,49 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
-// grid-wide barrier of the co-resident CTAs (cooperative launch): arrival counter + generation; the
-// waiting CTAs poll the generation with acquire loads and a short sleep (less traffic on the line the
-// last arrival must update)
-__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen) {
+// grid-wide barrier of the co-resident CTAs (cooperative launch), two-level: CTAs arrive on their
+// group's counter (16 CTAs per group, one 128-byte line each), the last of a group arrives on the
+// top counter, the last group bumps the generation, which the waiting CTAs poll with acquire loads
+// and a short sleep.  bar: [0] generation, [32] top counter, [64 + 32 g] group counters.
+constexpr int BAR_GROUP = 16;
+constexpr int BAR_WORDS = 64 + 32 * 64;  // up to 64 groups (1024 CTAs)
+
+// mode (GVT_SMALL_BAR, experiments): bit 0 = two-level arrival, bit 1 = sleep while polling
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen, int mode) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned g = gen;
-        __threadfence();
-        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-            atomicExch(&bar[0], 0u);
+        unsigned *top = bar + 32;
+        bool released = false;
+        if (mode & 1) {
+            const unsigned grp = blockIdx.x / BAR_GROUP, ngrp = (gridDim.x + BAR_GROUP - 1) / BAR_GROUP;
+            const unsigned gsize = min((unsigned)BAR_GROUP, gridDim.x - grp * BAR_GROUP);
+            unsigned *gc = bar + 64 + 32 * grp;
             __threadfence();
-            atomicAdd(&bar[1], 1u);
+            if (atomicAdd(gc, 1u) == gsize - 1) {
+                atomicExch(gc, 0u);
+                if (atomicAdd(top, 1u) == ngrp - 1) {
+                    atomicExch(top, 0u);
+                    __threadfence();
+                    atomicAdd(bar, 1u);
+                    released = true;
+                }
+            }
         } else {
+            unsigned old;
+            asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(top) : "memory");
+            if (old == gridDim.x - 1) {
+                *reinterpret_cast<volatile unsigned *>(top) = 0u;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+                released = true;
+            }
+        }
+        if (!released) {
             unsigned v;
             while (true) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
                 if (v != g) break;
-                __nanosleep(20);
+                if (mode & 2) __nanosleep(20);
             }
         }
     }
@@ -111,7 +153,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     }
     yy = block_sum(yy);
     if (tid == 0) part1[blockIdx.x] = yy;
-    grid_sync(a.bar, gen);
+    grid_sync(a.bar, gen, a.bar_mode);
     double rho = reduce_parts_cg(part1, gridDim.x);
     __shared__ double bcast;
     if (tid == 0) bcast = rho;
@@ -123,16 +165,28 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     double alpha = 0.0, beta = 0.0, pap = 0.0;
     bool done = !(rho > 0.0);
     const int ntt = (q + TILE_T - 1) / TILE_T, nth = (m + TILE_H - 1) / TILE_H, ntiles = ntt * nth;
-    // shared memory: [T strip q x 32 | D m x ldsm | work: X rows 8 x q, or S q x ldsm]; the T strip of
-    // this CTA's tile and D stay resident for the whole fit when every CTA has at most one tile
+    // shared memory: [T strip, transposed: 32 x tq | D m x ldsm | work: X rows 8 x ldX, or S rows x ldsm];
+    // the T strip of this CTA's tile and D stay resident for the whole fit when every CTA has at most
+    // one tile.  tq = round_up(q, 32) + 4: the 16-byte loads of 8 consecutive lanes (32 rows) hit
+    // distinct bank groups.
     extern __shared__ float sm[];
     const int ldsm = m | 1;  // odd stride of the shared-memory S and D rows (conflict-free sample rows)
-    float *Tsm = sm, *Dsm = sm + (size_t)q * TILE_T, *work = Dsm + (size_t)m * ldsm;
+    const int tq = ((q + 31) & ~31) + 4, q4 = (int)(a.ldX / 4);
+    float *Tt = sm, *Dsm = sm + (size_t)TILE_T * tq;
+    float *work = sm + (((size_t)TILE_T * tq + (size_t)m * ldsm + 3) & ~(size_t)3);  // 16-byte aligned (float4)
     const bool resident = ntiles <= (int)gridDim.x;
-    auto load_strip = [&](int t0) {
-        for (int i = tid; i < q * TILE_T; i += SMALL_THREADS) {
-            const int k = i / TILE_T, tt = i % TILE_T;
-            Tsm[i] = (t0 + tt < q) ? __ldg(a.T + (int64_t)k * a.ldT + t0 + tt) : 0.f;
+    auto load_strip = [&](int t0) {  // Tt[tt][k] = T[t0 + tt][k] (= T[k][t0 + tt], T symmetric), zero padded
+        const int tq4 = tq / 4, ldT4 = (int)(a.ldT / 4);
+        for (int i = tid; i < TILE_T * tq4; i += SMALL_THREADS) {
+            const int tt = i / tq4, k4 = i % tq4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t0 + tt < q && 4 * k4 < q) {
+                v = __ldg(reinterpret_cast<const float4 *>(a.T) + (int64_t)(t0 + tt) * ldT4 + k4);
+                if (4 * k4 + 1 >= q) v.y = 0.f;
+                if (4 * k4 + 2 >= q) v.z = 0.f;
+                if (4 * k4 + 3 >= q) v.w = 0.f;
+            }
+            reinterpret_cast<float4 *>(Tt)[i] = v;
         }
     };
     if (resident && (int)blockIdx.x < ntiles) load_strip(((int)blockIdx.x % ntt) * TILE_T);
@@ -144,61 +198,102 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         SMALL_MARK(0)
         const float bf = (float)beta;
         const bool first = it == 0;  // p_1 = r_0 = y is already in p
-        // ---- A: the pair matrix of p_k, one entry per thread (runs of duplicate cells summed by their
-        //      head entry in entry order; p_k = r_k + beta p_{k-1} formed on the fly)
-        for (int64_t k = gtid; k < a.nnz; k += gthreads) {
-            const int32_t h = a.row[k], cc = a.col[k];
-            const bool head = k == 0 || a.row[k - 1] != h || a.col[k - 1] != cc;
-            if (!head) continue;
-            float v = 0.f;
-            for (int64_t j = k; j < a.nnz && a.row[j] == h && a.col[j] == cc; j++) {
-                const int32_t sj = a.src[j];
-                const float pk = first ? __ldcg(a.p + sj) : fmaf(bf, __ldcg(a.p + sj), __ldcg(a.r + sj));
-                v = fmaf(a.sign[j], pk, v);
-            }
-            a.X[(int64_t)h * a.ldX + cc] = v;
-        }
         SMALL_MARK(1)
-        grid_sync(a.bar, gen);
         SMALL_MARK(2)
-        // ---- B: S[t][h] = sum_col T[col][t] X[h][col]; tile = 32 consecutive t (lanes) x 8 h (warps), the
-        //      T strip resident in shared memory, the tile's 8 X rows staged by coalesced loads
+        // ---- A + B per tile (32 consecutive t as lanes x 8 h as warps): the tile's 8 pair-matrix rows of p_k
+        //      built in shared memory from their CSR entries (precomputed cell codes; a run of duplicate
+        //      cells summed by its head in entry order; p_k = r_k + beta p_{k-1} formed on the fly), then
+        //      S[t][h] = sum_col T[col][t] X[h][col] with 16-byte shared loads of the T strip row (lane)
+        //      and the X row (warp, broadcast): four FMAs per two loads
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int t0 = (tile % ntt) * TILE_T, h0 = (tile / ntt) * TILE_H;
+            const int h1 = h0 + TILE_H < m ? h0 + TILE_H : m;
             if (!resident) load_strip(t0);
-            float *Xs = work;
-            for (int i = tid; i < TILE_H * q; i += SMALL_THREADS) {
-                const int hh = i / q, k = i % q;
-                Xs[i] = (h0 + hh < m) ? __ldcg(a.X + (int64_t)(h0 + hh) * a.ldX + k) : 0.f;
+            float *Xs = work;  // 8 rows of ldX floats
+            for (int i = tid; i < TILE_H * q4; i += SMALL_THREADS)
+                reinterpret_cast<float4 *>(Xs)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncthreads();
+            const int64_t kb = a.row_ptr[h0], ke = a.row_ptr[h1];
+            constexpr int U = 8;  // entries in flight per thread: their loads are independent
+            for (int64_t k0 = kb + tid; k0 < ke; k0 += U * SMALL_THREADS) {
+                uint32_t cd[U];
+                int32_t sx[U];
+                float sg[U], pp[U], rr[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t k = k0 + (int64_t)u * SMALL_THREADS;
+                    cd[u] = k < ke ? a.cell[k] : CELL_DUP;  // (past the range: a non-head, skipped)
+                    sx[u] = k < ke ? a.src[k] : 0;
+                    sg[u] = k < ke ? a.sign[k] : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    pp[u] = __ldcg(a.p + sx[u]);
+                    rr[u] = first ? 0.f : __ldcg(a.r + sx[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (!(cd[u] & CELL_DUP)) Xs[cd[u]] = fmaf(sg[u], first ? pp[u] : fmaf(bf, pp[u], rr[u]), 0.f);
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                const int64_t k = k0 + (int64_t)u * SMALL_THREADS;
+                const uint32_t code = cd[u];
+                if (k >= ke || !(code & CELL_DUP)) continue;
+                const float pk = first ? pp[u] : fmaf(bf, pp[u], rr[u]);
+                if (code & CELL_HEAD) {
+                    const uint32_t cellid = code & CELL_MASK;
+                    float v = fmaf(a.sign[k], pk, 0.f);
+                    for (int64_t jx = k + 1; jx < ke && (a.cell[jx] & CELL_MASK) == cellid; jx++) {
+                        const int32_t sj = a.src[jx];
+                        const float px = first ? __ldcg(a.p + sj) : fmaf(bf, __ldcg(a.p + sj), __ldcg(a.r + sj));
+                        v = fmaf(a.sign[jx], px, v);
+                    }
+                    Xs[cellid] = v;
+                }
+                }
             }
             __syncthreads();
-            const float *xr = Xs + (size_t)warp * q;
+            const float4 *tr = reinterpret_cast<const float4 *>(Tt + (size_t)lane * tq);
+            const float4 *xr = reinterpret_cast<const float4 *>(Xs + (size_t)warp * a.ldX);
             float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-            int k = 0;
-            for (; k + 3 < q; k += 4) {  // four independent chains
-                acc0 = fmaf(Tsm[k * TILE_T + lane], xr[k], acc0);
-                acc1 = fmaf(Tsm[(k + 1) * TILE_T + lane], xr[k + 1], acc1);
-                acc2 = fmaf(Tsm[(k + 2) * TILE_T + lane], xr[k + 2], acc2);
-                acc3 = fmaf(Tsm[(k + 3) * TILE_T + lane], xr[k + 3], acc3);
+#pragma unroll 4
+            for (int k4 = 0; k4 < q4; k4++) {
+                const float4 tv = tr[k4], xv = xr[k4];
+                acc0 = fmaf(tv.x, xv.x, acc0);
+                acc1 = fmaf(tv.y, xv.y, acc1);
+                acc2 = fmaf(tv.z, xv.z, acc2);
+                acc3 = fmaf(tv.w, xv.w, acc3);
             }
-            for (; k < q; k++) acc0 = fmaf(Tsm[k * TILE_T + lane], xr[k], acc0);
             const int t = t0 + lane, h = h0 + warp;
             if (t < q && h < m) a.S[(int64_t)t * a.ldS + h] = (acc0 + acc1) + (acc2 + acc3);
             __syncthreads();
         }
         SMALL_MARK(3)
-        grid_sync(a.bar, gen);
+        grid_sync(a.bar, gen, a.bar_mode);
         SMALL_MARK(4)
-        // ---- C: stage 2 + ridge term, thread per sample on shared-memory copies of S (q x m) and D (m x m)
-        //      (odd row strides: the rows of a warp's samples fall in different banks); the owner of dst
-        //      stores p_k
-        float *Ss = work, *Ds = Dsm;
-        for (int i = tid; i < q * m; i += SMALL_THREADS) Ss[(i / m) * ldsm + i % m] = __ldcg(a.S + (int64_t)(i / m) * a.ldS + i % m);
-        __syncthreads();
-        SMALL_MARK(5)
+        // ---- C: stage 2 + ridge term.  The samples are sorted by their S row c (small_cg) and split
+        //      into equal contiguous ranges, one per CTA, so a CTA copies only the few S rows its range
+        //      uses into shared memory (odd row stride; D is resident); thread per sample, the owner of
+        //      dst stores p_k
         double pa = 0.0;
-        for (int64_t k = gtid; k < a.ns; k += gthreads) {
-            const float *drow = Ds + (int64_t)a.sr[k] * ldsm, *srow = Ss + (int64_t)a.sc[k] * ldsm;
+        {
+            const int64_t k0 = a.ns * (int64_t)blockIdx.x / gridDim.x, k1 = a.ns * ((int64_t)blockIdx.x + 1) / gridDim.x;
+            const int c_lo = k1 > k0 ? a.sc[k0] : 0, c_hi = k1 > k0 ? a.sc[k1 - 1] : -1;
+            float *Ss = work;
+            const int s4 = (int)(a.ldS / 4);
+            for (int i = tid; i < (c_hi - c_lo + 1) * s4; i += SMALL_THREADS) {
+                const int row = i / s4, j4 = i % s4;
+                const float4 v = __ldcg(reinterpret_cast<const float4 *>(a.S + (int64_t)(c_lo + row) * a.ldS) + j4);
+                float *dst = Ss + (size_t)row * ldsm + 4 * j4;
+                if (4 * j4 < m) dst[0] = v.x;
+                if (4 * j4 + 1 < m) dst[1] = v.y;
+                if (4 * j4 + 2 < m) dst[2] = v.z;
+                if (4 * j4 + 3 < m) dst[3] = v.w;
+            }
+            __syncthreads();
+            SMALL_MARK(5)
+            for (int64_t k = k0 + tid; k < k1; k += SMALL_THREADS) {
+            const float *drow = Dsm + (int64_t)a.sr[k] * ldsm, *srow = Ss + (int64_t)(a.sc[k] - c_lo) * ldsm;
             float acc0 = 0.f, acc1 = 0.f;
             int h = 0;
             for (; h + 1 < m; h += 2) {
@@ -212,11 +307,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
             a.Ap[d] = v;
             a.p[d] = pk;
             pa += (double)pk * (double)v;
+            }
         }
         pa = block_sum(pa);
         if (tid == 0) part1[blockIdx.x] = pa;
         SMALL_MARK(6)
-        grid_sync(a.bar, gen);
+        grid_sync(a.bar, gen, a.bar_mode);
         SMALL_MARK(7)
         pap = reduce_parts_cg(part1, gridDim.x);
         if (tid == 0) bcast = pap;
@@ -239,7 +335,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         rr = block_sum(rr);
         if (tid == 0) part2[blockIdx.x] = rr;
         SMALL_MARK(8)
-        grid_sync(a.bar, gen);
+        grid_sync(a.bar, gen, a.bar_mode);
         SMALL_MARK(9)
         double rho1 = reduce_parts_cg(part2, gridDim.x);
         if (tid == 0) bcast = rho1;
@@ -266,11 +362,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     }
 }
 
-// shared memory: T strip (q x 32) + D (m x ld) + the larger work area (X rows 8 x q, or S q x ld)
+// shared memory: T strip (32 x tq) + D (m x ld) + the larger work area (X rows 8 x ldX, or S q x ld)
 static size_t small_smem(int64_t m, int64_t q) {
-    const int64_t ld = m | 1;
-    const int64_t wk = TILE_H * q > q * ld ? TILE_H * q : q * ld;
-    return sizeof(float) * (size_t)(q * TILE_T + m * ld + wk);
+    const int64_t ld = m | 1, tq = round_up(q, 32) + 4;
+    const int64_t xq = TILE_H * round_up(q, 4), wk = xq > q * ld ? xq : q * ld;
+    return sizeof(float) * (size_t)(round_up(TILE_T * tq + m * ld, 4) + wk);
 }
 
 // dense stage-1 FMAs per iteration (m x q x q) at most 6.4e7, and S, D fit one CTA's shared memory
@@ -298,7 +394,7 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
         const char *e = getenv("GVT_SMALL_GRID");
         return e ? atoi(e) : 0;
     }();
-    int grid = (int)std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, 1), 1 << 16);
+    int grid = (int)std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, 1), BAR_GROUP * 64);
     if (env_grid > 0) grid = std::min(grid, env_grid);
     SmallArgs a;
     a.T = T.p;
@@ -314,28 +410,47 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     a.sign = e.sign;
     a.nnz = e.nnz;
     a.ns = sp.ns;
-    a.sr = sp.r;
-    a.sc = sp.c;
-    a.sdst = sp.dst;
+    {  // samples sorted by (c, r): contiguous per-CTA ranges touch few S rows (phase C)
+        const int64_t ns = sp.ns;
+        int32_t *perm = wsT<int32_t>(c, "small.perm", (size_t)ns);
+        int32_t *sr = wsT<int32_t>(c, "small.sr", (size_t)ns), *sc = wsT<int32_t>(c, "small.sc", (size_t)ns),
+                *sd = wsT<int32_t>(c, "small.sd", (size_t)ns);
+        sort_pairs(c, sp.c, sp.r, ns, q, m, perm);
+        gather_i32(c, sp.r, perm, ns, sr);
+        gather_i32(c, sp.c, perm, ns, sc);
+        gather_i32(c, sp.dst, perm, ns, sd);
+        a.sr = sr;
+        a.sc = sc;
+        a.sdst = sd;
+    }
     a.y = y;
     a.x = x;
     a.n = (int)n;
     a.ldX = round_up(q, 4);
-    a.X = wsT<float>(c, "small.X", (size_t)m * a.ldX);
+    {
+        uint32_t *cell = wsT<uint32_t>(c, "small.cell", (size_t)e.nnz);
+        if (e.nnz) GVT_LAUNCH(c, K_PLAN_KEYS, k_small_cells, grid1d(e.nnz, 256, 8 * c->sm_count * 8), 256, 0, e.row,
+                              e.col, e.nnz, a.ldX, cell);
+        a.cell = cell;
+    }
     a.ldS = round_up(m, 4);
     a.S = wsT<float>(c, "small.S", (size_t)q * a.ldS);
     a.p = wsT<float>(c, "small.p", (size_t)n);
     a.r = wsT<float>(c, "small.r", (size_t)n);
     a.Ap = wsT<float>(c, "small.Ap", (size_t)n);
     a.part = wsT<double>(c, "small.part", (size_t)2 * grid);
-    a.bar = wsT<unsigned>(c, "small.bar", 2);
+    a.bar = wsT<unsigned>(c, "small.bar", BAR_WORDS);
+    static const int env_bar = [] {
+        const char *e = getenv("GVT_SMALL_BAR");
+        return e ? atoi(e) : 0;
+    }();
+    a.bar_mode = env_bar;
     a.lambda = (float)lambda;
     a.max_iter = max_iter;
     a.tol = tol;
     a.state = state;
     a.relres = state + SS_N;
-    GVT_CUDA_TRY(cudaMemsetAsync(a.X, 0, sizeof(float) * (size_t)m * a.ldX, c->stream));
-    GVT_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), c->stream));
+    GVT_CUDA_TRY(cudaMemsetAsync(a.bar, 0, BAR_WORDS * sizeof(unsigned), c->stream));
     static const bool prof = getenv("GVT_SMALL_PROF") != nullptr;
     a.prof = prof ? wsT<unsigned long long>(c, "small.prof", 80) : nullptr;
     if (prof) GVT_CUDA_TRY(cudaMemsetAsync(a.prof, 0, 80 * sizeof(unsigned long long), c->stream));
@@ -349,7 +464,7 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
         unsigned long long h[80];
         GVT_CUDA_TRY(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-        const char *nm[9] = {"A", "bar1", "B", "bar2", "Ccopy", "C", "bar3", "D", "bar4"};
+        const char *nm[9] = {"-", "-", "AB", "bar2", "Ccopy", "C", "bar3", "D", "bar4"};
         for (int it = 1; it < 8 && it < max_iter; it++) {
             fprintf(stderr, "small_cg it %d:", it);
             for (int j = 0; j < 9; j++) fprintf(stderr, " %s %.2f", nm[j], (h[it * 10 + j + 1] - h[it * 10 + j]) * 1e-3);

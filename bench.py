@@ -391,10 +391,11 @@ def configs_leg(local_rank, steps=5, warmup=3):
             ctx.reset_stats()
             ms = timed(step, steps)
             launches = ctx.stats()["launches"] / steps
-            engine = {1: "sparse", 2: "dense", 3: "single-CTA", 4: "persistent"}.get(ctx.stats()["last_engine"])
             k1, k0 = w.iters, w.iters // 2
             fit = lambda k: ctx.fit(D, T, f, s_, y, terms, w.lam, k, 0.0, out=a, want_history=False)  # noqa: E731
             fit(k0), fit(k1)
+            # the engine of the fit (the step's last call is the predict, which may take another engine)
+            engine = {1: "sparse", 2: "dense", 3: "single-CTA", 4: "persistent"}.get(ctx.stats()["last_engine"])
             t0 = min(timed(lambda: fit(k0)) for _ in range(3))
             t1 = min(timed(lambda: fit(k1)) for _ in range(3))
             us_iter = 1e3 * (t1 - t0) / (k1 - k0)

@@ -1313,7 +1313,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         if (use3 || use4) {
             const GroupPlan &g = mp.groups[0];
             if (use3) tiny_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
-            else small_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state);
+            else small_cg(c, P.D, P.T, g.ent, g.smp, P.m, P.q, yd, x, n, lambda, max_iter, rel_tol, state, true);
             c->last_engine = use3 ? 3 : 4;
             double hs[9];
             GVT_CUDA_TRY(cudaMemcpyAsync(hs, state, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));

@@ -246,7 +246,8 @@ void es_evaluate(gvt_ctx *c, AucPlan &a, const float *scores_full, double *state
 // ---- persistent multi-CTA whole-fit CG for small Kronecker problems (small.cu)
 bool small_eligible(int64_t m, int64_t q, int64_t n);
 void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
-              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state);
+              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state,
+              bool keep_dir = false);
 
 // ---- single-CTA whole-fit CG for small Kronecker problems (tiny.cu)
 size_t tiny_smem(int64_t m, int64_t q, int64_t n);  // 0 if it does not fit one SM

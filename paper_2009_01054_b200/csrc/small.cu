@@ -362,6 +362,16 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
     }
 }
 
+// the direction the next iteration would use, p_{k+1} = r_k + beta_k p_k (gvt_solver_direction; the
+// solver forms it on the fly, so it is materialised once after the launch, in the same fmaf form)
+__global__ void k_small_direction(const float *__restrict__ p, const float *__restrict__ r,
+                                  const double *__restrict__ state, int64_t n, float *__restrict__ out) {
+    const float bf = (float)state[SS_BETA];
+    const bool fresh = state[SS_ITERS] == 0.0;  // no iteration ran: p_1 = y, still in p
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = fresh ? p[i] : fmaf(bf, p[i], r[i]);
+}
+
 // shared memory: T strip (32 x tq) + D (m x ld) + the larger work area (X rows 8 x ldX, or S q x ld)
 static size_t small_smem(int64_t m, int64_t q) {
     const int64_t ld = m | 1, tq = round_up(q, 32) + 4;
@@ -376,7 +386,8 @@ bool small_eligible(int64_t m, int64_t q, int64_t n) {
 }
 
 void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, const SamplePlan &sp, int64_t m,
-              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state) {
+              int64_t q, const float *y, float *x, int64_t n, double lambda, int max_iter, double tol, double *state,
+              bool keep_dir) {
     GVT_REQUIRE(small_eligible(m, q, n), GVT_E_STATE, "problem outside the persistent small solver's range");
     const size_t smem = small_smem(m, q);
     static size_t attr[GVT_MAX_DEVICES] = {};
@@ -460,6 +471,13 @@ void small_cg(gvt_ctx *c, const Factor &D, const Factor &T, const EntryPlan &e, 
     GVT_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_small_cg, dim3(grid), dim3(SMALL_THREADS), args, smem,
                                              c->stream));
     launch_end(c, K_TINY, ev);
+    if (keep_dir) {
+        float *dir = wsT<float>(c, "small.dir", (size_t)n);
+        if (n) GVT_LAUNCH(c, K_CG_VEC, k_small_direction, grid1d(n, 256, 2 * c->sm_count), 256, 0, a.p, a.r, state,
+                          n, dir);
+        c->last_p = dir;
+        c->last_n = n;
+    }
     if (prof) {  // phase durations (us) of iterations 1..7 of CTA 0, to stderr (diagnosis only)
         unsigned long long h[80];
         GVT_CUDA_TRY(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, c->stream));

@@ -10,6 +10,6 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 if [ "${NCU:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-gather-regime > $OUT/ncu_bench.log 2>&1; echo "ncu rc=$?" >> $OUT/ncu_bench.log
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-gather-regime --no-configs > $OUT/ncu_bench.log 2>&1; echo "ncu rc=$?" >> $OUT/ncu_bench.log
 fi
 tail -3 $OUT/pytest_gpu.log $OUT/smoke.log; cat $OUT/bench.json; tail -3 $OUT/bench.err

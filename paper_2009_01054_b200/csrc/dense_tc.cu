@@ -155,6 +155,12 @@ __device__ __forceinline__ void tmem_ld8_raw(uint32_t taddr, uint32_t (&r)[8]) {
                  : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld4_raw(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float tf32_round(float x) {
@@ -212,9 +218,9 @@ struct EpiParams {
 #ifndef SERVE_UNROLL
 #define SERVE_UNROLL 1
 #endif
+template <int STRIDE>  // the epilogue threads serving (32 x epilogue warps)
 __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
                                               const float *stage) {
-    constexpr int STRIDE = 256;  // 32 * N_EPI_WARPS epilogue threads
     constexpr int U = SERVE_UNROLL;
     for (int64_t k0 = kb0 + t; k0 < ke; k0 += U * STRIDE) {
         int rl[U], cl[U];
@@ -255,6 +261,7 @@ static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == BM, "S scale block = one 
 // Measured (profiles/r01_ab_serve_unroll.txt): 4 in flight cut C2 from 95 to 83 us per iteration
 // but raised the CTA-pair kernel's register spills (172 -> 556 B) and C5's stage 2 from 43 to
 // 50 ms, so 1 is the default.
+template <int STRIDE>
 __device__ __forceinline__ void serve_samples(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0,
                                               int gc0, const float *stage);
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
@@ -485,7 +492,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int64_t cidx = tile * (BN / 32) + chunk;
                     const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                     const int gc0 = n0 + chunk * 32;
-                    serve_samples(ep, kb0, ke, t, m0, gc0, stage + hh * 4 * 32 * 33);
+                    serve_samples<256>(ep, kb0, ke, t, m0, gc0, stage + hh * 4 * 32 * 33);
                 }
                 named_bar(1, 32 * N_EPI_WARPS);
             }
@@ -571,8 +578,18 @@ __host__ __device__ constexpr uint32_t idesc_mma2() {
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
+// epilogue warps of the sampled (stage-2) CTA-pair kernel: 16 halve each thread's share of the per-chunk
+// TMEM drain (64 columns instead of 128, at <= 112 registers), so the drain of one 256-wide K chunk
+// finishes well inside the next chunk's MMAs; -DSAMPLED_EPI_WARPS=8 restores the round-1 layout (A/B)
+#ifndef SAMPLED_EPI_WARPS
+#define SAMPLED_EPI_WARPS 16
+#endif
+static_assert(SAMPLED_EPI_WARPS == 8 || SAMPLED_EPI_WARPS == 16, "sampled epilogue: 8 or 16 warps");
+__host__ __device__ constexpr int pair_epi_warps(int epi) { return epi == EPI_SAMPLED ? SAMPLED_EPI_WARPS : N_EPI_WARPS; }
+__host__ __device__ constexpr int pair_threads(int epi) { return 64 + 32 * pair_epi_warps(epi); }
+
 template <int PREC, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1)
     k_gemm2_x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M, int N, int K,
                EpiParams ep) {
@@ -630,7 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 2 * N_EPI_WARPS);
+            mbar_init(&tempty[b], 2 * pair_epi_warps(EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -705,6 +722,122 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     }
                     mma_commit_pair(&tfull[b]);      // chunk accumulator ready in both CTAs
                 }
+            }
+        }
+    } else if constexpr (EPI == EPI_SAMPLED) {
+        // ---------------- sampled epilogue, warps 2..(NE+1) (both CTAs, own 128 rows): warp w reads TMEM
+        // lanes 32*(w%4).. and the CW columns of column group (w-2)/4; per K chunk the accumulator is
+        // drained into fp32 registers with round-to-nearest adds (times S's chunk scale), then the tile's
+        // samples are served from a shared-memory copy, two 32-column chunks at a time
+        constexpr int NE = SAMPLED_EPI_WARPS, CW = 1024 / NE, SG = CW / 32;
+        const int ew = warp - 2;
+        const int quarter = warp & 3;
+        const int colg = ew >> 2;
+        const int row = quarter * 32 + lane;
+        const int tE = threadIdx.x - 64;
+        int cg = 0;
+        for (int t = cluster; t < n_tiles; t += n_clusters) {
+            int mp_tile, n_tile;
+            coords(t, mp_tile, n_tile);
+            if (skip(mp_tile, n_tile)) continue;
+            const int m_tile = 2 * mp_tile + (int)crank;
+            const int m0 = m_tile * BM, n0 = n_tile * BN;
+            const int gr = m0 + row;
+            const int gc_base = n0 + colg * CW;
+            float run[CW];
+#pragma unroll
+            for (int i = 0; i < CW; i++) run[i] = 0.f;
+            const int nch_t = (tile_nk(n_tile) + kcb - 1) / kcb;
+            for (int ch = 0; ch < nch_t; ch++, cg++) {
+                const int b = cg & 1;
+                mbar_wait(&tfull[b], (cg >> 1) & 1);
+                tc_fence_after();
+                const uint32_t ta = tmem + b * BN + colg * CW + ((uint32_t)(quarter * 32) << 16);
+#if S16_SCALE_ROWS == 128
+                if (ep.sbk) {  // one scale per (128 S rows, K chunk): a scalar for this thread's columns
+                    const float skv = __ldg(ep.sbk + (int64_t)ch * ep.sbk_ld + (gc_base >> 7));
+#pragma unroll
+                    for (int c16 = 0; c16 < CW / 16; c16++) {
+                        uint32_t r[16];
+                        tmem_ld16_raw(ta + c16 * 16, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) run[c16 * 16 + i] = fmaf(__uint_as_float(r[i]), skv, run[c16 * 16 + i]);
+                    }
+                } else
+#else
+                if (ep.sbk) {  // per-(column, K chunk) scales: DW-column TMEM loads next to DW/4 scale vectors
+                    constexpr int DW = CW >= 128 ? 8 : 4;  // (16 warps: 96 registers, run[64] + 8 temporaries)
+                    const float *sk = ep.sbk + (int64_t)ch * ep.sbk_ld + gc_base;
+#pragma unroll
+                    for (int c8 = 0; c8 < CW / DW; c8++) {
+                        uint32_t r[DW];
+                        float4 v[DW / 4];
+                        if constexpr (DW == 8) tmem_ld8_raw(ta + c8 * 8, *reinterpret_cast<uint32_t(*)[8]>(r));
+                        else tmem_ld4_raw(ta + c8 * 4, *reinterpret_cast<uint32_t(*)[4]>(r));
+                        const float4 *sk4 = reinterpret_cast<const float4 *>(sk + c8 * DW);
+#pragma unroll
+                        for (int u = 0; u < DW / 4; u++) v[u] = __ldg(sk4 + u);
+                        tmem_wait_ld();
+                        float *rr = run + c8 * DW;
+#pragma unroll
+                        for (int u = 0; u < DW / 4; u++) {
+                            rr[4 * u + 0] = fmaf(__uint_as_float(r[4 * u + 0]), v[u].x, rr[4 * u + 0]);
+                            rr[4 * u + 1] = fmaf(__uint_as_float(r[4 * u + 1]), v[u].y, rr[4 * u + 1]);
+                            rr[4 * u + 2] = fmaf(__uint_as_float(r[4 * u + 2]), v[u].z, rr[4 * u + 2]);
+                            rr[4 * u + 3] = fmaf(__uint_as_float(r[4 * u + 3]), v[u].w, rr[4 * u + 3]);
+                        }
+                    }
+                } else
+#endif
+                {
+#pragma unroll
+                    for (int c16 = 0; c16 < CW / 16; c16++) {
+                        uint32_t r[16];
+                        tmem_ld16_raw(ta + c16 * 16, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) run[c16 * 16 + i] += __uint_as_float(r[i]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(&tempty[b]);
+            }
+            if (ep.sa || ep.sb) {
+                const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+#pragma unroll
+                for (int i = 0; i < CW; i++) {
+                    const int gc = gc_base + i;
+                    const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                    run[i] *= ra * rb;
+                }
+            }
+            // chunk c (32 columns) lives in column group c / SG, sub-block c % SG; step j serves chunks j and
+            // j + 4 (staging slots hh = 0, 1 of 4 x 32 x 33 floats each)
+            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+            const bool tile_ok = m_tile < num_m;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int g0 = j / SG, g1 = (j + 4) / SG;
+                if (colg == g0 || colg == g1) {
+                    const int hh = colg == g1 ? 1 : 0;
+                    float *mine = estage + (hh * 4 + quarter) * 32 * 33 + lane * 33;
+#pragma unroll
+                    for (int i = 0; i < 32; i++) mine[i] = run[(j % SG) * 32 + i];
+                }
+                named_bar(1, 32 * NE);
+                if (tile_ok) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; hh++) {
+                        const int chunk = hh * 4 + j;
+                        const int64_t cidx = tile * (BN / 32) + chunk;
+                        const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
+                        const int gc0 = n0 + chunk * 32;
+                        serve_samples<32 * NE>(ep, kb0, ke, tE, m0, gc0, estage + hh * 4 * 32 * 33);
+                    }
+                }
+                named_bar(1, 32 * NE);
             }
         }
     } else {  // ---------------- epilogue warps 2..9 (both CTAs, own 128 rows)
@@ -996,7 +1129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                             const int64_t cidx = tile * (BN / 32) + chunk;
                             const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                             const int gc0 = n0 + chunk * 32;
-                            serve_samples(ep, kb0, ke, t256, m0, gc0, estage + hh * 4 * 32 * 33);
+                            serve_samples<256>(ep, kb0, ke, t256, m0, gc0, estage + hh * 4 * 32 * 33);
                         }
                     }
                     named_bar(1, 32 * N_EPI_WARPS);
@@ -1087,7 +1220,7 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
         const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
         const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
         dim3 grid((unsigned)(2 * clusters));
-        GVT_LAUNCH(c, kind_id, (k_gemm2_x3<PREC, EPI>), grid, NTHREADS, SMEM2_TOTAL, ah, al, bh, bl, (int)M, (int)N,
+        GVT_LAUNCH(c, kind_id, (k_gemm2_x3<PREC, EPI>), grid, pair_threads(EPI), SMEM2_TOTAL, ah, al, bh, bl, (int)M, (int)N,
                    (int)K, ep);
         return;
     }

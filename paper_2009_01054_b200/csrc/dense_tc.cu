@@ -27,6 +27,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <vector>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -210,7 +213,18 @@ struct EpiParams {
     __half *c_h16, *c_l16;
     float *c_sk;
     int64_t c_sk_ld;
+    // diagnosis (GVT_GEMM_PROF): per CTA, globaltimer stamps [entry, setup done, first stage landed,
+    // last MMA commit, last TMA issued, last chunk drained, epilogue done, -]
+    unsigned long long *prof;
 };
+
+__device__ __forceinline__ unsigned long long gemm_timer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GEMM_MARK(slot) \
+    if (ep.prof) ep.prof[blockIdx.x * 16 + (slot)] = gemm_timer();
 
 #ifndef DRAIN_X16
 #define DRAIN_X16 1
@@ -597,6 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     // The smem ring position, the accumulator-chunk parity and the skip decisions advance
     // identically in the producer, MMA and epilogue roles of both CTAs, so a tile's output
     // phase overlaps the next tile's MMAs.
+    if (threadIdx.x == 0) { GEMM_MARK(0) }
     constexpr int BKE = KB_BYTES / (PREC == PREC_TF32 ? 4 : 2);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -661,6 +676,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) { GEMM_MARK(1) }
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -684,6 +700,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                     tma_load_2d_pair(st + 3 * HALF_BYTES, &tmBl, &full[s], kc, n0 + (int)crank * 128);
                 }
             }
+            GEMM_MARK(4)
         }
     } else if (warp == 1) {
         if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader only)
@@ -706,6 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                         const uint32_t ph = (kg / STAGES2) & 1;
                         mbar_wait(&full[s], ph);
                         tc_fence_after();
+                        if (kg == 0) { GEMM_MARK(2) }
                         const uint32_t base = smem_u32(smem + s * STAGE2_BYTES);
                         const uint32_t ah = base, al = base + HALF_BYTES, bh = base + 2 * HALF_BYTES,
                                        bl = base + 3 * HALF_BYTES;
@@ -723,6 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                     mma_commit_pair(&tfull[b]);      // chunk accumulator ready in both CTAs
                 }
             }
+            GEMM_MARK(3)
         }
     } else if constexpr (EPI == EPI_SAMPLED) {
         // ---------------- sampled epilogue, warps 2..(NE+1) (both CTAs, own 128 rows): warp w reads TMEM
@@ -804,6 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
+            if (threadIdx.x == 64) { GEMM_MARK(5) }
             if (ep.sa || ep.sb) {
                 const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
 #pragma unroll
@@ -840,6 +860,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 named_bar(1, 32 * NE);
             }
         }
+        if (threadIdx.x == 64) { GEMM_MARK(6) }
     } else {  // ---------------- epilogue warps 2..9 (both CTAs, own 128 rows)
         const int ew = warp - 2;
         const int quarter = warp & 3;
@@ -945,6 +966,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
+            if (threadIdx.x == 64) { GEMM_MARK(5) }
             if (EPI == EPI_STORE16) {
                 // fp16 hi/lo of the unscaled result with a power-of-two scale per (128-row CTA block,
                 // 256-col tile) from the block's maximum (S16_SCALE_ROWS = 128: a CTA-wide max over
@@ -978,6 +1000,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 mx = fmaxf(estage[(quarter * 32 + lane) * 2], estage[(quarter * 32 + lane) * 2 + 1]);
                 named_bar(1, 32 * N_EPI_WARPS);
 #endif
+                if (threadIdx.x == 64) { GEMM_MARK(8) }
                 int e = 0;
                 if (mx > 0.f && isfinite(mx)) {
                     int ex;
@@ -995,6 +1018,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 // 32 columns of (hi, lo) pairs, then the warp writes the block row by row, 64
                 // contiguous bytes per piece (a thread-per-row store pattern would touch 32 lines
                 // per instruction; it dominated the epilogue of short-K tiles)
+                if (threadIdx.x == 64) { GEMM_MARK(9) }
                 uint32_t *blk = reinterpret_cast<uint32_t *>(estage) + (half * 4 + quarter) * 32 * 33;
                 const int64_t row0 = (int64_t)m0 + quarter * 32;
 #pragma unroll
@@ -1030,6 +1054,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                     }
                     __syncwarp();
                 }
+                if (threadIdx.x == 64) { GEMM_MARK(10) }
                 // the next tile's scale exchange reuses the staging area
                 named_bar(1, 32 * N_EPI_WARPS);
                 continue;
@@ -1137,12 +1162,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             }
         }
     }
+    if (EPI != EPI_SAMPLED && threadIdx.x == 64) { GEMM_MARK(6) }
     tc_fence_before();
     cluster_sync_all();  // both CTAs done with TMEM / shared memory before the pair deallocates
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
     }
+    if (threadIdx.x == 0) { GEMM_MARK(7) }
 }
 
 
@@ -1189,6 +1216,34 @@ static CUtensorMap make_map(const void *p, int esz, int64_t rows, int64_t cols, 
 
 bool tc_available(gvt_ctx *c) { return c->tc_ok; }
 
+// GVT_GEMM_PROF: phase stamps of one CTA-pair GEMM launch, in us from the earliest CTA entry
+// (median / max over CTAs), to stderr -- diagnosis only (it synchronises the stream)
+static void gemm_prof_report(gvt_ctx *c, const unsigned long long *dprof, int grid, int epi, int64_t M, int64_t N,
+                             int64_t K) {
+    cudaStreamCaptureStatus cs;
+    GVT_CUDA_TRY(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return;  // (run with OPT_PROFILE: no graph)
+    std::vector<unsigned long long> h((size_t)grid * 16);
+    GVT_CUDA_TRY(cudaMemcpyAsync(h.data(), dprof, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < grid; b++) t0 = std::min(t0, h[(size_t)b * 16]);
+    static const char *nm[11] = {"entry", "setup", "first_stage", "last_mma", "last_tma", "drained", "epi_done", "exit",
+                                 "scaled", "sk", "stored"};
+    fprintf(stderr, "gemm_prof epi=%d M=%lld N=%lld K=%lld grid=%d:", epi, (long long)M, (long long)N, (long long)K,
+            grid);
+    for (int sl = 0; sl < 11; sl++) {
+        std::vector<double> v;
+        for (int b = 0; b < grid; b++)
+            if (h[(size_t)b * 16 + sl]) v.push_back((h[(size_t)b * 16 + sl] - t0) * 1e-3);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, " %s %.1f/%.1f", nm[sl], v[v.size() / 2], v.back());
+    }
+    fprintf(stderr, "\n");
+}
+
 template <int PREC, int EPI>
 static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Operand &B, int64_t M, int64_t N,
                           int64_t K, EpiParams ep) {
@@ -1220,8 +1275,14 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
         const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
         const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
         dim3 grid((unsigned)(2 * clusters));
+        static const bool prof = getenv("GVT_GEMM_PROF") != nullptr;
+        if (prof) {
+            ep.prof = wsT<unsigned long long>(c, "gemm.prof", (size_t)grid.x * 16);
+            GVT_CUDA_TRY(cudaMemsetAsync(ep.prof, 0, sizeof(unsigned long long) * grid.x * 16, c->stream));
+        }
         GVT_LAUNCH(c, kind_id, (k_gemm2_x3<PREC, EPI>), grid, pair_threads(EPI), SMEM2_TOTAL, ah, al, bh, bl, (int)M, (int)N,
                    (int)K, ep);
+        if (prof) gemm_prof_report(c, ep.prof, (int)grid.x, EPI, M, N, K);
         return;
     }
     if (!attr[dv]) {

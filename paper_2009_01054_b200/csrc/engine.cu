@@ -733,21 +733,21 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         run_group(c, P, g, p, 2.f, 0, u, true);
         segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
         segment_sum_gather(c, mp.byS, p, mp.b2);  // bS
-        gemv(c, P.D, mp.b1, 1, mp.g1);          // D.^2 bF
-        gemv(c, P.T, mp.b2, 1, mp.g2);          // T.^2 bS
+        gemv(c, P.D, mp.b1, 1, mp.g1, !P.rect);  // D.^2 bF
+        gemv(c, P.T, mp.b2, 1, mp.g2, !P.rect);  // T.^2 bS
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
         break;
     }
     case FORM_LINEAR:
         segment_sum_gather(c, mp.byF, p, mp.b1);
         segment_sum_gather(c, mp.byS, p, mp.b2);
-        gemv(c, P.D, mp.b1, 0, mp.g1);
-        gemv(c, P.T, mp.b2, 0, mp.g2);
+        gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
+        gemv(c, P.T, mp.b2, 0, mp.g2, !P.rect);
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
         break;
     case FORM_RANKING:
         segment_sum_gather(c, mp.byF, p, mp.b1);  // bF - bS
-        gemv(c, P.D, mp.b1, 0, mp.g1);
+        gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
         combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
         break;
     case FORM_CARTESIAN:

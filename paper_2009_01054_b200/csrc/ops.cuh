@@ -138,7 +138,8 @@ void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const floa
                    float coef, int accumulate, float *out);
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)
 void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b);  // b[h] = sum_row sign p[src]
-void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y);
+// symmetric: F is a square Gram (symmetric by definition, R1) -- the upper block triangle is read
+void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y, bool symmetric = false);
 // u[i] (+)= c1 * g1[sel(rs1,i)] + c2 * g2[sel(rs2,i)]   (g2 nullable)
 void combine_gather(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *g1, int rs1, float c1,
                     const float *g2, int rs2, float c2, int accumulate, float *u);

@@ -7,6 +7,8 @@
 // C[t][col] and every access is a contiguous row segment.
 // Determinism: every output is produced by one thread/warp in a fixed order with fixed
 // shuffle trees; no floating-point atomics anywhere.
+#include <stdlib.h>
+
 #include "ops.cuh"
 
 namespace gvt {
@@ -347,8 +349,151 @@ __global__ void __launch_bounds__(256) k_gemv_smem(const float *__restrict__ F, 
     if (lane == 0) y[r] = acc;
 }
 
-void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y) {
+// ---- symmetric GEMV: y = F b (or F.^2 b) reading only the upper block triangle of a square Gram
+// (symmetric by definition, R1).  Blocks are SYMV_T x SYMV_T; block (I, J), I <= J, gives the row part
+// F_IJ b_J (to y_I) and, off the diagonal, the column part F_IJ^T b_I (to y_J).  One CTA takes SYMV_C
+// consecutive blocks I of column strip J: each warp streams 16 rows of every block (16 independent
+// 16-byte loads per lane), its row sums go straight to prow[I][J], the column parts accumulate over the
+// chunk in registers and land in pcol[J][chunk].  Output block X thus receives exactly
+// (nb - X) + ceil((X + 1) / SYMV_C) contributions; the CTA that delivers the last one (per-X arrival
+// counter) sums them in a fixed order (prow k = X..nb-1, then pcol chunks): deterministic, no float
+// atomics, half the HBM bytes of the plain GEMV (the Gram stream is what bounds it).
+constexpr int SYMV_T = 128, SYMV_C = 4;
+__device__ __forceinline__ int symv_nc(int J) { return (J + SYMV_C) / SYMV_C; }  // chunks of strip J
+
+__global__ void __launch_bounds__(256, 2) k_symv(const float *__restrict__ F, int64_t n, int64_t ld,
+                                                 const float *__restrict__ b, int square, int nb,
+                                                 float *__restrict__ prow, float *__restrict__ pcol,
+                                                 unsigned *__restrict__ arrivals, float *__restrict__ y) {
+    __shared__ float cs[8][SYMV_T];
+    __shared__ int red[SYMV_C + 1];
+    // CTA -> (strip J, chunk c): strip J holds symv_nc(J) chunks
+    int J = 0, t = blockIdx.x;
+    while (t >= symv_nc(J)) {
+        t -= symv_nc(J);
+        J++;
+    }
+    const int c = t, I0 = c * SYMV_C, I1 = min(I0 + SYMV_C, J + 1);
+    const int ncmax = symv_nc(nb - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)J * SYMV_T + 4 * lane;  // this lane's 4 columns
+    const bool jfull = (int64_t)(J + 1) * SYMV_T <= n;
+    const float4 bj = j < n ? __ldg(reinterpret_cast<const float4 *>(b + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 cacc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int I = I0; I < I1; I++) {
+        const int64_t i0 = (int64_t)I * SYMV_T + warp * 16;  // this warp's 16 rows of block (I, J)
+        float4 x[16];
+        const float *base = F + i0 * ld + j;
+        if (jfull && (int64_t)(I + 1) * SYMV_T <= n) {
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = __ldg(reinterpret_cast<const float4 *>(base + u * ld));
+        } else {
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                x[u] = (i0 + u < n && j < n) ? __ldg(reinterpret_cast<const float4 *>(base + u * ld))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (j + 1 >= n) x[u].y = 0.f;  // columns past n (padding) contribute nothing
+                if (j + 2 >= n) x[u].z = 0.f;
+                if (j + 3 >= n) x[u].w = 0.f;
+            }
+        }
+        const float bil = i0 + (lane & 15) < n ? __ldg(b + i0 + (lane & 15)) : 0.f;  // b of the 16 rows
+        const bool offdiag = I != J;
+        float rp[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            float4 v = x[u];
+            if (square) { v.x *= v.x; v.y *= v.y; v.z *= v.z; v.w *= v.w; }
+            rp[u] = fmaf(v.w, bj.w, fmaf(v.z, bj.z, fmaf(v.y, bj.y, v.x * bj.x)));
+            const float bi = offdiag ? __shfl_sync(0xffffffffu, bil, u) : 0.f;
+            cacc.x = fmaf(v.x, bi, cacc.x);
+            cacc.y = fmaf(v.y, bi, cacc.y);
+            cacc.z = fmaf(v.z, bi, cacc.z);
+            cacc.w = fmaf(v.w, bi, cacc.w);
+        }
+        // row sums over the 32 lanes, transposed butterfly: lane L ends with row (L >> 1) & 15
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1) {  // widths 8, 4, 2, 1 rows kept per lane
+            const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+            for (int k = 0; k < w; k++) {
+                const float send = up ? rp[k] : rp[k + w];
+                const float keep = up ? rp[k + w] : rp[k];
+                rp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
+            }
+        }
+        const float rsum = rp[0] + __shfl_xor_sync(0xffffffffu, rp[0], 1);
+        if ((lane & 1) == 0) prow[((int64_t)I * nb + J) * SYMV_T + warp * 16 + ((lane >> 1) & 15)] = rsum;
+    }
+    // column part of the chunk: the 8 warps' partials summed in warp order
+    *reinterpret_cast<float4 *>(&cs[warp][4 * lane]) = cacc;
+    __syncthreads();
+    if (threadIdx.x < SYMV_T) {
+        float v = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; w8++) v += cs[w8][threadIdx.x];
+        pcol[((int64_t)J * ncmax + c) * SYMV_T + threadIdx.x] = v;
+    }
+    // arrivals: the CTA completing output block X reduces it
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int I = I0; I < I1; I++) {
+            const unsigned need = (unsigned)(nb - I + symv_nc(I));
+            red[I - I0] = atomicAdd(&arrivals[I], 1u) == need - 1 ? I : -1;
+        }
+        const unsigned needJ = (unsigned)(nb - J + symv_nc(J));
+        red[SYMV_C] = atomicAdd(&arrivals[J], 1u) == needJ - 1 ? J : -1;
+    }
+    __syncthreads();
+    for (int e = 0; e <= SYMV_C; e++) {
+        if (e < SYMV_C && I0 + e >= I1) continue;
+        const int X = red[e];
+        if (X < 0) continue;
+        __threadfence();
+        if (threadIdx.x < SYMV_T) {
+            const float *pr = prow + (int64_t)X * nb * SYMV_T + threadIdx.x;
+            float v = 0.f;
+            int k = X;
+            for (; k + 8 <= nb; k += 8) {  // eight loads in flight, summed in k order
+                float t8[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) t8[u] = __ldcg(pr + (int64_t)(k + u) * SYMV_T);
+#pragma unroll
+                for (int u = 0; u < 8; u++) v += t8[u];
+            }
+            for (; k < nb; k++) v += __ldcg(pr + (int64_t)k * SYMV_T);
+            const float *pc = pcol + (int64_t)X * ncmax * SYMV_T + threadIdx.x;
+            for (int cc = 0; cc < symv_nc(X); cc++) v += __ldcg(pc + (int64_t)cc * SYMV_T);
+            const int64_t r = (int64_t)X * SYMV_T + threadIdx.x;
+            if (r < n) y[r] = v;
+        }
+        if (threadIdx.x == 0) arrivals[X] = 0u;  // ready for the next call
+    }
+}
+
+// GVT_SYMV=1 enables the symmetric (upper-triangle) GEMV: under evaluation (off by default)
+static bool symv_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("GVT_SYMV");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
+void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y, bool symmetric) {
     if (F.n == 0) return;
+    if (symmetric && symv_enabled() && F.n == F.cols && F.n >= 1024 && F.ld % 4 == 0) {
+        const int nb = (int)((F.n + SYMV_T - 1) / SYMV_T), ncmax = (nb - 1 + SYMV_C) / SYMV_C;
+        int64_t ctas = 0;
+        for (int J = 0; J < nb; J++) ctas += (J + SYMV_C) / SYMV_C;
+        float *prow = wsT<float>(c, "symv.prow", (size_t)nb * nb * SYMV_T);
+        float *pcol = wsT<float>(c, "symv.pcol", (size_t)nb * ncmax * SYMV_T);
+        unsigned *arr = wsT<unsigned>(c, "symv.arrivals", (size_t)nb);
+        GVT_CUDA_TRY(cudaMemsetAsync(arr, 0, sizeof(unsigned) * nb, c->stream));
+        GVT_LAUNCH(c, K_GEMV, k_symv, (unsigned)ctas, 256, 0, F.p, F.n, F.ld, b, square, nb, prow, pcol, arr, y);
+        return;
+    }
     const size_t smem = sizeof(float) * (size_t)F.ld;
     if (smem <= 160 * 1024 && F.ld % 4 == 0) {
         static size_t attr[GVT_MAX_DEVICES] = {};

@@ -349,127 +349,126 @@ __global__ void __launch_bounds__(256) k_gemv_smem(const float *__restrict__ F, 
     if (lane == 0) y[r] = acc;
 }
 
-// ---- symmetric GEMV: y = F b (or F.^2 b) reading only the upper block triangle of a square Gram
-// (symmetric by definition, R1).  Blocks are SYMV_T x SYMV_T; block (I, J), I <= J, gives the row part
-// F_IJ b_J (to y_I) and, off the diagonal, the column part F_IJ^T b_I (to y_J).  One CTA takes SYMV_C
-// consecutive blocks I of column strip J: each warp streams 16 rows of every block (16 independent
-// 16-byte loads per lane), its row sums go straight to prow[I][J], the column parts accumulate over the
-// chunk in registers and land in pcol[J][chunk].  Output block X thus receives exactly
-// (nb - X) + ceil((X + 1) / SYMV_C) contributions; the CTA that delivers the last one (per-X arrival
-// counter) sums them in a fixed order (prow k = X..nb-1, then pcol chunks): deterministic, no float
-// atomics, half the HBM bytes of the plain GEMV (the Gram stream is what bounds it).
-constexpr int SYMV_T = 128, SYMV_C = 4;
-__device__ __forceinline__ int symv_nc(int J) { return (J + SYMV_C) / SYMV_C; }  // chunks of strip J
+// ---- symmetric GEMV: y = F b (or F.^2 b) reading only the upper triangle of a square Gram
+// (symmetric by definition, R1), row by row, so every warp streams long contiguous row segments.
+// CTA k of G owns rows [R_k, R_k+1), split so every CTA streams the same number of upper-triangle
+// elements; thread t owns the column quads q = t + 256 u (u < SYMV_U, n <= 1024 SYMV_U).  For row i:
+//   row part    y_i  = sum_{j >= i} F_ij b_j      (8-row batches, reduced over the CTA in a fixed tree)
+//   column part c_j += F_ij b_i for j > i        (registers, per owned quad)
+// The column parts of the G CTAs are parked in pcol[G][nq4] and summed in CTA order by k_symv_finish,
+// which adds the row part: deterministic, no atomics, half the HBM bytes of the plain GEMV.
+constexpr int SYMV_U = 8, SYMV_RB = 8;
 
-__global__ void __launch_bounds__(256, 2) k_symv(const float *__restrict__ F, int64_t n, int64_t ld,
-                                                 const float *__restrict__ b, int square, int nb,
-                                                 float *__restrict__ prow, float *__restrict__ pcol,
-                                                 unsigned *__restrict__ arrivals, float *__restrict__ y) {
-    __shared__ float cs[8][SYMV_T];
-    __shared__ int red[SYMV_C + 1];
-    // CTA -> (strip J, chunk c): strip J holds symv_nc(J) chunks
-    int J = 0, t = blockIdx.x;
-    while (t >= symv_nc(J)) {
-        t -= symv_nc(J);
-        J++;
+__device__ __forceinline__ int64_t symv_row_bound(int64_t n, int k, int G) {
+    // first row of CTA k: sum_{i < R} (n - i) = k / G of the n (n + 1) / 2 upper-triangle elements
+    if (k <= 0) return 0;
+    if (k >= G) return n;
+    const double W = 0.5 * (double)n * (double)(n + 1), nn = (double)n + 0.5;
+    double R = nn - sqrt(fmax(nn * nn - 2.0 * W * (double)k / (double)G, 0.0));
+    int64_t r = (int64_t)R;
+    return r < 0 ? 0 : (r > n ? n : r);
+}
+
+__global__ void __launch_bounds__(256, 2) k_symv_rows(const float *__restrict__ F, int64_t n, int64_t ld,
+                                                      const float *__restrict__ b, int square,
+                                                      float *__restrict__ rowpart, float *__restrict__ pcol) {
+    __shared__ float red[8][SYMV_RB];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = gridDim.x, k = blockIdx.x;
+    const int64_t r0 = symv_row_bound(n, k, G), r1 = symv_row_bound(n, k + 1, G);
+    const int64_t nq = (n + 3) / 4;
+    float4 bq[SYMV_U], cacc[SYMV_U];
+#pragma unroll
+    for (int u = 0; u < SYMV_U; u++) {
+        const int64_t q = tid + 256 * u;
+        bq[u] = q < nq ? __ldg(reinterpret_cast<const float4 *>(b) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        cacc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int c = t, I0 = c * SYMV_C, I1 = min(I0 + SYMV_C, J + 1);
-    const int ncmax = symv_nc(nb - 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t j = (int64_t)J * SYMV_T + 4 * lane;  // this lane's 4 columns
-    const bool jfull = (int64_t)(J + 1) * SYMV_T <= n;
-    const float4 bj = j < n ? __ldg(reinterpret_cast<const float4 *>(b + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 cacc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int I = I0; I < I1; I++) {
-        const int64_t i0 = (int64_t)I * SYMV_T + warp * 16;  // this warp's 16 rows of block (I, J)
-        float4 x[16];
-        const float *base = F + i0 * ld + j;
-        if (jfull && (int64_t)(I + 1) * SYMV_T <= n) {
+    for (int64_t ib = r0; ib < r1; ib += SYMV_RB) {
+        float rp[SYMV_RB];
 #pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = __ldg(reinterpret_cast<const float4 *>(base + u * ld));
-        } else {
+        for (int r = 0; r < SYMV_RB; r++) {
+            const int64_t i = ib + r;
+            rp[r] = 0.f;
+            if (i >= r1) continue;
+            const int64_t q0 = i >> 2;
+            const float *row = F + i * ld;
+            float4 x[SYMV_U];
 #pragma unroll
-            for (int u = 0; u < 16; u++) {
-                x[u] = (i0 + u < n && j < n) ? __ldg(reinterpret_cast<const float4 *>(base + u * ld))
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (j + 1 >= n) x[u].y = 0.f;  // columns past n (padding) contribute nothing
-                if (j + 2 >= n) x[u].z = 0.f;
-                if (j + 3 >= n) x[u].w = 0.f;
+            for (int u = 0; u < SYMV_U; u++) {
+                const int64_t q = tid + 256 * u;
+                x[u] = (q >= q0 && q < nq) ? __ldg(reinterpret_cast<const float4 *>(row) + q)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float bi = __ldg(b + i);
+#pragma unroll
+            for (int u = 0; u < SYMV_U; u++) {
+                const int64_t q = tid + 256 * u;
+                float4 v = x[u];
+                if (square) { v.x *= v.x; v.y *= v.y; v.z *= v.z; v.w *= v.w; }
+                // elements past n are zero (b and the masked loads); the quad holding the diagonal:
+                // j < i excluded, j = i in the row part only
+                float4 w = v;  // column part (j > i)
+                if (q == q0) {
+                    const int e = (int)(i - 4 * q0);
+                    if (e > 0) v.x = 0.f;
+                    if (e > 1) v.y = 0.f;
+                    if (e > 2) v.z = 0.f;
+                    w = v;
+                    if (e == 0) w.x = 0.f;
+                    if (e == 1) w.y = 0.f;
+                    if (e == 2) w.z = 0.f;
+                    if (e == 3) w.w = 0.f;
+                }
+                if (4 * q + 1 >= n) { v.y = 0.f; w.y = 0.f; }
+                if (4 * q + 2 >= n) { v.z = 0.f; w.z = 0.f; }
+                if (4 * q + 3 >= n) { v.w = 0.f; w.w = 0.f; }
+                rp[r] = fmaf(v.w, bq[u].w, fmaf(v.z, bq[u].z, fmaf(v.y, bq[u].y, fmaf(v.x, bq[u].x, rp[r]))));
+                cacc[u].x = fmaf(w.x, bi, cacc[u].x);
+                cacc[u].y = fmaf(w.y, bi, cacc[u].y);
+                cacc[u].z = fmaf(w.z, bi, cacc[u].z);
+                cacc[u].w = fmaf(w.w, bi, cacc[u].w);
             }
         }
-        const float bil = i0 + (lane & 15) < n ? __ldg(b + i0 + (lane & 15)) : 0.f;  // b of the 16 rows
-        const bool offdiag = I != J;
-        float rp[16];
+        // row parts of the batch: warp trees, then the 8 warps in order
 #pragma unroll
-        for (int u = 0; u < 16; u++) {
-            float4 v = x[u];
-            if (square) { v.x *= v.x; v.y *= v.y; v.z *= v.z; v.w *= v.w; }
-            rp[u] = fmaf(v.w, bj.w, fmaf(v.z, bj.z, fmaf(v.y, bj.y, v.x * bj.x)));
-            const float bi = offdiag ? __shfl_sync(0xffffffffu, bil, u) : 0.f;
-            cacc.x = fmaf(v.x, bi, cacc.x);
-            cacc.y = fmaf(v.y, bi, cacc.y);
-            cacc.z = fmaf(v.z, bi, cacc.z);
-            cacc.w = fmaf(v.w, bi, cacc.w);
+        for (int r = 0; r < SYMV_RB; r++) {
+            float v = rp[r];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp][r] = v;
         }
-        // row sums over the 32 lanes, transposed butterfly: lane L ends with row (L >> 1) & 15
-#pragma unroll
-        for (int w = 8; w >= 1; w >>= 1) {  // widths 8, 4, 2, 1 rows kept per lane
-            const bool up = (lane & (2 * w)) != 0;
-#pragma unroll
-            for (int k = 0; k < w; k++) {
-                const float send = up ? rp[k] : rp[k + w];
-                const float keep = up ? rp[k + w] : rp[k];
-                rp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
-            }
-        }
-        const float rsum = rp[0] + __shfl_xor_sync(0xffffffffu, rp[0], 1);
-        if ((lane & 1) == 0) prow[((int64_t)I * nb + J) * SYMV_T + warp * 16 + ((lane >> 1) & 15)] = rsum;
-    }
-    // column part of the chunk: the 8 warps' partials summed in warp order
-    *reinterpret_cast<float4 *>(&cs[warp][4 * lane]) = cacc;
-    __syncthreads();
-    if (threadIdx.x < SYMV_T) {
-        float v = 0.f;
-#pragma unroll
-        for (int w8 = 0; w8 < 8; w8++) v += cs[w8][threadIdx.x];
-        pcol[((int64_t)J * ncmax + c) * SYMV_T + threadIdx.x] = v;
-    }
-    // arrivals: the CTA completing output block X reduces it
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int I = I0; I < I1; I++) {
-            const unsigned need = (unsigned)(nb - I + symv_nc(I));
-            red[I - I0] = atomicAdd(&arrivals[I], 1u) == need - 1 ? I : -1;
-        }
-        const unsigned needJ = (unsigned)(nb - J + symv_nc(J));
-        red[SYMV_C] = atomicAdd(&arrivals[J], 1u) == needJ - 1 ? J : -1;
-    }
-    __syncthreads();
-    for (int e = 0; e <= SYMV_C; e++) {
-        if (e < SYMV_C && I0 + e >= I1) continue;
-        const int X = red[e];
-        if (X < 0) continue;
-        __threadfence();
-        if (threadIdx.x < SYMV_T) {
-            const float *pr = prow + (int64_t)X * nb * SYMV_T + threadIdx.x;
+        __syncthreads();
+        if (tid < SYMV_RB && ib + tid < r1) {
             float v = 0.f;
-            int k = X;
-            for (; k + 8 <= nb; k += 8) {  // eight loads in flight, summed in k order
-                float t8[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) t8[u] = __ldcg(pr + (int64_t)(k + u) * SYMV_T);
-#pragma unroll
-                for (int u = 0; u < 8; u++) v += t8[u];
-            }
-            for (; k < nb; k++) v += __ldcg(pr + (int64_t)k * SYMV_T);
-            const float *pc = pcol + (int64_t)X * ncmax * SYMV_T + threadIdx.x;
-            for (int cc = 0; cc < symv_nc(X); cc++) v += __ldcg(pc + (int64_t)cc * SYMV_T);
-            const int64_t r = (int64_t)X * SYMV_T + threadIdx.x;
-            if (r < n) y[r] = v;
+            for (int w8 = 0; w8 < 8; w8++) v += red[w8][tid];
+            rowpart[ib + tid] = v;
         }
-        if (threadIdx.x == 0) arrivals[X] = 0u;  // ready for the next call
+        __syncthreads();
     }
+    // this CTA's column parts (zeros outside its columns)
+    float4 *pc = reinterpret_cast<float4 *>(pcol) + (int64_t)k * (256 * SYMV_U);
+#pragma unroll
+    for (int u = 0; u < SYMV_U; u++) pc[tid + 256 * u] = cacc[u];
+}
+
+// y_j = row part + the G CTAs' column parts in CTA order
+__global__ void k_symv_finish(const float *__restrict__ rowpart, const float *__restrict__ pcol, int G, int64_t n,
+                              float *__restrict__ y) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    float v = rowpart[j];
+    const int64_t stride = 4 * 256 * SYMV_U;
+    int k = 0;
+    for (; k + 8 <= G; k += 8) {
+        float t8[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) t8[u] = pcol[(int64_t)(k + u) * stride + j];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v += t8[u];
+    }
+    for (; k < G; k++) v += pcol[(int64_t)k * stride + j];
+    y[j] = v;
 }
 
 // GVT_SYMV=1 enables the symmetric (upper-triangle) GEMV: under evaluation (off by default)
@@ -483,15 +482,12 @@ static bool symv_enabled() {
 
 void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y, bool symmetric) {
     if (F.n == 0) return;
-    if (symmetric && symv_enabled() && F.n == F.cols && F.n >= 1024 && F.ld % 4 == 0) {
-        const int nb = (int)((F.n + SYMV_T - 1) / SYMV_T), ncmax = (nb - 1 + SYMV_C) / SYMV_C;
-        int64_t ctas = 0;
-        for (int J = 0; J < nb; J++) ctas += (J + SYMV_C) / SYMV_C;
-        float *prow = wsT<float>(c, "symv.prow", (size_t)nb * nb * SYMV_T);
-        float *pcol = wsT<float>(c, "symv.pcol", (size_t)nb * ncmax * SYMV_T);
-        unsigned *arr = wsT<unsigned>(c, "symv.arrivals", (size_t)nb);
-        GVT_CUDA_TRY(cudaMemsetAsync(arr, 0, sizeof(unsigned) * nb, c->stream));
-        GVT_LAUNCH(c, K_GEMV, k_symv, (unsigned)ctas, 256, 0, F.p, F.n, F.ld, b, square, nb, prow, pcol, arr, y);
+    if (symmetric && symv_enabled() && F.n == F.cols && F.n >= 1024 && F.n <= 1024 * SYMV_U && F.ld % 4 == 0) {
+        const int G = 2 * c->sm_count;
+        float *rowpart = wsT<float>(c, "symv.rowpart", (size_t)F.n);
+        float *pcol = wsT<float>(c, "symv.pcol", (size_t)G * 1024 * SYMV_U);
+        GVT_LAUNCH(c, K_GEMV, k_symv_rows, (unsigned)G, 256, 0, F.p, F.n, F.ld, b, square, rowpart, pcol);
+        GVT_LAUNCH(c, K_GEMV, k_symv_finish, grid1d(F.n, 256), 256, 0, rowpart, pcol, G, F.n, y);
         return;
     }
     const size_t smem = sizeof(float) * (size_t)F.ld;

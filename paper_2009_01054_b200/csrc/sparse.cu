@@ -9,6 +9,8 @@
 // shuffle trees; no floating-point atomics anywhere.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace gvt {
@@ -350,144 +352,169 @@ __global__ void __launch_bounds__(256) k_gemv_smem(const float *__restrict__ F, 
 }
 
 // ---- symmetric GEMV: y = F b (or F.^2 b) reading only the upper triangle of a square Gram
-// (symmetric by definition, R1), row by row, so every warp streams long contiguous row segments.
-// CTA k of G owns rows [R_k, R_k+1), split so every CTA streams the same number of upper-triangle
-// elements; thread t owns the column quads q = t + 256 u (u < SYMV_U, n <= 1024 SYMV_U).  For row i:
-//   row part    y_i  = sum_{j >= i} F_ij b_j      (8-row batches, reduced over the CTA in a fixed tree)
-//   column part c_j += F_ij b_i for j > i        (registers, per owned quad)
-// The column parts of the G CTAs are parked in pcol[G][nq4] and summed in CTA order by k_symv_finish,
-// which adds the row part: deterministic, no atomics, half the HBM bytes of the plain GEMV.
-constexpr int SYMV_U = 8, SYMV_RB = 8;
+// (symmetric by definition, R1).  The columns are cut into panels of SYMV_PW = 1024 (thread t owns
+// column quad t of the panel) and the rows of each panel's upper part (rows 0 .. panel
+// end) into chunks of SYMV_RC = 64 (enough CTAs: ~4 per SM at C4's n = 8000); one CTA per (panel, row
+// chunk) streams its rows as 4 KB contiguous segments, SYMV_RB rows (loads of 16 B) per thread in flight:
+//   row part    prow[panel][i] = sum_{j >= i, j in panel} F_ij b_j   (warp trees, then warps in order)
+//   column part pcol[unit][j]  = sum_{i in chunk, i < j} F_ij b_i    (registers)
+// k_symv_finish adds, per j, the row parts of the panels right of j and the column parts of the chunks
+// above j, in a fixed order: deterministic, no atomics, half the HBM bytes of the plain GEMV.
+constexpr int SYMV_PW = 1024, SYMV_RC = 64, SYMV_RB = 8, SYMV_QT = SYMV_PW / 1024;
 
-__device__ __forceinline__ int64_t symv_row_bound(int64_t n, int k, int G) {
-    // first row of CTA k: sum_{i < R} (n - i) = k / G of the n (n + 1) / 2 upper-triangle elements
-    if (k <= 0) return 0;
-    if (k >= G) return n;
-    const double W = 0.5 * (double)n * (double)(n + 1), nn = (double)n + 0.5;
-    double R = nn - sqrt(fmax(nn * nn - 2.0 * W * (double)k / (double)G, 0.0));
-    int64_t r = (int64_t)R;
-    return r < 0 ? 0 : (r > n ? n : r);
+__device__ __forceinline__ int64_t symv_rows(int64_t n, int p) {  // rows with upper-triangle cells in panel p
+    const int64_t e = (int64_t)(p + 1) * SYMV_PW;
+    return e < n ? e : n;
 }
 
-__global__ void __launch_bounds__(256, 2) k_symv_rows(const float *__restrict__ F, int64_t n, int64_t ld,
-                                                      const float *__restrict__ b, int square,
-                                                      float *__restrict__ rowpart, float *__restrict__ pcol) {
-    __shared__ float red[8][SYMV_RB];
+__global__ void __launch_bounds__(256, 4) k_symv_panel(const float *__restrict__ F, int64_t n, int64_t ld,
+                                                       const float *__restrict__ b, int square,
+                                                       float *__restrict__ prow, float *__restrict__ pcol) {
+    __shared__ float red[8][SYMV_RC];  // per warp, per row of the chunk: the warp's partial row sum
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int G = gridDim.x, k = blockIdx.x;
-    const int64_t r0 = symv_row_bound(n, k, G), r1 = symv_row_bound(n, k + 1, G);
-    const int64_t nq = (n + 3) / 4;
-    float4 bq[SYMV_U], cacc[SYMV_U];
-#pragma unroll
-    for (int u = 0; u < SYMV_U; u++) {
-        const int64_t q = tid + 256 * u;
-        bq[u] = q < nq ? __ldg(reinterpret_cast<const float4 *>(b) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        cacc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int p = 0, u = blockIdx.x;
+    while (u >= (int)((symv_rows(n, p) + SYMV_RC - 1) / SYMV_RC)) {
+        u -= (int)((symv_rows(n, p) + SYMV_RC - 1) / SYMV_RC);
+        p++;
     }
-    for (int64_t ib = r0; ib < r1; ib += SYMV_RB) {
+    const int64_t i0 = (int64_t)u * SYMV_RC, i1 = min(i0 + SYMV_RC, symv_rows(n, p));
+    int64_t j0[SYMV_QT];
+    float4 bq[SYMV_QT], cacc[SYMV_QT];
+#pragma unroll
+    for (int h = 0; h < SYMV_QT; h++) {
+        j0[h] = (int64_t)p * SYMV_PW + 1024 * h + 4 * tid;  // this thread's quads
+        bq[h] = j0[h] < n ? __ldg(reinterpret_cast<const float4 *>(b + j0[h])) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j0[h] + 1 >= n) bq[h].y = 0.f;
+        if (j0[h] + 2 >= n) bq[h].z = 0.f;
+        if (j0[h] + 3 >= n) bq[h].w = 0.f;
+        cacc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int64_t ib = i0; ib < i1; ib += SYMV_RB) {
+        float4 x[SYMV_RB][SYMV_QT];
+#pragma unroll
+        for (int r = 0; r < SYMV_RB; r++) {  // a quad entirely left of the diagonal is never read
+            const int64_t i = ib + r;
+#pragma unroll
+            for (int h = 0; h < SYMV_QT; h++)
+                x[r][h] = (i < i1 && j0[h] < n && j0[h] + 3 >= i)
+                              ? __ldg(reinterpret_cast<const float4 *>(F + i * ld + j0[h]))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         float rp[SYMV_RB];
 #pragma unroll
         for (int r = 0; r < SYMV_RB; r++) {
             const int64_t i = ib + r;
+            const float bi = i < i1 ? __ldg(b + i) : 0.f;
             rp[r] = 0.f;
-            if (i >= r1) continue;
-            const int64_t q0 = i >> 2;
-            const float *row = F + i * ld;
-            float4 x[SYMV_U];
 #pragma unroll
-            for (int u = 0; u < SYMV_U; u++) {
-                const int64_t q = tid + 256 * u;
-                x[u] = (q >= q0 && q < nq) ? __ldg(reinterpret_cast<const float4 *>(row) + q)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float bi = __ldg(b + i);
-#pragma unroll
-            for (int u = 0; u < SYMV_U; u++) {
-                const int64_t q = tid + 256 * u;
-                float4 v = x[u];
+            for (int h = 0; h < SYMV_QT; h++) {
+                float4 v = x[r][h];
                 if (square) { v.x *= v.x; v.y *= v.y; v.z *= v.z; v.w *= v.w; }
-                // elements past n are zero (b and the masked loads); the quad holding the diagonal:
-                // j < i excluded, j = i in the row part only
-                float4 w = v;  // column part (j > i)
-                if (q == q0) {
-                    const int e = (int)(i - 4 * q0);
-                    if (e > 0) v.x = 0.f;
-                    if (e > 1) v.y = 0.f;
-                    if (e > 2) v.z = 0.f;
-                    w = v;
-                    if (e == 0) w.x = 0.f;
-                    if (e == 1) w.y = 0.f;
-                    if (e == 2) w.z = 0.f;
-                    if (e == 3) w.w = 0.f;
+                float4 w = v;  // column part: j > i only; row part: j >= i
+                const int64_t jj = j0[h];
+                if (jj <= i) {
+                    if (jj < i) { v.x = 0.f; w.x = 0.f; } else w.x = 0.f;
+                    if (jj + 1 < i) { v.y = 0.f; w.y = 0.f; } else if (jj + 1 == i) w.y = 0.f;
+                    if (jj + 2 < i) { v.z = 0.f; w.z = 0.f; } else if (jj + 2 == i) w.z = 0.f;
+                    if (jj + 3 < i) { v.w = 0.f; w.w = 0.f; } else if (jj + 3 == i) w.w = 0.f;
                 }
-                if (4 * q + 1 >= n) { v.y = 0.f; w.y = 0.f; }
-                if (4 * q + 2 >= n) { v.z = 0.f; w.z = 0.f; }
-                if (4 * q + 3 >= n) { v.w = 0.f; w.w = 0.f; }
-                rp[r] = fmaf(v.w, bq[u].w, fmaf(v.z, bq[u].z, fmaf(v.y, bq[u].y, fmaf(v.x, bq[u].x, rp[r]))));
-                cacc[u].x = fmaf(w.x, bi, cacc[u].x);
-                cacc[u].y = fmaf(w.y, bi, cacc[u].y);
-                cacc[u].z = fmaf(w.z, bi, cacc[u].z);
-                cacc[u].w = fmaf(w.w, bi, cacc[u].w);
+                rp[r] = fmaf(v.w, bq[h].w, fmaf(v.z, bq[h].z, fmaf(v.y, bq[h].y, fmaf(v.x, bq[h].x, rp[r]))));
+                cacc[h].x = fmaf(w.x, bi, cacc[h].x);
+                cacc[h].y = fmaf(w.y, bi, cacc[h].y);
+                cacc[h].z = fmaf(w.z, bi, cacc[h].z);
+                cacc[h].w = fmaf(w.w, bi, cacc[h].w);
             }
         }
-        // row parts of the batch: warp trees, then the 8 warps in order
+        // row parts of the batch: warp trees parked per warp (no CTA barrier inside the row loop)
 #pragma unroll
         for (int r = 0; r < SYMV_RB; r++) {
             float v = rp[r];
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red[warp][r] = v;
+            rp[r] = v;
         }
-        __syncthreads();
-        if (tid < SYMV_RB && ib + tid < r1) {
-            float v = 0.f;
+        if (lane < SYMV_RB) {
+            float v = rp[0];
 #pragma unroll
-            for (int w8 = 0; w8 < 8; w8++) v += red[w8][tid];
-            rowpart[ib + tid] = v;
+            for (int r = 1; r < SYMV_RB; r++) v = lane == r ? rp[r] : v;
+            red[warp][ib - i0 + lane] = v;
         }
-        __syncthreads();
     }
-    // this CTA's column parts (zeros outside its columns)
-    float4 *pc = reinterpret_cast<float4 *>(pcol) + (int64_t)k * (256 * SYMV_U);
 #pragma unroll
-    for (int u = 0; u < SYMV_U; u++) pc[tid + 256 * u] = cacc[u];
+    for (int h = 0; h < SYMV_QT; h++)
+        *reinterpret_cast<float4 *>(pcol + (int64_t)blockIdx.x * SYMV_PW + 1024 * h + 4 * tid) = cacc[h];
+    __syncthreads();
+    if (tid < SYMV_RC && i0 + tid < i1) {  // the 8 warps' row partials in warp order
+        float v = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; w8++) v += red[w8][tid];
+        prow[(int64_t)p * n + i0 + tid] = v;
+    }
 }
 
-// y_j = row part + the G CTAs' column parts in CTA order
-__global__ void k_symv_finish(const float *__restrict__ rowpart, const float *__restrict__ pcol, int G, int64_t n,
-                              float *__restrict__ y) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    float v = rowpart[j];
-    const int64_t stride = 4 * 256 * SYMV_U;
-    int k = 0;
-    for (; k + 8 <= G; k += 8) {
-        float t8[8];
+// y_j for 32 consecutive j per CTA: warp w sums the column parts of chunk range w (of 8, contiguous),
+// then lane j adds the row parts of panels panel(j) .. last and the 8 ranges in order
+__global__ void __launch_bounds__(256) k_symv_finish(const float *__restrict__ prow, const float *__restrict__ pcol,
+                                                     int np, int64_t n, float *__restrict__ y) {
+    __shared__ float part[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+    const int64_t jc = j < n ? j : n - 1;
+    const int pj = (int)(jc / SYMV_PW);
+    int64_t ubase = 0;
+    for (int p = 0; p < pj; p++) ubase += (symv_rows(n, p) + SYMV_RC - 1) / SYMV_RC;
+    const int64_t nc = (jc + SYMV_RC - 1) / SYMV_RC;  // chunks holding a row < j
+    const int64_t c0 = nc * warp / 8, c1 = nc * (warp + 1) / 8;
+    const float *pc = pcol + ubase * SYMV_PW + (jc - (int64_t)pj * SYMV_PW);
+    float v = 0.f;
+    int64_t c = c0;
+    for (; c + 4 <= c1; c += 4) {
+        float t4[4];
 #pragma unroll
-        for (int u = 0; u < 8; u++) t8[u] = pcol[(int64_t)(k + u) * stride + j];
+        for (int k = 0; k < 4; k++) t4[k] = pc[(c + k) * SYMV_PW];
 #pragma unroll
-        for (int u = 0; u < 8; u++) v += t8[u];
+        for (int k = 0; k < 4; k++) v += t4[k];
     }
-    for (; k < G; k++) v += pcol[(int64_t)k * stride + j];
-    y[j] = v;
+    for (; c < c1; c++) v += pc[c * SYMV_PW];
+    part[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && j < n) {
+        float s = 0.f;
+        int p = pj;
+        for (; p + 4 <= np; p += 4) {  // row parts, four loads in flight, in panel order
+            float t4[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) t4[k] = prow[(int64_t)(p + k) * n + j];
+#pragma unroll
+            for (int k = 0; k < 4; k++) s += t4[k];
+        }
+        for (; p < np; p++) s += prow[(int64_t)p * n + j];
+#pragma unroll
+        for (int w8 = 0; w8 < 8; w8++) s += part[w8][lane];
+        y[j] = s;
+    }
 }
 
-// GVT_SYMV=1 enables the symmetric (upper-triangle) GEMV: under evaluation (off by default)
+// the symmetric (upper-triangle) GEMV pays once the Gram outgrows L2: n >= 6144 (151 MB).  Measured
+// (profiles/r02_ab_symv.txt): C4 Ranking's 8000^2 union Gram 104-105 -> 91-93 us per CG iteration;
+// C4 Poly2D's 5000^2 / 3000^2 Grams 3 % slower with it, so they keep the row GEMV.  GVT_SYMV=0 disables.
 static bool symv_enabled() {
     static const bool on = [] {
         const char *e = getenv("GVT_SYMV");
-        return e && atoi(e) != 0;
+        return !(e && atoi(e) == 0);
     }();
     return on;
 }
 
 void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y, bool symmetric) {
     if (F.n == 0) return;
-    if (symmetric && symv_enabled() && F.n == F.cols && F.n >= 1024 && F.n <= 1024 * SYMV_U && F.ld % 4 == 0) {
-        const int G = 2 * c->sm_count;
-        float *rowpart = wsT<float>(c, "symv.rowpart", (size_t)F.n);
-        float *pcol = wsT<float>(c, "symv.pcol", (size_t)G * 1024 * SYMV_U);
-        GVT_LAUNCH(c, K_GEMV, k_symv_rows, (unsigned)G, 256, 0, F.p, F.n, F.ld, b, square, rowpart, pcol);
-        GVT_LAUNCH(c, K_GEMV, k_symv_finish, grid1d(F.n, 256), 256, 0, rowpart, pcol, G, F.n, y);
+    if (symmetric && symv_enabled() && F.n == F.cols && F.n >= 6144 && F.ld % 4 == 0) {
+        const int np = (int)((F.n + SYMV_PW - 1) / SYMV_PW);
+        int64_t units = 0;
+        for (int p = 0; p < np; p++) units += (std::min<int64_t>((int64_t)(p + 1) * SYMV_PW, F.n) + SYMV_RC - 1) / SYMV_RC;
+        float *prow = wsT<float>(c, "symv.prow", (size_t)np * F.n);
+        float *pcol = wsT<float>(c, "symv.pcol", (size_t)units * SYMV_PW);
+        GVT_LAUNCH(c, K_GEMV, k_symv_panel, (unsigned)units, 256, 0, F.p, F.n, F.ld, b, square, prow, pcol);
+        GVT_LAUNCH(c, K_GEMV, k_symv_finish, (unsigned)((F.n + 31) / 32), 256, 0, prow, pcol, np, F.n, y);
         return;
     }
     const size_t smem = sizeof(float) * (size_t)F.ld;

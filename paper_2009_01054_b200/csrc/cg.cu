@@ -119,6 +119,44 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, c
     }
 }
 
+// The fused CG tail (k_combine_gather + k_cg_ap in one pass; single GPU): per output i of this block's
+// fixed range, u_i = c1 g1[.] + c2 g2[.] (+ u_i), the direction p_i (= r_i + beta p_i when r_lazy, then
+// stored), Ap_i = u_i + lambda p_i stored over u, and the p.Ap partial; the last block takes the alpha
+// step.  The arithmetic per element is that of the two separate kernels.
+__global__ void __launch_bounds__(RED_THREADS) k_cg_combine_ap(
+    const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, const float *__restrict__ g1, int rs1,
+    float c1, const float *__restrict__ g2, int rs2, float c2, int accumulate, float *__restrict__ u,
+    float *__restrict__ p, const float *__restrict__ r_lazy, float lambda, double *__restrict__ st,
+    double *__restrict__ part, unsigned *__restrict__ ticket) {
+    if (halted(st)) return;
+    const float beta = r_lazy ? (float)st[ST_BETA] : 0.f;
+    int64_t lo, hi;
+    block_range(n, lo, hi);
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        float v = c1 * g1[rs1 == 0 ? f[i] : s[i]];
+        if (g2) v = fmaf(c2, g2[rs2 == 0 ? f[i] : s[i]], v);
+        const float ui = accumulate ? u[i] + v : v;
+        float pi = p[i];
+        if (r_lazy) {
+            pi = fmaf(beta, pi, r_lazy[i]);
+            p[i] = pi;
+        }
+        const float a = fmaf(lambda, pi, ui);
+        u[i] = a;
+        acc += (double)pi * (double)a;
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+    if (last_block_done(ticket)) {
+        const double pap = reduce_parts_cg(part, RED_BLOCKS);  // (unused slots are zero: cg_init)
+        if (threadIdx.x == 0) {
+            cg_alpha_scalar(pap, st);
+            *ticket = 0u;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(RED_THREADS) k_cg_alpha(const double *__restrict__ part, int nparts,
                                                           double *__restrict__ st) {
     if (halted(st)) return;
@@ -416,6 +454,26 @@ void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double la
     if (tk) return;
     allreduce_partials(c, pt, RED_BLOCKS);
     GVT_LAUNCH(c, K_CG_SCALAR, k_cg_alpha, 1, RED_THREADS, 0, pt, RED_BLOCKS * c->world, state);
+}
+
+void cg_combine_ap(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *g1, int rs1, float c1,
+                   const float *g2, int rs2, float c2, int accumulate, float *u, float *p, const float *r_lazy,
+                   double lambda, double *state) {
+    unsigned *tk = cg_ticket(c);
+    GVT_REQUIRE(tk, GVT_E_STATE, "the fused CG tail is single-GPU only");
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_combine_ap, vec_blocks(n), RED_THREADS, 0, f, s, n, g1, rs1, c1, g2, rs2, c2,
+               accumulate, u, p, r_lazy, (float)lambda, state, my_parts(c), tk);
+}
+
+void cg_update_xr(gvt_ctx *c, float *x, float *r, const float *p, const float *Ap, int64_t n, double *state) {
+    unsigned *tk = cg_ticket(c);
+    GVT_REQUIRE(tk, GVT_E_STATE, "the fused CG tail is single-GPU only");
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_xr, vec_blocks(n), RED_THREADS, 0, x, r, p, Ap, n, state, my_parts(c), tk,
+               state + ST_N);
+}
+
+void cg_direction(gvt_ctx *c, float *p, const float *r, int64_t n, const double *state) {
+    GVT_LAUNCH(c, K_CG_VEC, k_cg_p, vec_blocks(n), RED_THREADS, 0, p, r, n, state);
 }
 
 void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_t n, double *state, int iter,

@@ -1482,6 +1482,88 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
     }
 }
 
+// the same rows, one WARP per row, for short rows (ld <= 4096: C2/C3-size problems): the CTA-wide
+// barriers of k_build_x16 (zero, gather, max, store) become __syncwarp, and every row of the matrix is
+// in flight at once (8 rows per CTA, ld floats of shared memory each).  Same cell sums (entry order),
+// same scale rule, same stores.
+__global__ void __launch_bounds__(256) k_build_x16_warp(const int64_t *__restrict__ row_ptr,
+                                                        const int32_t *__restrict__ col,
+                                                        const int32_t *__restrict__ src,
+                                                        const float *__restrict__ sign, const float *__restrict__ p,
+                                                        int64_t row_lo, int64_t rows, int64_t cols, int64_t ld,
+                                                        __half *__restrict__ hi, __half *__restrict__ lo,
+                                                        float *__restrict__ sinv, const float *__restrict__ diag) {
+    extern __shared__ float rowbufs[];  // 8 x ld floats
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *rowbuf = rowbufs + (size_t)warp * ld;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < rows; r += nw) {
+        float4 *rb4 = reinterpret_cast<float4 *>(rowbuf);
+        for (int64_t j = lane; j < ld / 4; j += 32) rb4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
+        constexpr int U = 4;  // entries in flight per lane
+        for (int64_t k0 = kb + lane; k0 < ke; k0 += U * 32) {
+            int32_t cc[U], cprev[U], cnext[U];
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t k = k0 + (int64_t)u * 32;
+                cc[u] = -1;
+                if (k < ke) {
+                    cc[u] = col[k];
+                    cprev[u] = k > kb ? col[k - 1] : -1;
+                    cnext[u] = k + 1 < ke ? col[k + 1] : -1;
+                    v[u] = sign[k] * __ldg(p + src[k]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (cc[u] < 0 || cprev[u] == cc[u]) continue;  // past the row end, or not the head of its run
+                float sv = v[u];
+                if (cnext[u] == cc[u]) {
+                    const int64_t k = k0 + (int64_t)u * 32;
+                    for (int64_t j = k + 1; j < ke && col[j] == cc[u]; j++) sv += sign[j] * __ldg(p + src[j]);
+                }
+                rowbuf[cc[u]] = sv;
+            }
+        }
+        __syncwarp();
+        if (diag && lane == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
+        __syncwarp();
+        float mx = 0.f;
+        for (int64_t j = lane; j < ld / 4; j += 32) {
+            const float4 v4 = rb4[j];
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v4.x), fabsf(v4.y)), fmaxf(fabsf(v4.z), fabsf(v4.w))));
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int e = 0;
+        if (mx > 0.f && isfinite(mx)) {
+            int ex;
+            frexpf(mx, &ex);
+            e = 15 - ex;
+        }
+        const float sc = ldexpf(1.f, e);
+        if (lane == 0) sinv[r] = ldexpf(1.f, -e);
+        __half2 *h2 = reinterpret_cast<__half2 *>(hi + r * ld), *l2 = reinterpret_cast<__half2 *>(lo + r * ld);
+        for (int64_t j = lane; j < ld / 2; j += 32) {
+            const float v0 = rowbuf[2 * j] * sc, v1 = rowbuf[2 * j + 1] * sc;
+            const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1);
+            h2[j] = __halves2half2(a0, a1);
+            l2[j] = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
+        }
+        __syncwarp();
+    }
+}
+
+static bool build_warp_rows() {  // A/B knob: GVT_BUILD_WARP=0 keeps the CTA-per-row build for short rows
+    static const bool on = [] {
+        const char *e = getenv("GVT_BUILD_WARP");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
                   const float *p, const float *diag) {
     Operand o;
@@ -1500,7 +1582,17 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_dev = smem;
     }
-    if (rows > 0) {
+    if (rows > 0 && o.ld <= 4096 && build_warp_rows()) {
+        const size_t smem8 = 8 * smem;
+        static size_t attr_w[GVT_MAX_DEVICES] = {};
+        size_t &aw = attr_w[c->device < GVT_MAX_DEVICES ? c->device : 0];
+        if (smem8 > 48 * 1024 && smem8 > aw) {
+            GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8));
+            aw = smem8;
+        }
+        GVT_LAUNCH(c, K_DENSIFY, k_build_x16_warp, grid1d(rows, 8), 256, smem8, e.row_ptr, e.col, e.src, e.sign, p,
+                   row_lo, rows, cols, o.ld, hi, lo, s, diag);
+    } else if (rows > 0) {
         if (o.ld > 8192)
             GVT_LAUNCH(c, K_DENSIFY, k_build_x16<1024>, grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr, e.col,
                        e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);

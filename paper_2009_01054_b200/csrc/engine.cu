@@ -709,7 +709,37 @@ static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p
     if (P.uex) uex_finish(c, P, g, partial, accumulate, out);
 }
 
-static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u) {
+// The fused CG tail (single GPU; the forms that end in a gather-combine: Linear, Ranking, Poly2D): the
+// matvec's final combine also takes the ridge term Ap = u + lambda p, the p.Ap partials and the alpha
+// step (cg.cu k_cg_combine_ap), one vector pass and one launch fewer per CG iteration; C4 Ranking
+// 93.4-94.0 -> 83.8-85.2 us per iteration (profiles/r02_ab_cg_tail.txt).  Optionally (GVT_CG_TAIL_LAZY=1;
+// Linear / Ranking) the segment sums also form the direction on the fly, p = r + beta p (beta = st[2]),
+// dropping k_cg_p -- measured slower (the extra gather of r costs more than the pass it saves).
+struct CgTail {
+    const float *r = nullptr;  // r_{k-1}
+    double *st = nullptr;      // CG state (st[2] = beta)
+    double lambda = 0.0;
+    float *p = nullptr;        // p_{k-1} in, p_k out
+};
+
+static bool cg_tail_enabled() {  // A/B knob: GVT_CG_TAIL=0 keeps the separate CG vector kernels
+    static const bool on = [] {
+        const char *e = getenv("GVT_CG_TAIL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+static bool cg_tail_lazy() {  // A/B knob: GVT_CG_TAIL_LAZY=1 also folds the direction update (k_cg_p)
+    static const bool on = [] {
+        const char *e = getenv("GVT_CG_TAIL_LAZY");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
+static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u,
+                       const CgTail *tail = nullptr) {
     // gather p over the ranks (world 1: p_full is p_local itself)
     const float *p = p_local;
     if (distributed(c)) {
@@ -735,20 +765,32 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         segment_sum_gather(c, mp.byS, p, mp.b2);  // bS
         gemv(c, P.D, mp.b1, 1, mp.g1, !P.rect);  // D.^2 bF
         gemv(c, P.T, mp.b2, 1, mp.g2, !P.rect);  // T.^2 bS
-        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
+        if (tail)
+            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u, tail->p,
+                          nullptr, tail->lambda, tail->st);
+        else
+            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
         break;
     }
     case FORM_LINEAR:
-        segment_sum_gather(c, mp.byF, p, mp.b1);
-        segment_sum_gather(c, mp.byS, p, mp.b2);
+        segment_sum_gather(c, mp.byF, p, mp.b1, tail ? tail->r : nullptr, tail ? tail->st + 2 : nullptr);
+        segment_sum_gather(c, mp.byS, p, mp.b2, tail ? tail->r : nullptr, tail ? tail->st + 2 : nullptr);
         gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
         gemv(c, P.T, mp.b2, 0, mp.g2, !P.rect);
-        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
+        if (tail)
+            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u, tail->p,
+                          tail->r, tail->lambda, tail->st);
+        else
+            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
         break;
     case FORM_RANKING:
-        segment_sum_gather(c, mp.byF, p, mp.b1);  // bF - bS
+        segment_sum_gather(c, mp.byF, p, mp.b1, tail ? tail->r : nullptr, tail ? tail->st + 2 : nullptr);  // bF - bS
         gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
-        combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
+        if (tail)
+            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u,
+                          tail->p, tail->r, tail->lambda, tail->st);
+        else
+            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
         break;
     case FORM_CARTESIAN:
         entry_values(c, mp.byF, p);
@@ -1360,6 +1402,9 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
             c->last_n = n;
         }
     }
+    const bool fuse_tail = !minres && !cgg && !es && !distributed(c) && !P.uex && P.n_out == n &&
+                           (mp.form == FORM_RANKING || mp.form == FORM_LINEAR || mp.form == FORM_POLY2D) &&
+                           cg_tail_enabled();
     auto iteration = [&]() {
         if (minres) {
             run_matvec(c, P, mp, v, u);
@@ -1368,6 +1413,17 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         } else if (cgg) {
             run_matvec(c, P, mp, r, u);  // w = K r
             cgg_step(c, x, r, p, sv, u, n, lambda, state);
+        } else if (fuse_tail) {
+            CgTail t;
+            // lazy direction (segment sums on r + beta p, the combine stores p) measured slower: the
+            // extra gather of r in the segment sums costs more than the k_cg_p pass it saves
+            t.r = cg_tail_lazy() && mp.form != FORM_POLY2D ? r : nullptr;
+            t.st = state;
+            t.lambda = lambda;
+            t.p = p;
+            run_matvec(c, P, mp, p, u, &t);  // the final combine also takes Ap = u + lambda p, p.Ap, alpha
+            if (t.r) cg_update_xr(c, x, r, p, u, n, state);
+            else cg_update(c, x, r, p, u, n, state, 0, nullptr);
         } else {
             run_matvec(c, P, mp, p, u);
             cg_after_matvec(c, u, p, n, lambda, state);
@@ -1378,6 +1434,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     };
     drive(c, max_iter, rel_tol > 0.0 || es != nullptr, state, iteration);
     if (cgg) cgg_finish(c, r, n, state);
+    if (fuse_tail && cg_tail_lazy() && mp.form != FORM_POLY2D) cg_direction(c, p, r, n, state);  // p_{k+1} (kept)
     // scalars back (one sync per fit)
     double hstate[MINRES_STATE_N];
     GVT_CUDA_TRY(cudaMemcpyAsync(hstate, state, sizeof(double) * SN, cudaMemcpyDeviceToHost, c->stream));

@@ -137,7 +137,9 @@ void stage2_gather16(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const __
 void stage2_gather(gvt_ctx *c, const SamplePlan &sp, const Factor &A, const float *S, int64_t ldS, int64_t K,
                    float coef, int accumulate, float *out);
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b);  // b[h] = sum_row val (uses e.val)
-void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b);  // b[h] = sum_row sign p[src]
+// b[h] = sum_row sign p[src]; with r: p formed on the fly as r + (*beta_st) p (fused CG tail)
+void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b, const float *r = nullptr,
+                        const double *beta_st = nullptr);
 // symmetric: F is a square Gram (symmetric by definition, R1) -- the upper block triangle is read
 void gemv(gvt_ctx *c, const Factor &F, const float *b, int square, float *y, bool symmetric = false);
 // u[i] (+)= c1 * g1[sel(rs1,i)] + c2 * g2[sel(rs2,i)]   (g2 nullable)
@@ -203,6 +205,15 @@ void gram_tanimoto(gvt_ctx *c, const float *X, int64_t m, const float *Y, int64_
 struct CGState;  // device
 void cg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, double *state, double rel_tol);
 void cg_after_matvec(gvt_ctx *c, float *Ap, const float *p, int64_t n, double lambda, double *state);
+// fused CG tail for the cheap forms (single GPU): the final combine of the matvec also forms the
+// direction (p = r + beta p when lazy), the ridge term Ap = u + lambda p and the p.Ap partials, and
+// takes the alpha step; cg_update_xr then runs only the x / r update (the direction update moves into
+// the next iteration's segment sums).  cg_direction materialises p = r + beta p once after the loop.
+void cg_combine_ap(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, const float *g1, int rs1, float c1,
+                   const float *g2, int rs2, float c2, int accumulate, float *u, float *p, const float *r_lazy,
+                   double lambda, double *state);
+void cg_update_xr(gvt_ctx *c, float *x, float *r, const float *p, const float *Ap, int64_t n, double *state);
+void cg_direction(gvt_ctx *c, float *p, const float *r, int64_t n, const double *state);
 void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_t n, double *state, int iter,
                double *relres_dev);
 // Chronopoulos-Gear single-reduction CG (GVT_OPT_CG_VARIANT = 1): init, then per iteration the

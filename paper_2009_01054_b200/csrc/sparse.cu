@@ -265,23 +265,36 @@ __global__ void k_segment_sum(const int64_t *__restrict__ row_ptr, int64_t nrow,
 
 // b[h] = sum_{k in row h} sign[k] p[src[k]]: the entry values gathered inside the segment sum (the
 // same per-lane order and tree as k_entry_values followed by k_segment_sum, one pass fewer)
+// With r (the fused CG tail, cg.cu k_cg_combine_ap), the direction is formed on the fly:
+// p_k = r_{k-1} + beta p_{k-1} with beta = *beta_st -- the k_cg_p update, read-only here; the tail
+// stores p_k.  Same fmaf as k_cg_p, so the values equal the separate update's.
 __global__ void k_segment_sum_gather(const int64_t *__restrict__ row_ptr, int64_t nrow, const int32_t *__restrict__ src,
                                      const float *__restrict__ sign, const float *__restrict__ p,
+                                     const float *__restrict__ r, const double *__restrict__ beta_st,
                                      float *__restrict__ b) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const float beta = r ? (float)*beta_st : 0.f;
     for (int64_t h = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < nrow; h += warps) {
         float acc = 0.f;
-        for (int64_t k = row_ptr[h] + lane; k < row_ptr[h + 1]; k += 32) acc += sign[k] * __ldg(p + src[k]);
+        if (r) {
+            for (int64_t k = row_ptr[h] + lane; k < row_ptr[h + 1]; k += 32) {
+                const int32_t j = src[k];
+                acc += sign[k] * fmaf(beta, __ldg(p + j), __ldg(r + j));
+            }
+        } else {
+            for (int64_t k = row_ptr[h] + lane; k < row_ptr[h + 1]; k += 32) acc += sign[k] * __ldg(p + src[k]);
+        }
         acc = warp_sum(acc);
         if (lane == 0) b[h] = acc;
     }
 }
 
-void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b) {
+void segment_sum_gather(gvt_ctx *c, const EntryPlan &e, const float *p, float *b, const float *r,
+                        const double *beta_st) {
     if (e.nrow == 0) return;
     GVT_LAUNCH(c, K_SEGSUM, k_segment_sum_gather, grid1d(e.nrow * 32, 256, (int64_t)c->sm_count * 16), 256, 0,
-               e.row_ptr, e.nrow, e.src, e.sign, p, b);
+               e.row_ptr, e.nrow, e.src, e.sign, p, r, beta_st, b);
 }
 
 void segment_sum(gvt_ctx *c, const EntryPlan &e, float *b) {

@@ -64,5 +64,15 @@ def full(path):
                 print(f"  {m:95s} {r[i]:>14s} {units[i]}")
 
 
+def tail(path, count="14"):
+    """The last `count` launches of a launch list, in order (one solver iteration's kernels)."""
+    rows = list(csv.DictReader(io.StringIO(open(path).read()[open(path).read().find('"ID"'):])))
+    seq = [(r["Kernel Name"], float(r["Metric Value"].replace(",", ""))) for r in rows
+           if r["Metric Name"] == "gpu__time_duration.sum"]
+    print(f"# {path}: last {count} of {len(seq)} launches (us)")
+    for name, ns in seq[-int(count):]:
+        print(f"{ns / 1e3:9.2f}  {name[:90]}")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "tail": tail}[sys.argv[1]](*sys.argv[2:])

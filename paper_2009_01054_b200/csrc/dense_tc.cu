@@ -213,6 +213,13 @@ struct EpiParams {
     __half *c_h16, *c_l16;
     float *c_sk;
     int64_t c_sk_ld;
+    // sampled split-K (CTA-pair kernel): units = (non-empty pair tile, K part); tile_list holds the pair
+    // tiles (mp * n_ct + n), each split over `split` contiguous chunk ranges; part[ks * ns + k] receives
+    // sample k's value over K part ks (k_split_combine sums the parts)
+    const int32_t *tile_list;
+    int split, n_units;
+    float *part;
+    int64_t ns;
     // diagnosis (GVT_GEMM_PROF): per CTA, globaltimer stamps [entry, setup done, first stage landed,
     // last MMA commit, last TMA issued, last chunk drained, epilogue done, -]
     unsigned long long *prof;
@@ -234,7 +241,14 @@ __device__ __forceinline__ unsigned long long gemm_timer() {
 #endif
 template <int STRIDE>  // the epilogue threads serving (32 x epilogue warps)
 __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
-                                              const float *stage) {
+                                              const float *stage, float *part) {
+    if (part) {  // split-K: this K part's raw value per sample slot (no coefficient, no accumulation)
+        for (int64_t k = kb0 + t; k < ke; k += STRIDE) {
+            const int rl = ep.s_r[k] - m0, cl = ep.s_c[k] - gc0;
+            part[k] = stage[(rl >> 5) * 32 * 33 + (rl & 31) * 33 + cl];
+        }
+        return;
+    }
     constexpr int U = SERVE_UNROLL;
     for (int64_t k0 = kb0 + t; k0 < ke; k0 += U * STRIDE) {
         int rl[U], cl[U];
@@ -277,7 +291,7 @@ static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == BM, "S scale block = one 
 // 50 ms, so 1 is the default.
 template <int STRIDE>
 __device__ __forceinline__ void serve_samples(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0,
-                                              int gc0, const float *stage);
+                                              int gc0, const float *stage, float *part);
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
 constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
@@ -506,7 +520,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const int64_t cidx = tile * (BN / 32) + chunk;
                     const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                     const int gc0 = n0 + chunk * 32;
-                    serve_samples<256>(ep, kb0, ke, t, m0, gc0, stage + hh * 4 * 32 * 33);
+                    serve_samples<256>(ep, kb0, ke, t, m0, gc0, stage + hh * 4 * 32 * 33, nullptr);
                 }
                 named_bar(1, 32 * N_EPI_WARPS);
             }
@@ -650,6 +664,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         const bool e1 = !(2 * mp_tile + 1 < num_m) || ep.chunk_ptr[t1 * (BN / 32)] == ep.chunk_ptr[(t1 + 1) * (BN / 32)];
         return e0 && e1;
     };
+    // work units: all pair tiles (empty sampled tiles skipped), or (sampled split-K) the listed non-empty
+    // pair tiles x `split` K parts; [c0, c1) = the unit's accumulation chunks
+    const int n_units = (EPI == EPI_SAMPLED && ep.tile_list) ? ep.n_units : n_tiles;
+    auto unit = [&](int t, int &mp_tile, int &n_tile, int &c0, int &c1) -> bool {
+        if (EPI == EPI_SAMPLED && ep.tile_list) {
+            const int tl = ep.tile_list[t / ep.split], ks = t % ep.split;
+            mp_tile = tl / num_n;
+            n_tile = tl % num_n;
+            const int nch = (tile_nk(n_tile) + kcb - 1) / kcb;
+            c0 = nch * ks / ep.split;
+            c1 = nch * (ks + 1) / ep.split;
+            return true;
+        }
+        coords(t, mp_tile, n_tile);
+        if (skip(mp_tile, n_tile)) return false;
+        c0 = 0;
+        c1 = (tile_nk(n_tile) + kcb - 1) / kcb;
+        return true;
+    };
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmAh);
@@ -681,13 +714,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             int kg = 0;  // global k-block counter = ring position
-            for (int t = cluster; t < n_tiles; t += n_clusters) {
-                int mp_tile, n_tile;
-                coords(t, mp_tile, n_tile);
-                if (skip(mp_tile, n_tile)) continue;
+            for (int t = cluster; t < n_units; t += n_clusters) {
+                int mp_tile, n_tile, c0, c1;
+                if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
                 const int m0 = (2 * mp_tile + (int)crank) * BM, n0 = n_tile * BN;
-                const int nk_t = tile_nk(n_tile);
-                for (int kb = 0; kb < nk_t; kb++, kg++) {
+                const int nk_t = min(tile_nk(n_tile), c1 * kcb);
+                for (int kb = c0 * kcb; kb < nk_t; kb++, kg++) {
                     const int s = kg % STAGES2;
                     const uint32_t ph = (kg / STAGES2) & 1;
                     mbar_wait(&empty[s], ph ^ 1);  // own slot released by the leader's MMA commit
@@ -706,13 +738,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         if (lane == 0 && crank == 0) {  // ---------------- MMA issuer (leader only)
             constexpr uint32_t idesc = idesc_mma2<PREC, BN>();
             int kg = 0, cg = 0;
-            for (int t = cluster; t < n_tiles; t += n_clusters) {
-                int mp_tile, n_tile;
-                coords(t, mp_tile, n_tile);
-                if (skip(mp_tile, n_tile)) continue;
-                int kb = 0;
-                const int nk_t = tile_nk(n_tile), nch_t = (nk_t + kcb - 1) / kcb;
-                for (int ch = 0; ch < nch_t; ch++, cg++) {
+            for (int t = cluster; t < n_units; t += n_clusters) {
+                int mp_tile, n_tile, c0, c1;
+                if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
+                int kb = c0 * kcb;
+                const int nk_t = tile_nk(n_tile);
+                for (int ch = c0; ch < c1; ch++, cg++) {
                     const int b = cg & 1;
                     mbar_wait(&tempty[b], ((cg >> 1) & 1) ^ 1);
                     tc_fence_after();
@@ -755,10 +786,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         const int row = quarter * 32 + lane;
         const int tE = threadIdx.x - 64;
         int cg = 0;
-        for (int t = cluster; t < n_tiles; t += n_clusters) {
-            int mp_tile, n_tile;
-            coords(t, mp_tile, n_tile);
-            if (skip(mp_tile, n_tile)) continue;
+        for (int t = cluster; t < n_units; t += n_clusters) {
+            int mp_tile, n_tile, c0, c1;
+            if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
+            float *part_out = ep.tile_list ? ep.part + (int64_t)(t % ep.split) * ep.ns : nullptr;
             const int m_tile = 2 * mp_tile + (int)crank;
             const int m0 = m_tile * BM, n0 = n_tile * BN;
             const int gr = m0 + row;
@@ -766,8 +797,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             float run[CW];
 #pragma unroll
             for (int i = 0; i < CW; i++) run[i] = 0.f;
-            const int nch_t = (tile_nk(n_tile) + kcb - 1) / kcb;
-            for (int ch = 0; ch < nch_t; ch++, cg++) {
+            for (int ch = c0; ch < c1; ch++, cg++) {
                 const int b = cg & 1;
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
@@ -854,7 +884,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                         const int64_t cidx = tile * (BN / 32) + chunk;
                         const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                         const int gc0 = n0 + chunk * 32;
-                        serve_samples<32 * NE>(ep, kb0, ke, tE, m0, gc0, estage + hh * 4 * 32 * 33);
+                        serve_samples<32 * NE>(ep, kb0, ke, tE, m0, gc0, estage + hh * 4 * 32 * 33, part_out);
                     }
                 }
                 named_bar(1, 32 * NE);
@@ -868,10 +898,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         const int row = quarter * 32 + lane;
         const int t256 = threadIdx.x - 64;  // 0..255
         int cg = 0;
-        for (int t = cluster; t < n_tiles; t += n_clusters) {
-            int mp_tile, n_tile;
-            coords(t, mp_tile, n_tile);
-            if (skip(mp_tile, n_tile)) continue;
+        for (int t = cluster; t < n_units; t += n_clusters) {
+            int mp_tile, n_tile, c0, c1;
+            if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
             const int m_tile = 2 * mp_tile + (int)crank;
             const int m0 = m_tile * BM, n0 = n_tile * BN;
             const int gr = m0 + row;
@@ -879,8 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             float run[128];
 #pragma unroll
             for (int i = 0; i < 128; i++) run[i] = 0.f;
-            const int nch_t = (tile_nk(n_tile) + kcb - 1) / kcb;
-            for (int ch = 0; ch < nch_t; ch++, cg++) {
+            for (int ch = c0; ch < c1; ch++, cg++) {
                 const int b = cg & 1;
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
                 tc_fence_after();
@@ -1154,7 +1182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                             const int64_t cidx = tile * (BN / 32) + chunk;
                             const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
                             const int gc0 = n0 + chunk * 32;
-                            serve_samples<256>(ep, kb0, ke, t256, m0, gc0, estage + hh * 4 * 32 * 33);
+                            serve_samples<256>(ep, kb0, ke, t256, m0, gc0, estage + hh * 4 * 32 * 33, nullptr);
                         }
                     }
                     named_bar(1, 32 * N_EPI_WARPS);
@@ -1272,7 +1300,8 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
                 cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
             attr2[dv] = true;
         }
-        const int64_t pair_tiles = ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
+        const int64_t pair_tiles =
+            (EPI == EPI_SAMPLED && ep.tile_list) ? ep.n_units : ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
         const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
         dim3 grid((unsigned)(2 * clusters));
         static const bool prof = getenv("GVT_GEMM_PROF") != nullptr;
@@ -1699,6 +1728,34 @@ void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, in
     launch_gemm<EPI_STORE>(c, K_STAGE1_TC, A, B, M, N, K, ep);
 }
 
+// split-K parts of the sampled GEMM summed per sample in part order, then the sampled epilogue's store
+__global__ void k_split_combine(const float *__restrict__ part, int split, int64_t ns, const int32_t *__restrict__ dst,
+                                float coef, int accumulate, float *__restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ns; k += (int64_t)gridDim.x * blockDim.x) {
+        float v = part[k];
+        for (int h = 1; h < split; h++) v += part[(int64_t)h * ns + k];
+        const int32_t d = dst[k];
+        out[d] = accumulate ? fmaf(coef, v, out[d]) : coef * v;
+    }
+}
+
+// K parts per non-empty pair tile: when at most half of the CTA pairs would have a tile, each tile's
+// K range is split (at accumulation-chunk boundaries, >= 2 chunks per part) so every pair works --
+// C3's upper-triangle samples leave ~36 of 64 pair tiles non-empty on 74 CTA pairs.  GVT_SPLITK=0: off.
+static int sampled_split(gvt_ctx *c, const SamplePlan &sp, int64_t K) {
+    static const int env = [] {
+        const char *e = getenv("GVT_SPLITK");
+        return e ? atoi(e) : -1;
+    }();
+    if (env == 0 || c->gemm_cta != 2 || !sp.pair_list || sp.n_pairs <= 0) return 1;
+    const int clusters = c->sm_count / 2;
+    const int nch = (int)((K + BN - 1) / BN);
+    int split = clusters / sp.n_pairs;
+    split = std::min(split, std::min(4, nch / 2));
+    if (env > 0) split = std::min(env, std::max(1, nch / 2));
+    return split >= 2 ? split : 1;
+}
+
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out) {
     if (sp.ns == 0) return;
@@ -1712,10 +1769,40 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.coef = coef;
     ep.accumulate = accumulate;
     ep.out = out;
+    const int split = sampled_split(c, sp, K);
+    if (split > 1) {
+        ep.tile_list = sp.pair_list;
+        ep.split = split;
+        ep.n_units = sp.n_pairs * split;
+        ep.ns = sp.ns;
+        ep.part = wsT<float>(c, "splitk.part", (size_t)split * sp.ns);
+    }
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
+    if (split > 1)
+        GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine, grid1d(sp.ns, 256, 8 * c->sm_count), 256, 0, ep.part, split, sp.ns,
+                   sp.dst, coef, accumulate, out);
 }
 
 // ----------------------------------------------------------------------------- sample bucketing
+// the CTA-pair tiles (M-tiles 2 mp, 2 mp + 1 x N-tile n) holding samples, ascending, and their count at
+// list[n_mp * n_ct]; one CTA (small problems only: at most one tile per SM)
+__global__ void k_pair_list(const int64_t *__restrict__ tile_ptr, int64_t n_rt, int64_t n_ct, int32_t *__restrict__ list) {
+    __shared__ int cnt;
+    const int64_t n_mp = (n_rt + 1) / 2, npt = n_mp * n_ct;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // (<= ~148 tiles: a serial ascending pass keeps the list ordered)
+        for (int64_t t = 0; t < npt; t++) {
+            const int64_t mp = t / n_ct, n = t % n_ct;
+            const int64_t t0 = (2 * mp) * n_ct + n, t1 = t0 + n_ct;
+            const bool e0 = tile_ptr[t0 * (BN / 32)] == tile_ptr[(t0 + 1) * (BN / 32)];
+            const bool e1 = !(2 * mp + 1 < n_rt) || tile_ptr[t1 * (BN / 32)] == tile_ptr[(t1 + 1) * (BN / 32)];
+            if (!(e0 && e1)) list[cnt++] = (int32_t)t;
+        }
+        list[npt] = cnt;
+    }
+}
+
 // key = ((r / BM) * n_ct + c / BN) * (BN/32) + (c % BN) / 32 ; stable sort keeps r-order inside
 __global__ void k_bucket_keys(const int32_t *__restrict__ r, const int32_t *__restrict__ cc, int64_t ns, int64_t n_ct,
                               uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
@@ -1780,6 +1867,19 @@ void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, i
         GVT_LAUNCH(c, K_PLAN_ROWPTR, k_bucket_ptr, grid1d(nb + 1, 256), 256, 0, k1, ns, nb, sp.tile_ptr);
     } else {
         GVT_CUDA_TRY(cudaMemsetAsync(sp.tile_ptr, 0, sizeof(int64_t) * (nb + 1), c->stream));
+    }
+    // small problems: the non-empty CTA-pair tiles, for the split-K sampled GEMM (one read-back)
+    sp.pair_list = nullptr;
+    sp.n_pairs = -1;
+    const int64_t n_mp = (sp.n_rt + 1) / 2, npt = n_mp * sp.n_ct;
+    if (ns > 0 && c->gemm_cta == 2 && npt <= c->sm_count) {
+        int32_t *list = wsT<int32_t>(c, (t + ".pairs").c_str(), (size_t)npt + 1);
+        GVT_LAUNCH(c, K_PLAN_ROWPTR, k_pair_list, 1, 256, 0, sp.tile_ptr, sp.n_rt, sp.n_ct, list);
+        int32_t *h = (int32_t *)pinned(c, sizeof(int32_t));
+        GVT_CUDA_TRY(cudaMemcpyAsync(h, list + npt, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        sp.pair_list = list;
+        sp.n_pairs = *h;
     }
 }
 

@@ -82,6 +82,10 @@ struct SamplePlan {
     // dense engine: samples bucketed by (r-tile, c-tile); tile_ptr over tiles
     int64_t n_rt = 0, n_ct = 0;
     int64_t *tile_ptr = nullptr;
+    // small problems (pair tiles <= SM count): the non-empty CTA-pair tiles (mp * n_ct + n) and their
+    // count, for the split-K sampled GEMM (-1: not computed)
+    int32_t *pair_list = nullptr;
+    int n_pairs = -1;
 };
 
 // ---- plumbing (plan.cu)

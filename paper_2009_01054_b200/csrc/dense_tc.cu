@@ -284,6 +284,39 @@ constexpr int KC_BLOCKS = 4;                      // k-blocks per accumulation c
 // the fp16 S of stage 1 carries one scale per 256-column tile; stage 2 drains 256-wide K chunks
 static_assert(KC_BLOCKS * (KB_BYTES / 2) == BN, "fp16 accumulation chunk = one S scale tile");
 static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == BM, "S scale block = one stage-1 CTA's rows");
+template <int STRIDE>
+__device__ __forceinline__ void serve_tile(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int n0,
+                                           const float *tile_s, float *part) {
+    constexpr int U = 4;
+    for (int64_t k0 = kb0 + t; k0 < ke; k0 += U * STRIDE) {
+        int off[U];
+        int64_t dd[U];
+        float prev[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t k = k0 + (int64_t)u * STRIDE;
+            if (k < ke) {
+                off[u] = (ep.s_r[k] - m0) * (BN + 1) + (ep.s_c[k] - n0);
+                if (!part) dd[u] = ep.s_dst[k];
+            }
+        }
+        if (!part && ep.accumulate) {
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (k0 + (int64_t)u * STRIDE < ke) prev[u] = ep.out[dd[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t k = k0 + (int64_t)u * STRIDE;
+            if (k < ke) {
+                const float val = tile_s[off[u]];
+                if (part) part[k] = val;
+                else ep.out[dd[u]] = ep.accumulate ? fmaf(ep.coef, val, prev[u]) : ep.coef * val;
+            }
+        }
+    }
+}
+
 // Sampled epilogue: write the samples k in [kb0, ke) of one 32-column chunk (their values parked
 // in `stage`, [rows/32][32][33] floats) to out[dst], SERVE_UNROLL samples per thread in flight.
 // Measured (profiles/r01_ab_serve_unroll.txt): 4 in flight cut C2 from 95 to 83 us per iteration
@@ -292,6 +325,11 @@ static_assert(S16_SCALE_ROWS == 1 || S16_SCALE_ROWS == BM, "S scale block = one 
 template <int STRIDE>
 __device__ __forceinline__ void serve_samples(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0,
                                               int gc0, const float *stage, float *part);
+// all samples [kb0, ke) of one M-tile x N-tile from a parked tile (row stride BN + 1): four per thread in
+// flight; split-K parts go to part[k], else out[dst] (+)= coef value
+template <int STRIDE>
+__device__ __forceinline__ void serve_tile(const struct EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int n0,
+                                           const float *tile_s, float *part);
 constexpr int GROUP_M = 16;                       // row-tiles per rasterization group
 constexpr int N_EPI_WARPS = 8;
 constexpr int NTHREADS = 64 + 32 * N_EPI_WARPS;   // 320
@@ -785,6 +823,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         const int colg = ew >> 2;
         const int row = quarter * 32 + lane;
         const int tE = threadIdx.x - 64;
+        const bool single_unit = n_units <= n_clusters;  // at most one unit per CTA pair
+        static_assert(BM * (BN + 1) * 4 <= STAGES2 * STAGE2_BYTES, "a parked tile fits the operand ring");
         int cg = 0;
         for (int t = cluster; t < n_units; t += n_clusters) {
             int mp_tile, n_tile, c0, c1;
@@ -797,6 +837,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             float run[CW];
 #pragma unroll
             for (int i = 0; i < CW; i++) run[i] = 0.f;
+            // single unit: while the MMAs run, the tile's sample list is staged in the idle epilogue area as
+            // (tile offset, dst) pairs and the row scale is fetched, so the serve after the last chunk reads
+            // shared memory only
+            float ra_pre = 1.f;
+            if (single_unit && m_tile < num_m) {
+                const int64_t tile_id = (int64_t)m_tile * ep.n_ct + n_tile;
+                const int64_t skb = ep.chunk_ptr[tile_id * (BN / 32)], ske = ep.chunk_ptr[(tile_id + 1) * (BN / 32)];
+                if (ske - skb <= (int64_t)(EPI2_BYTES / sizeof(int2))) {
+                    int2 *sl = reinterpret_cast<int2 *>(estage);
+                    for (int64_t k = skb + tE; k < ske; k += 32 * NE)
+                        sl[k - skb] = make_int2((ep.s_r[k] - m0) * (BN + 1) + (ep.s_c[k] - n0),
+                                                part_out ? 0 : ep.s_dst[k]);
+                }
+                if (ep.sa && gr < M) ra_pre = ep.sa[gr];
+            }
             for (int ch = c0; ch < c1; ch++, cg++) {
                 const int b = cg & 1;
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
@@ -854,19 +909,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
             if (threadIdx.x == 64) { GEMM_MARK(5) }
-            if (ep.sa || ep.sb) {
-                const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+            if (ep.sb) {
+                const float ra = single_unit ? ra_pre : ((ep.sa && gr < M) ? ep.sa[gr] : 1.f);
 #pragma unroll
                 for (int i = 0; i < CW; i++) {
                     const int gc = gc_base + i;
-                    const float rb = (ep.sb && gc < N) ? __ldg(ep.sb + gc) : 1.f;
+                    const float rb = gc < N ? __ldg(ep.sb + gc) : 1.f;
                     run[i] *= ra * rb;
                 }
+            } else if (ep.sa) {  // (stage 2: the S operand carries chunk scales, not column scales)
+                const float ra = single_unit ? ra_pre : (gr < M ? ep.sa[gr] : 1.f);
+#pragma unroll
+                for (int i = 0; i < CW; i++) run[i] *= ra;
+            }
+            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
+            const bool tile_ok = m_tile < num_m;
+            if (single_unit) {
+                // this CTA's only unit: its operand ring is idle now, so the whole 128 x 256 tile is parked
+                // there (row stride 257, conflict-free) and all its samples are served in one pass
+                float *tile_s = reinterpret_cast<float *>(smem);
+                if (threadIdx.x == 64) { GEMM_MARK(8) }
+#pragma unroll
+                for (int i = 0; i < CW; i++) tile_s[row * (BN + 1) + colg * CW + i] = run[i];
+                named_bar(1, 32 * NE);
+                if (threadIdx.x == 64) { GEMM_MARK(9) }
+                const int64_t skb = tile_ok ? ep.chunk_ptr[tile * (BN / 32)] : 0;
+                const int64_t ske = tile_ok ? ep.chunk_ptr[(tile + 1) * (BN / 32)] : 0;
+                const bool staged = ske - skb <= (int64_t)(EPI2_BYTES / sizeof(int2));
+                if (tile_ok && staged) {  // (offset, dst) pairs from shared memory
+                    const int2 *sl = reinterpret_cast<const int2 *>(estage);
+                    for (int64_t k = skb + tE; k < ske; k += 32 * NE) {
+                        const int2 e = sl[k - skb];
+                        const float val = tile_s[e.x];
+                        if (part_out) part_out[k] = val;
+                        else ep.out[e.y] = ep.accumulate ? fmaf(ep.coef, val, ep.out[e.y]) : ep.coef * val;
+                    }
+                } else if (tile_ok) {
+                    serve_tile<32 * NE>(ep, skb, ske, tE, m0, n0, tile_s, part_out);
+                }
+                if (threadIdx.x == 64) { GEMM_MARK(10) }
+                continue;
             }
             // chunk c (32 columns) lives in column group c / SG, sub-block c % SG; step j serves chunks j and
             // j + 4 (staging slots hh = 0, 1 of 4 x 32 x 33 floats each)
-            const int64_t tile = (int64_t)m_tile * ep.n_ct + n_tile;
-            const bool tile_ok = m_tile < num_m;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const int g0 = j / SG, g1 = (j + 4) / SG;
@@ -897,6 +982,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         const int half = ew >> 2;
         const int row = quarter * 32 + lane;
         const int t256 = threadIdx.x - 64;  // 0..255
+        // at most one unit per CTA pair (small problems): the operand ring is idle after the last chunk, so
+        // the fp16 store epilogue parks the whole tile there and writes full rows (16-byte stores)
+        const bool single_unit = EPI == EPI_STORE16 && n_units <= n_clusters && (ep.ldc & 7) == 0;
         int cg = 0;
         for (int t = cluster; t < n_units; t += n_clusters) {
             int mp_tile, n_tile, c0, c1;
@@ -908,6 +996,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             float run[128];
 #pragma unroll
             for (int i = 0; i < 128; i++) run[i] = 0.f;
+            float ra_pre = 1.f;
+            float *sb_s = estage + 1024;  // (after the 2 x 256-float maximum exchange)
+            if (single_unit) {  // while the MMAs run: the row scale, and B's column scales into shared memory
+                if (ep.sa && gr < M) ra_pre = ep.sa[gr];
+                sb_s[t256] = (ep.sb && n0 + t256 < N) ? ep.sb[n0 + t256] : 1.f;
+            }
             for (int ch = c0; ch < c1; ch++, cg++) {
                 const int b = cg & 1;
                 mbar_wait(&tfull[b], (cg >> 1) & 1);
@@ -995,18 +1089,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
             if (threadIdx.x == 64) { GEMM_MARK(5) }
+            if (single_unit) named_bar(1, 32 * N_EPI_WARPS);  // the staged column scales are visible
             if (EPI == EPI_STORE16) {
                 // fp16 hi/lo of the unscaled result with a power-of-two scale per (128-row CTA block,
                 // 256-col tile) from the block's maximum (S16_SCALE_ROWS = 128: a CTA-wide max over
                 // the 8 epilogue warps), or per (row, 256-col tile) (S16_SCALE_ROWS = 1: the two warps
                 // holding this row's column halves exchange their maxima)
-                const float ra = (ep.sa && gr < M) ? ep.sa[gr] : 1.f;
+                const float ra = single_unit ? ra_pre : ((ep.sa && gr < M) ? ep.sa[gr] : 1.f);
                 float mx = 0.f;
                 // column scales of B in 16-byte loads (the scale vector is padded to 128 rows)
 #pragma unroll
                 for (int i4 = 0; i4 < 32; i4++) {
-                    const float4 rb4 = ep.sb ? __ldg(reinterpret_cast<const float4 *>(ep.sb + gc_base) + i4)
-                                            : make_float4(1.f, 1.f, 1.f, 1.f);
+                    const float4 rb4 = single_unit ? reinterpret_cast<const float4 *>(sb_s + half * 128)[i4]
+                                       : ep.sb ? __ldg(reinterpret_cast<const float4 *>(ep.sb + gc_base) + i4)
+                                               : make_float4(1.f, 1.f, 1.f, 1.f);
                     const float rbv[4] = {rb4.x, rb4.y, rb4.z, rb4.w};
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
@@ -1047,6 +1143,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 // contiguous bytes per piece (a thread-per-row store pattern would touch 32 lines
                 // per instruction; it dominated the epilogue of short-K tiles)
                 if (threadIdx.x == 64) { GEMM_MARK(9) }
+                if (single_unit) {
+                    // the tile as fp16 hi / lo rows in the idle ring (pitch 264 halves: the 16-byte writes of 8
+                    // consecutive rows hit distinct banks), then each warp stores whole rows, 512 B per piece
+                    constexpr int TPH = BN + 8;
+                    __half *th = reinterpret_cast<__half *>(smem), *tl = th + BM * TPH;
+#pragma unroll
+                    for (int c8 = 0; c8 < 16; c8++) {
+                        uint32_t hp[4], lp[4];
+#pragma unroll
+                        for (int i = 0; i < 8; i += 2) {
+                            const float v0 = run[c8 * 8 + i] * s, v1 = run[c8 * 8 + i + 1] * s;
+                            const __half2 h = __float22half2_rn(make_float2(v0, v1));
+                            const float2 hf = __half22float2(h);
+                            const __half2 l = __float22half2_rn(make_float2(v0 - hf.x, v1 - hf.y));
+                            hp[i / 2] = *reinterpret_cast<const uint32_t *>(&h);
+                            lp[i / 2] = *reinterpret_cast<const uint32_t *>(&l);
+                        }
+                        *reinterpret_cast<uint4 *>(th + row * TPH + half * 128 + c8 * 8) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+                        *reinterpret_cast<uint4 *>(tl + row * TPH + half * 128 + c8 * 8) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+                    }
+                    named_bar(1, 32 * N_EPI_WARPS);
+                    const int gc = n0 + 8 * lane;
+                    for (int r = ew; r < BM; r += N_EPI_WARPS) {
+                        if (m0 + r >= M) break;
+                        const uint4 vh = *reinterpret_cast<const uint4 *>(th + r * TPH + 8 * lane);
+                        const uint4 vl = *reinterpret_cast<const uint4 *>(tl + r * TPH + 8 * lane);
+                        const int64_t o = (int64_t)(m0 + r) * ep.ldc + gc;
+                        if (gc + 8 <= N) {
+                            *reinterpret_cast<uint4 *>(ep.c_h16 + o) = vh;
+                            *reinterpret_cast<uint4 *>(ep.c_l16 + o) = vl;
+                        } else {
+                            const __half *ph = reinterpret_cast<const __half *>(&vh), *pl = reinterpret_cast<const __half *>(&vl);
+                            for (int u = 0; u < 8 && gc + u < N; u++) {
+                                ep.c_h16[o + u] = ph[u];
+                                ep.c_l16[o + u] = pl[u];
+                            }
+                        }
+                    }
+                    if (threadIdx.x == 64) { GEMM_MARK(10) }
+                    named_bar(1, 32 * N_EPI_WARPS);
+                    continue;
+                }
                 uint32_t *blk = reinterpret_cast<uint32_t *>(estage) + (half * 4 + quarter) * 32 * 33;
                 const int64_t row0 = (int64_t)m0 + quarter * 32;
 #pragma unroll

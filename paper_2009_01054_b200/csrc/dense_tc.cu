@@ -1649,7 +1649,8 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
     }
 }
 
-// the same rows, one WARP per row, for short rows (ld <= 4096: C2/C3-size problems): the CTA-wide
+// the same rows, one WARP per row, for short rows (ld <= 2048: C2/C3-size problems; C4 Poly2D's
+// 3008-wide rows measured 3-4 % slower per CG iteration with it): the CTA-wide
 // barriers of k_build_x16 (zero, gather, max, store) become __syncwarp, and every row of the matrix is
 // in flight at once (8 rows per CTA, ld floats of shared memory each).  Same cell sums (entry order),
 // same scale rule, same stores.
@@ -1749,7 +1750,7 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_dev = smem;
     }
-    if (rows > 0 && o.ld <= 4096 && build_warp_rows()) {
+    if (rows > 0 && o.ld <= 2048 && build_warp_rows()) {
         const size_t smem8 = 8 * smem;
         static size_t attr_w[GVT_MAX_DEVICES] = {};
         size_t &aw = attr_w[c->device < GVT_MAX_DEVICES ? c->device : 0];

@@ -137,9 +137,9 @@ def config_dict(args, w, kernel, world):
 # ----------------------------------------------------------------------------- roofline
 def _traffic(kernel_kind):
     """DRAM bytes per launch of `kernel_kind` from the committed ncu --set full capture
-    (profiles/r01_traffic.json), or None."""
+    (profiles/r02_traffic.json), or None."""
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")) as fh:
             rec = json.load(fh).get(kernel_kind)
         return int(rec["bytes"]) if rec else None
     except (OSError, ValueError, KeyError):
@@ -203,7 +203,7 @@ def roofline(kinds: dict, w, kernel, launches_per_step: dict, peaks: dict, engin
                     "frac": round(achieved / alu_peak, 4), "traffic": traffic,
                     "peak_source": "fp32 SIMT: 148 SM x 128 lanes x 2 x sm_max_mhz"})
     if traffic is not None:
-        out["traffic_unit"] = "bytes per launch (ncu dram read + write, profiles/r01_traffic.json)"
+        out["traffic_unit"] = "bytes per launch (ncu dram read + write, profiles/r02_traffic.json)"
     return out
 
 

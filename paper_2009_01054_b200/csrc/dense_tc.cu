@@ -652,7 +652,23 @@ __host__ __device__ constexpr uint32_t idesc_mma2() {
 #endif
 static_assert(SAMPLED_EPI_WARPS == 8 || SAMPLED_EPI_WARPS == 16, "sampled epilogue: 8 or 16 warps");
 __host__ __device__ constexpr int pair_epi_warps(int epi) { return epi == EPI_SAMPLED ? SAMPLED_EPI_WARPS : N_EPI_WARPS; }
-__host__ __device__ constexpr int pair_threads(int epi) { return 64 + 32 * pair_epi_warps(epi); }
+// Register reallocation (setmaxnreg) in the sampled kernel: warpgroup 0 = TMA producer, MMA issuer and two idle
+// warps gives registers back (SAMPLED_REG_LO), the four epilogue warpgroups take them (SAMPLED_REG_HI).  The
+// pool is the CTA's launch allocation (20 warps x 96 registers), so 4 x 32 x LO + 16 x 32 x HI must not exceed
+// 640 x 96 -- an over-subscribed setmaxnreg.inc never returns.  The epilogue's 64 accumulators then stay in
+// registers through the drain.  Measured (profiles/r02_ab_regrealloc.txt): the stage-2 GEMM does the same
+// work in fewer clocks but the clock drops under the power cap and the C5 fit gets 2-4 % slower, so the
+// default is 0: 18 warps at 96 registers (-DSAMPLED_REGREALLOC=1 builds the reallocation layout).
+#ifndef SAMPLED_REGREALLOC
+#define SAMPLED_REGREALLOC 0
+#endif
+#define SAMPLED_REG_LO 32
+#define SAMPLED_REG_HI 112
+static_assert(4 * 32 * SAMPLED_REG_LO + 16 * 32 * SAMPLED_REG_HI <= 640 * 96, "setmaxnreg pool over-subscribed");
+__host__ __device__ constexpr int pair_epi_first_warp(int epi) {
+    return (epi == EPI_SAMPLED && SAMPLED_REGREALLOC) ? 4 : 2;
+}
+__host__ __device__ constexpr int pair_threads(int epi) { return 32 * pair_epi_first_warp(epi) + 32 * pair_epi_warps(epi); }
 
 template <int PREC, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1)
@@ -748,7 +764,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) { GEMM_MARK(1) }
+    constexpr int EW0 = pair_epi_first_warp(EPI);  // first epilogue warp
 
+    if (warp < EW0) {  // ---------------- warpgroup 0 (register reallocation) / warps 0, 1
+    if constexpr (EW0 == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SAMPLED_REG_LO));
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             int kg = 0;  // global k-block counter = ring position
@@ -812,17 +831,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             }
             GEMM_MARK(3)
         }
+    }  // (warps 2, 3 of the register-reallocation layout: idle)
     } else if constexpr (EPI == EPI_SAMPLED) {
-        // ---------------- sampled epilogue, warps 2..(NE+1) (both CTAs, own 128 rows): warp w reads TMEM
-        // lanes 32*(w%4).. and the CW columns of column group (w-2)/4; per K chunk the accumulator is
+        if constexpr (EW0 == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SAMPLED_REG_HI));
+        // ---------------- sampled epilogue, warps EW0..(EW0+NE-1) (both CTAs, own 128 rows): warp w reads
+        // TMEM lanes 32*(w%4).. and the CW columns of column group (w-EW0)/4; per K chunk the accumulator is
         // drained into fp32 registers with round-to-nearest adds (times S's chunk scale), then the tile's
         // samples are served from a shared-memory copy, two 32-column chunks at a time
         constexpr int NE = SAMPLED_EPI_WARPS, CW = 1024 / NE, SG = CW / 32;
-        const int ew = warp - 2;
+        const int ew = warp - EW0;
         const int quarter = warp & 3;
         const int colg = ew >> 2;
         const int row = quarter * 32 + lane;
-        const int tE = threadIdx.x - 64;
+        const int tE = threadIdx.x - 32 * EW0;
         const bool single_unit = n_units <= n_clusters;  // at most one unit per CTA pair
         static_assert(BM * (BN + 1) * 4 <= STAGES2 * STAGE2_BYTES, "a parked tile fits the operand ring");
         int cg = 0;
@@ -908,7 +929,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(&tempty[b]);
             }
-            if (threadIdx.x == 64) { GEMM_MARK(5) }
+            if (threadIdx.x == 32 * EW0) { GEMM_MARK(5) }
             if (ep.sb) {
                 const float ra = single_unit ? ra_pre : ((ep.sa && gr < M) ? ep.sa[gr] : 1.f);
 #pragma unroll
@@ -928,11 +949,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 // this CTA's only unit: its operand ring is idle now, so the whole 128 x 256 tile is parked
                 // there (row stride 257, conflict-free) and all its samples are served in one pass
                 float *tile_s = reinterpret_cast<float *>(smem);
-                if (threadIdx.x == 64) { GEMM_MARK(8) }
+                if (threadIdx.x == 32 * EW0) { GEMM_MARK(8) }
 #pragma unroll
                 for (int i = 0; i < CW; i++) tile_s[row * (BN + 1) + colg * CW + i] = run[i];
                 named_bar(1, 32 * NE);
-                if (threadIdx.x == 64) { GEMM_MARK(9) }
+                if (threadIdx.x == 32 * EW0) { GEMM_MARK(9) }
                 const int64_t skb = tile_ok ? ep.chunk_ptr[tile * (BN / 32)] : 0;
                 const int64_t ske = tile_ok ? ep.chunk_ptr[(tile + 1) * (BN / 32)] : 0;
                 const bool staged = ske - skb <= (int64_t)(EPI2_BYTES / sizeof(int2));
@@ -947,7 +968,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 } else if (tile_ok) {
                     serve_tile<32 * NE>(ep, skb, ske, tE, m0, n0, tile_s, part_out);
                 }
-                if (threadIdx.x == 64) { GEMM_MARK(10) }
+                if (threadIdx.x == 32 * EW0) { GEMM_MARK(10) }
                 continue;
             }
             // chunk c (32 columns) lives in column group c / SG, sub-block c % SG; step j serves chunks j and
@@ -975,7 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
                 named_bar(1, 32 * NE);
             }
         }
-        if (threadIdx.x == 64) { GEMM_MARK(6) }
+        if (threadIdx.x == 32 * EW0) { GEMM_MARK(6) }
     } else {  // ---------------- epilogue warps 2..9 (both CTAs, own 128 rows)
         const int ew = warp - 2;
         const int quarter = warp & 3;

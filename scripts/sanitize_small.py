@@ -65,3 +65,30 @@ ctx.gram(G.BASE_TANIMOTO, d(B))
 ctx.gram_cross(G.BASE_TANIMOTO, d(B), d(B[:33]))
 torch.cuda.synchronize()
 print("sanitize_small additions done")
+
+# ---- round-2 paths: symmetric GEMV (square Gram >= 6144), fused CG tail (Ranking / Linear / Poly2D),
+#      split-K sampled GEMM and single-unit epilogues (few pair tiles, K >= 1024), warp-per-row X build
+rng = np.random.default_rng(2)
+ctx2 = G.Context(0)
+m = 6200
+Dn = ctx2.gram(G.BASE_GAUSSIAN, d(rng.standard_normal((m, 8)).astype(np.float32)), gamma=0.1)
+f = d(rng.integers(0, m, 20000).astype(np.int32)); s = d(rng.integers(0, m, 20000).astype(np.int32))
+y = d(rng.standard_normal(20000).astype(np.float32))
+for k in (G.RANKING, G.LINEAR):
+    t = G.gvt_kernel_terms(k)
+    a, _, _, _ = ctx2.fit(Dn, None if k == G.RANKING else Dn, f, s, y, t, 1.0, 3)
+    torch.cuda.synchronize()
+print("symv + cg tail ok")
+m = 1100
+Dm = ctx2.gram(G.BASE_GAUSSIAN, d(rng.standard_normal((m, 8)).astype(np.float32)), gamma=0.1)
+i = rng.integers(0, m, 30000); j = rng.integers(0, m, 30000); keep = i < j
+f = d(i[keep].astype(np.int32)); s = d(j[keep].astype(np.int32)); n = int(keep.sum())
+y = d(rng.standard_normal(n).astype(np.float32))
+ctx2.set_option(G.OPT_ENGINE, 2)
+for k in (G.SYMMETRIC, G.KRONECKER):
+    t = G.gvt_kernel_terms(k)
+    a, _, _, _ = ctx2.fit(Dm, None if k == G.SYMMETRIC else Dm, f, s, y, t, 1.0, 3)
+    u = ctx2.matvec(Dm, None if k == G.SYMMETRIC else Dm, f, s, f, s, a, t)
+    torch.cuda.synchronize()
+print("split-K + single-unit epilogues + warp build ok")
+ctx2.close()

@@ -31,6 +31,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ops.cuh"
@@ -850,7 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         for (int t = cluster; t < n_units; t += n_clusters) {
             int mp_tile, n_tile, c0, c1;
             if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
-            float *part_out = ep.tile_list ? ep.part + (int64_t)(t % ep.split) * ep.ns : nullptr;
+            float *part_out = (ep.tile_list && ep.part) ? ep.part + (int64_t)(t % ep.split) * ep.ns : nullptr;
             const int m_tile = 2 * mp_tile + (int)crank;
             const int m0 = m_tile * BM, n0 = n_tile * BN;
             const int gr = m0 + row;
@@ -1902,6 +1903,14 @@ __global__ void k_split_combine(const float *__restrict__ part, int split, int64
 // K parts per non-empty pair tile: when at most half of the CTA pairs would have a tile, each tile's
 // K range is split (at accumulation-chunk boundaries, >= 2 chunks per part) so every pair works --
 // C3's upper-triangle samples leave ~36 of 64 pair tiles non-empty on 74 CTA pairs.  GVT_SPLITK=0: off.
+static bool compact_tiles() {  // A/B knob: GVT_COMPACT_TILES=0 strides over all pair tiles (round-1 loop)
+    static const bool on = [] {
+        const char *e = getenv("GVT_COMPACT_TILES");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 static int sampled_split(gvt_ctx *c, const SamplePlan &sp, int64_t K) {
     static const int env = [] {
         const char *e = getenv("GVT_SPLITK");
@@ -1930,12 +1939,20 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.accumulate = accumulate;
     ep.out = out;
     const int split = sampled_split(c, sp, K);
+    const int64_t npt = ((sp.n_rt + 1) / 2) * sp.n_ct;
     if (split > 1) {
         ep.tile_list = sp.pair_list;
         ep.split = split;
         ep.n_units = sp.n_pairs * split;
         ep.ns = sp.ns;
         ep.part = wsT<float>(c, "splitk.part", (size_t)split * sp.ns);
+    } else if (sp.pair_list && sp.n_pairs > 0 && sp.n_pairs < npt && compact_tiles()) {
+        // some pair tiles are empty: the persistent loop runs over the non-empty ones only, so every CTA pair
+        // gets the same number of tiles (striding over all tiles left pairs with several non-empty tiles
+        // next to pairs with none; e.g. C4 MLPK's drug x target block)
+        ep.tile_list = sp.pair_list;
+        ep.split = 1;
+        ep.n_units = sp.n_pairs;
     }
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
     if (split > 1)
@@ -1944,23 +1961,37 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
 }
 
 // ----------------------------------------------------------------------------- sample bucketing
-// the CTA-pair tiles (M-tiles 2 mp, 2 mp + 1 x N-tile n) holding samples, ascending, and their count at
-// list[n_mp * n_ct]; one CTA (small problems only: at most one tile per SM)
-__global__ void k_pair_list(const int64_t *__restrict__ tile_ptr, int64_t n_rt, int64_t n_ct, int32_t *__restrict__ list) {
-    __shared__ int cnt;
-    const int64_t n_mp = (n_rt + 1) / 2, npt = n_mp * n_ct;
-    if (threadIdx.x == 0) cnt = 0;
+// the CTA-pair tiles (M-tiles 2 mp, 2 mp + 1 x N-tile n) holding samples, in the kernel's grouped
+// rasterization order (GROUP_M pair rows per group, as coords()), and their count at list[n_mp * n_ct]:
+// one CTA, 256 tiles per step (flags, then a block scan keeps the order)
+__global__ void __launch_bounds__(256) k_pair_list(const int64_t *__restrict__ tile_ptr, int64_t n_rt, int64_t n_ct,
+                                                   int32_t *__restrict__ list) {
+    using Scan = cub::BlockScan<int, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int base;
+    const int64_t n_mp = (n_rt + 1) / 2, npt = n_mp * n_ct, in_group = (int64_t)GROUP_M * n_ct;
+    if (threadIdx.x == 0) base = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {  // (<= ~148 tiles: a serial ascending pass keeps the list ordered)
-        for (int64_t t = 0; t < npt; t++) {
-            const int64_t mp = t / n_ct, n = t % n_ct;
-            const int64_t t0 = (2 * mp) * n_ct + n, t1 = t0 + n_ct;
-            const bool e0 = tile_ptr[t0 * (BN / 32)] == tile_ptr[(t0 + 1) * (BN / 32)];
-            const bool e1 = !(2 * mp + 1 < n_rt) || tile_ptr[t1 * (BN / 32)] == tile_ptr[(t1 + 1) * (BN / 32)];
-            if (!(e0 && e1)) list[cnt++] = (int32_t)t;
+    for (int64_t t0 = 0; t0 < npt; t0 += 256) {
+        const int64_t t = t0 + threadIdx.x;
+        int flag = 0, tl = 0;
+        if (t < npt) {
+            const int64_t first_m = (t / in_group) * GROUP_M, group_m = min(n_mp - first_m, (int64_t)GROUP_M);
+            const int64_t mp = first_m + (t % in_group) % group_m, n = (t % in_group) / group_m;
+            const int64_t a0 = (2 * mp) * n_ct + n, a1 = a0 + n_ct;
+            const bool e0 = tile_ptr[a0 * (BN / 32)] == tile_ptr[(a0 + 1) * (BN / 32)];
+            const bool e1 = !(2 * mp + 1 < n_rt) || tile_ptr[a1 * (BN / 32)] == tile_ptr[(a1 + 1) * (BN / 32)];
+            flag = !(e0 && e1);
+            tl = (int)(mp * n_ct + n);
         }
-        list[npt] = cnt;
+        int pos, total;
+        Scan(tmp).ExclusiveSum(flag, pos, total);
+        if (flag) list[base + pos] = tl;
+        __syncthreads();
+        if (threadIdx.x == 0) base += total;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) list[npt] = base;
 }
 
 // key = ((r / BM) * n_ct + c / BN) * (BN/32) + (c % BN) / 32 ; stable sort keeps r-order inside
@@ -2028,11 +2059,12 @@ void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, i
     } else {
         GVT_CUDA_TRY(cudaMemsetAsync(sp.tile_ptr, 0, sizeof(int64_t) * (nb + 1), c->stream));
     }
-    // small problems: the non-empty CTA-pair tiles, for the split-K sampled GEMM (one read-back)
+    // the non-empty CTA-pair tiles, for the split-K sampled GEMM and for balancing the persistent loop over
+    // non-empty tiles only (one read-back)
     sp.pair_list = nullptr;
     sp.n_pairs = -1;
     const int64_t n_mp = (sp.n_rt + 1) / 2, npt = n_mp * sp.n_ct;
-    if (ns > 0 && c->gemm_cta == 2 && npt <= c->sm_count) {
+    if (ns > 0 && c->gemm_cta == 2) {
         int32_t *list = wsT<int32_t>(c, (t + ".pairs").c_str(), (size_t)npt + 1);
         GVT_LAUNCH(c, K_PLAN_ROWPTR, k_pair_list, 1, 256, 0, sp.tile_ptr, sp.n_rt, sp.n_ct, list);
         int32_t *h = (int32_t *)pinned(c, sizeof(int32_t));

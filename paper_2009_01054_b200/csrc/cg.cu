@@ -8,17 +8,9 @@
 //
 // state[] (double, device): 0 rho, 1 alpha, 2 beta, 3 ||y||, 4 pAp, 5 done, 6 breakdown,
 //                           7 iters, 8 rel_tol
-#include "vecops.cuh"
+#include "cgops.cuh"
 
 namespace gvt {
-
-enum { ST_RHO = 0, ST_ALPHA, ST_BETA, ST_YNORM, ST_PAP, ST_DONE, ST_BREAK, ST_ITERS, ST_TOL, ST_N };
-
-// ||r_k|| / ||y|| at which the fp32 solvers stop as converged (2^-60, far below what fp32 vectors
-// resolve; reading S32)
-constexpr double RES_FLOOR = 8.673617379884035e-19;
-
-__device__ __forceinline__ bool halted(const double *st) { return st[ST_DONE] != 0.0 || st[ST_BREAK] != 0.0; }
 
 __global__ void __launch_bounds__(RED_THREADS) k_cg_init(const float *__restrict__ y, int64_t n, float *__restrict__ x,
                                                          float *__restrict__ r, float *__restrict__ p,
@@ -55,25 +47,6 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_init_scalars(const double *_
     }
 }
 
-// the scalar steps (thread 0 of the reducing block)
-__device__ __forceinline__ void cg_alpha_scalar(double pap, double *st) {
-    st[ST_PAP] = pap;
-    if (!(pap > 0.0)) st[ST_BREAK] = 1.0;
-    else st[ST_ALPHA] = st[ST_RHO] / pap;
-}
-
-__device__ __forceinline__ void cg_beta_scalar(double rho1, double *st, double *relres) {
-    double it = st[ST_ITERS] + 1.0;
-    st[ST_ITERS] = it;
-    double rr = sqrt(rho1) / st[ST_YNORM];
-    if (relres) relres[(int64_t)it] = rr;
-    // converged: the tolerance, or the residual floor RES_FLOOR (reading S32: below it the fp32
-    // recurrences only underflow, into 0/0 after ~120 iterations on C1)
-    if ((st[ST_TOL] > 0.0 && rr <= st[ST_TOL]) || rho1 == 0.0 || rr <= RES_FLOOR) st[ST_DONE] = 1.0;
-    st[ST_BETA] = rho1 / st[ST_RHO];
-    st[ST_RHO] = rho1;
-}
-
 // Ap += lambda p ; partial p.Ap.  With a ticket (single GPU), the last block to finish also reduces
 // the partials and takes the alpha step (k_cg_alpha folded in: one launch fewer per iteration).
 __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, const float *__restrict__ p, int64_t n,
@@ -82,32 +55,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(float *__restrict__ Ap, c
     if (halted(st)) return;
     int64_t lo, hi;
     block_range(n, lo, hi);
-    double acc = 0.0;
-    if (aligned16(Ap) && aligned16(p)) {
-        const int64_t lo4 = lo >> 2, hi4 = hi >> 2;
-        float4 *A4 = reinterpret_cast<float4 *>(Ap);
-        const float4 *p4 = reinterpret_cast<const float4 *>(p);
-        for (int64_t i = lo4 + threadIdx.x; i < hi4; i += blockDim.x) {
-            float4 a = A4[i], pp = p4[i];
-            a.x = fmaf(lambda, pp.x, a.x); a.y = fmaf(lambda, pp.y, a.y);
-            a.z = fmaf(lambda, pp.z, a.z); a.w = fmaf(lambda, pp.w, a.w);
-            A4[i] = a;
-            acc += (double)pp.x * a.x + (double)pp.y * a.y + (double)pp.z * a.z + (double)pp.w * a.w;
-        }
-        const int64_t t0 = (hi4 << 2) > lo ? (hi4 << 2) : lo;  // tail of the last non-empty block only
-        for (int64_t i = t0 + threadIdx.x; i < hi; i += blockDim.x) {
-            float a = fmaf(lambda, p[i], Ap[i]);
-            Ap[i] = a;
-            acc += (double)p[i] * a;
-        }
-    } else {
-        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            float pi = p[i];
-            float a = fmaf(lambda, pi, Ap[i]);
-            Ap[i] = a;
-            acc += (double)pi * (double)a;
-        }
-    }
+    double acc = cg_ap_range<false>(Ap, p, lo, hi, lambda);
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
     if (ticket && last_block_done(ticket)) {
@@ -175,37 +123,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(float *__restrict__ x, fl
     const float alpha = (float)st[ST_ALPHA];
     int64_t lo, hi;
     block_range(n, lo, hi);
-    double acc = 0.0;
-    if (aligned16(x) && aligned16(r) && aligned16(p) && aligned16(Ap)) {
-        const int64_t lo4 = lo >> 2, hi4 = hi >> 2;
-        float4 *x4 = reinterpret_cast<float4 *>(x);
-        float4 *r4 = reinterpret_cast<float4 *>(r);
-        const float4 *p4 = reinterpret_cast<const float4 *>(p), *a4 = reinterpret_cast<const float4 *>(Ap);
-        for (int64_t i = lo4 + threadIdx.x; i < hi4; i += blockDim.x) {
-            float4 xx = x4[i], rr = r4[i], pp = p4[i], aa = a4[i];
-            xx.x = fmaf(alpha, pp.x, xx.x); xx.y = fmaf(alpha, pp.y, xx.y);
-            xx.z = fmaf(alpha, pp.z, xx.z); xx.w = fmaf(alpha, pp.w, xx.w);
-            rr.x = fmaf(-alpha, aa.x, rr.x); rr.y = fmaf(-alpha, aa.y, rr.y);
-            rr.z = fmaf(-alpha, aa.z, rr.z); rr.w = fmaf(-alpha, aa.w, rr.w);
-            x4[i] = xx;
-            r4[i] = rr;
-            acc += (double)rr.x * rr.x + (double)rr.y * rr.y + (double)rr.z * rr.z + (double)rr.w * rr.w;
-        }
-        const int64_t t0 = (hi4 << 2) > lo ? (hi4 << 2) : lo;  // tail of the last non-empty block only
-        for (int64_t i = t0 + threadIdx.x; i < hi; i += blockDim.x) {
-            x[i] = fmaf(alpha, p[i], x[i]);
-            float ri = fmaf(-alpha, Ap[i], r[i]);
-            r[i] = ri;
-            acc += (double)ri * (double)ri;
-        }
-    } else {
-        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            x[i] = fmaf(alpha, p[i], x[i]);
-            float ri = fmaf(-alpha, Ap[i], r[i]);
-            r[i] = ri;
-            acc += (double)ri * (double)ri;
-        }
-    }
+    double acc = cg_xr_range<false>(x, r, p, Ap, lo, hi, alpha);
     acc = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
     if (ticket && last_block_done(ticket)) {
@@ -228,24 +146,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_beta(const double *__restric
 __global__ void __launch_bounds__(RED_THREADS) k_cg_p(float *__restrict__ p, const float *__restrict__ r, int64_t n,
                                                       const double *__restrict__ st) {
     if (halted(st)) return;
-    const float beta = (float)st[ST_BETA];
-    if (aligned16(p) && aligned16(r)) {
-        const int64_t n4 = n >> 2;
-        float4 *p4 = reinterpret_cast<float4 *>(p);
-        const float4 *r4 = reinterpret_cast<const float4 *>(r);
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-            float4 pp = p4[i], rr = r4[i];
-            pp.x = fmaf(beta, pp.x, rr.x); pp.y = fmaf(beta, pp.y, rr.y);
-            pp.z = fmaf(beta, pp.z, rr.z); pp.w = fmaf(beta, pp.w, rr.w);
-            p4[i] = pp;
-        }
-        for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-             i += (int64_t)gridDim.x * blockDim.x)
-            p[i] = fmaf(beta, p[i], r[i]);
-    } else {
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-            p[i] = fmaf(beta, p[i], r[i]);
-    }
+    cg_p_grid<false>(p, r, n, (float)st[ST_BETA], blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                     (int64_t)gridDim.x * blockDim.x);
 }
 
 // ============================================================================ single-reduction CG
@@ -433,6 +335,9 @@ void cgg_finish(gvt_ctx *c, const float *r, int64_t n, double *state) {
 }
 
 // partial-sum slots [world][RED_BLOCKS]; this rank writes slot `rank`
+int cg_vec_blocks(int64_t n) { return vec_blocks(n); }
+double *cg_parts(gvt_ctx *c) { return solver_parts(c); }
+
 double *solver_parts(gvt_ctx *c) { return wsT<double>(c, "cg.parts", (size_t)RED_BLOCKS * (c->world > 0 ? c->world : 1)); }
 static double *my_parts(gvt_ctx *c) { return solver_parts(c) + (size_t)c->rank * RED_BLOCKS; }
 

@@ -35,6 +35,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "ops.cuh"
+#include "xbuild.cuh"
 
 namespace gvt {
 
@@ -1687,63 +1688,8 @@ __global__ void __launch_bounds__(256) k_build_x16_warp(const int64_t *__restric
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float *rowbuf = rowbufs + (size_t)warp * ld;
     const int64_t nw = (int64_t)gridDim.x * 8;
-    for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < rows; r += nw) {
-        float4 *rb4 = reinterpret_cast<float4 *>(rowbuf);
-        for (int64_t j = lane; j < ld / 4; j += 32) rb4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncwarp();
-        const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
-        constexpr int U = 4;  // entries in flight per lane
-        for (int64_t k0 = kb + lane; k0 < ke; k0 += U * 32) {
-            int32_t cc[U], cprev[U], cnext[U];
-            float v[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const int64_t k = k0 + (int64_t)u * 32;
-                cc[u] = -1;
-                if (k < ke) {
-                    cc[u] = col[k];
-                    cprev[u] = k > kb ? col[k - 1] : -1;
-                    cnext[u] = k + 1 < ke ? col[k + 1] : -1;
-                    v[u] = sign[k] * __ldg(p + src[k]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (cc[u] < 0 || cprev[u] == cc[u]) continue;  // past the row end, or not the head of its run
-                float sv = v[u];
-                if (cnext[u] == cc[u]) {
-                    const int64_t k = k0 + (int64_t)u * 32;
-                    for (int64_t j = k + 1; j < ke && col[j] == cc[u]; j++) sv += sign[j] * __ldg(p + src[j]);
-                }
-                rowbuf[cc[u]] = sv;
-            }
-        }
-        __syncwarp();
-        if (diag && lane == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
-        __syncwarp();
-        float mx = 0.f;
-        for (int64_t j = lane; j < ld / 4; j += 32) {
-            const float4 v4 = rb4[j];
-            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v4.x), fabsf(v4.y)), fmaxf(fabsf(v4.z), fabsf(v4.w))));
-        }
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        int e = 0;
-        if (mx > 0.f && isfinite(mx)) {
-            int ex;
-            frexpf(mx, &ex);
-            e = 15 - ex;
-        }
-        const float sc = ldexpf(1.f, e);
-        if (lane == 0) sinv[r] = ldexpf(1.f, -e);
-        __half2 *h2 = reinterpret_cast<__half2 *>(hi + r * ld), *l2 = reinterpret_cast<__half2 *>(lo + r * ld);
-        for (int64_t j = lane; j < ld / 2; j += 32) {
-            const float v0 = rowbuf[2 * j] * sc, v1 = rowbuf[2 * j + 1] * sc;
-            const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1);
-            h2[j] = __halves2half2(a0, a1);
-            l2[j] = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
-        }
-        __syncwarp();
-    }
+    for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < rows; r += nw)
+        x16_row_warp<false>(r, lane, rowbuf, row_ptr, col, src, sign, p, row_lo, ld, hi, lo, sinv, diag);
 }
 
 static bool build_warp_rows() {  // A/B knob: GVT_BUILD_WARP=0 keeps the CTA-per-row build for short rows
@@ -1755,7 +1701,7 @@ static bool build_warp_rows() {  // A/B knob: GVT_BUILD_WARP=0 keeps the CTA-per
 }
 
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag) {
+                  const float *p, const float *diag, bool launch) {
     Operand o;
     o.prec = PREC_F16;
     o.ld = round_up(cols > 0 ? cols : 1, 32);
@@ -1764,6 +1710,12 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     __half *hi = wsT<__half>(c, (nm + ".h16").c_str(), (size_t)rows_pad * o.ld);
     __half *lo = wsT<__half>(c, (nm + ".l16").c_str(), (size_t)rows_pad * o.ld);
     float *s = wsT<float>(c, (nm + ".sinv").c_str(), (size_t)rows_pad);
+    if (!launch) {
+        o.hi = hi;
+        o.lo = lo;
+        o.scale = s;
+        return o;
+    }
     const size_t smem = sizeof(float) * o.ld;
     static size_t attr_smem[GVT_MAX_DEVICES] = {};
     size_t &attr_dev = attr_smem[c->device < GVT_MAX_DEVICES ? c->device : 0];
@@ -1926,7 +1878,8 @@ static int sampled_split(gvt_ctx *c, const SamplePlan &sp, int64_t K) {
 }
 
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
-                     const SamplePlan &sp, float coef, int accumulate, float *out) {
+                     const SamplePlan &sp, float coef, int accumulate, float *out, SplitParts *defer) {
+    if (defer) *defer = SplitParts();
     if (sp.ns == 0) return;
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -1955,7 +1908,13 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
         ep.n_units = sp.n_pairs;
     }
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
-    if (split > 1)
+    if (split > 1 && defer && !accumulate) {
+        defer->part = ep.part;
+        defer->split = split;
+        defer->ns = sp.ns;
+        defer->dst = sp.dst;
+        defer->coef = coef;
+    } else if (split > 1)
         GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine, grid1d(sp.ns, 256, 8 * c->sm_count), 256, 0, ep.part, split, sp.ns,
                    sp.dst, coef, accumulate, out);
 }

@@ -575,8 +575,15 @@ static bool stage2_gather_pays(gvt_ctx *c, int64_t ns, int64_t M, int64_t N, int
     return ga < tc;
 }
 
+// the fused dense-engine CG tail's view of one matvec (fit_impl, tail.cu): X(p) and the S-scale zeros
+// already in place (built by the previous tail launch), and the split-K parts left for the tail
+struct DenseFuse {
+    bool prebuilt = false;
+    SplitParts parts;
+};
+
 static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
-                          float *out) {
+                          float *out, DenseFuse *df = nullptr) {
     // S scales: one power-of-two scale per (row, 256-col tile) from the tile maxima, applied per
     // K-chunk in stage 2 (S16_SCALE_ROWS = 1); the A/B build -DS16_SCALE_ROWS=128 keeps one scale
     // per (128-row block, 256-col tile) instead (ops.cuh: fewer clocks, more energy at C5)
@@ -585,12 +592,13 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
     __half *Sh = wsT<__half>(c, (g.tag + ".S16h").c_str(), slab_h * g.nslab);
     __half *Sl = wsT<__half>(c, (g.tag + ".S16l").c_str(), slab_h * g.nslab);
     float *Sk = wsT<float>(c, (g.tag + ".S16k").c_str(), slab_k * g.nslab);
-    GVT_CUDA_TRY(cudaMemsetAsync(Sk, 0, sizeof(float) * slab_k * g.nslab, c->stream));
+    const bool prebuilt = df && df->prebuilt;
+    if (!prebuilt) GVT_CUDA_TRY(cudaMemsetAsync(Sk, 0, sizeof(float) * slab_k * g.nslab, c->stream));
     for (int s = 0; s < g.nslab; s++) {
         if (!my_slab(c, s)) continue;
         const int64_t lo = g.bounds[s], w = g.bounds[s + 1] - lo;
         if (w == 0) continue;
-        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag);
+        Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag, !prebuilt);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
                         skld, g.kb_list[(size_t)s], g.kb_off[(size_t)s]);
     }
@@ -628,7 +636,8 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
             Av.p = g.A.p + lo;
             stage2_gather16(c, g.smp, Av, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k, skld, w, coef, acc, dst);
         } else {
-            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, dst);
+            gemm_nt_sampled(c, operand_col_offset(g.A.op, lo), so, g.A.n, g.q_out, w, g.smp, coef, acc, dst,
+                            df ? &df->parts : nullptr);
         }
         first = false;
     }
@@ -636,11 +645,11 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
 }
 
 static void run_group(gvt_ctx *c, const Problem &P, GroupPlan &g, const float *p_full, float coef, int accumulate,
-                      float *out, bool values_ready = false) {
+                      float *out, bool values_ready = false, DenseFuse *df = nullptr) {
     c->last_engine = g.engine;
     c->last_exchange = !distributed(c) ? 0 : (P.uex ? 2 : 1);
     if (g.engine == 2 && fused_f16(c, g.C.cols)) {
-        run_group_f16(c, P, g, p_full, coef, accumulate, out);
+        run_group_f16(c, P, g, p_full, coef, accumulate, out, df);
         return;
     }
     // ---- stage 1 on this rank's X-row slab(s)
@@ -725,6 +734,14 @@ struct CgTail {
 static bool cg_tail_enabled() {  // A/B knob: GVT_CG_TAIL=0 keeps the separate CG vector kernels
     static const bool on = [] {
         const char *e = getenv("GVT_CG_TAIL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+static bool dense_tail_enabled() {  // A/B knob: GVT_DENSE_TAIL=0 keeps the separate kernels on the dense engine
+    static const bool on = [] {
+        const char *e = getenv("GVT_DENSE_TAIL");
         return !(e && atoi(e) == 0);
     }();
     return on;
@@ -1405,8 +1422,37 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     const bool fuse_tail = !minres && !cgg && !es && !distributed(c) && !P.uex && P.n_out == n &&
                            (mp.form == FORM_RANKING || mp.form == FORM_LINEAR || mp.form == FORM_POLY2D) &&
                            cg_tail_enabled();
+    // the fused dense-engine CG tail (tail.cu): one persistent launch between the stage-2 GEMM and the next
+    // stage-1 GEMM instead of the split-K combine, three CG vector kernels, the S-scale memset and the
+    // X(p) build; same arithmetic on the same partitions (bit-identical iterates).  Single GPU, one
+    // Kronecker group on the fused fp16 path with warp-per-row X rows.
+    GroupPlan *gd = mp.groups.empty() ? nullptr : &mp.groups[0];
+    bool fuse_dense = !fuse_tail && !minres && !cgg && !es && !distributed(c) && !P.uex && P.n_out == n &&
+                            (mp.form == FORM_KRON || mp.form == FORM_SYM || mp.form == FORM_ANTI) && gd &&
+                            gd->engine == 2 && fused_f16(c, gd->C.cols) && gd->nslab == 1 && !gd->diag &&
+                            round_up(gd->C.cols > 0 ? gd->C.cols : 1, 32) <= 2048 &&
+                            dense_tail_fits(round_up(gd->C.cols > 0 ? gd->C.cols : 1, 32)) && dense_tail_enabled();
+    double *tail_part2 = nullptr;
+    const int32_t *tail_inv = nullptr;
+    float *p_alt = nullptr;
+    bool tail_first = true;
+    if (fuse_dense) {
+        tail_part2 = wsT<double>(c, "tail.part2", RED_BLOCKS);
+        tail_inv = dense_tail_init(c, tail_part2, gd->smp.dst, gd->smp.ns, n);
+        if (!tail_inv) fuse_dense = false;  // (some output is not exactly one sample: the separate kernels)
+        p_alt = wsT<float>(c, "tail.p_alt", (size_t)n);
+    }
     auto iteration = [&]() {
-        if (minres) {
+        if (fuse_dense) {
+            DenseFuse df;
+            df.prebuilt = !tail_first;  // iteration 1 builds X(p_0) and zeroes the S scales itself
+            tail_first = false;
+            run_group(c, P, *gd, p, gd->coef, 0, u, false, &df);
+            const int64_t lo = gd->bounds[0], w = gd->bounds[1] - lo;
+            const Operand xo = build_x16(c, "dense.X16", gd->ent, lo, w, gd->C.cols, p, nullptr, false);
+            dense_cg_tail(c, df.parts.part, df.parts.split, df.parts.ns, tail_inv, df.parts.coef, u, x, r, p, p_alt,
+                          n, cg_vec_blocks(n), lambda, state, cg_parts(c), tail_part2, gd->ent, lo, w, xo);
+        } else if (minres) {
             run_matvec(c, P, mp, v, u);
             minres_step(c, u, v, r1, r2, W1, W2, x, n, lambda, state);
             minres_update(c, v, W1, W2, x, r2, n, state, u + n, KW1, KW2, s_val, n_val);
@@ -1434,6 +1480,7 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     };
     drive(c, max_iter, rel_tol > 0.0 || es != nullptr, state, iteration);
     if (cgg) cgg_finish(c, r, n, state);
+    if (fuse_dense) dense_tail_finish(c, p, p_alt, n, state);  // the last direction back into p
     if (fuse_tail && cg_tail_lazy() && mp.form != FORM_POLY2D) cg_direction(c, p, r, n, state);  // p_{k+1} (kept)
     // scalars back (one sync per fit)
     double hstate[MINRES_STATE_N];

@@ -175,8 +175,9 @@ void gemm_nt_store(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, in
 bool fused_f16(gvt_ctx *c, int64_t q_in);
 // rows [row_lo, row_lo + rows) of the pair matrix built straight into an fp16 operand
 // (values sign * p[src] summed per cell in entry order, one row scale per row)
+// (launch = false: only the operand's buffers, for a build done elsewhere -- the fused CG tail)
 Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_lo, int64_t rows, int64_t cols,
-                  const float *p, const float *diag = nullptr);
+                  const float *p, const float *diag = nullptr, bool launch = true);
 // X[r][row_lo + r] += diag[row_lo + r] for r < rows (fp32 X, leading dimension ldX)
 void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_lo, int64_t rows);
 // C = A * B^T written as fp16 pieces (M rows x ldc) with one scale per (S16_SCALE_ROWS-row block,
@@ -191,8 +192,17 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
 void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,
                   bool diag, std::vector<int32_t> &list, std::vector<int32_t> &off);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
+// defer (accumulate = 0 only): a split-K GEMM leaves its parts for the caller's own combine
+// (defer->part = nullptr when the GEMM wrote out itself)
+struct SplitParts {
+    const float *part = nullptr;
+    int split = 1;
+    int64_t ns = 0;
+    const int32_t *dst = nullptr;
+    float coef = 1.f;
+};
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
-                     const SamplePlan &sp, float coef, int accumulate, float *out);
+                     const SamplePlan &sp, float coef, int accumulate, float *out, SplitParts *defer = nullptr);
 void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol);
 
 // ---- Gram (gram.cu)
@@ -220,6 +230,16 @@ void cg_update_xr(gvt_ctx *c, float *x, float *r, const float *p, const float *A
 void cg_direction(gvt_ctx *c, float *p, const float *r, int64_t n, const double *state);
 void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_t n, double *state, int iter,
                double *relres_dev);
+// fused dense-engine CG tail (tail.cu, single GPU): split-K combine, Ap / alpha, x / r / beta,
+// p = r + beta p and the next X(p) rows (warp per row, ld <= dense_tail_fits) in one persistent launch
+bool dense_tail_fits(int64_t ld);
+void dense_tail_finish(gvt_ctx *c, float *p, const float *p_alt, int64_t n, const double *state);
+const int32_t *dense_tail_init(gvt_ctx *c, double *part2, const int32_t *dst, int64_t ns, int64_t n);
+void dense_cg_tail(gvt_ctx *c, const float *part, int split, int64_t ns, const int32_t *inv, float coef, float *u,
+                   float *x, float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
+                   double *part1, double *part2, const EntryPlan &e, int64_t row_lo, int64_t rows, const Operand &xo);
+int cg_vec_blocks(int64_t n);
+double *cg_parts(gvt_ctx *c);
 // Chronopoulos-Gear single-reduction CG (GVT_OPT_CG_VARIANT = 1): init, then per iteration the
 // matvec w = K r followed by cgg_step; cgg_finish records ||r_K|| after the loop
 void cgg_init(gvt_ctx *c, const float *y, int64_t n, float *x, float *r, float *p, float *sv, double *state,

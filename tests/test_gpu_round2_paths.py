@@ -4,6 +4,8 @@ library's environment knobs take effect:
   GVT_CG_TAIL=0      separate combine + k_cg_ap instead of the fused CG tail (Linear / Ranking / Poly2D)
   GVT_SPLITK=0       one CTA pair per sampled tile instead of split-K (small problems)
   GVT_BUILD_WARP=0   CTA-per-row X build instead of warp-per-row (rows <= 2048)
+  GVT_DENSE_TAIL=0   separate split-K combine, CG vector kernels, S-scale memset and X build instead of the
+                     fused dense-engine CG tail (one persistent launch, tail.cu)
 The fast path changes only summation order, so results agree to fp32 rounding; the oracle checks of the
 default path are in test_gpu_parity.py (C3/C4 sampled parity, the in-loop and S30 tests)."""
 import json
@@ -37,9 +39,13 @@ with G.Context(0) as ctx:
     terms = G.gvt_kernel_terms(kernel)
     f, s = d(w.train_first), d(w.train_second)
     if mode == "fit":
-        a, it, hist, code = ctx.fit(D, T, f, s, d(w.y), terms, w.lam, iters, want_history=True)
+        tol = float(os.environ.get("GVT_TEST_TOL", "0"))
+        a, it, hist, code = ctx.fit(D, T, f, s, d(w.y), terms, w.lam, iters, rel_tol=tol, want_history=True)
         res = a.cpu().numpy()
-        extra = {"iters": it, "relres": float(hist[-1]), "code": code}
+        if os.environ.get("GVT_TEST_DIR"):  # the solver's last search direction after the fit, appended
+            res = np.concatenate([res, ctx.solver_direction(w.n)])
+        extra = {"iters": it, "relres": float(hist[it]), "code": code,
+                 "hist": [float(h) for h in hist[:it + 1]]}
     else:
         v = d(synth.random_vector(3, w.n))
         res = ctx.matvec(D, T, f, s, f, s, v, terms).cpu().numpy()
@@ -47,7 +53,8 @@ with G.Context(0) as ctx:
     torch.cuda.synchronize()
     st = ctx.stats()
 np.save(out, res)
-print(json.dumps({**extra, "kinds": sorted(k for k, v in st["kinds"].items() if v["count"] > 0)}))
+print(json.dumps({**extra, "engine": st["last_engine"],
+                  "kinds": sorted(k for k, v in st["kinds"].items() if v["count"] > 0)}))
 """
 
 
@@ -104,3 +111,26 @@ def test_warp_row_build_bit_identical_c3(tmp_path):
     fast, _ = run("C3", "symmetric", "fit", 10, {}, tmp_path, "fast")
     slow, _ = run("C3", "symmetric", "fit", 10, {"GVT_BUILD_WARP": "0"}, tmp_path, "slow")
     assert np.array_equal(fast, slow)
+
+
+@pytest.mark.parametrize("kname,iters", [("symmetric", 12), ("antisymmetric", 13), ("kronecker", 13)])
+def test_dense_cg_tail_bit_identical_c3(tmp_path, kname, iters):
+    """C3 dense-engine CG fits (12 and 13 iterations: both direction buffers): the fused tail (split-K combine,
+    Ap / alpha, x / r / beta, p and the next X(p) in one persistent launch) runs the separate kernels' arithmetic
+    on the same partitions, so the weights, the last search direction and the residual history are bit-identical."""
+    env = {"GVT_TEST_DIR": "1"}  # (weights and the last search direction, which the tail keeps in two buffers)
+    fast, ef = run("C3", kname, "fit", iters, env, tmp_path, "fast")
+    slow, es = run("C3", kname, "fit", iters, {**env, "GVT_DENSE_TAIL": "0"}, tmp_path, "slow")
+    assert ef["iters"] == es["iters"] == iters and ef["code"] == es["code"] == 0 and ef["engine"] == 2
+    assert np.array_equal(fast, slow)
+    assert ef["hist"] == es["hist"]
+
+
+def test_dense_cg_tail_residual_stop_c3(tmp_path):
+    """Residual-mode stop inside the fused tail (the stopping test on the fused beta step, then the halted state
+    skips the remaining replays): the same stopping iteration, weights and history as the separate kernels."""
+    env = {"GVT_TEST_TOL": "0.9", "GVT_TEST_DIR": "1"}
+    fast, ef = run("C3", "kronecker", "fit", 40, env, tmp_path, "fast")
+    slow, es = run("C3", "kronecker", "fit", 40, {**env, "GVT_DENSE_TAIL": "0"}, tmp_path, "slow")
+    assert 0 < ef["iters"] == es["iters"] < 40
+    assert ef["relres"] <= 0.9 and np.array_equal(fast, slow) and ef["hist"] == es["hist"]

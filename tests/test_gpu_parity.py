@@ -501,7 +501,9 @@ def test_launch_accounting(ctx):
     ctx.set_option(G.OPT_PROFILE, 0)
     ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
     assert st["launches"] > 0
-    assert "cg_vector" in st["kinds"] and st["kinds"]["cg_vector"]["count"] >= 5 * 3
+    # one fused CG-tail launch per iteration on the dense engine (tail.cu; three vector kernels without it)
+    assert "cg_vector" in st["kinds"] and st["kinds"]["cg_vector"]["count"] >= 5
+    assert st["kinds"]["stage1_tc"]["count"] >= 5 and st["kinds"]["stage2_tc"]["count"] >= 5
     assert all(v["ms"] >= 0 for v in st["kinds"].values())
 
 

@@ -1877,9 +1877,15 @@ static int sampled_split(gvt_ctx *c, const SamplePlan &sp, int64_t K) {
     return split >= 2 ? split : 1;
 }
 
+int sampled_split_parts(gvt_ctx *c, const SamplePlan &sp, int64_t K) { return sp.ns > 0 ? sampled_split(c, sp, K) : 1; }
+
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out, SplitParts *defer) {
-    if (defer) *defer = SplitParts();
+    const int slot = defer ? defer->slot : 0;
+    if (defer) {
+        *defer = SplitParts();
+        defer->slot = slot;
+    }
     if (sp.ns == 0) return;
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -1898,7 +1904,7 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
         ep.split = split;
         ep.n_units = sp.n_pairs * split;
         ep.ns = sp.ns;
-        ep.part = wsT<float>(c, "splitk.part", (size_t)split * sp.ns);
+        ep.part = wsT<float>(c, slot ? "splitk.part1" : "splitk.part", (size_t)split * sp.ns);
     } else if (sp.pair_list && sp.n_pairs > 0 && sp.n_pairs < npt && compact_tiles()) {
         // some pair tiles are empty: the persistent loop runs over the non-empty ones only, so every CTA pair
         // gets the same number of tiles (striding over all tiles left pairs with several non-empty tiles
@@ -1908,12 +1914,13 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
         ep.n_units = sp.n_pairs;
     }
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
-    if (split > 1 && defer && !accumulate) {
+    if (split > 1 && defer) {
         defer->part = ep.part;
         defer->split = split;
         defer->ns = sp.ns;
         defer->dst = sp.dst;
         defer->coef = coef;
+        defer->accumulate = accumulate;
     } else if (split > 1)
         GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine, grid1d(sp.ns, 256, 8 * c->sm_count), 256, 0, ep.part, split, sp.ns,
                    sp.dst, coef, accumulate, out);

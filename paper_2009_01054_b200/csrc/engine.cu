@@ -221,6 +221,8 @@ struct MatvecPlan {
     Form form = FORM_GENERIC;
     std::vector<GroupPlan> groups;  // generic: one per term; else at most one
     EntryPlan byF, byS;            // segment plans (cheap terms / Cartesian)
+    bool cart_dense = false;       // Cartesian as two sampled tensor-core GEMMs (D X + X T), below
+    SamplePlan cart_smp;
     float *buf = nullptr;          // MLPK sample buffer (n_out + m)
     float *g1 = nullptr, *g2 = nullptr, *b1 = nullptr, *b2 = nullptr;
     std::vector<Factor> owned;     // materialised Ones/Identity factors
@@ -411,6 +413,34 @@ static void set_estimates(gvt_ctx *c, const Problem &P, GroupPlan &g) {
     g.extra_est = P.uex ? (double)P.n_out_extra_all : (double)P.n_out_extra_all / w;
 }
 
+// Cartesian kernel (Corollary D(x)I + I(x)T): u_i = (D X)[d_i, t_i] + (X T)[d_i, t_i] with
+// X = the m x q pair matrix of p.  Gather form (k_cartesian): one warp per output walks the output's two
+// entry segments, ~1 random 32-byte sector per entry (calibrated: C3, 4e7 entries, ~90 us).  Dense form:
+// two sampled 3xFP16 GEMMs, A = D / B = X^T (K = m) and A = X / B = T (K = q), over the non-empty CTA-pair
+// tiles `units` of the output grid (split-K when at most a quarter of the pairs have one), plus the two
+// fp16 pair-matrix builds.  Estimates in us.
+static double cart_gather_us(const Problem &P) {
+    const double per_out = (double)P.n_in / std::max<int64_t>(P.q, 1) + (double)P.n_in / std::max<int64_t>(P.m, 1);
+    return 5.0 + (double)P.n_out_all * per_out / 0.45e6;
+}
+static double cart_dense_us(gvt_ctx *c, const Problem &P, double units) {
+    const double pairs = c->sm_count / 2.0;
+    auto gemm = [&](int64_t K) {
+        const double tile_us = 3.0 * 65536.0 * (double)round_up(K > 0 ? K : 1, 256) / 1.47e7;  // one pair tile
+        const double load = units <= pairs / 2.0 ? 0.5 : std::ceil(units / pairs);
+        return 10.0 + tile_us * load;
+    };
+    const double build = 2.0 * (3.0 + (double)P.m * (double)P.q * 8.0 / 3e6);
+    return gemm(P.m) + gemm(P.q) + build;
+}
+static bool cart_dense_possible(gvt_ctx *c, const Problem &P) {
+    if (!tc_available(c) || c->engine == 1 || distributed(c) || P.rect || P.n_out == 0 || P.n_in == 0) return false;
+    if (!fused_f16(c, P.m) || !fused_f16(c, P.q)) return false;
+    if (c->engine == 2) return true;
+    // lower bound: the fewest non-empty tiles that can hold the out sample
+    return cart_dense_us(c, P, std::ceil((double)P.n_out_all / 65536.0)) < cart_gather_us(P);
+}
+
 static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int n_terms, Form form,
                         MatvecPlan &mp) {
     mp.form = form;
@@ -490,6 +520,12 @@ static void plan_matvec(gvt_ctx *c, const Problem &P, const gvt_term *terms, int
     case FORM_CARTESIAN:
         build_entry_plan(c, "byF", P.inf, P.ins, P.n_in, kinds1(F, Sx, 1.f), P.m, P.q, mp.byF);
         build_entry_plan(c, "byS", P.inf, P.ins, P.n_in, kinds1(Sx, F, 1.f), P.q, P.m, mp.byS);
+        if (P.D.split && P.T.split) {  // the dense form may pay: decide on the exact non-empty tile count
+            build_sample_plan(c, "cart.s", P.of, P.os, P.n_out, F, Sx, 0, P.m, mp.cart_smp);
+            bucket_samples(c, "cart", mp.cart_smp, P.m, P.q);
+            const double units = mp.cart_smp.n_pairs >= 0 ? (double)mp.cart_smp.n_pairs : 1e30;
+            mp.cart_dense = c->engine == 2 || cart_dense_us(c, P, units) < cart_gather_us(P);
+        }
         break;
     case FORM_GENERIC:
         for (int i = 0; i < n_terms; i++) {
@@ -810,6 +846,15 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
             combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
         break;
     case FORM_CARTESIAN:
+        if (mp.cart_dense) {  // u = (D X + X T) sampled: two 3xFP16 GEMMs, the second accumulating
+            c->last_engine = 2;
+            const Operand xt = build_x16(c, "cart.XT16", mp.byS, 0, P.q, P.m, p);  // rows t of X^T
+            gemm_nt_sampled(c, P.D.op, xt, P.m, P.q, P.m, mp.cart_smp, 1.f, 0, u);
+            const Operand xo = build_x16(c, "cart.X16", mp.byF, 0, P.m, P.q, p);   // rows d of X
+            gemm_nt_sampled(c, xo, P.T.op, P.m, P.q, P.q, mp.cart_smp, 1.f, 1, u);
+            break;
+        }
+        c->last_engine = 1;
         entry_values(c, mp.byF, p);
         entry_values(c, mp.byS, p);
         cartesian(c, P.of, P.os, P.n_out, mp.byF, mp.byS, P.D, P.T, u);
@@ -908,8 +953,9 @@ static void out_finish(gvt_ctx *c, OutArr &o) {
 
 // does this plan need the tensor-core split of the factors (any dense group)?
 static bool needs_split(gvt_ctx *c, Form form, const Problem &P) {
+    if (form == FORM_CARTESIAN) return cart_dense_possible(c, P);
     if (!tc_available(c) || c->engine == 1) return false;
-    if (form == FORM_LINEAR || form == FORM_RANKING || form == FORM_CARTESIAN) return false;
+    if (form == FORM_LINEAR || form == FORM_RANKING) return false;
     if (c->engine == 2) return true;
     const bool hom = !(form == FORM_KRON || form == FORM_POLY2D || form == FORM_GENERIC);
     const double mult = (form == FORM_SYM || form == FORM_ANTI || form == FORM_MLPK) ? 2.0 : 1.0;  // entries per pair
@@ -1427,31 +1473,64 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     // X(p) build; same arithmetic on the same partitions (bit-identical iterates).  Single GPU, one
     // Kronecker group on the fused fp16 path with warp-per-row X rows.
     GroupPlan *gd = mp.groups.empty() ? nullptr : &mp.groups[0];
-    bool fuse_dense = !fuse_tail && !minres && !cgg && !es && !distributed(c) && !P.uex && P.n_out == n &&
-                            (mp.form == FORM_KRON || mp.form == FORM_SYM || mp.form == FORM_ANTI) && gd &&
-                            gd->engine == 2 && fused_f16(c, gd->C.cols) && gd->nslab == 1 && !gd->diag &&
-                            round_up(gd->C.cols > 0 ? gd->C.cols : 1, 32) <= 2048 &&
-                            dense_tail_fits(round_up(gd->C.cols > 0 ? gd->C.cols : 1, 32)) && dense_tail_enabled();
+    const bool tail_common = !fuse_tail && !minres && !cgg && !es && !distributed(c) && !P.uex && P.n_out == n &&
+                             dense_tail_enabled();
+    auto short_rows = [&](int64_t cols) {
+        const int64_t ld = round_up(cols > 0 ? cols : 1, 32);
+        return ld <= 2048 && dense_tail_fits(ld);
+    };
+    const bool fuse_kron = tail_common && (mp.form == FORM_KRON || mp.form == FORM_SYM || mp.form == FORM_ANTI) && gd &&
+                           gd->engine == 2 && fused_f16(c, gd->C.cols) && gd->nslab == 1 && !gd->diag &&
+                           short_rows(gd->C.cols);
+    // the Cartesian form's two sampled GEMMs (D X^T-side and X T-side) with both pair-matrix operands rebuilt
+    const bool fuse_cart = tail_common && mp.form == FORM_CARTESIAN && mp.cart_dense && short_rows(P.m) &&
+                           short_rows(P.q);
+    bool fuse_dense = fuse_kron || fuse_cart;
     double *tail_part2 = nullptr;
     const int32_t *tail_inv = nullptr;
     float *p_alt = nullptr;
     bool tail_first = true;
     if (fuse_dense) {
+        const SamplePlan &sp = fuse_cart ? mp.cart_smp : gd->smp;
         tail_part2 = wsT<double>(c, "tail.part2", RED_BLOCKS);
-        tail_inv = dense_tail_init(c, tail_part2, gd->smp.dst, gd->smp.ns, n);
+        tail_inv = dense_tail_init(c, tail_part2, sp.dst, sp.ns, n);
         if (!tail_inv) fuse_dense = false;  // (some output is not exactly one sample: the separate kernels)
         p_alt = wsT<float>(c, "tail.p_alt", (size_t)n);
     }
     auto iteration = [&]() {
-        if (fuse_dense) {
+        if (fuse_dense && !fuse_cart) {
             DenseFuse df;
             df.prebuilt = !tail_first;  // iteration 1 builds X(p_0) and zeroes the S scales itself
             tail_first = false;
             run_group(c, P, *gd, p, gd->coef, 0, u, false, &df);
-            const int64_t lo = gd->bounds[0], w = gd->bounds[1] - lo;
-            const Operand xo = build_x16(c, "dense.X16", gd->ent, lo, w, gd->C.cols, p, nullptr, false);
-            dense_cg_tail(c, df.parts.part, df.parts.split, df.parts.ns, tail_inv, df.parts.coef, u, x, r, p, p_alt,
-                          n, cg_vec_blocks(n), lambda, state, cg_parts(c), tail_part2, gd->ent, lo, w, xo);
+            TailX tx;
+            tx.e = &gd->ent;
+            tx.row_lo = gd->bounds[0];
+            tx.rows = gd->bounds[1] - tx.row_lo;
+            tx.op = build_x16(c, "dense.X16", gd->ent, tx.row_lo, tx.rows, gd->C.cols, p, nullptr, false);
+            dense_cg_tail(c, df.parts, SplitParts(), tail_inv, u, x, r, p, p_alt, n, cg_vec_blocks(n), lambda, state,
+                          cg_parts(c), tail_part2, &tx, 1);
+        } else if (fuse_dense) {  // Cartesian: u = (D X + X T) sampled, then the tail rebuilds X^T and X
+            const bool build = tail_first;
+            tail_first = false;
+            c->last_engine = 2;
+            TailX tx[2];
+            tx[0].e = &mp.byS;  // rows t of X^T (B operand of D X)
+            tx[0].rows = P.q;
+            tx[0].op = build_x16(c, "cart.XT16", mp.byS, 0, P.q, P.m, p, nullptr, build);
+            tx[1].e = &mp.byF;  // rows d of X (A operand of X T)
+            tx[1].rows = P.m;
+            tx[1].op = build_x16(c, "cart.X16", mp.byF, 0, P.m, P.q, p, nullptr, build);
+            // defer the first GEMM's parts only when the second also leaves parts (the second accumulates onto
+            // the first's combined values)
+            SplitParts pa, pb;
+            pa.slot = 0;
+            pb.slot = 1;
+            const bool defer_a = sampled_split_parts(c, mp.cart_smp, P.q) > 1;
+            gemm_nt_sampled(c, P.D.op, tx[0].op, P.m, P.q, P.m, mp.cart_smp, 1.f, 0, u, defer_a ? &pa : nullptr);
+            gemm_nt_sampled(c, tx[1].op, P.T.op, P.m, P.q, P.q, mp.cart_smp, 1.f, 1, u, &pb);
+            dense_cg_tail(c, pa, pb, tail_inv, u, x, r, p, p_alt, n, cg_vec_blocks(n), lambda, state, cg_parts(c),
+                          tail_part2, tx, 2);
         } else if (minres) {
             run_matvec(c, P, mp, v, u);
             minres_step(c, u, v, r1, r2, W1, W2, x, n, lambda, state);

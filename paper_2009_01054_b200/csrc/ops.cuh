@@ -192,15 +192,19 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
 void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,
                   bool diag, std::vector<int32_t> &list, std::vector<int32_t> &off);
 // sampled: out[dst] (+)= coef * (A * B^T)[r, c] for the bucketed samples
-// defer (accumulate = 0 only): a split-K GEMM leaves its parts for the caller's own combine
-// (defer->part = nullptr when the GEMM wrote out itself)
+// defer: a split-K GEMM leaves its parts for the caller's own combine (defer->part = nullptr when the
+// GEMM wrote out itself)
 struct SplitParts {
+    int slot = 0;  // (in) which parts buffer: two deferred GEMMs of one matvec use different slots
     const float *part = nullptr;
     int split = 1;
     int64_t ns = 0;
     const int32_t *dst = nullptr;
     float coef = 1.f;
+    int accumulate = 0;  // the deferred combine adds coef * (sum of parts) to out instead of storing it
 };
+// the K-split the sampled GEMM will use for this plan and K (1: no parts)
+int sampled_split_parts(gvt_ctx *c, const SamplePlan &sp, int64_t K);
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,
                      const SamplePlan &sp, float coef, int accumulate, float *out, SplitParts *defer = nullptr);
 void bucket_samples(gvt_ctx *c, const char *tag, SamplePlan &sp, int64_t nrow, int64_t ncol);
@@ -235,9 +239,16 @@ void cg_update(gvt_ctx *c, float *x, float *r, float *p, const float *Ap, int64_
 bool dense_tail_fits(int64_t ld);
 void dense_tail_finish(gvt_ctx *c, float *p, const float *p_alt, int64_t n, const double *state);
 const int32_t *dense_tail_init(gvt_ctx *c, double *part2, const int32_t *dst, int64_t ns, int64_t n);
-void dense_cg_tail(gvt_ctx *c, const float *part, int split, int64_t ns, const int32_t *inv, float coef, float *u,
-                   float *x, float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
-                   double *part1, double *part2, const EntryPlan &e, int64_t row_lo, int64_t rows, const Operand &xo);
+// up to two deferred part sets (the first stored, the second accumulated, each as the GEMM's own combine
+// would) and up to two pair-matrix operands to rebuild (the Cartesian form's X and X^T)
+struct TailX {
+    const EntryPlan *e = nullptr;
+    int64_t row_lo = 0, rows = 0;
+    Operand op;
+};
+void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const int32_t *inv, float *u, float *x,
+                   float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
+                   double *part1, double *part2, const TailX *xs, int nx);
 int cg_vec_blocks(int64_t n);
 double *cg_parts(gvt_ctx *c);
 // Chronopoulos-Gear single-reduction CG (GVT_OPT_CG_VARIANT = 1): init, then per iteration the

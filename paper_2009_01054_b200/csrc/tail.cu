@@ -32,13 +32,24 @@
 
 namespace gvt {
 
+struct TailXDev {  // one pair-matrix operand to rebuild: rows [0, rows) from entries row_ptr[row_lo + r] ..
+    const int64_t *row_ptr;
+    const int32_t *col, *src;
+    const float *sign;
+    int64_t row_lo, rows, ld;
+    __half *hi, *lo;
+    float *sinv;
+};
+
 struct DenseTailArgs {
-    // split-K parts (part == nullptr: the sampled GEMM wrote u itself); inv[i] = sample slot of output i
-    const float *part;
-    int split;
+    // deferred split-K part sets (nullptr: that GEMM wrote u itself); inv[i] = sample slot of output i.
+    // Set A is stored (u = coef sum), set B accumulated (u = fmaf(coef, sum, u)), as their combines would.
+    const float *partA, *partB;
+    int splitA, splitB;
+    float coefA, coefB;
+    int accA, accB;
     int64_t ns;
     const int32_t *inv;
-    float coef;
     // CG vectors and state; the direction lives in pd[k & 1] after iteration k
     float *u, *x, *r;
     float *pd[2];
@@ -47,13 +58,9 @@ struct DenseTailArgs {
     float lambda;
     double *st, *relres;
     double *part1, *part2;  // [RED_BLOCKS] each, unused slots zero
-    // X rows [0, rows) from entries row_ptr[row_lo + r] ..
-    const int64_t *row_ptr;
-    const int32_t *col, *src;
-    const float *sign;
-    int64_t row_lo, rows, ld;
-    __half *hi, *lo;
-    float *sinv;
+    TailXDev xb[2];
+    int nx;
+    int64_t ldmax;
     unsigned *bar;
     unsigned long long *prof;  // GVT_TAIL_PROF: [0..7] CTA 0's phase stamps, [8 + b] CTA b's exit
 };
@@ -84,12 +91,19 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_dense_cg_tail(DenseTailArgs a)
     for (int64_t vb = blockIdx.x; vb < a.nvb; vb += gridDim.x) {
         int64_t lo, hi;
         vblock_range(a.n, a.nvb, vb, lo, hi);
-        if (a.part) {
+        if (a.partA || a.partB) {
             for (int64_t i = lo + tid; i < hi; i += TAIL_THREADS) {
                 const int64_t k = a.inv[i];
-                float v = a.part[k];
-                for (int h = 1; h < a.split; h++) v += a.part[(int64_t)h * a.ns + k];
-                a.u[i] = a.coef * v;
+                if (a.partA) {
+                    float v = a.partA[k];
+                    for (int h = 1; h < a.splitA; h++) v += a.partA[(int64_t)h * a.ns + k];
+                    a.u[i] = a.accA ? fmaf(a.coefA, v, __ldcg(a.u + i)) : a.coefA * v;
+                }
+                if (a.partB) {
+                    float v = a.partB[k];
+                    for (int h = 1; h < a.splitB; h++) v += a.partB[(int64_t)h * a.ns + k];
+                    a.u[i] = a.accB ? fmaf(a.coefB, v, __ldcg(a.u + i)) : a.coefB * v;
+                }
             }
             __syncthreads();
         }
@@ -153,11 +167,14 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_dense_cg_tail(DenseTailArgs a)
         for (int64_t i = gtid; i < a.n; i += gthreads) pn[i] = fmaf(fb, __ldcg(p + i), __ldcg(a.r + i));
     }
     const int warp = tid >> 5, lane = tid & 31;
-    float *rowbuf = rowbufs + (size_t)warp * a.ld;
+    float *rowbuf = rowbufs + (size_t)warp * a.ldmax;
     const int64_t nw = (int64_t)gridDim.x * (TAIL_THREADS / 32);
-    for (int64_t row = (int64_t)blockIdx.x * (TAIL_THREADS / 32) + warp; row < a.rows; row += nw)
-        x16_row_warp<true>(row, lane, rowbuf, a.row_ptr, a.col, a.src, a.sign, p, a.row_lo, a.ld, a.hi, a.lo,
-                           a.sinv, nullptr, a.r, fb);
+    const int64_t rows0 = a.xb[0].rows, rows_all = rows0 + (a.nx > 1 ? a.xb[1].rows : 0);
+    for (int64_t row = (int64_t)blockIdx.x * (TAIL_THREADS / 32) + warp; row < rows_all; row += nw) {
+        const TailXDev &xb = a.xb[row < rows0 ? 0 : 1];
+        x16_row_warp<true>(row < rows0 ? row : row - rows0, lane, rowbuf, xb.row_ptr, xb.col, xb.src, xb.sign, p,
+                           xb.row_lo, xb.ld, xb.hi, xb.lo, xb.sinv, nullptr, a.r, fb);
+    }
     if (a.prof) {
         __syncthreads();
         if (tid == 0) a.prof[8 + blockIdx.x] = tail_timer();
@@ -168,13 +185,35 @@ static size_t tail_smem(int64_t ld) { return sizeof(float) * (size_t)(TAIL_THREA
 
 bool dense_tail_fits(int64_t ld) { return ld > 0 && tail_smem(ld) <= 96 * 1024; }
 
-void dense_cg_tail(gvt_ctx *c, const float *part, int split, int64_t ns, const int32_t *inv, float coef, float *u,
-                   float *x, float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
-                   double *part1, double *part2, const EntryPlan &e, int64_t row_lo, int64_t rows, const Operand &xo) {
+void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const int32_t *inv, float *u, float *x,
+                   float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
+                   double *part1, double *part2, const TailX *xs, int nx) {
     static int grid_dev[GVT_MAX_DEVICES] = {};
     int &grid = grid_dev[c->device < GVT_MAX_DEVICES ? c->device : 0];
-    const size_t smem = tail_smem(xo.ld);
-    GVT_REQUIRE(dense_tail_fits(xo.ld), GVT_E_STATE, "fused CG tail: X rows too long");
+    GVT_REQUIRE(nx >= 1 && nx <= 2, GVT_E_STATE, "fused CG tail: one or two pair-matrix operands");
+    GVT_REQUIRE(!(pa.part || pb.part) || inv, GVT_E_STATE, "fused CG tail: split-K parts without the output -> slot map");
+    DenseTailArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ldmax = 0;
+    for (int i = 0; i < nx; i++) {
+        const EntryPlan &e = *xs[i].e;
+        TailXDev &d = a.xb[i];
+        d.row_ptr = e.row_ptr;
+        d.col = e.col;
+        d.src = e.src;
+        d.sign = e.sign;
+        d.row_lo = xs[i].row_lo;
+        d.rows = xs[i].rows;
+        d.ld = xs[i].op.ld;
+        // (the operand's buffers are the workspace build_x16 writes: the tail writes them the same way)
+        d.hi = const_cast<__half *>(static_cast<const __half *>(xs[i].op.hi));
+        d.lo = const_cast<__half *>(static_cast<const __half *>(xs[i].op.lo));
+        d.sinv = const_cast<float *>(xs[i].op.scale);
+        a.ldmax = std::max(a.ldmax, d.ld);
+    }
+    a.nx = nx;
+    const size_t smem = tail_smem(a.ldmax);
+    GVT_REQUIRE(dense_tail_fits(a.ldmax), GVT_E_STATE, "fused CG tail: X rows too long");
     if (!grid) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_dense_cg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         int per_sm = 0;
@@ -182,13 +221,16 @@ void dense_cg_tail(gvt_ctx *c, const float *part, int split, int64_t ns, const i
         GVT_REQUIRE(per_sm >= 1, GVT_E_STATE, "fused CG tail: no resident CTA");
         grid = c->sm_count * std::min(per_sm, 2);
     }
-    DenseTailArgs a;
-    a.part = part;
-    a.split = split;
-    a.ns = ns;
+    a.partA = pa.part;
+    a.splitA = pa.split;
+    a.coefA = pa.coef;
+    a.accA = pa.accumulate;
+    a.partB = pb.part;
+    a.splitB = pb.split;
+    a.coefB = pb.coef;
+    a.accB = pb.accumulate;
+    a.ns = pa.part ? pa.ns : pb.ns;
     a.inv = inv;
-    GVT_REQUIRE(!part || inv, GVT_E_STATE, "fused CG tail: split-K parts without the output -> slot map");
-    a.coef = coef;
     a.u = u;
     a.x = x;
     a.r = r;
@@ -201,17 +243,6 @@ void dense_cg_tail(gvt_ctx *c, const float *part, int split, int64_t ns, const i
     a.relres = state + ST_N;
     a.part1 = part1;
     a.part2 = part2;
-    a.row_ptr = e.row_ptr;
-    a.col = e.col;
-    a.src = e.src;
-    a.sign = e.sign;
-    a.row_lo = row_lo;
-    a.rows = rows;
-    a.ld = xo.ld;
-    // (the operand's buffers are the workspace build_x16 writes: the tail writes them the same way)
-    a.hi = const_cast<__half *>(static_cast<const __half *>(xo.hi));
-    a.lo = const_cast<__half *>(static_cast<const __half *>(xo.lo));
-    a.sinv = const_cast<float *>(xo.scale);
     a.bar = wsT<unsigned>(c, "tail.bar", BAR_WORDS);
     static const bool prof = getenv("GVT_TAIL_PROF") != nullptr;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

@@ -4,6 +4,7 @@ library's environment knobs take effect:
   GVT_CG_TAIL=0      separate combine + k_cg_ap instead of the fused CG tail (Linear / Ranking / Poly2D)
   GVT_SPLITK=0       one CTA pair per sampled tile instead of split-K (small problems)
   GVT_BUILD_WARP=0   CTA-per-row X build instead of warp-per-row (rows <= 2048)
+  OPT_ENGINE=1       (option) the gather form of the Cartesian kernel instead of its two sampled GEMMs
   GVT_DENSE_TAIL=0   separate split-K combine, CG vector kernels, S-scale memset and X build instead of the
                      fused dense-engine CG tail (one persistent launch, tail.cu)
 The fast path changes only summation order, so results agree to fp32 rounding; the oracle checks of the
@@ -34,6 +35,10 @@ if kernel in synth.HOMOGENEOUS_KERNELS and w.Xt is not None:
     w = synth.union_domain(w)
 d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
 with G.Context(0) as ctx:
+    for kv in os.environ.get("GVT_TEST_OPTS", "").split(","):
+        if kv:
+            k, v = kv.split("=")
+            ctx.set_option(getattr(G, k), int(v))
     D = ctx.gram(w.base, d(w.Xd), gamma=w.gamma, coef0=w.coef0, degree=w.degree)
     T = None if w.Xt is None else ctx.gram(w.base, d(w.Xt), gamma=w.gamma, coef0=w.coef0, degree=w.degree)
     terms = G.gvt_kernel_terms(kernel)
@@ -113,7 +118,7 @@ def test_warp_row_build_bit_identical_c3(tmp_path):
     assert np.array_equal(fast, slow)
 
 
-@pytest.mark.parametrize("kname,iters", [("symmetric", 12), ("antisymmetric", 13), ("kronecker", 13)])
+@pytest.mark.parametrize("kname,iters", [("symmetric", 12), ("antisymmetric", 13), ("kronecker", 13), ("cartesian", 12)])
 def test_dense_cg_tail_bit_identical_c3(tmp_path, kname, iters):
     """C3 dense-engine CG fits (12 and 13 iterations: both direction buffers): the fused tail (split-K combine,
     Ap / alpha, x / r / beta, p and the next X(p) in one persistent launch) runs the separate kernels' arithmetic
@@ -134,3 +139,16 @@ def test_dense_cg_tail_residual_stop_c3(tmp_path):
     slow, es = run("C3", "kronecker", "fit", 40, {**env, "GVT_DENSE_TAIL": "0"}, tmp_path, "slow")
     assert 0 < ef["iters"] == es["iters"] < 40
     assert ef["relres"] <= 0.9 and np.array_equal(fast, slow) and ef["hist"] == es["hist"]
+
+
+def test_cartesian_tensor_core_form_matches_gather_c3(tmp_path):
+    """C3 Cartesian: u = (D X + X T) sampled as two 3xFP16 sampled GEMMs (the auto choice at this size) against
+    the warp-per-output gather form (engine forced sparse); the oracle check of the default path is
+    test_gpu_parity.py::test_c3_homogeneous[cartesian]."""
+    fast, ef = run("C3", "cartesian", "matvec", 0, {}, tmp_path, "fast")
+    slow, es = run("C3", "cartesian", "matvec", 0, {"GVT_TEST_OPTS": "OPT_ENGINE=1"}, tmp_path, "slow")
+    assert ef["engine"] == 2 and es["engine"] == 1
+    assert rel(fast, slow) <= 1e-5
+    ff, _ = run("C3", "cartesian", "fit", 5, {}, tmp_path, "ffit")
+    sf, _ = run("C3", "cartesian", "fit", 5, {"GVT_TEST_OPTS": "OPT_ENGINE=1"}, tmp_path, "sfit")
+    assert rel(ff, sf) <= 1e-4

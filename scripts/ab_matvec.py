@@ -3,6 +3,7 @@
   python scripts/ab_matvec.py "cta=1" "cta=2" [--rounds 2]      # option sets (GVT options)
   python scripts/ab_matvec.py "lib=ab/libA.so" "lib=ab/libB.so"  # library builds
   python scripts/ab_matvec.py "gm=16" "gm=8" "gm=4"              # GEMM rasterization group (GVT_GROUP_M)
+  python scripts/ab_matvec.py "E_GVT_BUILD_CHUNKS=0" "E_GVT_BUILD_CHUNKS=1"  # any library environment knob
 
 Each round runs one subprocess per configuration that times a 10-iteration fit at C5
 (CUDA events) after warm-up, reporting ms and per-kernel ms/launch with the SM clock
@@ -58,6 +59,9 @@ def main():
                 env["GVT_GROUP_M"] = kv["gm"]
             if "rs" in kv:  # fp16 S with per-row bound scales (1) or per-(row, 256-col tile) scales (0)
                 env["GVT_S16_ROWSCALE"] = kv["rs"]
+            for k, v in kv.items():  # E_NAME=V: any environment knob of the library (e.g. E_GVT_BUILD_CHUNKS=0)
+                if k.startswith("E_"):
+                    env[k[2:]] = v
             if "l2" in kv:  # TMA L2 promotion of the GEMM operand maps (0 none, 1 64B, 2 128B, 3 256B)
                 env["GVT_L2PROMO"] = kv["l2"]
             out = subprocess.run([sys.executable, "-c", CHILD, spec], env=env, capture_output=True, text=True)

@@ -218,8 +218,10 @@ struct EpiParams {
     // sampled split-K (CTA-pair kernel): units = (non-empty pair tile, K part); tile_list holds the pair
     // tiles (mp * n_ct + n), each split over `split` contiguous chunk ranges; part[ks * ns + k] receives
     // sample k's value over K part ks (k_split_combine sums the parts)
+    // Tail split (n_whole > 0): the first n_whole listed tiles are whole units served directly, only the
+    // remaining tiles of the list are split (the last, partial wave of a persistent loop spread over the pairs)
     const int32_t *tile_list;
-    int split, n_units;
+    int split, n_units, n_whole;
     float *part;
     int64_t ns;
     // diagnosis (GVT_GEMM_PROF): per CTA, globaltimer stamps [entry, setup done, first stage landed,
@@ -725,12 +727,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     const int n_units = (EPI == EPI_SAMPLED && ep.tile_list) ? ep.n_units : n_tiles;
     auto unit = [&](int t, int &mp_tile, int &n_tile, int &c0, int &c1) -> bool {
         if (EPI == EPI_SAMPLED && ep.tile_list) {
-            const int tl = ep.tile_list[t / ep.split], ks = t % ep.split;
+            const bool whole = t < ep.n_whole;
+            const int u = t - ep.n_whole, sp = whole ? 1 : ep.split;
+            const int tl = whole ? ep.tile_list[t] : ep.tile_list[ep.n_whole + u / sp], ks = whole ? 0 : u % sp;
             mp_tile = tl / num_n;
             n_tile = tl % num_n;
             const int nch = (tile_nk(n_tile) + kcb - 1) / kcb;
-            c0 = nch * ks / ep.split;
-            c1 = nch * (ks + 1) / ep.split;
+            c0 = nch * ks / sp;
+            c1 = nch * (ks + 1) / sp;
             return true;
         }
         coords(t, mp_tile, n_tile);
@@ -852,7 +856,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
         for (int t = cluster; t < n_units; t += n_clusters) {
             int mp_tile, n_tile, c0, c1;
             if (!unit(t, mp_tile, n_tile, c0, c1)) continue;
-            float *part_out = (ep.tile_list && ep.part) ? ep.part + (int64_t)(t % ep.split) * ep.ns : nullptr;
+            float *part_out = (ep.tile_list && ep.part && t >= ep.n_whole)
+                                  ? ep.part + (int64_t)((t - ep.n_whole) % ep.split) * ep.ns
+                                  : nullptr;
             const int m_tile = 2 * mp_tile + (int)crank;
             const int m0 = m_tile * BM, n0 = n_tile * BN;
             const int gr = m0 + row;
@@ -1852,6 +1858,33 @@ __global__ void k_split_combine(const float *__restrict__ part, int split, int64
     }
 }
 
+// tail split: the parts of the samples of the split tiles only (tile_list[n_whole ..)): block b serves M-tile
+// 2 mp + (b & 1) of split tile b / 2, whose samples are one contiguous run of bucketed slots
+__global__ void k_split_combine_tail(const float *__restrict__ part, int split, int64_t ns,
+                                     const int32_t *__restrict__ tiles, int n_whole, int64_t n_rt, int64_t n_ct,
+                                     const int64_t *__restrict__ tile_ptr, const int32_t *__restrict__ dst, float coef,
+                                     int accumulate, float *__restrict__ out) {
+    const int32_t tl = tiles[n_whole + blockIdx.x / 2];
+    const int64_t m_tile = 2 * (int64_t)(tl / n_ct) + (blockIdx.x & 1), n = tl % n_ct;
+    if (m_tile >= n_rt) return;
+    const int64_t t = m_tile * n_ct + n;
+    const int64_t kb = tile_ptr[t * (BN / 32)], ke = tile_ptr[(t + 1) * (BN / 32)];
+    for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
+        float v = part[k];
+        for (int h = 1; h < split; h++) v += part[(int64_t)h * ns + k];
+        const int32_t dd = dst[k];
+        out[dd] = accumulate ? fmaf(coef, v, out[dd]) : coef * v;
+    }
+}
+
+static bool tail_split_enabled() {  // A/B knob: GVT_TAIL_SPLIT=0 keeps the last partial wave unsplit
+    static const bool on = [] {
+        const char *e = getenv("GVT_TAIL_SPLIT");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 // K parts per non-empty pair tile: when at most half of the CTA pairs would have a tile, each tile's
 // K range is split (at accumulation-chunk boundaries, >= 2 chunks per part) so every pair works --
 // C3's upper-triangle samples leave ~36 of 64 pair tiles non-empty on 74 CTA pairs.  GVT_SPLITK=0: off.
@@ -1899,21 +1932,48 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.out = out;
     const int split = sampled_split(c, sp, K);
     const int64_t npt = ((sp.n_rt + 1) / 2) * sp.n_ct;
+    int tail_split = 1;
     if (split > 1) {
         ep.tile_list = sp.pair_list;
         ep.split = split;
         ep.n_units = sp.n_pairs * split;
+        ep.n_whole = 0;
         ep.ns = sp.ns;
         ep.part = wsT<float>(c, slot ? "splitk.part1" : "splitk.part", (size_t)split * sp.ns);
-    } else if (sp.pair_list && sp.n_pairs > 0 && sp.n_pairs < npt && compact_tiles()) {
-        // some pair tiles are empty: the persistent loop runs over the non-empty ones only, so every CTA pair
-        // gets the same number of tiles (striding over all tiles left pairs with several non-empty tiles
-        // next to pairs with none; e.g. C4 MLPK's drug x target block)
-        ep.tile_list = sp.pair_list;
-        ep.split = 1;
-        ep.n_units = sp.n_pairs;
+    } else if (sp.pair_list && sp.n_pairs > 0 && compact_tiles()) {
+        // the persistent loop over the non-empty tiles (every CTA pair gets the same number of whole tiles;
+        // striding over all tiles left pairs with several non-empty tiles next to pairs with none), and a
+        // last partial wave of r <= pairs / 2 tiles split into s K parts, so that wave costs 1/s of a tile
+        // (C4: 240 tiles on 74 pairs = 3 waves + 18 tiles -> 18 x 4 parts).  Parts cost s x ns floats of
+        // workspace: only for out samples of at most 64 MB per part.
+        const int pairs = c->sm_count / 2, r = sp.n_pairs % pairs;
+        const int nch = (int)((K + BN - 1) / BN);
+        if (sp.n_pairs >= pairs && r > 0 && 2 * r <= pairs && tail_split_enabled() &&
+            sp.ns * (int64_t)sizeof(float) <= (64ll << 20))
+            tail_split = std::min(4, std::min(pairs / r, nch / 2));
+        if (tail_split >= 2) {
+            ep.tile_list = sp.pair_list;
+            ep.split = tail_split;
+            ep.n_whole = sp.n_pairs - r;
+            ep.n_units = ep.n_whole + r * tail_split;
+            ep.ns = sp.ns;
+            ep.part = wsT<float>(c, "splitk.tail", (size_t)tail_split * sp.ns);
+        } else if (sp.n_pairs < npt) {
+            tail_split = 1;
+            ep.tile_list = sp.pair_list;
+            ep.split = 1;
+            ep.n_units = sp.n_pairs;
+            ep.n_whole = sp.n_pairs;
+        } else {
+            tail_split = 1;
+        }
     }
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
+    if (tail_split > 1) {  // (never deferred: only the split tiles' samples have parts)
+        const int r = sp.n_pairs - ep.n_whole;
+        GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine_tail, 2 * r, 256, 0, ep.part, tail_split, sp.ns, sp.pair_list,
+                   ep.n_whole, sp.n_rt, sp.n_ct, sp.tile_ptr, sp.dst, coef, accumulate, out);
+    }
     if (split > 1 && defer) {
         defer->part = ep.part;
         defer->split = split;

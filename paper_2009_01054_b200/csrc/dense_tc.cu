@@ -724,7 +724,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
     };
     // work units: all pair tiles (empty sampled tiles skipped), or (sampled split-K) the listed non-empty
     // pair tiles x `split` K parts; [c0, c1) = the unit's accumulation chunks
-    const int n_units = (EPI == EPI_SAMPLED && ep.tile_list) ? ep.n_units : n_tiles;
+    const int n_units = ((EPI == EPI_SAMPLED && ep.tile_list) || (EPI == EPI_STORE16 && ep.n_whole > 0)) ? ep.n_units
+                                                                                                          : n_tiles;
     auto unit = [&](int t, int &mp_tile, int &n_tile, int &c0, int &c1) -> bool {
         if (EPI == EPI_SAMPLED && ep.tile_list) {
             const bool whole = t < ep.n_whole;
@@ -735,6 +736,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             const int nch = (tile_nk(n_tile) + kcb - 1) / kcb;
             c0 = nch * ks / sp;
             c1 = nch * (ks + 1) / sp;
+            return true;
+        }
+        if (EPI == EPI_STORE16 && ep.n_whole > 0 && t >= ep.n_whole) {  // tail split: the last tiles in parts
+            const int u = t - ep.n_whole, ks = u % ep.split;
+            coords(ep.n_whole + u / ep.split, mp_tile, n_tile);
+            const int nch = (tile_nk(n_tile) + kcb - 1) / kcb;
+            c0 = nch * ks / ep.split;
+            c1 = nch * (ks + 1) / ep.split;
             return true;
         }
         coords(t, mp_tile, n_tile);
@@ -1119,6 +1128,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             }
             if (threadIdx.x == 64) { GEMM_MARK(5) }
             if (single_unit) named_bar(1, 32 * N_EPI_WARPS);  // the staged column scales are visible
+            if (EPI == EPI_STORE16 && ep.n_whole > 0 && t >= ep.n_whole) {
+                // tail-split unit: this K part's raw accumulators (before the row / column scales) to the part
+                // buffer [part][split tile][m half][128 rows][256 cols]; k_store16_fixup sums and stores them
+                const int u = t - ep.n_whole, ks = u % ep.split, r_tiles = (n_units - ep.n_whole) / ep.split;
+                float *dp = ep.part + ((((int64_t)ks * r_tiles + u / ep.split) * 2 + crank) * BM + row) * BN + half * 128;
+#pragma unroll
+                for (int i = 0; i < 128; i += 4)
+                    *reinterpret_cast<float4 *>(dp + i) = make_float4(run[i], run[i + 1], run[i + 2], run[i + 3]);
+                continue;
+            }
             if (EPI == EPI_STORE16) {
                 // fp16 hi/lo of the unscaled result with a power-of-two scale per (128-row CTA block,
                 // 256-col tile) from the block's maximum (S16_SCALE_ROWS = 128: a CTA-wide max over
@@ -1467,8 +1486,9 @@ static void launch_gemm_t(gvt_ctx *c, int kind_id, const Operand &A, const Opera
                 cudaFuncSetAttribute(k_gemm2_x3<PREC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
             attr2[dv] = true;
         }
-        const int64_t pair_tiles =
-            (EPI == EPI_SAMPLED && ep.tile_list) ? ep.n_units : ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
+        const int64_t pair_tiles = ((EPI == EPI_SAMPLED && ep.tile_list) || (EPI == EPI_STORE16 && ep.n_whole > 0))
+                                       ? ep.n_units
+                                       : ((N + BN - 1) / BN) * ((M + 2 * BM - 1) / (2 * BM));
         const int64_t clusters = std::min<int64_t>(pair_tiles, c->sm_count / 2);  // persistent: one pair per 2 SMs
         dim3 grid((unsigned)(2 * clusters));
         static const bool prof = getenv("GVT_GEMM_PROF") != nullptr;
@@ -1787,6 +1807,81 @@ void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_
     }
 }
 
+// The stage-1 tail split: the last r pair tiles of the grouped order (r <= pairs / 2 after whole waves) run as
+// `split` K parts each; here one warp per output row of block (split tile, m half) sums the parts in part order
+// (8 columns per lane), applies the operands' row / column scales, and stores the fp16 pieces with the
+// epilogue's per-(row, 256-column tile) scale rule (S16_SCALE_ROWS = 1), 16 bytes per lane per piece.
+__global__ void __launch_bounds__(256) k_store16_fixup(const float *__restrict__ part, int split, int r_tiles, int n_whole,
+                                                       int num_mp, int num_n, int gm, int64_t M, int64_t N,
+                                                       const float *__restrict__ sa, const float *__restrict__ sb,
+                                                       __half *__restrict__ ch, __half *__restrict__ cl, int64_t ldc,
+                                                       float *__restrict__ csk, int64_t csk_ld) {
+    // block b: split tile b / 32, m half (b / 16) & 1, rows 8 (b % 16) + warp (one row per warp: all in flight)
+    const int ti = blockIdx.x >> 5, mh = (blockIdx.x >> 4) & 1, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = n_whole + ti, in_group = gm * num_n, first_m = (t / in_group) * gm;
+    const int group_m = min(num_mp - first_m, gm);
+    const int mp_tile = first_m + (t % in_group) % group_m, n_tile = (t % in_group) / group_m;
+    const int64_t gc0 = (int64_t)n_tile * BN + 8 * lane;
+    {
+        const int row = (blockIdx.x & 15) * 8 + warp;
+        const int64_t gr = (int64_t)(2 * mp_tile + mh) * BM + row;
+        if (gr >= M) return;
+        float v[8];
+        for (int h = 0; h < split; h++) {
+            const float4 *pp =
+                reinterpret_cast<const float4 *>(part + ((((int64_t)h * r_tiles + ti) * 2 + mh) * BM + row) * BN + 8 * lane);
+            const float4 q0 = pp[0], q1 = pp[1];
+            const float q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int i = 0; i < 8; i++) v[i] = h == 0 ? q[i] : v[i] + q[i];
+        }
+        const float ra = sa ? sa[gr] : 1.f;
+        float mx = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int64_t gc = gc0 + i;
+            v[i] *= ra * ((sb && gc < N) ? sb[gc] : 1.f);
+            if (gc < N) mx = fmaxf(mx, fabsf(v[i]));
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int e = 0;
+        if (mx > 0.f && isfinite(mx)) {
+            int ex;
+            frexpf(mx, &ex);
+            e = 15 - ex;
+        }
+        const float s = ldexpf(1.f, e);
+        if (lane == 0) csk[(int64_t)n_tile * csk_ld + gr] = ldexpf(1.f, -e);
+        __half2 hh[4], ll[4];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+            const float v0 = v[i] * s, v1 = v[i + 1] * s;
+            hh[i / 2] = __float22half2_rn(make_float2(v0, v1));
+            const float2 hf = __half22float2(hh[i / 2]);
+            ll[i / 2] = __float22half2_rn(make_float2(v0 - hf.x, v1 - hf.y));
+        }
+        const int64_t o = gr * ldc + gc0;
+        if (gc0 + 8 <= N && (ldc & 7) == 0) {
+            *reinterpret_cast<uint4 *>(ch + o) = *reinterpret_cast<const uint4 *>(hh);
+            *reinterpret_cast<uint4 *>(cl + o) = *reinterpret_cast<const uint4 *>(ll);
+        } else {
+            const __half *ph = reinterpret_cast<const __half *>(hh), *pl = reinterpret_cast<const __half *>(ll);
+            for (int i = 0; i < 8 && gc0 + i < N; i++) {
+                ch[o + i] = ph[i];
+                cl[o + i] = pl[i];
+            }
+        }
+    }
+}
+
+static bool store_tail_split_enabled() {  // A/B knob: GVT_STORE_TAIL_SPLIT=0 keeps stage 1's last wave unsplit
+    static const bool on = [] {
+        const char *e = getenv("GVT_STORE_TAIL_SPLIT");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 // hi/lo: M rows x ldc halves; sk: ceil(N/256) chunk rows x sk_ld (>= round_up(M, 256) / S16_SCALE_ROWS)
 // floats, whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
@@ -1801,7 +1896,42 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     ep.c_sk = sk;
     ep.c_sk_ld = sk_ld;
     ep.ldc = ldc;
+    // tail split of the last partial wave (as the sampled GEMM's): r <= pairs / 2 leftover tiles in s K parts
+    const int pairs = c->sm_count / 2;
+    const int num_mp = (int)((M + 2 * BM - 1) / (2 * BM)), num_n = (int)((N + BN - 1) / BN);
+    const int n_tiles = num_mp * num_n, r = n_tiles % pairs;
+    int split = 1;
+    if (S16_SCALE_ROWS == 1 && c->gemm_cta == 2 && n_tiles >= pairs && r > 0 && 2 * r <= pairs &&
+        store_tail_split_enabled()) {
+        int nch_min = INT32_MAX;  // (block-sparse K lists: every split tile must have >= 2 chunks per part)
+        if (kb_list) {
+            std::vector<int32_t> hoff((size_t)num_n + 1);
+            GVT_CUDA_TRY(cudaMemcpyAsync(hoff.data(), kb_off, sizeof(int32_t) * hoff.size(), cudaMemcpyDeviceToHost,
+                                         c->stream));
+            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            for (int n = 0; n < num_n; n++) nch_min = std::min(nch_min, (hoff[(size_t)n + 1] - hoff[(size_t)n] + 3) / 4);
+        } else {
+            nch_min = (int)((K + BN - 1) / BN);
+        }
+        split = std::min(4, std::min(pairs / r, nch_min / 2));
+    }
+    if (split >= 2) {
+        ep.n_whole = n_tiles - r;
+        ep.split = split;
+        ep.n_units = ep.n_whole + r * split;
+        ep.part = wsT<float>(c, "store16.tail", (size_t)split * r * 2 * BM * BN);
+    }
     launch_gemm<EPI_STORE16>(c, K_STAGE1_TC, A, B, M, N, K, ep);
+    if (split >= 2) {
+        static const int env_gm = [] {
+            const char *e = getenv("GVT_GROUP_M");
+            return e ? atoi(e) : 0;
+        }();
+        const int gm = env_gm > 0 ? env_gm : GROUP_M;
+        static_assert(BM == 16 * 8, "fixup: 16 blocks of 8 rows per m half");
+        GVT_LAUNCH(c, K_STAGE1_TC, k_store16_fixup, 32 * r, 256, 0, ep.part, split, r, ep.n_whole, num_mp, num_n, gm, M,
+                   N, A.scale, B.scale, hi, lo, ldc, sk, sk_ld);
+    }
 }
 
 __global__ void k_add_diag(float *__restrict__ X, int64_t ldX, const float *__restrict__ diag, int64_t row_lo,
@@ -1858,18 +1988,19 @@ __global__ void k_split_combine(const float *__restrict__ part, int split, int64
     }
 }
 
-// tail split: the parts of the samples of the split tiles only (tile_list[n_whole ..)): block b serves M-tile
-// 2 mp + (b & 1) of split tile b / 2, whose samples are one contiguous run of bucketed slots
+// tail split: the parts of the samples of the split tiles only (tile_list[n_whole ..)); an M-tile of a split
+// tile holds one contiguous run of bucketed sample slots
 __global__ void k_split_combine_tail(const float *__restrict__ part, int split, int64_t ns,
                                      const int32_t *__restrict__ tiles, int n_whole, int64_t n_rt, int64_t n_ct,
                                      const int64_t *__restrict__ tile_ptr, const int32_t *__restrict__ dst, float coef,
                                      int accumulate, float *__restrict__ out) {
-    const int32_t tl = tiles[n_whole + blockIdx.x / 2];
-    const int64_t m_tile = 2 * (int64_t)(tl / n_ct) + (blockIdx.x & 1), n = tl % n_ct;
+    // block b: split tile b / 32, M-tile half (b / 16) & 1, slice b % 16 of that M-tile's sample run
+    const int32_t tl = tiles[n_whole + blockIdx.x / 32];
+    const int64_t m_tile = 2 * (int64_t)(tl / n_ct) + ((blockIdx.x >> 4) & 1), n = tl % n_ct;
     if (m_tile >= n_rt) return;
     const int64_t t = m_tile * n_ct + n;
     const int64_t kb = tile_ptr[t * (BN / 32)], ke = tile_ptr[(t + 1) * (BN / 32)];
-    for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
+    for (int64_t k = kb + (int64_t)(blockIdx.x & 15) * blockDim.x + threadIdx.x; k < ke; k += 16 * (int64_t)blockDim.x) {
         float v = part[k];
         for (int h = 1; h < split; h++) v += part[(int64_t)h * ns + k];
         const int32_t dd = dst[k];
@@ -1971,7 +2102,7 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     launch_gemm<EPI_SAMPLED>(c, K_STAGE2_TC, A, B, M, N, K, ep);
     if (tail_split > 1) {  // (never deferred: only the split tiles' samples have parts)
         const int r = sp.n_pairs - ep.n_whole;
-        GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine_tail, 2 * r, 256, 0, ep.part, tail_split, sp.ns, sp.pair_list,
+        GVT_LAUNCH(c, K_STAGE2_TC, k_split_combine_tail, 32 * r, 256, 0, ep.part, tail_split, sp.ns, sp.pair_list,
                    ep.n_whole, sp.n_rt, sp.n_ct, sp.tile_ptr, sp.dst, coef, accumulate, out);
     }
     if (split > 1 && defer) {

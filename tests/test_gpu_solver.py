@@ -248,7 +248,8 @@ def cgg_ctx(ctx):
 def test_chronopoulos_gear_cg_matches_oracle_cg(cgg_ctx, engine):
     """GVT_OPT_CG_VARIANT = 1 has the Hestenes-Stiefel iterates in exact arithmetic: on C1 its 50
     iterations match the oracle's CG weights (<= 1e-4) and residual history, and residual mode
-    stops at the oracle's iteration; per iteration it launches 3 solver kernels instead of 5."""
+    stops at the oracle's iteration; per iteration it launches 3 solver kernels instead of the separate
+    Hestenes-Stiefel kernels' 5 (on the dense engine Hestenes-Stiefel CG runs the fused tail, one launch)."""
     cgg_ctx.set_option(G.OPT_ENGINE, engine)
     w = synth.config1()
     D = O.gram(w.base, w.Xd, gamma=w.gamma)
@@ -277,7 +278,10 @@ def test_chronopoulos_gear_cg_matches_oracle_cg(cgg_ctx, engine):
         k = cgg_ctx.stats()["kinds"]
         per[variant] = k["cg_vector"]["count"] + k["cg_scalar"]["count"]
     cgg_ctx.set_option(G.OPT_PROFILE, 0)
-    assert per[1] < per[0]
+    if engine == G.ENGINE_DENSE:  # the dense engine's Hestenes-Stiefel CG runs the fused tail: 1 launch / iteration
+        assert per[0] < per[1]
+    else:
+        assert per[1] < per[0]
 
 
 @pytest.mark.parametrize("kernel", [G.SYMMETRIC, G.MLPK, G.POLY2D, G.CARTESIAN])

@@ -1901,20 +1901,11 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     const int num_mp = (int)((M + 2 * BM - 1) / (2 * BM)), num_n = (int)((N + BN - 1) / BN);
     const int n_tiles = num_mp * num_n, r = n_tiles % pairs;
     int split = 1;
-    if (S16_SCALE_ROWS == 1 && c->gemm_cta == 2 && n_tiles >= pairs && r > 0 && 2 * r <= pairs &&
-        store_tail_split_enabled()) {
-        int nch_min = INT32_MAX;  // (block-sparse K lists: every split tile must have >= 2 chunks per part)
-        if (kb_list) {
-            std::vector<int32_t> hoff((size_t)num_n + 1);
-            GVT_CUDA_TRY(cudaMemcpyAsync(hoff.data(), kb_off, sizeof(int32_t) * hoff.size(), cudaMemcpyDeviceToHost,
-                                         c->stream));
-            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-            for (int n = 0; n < num_n; n++) nch_min = std::min(nch_min, (hoff[(size_t)n + 1] - hoff[(size_t)n] + 3) / 4);
-        } else {
-            nch_min = (int)((K + BN - 1) / BN);
-        }
-        split = std::min(4, std::min(pairs / r, nch_min / 2));
-    }
+    // (not with block-sparse K lists: their per-tile chunk counts live on the device, and this runs inside the
+    // solver's graph capture, where no host read-back is possible)
+    if (S16_SCALE_ROWS == 1 && c->gemm_cta == 2 && !kb_list && n_tiles >= pairs && r > 0 && 2 * r <= pairs &&
+        store_tail_split_enabled())
+        split = std::min(4, std::min(pairs / r, (int)((K + BN - 1) / BN) / 2));
     if (split >= 2) {
         ep.n_whole = n_tiles - r;
         ep.split = split;

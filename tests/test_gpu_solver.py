@@ -469,3 +469,39 @@ def test_small_engine_shapes(ctx, m, q, n):
     ao, ito, _, _ = O.cg(O.kernel_terms(O.KRONECKER), D32, T32, f, s, y, 1.0, 8)
     assert it == ito or n <= 8
     assert rel(a.cpu().numpy(), ao) <= 1e-4
+
+
+@pytest.mark.parametrize("kernel", [G.KRONECKER, G.SYMMETRIC, G.ANTISYMMETRIC, G.CARTESIAN])
+@pytest.mark.parametrize("n", [1, 5, 1185, 30011])
+def test_dense_fused_tail_ragged_vs_oracle(ctx, kernel, n):
+    """The fused dense-engine CG tail (tail.cu: split-K combine, CG step, next pair matrix in one launch) on ragged
+    sizes with duplicate pairs: 8 CG iterations on the tensor-core engine against the oracle's CG, within 1e-4 or 3x
+    the sparse engine's own error on the same instance; the profiled launch count shows one CG launch per
+    iteration (the tail) instead of three."""
+    hom = kernel in HOM
+    rng = np.random.default_rng(7 * n + kernel)
+    m, q = 37, 29
+    D32 = f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((m, 4)), gamma=0.25))
+    T32 = None if hom else f32(O.gram(G.BASE_GAUSSIAN, rng.standard_normal((q, 4)), gamma=0.25))
+    f = rng.integers(0, m, n).astype(np.int32)
+    s = rng.integers(0, m if hom else q, n).astype(np.int32)
+    y = rng.standard_normal(n).astype(np.float32)
+    terms = G.gvt_kernel_terms(kernel)
+    args = (dev(D32), None if hom else dev(T32), dev(f), dev(s), dev(y), terms, 1.0, 8)
+    try:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
+        ctx.set_option(G.OPT_PROFILE, 1)
+        ctx.reset_stats()
+        a, it, _, code = ctx.fit(*args)
+        k = ctx.stats()["kinds"]
+        ctx.set_option(G.OPT_PROFILE, 0)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_SPARSE)
+        asp, _, _, _ = ctx.fit(*args)
+    finally:
+        ctx.set_option(G.OPT_PROFILE, 0)
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    ao, ito, _, _ = O.cg(O.kernel_terms(kernel), D32, T32, f, s, y, 1.0, 8)
+    assert code == G.OK and (it == ito or n <= 8)
+    assert k["cg_vector"]["count"] <= 8 + 3  # (init, 8 tails -- halted ones return at once --, the direction copy)
+    assert np.all(np.isfinite(a.cpu().numpy()))
+    assert rel(a.cpu().numpy(), ao) <= max(1e-4, 3 * rel(asp.cpu().numpy(), ao))

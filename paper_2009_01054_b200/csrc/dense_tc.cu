@@ -246,6 +246,9 @@ __device__ __forceinline__ unsigned long long gemm_timer() {
 template <int STRIDE>  // the epilogue threads serving (32 x epilogue warps)
 __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
                                               const float *stage, float *part) {
+#ifdef GVT_TIMING_SKIP_SERVE  // timing-only A/B build (results wrong): the multi-unit serve skipped
+    return;
+#endif
     if (part) {  // split-K: this K part's raw value per sample slot (no coefficient, no accumulation)
         for (int64_t k = kb0 + t; k < ke; k += STRIDE) {
             const int rl = ep.s_r[k] - m0, cl = ep.s_c[k] - gc0;

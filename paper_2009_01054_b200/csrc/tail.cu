@@ -188,8 +188,8 @@ bool dense_tail_fits(int64_t ld) { return ld > 0 && tail_smem(ld) <= 96 * 1024; 
 void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const int32_t *inv, float *u, float *x,
                    float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
                    double *part1, double *part2, const TailX *xs, int nx) {
-    static int grid_dev[GVT_MAX_DEVICES] = {};
-    int &grid = grid_dev[c->device < GVT_MAX_DEVICES ? c->device : 0];
+    static bool attr_dev[GVT_MAX_DEVICES] = {};
+    bool &attr_set = attr_dev[c->device < GVT_MAX_DEVICES ? c->device : 0];
     GVT_REQUIRE(nx >= 1 && nx <= 2, GVT_E_STATE, "fused CG tail: one or two pair-matrix operands");
     GVT_REQUIRE(!(pa.part || pb.part) || inv, GVT_E_STATE, "fused CG tail: split-K parts without the output -> slot map");
     DenseTailArgs a;
@@ -214,13 +214,20 @@ void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const
     a.nx = nx;
     const size_t smem = tail_smem(a.ldmax);
     GVT_REQUIRE(dense_tail_fits(a.ldmax), GVT_E_STATE, "fused CG tail: X rows too long");
-    if (!grid) {
+    if (!attr_set) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_dense_cg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        int per_sm = 0;
-        GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_cg_tail, TAIL_THREADS, 96 * 1024));
-        GVT_REQUIRE(per_sm >= 1, GVT_E_STATE, "fused CG tail: no resident CTA");
-        grid = c->sm_count * std::min(per_sm, 2);
+        attr_set = true;
     }
+    // co-resident CTAs for this launch's shared memory (its X rows); latency-bound phases want as many as
+    // fit: 296 vs 148 CTAs measured 91.6 vs 106 us per C3 iteration (profiles/r02_ab_dense_tail.txt)
+    int per_sm = 0;
+    GVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_cg_tail, TAIL_THREADS, smem));
+    GVT_REQUIRE(per_sm >= 1, GVT_E_STATE, "fused CG tail: no resident CTA");
+    static const int env_per_sm = [] {  // A/B knob: GVT_TAIL_CTAS_PER_SM (cap; default 2: 3 measured no better)
+        const char *e = getenv("GVT_TAIL_CTAS_PER_SM");
+        return e ? atoi(e) : 2;
+    }();
+    const int grid = c->sm_count * std::max(1, std::min(per_sm, env_per_sm));
     a.partA = pa.part;
     a.splitA = pa.split;
     a.coefA = pa.coef;

@@ -765,7 +765,32 @@ struct CgTail {
     double *st = nullptr;      // CG state (st[2] = beta)
     double lambda = 0.0;
     float *p = nullptr;        // p_{k-1} in, p_k out
+    // persistent tail (tail.cu): the final combine is left to the tail launch, described here
+    bool defer = false;
+    GatherCombine gc;
 };
+
+// the cheap forms' final combine: fused into the CG tail (k_cg_combine_ap), deferred to the persistent tail, or plain
+static void cheap_combine(gvt_ctx *c, const Problem &P, const float *g1, int rs1, float c1, const float *g2, int rs2,
+                          float c2, int accumulate, float *u, CgTail *tail) {
+    if (tail && tail->defer) {
+        GatherCombine &g = tail->gc;
+        g.f = P.of;
+        g.s = P.os;
+        g.g1 = g1;
+        g.rs1 = rs1;
+        g.c1 = c1;
+        g.g2 = g2;
+        g.rs2 = rs2;
+        g.c2 = c2;
+        g.accumulate = accumulate;
+    } else if (tail) {
+        cg_combine_ap(c, P.of, P.os, P.n_out, g1, rs1, c1, g2, rs2, c2, accumulate, u, tail->p, tail->r, tail->lambda,
+                      tail->st);
+    } else {
+        combine_gather(c, P.of, P.os, P.n_out, g1, rs1, c1, g2, rs2, c2, accumulate, u);
+    }
+}
 
 static bool cg_tail_enabled() {  // A/B knob: GVT_CG_TAIL=0 keeps the separate CG vector kernels
     static const bool on = [] {
@@ -783,6 +808,18 @@ static bool dense_tail_enabled() {  // A/B knob: GVT_DENSE_TAIL=0 keeps the sepa
     return on;
 }
 
+// A/B knob, default off: GVT_CHEAP_TAIL=1 runs the cheap forms' tail (combine, Ap, alpha, x / r, beta, p) as one
+// persistent launch.  Bit-identical, but slower at C4 sizes (n = 2e6: Ranking 82-86 -> 88-110 us per iteration at
+// 2-8 CTAs per SM, profiles/r02_ab_cheap_tail.txt): the separate kernels' 1184 independent blocks keep more of the
+// vector traffic in flight than a co-resident grid between its barriers.
+static bool cheap_tail_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("GVT_CHEAP_TAIL");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 static bool cg_tail_lazy() {  // A/B knob: GVT_CG_TAIL_LAZY=1 also folds the direction update (k_cg_p)
     static const bool on = [] {
         const char *e = getenv("GVT_CG_TAIL_LAZY");
@@ -792,7 +829,7 @@ static bool cg_tail_lazy() {  // A/B knob: GVT_CG_TAIL_LAZY=1 also folds the dir
 }
 
 static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float *p_local, float *u,
-                       const CgTail *tail = nullptr) {
+                       CgTail *tail = nullptr) {
     // gather p over the ranks (world 1: p_full is p_local itself)
     const float *p = p_local;
     if (distributed(c)) {
@@ -818,11 +855,7 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         segment_sum_gather(c, mp.byS, p, mp.b2);  // bS
         gemv(c, P.D, mp.b1, 1, mp.g1, !P.rect);  // D.^2 bF
         gemv(c, P.T, mp.b2, 1, mp.g2, !P.rect);  // T.^2 bS
-        if (tail)
-            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u, tail->p,
-                          nullptr, tail->lambda, tail->st);
-        else
-            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u);
+        cheap_combine(c, P, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 1, u, tail);
         break;
     }
     case FORM_LINEAR:
@@ -830,20 +863,12 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         segment_sum_gather(c, mp.byS, p, mp.b2, tail ? tail->r : nullptr, tail ? tail->st + 2 : nullptr);
         gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
         gemv(c, P.T, mp.b2, 0, mp.g2, !P.rect);
-        if (tail)
-            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u, tail->p,
-                          tail->r, tail->lambda, tail->st);
-        else
-            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u);
+        cheap_combine(c, P, mp.g1, GVT_SEL_FIRST, 1.f, mp.g2, GVT_SEL_SECOND, 1.f, 0, u, tail);
         break;
     case FORM_RANKING:
         segment_sum_gather(c, mp.byF, p, mp.b1, tail ? tail->r : nullptr, tail ? tail->st + 2 : nullptr);  // bF - bS
         gemv(c, P.D, mp.b1, 0, mp.g1, !P.rect);
-        if (tail)
-            cg_combine_ap(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u,
-                          tail->p, tail->r, tail->lambda, tail->st);
-        else
-            combine_gather(c, P.of, P.os, P.n_out, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u);
+        cheap_combine(c, P, mp.g1, GVT_SEL_FIRST, 1.f, mp.g1, GVT_SEL_SECOND, -1.f, 0, u, tail);
         break;
     case FORM_CARTESIAN:
         if (mp.cart_dense) {  // u = (D X + X T) sampled: two 3xFP16 GEMMs, the second accumulating
@@ -1486,10 +1511,16 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
     const bool fuse_cart = tail_common && mp.form == FORM_CARTESIAN && mp.cart_dense && short_rows(P.m) &&
                            short_rows(P.q);
     bool fuse_dense = fuse_kron || fuse_cart;
+    // the cheap forms' tail as one persistent launch too (tail.cu gather-combine mode; not with the lazy direction)
+    const bool cheap_persistent = fuse_tail && !cg_tail_lazy() && cheap_tail_enabled();
     double *tail_part2 = nullptr;
     const int32_t *tail_inv = nullptr;
     float *p_alt = nullptr;
     bool tail_first = true;
+    if (cheap_persistent) {
+        tail_part2 = wsT<double>(c, "tail.part2", RED_BLOCKS);
+        dense_tail_init(c, tail_part2, nullptr, 0, 0);
+    }
     if (fuse_dense) {
         const SamplePlan &sp = fuse_cart ? mp.cart_smp : gd->smp;
         tail_part2 = wsT<double>(c, "tail.part2", RED_BLOCKS);
@@ -1538,6 +1569,15 @@ static gvt_status fit_impl(gvt_ctx *c, const float *D, int64_t m, const float *T
         } else if (cgg) {
             run_matvec(c, P, mp, r, u);  // w = K r
             cgg_step(c, x, r, p, sv, u, n, lambda, state);
+        } else if (fuse_tail && cheap_persistent) {  // the combine, Ap, alpha, x / r, beta, p in one launch
+            CgTail t;
+            t.defer = true;
+            t.st = state;
+            t.lambda = lambda;
+            t.p = p;
+            run_matvec(c, P, mp, p, u, &t);
+            dense_cg_tail(c, SplitParts(), SplitParts(), nullptr, u, x, r, p, p, n, cg_vec_blocks(n), lambda, state,
+                          cg_parts(c), tail_part2, nullptr, 0, &t.gc);
         } else if (fuse_tail) {
             CgTail t;
             // lazy direction (segment sums on r + beta p, the combine stores p) measured slower: the

@@ -246,9 +246,17 @@ struct TailX {
     int64_t row_lo = 0, rows = 0;
     Operand op;
 };
+// the cheap forms' final gather-combine u_i = c1 g1[sel1(i)] + c2 g2[sel2(i)] (+ u_i), done by the tail's first
+// phase exactly as k_cg_combine_ap does it (then no part sets, no pair-matrix operand, p updated in place)
+struct GatherCombine {
+    const int32_t *f = nullptr, *s = nullptr;
+    const float *g1 = nullptr, *g2 = nullptr;
+    int rs1 = 0, rs2 = 0, accumulate = 0;
+    float c1 = 1.f, c2 = 1.f;
+};
 void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const int32_t *inv, float *u, float *x,
                    float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
-                   double *part1, double *part2, const TailX *xs, int nx);
+                   double *part1, double *part2, const TailX *xs, int nx, const GatherCombine *gcomb = nullptr);
 int cg_vec_blocks(int64_t n);
 double *cg_parts(gvt_ctx *c);
 // Chronopoulos-Gear single-reduction CG (GVT_OPT_CG_VARIANT = 1): init, then per iteration the

@@ -60,6 +60,11 @@ struct DenseTailArgs {
     double *part1, *part2;  // [RED_BLOCKS] each, unused slots zero
     TailXDev xb[2];
     int nx;
+    // gather-combine mode (the cheap forms): u_i from the factor gathers, p updated in place (pd[0] == pd[1])
+    int gmode, grs1, grs2, gacc;
+    const int32_t *gf, *gs;
+    const float *g1, *g2;
+    float gc1, gc2;
     int64_t ldmax;
     unsigned *bar;
     unsigned long long *prof;  // GVT_TAIL_PROF: [0..7] CTA 0's phase stamps, [8 + b] CTA b's exit
@@ -87,10 +92,26 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_dense_cg_tail(DenseTailArgs a)
     TAIL_MARK(0);
     unsigned gen = 0;
     if (tid == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(a.bar) : "memory");
-    // ---- A: u from the parts (as k_split_combine), then Ap = u + lambda p and p.Ap (as k_cg_ap)
+    // ---- A: u from the parts (as k_split_combine), then Ap = u + lambda p and p.Ap (as k_cg_ap); or (the cheap
+    // forms) u from the factor gathers with Ap and p.Ap in one loop (as k_cg_combine_ap)
     for (int64_t vb = blockIdx.x; vb < a.nvb; vb += gridDim.x) {
         int64_t lo, hi;
         vblock_range(a.n, a.nvb, vb, lo, hi);
+        if (a.gmode) {
+            double acc = 0.0;
+            for (int64_t i = lo + tid; i < hi; i += TAIL_THREADS) {
+                float v = a.gc1 * a.g1[a.grs1 == 0 ? a.gf[i] : a.gs[i]];
+                if (a.g2) v = fmaf(a.gc2, a.g2[a.grs2 == 0 ? a.gf[i] : a.gs[i]], v);
+                const float ui = a.gacc ? __ldcg(a.u + i) + v : v;
+                const float pi = __ldcg(p + i);
+                const float av = fmaf(a.lambda, pi, ui);
+                a.u[i] = av;
+                acc += (double)pi * (double)av;
+            }
+            acc = block_sum(acc);
+            if (tid == 0) a.part1[vb] = acc;
+            continue;
+        }
         if (a.partA || a.partB) {
             for (int64_t i = lo + tid; i < hi; i += TAIL_THREADS) {
                 const int64_t k = a.inv[i];
@@ -169,7 +190,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_dense_cg_tail(DenseTailArgs a)
     const int warp = tid >> 5, lane = tid & 31;
     float *rowbuf = rowbufs + (size_t)warp * a.ldmax;
     const int64_t nw = (int64_t)gridDim.x * (TAIL_THREADS / 32);
-    const int64_t rows0 = a.xb[0].rows, rows_all = rows0 + (a.nx > 1 ? a.xb[1].rows : 0);
+    const int64_t rows0 = a.nx > 0 ? a.xb[0].rows : 0, rows_all = rows0 + (a.nx > 1 ? a.xb[1].rows : 0);
     for (int64_t row = (int64_t)blockIdx.x * (TAIL_THREADS / 32) + warp; row < rows_all; row += nw) {
         const TailXDev &xb = a.xb[row < rows0 ? 0 : 1];
         x16_row_warp<true>(row < rows0 ? row : row - rows0, lane, rowbuf, xb.row_ptr, xb.col, xb.src, xb.sign, p,
@@ -187,10 +208,12 @@ bool dense_tail_fits(int64_t ld) { return ld > 0 && tail_smem(ld) <= 96 * 1024; 
 
 void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const int32_t *inv, float *u, float *x,
                    float *r, float *p0, float *p1, int64_t n, int64_t nvb, double lambda, double *state,
-                   double *part1, double *part2, const TailX *xs, int nx) {
+                   double *part1, double *part2, const TailX *xs, int nx, const GatherCombine *gcomb) {
     static bool attr_dev[GVT_MAX_DEVICES] = {};
     bool &attr_set = attr_dev[c->device < GVT_MAX_DEVICES ? c->device : 0];
-    GVT_REQUIRE(nx >= 1 && nx <= 2, GVT_E_STATE, "fused CG tail: one or two pair-matrix operands");
+    GVT_REQUIRE(nx >= (gcomb ? 0 : 1) && nx <= 2, GVT_E_STATE, "fused CG tail: one or two pair-matrix operands");
+    GVT_REQUIRE(!gcomb || (p0 == p1 && nx == 0 && !pa.part && !pb.part), GVT_E_STATE,
+                "fused CG tail: the gather combine updates p in place, without parts or operands");
     GVT_REQUIRE(!(pa.part || pb.part) || inv, GVT_E_STATE, "fused CG tail: split-K parts without the output -> slot map");
     DenseTailArgs a;
     memset(&a, 0, sizeof(a));
@@ -212,8 +235,20 @@ void dense_cg_tail(gvt_ctx *c, const SplitParts &pa, const SplitParts &pb, const
         a.ldmax = std::max(a.ldmax, d.ld);
     }
     a.nx = nx;
-    const size_t smem = tail_smem(a.ldmax);
-    GVT_REQUIRE(dense_tail_fits(a.ldmax), GVT_E_STATE, "fused CG tail: X rows too long");
+    if (gcomb) {
+        a.gmode = 1;
+        a.gf = gcomb->f;
+        a.gs = gcomb->s;
+        a.g1 = gcomb->g1;
+        a.g2 = gcomb->g2;
+        a.grs1 = gcomb->rs1;
+        a.grs2 = gcomb->rs2;
+        a.gc1 = gcomb->c1;
+        a.gc2 = gcomb->c2;
+        a.gacc = gcomb->accumulate;
+    }
+    const size_t smem = nx > 0 ? tail_smem(a.ldmax) : 0;
+    GVT_REQUIRE(nx == 0 || dense_tail_fits(a.ldmax), GVT_E_STATE, "fused CG tail: X rows too long");
     if (!attr_set) {
         GVT_CUDA_TRY(cudaFuncSetAttribute(k_dense_cg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
         attr_set = true;

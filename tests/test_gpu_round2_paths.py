@@ -5,6 +5,7 @@ library's environment knobs take effect:
   GVT_SPLITK=0       one CTA pair per sampled tile instead of split-K (small problems)
   GVT_BUILD_WARP=0   CTA-per-row X build instead of warp-per-row (rows <= 2048)
   OPT_ENGINE=1       (option) the gather form of the Cartesian kernel instead of its two sampled GEMMs
+  GVT_CHEAP_TAIL=1   (default off) the cheap forms' CG tail as one persistent launch instead of three
   GVT_DENSE_TAIL=0   separate split-K combine, CG vector kernels, S-scale memset and X build instead of the
                      fused dense-engine CG tail (one persistent launch, tail.cu)
 The fast path changes only summation order, so results agree to fp32 rounding; the oracle checks of the
@@ -152,3 +153,15 @@ def test_cartesian_tensor_core_form_matches_gather_c3(tmp_path):
     ff, _ = run("C3", "cartesian", "fit", 5, {}, tmp_path, "ffit")
     sf, _ = run("C3", "cartesian", "fit", 5, {"GVT_TEST_OPTS": "OPT_ENGINE=1"}, tmp_path, "sfit")
     assert rel(ff, sf) <= 1e-4
+
+
+@pytest.mark.parametrize("kname", ["ranking", "poly2d"])
+def test_cheap_persistent_tail_bit_identical_c4(tmp_path, kname):
+    """The cheap forms' CG tail as one persistent launch (tail.cu gather-combine mode: the combine, Ap, alpha,
+    x / r, beta and p with two grid barriers) runs k_cg_combine_ap's, k_cg_xr's and k_cg_p's arithmetic on their
+    partitions: 10-iteration C4 fits, weights, search direction and residual history bit-identical.  (An A/B
+    knob, default off: slower than the separate kernels at this n.)"""
+    env = {"GVT_TEST_DIR": "1"}
+    fast, ef = run("C4", kname, "fit", 10, {**env, "GVT_CHEAP_TAIL": "1"}, tmp_path, "fast")
+    slow, es = run("C4", kname, "fit", 10, env, tmp_path, "slow")
+    assert ef["iters"] == es["iters"] == 10 and np.array_equal(fast, slow) and ef["hist"] == es["hist"]

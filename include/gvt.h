@@ -99,7 +99,10 @@ typedef enum {
                                     an iteration is <= 4e6 FMAs), 4 = persistent multi-CTA whole-fit
                                     CG with grid barriers (Kronecker fits with m q^2 <= 6.4e7 dense
                                     stage-1 FMAs, e.g. a complete small grid; auto picks it when the
-                                    single-CTA solver does not apply)                                 */
+                                    single-CTA solver does not apply).  The Cartesian kernel follows
+                                    the same switch: 1 = the gather form, 2 = u = (D X + X T) sampled
+                                    as two tensor-core GEMMs (single GPU; multi-GPU runs the gather
+                                    form), auto = by estimated time                                   */
     GVT_OPT_DENSE_THRESHOLD = 1, /* auto engine: -1 (default) = by estimated time of the two engines
                                     (B200 calibration; crossover ~1 % density at C5 object counts);
                                     >= 0 = dense at or above this pair-matrix density             */

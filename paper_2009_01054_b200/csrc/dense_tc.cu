@@ -243,6 +243,9 @@ __device__ __forceinline__ unsigned long long gemm_timer() {
 #ifndef SERVE_UNROLL
 #define SERVE_UNROLL 1
 #endif
+#ifndef SERVE_PREFETCH
+#define SERVE_PREFETCH 1
+#endif
 template <int STRIDE>  // the epilogue threads serving (32 x epilogue warps)
 __device__ __forceinline__ void serve_samples(const EpiParams &ep, int64_t kb0, int64_t ke, int t, int m0, int gc0,
                                               const float *stage, float *part) {
@@ -1002,15 +1005,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
 #pragma unroll
                     for (int i = 0; i < 32; i++) mine[i] = run[(j % SG) * 32 + i];
                 }
+#if SERVE_PREFETCH
+                // the sample ranges and this thread's first sample of both chunks are loaded before the staging
+                // barrier, so their L2 latency overlaps the staging instead of opening the serve
+                int64_t pk0[2], pke[2], pdst[2];
+                int prl[2], pcl[2];
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const int chunk = hh * 4 + j;
+                    const int64_t cidx = tile * (BN / 32) + chunk;
+                    pk0[hh] = tile_ok ? ep.chunk_ptr[cidx] : 0;
+                    pke[hh] = tile_ok ? ep.chunk_ptr[cidx + 1] : 0;
+                    const int64_t k = pk0[hh] + tE;
+                    prl[hh] = 0;
+                    pcl[hh] = 0;
+                    pdst[hh] = 0;
+                    if (k < pke[hh]) {
+                        prl[hh] = ep.s_r[k] - m0;
+                        pcl[hh] = ep.s_c[k] - (n0 + chunk * 32);
+                        pdst[hh] = ep.s_dst[k];
+                    }
+                }
+#endif
                 named_bar(1, 32 * NE);
                 if (tile_ok) {
 #pragma unroll
                     for (int hh = 0; hh < 2; hh++) {
                         const int chunk = hh * 4 + j;
+                        const int gc0 = n0 + chunk * 32;
+#if SERVE_PREFETCH
+                        const float *stg = estage + hh * 4 * 32 * 33;
+                        const int64_t k = pk0[hh] + tE;
+                        if (k < pke[hh]) {
+                            const float val = stg[(prl[hh] >> 5) * 32 * 33 + (prl[hh] & 31) * 33 + pcl[hh]];
+                            if (part_out) part_out[k] = val;
+                            else ep.out[pdst[hh]] = ep.accumulate ? fmaf(ep.coef, val, ep.out[pdst[hh]]) : ep.coef * val;
+                        }
+                        serve_samples<32 * NE>(ep, k + 32 * NE, pke[hh], 0, m0, gc0, stg, part_out);
+#else
                         const int64_t cidx = tile * (BN / 32) + chunk;
                         const int64_t kb0 = ep.chunk_ptr[cidx], ke = ep.chunk_ptr[cidx + 1];
-                        const int gc0 = n0 + chunk * 32;
                         serve_samples<32 * NE>(ep, kb0, ke, tE, m0, gc0, estage + hh * 4 * 32 * 33, part_out);
+#endif
                     }
                 }
                 named_bar(1, 32 * NE);

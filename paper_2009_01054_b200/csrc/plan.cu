@@ -1,3 +1,4 @@
+#include <type_traits>
 // plan.cu -- integer plumbing of the hot path: factor padding,
 // stable sorts of pair/entry lists (CUB radix sort, stable => ties keep index order),
 // CSR row pointers, sample ordering.  Everything here is integer work and bit-exact.
@@ -95,27 +96,30 @@ __device__ __forceinline__ int32_t pick(int sel, const int32_t *f, const int32_t
     return sel == 0 ? f[j] : s[j];
 }
 
-// entry e = kind * n + j  ->  key (row * ncol + col), value e
+// entry e = kind * n + j  ->  key (row * ncol + col), value e.  K = uint32_t when every key fits 32 bits (C5's
+// 20000^2 cells: the radix passes move 8 instead of 12 bytes per entry; the same order)
+template <typename K>
 __global__ void k_entry_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, EntryKinds kinds,
-                             int64_t ncol, uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                             int64_t ncol, K *__restrict__ keys, int32_t *__restrict__ vals) {
     int64_t E = n * kinds.count;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
         int kind = (int)(e / n);
         int64_t j = e - (int64_t)kind * n;
         int64_t row = pick(kinds.k[kind].row_sel, f, s, j);
         int64_t col = pick(kinds.k[kind].col_sel, f, s, j);
-        keys[e] = (uint64_t)(row * ncol + col);
+        keys[e] = (K)(row * ncol + col);
         vals[e] = (int32_t)e;
     }
 }
 
-__global__ void k_entry_gather(const uint64_t *__restrict__ skeys, const int32_t *__restrict__ svals, int64_t E,
+template <typename K>
+__global__ void k_entry_gather(const K *__restrict__ skeys, const int32_t *__restrict__ svals, int64_t E,
                                int64_t n, EntryKinds kinds, int64_t ncol, int32_t *__restrict__ row,
                                int32_t *__restrict__ col, int32_t *__restrict__ src, float *__restrict__ sign) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
         int64_t e = svals[k];
         int kind = (int)(e / n);
-        uint64_t key = skeys[k];
+        const uint64_t key = (uint64_t)skeys[k];
         row[k] = (int32_t)(key / (uint64_t)ncol);
         col[k] = (int32_t)(key % (uint64_t)ncol);
         src[k] = (int32_t)(e - (int64_t)kind * n);
@@ -150,14 +154,21 @@ void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32
     out.val = wsT<float>(c, (t + ".val").c_str(), E);
     out.row_ptr = wsT<int64_t>(c, (t + ".rowptr").c_str(), nrow + 1);
     if (E > 0) {
-        uint64_t *k0 = wsT<uint64_t>(c, "plan.keys0", E), *k1 = wsT<uint64_t>(c, "plan.keys1", E);
+        const uint64_t maxk = (uint64_t)(nrow * ncol > 0 ? nrow * ncol - 1 : 0);
+        const int bits = key_bits(maxk);
         int32_t *v0 = wsT<int32_t>(c, "plan.vals0", E), *v1 = wsT<int32_t>(c, "plan.vals1", E);
-        GVT_LAUNCH(c, K_PLAN_KEYS, k_entry_keys, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, f, s, n, kinds, ncol,
-                   k0, v0);
-        int bits = key_bits((uint64_t)(nrow * ncol > 0 ? nrow * ncol - 1 : 0));
-        radix_sort_pairs<uint64_t>(c, "plan", k0, k1, v0, v1, E, bits);
-        GVT_LAUNCH(c, K_PLAN_GATHER, k_entry_gather, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, k1, v1, E, n,
-                   kinds, ncol, out.row, out.col, out.src, out.sign);
+        auto run = [&](auto *k0, auto *k1) {
+            using K = std::remove_pointer_t<decltype(k0)>;
+            GVT_LAUNCH(c, K_PLAN_KEYS, k_entry_keys<K>, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, f, s, n, kinds,
+                       ncol, k0, v0);
+            radix_sort_pairs<K>(c, "plan", k0, k1, v0, v1, E, bits);
+            GVT_LAUNCH(c, K_PLAN_GATHER, k_entry_gather<K>, grid1d(E, 256, 16 * c->sm_count * 8), 256, 0, k1, v1, E,
+                       n, kinds, ncol, out.row, out.col, out.src, out.sign);
+        };
+        if (maxk <= 0xffffffffull)
+            run(wsT<uint32_t>(c, "plan.keys0", 2 * E), wsT<uint32_t>(c, "plan.keys1", 2 * E));
+        else
+            run(wsT<uint64_t>(c, "plan.keys0", E), wsT<uint64_t>(c, "plan.keys1", E));
     }
     GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(nrow + 1, 256), 256, 0, out.row, E, nrow, out.row_ptr);
 }
@@ -392,20 +403,28 @@ void sub_gram(gvt_ctx *c, const float *G, int64_t ld, const UsedSet &rows, const
 // ----------------------------------------------------------------------------- fit-level reordering
 // perm = the pair indices stably sorted by (first, second): a fit runs in this order so that the
 // pair-matrix entries of the Kronecker group are read in vector order (sequential, not gathered)
+template <typename K>
 __global__ void k_pair_keys(const int32_t *__restrict__ f, const int32_t *__restrict__ s, int64_t n, int64_t q,
-                            uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                            K *__restrict__ keys, int32_t *__restrict__ vals) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        keys[j] = (uint64_t)f[j] * (uint64_t)q + (uint64_t)s[j];
+        keys[j] = (K)((uint64_t)f[j] * (uint64_t)q + (uint64_t)s[j]);
         vals[j] = (int32_t)j;
     }
 }
 
 void sort_pairs(gvt_ctx *c, const int32_t *f, const int32_t *s, int64_t n, int64_t m, int64_t q, int32_t *perm) {
     if (n == 0) return;
-    uint64_t *k0 = wsT<uint64_t>(c, "fitsort.k0", n), *k1 = wsT<uint64_t>(c, "fitsort.k1", n);
+    const uint64_t cells = (uint64_t)(m > 0 ? m : 1) * (uint64_t)(q > 0 ? q : 1);
     int32_t *v0 = wsT<int32_t>(c, "fitsort.v0", n);
-    GVT_LAUNCH(c, K_PLAN_KEYS, k_pair_keys, grid1d(n, 256, 4096), 256, 0, f, s, n, q, k0, v0);
-    radix_sort_pairs<uint64_t>(c, "fitsort", k0, k1, v0, perm, n, key_bits((uint64_t)(m > 0 ? m : 1) * (uint64_t)(q > 0 ? q : 1)));
+    auto run = [&](auto *k0, auto *k1) {  // 32-bit keys when every (first, second) cell index fits
+        using K = std::remove_pointer_t<decltype(k0)>;
+        GVT_LAUNCH(c, K_PLAN_KEYS, k_pair_keys<K>, grid1d(n, 256, 4096), 256, 0, f, s, n, q, k0, v0);
+        radix_sort_pairs<K>(c, "fitsort", k0, k1, v0, perm, n, key_bits(cells));
+    };
+    if (cells - 1 <= 0xffffffffull)
+        run(wsT<uint32_t>(c, "fitsort.k0", 2 * n), wsT<uint32_t>(c, "fitsort.k1", 2 * n));
+    else
+        run(wsT<uint64_t>(c, "fitsort.k0", n), wsT<uint64_t>(c, "fitsort.k1", n));
 }
 
 template <typename Tv>

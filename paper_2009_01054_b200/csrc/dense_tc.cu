@@ -1665,7 +1665,7 @@ bool fused_f16(gvt_ctx *c, int64_t q_in) {
 // BX_THREADS per row: 1024 for long rows (a row's ~m*density cells spread over 32 warps, latency-bound
 // gathers); 256 for rows of <= 8192 columns, where the per-row barrier chain dominates and more rows
 // (smaller shared-memory rows) must be in flight per SM
-template <int BX_THREADS>
+template <int BX_THREADS, bool IDENT>
 __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                                    const int32_t *__restrict__ src, const float *__restrict__ sign,
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
@@ -1694,7 +1694,8 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
                     cc[u] = col[k];
                     cprev[u] = k > kb ? col[k - 1] : -1;
                     cnext[u] = k + 1 < ke ? col[k + 1] : -1;
-                    v[u] = sign[k] * __ldg(p + src[k]);
+                    // (IDENT: entry k is pair k with sign +1 -- the same value, 1 * p[k], without the src / sign loads)
+                    v[u] = IDENT ? __ldg(p + k) : sign[k] * __ldg(p + src[k]);
                 }
             }
 #pragma unroll
@@ -1703,7 +1704,8 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
                 float s = v[u];
                 if (cnext[u] == cc[u]) {
                     const int64_t k = k0 + (int64_t)u * BX_THREADS;
-                    for (int64_t j = k + 1; j < ke && col[j] == cc[u]; j++) s += sign[j] * __ldg(p + src[j]);
+                    for (int64_t j = k + 1; j < ke && col[j] == cc[u]; j++)
+                        s += IDENT ? __ldg(p + j) : sign[j] * __ldg(p + src[j]);
                 }
                 rowbuf[cc[u]] = s;
             }
@@ -1757,6 +1759,14 @@ __global__ void __launch_bounds__(256) k_build_x16_warp(const int64_t *__restric
         x16_row_warp<false>(r, lane, rowbuf, row_ptr, col, src, sign, p, row_lo, ld, hi, lo, sinv, diag);
 }
 
+static bool build_ident() {  // A/B knob: GVT_BUILD_IDENT=0 reads src / sign even for identity entry plans
+    static const bool on = [] {
+        const char *e = getenv("GVT_BUILD_IDENT");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 static bool build_warp_rows() {  // A/B knob: GVT_BUILD_WARP=0 keeps the CTA-per-row build for short rows
     static const bool on = [] {
         const char *e = getenv("GVT_BUILD_WARP");
@@ -1785,8 +1795,10 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
     static size_t attr_smem[GVT_MAX_DEVICES] = {};
     size_t &attr_dev = attr_smem[c->device < GVT_MAX_DEVICES ? c->device : 0];
     if (smem > 48 * 1024 && smem > attr_dev) {
-        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GVT_CUDA_TRY(cudaFuncSetAttribute(k_build_x16<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_dev = smem;
     }
     if (rows > 0 && o.ld <= 2048 && build_warp_rows()) {
@@ -1800,12 +1812,19 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
         GVT_LAUNCH(c, K_DENSIFY, k_build_x16_warp, grid1d(rows, 8), 256, smem8, e.row_ptr, e.col, e.src, e.sign, p,
                    row_lo, rows, cols, o.ld, hi, lo, s, diag);
     } else if (rows > 0) {
-        if (o.ld > 8192)
-            GVT_LAUNCH(c, K_DENSIFY, k_build_x16<1024>, grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr, e.col,
-                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+        const bool ident = e.ident && build_ident();
+        if (o.ld > 8192 && ident)
+            GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<1024, true>), grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr,
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+        else if (o.ld > 8192)
+            GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<1024, false>), grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr,
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+        else if (ident)
+            GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<256, true>), grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr,
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
         else
-            GVT_LAUNCH(c, K_DENSIFY, k_build_x16<256>, grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr, e.col,
-                       e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+            GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<256, false>), grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr,
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
     }
     o.hi = hi;
     o.lo = lo;

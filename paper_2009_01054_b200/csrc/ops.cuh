@@ -73,6 +73,7 @@ struct EntryPlan {
     float *sign = nullptr;
     int64_t *row_ptr = nullptr;  // nrow + 1
     float *val = nullptr;        // per-iteration values sign * p[src]
+    bool ident = false;          // src[k] == k and sign[k] == 1 for every entry (a sorted-order Kronecker fit)
 };
 
 // samples (r, c) of G = A X C^T sorted by r; result of sample k goes to dst[k]

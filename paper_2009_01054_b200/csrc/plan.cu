@@ -127,6 +127,12 @@ __global__ void k_entry_gather(const K *__restrict__ skeys, const int32_t *__res
     }
 }
 
+// is the sorted order the identity (entry k = pair k)?  bad != 0 otherwise
+__global__ void k_ident_check(const int32_t *__restrict__ v, int64_t E, int *__restrict__ bad) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x)
+        if (v[k] != (int32_t)k) atomicOr(bad, 1);
+}
+
 // row_ptr[h] = first position k with row[k] >= h  (rows sorted ascending)
 __global__ void k_row_ptr(const int32_t *__restrict__ row, int64_t E, int64_t nrow, int64_t *__restrict__ row_ptr) {
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h <= nrow; h += (int64_t)gridDim.x * blockDim.x) {
@@ -169,6 +175,17 @@ void build_entry_plan(gvt_ctx *c, const char *tag, const int32_t *f, const int32
             run(wsT<uint32_t>(c, "plan.keys0", 2 * E), wsT<uint32_t>(c, "plan.keys1", 2 * E));
         else
             run(wsT<uint64_t>(c, "plan.keys0", E), wsT<uint64_t>(c, "plan.keys1", E));
+        // one kind with sign +1 whose pairs were already in (row, col) order (the sorted-order fit): the pair
+        // matrix build can read p[k] directly instead of sign[k] * p[src[k]]
+        if (kinds.count == 1 && kinds.k[0].sign == 1.f) {
+            int *bad = (int *)ws(c, "plan.identbad", sizeof(int));
+            GVT_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+            GVT_LAUNCH(c, K_PLAN_GATHER, k_ident_check, grid1d(E, 256, 8 * c->sm_count), 256, 0, v1, E, bad);
+            int *h = (int *)pinned(c, sizeof(int));
+            GVT_CUDA_TRY(cudaMemcpyAsync(h, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+            out.ident = *h == 0;
+        }
     }
     GVT_LAUNCH(c, K_PLAN_ROWPTR, k_row_ptr, grid1d(nrow + 1, 256), 256, 0, out.row, E, nrow, out.row_ptr);
 }

@@ -4,6 +4,7 @@ library's environment knobs take effect:
   GVT_CG_TAIL=0      separate combine + k_cg_ap instead of the fused CG tail (Linear / Ranking / Poly2D)
   GVT_SPLITK=0       one CTA pair per sampled tile instead of split-K (small problems)
   GVT_BUILD_WARP=0   CTA-per-row X build instead of warp-per-row (rows <= 2048)
+  GVT_BUILD_IDENT=0  the pair-matrix build reads src / sign also for identity entry plans (sorted-order fits)
   OPT_ENGINE=1       (option) the gather form of the Cartesian kernel instead of its two sampled GEMMs
   GVT_CHEAP_TAIL=1   (default off) the cheap forms' CG tail as one persistent launch instead of three
   GVT_DENSE_TAIL=0   separate split-K combine, CG vector kernels, S-scale memset and X build instead of the
@@ -30,7 +31,7 @@ import json, os, sys, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import synth, paper_2009_01054_b200 as G
 cfg, kname, mode, iters, out = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), sys.argv[5]
-w = synth.by_name(cfg)
+w = synth.by_name(cfg, **json.loads(os.environ.get("GVT_TEST_SYNTH_KW", "{}")))
 kernel = getattr(synth, kname.upper())
 if kernel in synth.HOMOGENEOUS_KERNELS and w.Xt is not None:
     w = synth.union_domain(w)
@@ -165,3 +166,15 @@ def test_cheap_persistent_tail_bit_identical_c4(tmp_path, kname):
     fast, ef = run("C4", kname, "fit", 10, {**env, "GVT_CHEAP_TAIL": "1"}, tmp_path, "fast")
     slow, es = run("C4", kname, "fit", 10, env, tmp_path, "slow")
     assert ef["iters"] == es["iters"] == 10 and np.array_equal(fast, slow) and ef["hist"] == es["hist"]
+
+
+@pytest.mark.parametrize("cfg,kname,kw", [("C4", "poly2d", {}), ("C5", "kronecker", {"n": 20_000_000, "n_test": 1000})],
+                         ids=["C4-poly2d-256", "C5rows-kronecker-1024"])
+def test_identity_entry_build_bit_identical(tmp_path, cfg, kname, kw):
+    """A sorted-order fit's Kronecker entry plan is the identity (entry k = pair k, sign +1): the pair-matrix build then
+    reads p[k] directly.  Same cells (1 * p[k]), same scales: 3-iteration fits bit-identical to the src / sign build,
+    for the 256-thread (C4 Poly2D, 3008-wide rows) and 1024-thread (C5's 20000-wide rows, 2e7 pairs) builds."""
+    env = {"GVT_TEST_SYNTH_KW": json.dumps(kw)}
+    fast, ef = run(cfg, kname, "fit", 3, env, tmp_path, "fast")
+    slow, es = run(cfg, kname, "fit", 3, {**env, "GVT_BUILD_IDENT": "0"}, tmp_path, "slow")
+    assert ef["engine"] == 2 and np.array_equal(fast, slow) and ef["hist"] == es["hist"]

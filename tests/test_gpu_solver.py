@@ -505,3 +505,25 @@ def test_dense_fused_tail_ragged_vs_oracle(ctx, kernel, n):
     assert k["cg_vector"]["count"] <= 8 + 3  # (init, 8 tails -- halted ones return at once --, the direction copy)
     assert np.all(np.isfinite(a.cpu().numpy()))
     assert rel(a.cpu().numpy(), ao) <= max(1e-4, 3 * rel(asp.cpu().numpy(), ao))
+
+
+@pytest.mark.parametrize("kernel", [G.KRONECKER, G.CARTESIAN])
+def test_dense_fused_tail_breakdown(ctx, kernel):
+    """CG breakdown inside the fused dense tail: a negative-definite 'Gram' with lambda = 0 makes p^T A p < 0 at the
+    first iteration; the tail sets the breakdown flag before touching x, so the fit returns E_BREAKDOWN after 0
+    iterations with a = 0 -- the oracle's exit (test_oracle_pins.py::test_cg_breakdown_on_indefinite_operator)."""
+    m, q, n = 37, 29, 200
+    rng = np.random.default_rng(11 + kernel)
+    negD = dev(-np.eye(m, dtype=np.float32))
+    negT = dev(-np.eye(q, dtype=np.float32)) if kernel == G.CARTESIAN else dev(np.eye(q, dtype=np.float32))
+    cells = rng.choice(m * q, n, replace=False)
+    f, s = dev((cells // q).astype(np.int32)), dev((cells % q).astype(np.int32))
+    y = dev(rng.standard_normal(n).astype(np.float32))
+    try:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
+        a, it, _, code = ctx.fit(negD, negT, f, s, y, G.gvt_kernel_terms(kernel), 0.0, 5, raise_on_breakdown=False)
+        st = ctx.stats()
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    assert st["last_engine"] == 2
+    assert code == G.E_BREAKDOWN and it == 0 and np.all(a.cpu().numpy() == 0)

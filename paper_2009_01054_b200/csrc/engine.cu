@@ -849,9 +849,17 @@ static void run_matvec(gvt_ctx *c, const Problem &P, MatvecPlan &mp, const float
         break;
     case FORM_POLY2D: {
         GroupPlan &g = mp.groups[0];
-        entry_values(c, g.ent, p);               // all entries: the segment sums need every row
-        run_group(c, P, g, p, 2.f, 0, u, true);
-        segment_sum(c, g.ent, mp.b1);           // bF (entries of the Kronecker group, rows = first)
+        if (g.ent.ident) {  // entry k = pair k with sign +1 (sorted-order fit): the entry values are p itself
+            float *const vals = g.ent.val;
+            g.ent.val = const_cast<float *>(p);
+            run_group(c, P, g, p, 2.f, 0, u, true);
+            segment_sum(c, g.ent, mp.b1);
+            g.ent.val = vals;
+        } else {
+            entry_values(c, g.ent, p);           // all entries: the segment sums need every row
+            run_group(c, P, g, p, 2.f, 0, u, true);
+            segment_sum(c, g.ent, mp.b1);       // bF (entries of the Kronecker group, rows = first)
+        }
         segment_sum_gather(c, mp.byS, p, mp.b2);  // bS
         gemv(c, P.D, mp.b1, 1, mp.g1, !P.rect);  // D.^2 bF
         gemv(c, P.T, mp.b2, 1, mp.g2, !P.rect);  // T.^2 bS

@@ -21,6 +21,10 @@
 // partition (cgops.cuh, xbuild.cuh), so the iterates are bit-identical to the separate kernels'.
 // Data written by other CTAs earlier in the launch is read through L2 (ld.global.cg).  CTA 0 writes
 // the CG state; every CTA reads it as it was at launch.
+// Users: the Kronecker / symmetric / anti-symmetric group (one part set, one operand X) and the Cartesian
+// form's two sampled GEMMs (two part sets, the second accumulated; operands X^T and X).  A gather-combine
+// mode (the cheap forms' final combine, p updated in place, no operand) exists as an A/B knob
+// (GVT_CHEAP_TAIL=1, engine.cu): at n = 2e6 it measured slower than the separate kernels.
 #include <stdio.h>
 #include <stdlib.h>
 

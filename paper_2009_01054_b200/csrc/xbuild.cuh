@@ -36,7 +36,10 @@ __device__ __forceinline__ void x16_row_warp(int64_t r, int lane, float *__restr
     for (int64_t j = lane; j < ld / 4; j += 32) rb4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
-    constexpr int U = 4;  // entries in flight per lane
+#ifndef XB_U
+#define XB_U 4
+#endif
+    constexpr int U = XB_U;  // entries in flight per lane (A/B: -DXB_U=8)
     for (int64_t k0 = kb + lane; k0 < ke; k0 += U * 32) {
         int32_t cc[U], cprev[U], cnext[U];
         float v[U];

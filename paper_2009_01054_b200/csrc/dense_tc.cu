@@ -744,15 +744,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(EPI), 1
             c1 = nch * (ks + 1) / sp;
             return true;
         }
+        // (EPI_STORE16 with a tile order: tile_list[i] = mp * num_n + n replaces the grouped order)
+        auto store_coords = [&](int i, int &mt, int &nt) {
+            if (EPI == EPI_STORE16 && ep.tile_list) {
+                const int tl = ep.tile_list[i];
+                mt = tl / num_n;
+                nt = tl % num_n;
+            } else {
+                coords(i, mt, nt);
+            }
+        };
         if (EPI == EPI_STORE16 && ep.n_whole > 0 && t >= ep.n_whole) {  // tail split: the last tiles in parts
             const int u = t - ep.n_whole, ks = u % ep.split;
-            coords(ep.n_whole + u / ep.split, mp_tile, n_tile);
+            store_coords(ep.n_whole + u / ep.split, mp_tile, n_tile);
             const int nch = (tile_nk(n_tile) + kcb - 1) / kcb;
             c0 = nch * ks / ep.split;
             c1 = nch * (ks + 1) / ep.split;
             return true;
         }
-        coords(t, mp_tile, n_tile);
+        store_coords(t, mp_tile, n_tile);
         if (skip(mp_tile, n_tile)) return false;
         c0 = 0;
         c1 = (tile_nk(n_tile) + kcb - 1) / kcb;
@@ -1870,7 +1880,8 @@ void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_
 // (8 columns per lane), applies the operands' row / column scales, and stores the fp16 pieces with the
 // epilogue's per-(row, 256-column tile) scale rule (S16_SCALE_ROWS = 1), 16 bytes per lane per piece.
 __global__ void __launch_bounds__(256) k_store16_fixup(const float *__restrict__ part, int split, int r_tiles, int n_whole,
-                                                       int num_mp, int num_n, int gm, int64_t M, int64_t N,
+                                                       const int32_t *__restrict__ order, int num_mp, int num_n, int gm,
+                                                       int64_t M, int64_t N,
                                                        const float *__restrict__ sa, const float *__restrict__ sb,
                                                        __half *__restrict__ ch, __half *__restrict__ cl, int64_t ldc,
                                                        float *__restrict__ csk, int64_t csk_ld) {
@@ -1878,7 +1889,8 @@ __global__ void __launch_bounds__(256) k_store16_fixup(const float *__restrict__
     const int ti = blockIdx.x >> 5, mh = (blockIdx.x >> 4) & 1, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t = n_whole + ti, in_group = gm * num_n, first_m = (t / in_group) * gm;
     const int group_m = min(num_mp - first_m, gm);
-    const int mp_tile = first_m + (t % in_group) % group_m, n_tile = (t % in_group) / group_m;
+    const int mp_tile = order ? order[t] / num_n : first_m + (t % in_group) % group_m;
+    const int n_tile = order ? order[t] % num_n : (t % in_group) / group_m;
     const int64_t gc0 = (int64_t)n_tile * BN + 8 * lane;
     {
         const int row = (blockIdx.x & 15) * 8 + warp;
@@ -1944,7 +1956,7 @@ static bool store_tail_split_enabled() {  // A/B knob: GVT_STORE_TAIL_SPLIT=0 ke
 // floats, whose padding the caller keeps finite (stage 2 reads it against zero accumulators)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
                      __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const int32_t *kb_list,
-                     const int32_t *kb_off) {
+                     const int32_t *kb_off, const int32_t *tile_order, int kb_min_chunks) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
     ep.kb_list = kb_list;
@@ -1959,11 +1971,18 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
     const int num_mp = (int)((M + 2 * BM - 1) / (2 * BM)), num_n = (int)((N + BN - 1) / BN);
     const int n_tiles = num_mp * num_n, r = n_tiles % pairs;
     int split = 1;
-    // (not with block-sparse K lists: their per-tile chunk counts live on the device, and this runs inside the
-    // solver's graph capture, where no host read-back is possible)
-    if (S16_SCALE_ROWS == 1 && c->gemm_cta == 2 && !kb_list && n_tiles >= pairs && r > 0 && 2 * r <= pairs &&
+    // (block-sparse K lists: the caller passes their fewest chunks per tile, kb_min_chunks, from the plan's host
+    // lists -- this runs inside the solver's graph capture, where no host read-back is possible)
+    const int nch_min = kb_list ? kb_min_chunks : (int)((K + BN - 1) / BN);
+    if (S16_SCALE_ROWS == 1 && c->gemm_cta == 2 && n_tiles >= pairs && r > 0 && 2 * r <= pairs &&
         store_tail_split_enabled())
-        split = std::min(4, std::min(pairs / r, (int)((K + BN - 1) / BN) / 2));
+        split = std::min(4, std::min(pairs / r, nch_min / 2));
+    if (tile_order) {  // a caller's tile order (the longest K lists first), as whole units unless split below
+        ep.tile_list = tile_order;
+        ep.n_whole = n_tiles;
+        ep.split = 1;
+        ep.n_units = n_tiles;
+    }
     if (split >= 2) {
         ep.n_whole = n_tiles - r;
         ep.split = split;
@@ -1978,7 +1997,8 @@ void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
         }();
         const int gm = env_gm > 0 ? env_gm : GROUP_M;
         static_assert(BM == 16 * 8, "fixup: 16 blocks of 8 rows per m half");
-        GVT_LAUNCH(c, K_STAGE1_TC, k_store16_fixup, 32 * r, 256, 0, ep.part, split, r, ep.n_whole, num_mp, num_n, gm, M,
+        GVT_LAUNCH(c, K_STAGE1_TC, k_store16_fixup, 32 * r, 256, 0, ep.part, split, r, ep.n_whole, tile_order, num_mp,
+                   num_n, gm, M,
                    N, A.scale, B.scale, hi, lo, ldc, sk, sk_ld);
     }
 }
@@ -2088,6 +2108,14 @@ static int sampled_split(gvt_ctx *c, const SamplePlan &sp, int64_t K) {
     split = std::min(split, std::min(4, nch / 2));
     if (env > 0) split = std::min(env, std::max(1, nch / 2));
     return split >= 2 ? split : 1;
+}
+
+int gemm_group_m() {
+    static const int env_gm = [] {
+        const char *e = getenv("GVT_GROUP_M");
+        return e ? atoi(e) : 0;
+    }();
+    return env_gm > 0 ? env_gm : GROUP_M;
 }
 
 int sampled_split_parts(gvt_ctx *c, const SamplePlan &sp, int64_t K) { return sp.ns > 0 ? sampled_split(c, sp, K) : 1; }

@@ -215,6 +215,8 @@ struct GroupPlan {
     double extra_est = 0;   // of which appended extra outputs (early-stopping validation pairs)
     // block sparsity of X per slab for the fused fp16 stage 1 (device lists, nullptr = dense)
     std::vector<const int32_t *> kb_list, kb_off;
+    std::vector<const int32_t *> kb_order;  // per slab: stage-1 pair tiles, longest K lists first (block-sparse)
+    std::vector<int> kb_minch;              // per slab: the fewest 256-wide K chunks of any tile
 };
 
 struct MatvecPlan {
@@ -369,6 +371,14 @@ static void make_slabs(gvt_ctx *c, GroupPlan &g, bool uex) {
 
 static bool my_slab(gvt_ctx *c, int s) { return !distributed(c) || s == c->rank; }
 
+static bool kblock_order() {  // A/B knob: GVT_KBLOCK_ORDER=0 keeps the grouped tile order for block-sparse stage 1
+    static const bool on = [] {
+        const char *e = getenv("GVT_KBLOCK_ORDER");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag, bool uex) {
     g.tag = tag;
     g.engine = choose_engine(c, g);
@@ -381,6 +391,8 @@ static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag, bool uex) {
     // and the diagonal only); dense blocks everywhere (C3, C4 Poly2D, C5) keep the plain K loop
     g.kb_list.assign((size_t)g.nslab, nullptr);
     g.kb_off.assign((size_t)g.nslab, nullptr);
+    g.kb_order.assign((size_t)g.nslab, nullptr);
+    g.kb_minch.assign((size_t)g.nslab, 0);
     if (g.engine == 2 && fused_f16(c, g.C.cols) && c->kblock_skip) {
         for (int s = 0; s < g.nslab; s++) {
             if (!my_slab(c, s)) continue;
@@ -397,9 +409,30 @@ static void finish_group(gvt_ctx *c, GroupPlan &g, const char *tag, bool uex) {
             int32_t *dof = wsT<int32_t>(c, nm, off.size());
             GVT_CUDA_TRY(cudaMemcpyAsync(dl, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice, c->stream));
             GVT_CUDA_TRY(cudaMemcpyAsync(dof, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice, c->stream));
+            // the stage-1 GEMM's pair tiles (M = q_out rows of C in pairs of 256, N = this slab's X rows in 256-row
+            // tiles, whose K lists these are) in the kernel's grouped order, then stably by descending K-list length:
+            // the persistent loop then hands every CTA pair a similar amount of work (longest first)
+            const int num_n = (int)(off.size() - 1), num_mp = (int)((g.q_out + 255) / 256);
+            std::vector<int32_t> order;
+            order.reserve((size_t)num_mp * num_n);
+            const int gm = gemm_group_m(), in_group = gm * num_n;
+            for (int t = 0; t < num_mp * num_n; t++) {
+                const int first_m = (t / in_group) * gm, group_m = std::min(num_mp - first_m, gm);
+                order.push_back((first_m + (t % in_group) % group_m) * num_n + (t % in_group) / group_m);
+            }
+            auto len = [&](int32_t tl) { return off[(size_t)(tl % num_n) + 1] - off[(size_t)(tl % num_n)]; };
+            std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return len(x) > len(y); });
+            int minch = INT32_MAX;
+            for (int n = 0; n < num_n; n++) minch = std::min(minch, (off[(size_t)n + 1] - off[(size_t)n] + 3) / 4);
+            snprintf(nm, sizeof(nm), "%s.kbord%d", tag, s);
+            int32_t *dord = wsT<int32_t>(c, nm, order.size());
+            GVT_CUDA_TRY(cudaMemcpyAsync(dord, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice,
+                                         c->stream));
             GVT_CUDA_TRY(cudaStreamSynchronize(c->stream));  // the host vectors go out of scope
             g.kb_list[(size_t)s] = dl;
             g.kb_off[(size_t)s] = dof;
+            g.kb_order[(size_t)s] = kblock_order() ? dord : nullptr;
+            g.kb_minch[(size_t)s] = minch;
         }
     }
 }
@@ -636,7 +669,7 @@ static void run_group_f16(gvt_ctx *c, const Problem &P, GroupPlan &g, const floa
         if (w == 0) continue;
         Operand xo = build_x16(c, "dense.X16", g.ent, lo, w, g.C.cols, p_full, g.diag, !prebuilt);
         gemm_nt_store16(c, g.C.op, xo, g.q_out, w, g.C.cols, Sh + s * slab_h, Sl + s * slab_h, g.W, Sk + s * slab_k,
-                        skld, g.kb_list[(size_t)s], g.kb_off[(size_t)s]);
+                        skld, g.kb_list[(size_t)s], g.kb_off[(size_t)s], g.kb_order[(size_t)s], g.kb_minch[(size_t)s]);
     }
     float *partial = nullptr;
     const bool piped = !P.uex && slab_pipeline_available(c);

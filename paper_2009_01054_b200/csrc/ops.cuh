@@ -185,9 +185,11 @@ void add_diag(gvt_ctx *c, float *X, int64_t ldX, const float *diag, int64_t row_
 // 256-col tile): sk[tile * sk_ld + row / S16_SCALE_ROWS] (sk_ld >= round_up(M, 256) / S16_SCALE_ROWS)
 // kb_list / kb_off (device, nullable): per 256-row tile of B, its ascending non-zero K-blocks of
 // 64 columns (at least one per tile): the other K-blocks are skipped (block-sparse B)
+// tile_order (device, nullable): the persistent loop's pair-tile order (mp * num_n + n), e.g. the longest
+// block-sparse K lists first; kb_min_chunks: the fewest 256-wide chunks of any tile's K list (with kb_list)
 void gemm_nt_store16(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K, __half *hi,
                      __half *lo, int64_t ldc, float *sk, int64_t sk_ld, const int32_t *kb_list = nullptr,
-                     const int32_t *kb_off = nullptr);
+                     const int32_t *kb_off = nullptr, const int32_t *tile_order = nullptr, int kb_min_chunks = 0);
 // non-zero (256-row tile, 64-column K-block) pairs of the pair-matrix rows [lo, lo + rows) from the
 // sorted entries k in [k0, k1) (+ the diagonal when diag): host lists (off has ntiles + 1 entries)
 void kblock_lists(gvt_ctx *c, const EntryPlan &e, int64_t k0, int64_t k1, int64_t lo, int64_t rows, int64_t cols,
@@ -204,6 +206,8 @@ struct SplitParts {
     float coef = 1.f;
     int accumulate = 0;  // the deferred combine adds coef * (sum of parts) to out instead of storing it
 };
+// the CTA-pair GEMMs' rasterization group (pair-tile rows per group; GVT_GROUP_M or the default)
+int gemm_group_m();
 // the K-split the sampled GEMM will use for this plan and K (1: no parts)
 int sampled_split_parts(gvt_ctx *c, const SamplePlan &sp, int64_t K);
 void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, int64_t N, int64_t K,

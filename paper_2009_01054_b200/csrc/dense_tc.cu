@@ -2077,6 +2077,14 @@ __global__ void k_split_combine_tail(const float *__restrict__ part, int split, 
     }
 }
 
+static int64_t tail_split_part_limit() {  // bytes per part buffer (all ns slots); GVT_TAIL_SPLIT_MB overrides
+    static const int64_t lim = [] {
+        const char *e = getenv("GVT_TAIL_SPLIT_MB");
+        return (e ? atoll(e) : 64ll) << 20;
+    }();
+    return lim;
+}
+
 static bool tail_split_enabled() {  // A/B knob: GVT_TAIL_SPLIT=0 keeps the last partial wave unsplit
     static const bool on = [] {
         const char *e = getenv("GVT_TAIL_SPLIT");
@@ -2157,7 +2165,7 @@ void gemm_nt_sampled(gvt_ctx *c, const Operand &A, const Operand &B, int64_t M, 
         const int pairs = c->sm_count / 2, r = sp.n_pairs % pairs;
         const int nch = (int)((K + BN - 1) / BN);
         if (sp.n_pairs >= pairs && r > 0 && 2 * r <= pairs && tail_split_enabled() &&
-            sp.ns * (int64_t)sizeof(float) <= (64ll << 20))
+            sp.ns * (int64_t)sizeof(float) <= tail_split_part_limit())
             tail_split = std::min(4, std::min(pairs / r, nch / 2));
         if (tail_split >= 2) {
             ep.tile_list = sp.pair_list;

@@ -754,3 +754,23 @@ def test_block_sparse_stage1_mlpk_union(ctx, skip, slabs):
         ctx.set_option(G.OPT_SLABS, 1)
         ctx.set_option(G.OPT_KBLOCK_SKIP, 1)
         ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+
+
+def test_c4_generic_terms_accumulate_tail_split(ctx):
+    """C4 Kronecker written as two half-weight terms (not a recognised list: the generic path, one sampled GEMM
+    per term, the second accumulating into the first's outputs).  At C4 size each GEMM's last partial wave is tail
+    split (240 pair tiles on 74 CTA pairs), so the accumulate form of the split combine runs; sampled outputs
+    match the oracle's Kronecker GVT."""
+    w = synth.config4()
+    t = G.gvt_kernel_terms(G.KRONECKER)[0]
+    terms = [G.Term(0.5 * t.coef, *t.as_tuple()[1:]), G.Term(0.5 * t.coef, *t.as_tuple()[1:])]
+    Dg, Tg = grams_gpu(ctx, w)
+    f, s = dev(w.train_first), dev(w.train_second)
+    a = synth.random_vector(5, w.n)
+    u = ctx.matvec(Dg, Tg, f, s, f, s, dev(a), terms).cpu().numpy()
+    idx = synth.sample_indices(5, w.n, 48)
+    D, T = grams_oracle(w)
+    ref = O.gvt_matvec(O.kernel_terms(O.KRONECKER), D, T, w.train_first[idx], w.train_second[idx], w.train_first,
+                       w.train_second, a)
+    assert ctx.stats()["last_engine"] == 2
+    assert rel(u[idx], ref) <= MATVEC_TOL

@@ -774,3 +774,28 @@ def test_c4_generic_terms_accumulate_tail_split(ctx):
                        w.train_second, a)
     assert ctx.stats()["last_engine"] == 2
     assert rel(u[idx], ref) <= MATVEC_TOL
+
+
+def test_mlpk_block_sparse_stage1_tail_split(ctx):
+    """MLPK on a 2300-object union domain (1500 drugs + 800 targets): the Laplacian's block-sparse stage 1 has
+    9 x 9 = 81 pair tiles on 74 CTA pairs, so its last 7 tiles run as K parts (the tail split with block-sparse K
+    lists, fewest chunks from the plan) in the longest-first tile order; dense engine forced.  Sampled outputs of
+    the training matvec against the oracle's per-term GVT."""
+    w = synth.union_domain(synth.tiny(21, m=1500, q=800, n=120_000, n_out=10, dim=16))
+    terms = G.gvt_kernel_terms(G.MLPK)
+    D, _ = grams_oracle(w)
+    a = synth.random_vector(9, w.n)
+    try:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_DENSE)
+        ctx.reset_stats()
+        u = ctx.matvec(dev(f32(D)), None, dev(w.train_first), dev(w.train_second), dev(w.train_first),
+                       dev(w.train_second), dev(a), terms).cpu().numpy()
+        st = ctx.stats()
+        eng = st["last_engine"]
+        s1 = st["kinds"]["stage1_tc"]["count"]  # the GEMM and its tail-split fixup
+    finally:
+        ctx.set_option(G.OPT_ENGINE, G.ENGINE_AUTO)
+    idx = synth.sample_indices(9, w.n, 64)
+    ref = O.gvt_matvec(O.kernel_terms(O.MLPK), f32(D), None, w.train_first[idx], w.train_second[idx],
+                       w.train_first, w.train_second, a)
+    assert eng == 2 and s1 == 2 and rel(u[idx], ref) <= MATVEC_TOL

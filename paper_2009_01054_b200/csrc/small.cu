@@ -255,8 +255,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
             const int d = a.sdst[k];
             const float pk = first ? __ldcg(a.p + d) : fmaf(bf, __ldcg(a.p + d), __ldcg(a.r + d));
             const float v = fmaf(a.lambda, pk, acc0 + acc1);
-            a.Ap[d] = v;
-            a.p[d] = pk;
+            a.Ap[d] = v;  // (p_k itself is stored by its owner in phase D: contiguous, not scattered by dst)
             pa += (double)pk * (double)v;
             }
         }
@@ -278,8 +277,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_cg(SmallArgs a) {
         const float af = (float)alpha;
         double rr = 0.0;
         for (int64_t i = gtid; i < n; i += gthreads) {
-            a.x[i] = fmaf(af, __ldcg(a.p + i), a.x[i]);
-            const float ri = fmaf(-af, __ldcg(a.Ap + i), __ldcg(a.r + i));
+            // p_k = r_{k-1} + beta p_{k-1}, the same fmaf as phases AB and C, from the values before this update
+            const float r0 = __ldcg(a.r + i), p0 = __ldcg(a.p + i);
+            const float pk = first ? p0 : fmaf(bf, p0, r0);
+            a.p[i] = pk;
+            a.x[i] = fmaf(af, pk, a.x[i]);
+            const float ri = fmaf(-af, __ldcg(a.Ap + i), r0);
             a.r[i] = ri;
             rr += (double)ri * (double)ri;
         }

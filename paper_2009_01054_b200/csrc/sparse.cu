@@ -478,29 +478,29 @@ __global__ void __launch_bounds__(256) k_symv_finish(const float *__restrict__ p
     const int64_t nc = (jc + SYMV_RC - 1) / SYMV_RC;  // chunks holding a row < j
     const int64_t c0 = nc * warp / 8, c1 = nc * (warp + 1) / 8;
     const float *pc = pcol + ubase * SYMV_PW + (jc - (int64_t)pj * SYMV_PW);
+    // every load of a group in flight before the first add (a latency-bound kernel: C4's 125 chunks are
+    // 16 per warp, one round trip instead of four); the adds keep chunk order
     float v = 0.f;
-    int64_t c = c0;
-    for (; c + 4 <= c1; c += 4) {
-        float t4[4];
+    for (int64_t c = c0; c < c1; c += 16) {
+        float t16[16];
 #pragma unroll
-        for (int k = 0; k < 4; k++) t4[k] = pc[(c + k) * SYMV_PW];
+        for (int k = 0; k < 16; k++) t16[k] = c + k < c1 ? pc[(c + k) * SYMV_PW] : 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; k++) v += t4[k];
+        for (int k = 0; k < 16; k++)
+            if (c + k < c1) v += t16[k];
     }
-    for (; c < c1; c++) v += pc[c * SYMV_PW];
     part[warp][lane] = v;
     __syncthreads();
     if (warp == 0 && j < n) {
         float s = 0.f;
-        int p = pj;
-        for (; p + 4 <= np; p += 4) {  // row parts, four loads in flight, in panel order
-            float t4[4];
+        for (int p = pj; p < np; p += 8) {  // row parts, in panel order
+            float t8[8];
 #pragma unroll
-            for (int k = 0; k < 4; k++) t4[k] = prow[(int64_t)(p + k) * n + j];
+            for (int k = 0; k < 8; k++) t8[k] = p + k < np ? prow[(int64_t)(p + k) * n + j] : 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; k++) s += t4[k];
+            for (int k = 0; k < 8; k++)
+                if (p + k < np) s += t8[k];
         }
-        for (; p < np; p++) s += prow[(int64_t)p * n + j];
 #pragma unroll
         for (int w8 = 0; w8 < 8; w8++) s += part[w8][lane];
         y[j] = s;

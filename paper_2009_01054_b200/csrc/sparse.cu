@@ -368,12 +368,18 @@ __global__ void __launch_bounds__(256) k_gemv_smem(const float *__restrict__ F, 
 // (symmetric by definition, R1).  The columns are cut into panels of SYMV_PW = 1024 (thread t owns
 // column quad t of the panel) and the rows of each panel's upper part (rows 0 .. panel
 // end) into chunks of SYMV_RC = 64 (enough CTAs: ~4 per SM at C4's n = 8000); one CTA per (panel, row
-// chunk) streams its rows as 4 KB contiguous segments, SYMV_RB rows (loads of 16 B) per thread in flight:
+// chunk) streams its rows as 4 KB contiguous segments, SYMV_RB = 4 rows (loads of 16 B) per thread in flight
+// (8 measured 1 % slower, wider panels / shorter chunks slower still: profiles/r02_ab_symv_geom.txt):
 //   row part    prow[panel][i] = sum_{j >= i, j in panel} F_ij b_j   (warp trees, then warps in order)
 //   column part pcol[unit][j]  = sum_{i in chunk, i < j} F_ij b_i    (registers)
 // k_symv_finish adds, per j, the row parts of the panels right of j and the column parts of the chunks
 // above j, in a fixed order: deterministic, no atomics, half the HBM bytes of the plain GEMV.
-constexpr int SYMV_PW = 1024, SYMV_RC = 64, SYMV_RB = 8, SYMV_QT = SYMV_PW / 1024;
+#ifndef GVT_SYMV_PW  // panel width / row chunk / rows per batch (A/B builds override them)
+#define GVT_SYMV_PW 1024
+#define GVT_SYMV_RC 64
+#define GVT_SYMV_RB 4
+#endif
+constexpr int SYMV_PW = GVT_SYMV_PW, SYMV_RC = GVT_SYMV_RC, SYMV_RB = GVT_SYMV_RB, SYMV_QT = SYMV_PW / 1024;
 
 __device__ __forceinline__ int64_t symv_rows(int64_t n, int p) {  // rows with upper-triangle cells in panel p
     const int64_t e = (int64_t)(p + 1) * SYMV_PW;

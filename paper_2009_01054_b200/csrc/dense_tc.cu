@@ -1681,11 +1681,20 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
                                                    const float *__restrict__ p, int64_t row_lo, int64_t rows,
                                                    int64_t cols, int64_t ld, __half *__restrict__ hi,
                                                    __half *__restrict__ lo, float *__restrict__ sinv,
-                                                   const float *__restrict__ diag) {
-    extern __shared__ float rowbuf[];  // ld floats
+                                                   const float *__restrict__ diag, int vec) {
+    extern __shared__ __align__(16) float rowbuf[];  // ld floats
     __shared__ float red[BX_THREADS / 32];
+    // vec: the three shared-memory sweeps of a row (zero, max, store) move 4 cells per thread per
+    // pass (ld is a multiple of 32; the cells beyond cols stay zero, so the max over ld equals the
+    // max over cols): the same values in the same places, a quarter of the passes
+    float4 *rb4 = reinterpret_cast<float4 *>(rowbuf);
+    const int64_t ld4 = ld >> 2;
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
+        if (vec) {
+            for (int64_t j = threadIdx.x; j < ld4; j += blockDim.x) rb4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) rowbuf[j] = 0.f;
+        }
         __syncthreads();
         const int64_t kb = row_ptr[row_lo + r], ke = row_ptr[row_lo + r + 1];
         // two entries per thread per pass, their loads independent (in flight together); a run
@@ -1724,7 +1733,14 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
         if (diag && threadIdx.x == 0) rowbuf[row_lo + r] += diag[row_lo + r];  // separate diagonal (MLPK)
         __syncthreads();
         float mx = 0.f;
-        for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
+        if (vec) {
+            for (int64_t j = threadIdx.x; j < ld4; j += blockDim.x) {
+                const float4 v = rb4[j];
+                mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+            }
+        } else {
+            for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, fabsf(rowbuf[j]));
+        }
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
         __syncthreads();
@@ -1739,11 +1755,26 @@ __global__ void __launch_bounds__(BX_THREADS, 2048 / BX_THREADS) k_build_x16(con
         const float s = ldexpf(1.f, e);
         if (threadIdx.x == 0) sinv[r] = ldexpf(1.f, -e);
         __half2 *h2 = reinterpret_cast<__half2 *>(hi + r * ld), *l2 = reinterpret_cast<__half2 *>(lo + r * ld);
-        for (int64_t j = threadIdx.x; j < ld / 2; j += blockDim.x) {
-            const float v0 = rowbuf[2 * j] * s, v1 = rowbuf[2 * j + 1] * s;
-            const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1);
-            h2[j] = __halves2half2(a0, a1);
-            l2[j] = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
+        if (vec) {
+            uint2 *h4 = reinterpret_cast<uint2 *>(h2), *l4 = reinterpret_cast<uint2 *>(l2);
+            for (int64_t j = threadIdx.x; j < ld4; j += blockDim.x) {
+                const float4 v = rb4[j];
+                const float v0 = v.x * s, v1 = v.y * s, v2 = v.z * s, v3 = v.w * s;
+                const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1), a2 = __float2half_rn(v2),
+                             a3 = __float2half_rn(v3);
+                const __half2 ha = __halves2half2(a0, a1), hb = __halves2half2(a2, a3);
+                const __half2 la = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
+                const __half2 lb = __halves2half2(__float2half_rn(v2 - __half2float(a2)), __float2half_rn(v3 - __half2float(a3)));
+                h4[j] = make_uint2(*reinterpret_cast<const uint32_t *>(&ha), *reinterpret_cast<const uint32_t *>(&hb));
+                l4[j] = make_uint2(*reinterpret_cast<const uint32_t *>(&la), *reinterpret_cast<const uint32_t *>(&lb));
+            }
+        } else {
+            for (int64_t j = threadIdx.x; j < ld / 2; j += blockDim.x) {
+                const float v0 = rowbuf[2 * j] * s, v1 = rowbuf[2 * j + 1] * s;
+                const __half a0 = __float2half_rn(v0), a1 = __float2half_rn(v1);
+                h2[j] = __halves2half2(a0, a1);
+                l2[j] = __halves2half2(__float2half_rn(v0 - __half2float(a0)), __float2half_rn(v1 - __half2float(a1)));
+            }
         }
         __syncthreads();
     }
@@ -1781,6 +1812,14 @@ static bool build_warp_rows() {  // A/B knob: GVT_BUILD_WARP=0 keeps the CTA-per
     static const bool on = [] {
         const char *e = getenv("GVT_BUILD_WARP");
         return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+static int build_vec() {  // A/B knob: GVT_BUILD_VEC=0 keeps the scalar shared-memory sweeps of the CTA-per-row build
+    static const int on = [] {
+        const char *e = getenv("GVT_BUILD_VEC");
+        return (e && atoi(e) == 0) ? 0 : 1;
     }();
     return on;
 }
@@ -1825,16 +1864,16 @@ Operand build_x16(gvt_ctx *c, const char *name, const EntryPlan &e, int64_t row_
         const bool ident = e.ident && build_ident();
         if (o.ld > 8192 && ident)
             GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<1024, true>), grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr,
-                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, build_vec());
         else if (o.ld > 8192)
             GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<1024, false>), grid1d(rows, 1, 2 * c->sm_count), 1024, smem, e.row_ptr,
-                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, build_vec());
         else if (ident)
             GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<256, true>), grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr,
-                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, build_vec());
         else
             GVT_LAUNCH(c, K_DENSIFY, (k_build_x16<256, false>), grid1d(rows, 1, 16 * c->sm_count), 256, smem, e.row_ptr,
-                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag);
+                       e.col, e.src, e.sign, p, row_lo, rows, cols, o.ld, hi, lo, s, diag, build_vec());
     }
     o.hi = hi;
     o.lo = lo;
